@@ -1,0 +1,194 @@
+/*
+ * sdattn_b200.h -- C ABI of the B200-native scrambled distributed attention path.
+ *
+ * This is the drop-in boundary for the reference's hot path (/root/reference/proj/core).
+ * Every entry point names the reference interface it replaces (file:line relative to
+ * proj/core/). Conventions, chosen to make the ABI bindable from ctypes / cgo / JNI:
+ *   - extern "C", plain pointers and sizes, no C++ or torch types, no exceptions;
+ *   - every call returns an sda_status mapping the reference's exception cases;
+ *   - device buffers are caller-owned; device calls take an explicit cudaStream_t
+ *     (passed as void*) and are stream-ordered with no hidden synchronisation;
+ *   - no global mutable state: key material lives in caller buffers.
+ *
+ * Host key derivation (sda_derive_seed .. sda_span_perm) is pure CPU code and is
+ * bit-exact with the reference's SplitMix64 / Fisher-Yates / log-uniform draws.
+ *
+ * Device layouts (row-major, contiguous):
+ *   activations / caches : [batch][heads][rows][d]          (bf16 or f32)
+ *   partial outputs O'    : [split][batch][q_heads][rows][d] f32
+ *   partial stats         : [split][batch][q_heads][rows][2] f32 = (row_max, exp_sum)
+ *                           exactly the reference's ShardStats / SCR_SHARD stats frame
+ *                           (attention.hpp:38-41, protocol.cpp:1089-1093).
+ *   packed key set        : per (request, domain): [kv_heads][2 = {phi_kq, phi_v}] packed
+ *                           scramblers, SDA_SCRAMBLER_BYTES(d) each (see sda_pack_keyset).
+ */
+#ifndef SDATTN_B200_H
+#define SDATTN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDA_ABI_VERSION 1
+#define SDA_MAX_SOURCES 64
+
+typedef enum {
+    SDA_OK = 0,
+    SDA_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument: shapes / ranges (scrambler.cpp:128-130, attention.cpp:32-37) */
+    SDA_ERR_NOT_POW2 = 2,         /* build_scrambler: d must be a power of two (scrambler.cpp:27) */
+    SDA_ERR_EMPTY_SHARDS = 3,     /* merge_shards: empty shard list (attention.cpp:90) */
+    SDA_ERR_MASKED_ROW = 4,       /* merge_shards / attention: row masked in every shard (attention.cpp:99,109-110) */
+    SDA_ERR_UNSUPPORTED = 5,      /* valid for the reference but not compiled for the device (e.g. d not in {32,64,128,256}) */
+    SDA_ERR_CUDA = 6,             /* a CUDA runtime error (launch / config) */
+    SDA_ERR_NO_DEVICE = 7,        /* no sm_100 device visible */
+    SDA_ERR_ROLE_VIOLATION = 8    /* protocol.cpp:215-216: compute node asked for its own domain's keys */
+} sda_status;
+
+typedef enum { SDA_BF16 = 0, SDA_F32 = 1 } sda_dtype;
+
+/* Which transform of phi a scramble applies (scrambler.cpp:75-85). */
+typedef enum {
+    SDA_PHI_FORWARD = 0, /* x * phi          : Q (phi_kq) and V (phi_v) */
+    SDA_PHI_INV_T = 1,   /* x * phi^{-T}     : K (phi_kq)               */
+    SDA_PHI_INV = 2      /* x * phi^{-1}     : O' (phi_v), used by sda_unscramble_merge */
+} sda_phi_variant;
+
+typedef enum { SDA_KEYS_KQ = 0, SDA_KEYS_V = 1 } sda_key_which;
+
+typedef enum { SDA_MODE_S1_AND_S2 = 0, SDA_MODE_S1_ONLY = 1 } sda_scrambler_mode; /* scrambler.hpp:33-36 */
+
+/* ------------------------------------------------------------------------------------------
+ * Host key derivation -- bit-exact restatement of the protocol key contract.
+ * ------------------------------------------------------------------------------------------ */
+
+/* rng.cpp:35-39 derive_seed(base, {tags...}) */
+uint64_t sda_derive_seed(uint64_t base, const uint64_t* tags, size_t n_tags);
+/* protocol.cpp:143-145 RequestSpec::shared_seed() = derive_seed(master, {request_id, 0x7365656B}) */
+uint64_t sda_shared_seed(uint64_t master_seed, uint64_t request_id);
+/* permutation.cpp:29-37 random_permutation(n, RngStream(seed)) -> forward[n] */
+sda_status sda_random_permutation(size_t n, uint64_t seed, uint32_t* forward);
+
+/* KeySetSpec (scrambler.hpp:77-88) minus l_q/l_k: token permutations are drawn per span. */
+typedef struct {
+    uint64_t request_id;
+    uint32_t layer;
+    uint32_t domain;
+    uint32_t n_heads;  /* scrambler heads (= kv heads; GQA extension of scrambler.cpp:113-118) */
+    uint32_t head_dim; /* power of two */
+    double mag_lo;     /* default 0.125 (protocol.hpp:20-27) */
+    double mag_hi;     /* default 8.0 */
+    int32_t mode;      /* sda_scrambler_mode */
+} sda_keyspec;
+
+/* Host key set, f64 factors and u32 permutations exactly as the reference draws them.
+ * All arrays [n_heads][head_dim], caller-owned. */
+typedef struct {
+    double* kq_s1; uint32_t* kq_p1; uint32_t* kq_p2; double* kq_s2;
+    double* v_s1;  uint32_t* v_p1;  uint32_t* v_p2;  double* v_s2;
+    uint64_t token_perm_seed;
+} sda_host_keyset;
+
+/* scrambler.cpp:105-124 negotiate_keyset (feature scramblers + token_perm_seed). */
+sda_status sda_negotiate_keyset(uint64_t shared_seed, const sda_keyspec* spec, sda_host_keyset* out);
+/* scrambler.cpp:99-103 ScramblerKeySet::span_perm(tag, first_pos, len): tag 0 = Q, 1 = KV. */
+sda_status sda_span_perm(uint64_t token_perm_seed, uint64_t tag, uint64_t first_pos, size_t len,
+                         uint32_t* forward);
+/* inverse permutation: inv[forward[i]] = i (permutation.cpp:15-20) */
+sda_status sda_invert_permutation(const uint32_t* forward, size_t n, uint32_t* inverse);
+
+/* Bytes of one packed device scrambler / one head (phi_kq + phi_v) / one key set. */
+#define SDA_SCRAMBLER_BYTES(d) ((size_t)32 * (size_t)(d))
+#define SDA_KEYSET_HEAD_BYTES(d) ((size_t)64 * (size_t)(d))
+size_t sda_keyset_bytes(uint32_t n_heads, uint32_t head_dim);
+/* Packs a host key set into the device image (f32 factor tables with the 1/sqrt(d) of the
+ * normalised FWHT folded in, u16 permutations and their inverses). `out` is host memory of
+ * sda_keyset_bytes(); the caller uploads it (cudaMemcpyAsync) next to its other key sets. */
+sda_status sda_pack_keyset(const sda_host_keyset* ks, uint32_t n_heads, uint32_t head_dim, void* out);
+
+/* ------------------------------------------------------------------------------------------
+ * K1  scramble + token permutation, fused into the cache / wire write.
+ *   replaces apply_phi / apply_phi_inv_t + permute_rows_gather (scrambler.cpp:126-136;
+ *   protocol.cpp:889-891 for Q, protocol.cpp:998-1001 for the KV write)
+ *
+ *   out[b][h][out_row_offset + i][:] = x[b][h][perm_b[i]][:] * phi_{b, h / (n_heads/key_heads)}
+ *
+ *   x    : [n_batch][n_heads][rows][d]              x_dtype
+ *   out  : [n_batch][n_heads][out_rows_cap][d]      out_dtype (rounded once, RNE)
+ *   keys : device; request b's key set at keys + b * keys_batch_stride (bytes)
+ *   perm : device u32; request b's span permutation at perm + b * perm_batch_stride,
+ *          NULL = identity (e.g. L_q = 1)
+ * ------------------------------------------------------------------------------------------ */
+sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys,
+                        const void* x, int32_t x_dtype, int64_t n_batch, int32_t n_heads,
+                        int64_t rows, int32_t head_dim,
+                        const void* keys, int64_t keys_batch_stride, int32_t key_heads,
+                        const uint32_t* perm, int64_t perm_batch_stride,
+                        void* out, int32_t out_dtype, int64_t out_rows_cap, int64_t out_row_offset);
+
+/* ------------------------------------------------------------------------------------------
+ * K2  keyless delegated partial attention over the scrambled KV shard.
+ *   replaces shard_attention(q', K', V', none) as run by try_serve_q (attention.cpp:42-78;
+ *   protocol.cpp:1072-1095). The shard is split along keys into n_splits ranges; every
+ *   split emits a locally normalised O' and its (row_max, exp_sum); sda_unscramble_merge
+ *   folds splits and nodes in one pass (merge_shards is associative).
+ *
+ *   q      : [n_batch][q_heads][q_rows][d]  (bf16 or f32; already scrambled)
+ *   k, v   : [n_batch][kv_heads][kv_cap][d] (same dtype for k and v)
+ *   kv_len : device i32[n_batch] valid rows per request, NULL = kv_cap for all
+ *   out_o     : f32 [n_splits][n_batch][q_heads][q_rows][d]
+ *   out_stats : f32 [n_splits][n_batch][q_heads][q_rows][2]
+ *   q_heads must be a multiple of kv_heads (GQA: q head h reads kv head h / (q_heads/kv_heads)).
+ *   The logit scale is 1/sqrt(d) (attention.cpp:45). Rows with no key in a split get
+ *   row_max = -inf, exp_sum = 0, O' = 0 (attention.cpp:66-67).
+ * ------------------------------------------------------------------------------------------ */
+sda_status sda_partial_attention(void* stream, const void* q, int32_t q_dtype,
+                                 const void* k, const void* v, int32_t kv_dtype, int64_t kv_cap,
+                                 const int32_t* kv_len, int64_t n_batch, int32_t q_heads,
+                                 int32_t kv_heads, int64_t q_rows, int32_t head_dim, int32_t n_splits,
+                                 float* out_o, float* out_stats);
+/* Splits sda_partial_attention would choose for a full-GPU decode launch. */
+int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int64_t kv_cap);
+
+/* ------------------------------------------------------------------------------------------
+ * K3  cross-node LSE-weighted merge + inverse token permutation + unscramble.
+ *   replaces dec_output (scrambler.cpp:138-149) for every remote shard followed by
+ *   merge_shards (attention.cpp:89-123), as span_finish_layer does (protocol.cpp:926-948).
+ *
+ *   Source s contributes rows o_s[b][h][pq_inv_s[b][r]] (its rows are in its domain's P_Q
+ *   order) with stats stats_s. Sources with the same `keys` pointer form one group: their
+ *   weighted sum is unscrambled once with that group's phi_v^{-1} (linearity). keys == NULL
+ *   marks a plaintext source (e.g. the inquirer's local shard). A single source is returned
+ *   unweighted, as merge_shards returns one shard verbatim (attention.cpp:97-101).
+ *
+ *   out       : [n_batch][q_heads][q_rows][d] out_dtype
+ *   out_stats : optional f32 [n_batch][q_heads][q_rows][2] merged (row_max, exp_sum), may be NULL
+ *   err_flag  : optional device i32; set to SDA_ERR_MASKED_ROW when a row has exp_sum == 0 in
+ *               every source (that row is written as NaN). May be NULL.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct {
+    const float* o;          /* [n_batch][q_heads][q_rows][d] */
+    const float* stats;      /* [n_batch][q_heads][q_rows][2] */
+    const void* keys;        /* device key set of the domain (phi_v used), NULL = plaintext */
+    const uint32_t* pq_inv;  /* device u32 inverse span perm per request, NULL = identity */
+} sda_merge_source;
+
+sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, int32_t n_sources,
+                                int64_t keys_batch_stride, int32_t key_heads, int64_t pq_batch_stride,
+                                int64_t n_batch, int32_t q_heads, int64_t q_rows, int32_t head_dim,
+                                void* out, int32_t out_dtype, float* out_stats, int32_t* err_flag);
+
+/* ------------------------------------------------------------------------------------------
+ * Misc
+ * ------------------------------------------------------------------------------------------ */
+int32_t sda_abi_version(void);
+const char* sda_status_string(int32_t status);
+/* Number of kernel launches issued by this library since load (for bench gpu_launches). */
+uint64_t sda_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDATTN_B200_H */

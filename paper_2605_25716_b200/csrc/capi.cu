@@ -1,0 +1,130 @@
+// capi.cu -- the extern "C" boundary (include/sdattn_b200.h): argument validation that
+// mirrors the reference's std::invalid_argument cases, then stream-ordered kernel launches.
+#include <atomic>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+bool supported_dim(int d) { return d == 32 || d == 64 || d == 128 || d == 256; }
+bool pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+bool valid_dtype(int t) { return t == SDA_BF16 || t == SDA_F32; }
+
+sda_status from_cuda(cudaError_t e) {
+    if (e == cudaSuccess) return SDA_OK;
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) return SDA_ERR_NO_DEVICE;
+    return SDA_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t sda_abi_version(void) { return SDA_ABI_VERSION; }
+
+uint64_t sda_launch_count(void) { return g_launches.load(); }
+
+const char* sda_status_string(int32_t s) {
+    switch (s) {
+        case SDA_OK: return "ok";
+        case SDA_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case SDA_ERR_NOT_POW2: return "head dim must be a power of two";
+        case SDA_ERR_EMPTY_SHARDS: return "merge: empty shard list";
+        case SDA_ERR_MASKED_ROW: return "merge: row masked in every shard";
+        case SDA_ERR_UNSUPPORTED: return "unsupported on device (head dim not in {32,64,128,256})";
+        case SDA_ERR_CUDA: return "CUDA error";
+        case SDA_ERR_NO_DEVICE: return "no CUDA device";
+        case SDA_ERR_ROLE_VIOLATION: return "role violation";
+        default: return "unknown status";
+    }
+}
+
+sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys, const void* x, int32_t x_dtype,
+                        int64_t n_batch, int32_t n_heads, int64_t rows, int32_t head_dim, const void* keys,
+                        int64_t keys_batch_stride, int32_t key_heads, const uint32_t* perm,
+                        int64_t perm_batch_stride, void* out, int32_t out_dtype, int64_t out_rows_cap,
+                        int64_t out_row_offset) {
+    if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
+    if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
+    if (variant != SDA_PHI_FORWARD && variant != SDA_PHI_INV_T) return SDA_ERR_INVALID_ARGUMENT;
+    if (which_keys != SDA_KEYS_KQ && which_keys != SDA_KEYS_V) return SDA_ERR_INVALID_ARGUMENT;
+    if (!x || !out || !keys || !valid_dtype(x_dtype) || !valid_dtype(out_dtype)) return SDA_ERR_INVALID_ARGUMENT;
+    if (n_batch < 0 || n_heads <= 0 || key_heads <= 0 || n_heads % key_heads != 0 || rows < 0)
+        return SDA_ERR_INVALID_ARGUMENT;
+    if (out_row_offset < 0 || out_row_offset + rows > out_rows_cap) return SDA_ERR_INVALID_ARGUMENT;
+    if (n_batch > 65535 || n_heads > 65535) return SDA_ERR_UNSUPPORTED;
+    if (rows == 0 || n_batch == 0) return SDA_OK;
+    sda::K1Params p{x, out, keys, perm, keys_batch_stride, perm_batch_stride, rows, out_rows_cap, out_row_offset,
+                    n_heads, key_heads, which_keys, variant == SDA_PHI_INV_T ? 1 : 0};
+    ++g_launches;
+    return from_cuda(sda::launch_k1(p, head_dim, x_dtype, out_dtype, n_batch, static_cast<cudaStream_t>(stream)));
+}
+
+int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int64_t kv_cap) {
+    // Aim for >= 8 resident CTAs per SM (148 SMs) with >= 256 keys per split.
+    const int64_t ctas = n_batch * q_heads * q_rows;
+    if (ctas <= 0 || kv_cap <= 0) return 1;
+    const int64_t want = (148 * 8 + ctas - 1) / ctas;
+    const int64_t max_by_len = kv_cap / 256 > 0 ? kv_cap / 256 : 1;
+    int64_t s = want < max_by_len ? want : max_by_len;
+    if (s < 1) s = 1;
+    if (s > 1024) s = 1024;
+    return (int32_t)s;
+}
+
+sda_status sda_partial_attention(void* stream, const void* q, int32_t q_dtype, const void* k, const void* v,
+                                 int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int64_t n_batch,
+                                 int32_t q_heads, int32_t kv_heads, int64_t q_rows, int32_t head_dim,
+                                 int32_t n_splits, float* out_o, float* out_stats) {
+    if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
+    if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
+    if (!q || !k || !v || !out_o || !out_stats || !valid_dtype(q_dtype) || !valid_dtype(kv_dtype))
+        return SDA_ERR_INVALID_ARGUMENT;
+    if (n_batch < 0 || q_rows < 0 || kv_cap < 0 || q_heads <= 0 || kv_heads <= 0 || q_heads % kv_heads != 0 ||
+        n_splits <= 0)
+        return SDA_ERR_INVALID_ARGUMENT;
+    if (n_batch * q_rows > 65535 || q_heads > 65535 || n_splits > 65535) return SDA_ERR_UNSUPPORTED;
+    if (n_batch == 0 || q_rows == 0) return SDA_OK;
+    sda::K2Params p{q, k, v, kv_len, out_o, out_stats, kv_cap, n_batch, q_rows, q_heads, kv_heads, n_splits,
+                    (float)(1.0 / std::sqrt((double)head_dim))};
+    ++g_launches;
+    return from_cuda(sda::launch_k2_decode(p, head_dim, q_dtype, kv_dtype, static_cast<cudaStream_t>(stream)));
+}
+
+sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, int32_t n_sources,
+                                int64_t keys_batch_stride, int32_t key_heads, int64_t pq_batch_stride,
+                                int64_t n_batch, int32_t q_heads, int64_t q_rows, int32_t head_dim, void* out,
+                                int32_t out_dtype, float* out_stats, int32_t* err_flag) {
+    if (n_sources <= 0) return SDA_ERR_EMPTY_SHARDS;  // attention.cpp:90
+    if (n_sources > SDA_MAX_SOURCES || !sources) return SDA_ERR_INVALID_ARGUMENT;
+    if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
+    if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
+    if (!out || !valid_dtype(out_dtype) || n_batch < 0 || q_rows < 0 || q_heads <= 0) return SDA_ERR_INVALID_ARGUMENT;
+    bool any_keys = false;
+    for (int i = 0; i < n_sources; ++i) {
+        if (!sources[i].o || !sources[i].stats) return SDA_ERR_INVALID_ARGUMENT;
+        any_keys |= sources[i].keys != nullptr;
+    }
+    if (any_keys && (key_heads <= 0 || q_heads % key_heads != 0)) return SDA_ERR_INVALID_ARGUMENT;
+    if (n_batch == 0 || q_rows == 0) return SDA_OK;
+    sda::K3Params p{};
+    for (int i = 0; i < n_sources; ++i)
+        p.src[i] = {sources[i].o, sources[i].stats, static_cast<const uint8_t*>(sources[i].keys), sources[i].pq_inv};
+    p.n_src = n_sources;
+    p.keys_bstride = keys_batch_stride;
+    p.key_heads = key_heads > 0 ? key_heads : q_heads;
+    p.pq_bstride = pq_batch_stride;
+    p.n_batch = n_batch;
+    p.q_heads = q_heads;
+    p.q_rows = q_rows;
+    p.out = out;
+    p.out_stats = out_stats;
+    p.err = err_flag;
+    ++g_launches;
+    return from_cuda(sda::launch_k3(p, head_dim, out_dtype, static_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,162 @@
+// common.cuh -- small device helpers shared by the sm_100a kernels.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sdattn_internal.h"
+
+namespace sda {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// 16-byte streaming load that bypasses L1 allocation (KV tiles are read once).
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void bf16x2_to_f2(uint32_t w, float& a, float& b) {
+    a = __uint_as_float(w << 16);
+    b = __uint_as_float(w & 0xFFFF0000u);
+}
+
+__device__ __forceinline__ uint32_t f2_to_bf16x2(float a, float b) {
+    __nv_bfloat162 t = __floats2bfloat162_rn(a, b);  // RNE, single rounding
+    return *reinterpret_cast<uint32_t*>(&t);
+}
+
+// Load N consecutive elements (N multiple of 8) of T starting at p (16-byte aligned) into f32.
+template <int N, typename T>
+__device__ __forceinline__ void load_vec(const T* p, float* v);
+
+template <int N>
+__device__ __forceinline__ void load_vec(const __nv_bfloat16* p, float* v) {
+    static_assert(N % 8 == 0, "");
+#pragma unroll
+    for (int i = 0; i < N / 8; ++i) {
+        const uint4 w = *reinterpret_cast<const uint4*>(p + 8 * i);
+        bf16x2_to_f2(w.x, v[8 * i + 0], v[8 * i + 1]);
+        bf16x2_to_f2(w.y, v[8 * i + 2], v[8 * i + 3]);
+        bf16x2_to_f2(w.z, v[8 * i + 4], v[8 * i + 5]);
+        bf16x2_to_f2(w.w, v[8 * i + 6], v[8 * i + 7]);
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void load_vec(const float* p, float* v) {
+    static_assert(N % 4 == 0, "");
+#pragma unroll
+    for (int i = 0; i < N / 4; ++i) {
+        const float4 w = *reinterpret_cast<const float4*>(p + 4 * i);
+        v[4 * i + 0] = w.x; v[4 * i + 1] = w.y; v[4 * i + 2] = w.z; v[4 * i + 3] = w.w;
+    }
+}
+
+template <int N, typename T>
+__device__ __forceinline__ void store_vec(T* p, const float* v);
+
+template <int N>
+__device__ __forceinline__ void store_vec(__nv_bfloat16* p, const float* v) {
+    static_assert(N % 8 == 0, "");
+#pragma unroll
+    for (int i = 0; i < N / 8; ++i) {
+        uint4 w;
+        w.x = f2_to_bf16x2(v[8 * i + 0], v[8 * i + 1]);
+        w.y = f2_to_bf16x2(v[8 * i + 2], v[8 * i + 3]);
+        w.z = f2_to_bf16x2(v[8 * i + 4], v[8 * i + 5]);
+        w.w = f2_to_bf16x2(v[8 * i + 6], v[8 * i + 7]);
+        *reinterpret_cast<uint4*>(p + 8 * i) = w;
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void store_vec(float* p, const float* v) {
+#pragma unroll
+    for (int i = 0; i < N / 4; ++i)
+        *reinterpret_cast<float4*>(p + 4 * i) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+}
+
+// Small-vector variants for N in {1, 2, 4, 8, 16, ...} f32 loads / any-typed stores.
+template <int N>
+__device__ __forceinline__ void load_vec_any(const float* p, float* v) {
+    if constexpr (N % 4 == 0) {
+        load_vec<N>(p, v);
+    } else if constexpr (N == 2) {
+        const float2 w = *reinterpret_cast<const float2*>(p);
+        v[0] = w.x; v[1] = w.y;
+    } else {
+        v[0] = p[0];
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void store_vec_any(float* p, const float* v) {
+    if constexpr (N % 4 == 0) {
+        store_vec<N>(p, v);
+    } else if constexpr (N == 2) {
+        *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+    } else {
+        p[0] = v[0];
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void store_vec_any(__nv_bfloat16* p, const float* v) {
+    if constexpr (N % 8 == 0) {
+        store_vec<N>(p, v);
+    } else if constexpr (N == 4) {
+        uint2 w;
+        w.x = f2_to_bf16x2(v[0], v[1]);
+        w.y = f2_to_bf16x2(v[2], v[3]);
+        *reinterpret_cast<uint2*>(p) = w;
+    } else if constexpr (N == 2) {
+        *reinterpret_cast<uint32_t*>(p) = f2_to_bf16x2(v[0], v[1]);
+    } else {
+        p[0] = __float2bfloat16_rn(v[0]);
+    }
+}
+
+// Raw (unnormalised) Walsh-Hadamard butterflies over a vector of E*LPR elements held by a
+// group of LPR consecutive lanes, lane lg owning elements [lg*E, lg*E+E). The 1/sqrt(d)
+// normalisation of fwht.cpp:24 is folded into the packed output factors.
+template <int E, int LPR>
+__device__ __forceinline__ void fwht_group(float* v, int lane) {
+#pragma unroll
+    for (int h = 1; h < E; h <<= 1) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            if ((i & h) == 0) {
+                const float a = v[i], b = v[i + h];
+                v[i] = a + b;
+                v[i + h] = a - b;
+            }
+        }
+    }
+#pragma unroll
+    for (int m = 1; m < LPR; m <<= 1) {
+        const bool upper = (lane & m) != 0;
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            const float o = __shfl_xor_sync(0xffffffffu, v[i], m);
+            v[i] = upper ? (o - v[i]) : (v[i] + o);
+        }
+    }
+}
+
+__host__ __device__ __forceinline__ const uint8_t* scrambler_ptr(const void* keys, int64_t batch_stride,
+                                                                 int64_t b, int kh, int d, int which) {
+    return static_cast<const uint8_t*>(keys) + b * batch_stride + (int64_t)kh * 64 * d +
+           (int64_t)which * 32 * d;
+}
+
+}  // namespace sda

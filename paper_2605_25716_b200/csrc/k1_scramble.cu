@@ -1,0 +1,122 @@
+// k1_scramble.cu -- K1: feature scramble (phi / phi^{-T}) fused with the token permutation
+// and the single RNE rounding into the cache / wire layout.
+//
+// Replaces apply_phi / apply_phi_inv_t + permute_rows_gather (scrambler.cpp:42-85,
+// permutation.cpp:58-67) as called by enc_qkv (scrambler.cpp:126-136), the inquirer's Q
+// scramble (protocol.cpp:885-891) and the context owner's KV shipping
+// (protocol.cpp:993-1001).
+//
+// SIMT design (HBM-bound: 4 B/elem moved vs ~10 flop/elem): every output row is owned by a
+// group of LPR = d/16 lanes, 16 elements per lane. P1 is applied as a scatter into shared
+// memory, the Walsh-Hadamard butterflies run 4 stages in registers plus log2(LPR) shuffle
+// stages, and P2 is applied as a gather from shared memory. Row permutation is a gather on
+// the input side (output rows are written in order), so stores stay contiguous.
+#include "common.cuh"
+
+namespace sda {
+
+template <int D>
+struct K1Shape {
+    static constexpr int E = 16;              // elements per lane
+    static constexpr int LPR = D / E;         // lanes per row
+    static constexpr int R = 32 / LPR;        // rows per warp
+    static constexpr int CS = E + 4;          // padded chunk stride (conflict-free LDS/STS.128)
+    static constexpr int RS = LPR * CS;       // row stride in smem (floats)
+    static constexpr int WARPS = 4;
+    static constexpr int ROWS_PER_CTA = 64 > WARPS * R ? 64 : WARPS * R;
+    static constexpr int ITERS = ROWS_PER_CTA / (WARPS * R);
+};
+
+__device__ __forceinline__ int k1_sidx(int j) { return (j >> 4) * 20 + (j & 15); }
+
+template <int D, typename Tin, typename Tout>
+__global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p) {
+    using S = K1Shape<D>;
+    constexpr int E = S::E, LPR = S::LPR, R = S::R;
+    __shared__ __align__(16) float sbuf[S::WARPS][R * S::RS];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane / LPR, lg = lane % LPR;
+    const int h = blockIdx.y;
+    const int64_t b = blockIdx.z;
+    const int kh = h / (p.n_heads / p.key_heads);
+    const uint8_t* sc = scrambler_ptr(p.keys, p.keys_bstride, b, kh, D, p.which);
+    const float* ftab = reinterpret_cast<const float*>(sc);
+    const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + 24 * D);
+
+    // This lane's key material for its element chunk [lg*E, lg*E+E).
+    float kin[E], kout[E];
+    int p1[E], p2i[E];
+    {
+        const float* fin = ftab + (p.inv_t ? kInInvT : kInFwd) * D + lg * E;
+        const float* fout = ftab + (p.inv_t ? kOutInvT : kOutFwd) * D + lg * E;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            kin[e] = fin[e];
+            kout[e] = fout[e];
+            p1[e] = k1_sidx(utab[kP1 * D + lg * E + e]);
+            p2i[e] = k1_sidx(utab[kP2Inv * D + lg * E + e]);
+        }
+    }
+
+    const Tin* x = static_cast<const Tin*>(p.x) + (b * p.n_heads + h) * p.rows * D;
+    Tout* out = static_cast<Tout*>(p.out) + ((b * p.n_heads + h) * p.out_rows_cap + p.out_row_offset) * D;
+    const uint32_t* perm = p.perm ? p.perm + b * p.perm_bstride : nullptr;
+    float* u = &sbuf[warp][g * S::RS];
+
+    for (int it = 0; it < S::ITERS; ++it) {
+        const int64_t r = (int64_t)blockIdx.x * S::ROWS_PER_CTA + (int64_t)it * S::WARPS * R + warp * R + g;
+        const bool valid = r < p.rows;
+        const int64_t src = valid ? (perm ? (int64_t)perm[r] : r) : 0;
+
+        float v[E];
+        load_vec<E>(x + src * D + lg * E, v);
+#pragma unroll
+        for (int e = 0; e < E; ++e) u[p1[e]] = v[e] * kin[e];   // u[P1[i]] = x[i] * s1^{+-1}[i]
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < E / 4; ++c) {
+            const float4 t = *reinterpret_cast<const float4*>(&u[lg * S::CS + 4 * c]);
+            v[4 * c] = t.x; v[4 * c + 1] = t.y; v[4 * c + 2] = t.z; v[4 * c + 3] = t.w;
+        }
+        fwht_group<E, LPR>(v, lane);
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < E / 4; ++c)
+            *reinterpret_cast<float4*>(&u[lg * S::CS + 4 * c]) = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = u[p2i[e]] * kout[e];  // y[k] = H(u)[P2inv[k]] * s2^{+-1}[k]/sqrt(d)
+        if (valid) store_vec<E>(out + r * D + lg * E, v);
+        __syncwarp();
+    }
+}
+
+template <int D, typename Tin, typename Tout>
+static cudaError_t launch_k1_t(const K1Params& p, int64_t n_batch, cudaStream_t st) {
+    using S = K1Shape<D>;
+    const dim3 grid((unsigned)((p.rows + S::ROWS_PER_CTA - 1) / S::ROWS_PER_CTA), (unsigned)p.n_heads,
+                    (unsigned)n_batch);
+    k1_scramble_kernel<D, Tin, Tout><<<grid, 128, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_k1_d(const K1Params& p, int xdt, int odt, int64_t n_batch, cudaStream_t st) {
+    if (xdt == SDA_BF16 && odt == SDA_BF16) return launch_k1_t<D, __nv_bfloat16, __nv_bfloat16>(p, n_batch, st);
+    if (xdt == SDA_BF16 && odt == SDA_F32) return launch_k1_t<D, __nv_bfloat16, float>(p, n_batch, st);
+    if (xdt == SDA_F32 && odt == SDA_BF16) return launch_k1_t<D, float, __nv_bfloat16>(p, n_batch, st);
+    return launch_k1_t<D, float, float>(p, n_batch, st);
+}
+
+cudaError_t launch_k1(const K1Params& p, int d, int xdt, int odt, int64_t n_batch, cudaStream_t st) {
+    switch (d) {
+        case 32: return launch_k1_d<32>(p, xdt, odt, n_batch, st);
+        case 64: return launch_k1_d<64>(p, xdt, odt, n_batch, st);
+        case 128: return launch_k1_d<128>(p, xdt, odt, n_batch, st);
+        case 256: return launch_k1_d<256>(p, xdt, odt, n_batch, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace sda

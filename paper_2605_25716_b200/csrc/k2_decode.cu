@@ -1,0 +1,156 @@
+// k2_decode.cu -- K2 (decode / few-row form): keyless split-KV partial attention.
+//
+// Replaces shard_attention(q', K', V', none) (attention.cpp:42-78) as the compute node runs
+// it in try_serve_q (protocol.cpp:1072-1095) -- without the per-call concatenation copy of
+// the domain's segments (:1073-1085): the KV shard stays resident as one [kv_cap x d] slab
+// per (request, kv head) and the kernel reads it in place.
+//
+// Decode is purely HBM-bound (each request owns its own key set, so scrambled KV is never
+// shared: ~1 flop/B for MHA). Design: one CTA per (split, q head, request x q row); 16-byte
+// streaming loads (8 elements per lane, d/8 lanes per key row, U keys in flight per lane);
+// warp-shuffle dot-product reduction; per-lane-group online softmax in f32; a final
+// shared-memory merge of the CTA's lane groups. Emits the split's locally normalised O'
+// and (row_max, exp_sum) exactly as ShardStats defines them (attention.hpp:34-41).
+#include <cmath>
+
+#include "common.cuh"
+
+namespace sda {
+
+template <int D>
+struct K2Shape {
+    static constexpr int VEC = 8;
+    static constexpr int LPR = D / VEC;          // lanes per key row
+    static constexpr int RW = 32 / LPR;          // key rows per warp step
+    static constexpr int WARPS = 4;
+    static constexpr int NG = WARPS * RW;        // lane groups per CTA
+    static constexpr int U = 4;                  // keys in flight per lane group
+};
+
+template <int D, typename TQ, typename TKV>
+__global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
+    using S = K2Shape<D>;
+    constexpr int VEC = S::VEC, LPR = S::LPR, NG = S::NG, U = S::U;
+    __shared__ float sm_m[NG], sm_s[NG];
+    __shared__ __align__(16) float sm_o[NG][D];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane / LPR, lg = lane % LPR;
+    const int grp = warp * S::RW + g;
+    const int split = blockIdx.x, h = blockIdx.y;
+    const int64_t b = (int64_t)blockIdx.z / p.q_rows, qr = (int64_t)blockIdx.z % p.q_rows;
+    const int kvh = h / (p.q_heads / p.kv_heads);
+
+    const int64_t len = p.kv_len ? (int64_t)p.kv_len[b] : p.kv_cap;
+    const int64_t chunk = (len + p.n_splits - 1) / p.n_splits;
+    const int64_t k0 = (int64_t)split * chunk;
+    const int64_t k1 = min(len, k0 + chunk);
+
+    float qv[VEC];
+    load_vec<VEC>(static_cast<const TQ*>(p.q) + ((b * p.q_heads + h) * p.q_rows + qr) * D + lg * VEC, qv);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) qv[i] *= p.scale * kLog2e;   // logits in log2 units
+
+    const TKV* kb = static_cast<const TKV*>(p.k) + ((b * p.kv_heads + kvh) * p.kv_cap) * D + lg * VEC;
+    const TKV* vb = static_cast<const TKV*>(p.v) + ((b * p.kv_heads + kvh) * p.kv_cap) * D + lg * VEC;
+
+    float m = -INFINITY, s = 0.f;
+    float o[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) o[i] = 0.f;
+
+    for (int64_t j0 = k0 + grp; j0 < k1; j0 += (int64_t)NG * U) {
+        float kf[U][VEC], vf[U][VEC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t j = j0 + (int64_t)u * NG;
+            const int64_t jj = j < k1 ? j : j0;
+            load_vec<VEC>(kb + jj * D, kf[u]);
+            load_vec<VEC>(vb + jj * D, vf[u]);
+        }
+        float l[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            float acc = 0.f;
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) acc = fmaf(qv[i], kf[u][i], acc);
+#pragma unroll
+            for (int msk = LPR / 2; msk >= 1; msk >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, msk);
+            l[u] = (j0 + (int64_t)u * NG < k1) ? acc : -INFINITY;
+        }
+        float mn = m;
+#pragma unroll
+        for (int u = 0; u < U; ++u) mn = fmaxf(mn, l[u]);
+        const float alpha = ex2(m - mn);   // m = -inf -> 0
+        s *= alpha;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) o[i] *= alpha;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float pu = ex2(l[u] - mn);
+            s += pu;
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) o[i] = fmaf(pu, vf[u][i], o[i]);
+        }
+        m = mn;
+    }
+
+    if (lg == 0) {
+        sm_m[grp] = m;
+        sm_s[grp] = s;
+    }
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) sm_o[grp][lg * VEC + i] = o[i];
+    __syncthreads();
+
+    float M = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < NG; ++i) M = fmaxf(M, sm_m[i]);
+    float S_ = 0.f;
+    float wgt[NG];
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+        wgt[i] = (M == -INFINITY) ? 0.f : ex2(sm_m[i] - M);
+        S_ = fmaf(sm_s[i], wgt[i], S_);
+    }
+    const int64_t orow = ((int64_t)split * p.n_batch * p.q_heads + b * p.q_heads + h) * p.q_rows + qr;
+    const float inv = S_ > 0.f ? 1.f / S_ : 0.f;
+    for (int dim = threadIdx.x; dim < D; dim += blockDim.x) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < NG; ++i) acc = fmaf(sm_o[i][dim], wgt[i], acc);
+        p.out_o[orow * D + dim] = acc * inv;
+    }
+    if (threadIdx.x == 0) {
+        // back to natural-log units: row_max = max_j q.k_j / sqrt(d)
+        p.out_stats[orow * 2 + 0] = S_ > 0.f ? M / kLog2e : -INFINITY;
+        p.out_stats[orow * 2 + 1] = S_;
+    }
+}
+
+template <int D, typename TQ, typename TKV>
+static cudaError_t launch_k2_t(const K2Params& p, cudaStream_t st) {
+    const dim3 grid((unsigned)p.n_splits, (unsigned)p.q_heads, (unsigned)(p.n_batch * p.q_rows));
+    k2_decode_kernel<D, TQ, TKV><<<grid, 128, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_k2_d(const K2Params& p, int qdt, int kvdt, cudaStream_t st) {
+    if (qdt == SDA_BF16 && kvdt == SDA_BF16) return launch_k2_t<D, __nv_bfloat16, __nv_bfloat16>(p, st);
+    if (qdt == SDA_F32 && kvdt == SDA_BF16) return launch_k2_t<D, float, __nv_bfloat16>(p, st);
+    if (qdt == SDA_BF16 && kvdt == SDA_F32) return launch_k2_t<D, __nv_bfloat16, float>(p, st);
+    return launch_k2_t<D, float, float>(p, st);
+}
+
+cudaError_t launch_k2_decode(const K2Params& p, int d, int qdt, int kvdt, cudaStream_t st) {
+    switch (d) {
+        case 32: return launch_k2_d<32>(p, qdt, kvdt, st);
+        case 64: return launch_k2_d<64>(p, qdt, kvdt, st);
+        case 128: return launch_k2_d<128>(p, qdt, kvdt, st);
+        case 256: return launch_k2_d<256>(p, qdt, kvdt, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace sda

@@ -1,0 +1,130 @@
+// k3_merge.cu -- K3: cross-node LSE-weighted merge + inverse token permutation + unscramble.
+//
+// Replaces, per output row, dec_output for every remote domain (scrambler.cpp:138-149:
+// O = scatter_rows(O' phi_V^{-1}, p_q), stats scattered by p_q) followed by merge_shards
+// (attention.cpp:89-123: M* = max row_max over shards with exp_sum > 0,
+// w_i = exp_sum_i exp(row_max_i - M*), O = sum w_i O_i / sum w_i), as span_finish_layer
+// composes them (protocol.cpp:926-948).
+//
+// One warp per output row (b, h, r). The scatter by p_q becomes a gather by p_q^{-1} on the
+// read side. Because phi_V^{-1} is linear, the weighted sum of every source that shares a
+// key set (the K2 splits of one domain) is accumulated in scrambled space and unscrambled
+// once per domain: one 128-point FWHT per (row, domain) instead of per split.
+// HBM-bound: reads (4d + 8) B per (row, source), writes d * sizeof(out) B per row.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace sda {
+
+template <int D>
+__device__ __forceinline__ void unscramble_acc(const uint8_t* sc, float* acc, float* out, float* sh, int lane) {
+    constexpr int E = D / 32;
+    const float* ftab = reinterpret_cast<const float*>(sc);
+    const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + 24 * D);
+    // t[i] = acc[i] / s2[i] ; u[j] = t[P2[j]] ; w = H u ; y[i] = w[P1[i]] / (s1[i] sqrt(d))
+#pragma unroll
+    for (int e = 0; e < E; ++e) sh[lane * E + e] = acc[e] * ftab[kInvIn * D + lane * E + e];
+    __syncwarp();
+    float v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = sh[utab[kP2 * D + lane * E + e]];
+    fwht_group<E, 32>(v, lane);
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; ++e) sh[lane * E + e] = v[e];
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; ++e) out[e] += sh[utab[kP1 * D + lane * E + e]] * ftab[kInvOut * D + lane * E + e];
+    __syncwarp();
+}
+
+template <int D, typename TOut>
+__global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
+    constexpr int E = D / 32;
+    __shared__ __align__(16) float sh_all[4][D];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* sh = sh_all[warp];
+    const int64_t total = p.n_batch * p.q_heads * p.q_rows;
+    const int64_t row = (int64_t)blockIdx.x * 4 + warp;
+    if (row >= total) return;
+    const int64_t r = row % p.q_rows;
+    const int64_t bh = row / p.q_rows;
+    const int h = (int)(bh % p.q_heads);
+    const int64_t b = bh / p.q_heads;
+    const int kh = h / (p.q_heads / p.key_heads);
+
+    // pass 1: M* over sources with exp_sum > 0 (attention.cpp:103-105); lanes stride sources
+    float mstar = -INFINITY;
+    for (int s = lane; s < p.n_src; s += 32) {
+        const K3Source& src = p.src[s];
+        const int64_t ri = src.pq_inv ? (int64_t)src.pq_inv[b * p.pq_bstride + r] : r;
+        const float2 st = *reinterpret_cast<const float2*>(src.stats + (bh * p.q_rows + ri) * 2);
+        if (st.y > 0.f) mstar = fmaxf(mstar, st.x);
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) mstar = fmaxf(mstar, __shfl_xor_sync(0xffffffffu, mstar, m));
+
+    float out[E], acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) out[e] = acc[e] = 0.f;
+    float denom = 0.f;
+    const bool single = p.n_src == 1;
+    bool pending = false;
+    for (int s = 0; s < p.n_src; ++s) {
+        const K3Source& src = p.src[s];
+        const int64_t ri = src.pq_inv ? (int64_t)src.pq_inv[b * p.pq_bstride + r] : r;
+        const float2 st = *reinterpret_cast<const float2*>(src.stats + (bh * p.q_rows + ri) * 2);
+        if (st.y > 0.f) {
+            const float w = single ? 1.f : st.y * expf(st.x - mstar);
+            denom += single ? st.y : w;
+            float ov[E];
+            load_vec_any<E>(src.o + (bh * p.q_rows + ri) * D + lane * E, ov);
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc[e] = fmaf(w, ov[e], acc[e]);
+            pending = true;
+        }
+        const bool group_end = (s + 1 == p.n_src) || (p.src[s + 1].keys != src.keys);
+        if (group_end && pending) {
+            if (src.keys) {
+                unscramble_acc<D>(scrambler_ptr(src.keys, p.keys_bstride, b, kh, D, 1), acc, out, sh, lane);
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) out[e] += acc[e];
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc[e] = 0.f;
+            pending = false;
+        }
+    }
+    const bool masked = !(mstar > -INFINITY);
+    if (masked && lane == 0 && p.err) atomicExch(p.err, (int32_t)SDA_ERR_MASKED_ROW);
+    const float inv = masked ? __int_as_float(0x7fc00000) : (single ? 1.f : 1.f / denom);
+#pragma unroll
+    for (int e = 0; e < E; ++e) out[e] *= inv;
+    store_vec_any<E>(static_cast<TOut*>(p.out) + row * D + lane * E, out);
+    if (p.out_stats && lane == 0) {
+        p.out_stats[row * 2 + 0] = single ? (masked ? -INFINITY : mstar) : mstar;
+        p.out_stats[row * 2 + 1] = masked ? 0.f : denom;
+    }
+}
+
+template <int D, typename TOut>
+static cudaError_t launch_k3_t(const K3Params& p, cudaStream_t st) {
+    const int64_t total = p.n_batch * p.q_heads * p.q_rows;
+    k3_merge_kernel<D, TOut><<<(unsigned)((total + 3) / 4), 128, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k3(const K3Params& p, int d, int odt, cudaStream_t st) {
+    const bool bf = odt == SDA_BF16;
+    switch (d) {
+        case 32: return bf ? launch_k3_t<32, __nv_bfloat16>(p, st) : launch_k3_t<32, float>(p, st);
+        case 64: return bf ? launch_k3_t<64, __nv_bfloat16>(p, st) : launch_k3_t<64, float>(p, st);
+        case 128: return bf ? launch_k3_t<128, __nv_bfloat16>(p, st) : launch_k3_t<128, float>(p, st);
+        case 256: return bf ? launch_k3_t<256, __nv_bfloat16>(p, st) : launch_k3_t<256, float>(p, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace sda

@@ -1,0 +1,153 @@
+"""Torch-facing wrappers over the C ABI, named after the reference operators they replace.
+
+torch is only plumbing here (device memory, the current CUDA stream); every computation is a
+call into libsdattn_b200.so. Tensors must be CUDA, contiguous, bf16 or f32.
+
+  scramble            K1  apply_phi / apply_phi_inv_t + permute_rows_gather  (scrambler.cpp:126-136)
+  partial_attention   K2  shard_attention(q', K', V', none)                  (attention.cpp:42-78)
+  unscramble_merge    K3  dec_output per source + merge_shards               (scrambler.cpp:138-149,
+                                                                             attention.cpp:89-123)
+"""
+from __future__ import annotations
+
+import ctypes as ct
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import torch
+
+from . import capi
+from .capi import check
+
+_DT = {torch.bfloat16: capi.SDA_BF16, torch.float32: capi.SDA_F32}
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype not in _DT:
+        raise TypeError(f"unsupported dtype {t.dtype} (bf16 or f32)")
+    return _DT[t.dtype]
+
+
+def _cuda(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _stream(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def upload_keys(packed: Sequence, device) -> torch.Tensor:
+    """Stack per-request packed key sets (numpy uint8) into one device tensor [B, keyset_bytes]."""
+    import numpy as np
+    arr = np.stack([np.asarray(p, np.uint8) for p in packed])
+    return torch.from_numpy(arr).to(device)
+
+
+def upload_perms(perms: Sequence, device) -> torch.Tensor:
+    """Stack per-request u32 permutations into a device int32 tensor [B, L] (same bits as u32)."""
+    import numpy as np
+    arr = np.stack([np.asarray(p, np.uint32) for p in perms]).view(np.int32)
+    return torch.from_numpy(arr).to(device)
+
+
+def scramble(x: torch.Tensor, keys: torch.Tensor, variant: int, which: int, perm: Optional[torch.Tensor] = None,
+             out: Optional[torch.Tensor] = None, out_dtype: Optional[torch.dtype] = None, out_row_offset: int = 0,
+             key_heads: Optional[int] = None, stream=None) -> torch.Tensor:
+    """K1. x [B, H, rows, d] -> out [B, H, cap, d] with out[b,h,off+i] = x[b,h,perm_b[i]] @ phi.
+
+    keys: uint8 [B, keyset_bytes] (request b's key set in row b); perm: int32/u32 [B, rows] or None.
+    """
+    _cuda(x, "x")
+    B, H, rows, d = x.shape
+    kh = key_heads if key_heads is not None else H
+    if out is None:
+        out = torch.empty((B, H, rows, d), dtype=out_dtype or x.dtype, device=x.device)
+    _cuda(out, "out")
+    _cuda(keys, "keys")
+    if perm is not None:
+        _cuda(perm, "perm")
+    check(capi.LIB.sda_scramble(_stream(stream), variant, which, x.data_ptr(), _dtype_code(x), B, H, rows, d,
+                                keys.data_ptr(), keys.stride(0) if keys.dim() > 1 else 0, kh, _ptr(perm),
+                                perm.stride(0) if perm is not None and perm.dim() > 1 else 0, out.data_ptr(),
+                                _dtype_code(out), out.shape[2], out_row_offset), "sda_scramble")
+    return out
+
+
+def partial_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, kv_len: Optional[torch.Tensor] = None,
+                      n_splits: Optional[int] = None, out_o: Optional[torch.Tensor] = None,
+                      out_stats: Optional[torch.Tensor] = None, stream=None):
+    """K2. q [B, Hq, Lq, d]; k, v [B, Hkv, cap, d]. Returns (o [S,B,Hq,Lq,d] f32, stats [S,B,Hq,Lq,2] f32)."""
+    _cuda(q, "q"), _cuda(k, "k"), _cuda(v, "v")
+    B, Hq, Lq, d = q.shape
+    Hkv, cap = k.shape[1], k.shape[2]
+    if k.dtype != v.dtype or k.shape != v.shape:
+        raise ValueError("k and v must have the same shape and dtype")
+    S = n_splits or capi.default_splits(B, Hq, Lq, cap)
+    if out_o is None:
+        out_o = torch.empty((S, B, Hq, Lq, d), dtype=torch.float32, device=q.device)
+    if out_stats is None:
+        out_stats = torch.empty((S, B, Hq, Lq, 2), dtype=torch.float32, device=q.device)
+    if kv_len is not None:
+        _cuda(kv_len, "kv_len")
+        if kv_len.dtype != torch.int32:
+            raise TypeError("kv_len must be int32")
+    check(capi.LIB.sda_partial_attention(_stream(stream), q.data_ptr(), _dtype_code(q), k.data_ptr(), v.data_ptr(),
+                                         _dtype_code(k), cap, _ptr(kv_len), B, Hq, Hkv, Lq, d, S,
+                                         out_o.data_ptr(), out_stats.data_ptr()), "sda_partial_attention")
+    return out_o, out_stats
+
+
+@dataclass
+class MergeSource:
+    """One shard for K3: o [B,Hq,Lq,d] f32, stats [B,Hq,Lq,2] f32, keys (phi_v of its domain,
+    uint8 [B, keyset_bytes]) or None for plaintext, pq_inv int32/u32 [B, Lq] or None."""
+    o: torch.Tensor
+    stats: torch.Tensor
+    keys: Optional[torch.Tensor] = None
+    pq_inv: Optional[torch.Tensor] = None
+
+
+def sources_from_splits(o: torch.Tensor, stats: torch.Tensor, keys: Optional[torch.Tensor] = None,
+                        pq_inv: Optional[torch.Tensor] = None) -> list:
+    return [MergeSource(o[s], stats[s], keys, pq_inv) for s in range(o.shape[0])]
+
+
+def unscramble_merge(sources: Sequence[MergeSource], out: Optional[torch.Tensor] = None,
+                     out_dtype: torch.dtype = torch.float32, key_heads: Optional[int] = None,
+                     out_stats: Optional[torch.Tensor] = None, err_flag: Optional[torch.Tensor] = None,
+                     stream=None) -> torch.Tensor:
+    """K3. Merged, unscrambled, inverse-permuted output [B, Hq, Lq, d]."""
+    n = len(sources)
+    if n > capi.MAX_SOURCES:
+        raise ValueError(f"at most {capi.MAX_SOURCES} sources")
+    if n == 0:
+        check(capi.LIB.sda_unscramble_merge(_stream(stream), None, 0, 0, 0, 0, 0, 1, 0, 32, None, 0, None, None),
+              "sda_unscramble_merge")
+    B, Hq, Lq, d = sources[0].o.shape
+    arr = (capi.MergeSource * n)()
+    kstride = 0
+    pstride = 0
+    for i, s in enumerate(sources):
+        _cuda(s.o, "o"), _cuda(s.stats, "stats")
+        arr[i].o, arr[i].stats = s.o.data_ptr(), s.stats.data_ptr()
+        arr[i].keys = _ptr(s.keys)
+        arr[i].pq_inv = _ptr(s.pq_inv)
+        if s.keys is not None:
+            kstride = s.keys.stride(0) if s.keys.dim() > 1 else 0
+        if s.pq_inv is not None:
+            pstride = s.pq_inv.stride(0) if s.pq_inv.dim() > 1 else 0
+    if out is None:
+        out = torch.empty((B, Hq, Lq, d), dtype=out_dtype, device=sources[0].o.device)
+    check(capi.LIB.sda_unscramble_merge(_stream(stream), arr, n, kstride, key_heads or Hq, pstride, B, Hq, Lq, d,
+                                        out.data_ptr(), _dtype_code(out), _ptr(out_stats), _ptr(err_flag)),
+          "sda_unscramble_merge")
+    return out

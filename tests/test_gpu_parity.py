@@ -1,0 +1,225 @@
+"""GPU parity: every kernel and the composed path against the CPU oracle (the reference's
+algorithm restated in C, pinned to the reference by tests/test_oracle_*.py) on identical seeded
+inputs. Tolerances (BASELINE north_star): index maps bit-exact; outputs within 1e-3 (FP32 mode)
+and 2e-2 (BF16 mode) max-abs/max|ref| per (request, head) slab and rel-Frobenius."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import C
+from paper_2605_25716_b200 import capi, ops, protocol
+from tests.gpu_helpers import Case, dev, gauss, max_abs_rel, rel_fro
+
+pytestmark = pytest.mark.gpu
+
+TOL_FP32 = 1e-3
+TOL_BF16 = 2e-2
+
+
+def _keys(B, H, d, domain=1, mode=0):
+    kh = [capi.negotiate_keyset(capi.shared_seed(1, b + 1), b + 1, 0, domain, H, d, mode=mode) for b in range(B)]
+    return kh, ops.upload_keys([k.pack() for k in kh], "cuda")
+
+
+def _sc(ks, h, which):
+    p = "kq" if which == 0 else "v"
+    return (getattr(ks, p + "_s1")[h], getattr(ks, p + "_p1")[h], getattr(ks, p + "_p2")[h], getattr(ks, p + "_s2")[h])
+
+
+@pytest.mark.parametrize("d", [32, 64, 128, 256])
+@pytest.mark.parametrize("variant,which", [(capi.PHI_FORWARD, capi.KEYS_KQ), (capi.PHI_INV_T, capi.KEYS_KQ),
+                                           (capi.PHI_FORWARD, capi.KEYS_V)])
+def test_k1_scramble_f32(d, variant, which):
+    B, H, rows = 2, 3, 77
+    kh, kd = _keys(B, H, d)
+    x = gauss(3, (B, H, rows, d))
+    perms = [kh[b].span_perm(1, 100 * b, rows) for b in range(B)]
+    out = ops.scramble(dev(x, torch.float32), kd, variant, which, ops.upload_perms(perms, "cuda"))
+    got = out.double().cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            ref = C.apply_phi(x[b, h], *_sc(kh[b], h, which), variant)[perms[b]]
+            assert max_abs_rel(got[b, h], ref) < 1e-5
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_k1_scramble_bf16_cache_write_with_offset(d):
+    """bf16 in -> bf16 cache rows [off, off+rows); other rows untouched; one RNE rounding."""
+    B, H, rows, cap, off = 2, 2, 50, 128, 33
+    kh, kd = _keys(B, H, d)
+    x = C.round_to_format(gauss(4, (B, H, rows, d)), 2)
+    perms = [kh[b].span_perm(1, off, rows) for b in range(B)]
+    cache = torch.zeros((B, H, cap, d), dtype=torch.bfloat16, device="cuda")
+    ops.scramble(dev(x, torch.bfloat16), kd, capi.PHI_INV_T, capi.KEYS_KQ, ops.upload_perms(perms, "cuda"),
+                 out=cache, out_row_offset=off)
+    got = cache.double().cpu().numpy()
+    assert not got[:, :, :off].any() and not got[:, :, off + rows:].any()
+    for b in range(B):
+        for h in range(H):
+            ref = C.round_to_format(C.apply_phi(x[b, h], *_sc(kh[b], h, 0), 1)[perms[b]], 2)
+            g = got[b, h, off:off + rows]
+            # identical except where f32 vs f64 land on opposite sides of a bf16 tie (1 ulp)
+            assert (g == ref).mean() > 0.99
+            assert np.all(np.abs(g - ref) <= 2.0**-7 * np.abs(ref) + 1e-30)
+
+
+def test_k1_gqa_key_heads():
+    B, Hq, Hkv, d, rows = 1, 8, 2, 128, 9
+    kh, kd = _keys(B, Hkv, d)
+    x = gauss(5, (B, Hq, rows, d))
+    out = ops.scramble(dev(x, torch.float32), kd, capi.PHI_FORWARD, capi.KEYS_KQ, key_heads=Hkv)
+    got = out.double().cpu().numpy()
+    for h in range(Hq):
+        ref = C.apply_phi(x[0, h], *_sc(kh[0], h // 4, 0), 0)
+        assert max_abs_rel(got[0, h], ref) < 1e-5
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("kv_dtype", [torch.float32, torch.bfloat16])
+def test_k2_partial_attention_splits_and_ragged(d, kv_dtype):
+    B, Hq, Hkv, lq, cap = 3, 4, 2, 2, 1000
+    fmt = 2 if kv_dtype == torch.bfloat16 else 1
+    q = C.round_to_format(gauss(6, (B, Hq, lq, d)), fmt)
+    k = C.round_to_format(gauss(7, (B, Hkv, cap, d)), fmt)
+    v = C.round_to_format(gauss(8, (B, Hkv, cap, d)), fmt)
+    kv_len = np.array([1000, 517, 3], np.int32)
+    n_splits = 7
+    o, st = ops.partial_attention(dev(q, kv_dtype), dev(k, kv_dtype), dev(v, kv_dtype),
+                                  torch.from_numpy(kv_len).cuda(), n_splits=n_splits)
+    o = o.double().cpu().numpy()
+    st = st.double().cpu().numpy()
+    for b in range(B):
+        L = int(kv_len[b])
+        chunk = -(-L // n_splits)
+        for h in range(Hq):
+            kk, vv = k[b, h // 2, :L], v[b, h // 2, :L]
+            for s in range(n_splits):
+                a, e = s * chunk, min(L, (s + 1) * chunk)
+                if a >= e:  # empty split: row_max = -inf, exp_sum = 0 (attention.cpp:66-67)
+                    assert np.all(st[s, b, h, :, 1] == 0) and np.all(np.isneginf(st[s, b, h, :, 0]))
+                    continue
+                ro, rm, rs = C.shard_attention(q[b, h], kk[a:e], vv[a:e])
+                assert max_abs_rel(o[s, b, h], ro) < 1e-4
+                assert np.allclose(st[s, b, h, :, 0], rm, atol=1e-5, rtol=1e-5)
+                assert np.allclose(st[s, b, h, :, 1], rs, rtol=1e-4)
+
+
+def test_k3_merge_unscramble_vs_dec_output_and_merge_shards():
+    B, H, lq, d = 2, 3, 6, 64
+    srcs, oracle_shards = [], [[] for _ in range(B * H)]
+    for i, (domain, keyed) in enumerate([(1, True), (2, True), (0, False)]):
+        o = gauss(20 + i, (B, H, lq, d))
+        m = gauss(30 + i, (B, H, lq)) * 3 + (1000.0 if i == 1 else 0.0)   # +1000 shift (test_attention.cpp:149-169)
+        s = np.abs(gauss(40 + i, (B, H, lq))) + 0.5
+        if i == 2:
+            s[0, 0, 2] = 0.0   # partially masked row in one shard
+        st = np.stack([m, s], -1)
+        kd = pqi = None
+        if keyed:
+            kh, kd = _keys(B, H, d, domain=domain)
+            pq = [kh[b].span_perm(0, 40, lq) for b in range(B)]
+            pqi = ops.upload_perms([capi.invert_permutation(p) for p in pq], "cuda")
+        srcs.append(ops.MergeSource(dev(o, torch.float32), dev(st, torch.float32), kd, pqi))
+        for b in range(B):
+            for h in range(H):
+                if keyed:
+                    od = C.apply_phi(o[b, h], *_sc(kh[b], h, 1), 2)
+                    oo, mm, ss = np.zeros_like(od), np.zeros(lq), np.zeros(lq)
+                    oo[pq[b]], mm[pq[b]], ss[pq[b]] = od, m[b, h], s[b, h]   # dec_output scatter by p_q
+                else:
+                    oo, mm, ss = o[b, h], m[b, h], s[b, h]
+                oracle_shards[b * H + h].append((oo, mm, ss))
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    got = ops.unscramble_merge(srcs, err_flag=err).double().cpu().numpy()
+    assert int(err.item()) == 0
+    for b in range(B):
+        for h in range(H):
+            sh = oracle_shards[b * H + h]
+            ref = C.merge_shards([x[0] for x in sh], [x[1] for x in sh], [x[2] for x in sh])
+            assert max_abs_rel(got[b, h], ref) < 1e-5
+
+
+def test_k3_single_source_verbatim_and_masked_row_flag():
+    B, H, lq, d = 1, 2, 4, 128
+    o = gauss(50, (B, H, lq, d))
+    st = np.stack([gauss(51, (B, H, lq)), np.abs(gauss(52, (B, H, lq))) + 1], -1)
+    got = ops.unscramble_merge([ops.MergeSource(dev(o, torch.float32), dev(st, torch.float32))]).cpu().numpy()
+    assert np.array_equal(got, o.astype(np.float32))   # one shard returned verbatim (attention.cpp:97-101)
+    st[0, 1, 3, 1] = 0.0
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    got = ops.unscramble_merge([ops.MergeSource(dev(o, torch.float32), dev(st, torch.float32))] * 2,
+                               err_flag=err).cpu().numpy()
+    assert int(err.item()) == 4  # SDA_ERR_MASKED_ROW (attention.cpp:109-110)
+    assert np.all(np.isnan(got[0, 1, 3])) and np.all(np.isfinite(got[0, 0]))
+
+
+def test_c1_toy_fp32_end_to_end():
+    """BASELINE config 1: 2 nodes, 1 layer, 8 heads x d64, 1K-token shard per node, 1 query, FP32."""
+    case = Case(B=1, Hq=8, Hkv=8, d=64, lk=1024, n_nodes=2, lq=1, dtype=torch.float32)
+    got = case.run_device(n_splits=4)
+    ref = case.oracle()
+    plain = case.plain()
+    assert max_abs_rel(got, ref) < TOL_FP32 and rel_fro(got, ref) < TOL_FP32
+    assert max_abs_rel(got, plain) < TOL_FP32 and rel_fro(got, plain) < TOL_FP32
+
+
+def test_bf16_mode_end_to_end_rounding_matched():
+    case = Case(B=2, Hq=4, Hkv=4, d=128, lk=1536, n_nodes=3, lq=1, dtype=torch.bfloat16, seed=3)
+    got = case.run_device()
+    ref = case.oracle()
+    assert max_abs_rel(got, ref) < TOL_BF16 and rel_fro(got, ref) < TOL_BF16
+    # vs plain attention: the intrinsic bf16-storage floor at mag [1/8, 8] is ~2-3e-2
+    plain = case.plain()
+    assert rel_fro(got, plain) < 4e-2
+
+
+def test_bf16_mode_vs_plain_narrow_scaling():
+    # with the scaling range narrowed to [1/2, 2] the bf16 floor vs plain attention drops below 2e-2
+    case = Case(B=1, Hq=4, Hkv=4, d=128, lk=1024, n_nodes=2, lq=1, dtype=torch.bfloat16, seed=9, mag=(0.5, 2.0))
+    got = case.run_device()
+    plain = case.plain()
+    assert max_abs_rel(got, plain) < TOL_BF16 and rel_fro(got, plain) < TOL_BF16
+
+
+def test_prefill_rows_with_token_permutations_and_gqa():
+    case = Case(B=1, Hq=8, Hkv=2, d=64, lk=300, n_nodes=2, lq=37, dtype=torch.float32, seed=5)
+    got = case.run_device(n_splits=3)
+    ref = case.oracle()
+    assert max_abs_rel(got, ref) < TOL_FP32
+
+
+def test_s1_only_mode():
+    case = Case(B=1, Hq=2, Hkv=2, d=128, lk=256, n_nodes=2, lq=1, dtype=torch.float32, mode=1)
+    assert max_abs_rel(case.run_device(), case.oracle()) < TOL_FP32
+
+
+def test_negative_control_wrong_keys_diverge():
+    """sabotage_dec (protocol.cpp:232-243): decoding with the wrong key set must NOT match."""
+    case = Case(B=1, Hq=4, Hkv=4, d=64, lk=256, n_nodes=2, lq=1, dtype=torch.float32)
+    bad = case.run_device(wrong_keys_at_finish=True)
+    assert rel_fro(bad, case.plain()) > 0.3
+
+
+def test_full_size_c2_sampled_parity():
+    """BASELINE config 2 at full size (32 heads x d128, 8K KV, batch 16, BF16): the oracle on a
+    deterministic sample of (request, head) pairs, plus a size-independent property on all pairs
+    (scrambled result == plain attention up to the bf16 storage floor, plain computed in f32)."""
+    B, H, d, L = 16, 32, 128, 8192
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    q = torch.randn((B, H, 1, d), generator=g, device="cuda").to(torch.bfloat16)
+    k = torch.randn((B, H, L, d), generator=g, device="cuda").to(torch.bfloat16)
+    v = torch.randn((B, H, L, d), generator=g, device="cuda").to(torch.bfloat16)
+    rids = [b + 1 for b in range(B)]
+    keys = protocol.DomainKeys(rids, 0, 1, H, d, "cuda")
+    shard = protocol.KVShard(B, H, L, d, "cuda")
+    shard.ship_segment(k, v, keys, first_pos=0)
+    got = protocol.scrambled_attention(q, [(keys, shard)], q_first_pos=L).double().cpu().numpy()
+    qf, kf, vf = q.float(), k.float(), v.float()
+    plain = (torch.softmax((qf @ kf.transpose(-1, -2)) / np.sqrt(d), -1) @ vf).double().cpu().numpy()
+    assert rel_fro(got, plain) < 4e-2
+    for b, h in [(0, 0), (5, 17), (15, 31), (9, 3)]:
+        ss = C.derive_seed(1, [b + 1, 0x7365656B])
+        ref = C.scrambled_step(ss, b + 1, 0, H, h, qf[b, h].double().cpu().numpy(), L,
+                               [kf[b, h].double().cpu().numpy()], [vf[b, h].double().cpu().numpy()], wire_fmt=2,
+                               shard_first_pos=[0])
+        assert max_abs_rel(got[b, h], ref) < TOL_BF16 and rel_fro(got[b, h], ref) < TOL_BF16
