@@ -20,7 +20,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -35,11 +34,11 @@ METRIC = "scrambled-attn decode tokens/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-pairs", type=int, default=64, help="(request, head) pairs in the CPU sample")
+    ap.add_argument("--cpu-pairs", type=int, default=128, help="(request, head) pairs in the CPU sample")
     return ap.parse_args()
 
 
@@ -66,79 +65,89 @@ def workload_config(n):
 # clocks during the timed region
 # ---------------------------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """Samples SM clock and clock-event (throttle) reasons through NVML every ~2 ms while the
+    timed region runs (nvidia-smi's 100 ms floor is too coarse for a sub-second region)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
         self.index = index
         self.samples = []
-        self.proc = None
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+            self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
-        except OSError:
-            self.proc = None
+        except Exception:  # noqa: BLE001
+            self.ok = False
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                self.samples.append(parts)
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self.ok:
+            self.thread.join(timeout=1)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples), "source": "NVML every ~2 ms during the timed region"}
 
 
 # ---------------------------------------------------------------------------------------------
 # reference arm / CPU baseline: the reference's own C++ (oracle/_ref) on the host cores
 # ---------------------------------------------------------------------------------------------
-def cpu_reference(n_nodes: int, pairs: int, threads: int):
+def cpu_reference(n_nodes: int, pairs: int, threads: int, steps: int = 3):
     """Times the reference composition enc Q -> shard_attention -> dec_output -> merge_shards
-    (protocol.cpp:885-948) for `pairs` (request, head) pairs of the bench workload, n_nodes shards
-    of CTX/n_nodes keys each, on `threads` host threads. Returns tokens/s (= pairs/s / heads)."""
+    (protocol.cpp:885-948) for `pairs` (request, head) pairs of the bench workload (n_nodes shards of
+    CTX/n_nodes keys each, scrambled K'/V' built once outside the timing, like the resident cache)
+    on `threads` host threads, `steps` times. Returns (per-step tokens/s list, per-step seconds):
+    tokens/s = pairs/s / heads (one token needs all heads)."""
+    import numpy as np
+
     from oracle import REF
     if REF is None:
         raise RuntimeError("oracle/_ref/libsdattn_ref.so not built")
-    t = REF.lib.ref_bench_decode(pairs, n_nodes, CTX // n_nodes, D, H, threads, 2)
-    return (pairs / t) / H, t
+    secs = np.zeros(max(steps, 1))
+    REF.lib.ref_bench_decode(pairs, n_nodes, CTX // n_nodes, D, H, threads, 2, max(steps, 1),
+                             secs.ctypes.data_as(__import__("ctypes").POINTER(__import__("ctypes").c_double)))
+    return [(pairs / t) / H for t in secs], list(secs)
 
 
 def run_reference_arm(args, ws, rank):
+    """--impl reference: the reference's own C++ hot path (oracle/_ref) on all host cores. Under
+    torchrun only rank 0 runs; the others exit without work."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    vals, walls = [], []
-    for _ in range(args.warmup):
-        cpu_reference(ws, args.cpu_pairs, threads)
-    for _ in range(args.steps):
-        v, w = cpu_reference(ws, args.cpu_pairs, threads)
-        vals.append(v)
-        walls.append(w)
+    vals, walls = cpu_reference(ws, args.cpu_pairs, threads, args.warmup + args.steps)
+    vals, walls = vals[args.warmup:], walls[args.warmup:]
     value = statistics.median(vals)
-    sample = (f"{args.cpu_pairs} (request, head) pairs of the workload per step "
-              f"({ws} shard(s) x {CTX // ws} keys, d{D}, bf16 wire), {threads} threads; tokens/s = pairs/s / {H}")
+    sample = (f"{args.cpu_pairs} (request, head) pairs of the workload per step ({ws} shard(s) x {CTX // ws} keys, "
+              f"d{D}, bf16 wire, f64 math), {threads} threads; tokens/s = pairs/s / {H} heads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(walls),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -189,46 +198,48 @@ def run_ours(args, ws, rank, local):
     inq_keys = [protocol.DomainKeys([rid(b) for b in my_reqs], 0, dom + 1, H, D, devn) for dom in range(ws)]
     q = torch.randn((B_PER, H, 1, D), generator=g, device=devn).to(torch.bfloat16)
     S = capi.default_splits(B_tot, H, 1, L)
-    qs_send = torch.empty((ws, B_PER, H, 1, D), dtype=torch.bfloat16, device=devn)
-    qs_recv = torch.empty_like(qs_send)
-    o_parts = torch.empty((S, B_tot, H, 1, D), dtype=torch.float32, device=devn)
-    st_parts = torch.empty((S, B_tot, H, 1, 2), dtype=torch.float32, device=devn)
-    o_fold = torch.empty((ws, B_PER, H, 1, D), dtype=torch.float32, device=devn)
-    st_fold = torch.empty((ws, B_PER, H, 1, 2), dtype=torch.float32, device=devn)
-    o_back = torch.empty_like(o_fold)
-    st_back = torch.empty_like(st_fold)
     out = torch.empty((B_PER, H, 1, D), dtype=torch.float32, device=devn)
     stream = torch.cuda.current_stream()
     k2_ev = []
+    record = {"on": False}
 
-    def step(qin, record=False):
-        # K1: Q' per destination domain (span_perm over one row is the identity)
-        for dom in range(ws):
-            ops.scramble(qin, inq_keys[dom].dev, capi.PHI_FORWARD, capi.KEYS_KQ, None, out=qs_send[dom],
-                         key_heads=H)
-        if ws > 1:
-            dist.all_to_all_single(qs_recv, qs_send)
-            q_all = qs_recv.view(B_tot, H, 1, D)
-        else:
-            q_all = qs_send.view(B_tot, H, 1, D)
-        if record:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        ops.partial_attention(q_all, shard.k, shard.v, shard.kv_len, n_splits=S, out_o=o_parts, out_stats=st_parts)
-        if record:
-            e1.record(stream)
-            k2_ev.append((e0, e1))
-        if ws == 1:
-            srcs = ops.sources_from_splits(o_parts, st_parts, inq_keys[0].dev, None)
+    if ws == 1:
+        q_s = torch.empty((B_PER, H, 1, D), dtype=torch.bfloat16, device=devn)
+        o_parts = torch.empty((S, B_tot, H, 1, D), dtype=torch.float32, device=devn)
+        st_parts = torch.empty((S, B_tot, H, 1, 2), dtype=torch.float32, device=devn)
+        srcs = ops.sources_from_splits(o_parts, st_parts, inq_keys[0].dev, None)
+
+        def step(qin):
+            # K1 (Q', span_perm over one row is the identity) -> K2 -> K3 (fold splits + unscramble)
+            ops.scramble(qin, inq_keys[0].dev, capi.PHI_FORWARD, capi.KEYS_KQ, None, out=q_s, key_heads=H)
+            if record["on"]:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            ops.partial_attention(q_s, shard.k, shard.v, shard.kv_len, n_splits=S, out_o=o_parts,
+                                  out_stats=st_parts)
+            if record["on"]:
+                e1.record(stream)
+                k2_ev.append((e0, e1))
             return ops.unscramble_merge(srcs, out=out, key_heads=H)
-        # fold this domain's splits in scrambled space (plain merge, no keys), then return partials
-        ops.unscramble_merge(ops.sources_from_splits(o_parts, st_parts), out=o_fold.view(B_tot, H, 1, D),
-                             out_stats=st_fold.view(B_tot, H, 1, 2))
-        dist.all_to_all_single(o_back, o_fold)
-        dist.all_to_all_single(st_back, st_fold)
-        srcs = [ops.MergeSource(o_back[dom], st_back[dom], inq_keys[dom].dev, None) for dom in range(ws)]
-        return ops.unscramble_merge(srcs, out=out, key_heads=H)
+    else:
+        from paper_2605_25716_b200 import distributed as sdist
+        bufs = sdist.StepBuffers.allocate(ws, B_PER, H, 1, D, torch.bfloat16, devn)
+        comp = sdist.gpu_rank_compute(inq_keys, shard, n_splits=S, kv_heads=H)
+        serve0 = comp.serve
+
+        def serve_timed(q_all, o_out, st_out):
+            if record["on"]:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                serve0(q_all, o_out, st_out)
+                e1.record(stream)
+                k2_ev.append((e0, e1))
+            else:
+                serve0(q_all, o_out, st_out)
+        comp.serve = serve_timed
+
+        def step(qin):
+            return sdist.scrambled_decode_step(qin, comp, bufs, out)
 
     def barrier():
         if ws > 1:
@@ -245,8 +256,10 @@ def run_ours(args, ws, rank, local):
     t1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         t0.record(stream)
+        record["on"] = True
         for _ in range(args.steps):
-            step(q, record=True)
+            step(q)
+        record["on"] = False
         t1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -309,7 +322,7 @@ def run_ours(args, ws, rank, local):
             "e2e": {"value": B_tot / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": B_PER * H * D * 2, "d2h_bytes_per_step": B_PER * H * D * 4},
             "gpu_launches": int(launches) * args.steps,
-            "roofline": {"bound": "hbm", "kernel": "k2_decode_kernel<128,bf16,bf16>", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": "k2_decode_kernel<128,bf16,bf16>" + ("" if ws == 1 else " + split fold"), "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": k2_bytes, "k2_ms": k2_ms,
                          "k2_share_of_step": k2_ms / ms_max, "peak_source": "MEASURED_PEAKS.json hbm_gbs"
@@ -319,11 +332,13 @@ def run_ours(args, ws, rank, local):
         if ws == 1 and not args.no_cpu_baseline:
             try:
                 threads = os.cpu_count() or 1
-                v, t = cpu_reference(1, args.cpu_pairs, threads)
-                line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                vals, secs = cpu_reference(1, args.cpu_pairs, threads, 5)
+                line["cpu_baseline"] = {"value": statistics.median(vals), "unit": "tokens/s", "cores": threads,
+                                        "kind": "reference",
                                         "sample": f"{args.cpu_pairs} (request, head) pairs x 8192 keys x d128 of "
                                                   f"the workload through the reference's own enc->shard_attention->"
-                                                  f"dec->merge (oracle/_ref), {t:.2f} s wall on {threads} threads"}
+                                                  f"dec->merge (oracle/_ref, f64), median of 5 steps of "
+                                                  f"{statistics.median(secs):.3f} s wall on {threads} threads"}
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "unavailable": str(e)}
         print(json.dumps(line), flush=True)

@@ -282,7 +282,7 @@ def _setup_ref(lib: ct.CDLL) -> None:
     lib.ref_round_to_format.restype = _f64
     lib.ref_round_to_format.argtypes = [_f64, ct.c_int]
     lib.ref_bench_decode.restype = _f64
-    lib.ref_bench_decode.argtypes = [_sz, _sz, _sz, _sz, _sz, ct.c_int, ct.c_int]
+    lib.ref_bench_decode.argtypes = [_sz, _sz, _sz, _sz, _sz, ct.c_int, ct.c_int, ct.c_int, _pd]
 
 
 def load_oracle() -> Oracle:

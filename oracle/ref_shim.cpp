@@ -7,6 +7,7 @@
 // source is copied into this repo) into oracle/_ref/libsdattn_ref.so.
 //
 // Nothing here is shipped: the product library never links this file.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -270,9 +271,10 @@ int ref_scrambled_step(std::uint64_t shared_seed, std::uint64_t request_id, std:
 // shards of `lk` keys, spread over `n_threads` std::threads (the reference
 // functions are pure). The scrambled K'/V' shards are
 // built once, outside the timed region (they are the resident KV cache).
-// Returns wall seconds for the timed region.
+// Runs n_steps timed steps over the same resident shards, writing each step's wall seconds to
+// step_seconds[i]; returns the median.
 double ref_bench_decode(std::size_t n_pairs, std::size_t n_nodes, std::size_t lk, std::size_t d,
-                        std::size_t n_heads, int n_threads, int wire_fmt) {
+                        std::size_t n_heads, int n_threads, int wire_fmt, int n_steps, double* step_seconds) {
     const FloatFormat wf = static_cast<FloatFormat>(wire_fmt);
     struct Pair {
         Matrix q;
@@ -331,12 +333,19 @@ double ref_bench_decode(std::size_t n_pairs, std::size_t n_nodes, std::size_t lk
             pr.out = merge_shards(shards);
         }
     };
-    const auto t0 = std::chrono::steady_clock::now();
-    std::vector<std::thread> th;
-    for (int i = 0; i < n_threads; ++i) th.emplace_back(worker);
-    for (auto& t : th) t.join();
-    const auto t1 = std::chrono::steady_clock::now();
-    return std::chrono::duration<double>(t1 - t0).count();
+    std::vector<double> times;
+    for (int step = 0; step < (n_steps > 0 ? n_steps : 1); ++step) {
+        next = 0;
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> th;
+        for (int i = 0; i < n_threads; ++i) th.emplace_back(worker);
+        for (auto& t : th) t.join();
+        const auto t1 = std::chrono::steady_clock::now();
+        times.push_back(std::chrono::duration<double>(t1 - t0).count());
+        if (step_seconds) step_seconds[step] = times.back();
+    }
+    std::sort(times.begin(), times.end());
+    return times[times.size() / 2];
 }
 
 }  // extern "C"

@@ -64,10 +64,13 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys, const
 }
 
 int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int64_t kv_cap) {
-    // Aim for >= 8 resident CTAs per SM (148 SMs) with >= 256 keys per split.
+    // Decode is HBM-bound: give the grid >= ~4 full waves of the 148 SMs (at ~8 resident CTAs
+    // per SM) so the last partial wave is a small fraction of the launch, while keeping every
+    // split >= 256 keys.
     const int64_t ctas = n_batch * q_heads * q_rows;
     if (ctas <= 0 || kv_cap <= 0) return 1;
-    const int64_t want = (148 * 8 + ctas - 1) / ctas;
+    const int64_t target = 148 * 8 * 4;
+    const int64_t want = (target + ctas - 1) / ctas;
     const int64_t max_by_len = kv_cap / 256 > 0 ? kv_cap / 256 : 1;
     int64_t s = want < max_by_len ? want : max_by_len;
     if (s < 1) s = 1;

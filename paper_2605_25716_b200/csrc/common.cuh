@@ -86,6 +86,35 @@ __device__ __forceinline__ void store_vec(float* p, const float* v) {
         *reinterpret_cast<float4*>(p + 4 * i) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
 }
 
+// Eight consecutive elements kept in their storage format until they are consumed (halves the
+// registers a bf16 load needs, so more loads can be in flight per thread).
+template <typename T>
+struct Raw8;
+
+template <>
+struct Raw8<__nv_bfloat16> {
+    uint4 w;
+    __device__ __forceinline__ void load(const __nv_bfloat16* p) { w = ld_stream(p); }
+    __device__ __forceinline__ float get(int i) const {
+        const uint32_t x = i < 2 ? w.x : i < 4 ? w.y : i < 6 ? w.z : w.w;
+        return (i & 1) ? __uint_as_float(x & 0xFFFF0000u) : __uint_as_float(x << 16);
+    }
+};
+
+template <>
+struct Raw8<float> {
+    uint4 a, b;
+    __device__ __forceinline__ void load(const float* p) {
+        a = ld_stream(p);
+        b = ld_stream(p + 4);
+    }
+    __device__ __forceinline__ float get(int i) const {
+        const uint4& t = i < 4 ? a : b;
+        const int j = i & 3;
+        return __uint_as_float(j == 0 ? t.x : j == 1 ? t.y : j == 2 ? t.z : t.w);
+    }
+};
+
 // Small-vector variants for N in {1, 2, 4, 8, 16, ...} f32 loads / any-typed stores.
 template <int N>
 __device__ __forceinline__ void load_vec_any(const float* p, float* v) {

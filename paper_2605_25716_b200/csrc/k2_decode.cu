@@ -24,7 +24,7 @@ struct K2Shape {
     static constexpr int RW = 32 / LPR;          // key rows per warp step
     static constexpr int WARPS = 4;
     static constexpr int NG = WARPS * RW;        // lane groups per CTA
-    static constexpr int U = 4;                  // keys in flight per lane group
+    static constexpr int U = 8;                  // keys in flight per lane group
 };
 
 template <int D, typename TQ, typename TKV>
@@ -59,21 +59,24 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
 #pragma unroll
     for (int i = 0; i < VEC; ++i) o[i] = 0.f;
 
-    for (int64_t j0 = k0 + grp; j0 < k1; j0 += (int64_t)NG * U) {
-        float kf[U][VEC], vf[U][VEC];
+    // The loop bound is warp-uniform (every lane of the warp runs the same trip count) so the
+    // full-mask shuffles below are always executed by all 32 lanes; rows past k1 are masked.
+    for (int64_t jw = k0 + warp * S::RW; jw < k1; jw += (int64_t)NG * U) {
+        const int64_t j0 = jw + g;
+        Raw8<TKV> kr[U], vr[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t j = j0 + (int64_t)u * NG;
-            const int64_t jj = j < k1 ? j : j0;
-            load_vec<VEC>(kb + jj * D, kf[u]);
-            load_vec<VEC>(vb + jj * D, vf[u]);
+            const int64_t jj = j < k1 ? j : k0;
+            kr[u].load(kb + jj * D);
+            vr[u].load(vb + jj * D);
         }
         float l[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             float acc = 0.f;
 #pragma unroll
-            for (int i = 0; i < VEC; ++i) acc = fmaf(qv[i], kf[u][i], acc);
+            for (int i = 0; i < VEC; ++i) acc = fmaf(qv[i], kr[u].get(i), acc);
 #pragma unroll
             for (int msk = LPR / 2; msk >= 1; msk >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, msk);
             l[u] = (j0 + (int64_t)u * NG < k1) ? acc : -INFINITY;
@@ -81,6 +84,7 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
         float mn = m;
 #pragma unroll
         for (int u = 0; u < U; ++u) mn = fmaxf(mn, l[u]);
+        if (mn == -INFINITY) continue;     // this lane group has no valid row yet (ragged tail)
         const float alpha = ex2(m - mn);   // m = -inf -> 0
         s *= alpha;
 #pragma unroll
@@ -90,7 +94,7 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
             const float pu = ex2(l[u] - mn);
             s += pu;
 #pragma unroll
-            for (int i = 0; i < VEC; ++i) o[i] = fmaf(pu, vf[u][i], o[i]);
+            for (int i = 0; i < VEC; ++i) o[i] = fmaf(pu, vr[u].get(i), o[i]);
         }
         m = mn;
     }
