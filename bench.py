@@ -31,6 +31,13 @@ H, D, CTX, B_PER = 32, 128, 8192, 16
 METRIC = "scrambled-attn decode tokens/s"
 
 
+_OUT_FD = 1
+
+
+def emit(line: dict) -> None:
+    os.write(_OUT_FD, (json.dumps(line) + "\n").encode())
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -155,7 +162,7 @@ def run_reference_arm(args, ws, rank):
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference",
                              "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------------------------
@@ -341,7 +348,7 @@ def run_ours(args, ws, rank, local):
                                                   f"{statistics.median(secs):.3f} s wall on {threads} threads"}
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "unavailable": str(e)}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if ws > 1:
         dist.destroy_process_group()
 
@@ -349,6 +356,11 @@ def run_ours(args, ws, rank, local):
 def main():
     args = parse()
     ws, rank, local = dist_env()
+    # Libraries (NCCL prints its version banner) may write to fd 1; keep stdout for the single
+    # JSON line and send everything else to stderr.
+    global _OUT_FD
+    _OUT_FD = os.dup(1)
+    os.dup2(2, 1)
     if args.gpus != ws and ws > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {ws}", file=sys.stderr)
     if args.impl == "reference":
