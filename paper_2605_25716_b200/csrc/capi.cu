@@ -2,6 +2,7 @@
 // mirrors the reference's std::invalid_argument cases, then stream-ordered kernel launches.
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -11,6 +12,12 @@ std::atomic<uint64_t> g_launches{0};
 
 bool supported_dim(int d) { return d == 32 || d == 64 || d == 128 || d == 256; }
 bool pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+// Debug knob (tests compare kernel variants): SDA_K1_SIMT=1 forces the SIMT K1.
+bool env_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return v && v[0] && v[0] != '0';
+}
+
 bool valid_dtype(int t) { return t == SDA_BF16 || t == SDA_F32; }
 
 sda_status from_cuda(cudaError_t e) {
@@ -60,6 +67,8 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys, const
     sda::K1Params p{x, out, keys, perm, keys_batch_stride, perm_batch_stride, rows, out_rows_cap, out_row_offset,
                     n_heads, key_heads, which_keys, variant == SDA_PHI_INV_T ? 1 : 0};
     ++g_launches;
+    if (sda::k1_tc_eligible(p, head_dim, x_dtype, out_dtype) && !env_flag("SDA_K1_SIMT"))
+        return from_cuda(sda::launch_k1_tc(p, head_dim, n_batch, static_cast<cudaStream_t>(stream)));
     return from_cuda(sda::launch_k1(p, head_dim, x_dtype, out_dtype, n_batch, static_cast<cudaStream_t>(stream)));
 }
 

@@ -1,0 +1,391 @@
+// k1_tc.cu -- K1 on the 5th-generation tensor cores: scramble + token permutation as a
+// tcgen05 GEMM with a signed-diagonal-times-±1 B operand, cp.async row gather into swizzled
+// SMEM, TMEM accumulators and a TMA store.
+//
+// Replaces apply_phi / apply_phi_inv_t + permute_rows_gather (scrambler.cpp:42-85,
+// permutation.cpp:58-67) for the large, bf16 case: the context owner's KV shipping
+// (protocol.cpp:993-1001) and prefill Q (protocol.cpp:885-891).
+//
+// With R = 1/sqrt(d) and the raw Sylvester matrix, x phi = ((x o s1) M) o (s2 R) where
+//   M[i][n] = (-1)^popcount(P1[i] & P2^{-1}[n])
+// (P1 and P2 collapse into the sign pattern), and the inverse-transpose uses
+// 1/s1 and R/s2 with the same M. M is exact in bf16; diag(s1) M is split into bf16 hi + lo
+// (16 significant bits), so D = x B_hi + x B_lo in f32 is accurate to ~2^-17 before the single
+// RNE rounding to bf16 -- the same numerics as the f64 reference up to that rounding.
+//
+// Per CTA (persistent, one per SM, a contiguous run of 128-row tiles of one or more
+// (request, head) slabs), warp-specialised, 9 warps:
+//   warps 4-7 (loaders) : cp.async 16-byte chunks of the gathered input rows perm[r] straight
+//                         into a SWIZZLE_128B K-major A stage (4 stages); completion is signalled
+//                         with cp.async.mbarrier.arrive.noinc on the stage's `full` barrier;
+//   warp 8     (MMA)    : one lane issues 2 x d/16 tcgen05.mma (M=128, N=d, K=16) into one of
+//                         two TMEM accumulators; tcgen05.commit frees the A stage and hands the
+//                         accumulator to the epilogue;
+//   warps 0-3 (epilogue): tcgen05.ld -> bf16 -> swizzled SMEM -> TMA tensor
+//                         store (a tile's output rows are contiguous in the cache), masked plain
+//                         stores on a partial tile; they also (re)build B when the key set changes.
+// B folds both diagonals: B[n][i] = (-1)^popc(P1[i] & P2inv[n]) * s1^{+-1}[i] * s2^{+-1}[n] R,
+// split into bf16 hi + lo (16 significant bits), so x needs no prologue and the epilogue no
+// scaling: D = x B_hi^T + x B_lo^T in f32 (~2^-17 relative) -> one RNE rounding to bf16.
+// HBM-bound: 2 x 128 x d x 2 B per tile vs 2 x 128 x d x d x 2 flop (128 flop/B at d=128, below
+// the 258 flop/B ridge).
+#include "common.cuh"
+#include "tc_util.cuh"
+
+#include <algorithm>
+
+namespace sda {
+
+struct K1TcParams {
+    const __nv_bfloat16* x;
+    __nv_bfloat16* out;
+    const uint8_t* keys;
+    const uint32_t* perm;
+    int64_t keys_bstride;
+    int64_t perm_bstride;
+    int64_t rows;
+    int64_t out_rows_cap;
+    int64_t out_row_offset;
+    int n_heads;
+    int key_heads;
+    int which;
+    int inv_t;
+    int64_t tiles_per_slab;
+    int64_t total_tiles;
+    int64_t tiles_per_cta;
+};
+
+template <int D>
+struct K1TcShape {
+    static constexpr int TILE = 128;
+    static constexpr int STAGES = 4;
+    static constexpr int ROW_BYTES = D * 2;
+    static constexpr int TILE_BYTES = TILE * ROW_BYTES;      // one bf16 tile (A stage / out staging)
+    static constexpr int KB = D / 64;                        // 64-wide K (or N) blocks
+    static constexpr int BLK_BYTES = TILE * 128;             // one [128 x 64] swizzled block of A
+    static constexpr int BBLK_BYTES = D * 128;               // one [D x 64] swizzled block of B
+    static constexpr int OFF_A = 0;                          // STAGES x A
+    static constexpr int OFF_BHI = OFF_A + STAGES * TILE_BYTES;
+    static constexpr int OFF_BLO = OFF_BHI + D * D * 2;
+    static constexpr int OFF_OUT = OFF_BLO + D * D * 2;      // output staging
+    static constexpr int OFF_BAR = OFF_OUT + TILE_BYTES;
+    static constexpr int NBAR = 2 * STAGES + 4 + 2;          // full, empty, tmem_full, tmem_empty, bfree, bready
+    static constexpr int SMEM = OFF_BAR + 8 * NBAR + 16;
+    static constexpr uint32_t TMEM_COLS = 2 * D;
+    static constexpr int THREADS = 288;
+    static constexpr int LOADERS = 128;                      // warps 4-7
+};
+
+template <int D>
+__global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const __grid_constant__ CUtensorMap out_map) {
+    using S = K1TcShape<D>;
+    constexpr int ST = S::STAGES;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* const a_base = smem + S::OFF_A;
+    uint8_t* const b_hi = smem + S::OFF_BHI;
+    uint8_t* const b_lo = smem + S::OFF_BLO;
+    uint8_t* const ostg = smem + S::OFF_OUT;
+    uint64_t* const full = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
+    uint64_t* const empty = full + ST;
+    uint64_t* const tfull = empty + ST;
+    uint64_t* const tempty = tfull + 2;
+    uint64_t* const bfree = tempty + 2;
+    uint64_t* const bready = bfree + 1;
+    uint32_t* const tmem_slot = reinterpret_cast<uint32_t*>(bready + 1);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t first = (int64_t)blockIdx.x * p.tiles_per_cta;
+    const int64_t last = min(first + p.tiles_per_cta, p.total_tiles);
+    if (first >= last) return;
+    const int64_t ntiles = last - first;
+    const int H = p.n_heads;
+    const int G = H / p.key_heads;
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < ST; ++s) {
+            tc::mbar_init(&full[s], S::LOADERS);
+            tc::mbar_init(&empty[s], 1);
+        }
+        tc::mbar_init(&tfull[0], 1);
+        tc::mbar_init(&tfull[1], 1);
+        tc::mbar_init(&tempty[0], 128);
+        tc::mbar_init(&tempty[1], 128);
+        tc::mbar_init(bfree, 1);
+        tc::mbar_init(bready, 128);
+        tc::fence_mbar_init();
+        tc::prefetch_tmap(&out_map);
+    }
+    if (warp == 0) tc::tmem_alloc<S::TMEM_COLS>(tmem_slot);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    auto tile_rows = [&](int64_t id) -> int {
+        const int64_t rem = p.rows - (id % p.tiles_per_slab) * S::TILE;
+        return (int)(rem < S::TILE ? rem : (int64_t)S::TILE);
+    };
+    auto kslab_of = [&](int64_t id) -> int64_t {
+        const int64_t slab = id / p.tiles_per_slab;
+        return (slab / H) * p.key_heads + (slab % H) / G;
+    };
+    constexpr int CPR = D / 8;   // 16-byte chunks per row
+
+    if (warp >= 4 && warp < 8) {
+        // ------------------------------------------------------------------ loaders
+        const int lt = tid - 128;                  // 0..127
+        constexpr int RSTEP = S::LOADERS / CPR, NR = S::TILE / RSTEP;
+        const int c = lt % CPR, r0 = lt / CPR;
+        // source rows of a tile for this thread (-1: past the segment end); fetched two tiles
+        // ahead so the perm-load latency overlaps earlier tiles' copies
+        auto fetch_src = [&](int64_t it, int32_t* src) {
+            const int64_t id = first + it;
+            const int64_t slab = id / p.tiles_per_slab, t = id % p.tiles_per_slab;
+            const int nrows = tile_rows(id);
+            const uint32_t* pm = p.perm ? p.perm + (slab / H) * p.perm_bstride + t * S::TILE : nullptr;
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                const int r = r0 + k * RSTEP;
+                src[k] = r < nrows ? (pm ? (int32_t)__ldg(pm + r) : (int32_t)(t * S::TILE + r)) : -1;
+            }
+        };
+        int32_t cur[NR], nxt[NR], nxt2[NR];
+        fetch_src(0, cur);
+        if (1 < ntiles) fetch_src(1, nxt);
+        for (int64_t it = 0; it < ntiles; ++it) {
+            const int st = (int)(it % ST);
+            if (it + 2 < ntiles) fetch_src(it + 2, nxt2);
+            if (it >= ST) tc::mbar_wait(&empty[st], (uint32_t)(((it / ST) - 1) & 1));
+            const int64_t slab = (first + it) / p.tiles_per_slab;
+            const __nv_bfloat16* xs = p.x + slab * p.rows * D + c * 8;
+            uint8_t* a = a_base + st * S::TILE_BYTES + (c >> 3) * S::BLK_BYTES;
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                const int r = r0 + k * RSTEP;
+                if (cur[k] >= 0) tc::cp_async16(a + tc::sw128_off(r, c & 7), xs + (int64_t)cur[k] * D);
+            }
+            tc::cp_async_arrive_noinc(&full[st]);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                cur[k] = nxt[k];
+                nxt[k] = nxt2[k];
+            }
+        }
+    } else if (warp == 8) {
+        // ------------------------------------------------------------------ MMA issuer
+        constexpr uint32_t IDESC = tc::idesc_bf16_f32(128, D, false, false);
+        const uint32_t bh = tc::smem_u32(b_hi), bl = tc::smem_u32(b_lo);
+        int64_t cur = -1;
+        uint32_t nbuild = 0;
+        for (int64_t it = 0; it < ntiles; ++it) {
+            const int st = (int)(it % ST), acc = (int)(it & 1);
+            const int64_t ks = kslab_of(first + it);
+            if (ks != cur) {
+                if (it > 0 && lane == 0) tc::mma_commit(bfree);   // old B free once prior MMAs finish
+                tc::mbar_wait(bready, nbuild & 1);
+                ++nbuild;
+                cur = ks;
+            }
+            tc::mbar_wait(&full[st], (uint32_t)((it / ST) & 1));
+            if (it >= 2) tc::mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) - 1) & 1));
+            tc::fence_proxy_async_smem();          // cp.async (generic proxy) -> tcgen05 (async proxy)
+            tc::tc_fence_after();
+            if (lane == 0) {
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * D);
+                const uint32_t a = tc::smem_u32(a_base + st * S::TILE_BYTES);
+#pragma unroll
+                for (int k = 0; k < D / 16; ++k) {
+                    const uint32_t aoff = (k >> 2) * S::BLK_BYTES + (k & 3) * 32;   // 64-wide K block, 16-elem step
+                    const uint32_t boff = (k >> 2) * S::BBLK_BYTES + (k & 3) * 32;
+                    tc::mma_bf16_ss(d_tmem, tc::sw128_desc(a + aoff, 16, 1024), tc::sw128_desc(bh + boff, 16, 1024),
+                                    IDESC, k > 0 ? 1u : 0u);
+                    tc::mma_bf16_ss(d_tmem, tc::sw128_desc(a + aoff, 16, 1024), tc::sw128_desc(bl + boff, 16, 1024),
+                                    IDESC, 1u);
+                }
+                tc::mma_commit(&empty[st]);
+                tc::mma_commit(&tfull[acc]);
+            }
+            __syncwarp();
+        }
+    } else if (warp < 4) {
+        // ------------------------------------------------------------------ epilogue (+ B build)
+        const int row = tid;                       // TMEM lane = tile row
+        int64_t cur = -1;
+        uint32_t nbuild = 0;
+        for (int64_t it = 0; it < ntiles; ++it) {
+            const int64_t id = first + it;
+            const int acc = (int)(it & 1);
+            const int64_t ks = kslab_of(id);
+            if (ks != cur) {
+                if (it > 0) tc::mbar_wait(bfree, (nbuild - 1) & 1);
+                const int64_t slab = id / p.tiles_per_slab;
+                const int64_t b = slab / H;
+                const uint8_t* sc = p.keys + b * p.keys_bstride + (int64_t)((slab % H) / G) * 64 * D +
+                                    (int64_t)p.which * 32 * D;
+                const float* fin = reinterpret_cast<const float*>(sc) + (p.inv_t ? kInInvT : kInFwd) * D;
+                const float* fout = reinterpret_cast<const float*>(sc) + (p.inv_t ? kOutInvT : kOutFwd) * D;
+                const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + 24 * D);
+                for (int e = tid; e < D * CPR; e += 128) {
+                    const int n = e / CPR, c = e % CPR;   // B row n (output column), K chunk c
+                    const uint32_t pn = utab[kP2Inv * D + n];
+                    const float on = fout[n];
+                    uint4 hv, lv;
+                    uint32_t* hw = reinterpret_cast<uint32_t*>(&hv);
+                    uint32_t* lw = reinterpret_cast<uint32_t*>(&lv);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int i0 = 8 * c + 2 * j, i1 = i0 + 1;
+                        const float v0 = ((__popc(utab[kP1 * D + i0] & pn) & 1) ? -fin[i0] : fin[i0]) * on;
+                        const float v1 = ((__popc(utab[kP1 * D + i1] & pn) & 1) ? -fin[i1] : fin[i1]) * on;
+                        hw[j] = tc::pack_bf16(v0, v1);
+                        float h0, h1;
+                        bf16x2_to_f2(hw[j], h0, h1);
+                        lw[j] = tc::pack_bf16(v0 - h0, v1 - h1);
+                    }
+                    const uint32_t off = (c >> 3) * S::BBLK_BYTES + tc::sw128_off(n, c & 7);
+                    *reinterpret_cast<uint4*>(b_hi + off) = hv;
+                    *reinterpret_cast<uint4*>(b_lo + off) = lv;
+                }
+                tc::fence_proxy_async_smem();
+                tc::mbar_arrive(bready);
+                ++nbuild;
+                cur = ks;
+            }
+            // the output staging is free once the previous tile's TMA store has read it
+            if (tid == 0) tc::bulk_wait_read0();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            tc::mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
+            tc::tc_fence_after();
+            uint8_t* o = ostg;
+#pragma unroll
+            for (int cc = 0; cc < D / 16; ++cc) {
+                uint32_t r[16];
+                tc::tmem_ld16(tmem_base + (uint32_t)(acc * D + cc * 16) + ((uint32_t)(warp * 32) << 16), r);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    uint4 w;
+                    w.x = tc::pack_bf16(__uint_as_float(r[half * 8 + 0]), __uint_as_float(r[half * 8 + 1]));
+                    w.y = tc::pack_bf16(__uint_as_float(r[half * 8 + 2]), __uint_as_float(r[half * 8 + 3]));
+                    w.z = tc::pack_bf16(__uint_as_float(r[half * 8 + 4]), __uint_as_float(r[half * 8 + 5]));
+                    w.w = tc::pack_bf16(__uint_as_float(r[half * 8 + 6]), __uint_as_float(r[half * 8 + 7]));
+                    const int c8 = cc * 2 + half;
+                    *reinterpret_cast<uint4*>(o + (c8 >> 3) * S::BLK_BYTES + tc::sw128_off(row, c8 & 7)) = w;
+                }
+            }
+            tc::tc_fence_before();
+            tc::mbar_arrive(&tempty[acc]);          // accumulator may be overwritten
+            tc::fence_proxy_async_smem();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int64_t slab = id / p.tiles_per_slab, t = id % p.tiles_per_slab;
+            const int nrows = tile_rows(id);
+            const int64_t orow0 = slab * p.out_rows_cap + p.out_row_offset + t * S::TILE;
+            if (nrows == S::TILE) {
+                if (tid == 0) {
+#pragma unroll
+                    for (int cb = 0; cb < S::KB; ++cb)
+                        tc::tma_store_2d(&out_map, o + cb * S::BLK_BYTES, cb * 64, (int)orow0);
+                    tc::bulk_commit();
+                }
+            } else if (tid < nrows) {  // partial tile: never write past the segment
+#pragma unroll
+                for (int c8 = 0; c8 < CPR; ++c8)
+                    *reinterpret_cast<uint4*>(p.out + (orow0 + tid) * D + c8 * 8) =
+                        *reinterpret_cast<const uint4*>(o + (c8 >> 3) * S::BLK_BYTES + tc::sw128_off(tid, c8 & 7));
+            }
+        }
+        if (tid == 0) tc::bulk_wait0();
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    if (warp == 0) tc::tmem_dealloc<S::TMEM_COLS>(tmem_base);
+}
+
+// ------------------------------------------------------------------------------------------ host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+    return fn;
+}
+
+// 2D bf16 tensor map over a row-major [rows x cols] matrix, box {64, box_rows}, 128B swizzle.
+bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int D>
+static cudaError_t launch_k1_tc_d(const K1Params& q, int64_t n_batch, cudaStream_t st) {
+    using S = K1TcShape<D>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k1_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    K1TcParams p;
+    p.x = static_cast<const __nv_bfloat16*>(q.x);
+    p.out = static_cast<__nv_bfloat16*>(q.out);
+    p.keys = static_cast<const uint8_t*>(q.keys);
+    p.perm = q.perm;
+    p.keys_bstride = q.keys_bstride;
+    p.perm_bstride = q.perm_bstride;
+    p.rows = q.rows;
+    p.out_rows_cap = q.out_rows_cap;
+    p.out_row_offset = q.out_row_offset;
+    p.n_heads = q.n_heads;
+    p.key_heads = q.key_heads;
+    p.which = q.which;
+    p.inv_t = q.inv_t;
+    p.tiles_per_slab = (q.rows + 127) / 128;
+    p.total_tiles = p.tiles_per_slab * n_batch * q.n_heads;
+    const int64_t grid = std::min<int64_t>(p.total_tiles, num_sms());
+    p.tiles_per_cta = (p.total_tiles + grid - 1) / grid;
+    const int64_t ngrid = (p.total_tiles + p.tiles_per_cta - 1) / p.tiles_per_cta;
+    CUtensorMap map;
+    if (!make_tmap_bf16_2d(&map, q.out, n_batch * q.n_heads * q.out_rows_cap, D, 128)) return cudaErrorInvalidValue;
+    k1_tc_kernel<D><<<(unsigned)ngrid, S::THREADS, S::SMEM, st>>>(p, map);
+    return cudaGetLastError();
+}
+
+bool k1_tc_eligible(const K1Params& p, int d, int xdt, int odt) {
+    return xdt == SDA_BF16 && odt == SDA_BF16 && (d == 64 || d == 128) && p.rows >= 128;
+}
+
+cudaError_t launch_k1_tc(const K1Params& p, int d, int64_t n_batch, cudaStream_t st) {
+    if (d == 64) return launch_k1_tc_d<64>(p, n_batch, st);
+    if (d == 128) return launch_k1_tc_d<128>(p, n_batch, st);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace sda

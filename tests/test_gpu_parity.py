@@ -60,7 +60,7 @@ def test_k1_scramble_bf16_cache_write_with_offset(d):
             g = got[b, h, off:off + rows]
             # identical except where f32 vs f64 land on opposite sides of a bf16 tie (1 ulp)
             assert (g == ref).mean() > 0.99
-            assert np.all(np.abs(g - ref) <= 2.0**-7 * np.abs(ref) + 1e-30)
+            assert np.all(np.abs(g - ref) <= 2.0**-7 * np.abs(ref) + 1e-5 * np.abs(ref).max())
 
 
 def test_k1_gqa_key_heads():
