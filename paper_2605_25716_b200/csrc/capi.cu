@@ -1,5 +1,6 @@
 // capi.cu -- the extern "C" boundary (include/sdattn_b200.h): argument validation that
 // mirrors the reference's std::invalid_argument cases, then stream-ordered kernel launches.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -12,7 +13,8 @@ std::atomic<uint64_t> g_launches{0};
 
 bool supported_dim(int d) { return d == 32 || d == 64 || d == 128 || d == 256; }
 bool pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
-// Debug knob (tests compare kernel variants): SDA_K1_SIMT=1 forces the SIMT K1.
+// Debug knobs (tests compare kernel variants): SDA_K1_SIMT=1 / SDA_K2_SIMT=1 force the SIMT
+// K1 / K2 kernels.
 bool env_flag(const char* name) {
     const char* v = std::getenv(name);
     return v && v[0] && v[0] != '0';
@@ -73,11 +75,28 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys, const
 }
 
 int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int64_t kv_cap) {
+    if (n_batch <= 0 || q_heads <= 0 || q_rows <= 0 || kv_cap <= 0) return 1;
+    if (q_rows >= 64) {
+        // prefill (tcgen05 kernel, one CTA per SM per 256 query rows): pick the split count whose
+        // grid fills the last wave of 148 SMs best, at least 4 KV tiles per split
+        const int64_t units = ((q_rows + 255) / 256) * q_heads * n_batch;
+        const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(8, (kv_cap / 128) / 4));
+        int32_t best = 1;
+        double best_eff = -1.0;
+        for (int64_t s = 1; s <= max_s; ++s) {
+            const double waves = (double)(units * s) / 148.0;
+            const double eff = waves / std::ceil(waves) - (s > 1 ? 0.01 * (double)s : 0.0);  // small merge cost
+            if (eff > best_eff + 1e-9) {
+                best_eff = eff;
+                best = (int32_t)s;
+            }
+        }
+        return best;
+    }
     // Decode is HBM-bound: give the grid >= ~4 full waves of the 148 SMs (at ~8 resident CTAs
     // per SM) so the last partial wave is a small fraction of the launch, while keeping every
     // split >= 256 keys.
     const int64_t ctas = n_batch * q_heads * q_rows;
-    if (ctas <= 0 || kv_cap <= 0) return 1;
     const int64_t target = 148 * 8 * 4;
     const int64_t want = (target + ctas - 1) / ctas;
     const int64_t max_by_len = kv_cap / 256 > 0 ? kv_cap / 256 : 1;
@@ -103,6 +122,8 @@ sda_status sda_partial_attention(void* stream, const void* q, int32_t q_dtype, c
     sda::K2Params p{q, k, v, kv_len, out_o, out_stats, kv_cap, n_batch, q_rows, q_heads, kv_heads, n_splits,
                     (float)(1.0 / std::sqrt((double)head_dim))};
     ++g_launches;
+    if (sda::k2_prefill_tc_eligible(p, head_dim, q_dtype, kv_dtype) && !env_flag("SDA_K2_SIMT"))
+        return from_cuda(sda::launch_k2_prefill_tc(p, static_cast<cudaStream_t>(stream)));
     return from_cuda(sda::launch_k2_decode(p, head_dim, q_dtype, kv_dtype, static_cast<cudaStream_t>(stream)));
 }
 

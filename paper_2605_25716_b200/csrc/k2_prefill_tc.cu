@@ -1,0 +1,333 @@
+// k2_prefill_tc.cu -- K2 prefill form on the 5th-generation tensor cores: keyless partial
+// attention over the scrambled KV shard for many query rows (flash attention with tcgen05).
+//
+// Replaces shard_attention(q', K', V', none) (attention.cpp:42-78) when the delegated span has
+// many rows (prefill; try_serve_q, protocol.cpp:1072-1095). The mask is always `none` for
+// delegated shards. Output per split: locally normalised O' (f32) and the
+// reference's (row_max, exp_sum) statistics, exactly like the decode kernel.
+//
+// One CTA = two 128-row Q tiles of one (request, q head) x one KV split; 10 warps:
+//   warp 8      TMA producer: Q0/Q1 once, then K_j / V_j tiles (128 keys) into 2-stage rings
+//   warp 9      MMA issuer (one lane): S_g = Q_g K_j^T (SS, K-major) into TMEM, and
+//               O_g += P_g V_j with P_g read straight from TMEM (TS form; V as an MN-major B)
+//   warps 0-3   softmax for Q tile 0, warps 4-7 for Q tile 1 (thread = row = TMEM lane):
+//               tcgen05.ld S, online softmax in the log2 domain, P in bf16 written back over
+//               S with tcgen05.st; lazy rescaling of O (only when the running max grows by
+//               more than 2^8, FA4-style) so most tiles never touch O.
+// The issue order S0(j) S1(j) PV0(j) S0(j+1) PV1(j) S1(j+1) ... ping-pongs the two softmax
+// groups so the tensor pipe always has the other tile's work queued. TMEM: S0|S1|O0|O1 =
+// 4 x 128 columns (P_g aliases the first 64 columns of S_g).
+#include <cmath>
+
+#include "common.cuh"
+#include "tc_util.cuh"
+
+namespace sda {
+
+struct K2TcParams {
+    int64_t q_rows;        // Lq
+    int64_t kv_cap;
+    const int32_t* kv_len;
+    float* out_o;
+    float* out_stats;
+    int64_t n_batch;
+    int q_heads;
+    int kv_heads;
+    int n_splits;
+    int n_qpairs;          // ceil(Lq / 256)
+    float scale_log2;      // log2(e) / sqrt(d)
+};
+
+namespace k2tc {
+constexpr int D = 128;
+constexpr int TILE = 128;
+constexpr int TILE_BYTES = TILE * D * 2;          // 32 KB bf16 tile
+constexpr int BLK = TILE * 128;                   // [128 x 64] swizzled block (16 KB)
+constexpr int OFF_Q0 = 0, OFF_Q1 = OFF_Q0 + TILE_BYTES;
+constexpr int OFF_K = OFF_Q1 + TILE_BYTES;        // 2 stages
+constexpr int OFF_V = OFF_K + 2 * TILE_BYTES;     // 2 stages
+constexpr int OFF_BAR = OFF_V + 2 * TILE_BYTES;
+// barriers: q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], o_final[2]
+constexpr int NBAR = 15;
+constexpr int SMEM = OFF_BAR + NBAR * 8 + 16;
+constexpr int THREADS = 320;
+constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 384;
+}  // namespace k2tc
+
+__global__ void __launch_bounds__(320, 1)
+k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+                     const __grid_constant__ CUtensorMap vmap) {
+    using namespace k2tc;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* const bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* const q_full = bars;
+    uint64_t* const k_full = bars + 1;
+    uint64_t* const k_empty = bars + 3;
+    uint64_t* const v_full = bars + 5;
+    uint64_t* const v_empty = bars + 7;
+    uint64_t* const s_full = bars + 9;
+    uint64_t* const p_full = bars + 11;
+    uint64_t* const o_final = bars + 13;
+    uint32_t* const tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // work unit: blockIdx.x = q pair, blockIdx.y = q head, blockIdx.z = request * n_splits + split
+    const int qp = blockIdx.x, h = blockIdx.y;
+    const int64_t b = blockIdx.z / p.n_splits;
+    const int split = blockIdx.z % p.n_splits;
+    const int kvh = h / (p.q_heads / p.kv_heads);
+    const int64_t len = p.kv_len ? (int64_t)p.kv_len[b] : p.kv_cap;
+    // split ranges aligned to whole 128-key tiles
+    const int64_t ntile_all = (len + TILE - 1) / TILE;
+    const int64_t tps = (ntile_all + p.n_splits - 1) / p.n_splits;
+    const int64_t t0 = (int64_t)split * tps;
+    const int64_t t1 = min(ntile_all, t0 + tps);
+    const int64_t nkv = t1 > t0 ? t1 - t0 : 0;
+    const int64_t k_end = min(len, t1 * TILE);      // keys >= k_end are masked
+
+    if (tid == 0) {
+        tc::mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&k_full[i], 1);
+            tc::mbar_init(&k_empty[i], 1);
+            tc::mbar_init(&v_full[i], 1);
+            tc::mbar_init(&v_empty[i], 1);
+            tc::mbar_init(&s_full[i], 1);
+            tc::mbar_init(&p_full[i], 128);
+            tc::mbar_init(&o_final[i], 1);
+        }
+        tc::fence_mbar_init();
+    }
+    if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const int64_t qrow0 = ((b * p.q_heads + h) * p.q_rows) + (int64_t)qp * 2 * TILE;   // global row in qmap
+    const int64_t kvrow0 = ((b * p.kv_heads + kvh) * p.kv_cap) + t0 * TILE;
+
+    if (warp == 8) {
+        // ------------------------------------------------------------------ TMA producer
+        if (lane == 0 && nkv > 0) {
+            tc::prefetch_tmap(&qmap);
+            tc::prefetch_tmap(&kmap);
+            tc::prefetch_tmap(&vmap);
+            tc::mbar_arrive_expect_tx(q_full, 2 * TILE_BYTES);
+            for (int g = 0; g < 2; ++g)
+                for (int kb = 0; kb < 2; ++kb)
+                    tc::tma_load_2d(smem + (g ? OFF_Q1 : OFF_Q0) + kb * BLK, &qmap, kb * 64, (int)(qrow0 + g * TILE), q_full);
+            for (int64_t j = 0; j < nkv; ++j) {
+                const int st = (int)(j & 1);
+                const uint32_t ph = (uint32_t)(((j >> 1) - 1) & 1);
+                if (j >= 2) tc::mbar_wait(&k_empty[st], ph);
+                tc::mbar_arrive_expect_tx(&k_full[st], TILE_BYTES);
+                for (int kb = 0; kb < 2; ++kb)
+                    tc::tma_load_2d(smem + OFF_K + st * TILE_BYTES + kb * BLK, &kmap, kb * 64, (int)(kvrow0 + j * TILE), &k_full[st]);
+                if (j >= 2) tc::mbar_wait(&v_empty[st], ph);
+                tc::mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
+                for (int kb = 0; kb < 2; ++kb)
+                    tc::tma_load_2d(smem + OFF_V + st * TILE_BYTES + kb * BLK, &vmap, kb * 64, (int)(kvrow0 + j * TILE), &v_full[st]);
+            }
+        }
+    } else if (warp == 9) {
+        // ------------------------------------------------------------------ MMA issuer
+        if (lane == 0 && nkv > 0) {
+            constexpr uint32_t IDESC_S = tc::idesc_bf16_f32(128, 128, false, false);   // Q K^T, both K-major
+            constexpr uint32_t IDESC_O = tc::idesc_bf16_f32(128, 128, false, true);    // P V, V MN-major
+            const uint32_t q0 = tc::smem_u32(smem + OFF_Q0), q1 = tc::smem_u32(smem + OFF_Q1);
+            const uint32_t kbase = tc::smem_u32(smem + OFF_K), vbase = tc::smem_u32(smem + OFF_V);
+            auto issue_s = [&](int g, int64_t j) {
+                const int st = (int)(j & 1);
+                const uint32_t qa = g ? q1 : q0;
+                const uint32_t kb = kbase + st * TILE_BYTES;
+                const uint32_t d_tmem = tmem + (g ? COL_S1 : COL_S0);
+#pragma unroll
+                for (int k = 0; k < D / 16; ++k) {
+                    const uint32_t off = (k >> 2) * BLK + (k & 3) * 32;
+                    tc::mma_bf16_ss(d_tmem, tc::sw128_desc(qa + off, 16, 1024), tc::sw128_desc(kb + off, 16, 1024), IDESC_S,
+                                    k > 0 ? 1u : 0u);
+                }
+                tc::mma_commit(&s_full[g]);
+            };
+            auto issue_pv = [&](int g, int64_t j) {
+                const int st = (int)(j & 1);
+                const uint32_t vb = vbase + st * TILE_BYTES;
+                const uint32_t d_tmem = tmem + (g ? COL_O1 : COL_O0);
+                const uint32_t p_tmem = tmem + (g ? COL_S1 : COL_S0);
+#pragma unroll
+                for (int k = 0; k < TILE / 16; ++k)   // 16 keys per step: P columns 8k.., V rows 16k..
+                    tc::mma_bf16_ts(d_tmem, p_tmem + k * 8, tc::sw128_desc(vb + k * 2048, BLK, 1024), IDESC_O,
+                                    (j > 0 || k > 0) ? 1u : 0u);
+            };
+            tc::mbar_wait(q_full, 0);
+            tc::mbar_wait(&k_full[0], 0);
+            tc::tc_fence_after();
+            issue_s(0, 0);
+            issue_s(1, 0);
+            tc::mma_commit(&k_empty[0]);
+            for (int64_t j = 0; j < nkv; ++j) {
+                const int st = (int)(j & 1);
+                const uint32_t ph = (uint32_t)((j >> 1) & 1);
+                tc::mbar_wait(&v_full[st], ph);
+                tc::mbar_wait(&p_full[0], (uint32_t)(j & 1));
+                tc::tc_fence_after();
+                issue_pv(0, j);
+                if (j + 1 == nkv) tc::mma_commit(&o_final[0]);
+                if (j + 1 < nkv) {
+                    const int sn = (int)((j + 1) & 1);
+                    tc::mbar_wait(&k_full[sn], (uint32_t)(((j + 1) >> 1) & 1));
+                    tc::tc_fence_after();
+                    issue_s(0, j + 1);
+                }
+                tc::mbar_wait(&p_full[1], (uint32_t)(j & 1));
+                tc::tc_fence_after();
+                issue_pv(1, j);
+                tc::mma_commit(&v_empty[st]);
+                if (j + 1 == nkv) tc::mma_commit(&o_final[1]);
+                if (j + 1 < nkv) {
+                    issue_s(1, j + 1);
+                    tc::mma_commit(&k_empty[(j + 1) & 1]);
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------------ softmax groups
+        const int g = warp >> 2;                               // Q tile
+        const int row = (warp & 3) * 32 + lane;                // TMEM lane = tile row
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t s_col = tmem + (g ? COL_S1 : COL_S0) + lane_off;
+        const uint32_t o_col = tmem + (g ? COL_O1 : COL_O0) + lane_off;
+        float m_run = -INFINITY, m_use = -INFINITY, l = 0.f;
+        for (int64_t j = 0; j < nkv; ++j) {
+            tc::mbar_wait(&s_full[g], (uint32_t)(j & 1));
+            tc::tc_fence_after();
+            uint32_t s[128];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) tc::tmem_ld16(s_col + c * 16, s + c * 16);
+            tc::tmem_ld_wait();
+            const int64_t valid = k_end - (t0 + j) * TILE;      // keys of this tile still in range
+            float mt = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 128; ++i) {
+                float x = __uint_as_float(s[i]) * p.scale_log2;
+                x = (i < valid) ? x : -INFINITY;
+                s[i] = __float_as_uint(x);
+                mt = fmaxf(mt, x);
+            }
+            const float m_new = fmaxf(m_run, mt);
+            m_run = m_new;
+            // lazy rescale: keep the exponent base unless the max grew by more than 8 (x256)
+            const bool need = m_new > m_use + 8.f;
+            if (__any_sync(0xffffffffu, need && j > 0 && m_use > -INFINITY)) {
+                const float alpha = (need && m_use > -INFINITY) ? ex2(m_use - m_new) : 1.f;
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    uint32_t o[8];
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                                 : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(o[6]),
+                                   "=r"(o[7])
+                                 : "r"(o_col + c * 8));
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                    tc::tmem_st8(o_col + c * 8, o);
+                }
+                tc::tmem_st_wait();
+            }
+            if (need) {
+                if (m_use > -INFINITY) l *= ex2(m_use - m_new);
+                m_use = m_new;
+            }
+            const float mu = (m_use == -INFINITY) ? 0.f : m_use;
+            float ls = 0.f;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {   // P packed in place: s[i] <- bf16x2(p[2i], p[2i+1])
+                const float p0 = ex2(__uint_as_float(s[2 * i]) - mu);
+                const float p1 = ex2(__uint_as_float(s[2 * i + 1]) - mu);
+                ls += p0 + p1;
+                s[i] = tc::pack_bf16(p0, p1);
+            }
+            l += ls;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) tc::tmem_st8(s_col + c * 8, s + c * 8);
+            tc::tmem_st_wait();
+            tc::tc_fence_before();
+            tc::mbar_arrive(&p_full[g]);
+        }
+        // epilogue: O / l, (row_max, exp_sum) in natural units
+        const int64_t qrow = (int64_t)qp * 2 * TILE + g * TILE + row;
+        const bool store = qrow < p.q_rows;
+        const int64_t orow = (((int64_t)split * p.n_batch + b) * p.q_heads + h) * p.q_rows + qrow;
+        if (nkv > 0) {
+            tc::mbar_wait(&o_final[g], 0);
+            tc::tc_fence_after();
+        }
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            uint32_t o[16];
+            if (nkv > 0) {
+                tc::tmem_ld16(o_col + c * 16, o);
+                tc::tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) o[e] = 0u;
+            }
+            if (store) {
+                float4* dst = reinterpret_cast<float4*>(p.out_o + orow * D + c * 16);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                         __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+            }
+        }
+        if (store) {
+            const bool any = l > 0.f;
+            p.out_stats[orow * 2 + 0] = any ? m_run / kLog2e : -INFINITY;
+            p.out_stats[orow * 2 + 1] = any ? l * ex2(m_use - m_run) : 0.f;
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
+
+bool k2_prefill_tc_eligible(const K2Params& p, int d, int qdt, int kvdt) {
+    return d == 128 && qdt == SDA_BF16 && kvdt == SDA_BF16 && p.q_rows >= 64;
+}
+
+cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
+    using namespace k2tc;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k2_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    K2TcParams p;
+    p.q_rows = q.q_rows;
+    p.kv_cap = q.kv_cap;
+    p.kv_len = q.kv_len;
+    p.out_o = q.out_o;
+    p.out_stats = q.out_stats;
+    p.n_batch = q.n_batch;
+    p.q_heads = q.q_heads;
+    p.kv_heads = q.kv_heads;
+    p.n_splits = q.n_splits;
+    p.n_qpairs = (int)((q.q_rows + 2 * TILE - 1) / (2 * TILE));
+    p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+    CUtensorMap qm, km, vm;
+    if (!make_tmap_bf16_2d(&qm, q.q, q.n_batch * q.q_heads * q.q_rows, D, TILE) ||
+        !make_tmap_bf16_2d(&km, q.k, q.n_batch * q.kv_heads * q.kv_cap, D, TILE) ||
+        !make_tmap_bf16_2d(&vm, q.v, q.n_batch * q.kv_heads * q.kv_cap, D, TILE))
+        return cudaErrorInvalidValue;
+    const dim3 grid((unsigned)p.n_qpairs, (unsigned)q.q_heads, (unsigned)(q.n_batch * q.n_splits));
+    k2_prefill_tc_kernel<<<grid, THREADS, SMEM, st>>>(p, qm, km, vm);
+    return cudaGetLastError();
+}
+
+}  // namespace sda

@@ -1,0 +1,85 @@
+"""K2 prefill on tcgen05 (k2_prefill_tc.cu): partial attention for many query rows against the
+oracle's shard_attention (per split), the SIMT kernel, and the composed scrambled prefill."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import C
+from paper_2605_25716_b200 import ops
+from tests.gpu_helpers import Case, dev, gauss, max_abs_rel, rel_fro
+
+pytestmark = pytest.mark.gpu
+
+
+def _k2(q, k, v, kv_len, n_splits, simt=False):
+    old = os.environ.get("SDA_K2_SIMT")
+    if simt:
+        os.environ["SDA_K2_SIMT"] = "1"
+    else:
+        os.environ.pop("SDA_K2_SIMT", None)
+    try:
+        o, st = ops.partial_attention(dev(q, torch.bfloat16), dev(k, torch.bfloat16), dev(v, torch.bfloat16),
+                                      torch.from_numpy(np.asarray(kv_len, np.int32)).cuda(), n_splits=n_splits)
+        torch.cuda.synchronize()
+        return o.double().cpu().numpy(), st.double().cpu().numpy()
+    finally:
+        if old is None:
+            os.environ.pop("SDA_K2_SIMT", None)
+        else:
+            os.environ["SDA_K2_SIMT"] = old
+
+
+@pytest.mark.parametrize("lq,cap,kv_len,n_splits,hq,hkv", [
+    (128, 1024, [1024], 1, 2, 2),
+    (300, 1000, [1000, 517], 3, 4, 2),
+    (64, 4096, [4096], 2, 2, 1),
+    (256, 2048, [129, 2048], 4, 2, 2),
+    (513, 384, [384], 1, 1, 1),
+])
+def test_prefill_tc_vs_oracle(lq, cap, kv_len, n_splits, hq, hkv):
+    B, d = len(kv_len), 128
+    q = C.round_to_format(gauss(31, (B, hq, lq, d)), 2)
+    k = C.round_to_format(gauss(32, (B, hkv, cap, d)), 2)
+    v = C.round_to_format(gauss(33, (B, hkv, cap, d)), 2)
+    o, st = _k2(q, k, v, kv_len, n_splits)
+    G = hq // hkv
+    for b in range(B):
+        L = kv_len[b]
+        ntile = -(-L // 128)
+        tps = -(-ntile // n_splits)
+        for h in range(hq):
+            for s in range(n_splits):
+                a, e = s * tps * 128, min(L, (s + 1) * tps * 128)
+                if a >= e:
+                    assert np.all(st[s, b, h, :, 1] == 0)
+                    continue
+                ro, rm, rs = C.shard_attention(q[b, h], k[b, h // G, a:e], v[b, h // G, a:e])
+                # P is rounded to bf16 before the PV product (as every tensor-core flash kernel)
+                assert max_abs_rel(o[s, b, h], ro) < 1e-2, (b, h, s)
+                assert rel_fro(o[s, b, h], ro) < 5e-3
+                assert np.allclose(st[s, b, h, :, 0], rm, atol=1e-3)
+                assert np.allclose(st[s, b, h, :, 1], rs, rtol=5e-3)
+
+
+def test_prefill_tc_matches_simt_merged():
+    B, H, lq, cap, d = 1, 2, 200, 3000, 128
+    q = C.round_to_format(gauss(41, (B, H, lq, d)), 2) * 2
+    k = C.round_to_format(gauss(42, (B, H, cap, d)), 2)
+    v = C.round_to_format(gauss(43, (B, H, cap, d)), 2)
+    a_o, a_s = _k2(q, k, v, [cap], 3)
+    b_o, b_s = _k2(q, k, v, [cap], 3, simt=True)
+    merged = []
+    for o, s in ((a_o, a_s), (b_o, b_s)):
+        w = s[..., 1] * np.exp(s[..., 0] - s[..., 0].max(0))
+        merged.append((o * w[..., None]).sum(0) / w.sum(0)[..., None])
+    assert max_abs_rel(merged[0], merged[1]) < 1e-2 and rel_fro(merged[0], merged[1]) < 5e-3
+
+
+def test_scrambled_prefill_end_to_end_tc():
+    """2 domains x 640-key shards, 300-row prefill span with p_q / p_kv permutations, bf16."""
+    case = Case(B=1, Hq=4, Hkv=2, d=128, lk=640, n_nodes=2, lq=300, dtype=torch.bfloat16, seed=21)
+    got = case.run_device(n_splits=2)
+    ref = case.oracle()
+    assert max_abs_rel(got, ref) < 2e-2 and rel_fro(got, ref) < 2e-2
