@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the cfg3 prefill sub-measurement")
     ap.add_argument("--cpu-pairs", type=int, default=128, help="(request, head) pairs in the CPU sample")
     return ap.parse_args()
 
@@ -336,6 +337,11 @@ def run_ours(args, ws, rank, local):
                          if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"},
             "clocks": clk.summary(),
         }
+        if ws == 1 and not args.no_prefill:
+            try:
+                line["prefill"] = run_prefill(devn, 10, 3, peaks)
+            except Exception as e:  # noqa: BLE001
+                line["prefill"] = {"unavailable": str(e)}
         if ws == 1 and not args.no_cpu_baseline:
             try:
                 threads = os.cpu_count() or 1
@@ -351,6 +357,77 @@ def run_ours(args, ws, rank, local):
         emit(line)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def run_prefill(devn, steps: int, warmup: int, peaks: dict):
+    """BASELINE config 3 per GPU: a 2048-token prefill span against a 16K-token scrambled shard,
+    32 heads x d128, bf16. One step = the span's own K/V scrambled + permuted into the cache
+    (K1, fused into the KV write), its Q scrambled (K1), tcgen05 partial attention over the
+    shard (K2) and the LSE merge + unscramble (K3). Returns the JSON object for the line."""
+    import torch
+
+    from paper_2605_25716_b200 import capi, ops, protocol
+
+    LQ, LK = 2048, 16384
+    keys = protocol.DomainKeys([1], 0, 1, H, D, devn)
+    shard = protocol.KVShard(1, H, LK + LQ, D, devn, torch.bfloat16)
+    g = torch.Generator(device=devn).manual_seed(7)
+    kp = torch.randn((1, H, LK, D), generator=g, device=devn).to(torch.bfloat16)
+    vp = torch.randn((1, H, LK, D), generator=g, device=devn).to(torch.bfloat16)
+    shard.ship_segment(kp, vp, keys, first_pos=0)
+    q = torch.randn((1, H, LQ, D), generator=g, device=devn).to(torch.bfloat16)
+    kn = torch.randn((1, H, LQ, D), generator=g, device=devn).to(torch.bfloat16)
+    vn = torch.randn((1, H, LQ, D), generator=g, device=devn).to(torch.bfloat16)
+    pq, pq_inv = keys.span_perms(0, LK, LQ)
+    pkv, _ = keys.span_perms(1, LK, LQ)
+    S = capi.default_splits(1, H, LQ, LK)
+    kv16k = torch.full((1,), LK, dtype=torch.int32, device=devn)   # the delegated shard (earlier context)
+    qs = torch.empty_like(q)
+    o = torch.empty((S, 1, H, LQ, D), dtype=torch.float32, device=devn)
+    st = torch.empty((S, 1, H, LQ, 2), dtype=torch.float32, device=devn)
+    out = torch.empty((1, H, LQ, D), dtype=torch.float32, device=devn)
+    srcs = ops.sources_from_splits(o, st, keys.dev, pq_inv)
+    stream = torch.cuda.current_stream()
+    ev = []
+
+    def step(rec):
+        # the span's K/V go into the cache rows after the shard (scramble + permute fused into the write)
+        ops.scramble(kn, keys.dev, capi.PHI_INV_T, capi.KEYS_KQ, pkv, out=shard.k, out_row_offset=LK, key_heads=H)
+        ops.scramble(vn, keys.dev, capi.PHI_FORWARD, capi.KEYS_V, pkv, out=shard.v, out_row_offset=LK, key_heads=H)
+        ops.scramble(q, keys.dev, capi.PHI_FORWARD, capi.KEYS_KQ, pq, out=qs, key_heads=H)
+        if rec:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        # delegated shards are strictly earlier context: attend the resident 16K rows (mask none)
+        ops.partial_attention(qs, shard.k, shard.v, kv16k, n_splits=S, out_o=o, out_stats=st)
+        if rec:
+            e1.record(stream)
+            ev.append((e0, e1))
+        ops.unscramble_merge(srcs, out=out, key_heads=H)
+
+    for _ in range(warmup):
+        step(False)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        step(True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    k2_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    flops = 4.0 * LQ * LK * H * D
+    peak = float(peaks.get("bf16_tflops", 1590.0))
+    tf_k2 = flops / (k2_ms * 1e-3) / 1e12
+    return {"metric": "scrambled-attn prefill TFLOP/s", "value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "ms_per_step": ms, "steps": steps, "warmup": warmup,
+            "config": {"workload": "BASELINE cfg3 per GPU: 2K-token prefill span vs 16K-token scrambled KV shard "
+                                   "(+ the span's own 2K K/V rows scrambled into the cache), 32 heads x d128, bf16",
+                       "q_rows": LQ, "kv_rows": LK, "kv_rows_written": LQ, "heads": H, "head_dim": D, "splits": S},
+            "flops_per_step": flops,
+            "roofline": {"bound": "tensor", "kernel": "k2_prefill_tc_kernel", "achieved": tf_k2, "peak": peak,
+                         "unit": "TFLOP/s", "frac": tf_k2 / peak, "k2_ms": k2_ms, "k2_share_of_step": k2_ms / ms,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"}}
 
 
 def main():
