@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true", help="skip the cfg3 prefill sub-measurement")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=None,
+                    help="replay the step as a CUDA graph (default: on for N=1, off for N>1)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false")
     ap.add_argument("--cpu-pairs", type=int, default=128, help="(request, head) pairs in the CPU sample")
     return ap.parse_args()
 
@@ -177,6 +180,8 @@ def run_ours(args, ws, rank, local):
 
     torch.cuda.set_device(local)
     devn = torch.device("cuda", local)
+    if args.graph is None:
+        args.graph = ws == 1
     if ws > 1:
         dist.init_process_group("nccl", device_id=devn)
     B_tot = B_PER * ws
@@ -257,6 +262,19 @@ def run_ours(args, ws, rank, local):
     for _ in range(args.warmup):
         step(q)
     torch.cuda.synchronize()
+    c0 = capi.launch_count()
+    step(q)
+    launches_per_step = capi.launch_count() - c0
+    run = lambda: step(q)  # noqa: E731
+    if args.graph:
+        # the whole layer step (kernels + NCCL all-to-alls) captured once and replayed: no host
+        # launch gaps between the short kernels around K2
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step(q)
+        graph.replay()
+        torch.cuda.synchronize()
+        run = graph.replay
     barrier()
     torch.cuda.synchronize()
     l0 = capi.launch_count()
@@ -264,15 +282,22 @@ def run_ours(args, ws, rank, local):
     t1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         t0.record(stream)
-        record["on"] = True
+        record["on"] = not args.graph
         for _ in range(args.steps):
-            step(q)
+            run()
         record["on"] = False
         t1.record(stream)
         torch.cuda.synchronize()
     barrier()
-    launches = (capi.launch_count() - l0) // args.steps
+    launches = (capi.launch_count() - l0) // args.steps if not args.graph else launches_per_step
     ms = t0.elapsed_time(t1) / args.steps
+    if args.graph:
+        # K2 duration: the same launch, event-bracketed on the same stream, back to back
+        record["on"] = True
+        for _ in range(max(10, args.steps // 10)):
+            step(q)
+        record["on"] = False
+        torch.cuda.synchronize()
     k2_ms = statistics.mean(a.elapsed_time(b) for a, b in k2_ev)
     ms_max = ms
     if ws > 1:
@@ -283,16 +308,30 @@ def run_ours(args, ws, rank, local):
     # ---- end to end through the public API with host buffers -----------------------------------
     q_host = q.cpu().pin_memory()
     out_host = torch.empty((B_PER, H, 1, D), dtype=torch.float32).pin_memory()
+    q_dev = torch.empty_like(q)
+
+    def e2e_step():
+        q_dev.copy_(q_host, non_blocking=True)
+        out_host.copy_(step(q_dev), non_blocking=True)
+
     for _ in range(2):
-        out_host.copy_(step(q_host.to(devn, non_blocking=True)), non_blocking=True)
+        e2e_step()
     torch.cuda.synchronize()
+    run_e2e = e2e_step
+    if args.graph:
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2):
+            e2e_step()
+        g2.replay()
+        torch.cuda.synchronize()
+        run_e2e = g2.replay
     barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        out_host.copy_(step(q_host.to(devn, non_blocking=True)), non_blocking=True)
+        run_e2e()
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
@@ -329,7 +368,7 @@ def run_ours(args, ws, rank, local):
             "config": workload_config(ws),
             "e2e": {"value": B_tot / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": B_PER * H * D * 2, "d2h_bytes_per_step": B_PER * H * D * 4},
-            "gpu_launches": int(launches) * args.steps,
+            "gpu_launches": int(launches) * args.steps, "cuda_graph": bool(args.graph),
             "roofline": {"bound": "hbm", "kernel": "k2_decode_kernel<128,bf16,bf16>" + ("" if ws == 1 else " + split fold"), "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": k2_bytes, "k2_ms": k2_ms,
@@ -356,7 +395,12 @@ def run_ours(args, ws, rank, local):
                 line["cpu_baseline"] = {"value": None, "unavailable": str(e)}
         emit(line)
     if ws > 1:
-        dist.destroy_process_group()
+        torch.cuda.synchronize()
+        dist.barrier(device_ids=[local])
+        # leave without tearing NCCL down (communicator teardown can stall at exit); all work is done
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
 
 
 def run_prefill(devn, steps: int, warmup: int, peaks: dict):
