@@ -141,6 +141,7 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys,
  *   out_o     : f32 [n_splits][n_batch][q_heads][q_rows][d]
  *   out_stats : f32 [n_splits][n_batch][q_heads][q_rows][2]
  *   q_heads must be a multiple of kv_heads (GQA: q head h reads kv head h / (q_heads/kv_heads)).
+ *   Split s covers keys [s*T, min(len, (s+1)*T)) with T = 128 * ceil(ceil(len/128) / n_splits).
  *   The logit scale is 1/sqrt(d) (attention.cpp:45). Rows with no key in a split get
  *   row_max = -inf, exp_sum = 0, O' = 0 (attention.cpp:66-67).
  * ------------------------------------------------------------------------------------------ */
@@ -149,8 +150,11 @@ sda_status sda_partial_attention(void* stream, const void* q, int32_t q_dtype,
                                  const int32_t* kv_len, int64_t n_batch, int32_t q_heads,
                                  int32_t kv_heads, int64_t q_rows, int32_t head_dim, int32_t n_splits,
                                  float* out_o, float* out_stats);
-/* Splits sda_partial_attention would choose for a full-GPU decode launch. */
+/* Split count sized for a full-GPU launch of sda_partial_attention (MHA shapes). */
 int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int64_t kv_cap);
+/* Same, aware of GQA (q_heads > kv_heads) and of which kernel the shape dispatches to. */
+int32_t sda_default_splits_gqa(int64_t n_batch, int32_t q_heads, int32_t kv_heads, int64_t q_rows,
+                               int64_t kv_cap, int32_t head_dim);
 
 /* ------------------------------------------------------------------------------------------
  * K3  cross-node LSE-weighted merge + inverse token permutation + unscramble.

@@ -27,7 +27,7 @@ STATUS_NAMES = {0: "SDA_OK", 1: "SDA_ERR_INVALID_ARGUMENT", 2: "SDA_ERR_NOT_POW2
 # Every symbol include/sdattn_b200.h declares (checked by tests/test_capi_load.py).
 EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_negotiate_keyset",
            "sda_span_perm", "sda_invert_permutation", "sda_keyset_bytes", "sda_pack_keyset", "sda_scramble",
-           "sda_partial_attention", "sda_default_splits", "sda_unscramble_merge", "sda_abi_version",
+           "sda_partial_attention", "sda_default_splits", "sda_default_splits_gqa", "sda_unscramble_merge", "sda_abi_version",
            "sda_status_string", "sda_launch_count")
 
 
@@ -82,6 +82,8 @@ def _load() -> ct.CDLL:
                                           ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int32, _vp, _vp]
     lib.sda_default_splits.restype = ct.c_int32
     lib.sda_default_splits.argtypes = [ct.c_int64, ct.c_int32, ct.c_int64, ct.c_int64]
+    lib.sda_default_splits_gqa.restype = ct.c_int32
+    lib.sda_default_splits_gqa.argtypes = [ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32]
     lib.sda_unscramble_merge.argtypes = [_vp, ct.POINTER(MergeSource), ct.c_int32, ct.c_int64, ct.c_int32,
                                          ct.c_int64, ct.c_int64, ct.c_int32, ct.c_int64, ct.c_int32, _vp, ct.c_int32,
                                          _vp, _vp]
@@ -184,5 +186,8 @@ def keyset_bytes(n_heads: int, head_dim: int) -> int:
     return int(LIB.sda_keyset_bytes(n_heads, head_dim))
 
 
-def default_splits(n_batch: int, q_heads: int, q_rows: int, kv_cap: int) -> int:
-    return int(LIB.sda_default_splits(n_batch, q_heads, q_rows, kv_cap))
+def default_splits(n_batch: int, q_heads: int, q_rows: int, kv_cap: int, kv_heads: int = None,
+                   head_dim: int = 128) -> int:
+    if kv_heads is None:
+        return int(LIB.sda_default_splits(n_batch, q_heads, q_rows, kv_cap))
+    return int(LIB.sda_default_splits_gqa(n_batch, q_heads, kv_heads, q_rows, kv_cap, head_dim))

@@ -106,6 +106,30 @@ int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int
     return (int32_t)s;
 }
 
+int32_t sda_default_splits_gqa(int64_t n_batch, int32_t q_heads, int32_t kv_heads, int64_t q_rows, int64_t kv_cap,
+                               int32_t head_dim) {
+    if (n_batch <= 0 || q_heads <= 0 || kv_heads <= 0 || q_rows <= 0 || kv_cap <= 0) return 1;
+    const int64_t G = q_heads / kv_heads;
+    if (head_dim == 128 && G > 1 && G * q_rows <= 128 && q_rows < 64) {
+        // grouped tensor-core decode: one CTA per (request, kv head, split), >= 4 KV tiles per split
+        const int64_t units = n_batch * kv_heads;
+        const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(64, (kv_cap / 128) / 4));
+        int32_t best = 1;
+        double best_eff = -1.0;
+        for (int64_t s = 1; s <= max_s; ++s) {
+            const double waves = (double)(units * s) / 148.0;
+            // prefer >= 2 waves, then the fullest last wave
+            const double eff = std::min(1.0, waves / 2.0) * (waves / std::ceil(waves));
+            if (eff > best_eff + 1e-9) {
+                best_eff = eff;
+                best = (int32_t)s;
+            }
+        }
+        return best;
+    }
+    return sda_default_splits(n_batch, q_heads, q_rows, kv_cap);
+}
+
 sda_status sda_partial_attention(void* stream, const void* q, int32_t q_dtype, const void* k, const void* v,
                                  int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int64_t n_batch,
                                  int32_t q_heads, int32_t kv_heads, int64_t q_rows, int32_t head_dim,

@@ -42,7 +42,9 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
     const int kvh = h / (p.q_heads / p.kv_heads);
 
     const int64_t len = p.kv_len ? (int64_t)p.kv_len[b] : p.kv_cap;
-    const int64_t chunk = (len + p.n_splits - 1) / p.n_splits;
+    // splits are whole 128-key tiles (the same ranges as the tensor-core kernels)
+    const int64_t tiles = (len + 127) / 128;
+    const int64_t chunk = ((tiles + p.n_splits - 1) / p.n_splits) * 128;
     const int64_t k0 = (int64_t)split * chunk;
     const int64_t k1 = min(len, k0 + chunk);
 

@@ -6,7 +6,9 @@
 // delegated shards. Output per split: locally normalised O' (f32) and the
 // reference's (row_max, exp_sum) statistics, exactly like the decode kernel.
 //
-// One CTA = two 128-row Q tiles of one (request, q head) x one KV split; 10 warps:
+// One CTA = up to two 128-row Q tiles of one (request, q head) x one KV split -- or, for GQA
+// decode ("grouped" mode), the G q heads x L_q rows of one (request, kv head), so K/V stream
+// from HBM once per group instead of once per q head; 10 warps:
 //   warp 8      TMA producer: Q0/Q1 once, then K_j / V_j tiles (128 keys) into 2-stage rings
 //   warp 9      MMA issuer (one lane): S_g = Q_g K_j^T (SS, K-major) into TMEM, and
 //               O_g += P_g V_j with P_g read straight from TMEM (TS form; V as an MN-major B)
@@ -34,7 +36,9 @@ struct K2TcParams {
     int q_heads;
     int kv_heads;
     int n_splits;
-    int n_qpairs;          // ceil(Lq / 256)
+    int n_qpairs;          // ceil(Lq / 256) (normal mode)
+    int grouped;           // 1: GQA decode mode, one CTA per (request, kv head): its G = Hq/Hkv
+                           //    q heads x Lq rows (contiguous in Q) form the Q tile
     float scale_log2;      // log2(e) / sqrt(d)
 };
 
@@ -71,11 +75,18 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
     uint32_t* const tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // work unit: blockIdx.x = q pair, blockIdx.y = q head, blockIdx.z = request * n_splits + split
-    const int qp = blockIdx.x, h = blockIdx.y;
+    // work unit: blockIdx.z = request * n_splits + split;
+    //   normal : blockIdx.x = 256-row pair of Q tiles, blockIdx.y = q head
+    //   grouped: blockIdx.y = kv head; the tile rows are its G q heads x Lq rows
     const int64_t b = blockIdx.z / p.n_splits;
     const int split = blockIdx.z % p.n_splits;
-    const int kvh = h / (p.q_heads / p.kv_heads);
+    const int G = p.q_heads / p.kv_heads;
+    const int kvh = p.grouped ? (int)blockIdx.y : (int)blockIdx.y / G;
+    const int64_t head_row = p.grouped ? (b * p.q_heads + (int64_t)kvh * G) * p.q_rows
+                                       : (b * p.q_heads + blockIdx.y) * p.q_rows + (int64_t)blockIdx.x * 2 * TILE;
+    const int64_t nrows = p.grouped ? (int64_t)G * p.q_rows
+                                    : min((int64_t)2 * TILE, p.q_rows - (int64_t)blockIdx.x * 2 * TILE);
+    const bool two = nrows > TILE;                  // second Q tile in use
     const int64_t len = p.kv_len ? (int64_t)p.kv_len[b] : p.kv_cap;
     // split ranges aligned to whole 128-key tiles
     const int64_t ntile_all = (len + TILE - 1) / TILE;
@@ -104,7 +115,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    const int64_t qrow0 = ((b * p.q_heads + h) * p.q_rows) + (int64_t)qp * 2 * TILE;   // global row in qmap
+    const int64_t qrow0 = head_row;                       // global row of this CTA's first Q row
     const int64_t kvrow0 = ((b * p.kv_heads + kvh) * p.kv_cap) + t0 * TILE;
 
     if (warp == 8) {
@@ -113,8 +124,8 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             tc::prefetch_tmap(&qmap);
             tc::prefetch_tmap(&kmap);
             tc::prefetch_tmap(&vmap);
-            tc::mbar_arrive_expect_tx(q_full, 2 * TILE_BYTES);
-            for (int g = 0; g < 2; ++g)
+            tc::mbar_arrive_expect_tx(q_full, (two ? 2 : 1) * TILE_BYTES);
+            for (int g = 0; g < (two ? 2 : 1); ++g)
                 for (int kb = 0; kb < 2; ++kb)
                     tc::tma_load_2d(smem + (g ? OFF_Q1 : OFF_Q0) + kb * BLK, &qmap, kb * 64, (int)(qrow0 + g * TILE), q_full);
             for (int64_t j = 0; j < nkv; ++j) {
@@ -164,7 +175,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             tc::mbar_wait(&k_full[0], 0);
             tc::tc_fence_after();
             issue_s(0, 0);
-            issue_s(1, 0);
+            if (two) issue_s(1, 0);
             tc::mma_commit(&k_empty[0]);
             for (int64_t j = 0; j < nkv; ++j) {
                 const int st = (int)(j & 1);
@@ -173,13 +184,16 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 tc::mbar_wait(&p_full[0], (uint32_t)(j & 1));
                 tc::tc_fence_after();
                 issue_pv(0, j);
+                if (!two) tc::mma_commit(&v_empty[st]);
                 if (j + 1 == nkv) tc::mma_commit(&o_final[0]);
                 if (j + 1 < nkv) {
                     const int sn = (int)((j + 1) & 1);
                     tc::mbar_wait(&k_full[sn], (uint32_t)(((j + 1) >> 1) & 1));
                     tc::tc_fence_after();
                     issue_s(0, j + 1);
+                    if (!two) tc::mma_commit(&k_empty[sn]);
                 }
+                if (!two) continue;
                 tc::mbar_wait(&p_full[1], (uint32_t)(j & 1));
                 tc::tc_fence_after();
                 issue_pv(1, j);
@@ -195,13 +209,22 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
         // ------------------------------------------------------------------ softmax groups
         const int g = warp >> 2;                               // Q tile
         const int row = (warp & 3) * 32 + lane;                // TMEM lane = tile row
+        const int64_t tile_row0 = (int64_t)g * TILE + (warp & 3) * 32;
+        const bool group_live = g == 0 || two;
+        // warps whose 32 rows are all past the CTA's rows only keep the barrier protocol going
+        const bool warp_live = tile_row0 < nrows;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const uint32_t s_col = tmem + (g ? COL_S1 : COL_S0) + lane_off;
         const uint32_t o_col = tmem + (g ? COL_O1 : COL_O0) + lane_off;
         float m_run = -INFINITY, m_use = -INFINITY, l = 0.f;
-        for (int64_t j = 0; j < nkv; ++j) {
+        for (int64_t j = 0; group_live && j < nkv; ++j) {
             tc::mbar_wait(&s_full[g], (uint32_t)(j & 1));
             tc::tc_fence_after();
+            if (!warp_live) {
+                tc::tc_fence_before();
+                tc::mbar_arrive(&p_full[g]);
+                continue;
+            }
             uint32_t s[128];
 #pragma unroll
             for (int c = 0; c < 8; ++c) tc::tmem_ld16(s_col + c * 16, s + c * 16);
@@ -256,36 +279,40 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             tc::mbar_arrive(&p_full[g]);
         }
         // epilogue: O / l, (row_max, exp_sum) in natural units
-        const int64_t qrow = (int64_t)qp * 2 * TILE + g * TILE + row;
-        const bool store = qrow < p.q_rows;
-        const int64_t orow = (((int64_t)split * p.n_batch + b) * p.q_heads + h) * p.q_rows + qrow;
-        if (nkv > 0) {
-            tc::mbar_wait(&o_final[g], 0);
-            tc::tc_fence_after();
-        }
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            uint32_t o[16];
+        const int64_t r_in = (int64_t)g * TILE + row;          // row within this CTA's rows
+        const bool store = r_in < nrows;
+        // output rows mirror the Q rows ([split][request][q head][q row]); head_row already holds
+        // request, head and row-tile offsets
+        const int64_t orow = (int64_t)split * p.n_batch * p.q_heads * p.q_rows + head_row + r_in;
+        if (group_live && warp_live) {
             if (nkv > 0) {
-                tc::tmem_ld16(o_col + c * 16, o);
-                tc::tmem_ld_wait();
-            } else {
+                tc::mbar_wait(&o_final[g], 0);
+                tc::tc_fence_after();
+            }
+            const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll
-                for (int e = 0; e < 16; ++e) o[e] = 0u;
+            for (int c = 0; c < 8; ++c) {
+                uint32_t o[16];
+                if (nkv > 0) {
+                    tc::tmem_ld16(o_col + c * 16, o);
+                    tc::tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) o[e] = 0u;
+                }
+                if (store) {
+                    float4* dst = reinterpret_cast<float4*>(p.out_o + orow * D + c * 16);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                             __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+                }
             }
             if (store) {
-                float4* dst = reinterpret_cast<float4*>(p.out_o + orow * D + c * 16);
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
-                                         __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+                const bool any = l > 0.f;
+                p.out_stats[orow * 2 + 0] = any ? m_run / kLog2e : -INFINITY;
+                p.out_stats[orow * 2 + 1] = any ? l * ex2(m_use - m_run) : 0.f;
             }
-        }
-        if (store) {
-            const bool any = l > 0.f;
-            p.out_stats[orow * 2 + 0] = any ? m_run / kLog2e : -INFINITY;
-            p.out_stats[orow * 2 + 1] = any ? l * ex2(m_use - m_run) : 0.f;
         }
     }
     tc::tc_fence_before();
@@ -296,8 +323,15 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
 
 bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
 
+// Normal mode for prefill spans (>= 64 rows per head); grouped mode for GQA decode, where the
+// G q heads of a kv head (x a few rows) fill one 128-row tile and K/V are streamed once per group.
+static bool k2_grouped(const K2Params& p) {
+    const int64_t G = p.q_heads / p.kv_heads;
+    return G > 1 && G * p.q_rows <= 128 && p.q_rows < 64;
+}
+
 bool k2_prefill_tc_eligible(const K2Params& p, int d, int qdt, int kvdt) {
-    return d == 128 && qdt == SDA_BF16 && kvdt == SDA_BF16 && p.q_rows >= 64;
+    return d == 128 && qdt == SDA_BF16 && kvdt == SDA_BF16 && (p.q_rows >= 64 || k2_grouped(p));
 }
 
 cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
@@ -318,14 +352,16 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
     p.q_heads = q.q_heads;
     p.kv_heads = q.kv_heads;
     p.n_splits = q.n_splits;
-    p.n_qpairs = (int)((q.q_rows + 2 * TILE - 1) / (2 * TILE));
+    p.grouped = k2_grouped(q) ? 1 : 0;
+    p.n_qpairs = p.grouped ? 1 : (int)((q.q_rows + 2 * TILE - 1) / (2 * TILE));
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
     CUtensorMap qm, km, vm;
     if (!make_tmap_bf16_2d(&qm, q.q, q.n_batch * q.q_heads * q.q_rows, D, TILE) ||
         !make_tmap_bf16_2d(&km, q.k, q.n_batch * q.kv_heads * q.kv_cap, D, TILE) ||
         !make_tmap_bf16_2d(&vm, q.v, q.n_batch * q.kv_heads * q.kv_cap, D, TILE))
         return cudaErrorInvalidValue;
-    const dim3 grid((unsigned)p.n_qpairs, (unsigned)q.q_heads, (unsigned)(q.n_batch * q.n_splits));
+    const dim3 grid((unsigned)p.n_qpairs, (unsigned)(p.grouped ? q.kv_heads : q.q_heads),
+                    (unsigned)(q.n_batch * q.n_splits));
     k2_prefill_tc_kernel<<<grid, THREADS, SMEM, st>>>(p, qm, km, vm);
     return cudaGetLastError();
 }

@@ -91,7 +91,7 @@ def partial_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, kv_len:
     Hkv, cap = k.shape[1], k.shape[2]
     if k.dtype != v.dtype or k.shape != v.shape:
         raise ValueError("k and v must have the same shape and dtype")
-    S = n_splits or capi.default_splits(B, Hq, Lq, cap)
+    S = n_splits or capi.default_splits(B, Hq, Lq, cap, kv_heads=Hkv, head_dim=d)
     if out_o is None:
         out_o = torch.empty((S, B, Hq, Lq, d), dtype=torch.float32, device=q.device)
     if out_stats is None:

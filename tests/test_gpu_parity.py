@@ -90,7 +90,7 @@ def test_k2_partial_attention_splits_and_ragged(d, kv_dtype):
     st = st.double().cpu().numpy()
     for b in range(B):
         L = int(kv_len[b])
-        chunk = -(-L // n_splits)
+        chunk = -(-(-(-L // 128)) // n_splits) * 128   # whole 128-key tiles per split
         for h in range(Hq):
             kk, vv = k[b, h // 2, :L], v[b, h // 2, :L]
             for s in range(n_splits):
@@ -99,9 +99,12 @@ def test_k2_partial_attention_splits_and_ragged(d, kv_dtype):
                     assert np.all(st[s, b, h, :, 1] == 0) and np.all(np.isneginf(st[s, b, h, :, 0]))
                     continue
                 ro, rm, rs = C.shard_attention(q[b, h], kk[a:e], vv[a:e])
-                assert max_abs_rel(o[s, b, h], ro) < 1e-4
-                assert np.allclose(st[s, b, h, :, 0], rm, atol=1e-5, rtol=1e-5)
-                assert np.allclose(st[s, b, h, :, 1], rs, rtol=1e-4)
+                # bf16 KV at d=128 with GQA takes the tensor-core grouped kernel (P rounded to
+                # bf16 before P.V); everything else the f32 SIMT kernel
+                tc = kv_dtype == torch.bfloat16 and d == 128
+                assert max_abs_rel(o[s, b, h], ro) < (1e-2 if tc else 1e-4)
+                assert np.allclose(st[s, b, h, :, 0], rm, atol=1e-3 if tc else 1e-5, rtol=1e-5)
+                assert np.allclose(st[s, b, h, :, 1], rs, rtol=5e-3 if tc else 1e-4)
 
 
 def test_k3_merge_unscramble_vs_dec_output_and_merge_shards():

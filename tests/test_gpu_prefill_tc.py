@@ -83,3 +83,40 @@ def test_scrambled_prefill_end_to_end_tc():
     got = case.run_device(n_splits=2)
     ref = case.oracle()
     assert max_abs_rel(got, ref) < 2e-2 and rel_fro(got, ref) < 2e-2
+
+
+@pytest.mark.parametrize("hq,hkv,lq,cap,kv_len,n_splits", [
+    (16, 2, 1, 4096, [4096, 1000], 4),     # G=8 decode
+    (64, 8, 1, 2048, [2048], 2),           # BASELINE cfg5 head layout
+    (8, 1, 4, 1536, [1536], 3),            # G*Lq = 32 (multi-row decode)
+    (8, 2, 16, 1024, [700], 2),            # G*Lq = 64
+])
+def test_gqa_grouped_decode_tc(hq, hkv, lq, cap, kv_len, n_splits):
+    B, d = len(kv_len), 128
+    q = C.round_to_format(gauss(51, (B, hq, lq, d)), 2)
+    k = C.round_to_format(gauss(52, (B, hkv, cap, d)), 2)
+    v = C.round_to_format(gauss(53, (B, hkv, cap, d)), 2)
+    o, st = _k2(q, k, v, kv_len, n_splits)
+    simt_o, simt_st = _k2(q, k, v, kv_len, n_splits, simt=True)
+    G = hq // hkv
+    for b in range(B):
+        L = kv_len[b]
+        ntile = -(-L // 128)
+        tps = -(-ntile // n_splits)
+        for h in range(hq):
+            for s in range(n_splits):
+                a, e = s * tps * 128, min(L, (s + 1) * tps * 128)
+                if a >= e:
+                    assert np.all(st[s, b, h, :, 1] == 0)
+                    continue
+                ro, rm, rs = C.shard_attention(q[b, h], k[b, h // G, a:e], v[b, h // G, a:e])
+                assert max_abs_rel(o[s, b, h], ro) < 1e-2, (b, h, s)
+                assert np.allclose(st[s, b, h, :, 0], rm, atol=1e-3)
+                assert np.allclose(st[s, b, h, :, 1], rs, rtol=5e-3)
+    # merged over splits, the grouped tensor-core kernel and the SIMT kernel agree
+    def merged(o_, st_):
+        m = np.where(st_[..., 1] > 0, st_[..., 0], -np.inf)
+        w = st_[..., 1] * np.exp(m - m.max(0))
+        return (o_ * w[..., None]).sum(0) / w.sum(0)[..., None]
+    a, b_ = merged(o, st), merged(simt_o, simt_st)
+    assert max_abs_rel(a, b_) < 1e-2 and rel_fro(a, b_) < 5e-3
