@@ -14,7 +14,7 @@ std::atomic<uint64_t> g_launches{0};
 bool supported_dim(int d) { return d == 32 || d == 64 || d == 128 || d == 256; }
 bool pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
 // Debug knobs (tests compare kernel variants): SDA_K1_SIMT=1 / SDA_K2_SIMT=1 force the SIMT
-// K1 / K2 kernels.
+// K1 / K2 kernels; SDA_K2_GROUPED=1 routes small GQA groups to the grouped-row kernel.
 bool env_flag(const char* name) {
     const char* v = std::getenv(name);
     return v && v[0] && v[0] != '0';
@@ -146,6 +146,9 @@ sda_status sda_partial_attention(void* stream, const void* q, int32_t q_dtype, c
     sda::K2Params p{q, k, v, kv_len, out_o, out_stats, kv_cap, n_batch, q_rows, q_heads, kv_heads, n_splits,
                     (float)(1.0 / std::sqrt((double)head_dim))};
     ++g_launches;
+    if (sda::k2_gqa_tc_eligible(p, head_dim, q_dtype, kv_dtype) && !env_flag("SDA_K2_SIMT") &&
+        !env_flag("SDA_K2_GROUPED"))
+        return from_cuda(sda::launch_k2_gqa_tc(p, static_cast<cudaStream_t>(stream)));
     if (sda::k2_prefill_tc_eligible(p, head_dim, q_dtype, kv_dtype) && !env_flag("SDA_K2_SIMT"))
         return from_cuda(sda::launch_k2_prefill_tc(p, static_cast<cudaStream_t>(stream)));
     return from_cuda(sda::launch_k2_decode(p, head_dim, q_dtype, kv_dtype, static_cast<cudaStream_t>(stream)));

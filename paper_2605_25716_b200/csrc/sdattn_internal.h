@@ -83,6 +83,8 @@ cudaError_t launch_k1_tc(const K1Params& p, int d, int64_t n_batch, cudaStream_t
 cudaError_t launch_k2_decode(const K2Params& p, int d, int qdt, int kvdt, cudaStream_t st);
 bool k2_prefill_tc_eligible(const K2Params& p, int d, int qdt, int kvdt);
 cudaError_t launch_k2_prefill_tc(const K2Params& p, cudaStream_t st);
+bool k2_gqa_tc_eligible(const K2Params& p, int d, int qdt, int kvdt);
+cudaError_t launch_k2_gqa_tc(const K2Params& p, cudaStream_t st);
 cudaError_t launch_k3(const K3Params& p, int d, int odt, cudaStream_t st);
 
 }  // namespace sda

@@ -13,12 +13,16 @@ from tests.gpu_helpers import Case, dev, gauss, max_abs_rel, rel_fro
 pytestmark = pytest.mark.gpu
 
 
-def _k2(q, k, v, kv_len, n_splits, simt=False):
+def _k2(q, k, v, kv_len, n_splits, simt=False, grouped=False):
     old = os.environ.get("SDA_K2_SIMT")
     if simt:
         os.environ["SDA_K2_SIMT"] = "1"
     else:
         os.environ.pop("SDA_K2_SIMT", None)
+    if grouped:
+        os.environ["SDA_K2_GROUPED"] = "1"
+    else:
+        os.environ.pop("SDA_K2_GROUPED", None)
     try:
         o, st = ops.partial_attention(dev(q, torch.bfloat16), dev(k, torch.bfloat16), dev(v, torch.bfloat16),
                                       torch.from_numpy(np.asarray(kv_len, np.int32)).cuda(), n_splits=n_splits)
@@ -85,18 +89,21 @@ def test_scrambled_prefill_end_to_end_tc():
     assert max_abs_rel(got, ref) < 2e-2 and rel_fro(got, ref) < 2e-2
 
 
+@pytest.mark.parametrize("grouped", [False, True])
 @pytest.mark.parametrize("hq,hkv,lq,cap,kv_len,n_splits", [
     (16, 2, 1, 4096, [4096, 1000], 4),     # G=8 decode
     (64, 8, 1, 2048, [2048], 2),           # BASELINE cfg5 head layout
     (8, 1, 4, 1536, [1536], 3),            # G*Lq = 32 (multi-row decode)
     (8, 2, 16, 1024, [700], 2),            # G*Lq = 64
 ])
-def test_gqa_grouped_decode_tc(hq, hkv, lq, cap, kv_len, n_splits):
+def test_gqa_grouped_decode_tc(hq, hkv, lq, cap, kv_len, n_splits, grouped):
+    """GQA decode: the swapped kernel (keys on M, k2_gqa_tc.cu; G*Lq <= 32) and the grouped-row
+    mode of the prefill kernel (G*Lq <= 128) against the oracle and the SIMT kernel."""
     B, d = len(kv_len), 128
     q = C.round_to_format(gauss(51, (B, hq, lq, d)), 2)
     k = C.round_to_format(gauss(52, (B, hkv, cap, d)), 2)
     v = C.round_to_format(gauss(53, (B, hkv, cap, d)), 2)
-    o, st = _k2(q, k, v, kv_len, n_splits)
+    o, st = _k2(q, k, v, kv_len, n_splits, grouped=grouped)
     simt_o, simt_st = _k2(q, k, v, kv_len, n_splits, simt=True)
     G = hq // hkv
     for b in range(B):
