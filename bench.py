@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true", help="skip the cfg3 prefill sub-measurement")
+    ap.add_argument("--no-gqa", action="store_true", help="skip the cfg5 GQA mixed sub-measurement")
     ap.add_argument("--graph", dest="graph", action="store_true", default=None,
                     help="replay the step as a CUDA graph (default: on for N=1, off for N>1)")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
@@ -381,6 +382,11 @@ def run_ours(args, ws, rank, local):
                 line["prefill"] = run_prefill(devn, 10, 3, peaks)
             except Exception as e:  # noqa: BLE001
                 line["prefill"] = {"unavailable": str(e)}
+        if ws == 1 and not args.no_gqa:
+            try:
+                line["gqa"] = run_gqa_mixed(devn, 10, 3, peaks)
+            except Exception as e:  # noqa: BLE001
+                line["gqa"] = {"unavailable": str(e)}
         if ws == 1 and not args.no_cpu_baseline:
             try:
                 threads = os.cpu_count() or 1
@@ -472,6 +478,106 @@ def run_prefill(devn, steps: int, warmup: int, peaks: dict):
             "roofline": {"bound": "tensor", "kernel": "k2_prefill_tc_kernel", "achieved": tf_k2, "peak": peak,
                          "unit": "TFLOP/s", "frac": tf_k2 / peak, "k2_ms": k2_ms, "k2_share_of_step": k2_ms / ms,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"}}
+
+
+def run_gqa_mixed(devn, steps: int, warmup: int, peaks: dict):
+    """BASELINE config 5 per GPU: GQA 64 q heads / 8 kv heads x d128, 64K-token scrambled KV shard
+    per request. Mixed step = 32 decode requests (one token each) + one 2K-token prefill chunk of
+    another request (its K/V scrambled into its cache, its Q against its 64K shard). Reports
+    decode-only and mixed timings; roofline of the swapped GQA decode kernel vs HBM."""
+    import torch
+
+    from paper_2605_25716_b200 import capi, ops, protocol
+
+    HQ, HKV, L, BD, LP = 64, 8, 65536, 32, 2048
+    keys = protocol.DomainKeys(list(range(1, BD + 2)), 0, 1, HKV, D, devn)
+    k = torch.empty((BD + 1, HKV, L + LP, D), dtype=torch.bfloat16, device=devn)
+    v = torch.empty_like(k)
+    g = torch.Generator(device=devn).manual_seed(11)
+    for b0 in range(0, BD + 1, 4):   # resident shards, scrambled + permuted by K1 (setup, untimed)
+        b1 = min(BD + 1, b0 + 4)
+        x = torch.randn((b1 - b0, HKV, L, D), generator=g, device=devn).to(torch.bfloat16)
+        pkv, _ = keys.span_perms(1, 0, L)
+        ops.scramble(x, keys.dev[b0:b1], capi.PHI_INV_T, capi.KEYS_KQ, pkv[b0:b1].contiguous(), out=k[b0:b1], key_heads=HKV)
+        ops.scramble(x, keys.dev[b0:b1], capi.PHI_FORWARD, capi.KEYS_V, pkv[b0:b1].contiguous(), out=v[b0:b1], key_heads=HKV)
+        del x
+    kv_len = torch.full((BD + 1,), L, dtype=torch.int32, device=devn)
+    kd, vd, ld = k[:BD], v[:BD], kv_len[:BD]
+    kp, vp, lp = k[BD:], v[BD:], kv_len[BD:]
+    keys_d, keys_p = keys.dev[:BD], keys.dev[BD:]
+    qd = torch.randn((BD, HQ, 1, D), generator=g, device=devn).to(torch.bfloat16)
+    qp = torch.randn((1, HQ, LP, D), generator=g, device=devn).to(torch.bfloat16)
+    knew = torch.randn((1, HKV, LP, D), generator=g, device=devn).to(torch.bfloat16)
+    vnew = torch.randn((1, HKV, LP, D), generator=g, device=devn).to(torch.bfloat16)
+    pq, pq_inv = keys.span_perms(0, L, LP)
+    pkv_new, _ = keys.span_perms(1, L, LP)
+    Sd = capi.default_splits(BD, HQ, 1, L, kv_heads=HKV, head_dim=D)
+    Sp = capi.default_splits(1, HQ, LP, L, kv_heads=HKV, head_dim=D)
+    qd_s, qp_s = torch.empty_like(qd), torch.empty_like(qp)
+    od = torch.empty((Sd, BD, HQ, 1, D), dtype=torch.float32, device=devn)
+    sd = torch.empty((Sd, BD, HQ, 1, 2), dtype=torch.float32, device=devn)
+    op_ = torch.empty((Sp, 1, HQ, LP, D), dtype=torch.float32, device=devn)
+    sp_ = torch.empty((Sp, 1, HQ, LP, 2), dtype=torch.float32, device=devn)
+    outd = torch.empty((BD, HQ, 1, D), dtype=torch.float32, device=devn)
+    outp = torch.empty((1, HQ, LP, D), dtype=torch.float32, device=devn)
+    srcd = ops.sources_from_splits(od, sd, keys_d, None)
+    srcp = ops.sources_from_splits(op_, sp_, keys_p, pq_inv[BD:].contiguous())
+    pq_p = pq[BD:].contiguous()
+    stream = torch.cuda.current_stream()
+    ev = []
+
+    def decode(rec):
+        ops.scramble(qd, keys_d, capi.PHI_FORWARD, capi.KEYS_KQ, None, out=qd_s, key_heads=HKV)
+        if rec:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        ops.partial_attention(qd_s, kd, vd, ld, n_splits=Sd, out_o=od, out_stats=sd)
+        if rec:
+            e1.record(stream)
+            ev.append((e0, e1))
+        ops.unscramble_merge(srcd, out=outd, key_heads=HKV)
+
+    def prefill():
+        ops.scramble(knew, keys_p, capi.PHI_INV_T, capi.KEYS_KQ, pkv_new[BD:].contiguous(), out=kp,
+                     out_row_offset=L, key_heads=HKV)
+        ops.scramble(vnew, keys_p, capi.PHI_FORWARD, capi.KEYS_V, pkv_new[BD:].contiguous(), out=vp,
+                     out_row_offset=L, key_heads=HKV)
+        ops.scramble(qp, keys_p, capi.PHI_FORWARD, capi.KEYS_KQ, pq_p, out=qp_s, key_heads=HKV)
+        ops.partial_attention(qp_s, kp, vp, lp, n_splits=Sp, out_o=op_, out_stats=sp_)
+        ops.unscramble_merge(srcp, out=outp, key_heads=HKV)
+
+    def timed(fn, n):
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(n):
+            fn()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        return t0.elapsed_time(t1) / n
+
+    for _ in range(warmup):
+        decode(False)
+        prefill()
+    torch.cuda.synchronize()
+    ms_dec = timed(lambda: decode(True), steps)
+    k2_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    ms_mix = timed(lambda: (decode(False), prefill()), steps)
+    kv_bytes = BD * HKV * L * D * 2 * 2
+    k2_bytes = kv_bytes + BD * HQ * D * 2 + BD * HQ * (4 * D + 8)
+    achieved = k2_bytes / (k2_ms * 1e-3) / 1e9
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    pf_flops = 4.0 * LP * L * HQ * D
+    return {"metric": "scrambled-attn GQA decode tokens/s (mixed step also reported)",
+            "value": BD / (ms_dec * 1e-3), "unit": "tokens/s", "ms_per_step_decode": ms_dec,
+            "ms_per_step_mixed": ms_mix, "mixed_tokens_per_s": (BD + LP) / (ms_mix * 1e-3),
+            "mixed_prefill_tflops_incl_decode": pf_flops / ((ms_mix) * 1e-3) / 1e12, "steps": steps,
+            "config": {"workload": "BASELINE cfg5 per GPU: GQA 64 q / 8 kv heads x d128, 64K-token scrambled KV "
+                                   "shard per request; mixed step = 32 decode requests + one 2K-token prefill chunk",
+                       "decode_requests": BD, "prefill_chunk": LP, "kv_rows": L, "splits_decode": Sd,
+                       "splits_prefill": Sp},
+            "roofline": {"bound": "hbm", "kernel": "k2_gqa_tc_kernel<16>", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "k2_ms": k2_ms,
+                         "algorithmic_bytes_per_launch": k2_bytes}}
 
 
 def main():
