@@ -150,6 +150,14 @@ sda_status sda_partial_attention(void* stream, const void* q, int32_t q_dtype,
                                  const int32_t* kv_len, int64_t n_batch, int32_t q_heads,
                                  int32_t kv_heads, int64_t q_rows, int32_t head_dim, int32_t n_splits,
                                  float* out_o, float* out_stats);
+/* The inquirer's own span is attended in plaintext with a causal mask (protocol.cpp:944-947,
+ * AttentionMask::causal(offset), attention.hpp:25-27): key j is visible to query row i iff
+ * j <= i + causal_offset. Same layouts and outputs as sda_partial_attention (SIMT kernel). */
+sda_status sda_partial_attention_causal(void* stream, const void* q, int32_t q_dtype,
+                                        const void* k, const void* v, int32_t kv_dtype, int64_t kv_cap,
+                                        const int32_t* kv_len, int64_t n_batch, int32_t q_heads,
+                                        int32_t kv_heads, int64_t q_rows, int32_t head_dim, int32_t n_splits,
+                                        int64_t causal_offset, float* out_o, float* out_stats);
 /* Split count sized for a full-GPU launch of sda_partial_attention (MHA shapes). */
 int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int64_t kv_cap);
 /* Same, aware of GQA (q_heads > kv_heads) and of which kernel the shape dispatches to. */

@@ -27,7 +27,7 @@ STATUS_NAMES = {0: "SDA_OK", 1: "SDA_ERR_INVALID_ARGUMENT", 2: "SDA_ERR_NOT_POW2
 # Every symbol include/sdattn_b200.h declares (checked by tests/test_capi_load.py).
 EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_negotiate_keyset",
            "sda_span_perm", "sda_invert_permutation", "sda_keyset_bytes", "sda_pack_keyset", "sda_scramble",
-           "sda_partial_attention", "sda_default_splits", "sda_default_splits_gqa", "sda_unscramble_merge", "sda_abi_version",
+           "sda_partial_attention", "sda_partial_attention_causal", "sda_default_splits", "sda_default_splits_gqa", "sda_unscramble_merge", "sda_abi_version",
            "sda_status_string", "sda_launch_count")
 
 
@@ -80,6 +80,9 @@ def _load() -> ct.CDLL:
                                  ct.c_int64, ct.c_int64]
     lib.sda_partial_attention.argtypes = [_vp, _vp, ct.c_int32, _vp, _vp, ct.c_int32, ct.c_int64, _vp, ct.c_int64,
                                           ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int32, _vp, _vp]
+    lib.sda_partial_attention_causal.argtypes = [_vp, _vp, ct.c_int32, _vp, _vp, ct.c_int32, ct.c_int64, _vp,
+                                                 ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32,
+                                                 ct.c_int32, ct.c_int64, _vp, _vp]
     lib.sda_default_splits.restype = ct.c_int32
     lib.sda_default_splits.argtypes = [ct.c_int64, ct.c_int32, ct.c_int64, ct.c_int64]
     lib.sda_default_splits_gqa.restype = ct.c_int32

@@ -144,13 +144,32 @@ sda_status sda_partial_attention(void* stream, const void* q, int32_t q_dtype, c
     if (n_batch * q_rows > 65535 || q_heads > 65535 || n_splits > 65535) return SDA_ERR_UNSUPPORTED;
     if (n_batch == 0 || q_rows == 0) return SDA_OK;
     sda::K2Params p{q, k, v, kv_len, out_o, out_stats, kv_cap, n_batch, q_rows, q_heads, kv_heads, n_splits,
-                    (float)(1.0 / std::sqrt((double)head_dim))};
+                    (float)(1.0 / std::sqrt((double)head_dim)), 0, 0};
     ++g_launches;
     if (sda::k2_gqa_tc_eligible(p, head_dim, q_dtype, kv_dtype) && !env_flag("SDA_K2_SIMT") &&
         !env_flag("SDA_K2_GROUPED"))
         return from_cuda(sda::launch_k2_gqa_tc(p, static_cast<cudaStream_t>(stream)));
     if (sda::k2_prefill_tc_eligible(p, head_dim, q_dtype, kv_dtype) && !env_flag("SDA_K2_SIMT"))
         return from_cuda(sda::launch_k2_prefill_tc(p, static_cast<cudaStream_t>(stream)));
+    return from_cuda(sda::launch_k2_decode(p, head_dim, q_dtype, kv_dtype, static_cast<cudaStream_t>(stream)));
+}
+
+sda_status sda_partial_attention_causal(void* stream, const void* q, int32_t q_dtype, const void* k, const void* v,
+                                        int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int64_t n_batch,
+                                        int32_t q_heads, int32_t kv_heads, int64_t q_rows, int32_t head_dim,
+                                        int32_t n_splits, int64_t causal_offset, float* out_o, float* out_stats) {
+    if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
+    if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
+    if (!q || !k || !v || !out_o || !out_stats || !valid_dtype(q_dtype) || !valid_dtype(kv_dtype))
+        return SDA_ERR_INVALID_ARGUMENT;
+    if (n_batch < 0 || q_rows < 0 || kv_cap < 0 || q_heads <= 0 || kv_heads <= 0 || q_heads % kv_heads != 0 ||
+        n_splits <= 0)
+        return SDA_ERR_INVALID_ARGUMENT;
+    if (n_batch * q_rows > 65535 || q_heads > 65535 || n_splits > 65535) return SDA_ERR_UNSUPPORTED;
+    if (n_batch == 0 || q_rows == 0) return SDA_OK;
+    sda::K2Params p{q, k, v, kv_len, out_o, out_stats, kv_cap, n_batch, q_rows, q_heads, kv_heads, n_splits,
+                    (float)(1.0 / std::sqrt((double)head_dim)), 1, causal_offset};
+    ++g_launches;
     return from_cuda(sda::launch_k2_decode(p, head_dim, q_dtype, kv_dtype, static_cast<cudaStream_t>(stream)));
 }
 

@@ -41,7 +41,11 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
     const int64_t b = (int64_t)blockIdx.z / p.q_rows, qr = (int64_t)blockIdx.z % p.q_rows;
     const int kvh = h / (p.q_heads / p.kv_heads);
 
-    const int64_t len = p.kv_len ? (int64_t)p.kv_len[b] : p.kv_cap;
+    int64_t len = p.kv_len ? (int64_t)p.kv_len[b] : p.kv_cap;
+    if (p.causal) {   // keys j <= qr + offset only (AttentionMask::causal, attention.cpp:16-27)
+        const int64_t lim = qr + p.causal_offset + 1;
+        len = lim < 0 ? 0 : (lim < len ? lim : len);
+    }
     // splits are whole 128-key tiles (the same ranges as the tensor-core kernels)
     const int64_t tiles = (len + 127) / 128;
     const int64_t chunk = ((tiles + p.n_splits - 1) / p.n_splits) * 128;

@@ -50,6 +50,8 @@ struct K2Params {
     int kv_heads;
     int n_splits;
     float scale;   // 1/sqrt(d) (attention.cpp:45)
+    int causal;            // 1: key j visible to query row i iff j <= i + causal_offset (attention.hpp:25-27)
+    int64_t causal_offset;
 };
 
 struct K3Source {

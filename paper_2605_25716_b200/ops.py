@@ -106,6 +106,22 @@ def partial_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, kv_len:
     return out_o, out_stats
 
 
+def partial_attention_causal(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal_offset: int = 0,
+                             kv_len: Optional[torch.Tensor] = None, n_splits: int = 1, stream=None):
+    """Plaintext causal shard (the inquirer's own span, protocol.cpp:944-947): key j is visible to
+    query row i iff j <= i + causal_offset. Returns (o [S,B,Hq,Lq,d], stats [S,B,Hq,Lq,2])."""
+    _cuda(q, "q"), _cuda(k, "k"), _cuda(v, "v")
+    B, Hq, Lq, d = q.shape
+    Hkv, cap = k.shape[1], k.shape[2]
+    out_o = torch.empty((n_splits, B, Hq, Lq, d), dtype=torch.float32, device=q.device)
+    out_stats = torch.empty((n_splits, B, Hq, Lq, 2), dtype=torch.float32, device=q.device)
+    check(capi.LIB.sda_partial_attention_causal(_stream(stream), q.data_ptr(), _dtype_code(q), k.data_ptr(),
+                                                v.data_ptr(), _dtype_code(k), cap, _ptr(kv_len), B, Hq, Hkv, Lq, d,
+                                                n_splits, causal_offset, out_o.data_ptr(), out_stats.data_ptr()),
+          "sda_partial_attention_causal")
+    return out_o, out_stats
+
+
 @dataclass
 class MergeSource:
     """One shard for K3: o [B,Hq,Lq,d] f32, stats [B,Hq,Lq,2] f32, keys (phi_v of its domain,
