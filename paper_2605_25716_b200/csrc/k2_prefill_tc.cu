@@ -230,14 +230,19 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             for (int c = 0; c < 8; ++c) tc::tmem_ld16(s_col + c * 16, s + c * 16);
             tc::tmem_ld_wait();
             const int64_t valid = k_end - (t0 + j) * TILE;      // keys of this tile still in range
-            float mt = -INFINITY;
+            if (valid < TILE) {                                   // only the split's last tile
 #pragma unroll
-            for (int i = 0; i < 128; ++i) {
-                float x = __uint_as_float(s[i]) * p.scale_log2;
-                x = (i < valid) ? x : -INFINITY;
-                s[i] = __float_as_uint(x);
-                mt = fmaxf(mt, x);
+                for (int i = 0; i < 128; ++i)
+                    if (i >= valid) s[i] = 0xFF800000u;           // -inf
             }
+            // row max on the raw logits (scale > 0), two new values per 3-input max
+            float mr0 = -INFINITY, mr1 = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 64; i += 2) {
+                mr0 = tc::fmax3(mr0, __uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
+                mr1 = tc::fmax3(mr1, __uint_as_float(s[2 * i + 2]), __uint_as_float(s[2 * i + 3]));
+            }
+            const float mt = fmaxf(mr0, mr1) * p.scale_log2;
             const float m_new = fmaxf(m_run, mt);
             m_run = m_new;
             // lazy rescale: keep the exponent base unless the max grew by more than 8 (x256)
@@ -263,15 +268,24 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 m_use = m_new;
             }
             const float mu = (m_use == -INFINITY) ? 0.f : m_use;
-            float ls = 0.f;
+            // p = exp2(s * scale - mu): one packed FFMA2 per two logits, packed FADD2 row sums
+            const uint64_t sc2 = tc::f2(p.scale_log2, p.scale_log2), nmu2 = tc::f2(-mu, -mu);
+            uint64_t acc0 = tc::f2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
             for (int i = 0; i < 64; ++i) {   // P packed in place: s[i] <- bf16x2(p[2i], p[2i+1])
-                const float p0 = ex2(__uint_as_float(s[2 * i]) - mu);
-                const float p1 = ex2(__uint_as_float(s[2 * i + 1]) - mu);
-                ls += p0 + p1;
+                float x0, x1;
+                tc::f2_split(tc::ffma2(tc::f2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sc2, nmu2), x0, x1);
+                const float p0 = ex2(x0), p1 = ex2(x1);
+                if (i & 1)
+                    acc1 = tc::fadd2(acc1, tc::f2(p0, p1));
+                else
+                    acc0 = tc::fadd2(acc0, tc::f2(p0, p1));
                 s[i] = tc::pack_bf16(p0, p1);
             }
-            l += ls;
+            float a0, a1, b0, b1;
+            tc::f2_split(acc0, a0, a1);
+            tc::f2_split(acc1, b0, b1);
+            l += (a0 + a1) + (b0 + b1);
 #pragma unroll
             for (int c = 0; c < 8; ++c) tc::tmem_st8(s_col + c * 8, s + c * 8);
             tc::tmem_st_wait();
