@@ -179,18 +179,24 @@ int32_t sda_default_splits_gqa(int64_t n_batch, int32_t q_heads, int32_t kv_head
  *   out_stats : optional f32 [n_batch][q_heads][q_rows][2] merged (row_max, exp_sum), may be NULL
  *   err_flag  : optional device i32; set to SDA_ERR_MASKED_ROW when a row has exp_sum == 0 in
  *               every source (that row is written as NaN). May be NULL.
+ *   out_batch_stride : elements between requests in out and out_stats (0 = dense); a packed
+ *               per-request record [q_heads*q_rows*d | q_heads*q_rows*2] is what one NCCL
+ *               all-to-all carries back to the inquirer (O' and stats together).
  * ------------------------------------------------------------------------------------------ */
 typedef struct {
     const float* o;          /* [n_batch][q_heads][q_rows][d] */
     const float* stats;      /* [n_batch][q_heads][q_rows][2] */
     const void* keys;        /* device key set of the domain (phi_v used), NULL = plaintext */
     const uint32_t* pq_inv;  /* device u32 inverse span perm per request, NULL = identity */
+    int64_t batch_stride;    /* elements between requests in o and stats (0 = dense as above);
+                                lets O' and stats share one packed per-request record */
 } sda_merge_source;
 
 sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, int32_t n_sources,
                                 int64_t keys_batch_stride, int32_t key_heads, int64_t pq_batch_stride,
                                 int64_t n_batch, int32_t q_heads, int64_t q_rows, int32_t head_dim,
-                                void* out, int32_t out_dtype, float* out_stats, int32_t* err_flag);
+                                void* out, int32_t out_dtype, float* out_stats, int32_t* err_flag,
+                                int64_t out_batch_stride);
 
 /* ------------------------------------------------------------------------------------------
  * Misc

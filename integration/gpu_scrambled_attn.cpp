@@ -126,7 +126,7 @@ sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt) {
             ck(sda_partial_attention(st, q_s.p, dt, ks->p, vs->p, dt, (int64_t)L, nullptr, 1, 1, 1, (int64_t)lq, (int)d, 1,
                                      o->as<float>(), s->as<float>()),
                "partial attention");
-            src.push_back({o->as<float>(), s->as<float>(), hk.image->p, pq_inv_d->as<uint32_t>()});
+            src.push_back({o->as<float>(), s->as<float>(), hk.image->p, pq_inv_d->as<uint32_t>(), 0});
             keep.push_back(std::move(ks));
             keep.push_back(std::move(vs));
             keep.push_back(std::move(o));
@@ -146,12 +146,12 @@ sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt) {
             ck(sda_partial_attention(st, q32->p, SDA_F32, k32->p, v32->p, SDA_F32, (int64_t)lk, nullptr, 1, 1, 1,
                                      (int64_t)lq, (int)d, 1, lo.as<float>(), ls.as<float>()),
                "local shard");
-        src.push_back({lo.as<float>(), ls.as<float>(), nullptr, nullptr});
+        src.push_back({lo.as<float>(), ls.as<float>(), nullptr, nullptr, 0});
 
         DevBuf out(lq * d * 4), err(4);
         ckc(cudaMemset(err.p, 0, 4), "memset");
         ck(sda_unscramble_merge(st, src.data(), (int)src.size(), 0, 1, 0, 1, 1, (int64_t)lq, (int)d, out.p, SDA_F32,
-                                nullptr, err.as<int32_t>()),
+                                nullptr, err.as<int32_t>(), 0),
            "unscramble_merge");
         std::vector<float> h(lq * d);
         int32_t e = 0;

@@ -56,7 +56,7 @@ class HostKeysetC(ct.Structure):
 
 
 class MergeSource(ct.Structure):
-    _fields_ = [("o", _vp), ("stats", _vp), ("keys", _vp), ("pq_inv", _vp)]
+    _fields_ = [("o", _vp), ("stats", _vp), ("keys", _vp), ("pq_inv", _vp), ("batch_stride", ct.c_int64)]
 
 
 def _load() -> ct.CDLL:
@@ -89,7 +89,7 @@ def _load() -> ct.CDLL:
     lib.sda_default_splits_gqa.argtypes = [ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32]
     lib.sda_unscramble_merge.argtypes = [_vp, ct.POINTER(MergeSource), ct.c_int32, ct.c_int64, ct.c_int32,
                                          ct.c_int64, ct.c_int64, ct.c_int32, ct.c_int64, ct.c_int32, _vp, ct.c_int32,
-                                         _vp, _vp]
+                                         _vp, _vp, ct.c_int64]
     lib.sda_abi_version.restype = ct.c_int32
     lib.sda_status_string.restype = ct.c_char_p
     lib.sda_status_string.argtypes = [ct.c_int32]

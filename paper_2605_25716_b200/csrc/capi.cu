@@ -176,7 +176,7 @@ sda_status sda_partial_attention_causal(void* stream, const void* q, int32_t q_d
 sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, int32_t n_sources,
                                 int64_t keys_batch_stride, int32_t key_heads, int64_t pq_batch_stride,
                                 int64_t n_batch, int32_t q_heads, int64_t q_rows, int32_t head_dim, void* out,
-                                int32_t out_dtype, float* out_stats, int32_t* err_flag) {
+                                int32_t out_dtype, float* out_stats, int32_t* err_flag, int64_t out_batch_stride) {
     if (n_sources <= 0) return SDA_ERR_EMPTY_SHARDS;  // attention.cpp:90
     if (n_sources > SDA_MAX_SOURCES || !sources) return SDA_ERR_INVALID_ARGUMENT;
     if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
@@ -191,7 +191,8 @@ sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, i
     if (n_batch == 0 || q_rows == 0) return SDA_OK;
     sda::K3Params p{};
     for (int i = 0; i < n_sources; ++i)
-        p.src[i] = {sources[i].o, sources[i].stats, static_cast<const uint8_t*>(sources[i].keys), sources[i].pq_inv};
+        p.src[i] = {sources[i].o, sources[i].stats, static_cast<const uint8_t*>(sources[i].keys), sources[i].pq_inv,
+                    sources[i].batch_stride};
     p.n_src = n_sources;
     p.keys_bstride = keys_batch_stride;
     p.key_heads = key_heads > 0 ? key_heads : q_heads;
@@ -202,6 +203,7 @@ sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, i
     p.out = out;
     p.out_stats = out_stats;
     p.err = err_flag;
+    p.out_bstride = out_batch_stride;
     ++g_launches;
     return from_cuda(sda::launch_k3(p, head_dim, out_dtype, static_cast<cudaStream_t>(stream)));
 }

@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
     for (int s = lane; s < p.n_src; s += 32) {
         const K3Source& src = p.src[s];
         const int64_t ri = src.pq_inv ? (int64_t)src.pq_inv[b * p.pq_bstride + r] : r;
-        const float2 st = *reinterpret_cast<const float2*>(src.stats + (bh * p.q_rows + ri) * 2);
+        const int64_t st_off = src.bstride ? b * src.bstride + ((int64_t)h * p.q_rows + ri) * 2 : (bh * p.q_rows + ri) * 2;
+        const float2 st = *reinterpret_cast<const float2*>(src.stats + st_off);
         if (st.y > 0.f) mstar = fmaxf(mstar, st.x);
     }
 #pragma unroll
@@ -74,12 +75,14 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
     for (int s = 0; s < p.n_src; ++s) {
         const K3Source& src = p.src[s];
         const int64_t ri = src.pq_inv ? (int64_t)src.pq_inv[b * p.pq_bstride + r] : r;
-        const float2 st = *reinterpret_cast<const float2*>(src.stats + (bh * p.q_rows + ri) * 2);
+        const int64_t st_off = src.bstride ? b * src.bstride + ((int64_t)h * p.q_rows + ri) * 2 : (bh * p.q_rows + ri) * 2;
+        const int64_t o_off = src.bstride ? b * src.bstride + ((int64_t)h * p.q_rows + ri) * D : (bh * p.q_rows + ri) * D;
+        const float2 st = *reinterpret_cast<const float2*>(src.stats + st_off);
         if (st.y > 0.f) {
             const float w = single ? 1.f : st.y * expf(st.x - mstar);
             denom += single ? st.y : w;
             float ov[E];
-            load_vec_any<E>(src.o + (bh * p.q_rows + ri) * D + lane * E, ov);
+            load_vec_any<E>(src.o + o_off + lane * E, ov);
 #pragma unroll
             for (int e = 0; e < E; ++e) acc[e] = fmaf(w, ov[e], acc[e]);
             pending = true;
@@ -102,10 +105,12 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
     const float inv = masked ? __int_as_float(0x7fc00000) : (single ? 1.f : 1.f / denom);
 #pragma unroll
     for (int e = 0; e < E; ++e) out[e] *= inv;
-    store_vec_any<E>(static_cast<TOut*>(p.out) + row * D + lane * E, out);
+    const int64_t hr = (int64_t)h * p.q_rows + r;
+    store_vec_any<E>(static_cast<TOut*>(p.out) + (p.out_bstride ? b * p.out_bstride + hr * D : row * D) + lane * E, out);
     if (p.out_stats && lane == 0) {
-        p.out_stats[row * 2 + 0] = single ? (masked ? -INFINITY : mstar) : mstar;
-        p.out_stats[row * 2 + 1] = masked ? 0.f : denom;
+        const int64_t so = p.out_bstride ? b * p.out_bstride + hr * 2 : row * 2;
+        p.out_stats[so + 0] = single ? (masked ? -INFINITY : mstar) : mstar;
+        p.out_stats[so + 1] = masked ? 0.f : denom;
     }
 }
 

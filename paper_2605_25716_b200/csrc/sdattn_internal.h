@@ -59,6 +59,7 @@ struct K3Source {
     const float* stats;
     const uint8_t* keys;
     const uint32_t* pq_inv;
+    int64_t bstride;       // elements between requests (o and stats); 0 = dense
 };
 
 struct K3Params {
@@ -73,6 +74,7 @@ struct K3Params {
     void* out;
     float* out_stats;
     int32_t* err;
+    int64_t out_bstride;   // elements between requests (out and out_stats); 0 = dense
 };
 
 }  // namespace sda

@@ -25,30 +25,41 @@ import torch.distributed as dist
 
 @dataclass
 class StepBuffers:
-    """Preallocated exchange buffers for one rank (world W, B_p requests per inquirer)."""
+    """Preallocated exchange buffers for one rank (world W, B_p requests per inquirer).
+
+    The partials travel back as ONE packed f32 record per request, [Hq*Lq*d O' | Hq*Lq*2 stats]
+    (K3 writes and reads it with a batch stride), so one all-to-all carries both SCR_SHARD
+    frames (protocol.cpp:1097-1102)."""
     q_send: torch.Tensor    # [W, B_p, Hq, Lq, d]   Q' for each destination domain
     q_recv: torch.Tensor    # [W, B_p, Hq, Lq, d]   Q' from each inquirer = [W*B_p, ...] for K2
-    o_fold: torch.Tensor    # [W, B_p, Hq, Lq, d]   this domain's partial per inquirer (f32)
-    st_fold: torch.Tensor   # [W, B_p, Hq, Lq, 2]
-    o_back: torch.Tensor    # [W, B_p, Hq, Lq, d]   partial of every domain for my requests
-    st_back: torch.Tensor   # [W, B_p, Hq, Lq, 2]
+    ret_send: torch.Tensor  # [W, B_p, rec] f32     this domain's partial for each inquirer's requests
+    ret_recv: torch.Tensor  # [W, B_p, rec] f32     every domain's partial for my requests
+    dims: tuple             # (Hq, Lq, d)
 
     @staticmethod
     def allocate(world: int, b_per: int, q_heads: int, q_rows: int, d: int, q_dtype, device) -> "StepBuffers":
         shp = (world, b_per, q_heads, q_rows, d)
+        rec = q_heads * q_rows * (d + 2)
         f32 = dict(dtype=torch.float32, device=device)
-        return StepBuffers(torch.empty(shp, dtype=q_dtype, device=device),
-                           torch.empty(shp, dtype=q_dtype, device=device),
-                           torch.empty(shp, **f32), torch.empty(shp[:-1] + (2,), **f32),
-                           torch.empty(shp, **f32), torch.empty(shp[:-1] + (2,), **f32))
+        return StepBuffers(torch.empty(shp, dtype=q_dtype, device=device), torch.empty(shp, dtype=q_dtype, device=device),
+                           torch.empty((world, b_per, rec), **f32), torch.empty((world, b_per, rec), **f32),
+                           (q_heads, q_rows, d))
+
+
+def record_views(ret: torch.Tensor, dims):
+    """(o, stats) views [.., B, Hq, Lq, d] / [.., B, Hq, Lq, 2] of packed per-request records."""
+    Hq, Lq, d = dims
+    n = Hq * Lq * d
+    lead = ret.shape[:-1]
+    return ret[..., :n].unflatten(-1, (Hq, Lq, d)), ret[..., n:].unflatten(-1, (Hq, Lq, 2))
 
 
 @dataclass
 class RankCompute:
     """The per-rank compute of one step (GPU: the K1/K2/K3 calls of ops.py)."""
-    scramble_q: Callable[[torch.Tensor, int, torch.Tensor], None]          # (q, dst_domain, out)
-    serve: Callable[[torch.Tensor, torch.Tensor, torch.Tensor], None]       # (q_all, o_out, st_out) K2 + fold
-    finish: Callable[[torch.Tensor, torch.Tensor, torch.Tensor], None]      # (o_back, st_back, out) K3
+    scramble_q: Callable[[torch.Tensor, int, torch.Tensor], None]   # (q, dst_domain, out)
+    serve: Callable[[torch.Tensor, torch.Tensor, tuple], None]       # (q_all, ret [B_tot, rec], dims): K2 + fold
+    finish: Callable[[torch.Tensor, torch.Tensor, tuple], None]      # (ret_back [W, B_p, rec], out, dims): K3
 
 
 def scrambled_decode_step(q: torch.Tensor, compute: RankCompute, bufs: StepBuffers, out: torch.Tensor,
@@ -64,15 +75,13 @@ def scrambled_decode_step(q: torch.Tensor, compute: RankCompute, bufs: StepBuffe
         q_all = bufs.q_send
     b_tot = q_all.shape[0] * q_all.shape[1]
     compute.serve(q_all.view((b_tot,) + tuple(q_all.shape[2:])),     # try_serve_q on my shard
-                  bufs.o_fold.view((b_tot,) + tuple(bufs.o_fold.shape[2:])),
-                  bufs.st_fold.view((b_tot,) + tuple(bufs.st_fold.shape[2:])))
+                  bufs.ret_send.view(b_tot, -1), bufs.dims)
     if world > 1:
-        dist.all_to_all_single(bufs.o_back, bufs.o_fold, group=group)    # SCR_SHARD (O')
-        dist.all_to_all_single(bufs.st_back, bufs.st_fold, group=group)  # SCR_SHARD (stats)
-        o_back, st_back = bufs.o_back, bufs.st_back
+        dist.all_to_all_single(bufs.ret_recv, bufs.ret_send, group=group)   # SCR_SHARD (O' + stats)
+        back = bufs.ret_recv
     else:
-        o_back, st_back = bufs.o_fold, bufs.st_fold
-    compute.finish(o_back, st_back, out)                          # span_finish_layer
+        back = bufs.ret_send
+    compute.finish(back, out, bufs.dims)                          # span_finish_layer
     return out
 
 
@@ -88,9 +97,9 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
         ops.scramble(q, inquirer_keys[dom].dev, capi.PHI_FORWARD, capi.KEYS_KQ, None, out=out,
                      key_heads=kv_heads or inquirer_keys[dom].kv_heads)
 
-    def serve(q_all, o_out, st_out):
+    def serve(q_all, ret, dims):
         B, Hq, Lq, d = q_all.shape
-        S = n_splits or capi.default_splits(B, Hq, Lq, shard.capacity)
+        S = n_splits or capi.default_splits(B, Hq, Lq, shard.capacity, kv_heads=shard.k.shape[1], head_dim=d)
         key = (S, B, Hq, Lq, d)
         if state.get("key") != key:
             state["key"] = key
@@ -98,13 +107,17 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
             state["st"] = torch.empty((S, B, Hq, Lq, 2), dtype=torch.float32, device=q_all.device)
         ops.partial_attention(q_all, shard.k, shard.v, shard.kv_len, n_splits=S, out_o=state["o"],
                               out_stats=state["st"])
-        # fold the splits of this domain in scrambled space (plain merge, no keys): one O' and one
-        # (row_max, exp_sum) per request row, exactly what SCR_SHARD carries
-        ops.unscramble_merge(ops.sources_from_splits(state["o"], state["st"]), out=o_out, out_stats=st_out)
+        # fold this domain's splits in scrambled space (plain merge, no keys) straight into the packed
+        # per-request records: one O' and one (row_max, exp_sum) per row, what SCR_SHARD carries
+        rec = ret.shape[-1]
+        ops.unscramble_merge(ops.sources_from_splits(state["o"], state["st"]), out=ret,
+                             out_stats=ret[:, Hq * Lq * d:], out_batch_stride=rec)
 
-    def finish(o_back, st_back, out):
-        srcs = [ops.MergeSource(o_back[dom], st_back[dom], inquirer_keys[dom].dev, None)
-                for dom in range(o_back.shape[0])]
+    def finish(back, out, dims):
+        Hq, Lq, d = dims
+        W, Bp, rec = back.shape
+        srcs = [ops.MergeSource(back[dom], back[dom, :, Hq * Lq * d:], inquirer_keys[dom].dev, None,
+                                batch_stride=rec, shape=(Bp, Hq, Lq, d)) for dom in range(W)]
         ops.unscramble_merge(srcs, out=out, key_heads=kv_heads or inquirer_keys[0].kv_heads)
 
     return RankCompute(scramble_q, serve, finish)

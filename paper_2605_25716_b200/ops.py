@@ -130,6 +130,8 @@ class MergeSource:
     stats: torch.Tensor
     keys: Optional[torch.Tensor] = None
     pq_inv: Optional[torch.Tensor] = None
+    batch_stride: int = 0     # elements between requests in o and stats (0 = dense)
+    shape: Optional[tuple] = None  # (B, Hq, Lq, d) when o is a flat packed record view
 
 
 def sources_from_splits(o: torch.Tensor, stats: torch.Tensor, keys: Optional[torch.Tensor] = None,
@@ -140,21 +142,24 @@ def sources_from_splits(o: torch.Tensor, stats: torch.Tensor, keys: Optional[tor
 def unscramble_merge(sources: Sequence[MergeSource], out: Optional[torch.Tensor] = None,
                      out_dtype: torch.dtype = torch.float32, key_heads: Optional[int] = None,
                      out_stats: Optional[torch.Tensor] = None, err_flag: Optional[torch.Tensor] = None,
-                     stream=None) -> torch.Tensor:
-    """K3. Merged, unscrambled, inverse-permuted output [B, Hq, Lq, d]."""
+                     out_batch_stride: int = 0, stream=None) -> torch.Tensor:
+    """K3. Merged, unscrambled, inverse-permuted output [B, Hq, Lq, d] (or a packed per-request
+    record when out_batch_stride is given: out and out_stats then point into the same buffer)."""
     n = len(sources)
     if n > capi.MAX_SOURCES:
         raise ValueError(f"at most {capi.MAX_SOURCES} sources")
     if n == 0:
-        check(capi.LIB.sda_unscramble_merge(_stream(stream), None, 0, 0, 0, 0, 0, 1, 0, 32, None, 0, None, None),
+        check(capi.LIB.sda_unscramble_merge(_stream(stream), None, 0, 0, 0, 0, 0, 1, 0, 32, None, 0, None, None, 0),
               "sda_unscramble_merge")
-    B, Hq, Lq, d = sources[0].o.shape
+    B, Hq, Lq, d = sources[0].shape or sources[0].o.shape
     arr = (capi.MergeSource * n)()
     kstride = 0
     pstride = 0
     for i, s in enumerate(sources):
-        _cuda(s.o, "o"), _cuda(s.stats, "stats")
+        if not s.o.is_cuda or not s.stats.is_cuda:
+            raise ValueError("o and stats must be CUDA tensors")
         arr[i].o, arr[i].stats = s.o.data_ptr(), s.stats.data_ptr()
+        arr[i].batch_stride = s.batch_stride
         arr[i].keys = _ptr(s.keys)
         arr[i].pq_inv = _ptr(s.pq_inv)
         if s.keys is not None:
@@ -164,6 +169,7 @@ def unscramble_merge(sources: Sequence[MergeSource], out: Optional[torch.Tensor]
     if out is None:
         out = torch.empty((B, Hq, Lq, d), dtype=out_dtype, device=sources[0].o.device)
     check(capi.LIB.sda_unscramble_merge(_stream(stream), arr, n, kstride, key_heads or Hq, pstride, B, Hq, Lq, d,
-                                        out.data_ptr(), _dtype_code(out), _ptr(out_stats), _ptr(err_flag)),
+                                        out.data_ptr(), _dtype_code(out), _ptr(out_stats), _ptr(err_flag),
+                                        out_batch_stride),
           "sda_unscramble_merge")
     return out

@@ -36,7 +36,7 @@ def test_status_mapping_without_device():
     # q heads not a multiple of kv heads
     assert L.sda_partial_attention(None, 1, 0, 1, 1, 0, 8, None, 1, 3, 2, 1, 64, 1, 1, 1) == 1
     # merge_shards: empty shard list (attention.cpp:90)
-    assert L.sda_unscramble_merge(None, None, 0, 0, 1, 0, 1, 1, 1, 64, 1, 0, None, None) == 3
+    assert L.sda_unscramble_merge(None, None, 0, 0, 1, 0, 1, 1, 1, 64, 1, 0, None, None, 0) == 3
     with pytest.raises(capi.SdaError):
         capi.span_perm(1, 1, 0, 0)  # negotiate_keyset: lengths must be >= 1
     with pytest.raises(capi.SdaError):

@@ -12,7 +12,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2605_25716_b200.distributed import RankCompute, StepBuffers, scrambled_decode_step
+from paper_2605_25716_b200.distributed import RankCompute, StepBuffers, record_views, scrambled_decode_step
 
 H, D, LK, BP = 2, 16, 24, 2   # heads, head dim, rows per domain per request, requests per inquirer
 
@@ -63,7 +63,8 @@ def _oracle_compute(rank, world, k, v):
             for h in range(H):
                 out[i, h] = torch.from_numpy(C.apply_phi(q[i, h].numpy(), *_sc(ks, h, 0), 0))
 
-    def serve(q_all, o_out, st_out):
+    def serve(q_all, ret, dims):
+        o_out, st_out = record_views(ret, dims)
         for b in range(B):
             for h in range(H):
                 o, m, s = C.shard_attention(q_all[b, h].numpy(), kp[b, h], vp[b, h])
@@ -71,7 +72,8 @@ def _oracle_compute(rank, world, k, v):
                 st_out[b, h, :, 0] = torch.from_numpy(m)
                 st_out[b, h, :, 1] = torch.from_numpy(s)
 
-    def finish(o_back, st_back, out):
+    def finish(back, out, dims):
+        o_back, st_back = record_views(back, dims)
         for i in range(BP):
             for h in range(H):
                 outs, ms, ss = [], [], []
@@ -95,9 +97,9 @@ def _worker(rank, world, port, ret):
         comp = _oracle_compute(rank, world, k, v)
         f64 = dict(dtype=torch.float64)
         shp = (world, BP, H, 1, D)
-        bufs = StepBuffers(torch.empty(shp, **f64), torch.empty(shp, **f64), torch.empty(shp, **f64),
-                           torch.empty(shp[:-1] + (2,), **f64), torch.empty(shp, **f64),
-                           torch.empty(shp[:-1] + (2,), **f64))
+        rec = H * 1 * (D + 2)
+        bufs = StepBuffers(torch.empty(shp, **f64), torch.empty(shp, **f64), torch.empty((world, BP, rec), **f64),
+                           torch.empty((world, BP, rec), **f64), (H, 1, D))
         out = torch.empty((BP, H, 1, D), **f64)
         mine = torch.from_numpy(q[rank * BP:(rank + 1) * BP].copy())
         scrambled_decode_step(mine, comp, bufs, out)

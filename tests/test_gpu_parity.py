@@ -226,3 +226,20 @@ def test_full_size_c2_sampled_parity():
                                [kf[b, h].double().cpu().numpy()], [vf[b, h].double().cpu().numpy()], wire_fmt=2,
                                shard_first_pos=[0])
         assert max_abs_rel(got[b, h], ref) < TOL_BF16 and rel_fro(got[b, h], ref) < TOL_BF16
+
+
+def test_distributed_step_packed_records_world1():
+    """distributed.scrambled_decode_step with the GPU rank compute at world 1: K1 -> K2 -> split fold
+    into packed (O', stats) records -> K3 from the packed records, against the oracle."""
+    from paper_2605_25716_b200 import distributed as sdist
+    case = Case(B=3, Hq=4, Hkv=4, d=128, lk=2048, n_nodes=1, lq=1, dtype=torch.bfloat16, seed=17)
+    keys = protocol.DomainKeys(case.request_ids(), 0, 1, 4, 128, "cuda")
+    shard = protocol.KVShard(3, 4, 2048, 128, "cuda")
+    shard.ship_segment(dev(case.k[0], torch.bfloat16), dev(case.v[0], torch.bfloat16), keys, first_pos=0)
+    bufs = sdist.StepBuffers.allocate(1, 3, 4, 1, 128, torch.bfloat16, "cuda")
+    comp = sdist.gpu_rank_compute([keys], shard, n_splits=5)
+    out = torch.empty((3, 4, 1, 128), dtype=torch.float32, device="cuda")
+    sdist.scrambled_decode_step(dev(case.q, torch.bfloat16), comp, bufs, out)
+    got = out.double().cpu().numpy()
+    ref = case.oracle()
+    assert max_abs_rel(got, ref) < TOL_BF16 and rel_fro(got, ref) < TOL_BF16
