@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--no-prefill", action="store_true", help="skip the cfg3 prefill sub-measurement")
     ap.add_argument("--no-gqa", action="store_true", help="skip the cfg5 GQA mixed sub-measurement")
     ap.add_argument("--graph", dest="graph", action="store_true", default=None,
-                    help="replay the step as a CUDA graph (default: on for N=1, off for N>1)")
+                    help="replay the step (kernels + NCCL all-to-alls) as a CUDA graph (default on)")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
     ap.add_argument("--cpu-pairs", type=int, default=128, help="(request, head) pairs in the CPU sample")
     return ap.parse_args()
@@ -182,7 +182,7 @@ def run_ours(args, ws, rank, local):
     torch.cuda.set_device(local)
     devn = torch.device("cuda", local)
     if args.graph is None:
-        args.graph = ws == 1
+        args.graph = True
     if ws > 1:
         dist.init_process_group("nccl", device_id=devn)
     B_tot = B_PER * ws

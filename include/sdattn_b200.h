@@ -120,13 +120,16 @@ sda_status sda_pack_keyset(const sda_host_keyset* ks, uint32_t n_heads, uint32_t
  *   keys : device; request b's key set at keys + b * keys_batch_stride (bytes)
  *   perm : device u32; request b's span permutation at perm + b * perm_batch_stride,
  *          NULL = identity (e.g. L_q = 1)
+ *   x_batch_mod : 0, or > 0 to read x[b % x_batch_mod] -- one query batch scrambled for several
+ *          destination domains (key sets stacked per domain) in a single launch
  * ------------------------------------------------------------------------------------------ */
 sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys,
                         const void* x, int32_t x_dtype, int64_t n_batch, int32_t n_heads,
                         int64_t rows, int32_t head_dim,
                         const void* keys, int64_t keys_batch_stride, int32_t key_heads,
                         const uint32_t* perm, int64_t perm_batch_stride,
-                        void* out, int32_t out_dtype, int64_t out_rows_cap, int64_t out_row_offset);
+                        void* out, int32_t out_dtype, int64_t out_rows_cap, int64_t out_row_offset,
+                        int64_t x_batch_mod);
 
 /* ------------------------------------------------------------------------------------------
  * K2  keyless delegated partial attention over the scrambled KV shard.

@@ -104,7 +104,7 @@ sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt) {
         auto pq_d = upload_u32(pq), pq_inv_d = upload_u32(pq_inv);
         DevBuf q_s(lq * d * esz);
         ck(sda_scramble(st, SDA_PHI_FORWARD, SDA_KEYS_KQ, q32->p, SDA_F32, 1, 1, (int64_t)lq, (int)d, hk.image->p, 0, 1,
-                        pq_d->as<uint32_t>(), 0, q_s.p, dt, (int64_t)lq, 0),
+                        pq_d->as<uint32_t>(), 0, q_s.p, dt, (int64_t)lq, 0, 0),
            "scramble Q");
 
         std::vector<std::unique_ptr<DevBuf>> keep;
@@ -117,10 +117,10 @@ sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt) {
             auto pkv = upload_u32(span_perm(hk.token_perm_seed, 1, seg->first_pos, L));
             auto ks = std::make_unique<DevBuf>(L * d * esz), vs = std::make_unique<DevBuf>(L * d * esz);
             ck(sda_scramble(st, SDA_PHI_INV_T, SDA_KEYS_KQ, k32->p, SDA_F32, 1, 1, (int64_t)L, (int)d, hk.image->p, 0, 1,
-                            pkv->as<uint32_t>(), 0, ks->p, dt, (int64_t)L, 0),
+                            pkv->as<uint32_t>(), 0, ks->p, dt, (int64_t)L, 0, 0),
                "scramble K");
             ck(sda_scramble(st, SDA_PHI_FORWARD, SDA_KEYS_V, v32->p, SDA_F32, 1, 1, (int64_t)L, (int)d, hk.image->p, 0, 1,
-                            pkv->as<uint32_t>(), 0, vs->p, dt, (int64_t)L, 0),
+                            pkv->as<uint32_t>(), 0, vs->p, dt, (int64_t)L, 0, 0),
                "scramble V");
             auto o = std::make_unique<DevBuf>(lq * d * 4), s = std::make_unique<DevBuf>(lq * 2 * 4);
             ck(sda_partial_attention(st, q_s.p, dt, ks->p, vs->p, dt, (int64_t)L, nullptr, 1, 1, 1, (int64_t)lq, (int)d, 1,

@@ -77,7 +77,7 @@ def _load() -> ct.CDLL:
     lib.sda_pack_keyset.argtypes = [ct.POINTER(HostKeysetC), ct.c_uint32, ct.c_uint32, _vp]
     lib.sda_scramble.argtypes = [_vp, ct.c_int32, ct.c_int32, _vp, ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int64,
                                  ct.c_int32, _vp, ct.c_int64, ct.c_int32, _vp, ct.c_int64, _vp, ct.c_int32,
-                                 ct.c_int64, ct.c_int64]
+                                 ct.c_int64, ct.c_int64, ct.c_int64]
     lib.sda_partial_attention.argtypes = [_vp, _vp, ct.c_int32, _vp, _vp, ct.c_int32, ct.c_int64, _vp, ct.c_int64,
                                           ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int32, _vp, _vp]
     lib.sda_partial_attention_causal.argtypes = [_vp, _vp, ct.c_int32, _vp, _vp, ct.c_int32, ct.c_int64, _vp,

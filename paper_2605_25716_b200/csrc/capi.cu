@@ -55,7 +55,7 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys, const
                         int64_t n_batch, int32_t n_heads, int64_t rows, int32_t head_dim, const void* keys,
                         int64_t keys_batch_stride, int32_t key_heads, const uint32_t* perm,
                         int64_t perm_batch_stride, void* out, int32_t out_dtype, int64_t out_rows_cap,
-                        int64_t out_row_offset) {
+                        int64_t out_row_offset, int64_t x_batch_mod) {
     if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
     if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
     if (variant != SDA_PHI_FORWARD && variant != SDA_PHI_INV_T) return SDA_ERR_INVALID_ARGUMENT;
@@ -63,11 +63,11 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys, const
     if (!x || !out || !keys || !valid_dtype(x_dtype) || !valid_dtype(out_dtype)) return SDA_ERR_INVALID_ARGUMENT;
     if (n_batch < 0 || n_heads <= 0 || key_heads <= 0 || n_heads % key_heads != 0 || rows < 0)
         return SDA_ERR_INVALID_ARGUMENT;
-    if (out_row_offset < 0 || out_row_offset + rows > out_rows_cap) return SDA_ERR_INVALID_ARGUMENT;
+    if (out_row_offset < 0 || out_row_offset + rows > out_rows_cap || x_batch_mod < 0) return SDA_ERR_INVALID_ARGUMENT;
     if (n_batch > 65535 || n_heads > 65535) return SDA_ERR_UNSUPPORTED;
     if (rows == 0 || n_batch == 0) return SDA_OK;
     sda::K1Params p{x, out, keys, perm, keys_batch_stride, perm_batch_stride, rows, out_rows_cap, out_row_offset,
-                    n_heads, key_heads, which_keys, variant == SDA_PHI_INV_T ? 1 : 0};
+                    n_heads, key_heads, which_keys, variant == SDA_PHI_INV_T ? 1 : 0, x_batch_mod};
     ++g_launches;
     if (sda::k1_tc_eligible(p, head_dim, x_dtype, out_dtype) && !env_flag("SDA_K1_SIMT"))
         return from_cuda(sda::launch_k1_tc(p, head_dim, n_batch, static_cast<cudaStream_t>(stream)));

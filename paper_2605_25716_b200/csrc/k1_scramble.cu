@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p) {
         }
     }
 
-    const Tin* x = static_cast<const Tin*>(p.x) + (b * p.n_heads + h) * p.rows * D;
+    const int64_t xb = p.x_batch_mod > 0 ? b % p.x_batch_mod : b;
+    const Tin* x = static_cast<const Tin*>(p.x) + (xb * p.n_heads + h) * p.rows * D;
     Tout* out = static_cast<Tout*>(p.out) + ((b * p.n_heads + h) * p.out_rows_cap + p.out_row_offset) * D;
     const uint32_t* perm = p.perm ? p.perm + b * p.perm_bstride : nullptr;
     float* u = &sbuf[warp][g * S::RS];

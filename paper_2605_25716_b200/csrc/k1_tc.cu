@@ -53,6 +53,7 @@ struct K1TcParams {
     int64_t tiles_per_slab;
     int64_t total_tiles;
     int64_t tiles_per_cta;
+    int64_t x_batch_mod;
 };
 
 template <int D>
@@ -158,7 +159,8 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
             if (it + 2 < ntiles) fetch_src(it + 2, nxt2);
             if (it >= ST) tc::mbar_wait(&empty[st], (uint32_t)(((it / ST) - 1) & 1));
             const int64_t slab = (first + it) / p.tiles_per_slab;
-            const __nv_bfloat16* xs = p.x + slab * p.rows * D + c * 8;
+            const int64_t xslab = p.x_batch_mod > 0 ? ((slab / H) % p.x_batch_mod) * H + slab % H : slab;
+            const __nv_bfloat16* xs = p.x + xslab * p.rows * D + c * 8;
             uint8_t* a = a_base + st * S::TILE_BYTES + (c >> 3) * S::BLK_BYTES;
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
@@ -367,6 +369,7 @@ static cudaError_t launch_k1_tc_d(const K1Params& q, int64_t n_batch, cudaStream
     p.key_heads = q.key_heads;
     p.which = q.which;
     p.inv_t = q.inv_t;
+    p.x_batch_mod = q.x_batch_mod;
     p.tiles_per_slab = (q.rows + 127) / 128;
     p.total_tiles = p.tiles_per_slab * n_batch * q.n_heads;
     const int64_t grid = std::min<int64_t>(p.total_tiles, num_sms());

@@ -34,6 +34,7 @@ struct K1Params {
     int key_heads;
     int which;    // 0 phi_kq, 1 phi_v
     int inv_t;    // 1: phi^{-T}
+    int64_t x_batch_mod;   // > 0: request b reads x[b % x_batch_mod] (one Q, many key sets)
 };
 
 struct K2Params {

@@ -60,14 +60,18 @@ class RankCompute:
     scramble_q: Callable[[torch.Tensor, int, torch.Tensor], None]   # (q, dst_domain, out)
     serve: Callable[[torch.Tensor, torch.Tensor, tuple], None]       # (q_all, ret [B_tot, rec], dims): K2 + fold
     finish: Callable[[torch.Tensor, torch.Tensor, tuple], None]      # (ret_back [W, B_p, rec], out, dims): K3
+    scramble_q_all: Optional[Callable[[torch.Tensor, torch.Tensor], None]] = None   # (q, q_send [W, ...]) one launch
 
 
 def scrambled_decode_step(q: torch.Tensor, compute: RankCompute, bufs: StepBuffers, out: torch.Tensor,
                           group: Optional[dist.ProcessGroup] = None) -> torch.Tensor:
     """One layer step for this rank's requests q [B_p, Hq, Lq, d]; returns out [B_p, Hq, Lq, d]."""
     world = bufs.q_send.shape[0]
-    for dom in range(world):                                     # span_send_layer, per domain
-        compute.scramble_q(q, dom, bufs.q_send[dom])
+    if compute.scramble_q_all is not None:                       # span_send_layer, all domains at once
+        compute.scramble_q_all(q, bufs.q_send)
+    else:
+        for dom in range(world):
+            compute.scramble_q(q, dom, bufs.q_send[dom])
     if world > 1:
         dist.all_to_all_single(bufs.q_recv, bufs.q_send, group=group)   # SCR_Q
         q_all = bufs.q_recv
@@ -92,6 +96,13 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
     from . import capi, ops
 
     state = {}
+    # key sets of my requests for every destination domain, stacked domain-major [W * B_p, bytes]
+    keys_all = torch.cat([k.dev for k in inquirer_keys], 0).contiguous()
+
+    def scramble_q_all(q, q_send):
+        W = q_send.shape[0]
+        ops.scramble(q, keys_all, capi.PHI_FORWARD, capi.KEYS_KQ, None, out=q_send.view((-1,) + tuple(q_send.shape[2:])),
+                     key_heads=kv_heads or inquirer_keys[0].kv_heads, n_batch=W * q.shape[0])
 
     def scramble_q(q, dom, out):
         ops.scramble(q, inquirer_keys[dom].dev, capi.PHI_FORWARD, capi.KEYS_KQ, None, out=out,
@@ -120,4 +131,4 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
                                 batch_stride=rec, shape=(Bp, Hq, Lq, d)) for dom in range(W)]
         ops.unscramble_merge(srcs, out=out, key_heads=kv_heads or inquirer_keys[0].kv_heads)
 
-    return RankCompute(scramble_q, serve, finish)
+    return RankCompute(scramble_q, serve, finish, scramble_q_all)

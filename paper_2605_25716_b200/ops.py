@@ -61,13 +61,16 @@ def upload_perms(perms: Sequence, device) -> torch.Tensor:
 
 def scramble(x: torch.Tensor, keys: torch.Tensor, variant: int, which: int, perm: Optional[torch.Tensor] = None,
              out: Optional[torch.Tensor] = None, out_dtype: Optional[torch.dtype] = None, out_row_offset: int = 0,
-             key_heads: Optional[int] = None, stream=None) -> torch.Tensor:
+             key_heads: Optional[int] = None, n_batch: Optional[int] = None, stream=None) -> torch.Tensor:
     """K1. x [B, H, rows, d] -> out [B, H, cap, d] with out[b,h,off+i] = x[b,h,perm_b[i]] @ phi.
 
     keys: uint8 [B, keyset_bytes] (request b's key set in row b); perm: int32/u32 [B, rows] or None.
+    n_batch > B scrambles x once per stacked key set: request b reads x[b % B] (one query batch
+    for several destination domains in one launch).
     """
     _cuda(x, "x")
-    B, H, rows, d = x.shape
+    Bx, H, rows, d = x.shape
+    B = n_batch or Bx
     kh = key_heads if key_heads is not None else H
     if out is None:
         out = torch.empty((B, H, rows, d), dtype=out_dtype or x.dtype, device=x.device)
@@ -78,7 +81,8 @@ def scramble(x: torch.Tensor, keys: torch.Tensor, variant: int, which: int, perm
     check(capi.LIB.sda_scramble(_stream(stream), variant, which, x.data_ptr(), _dtype_code(x), B, H, rows, d,
                                 keys.data_ptr(), keys.stride(0) if keys.dim() > 1 else 0, kh, _ptr(perm),
                                 perm.stride(0) if perm is not None and perm.dim() > 1 else 0, out.data_ptr(),
-                                _dtype_code(out), out.shape[2], out_row_offset), "sda_scramble")
+                                _dtype_code(out), out.shape[2], out_row_offset, Bx if B != Bx else 0),
+          "sda_scramble")
     return out
 
 

@@ -28,11 +28,11 @@ def test_exports_every_declared_symbol():
 def test_status_mapping_without_device():
     L = capi.LIB
     # build_scrambler: d must be a power of two (scrambler.cpp:27)
-    assert L.sda_scramble(None, 0, 0, 1, 0, 1, 1, 1, 48, 1, 0, 1, None, 0, 1, 0, 1, 0) == 2
+    assert L.sda_scramble(None, 0, 0, 1, 0, 1, 1, 1, 48, 1, 0, 1, None, 0, 1, 0, 1, 0, 0) == 2
     # d = 16 is valid for the reference but not compiled for the device
-    assert L.sda_scramble(None, 0, 0, 1, 0, 1, 1, 1, 16, 1, 0, 1, None, 0, 1, 0, 1, 0) == 5
+    assert L.sda_scramble(None, 0, 0, 1, 0, 1, 1, 1, 16, 1, 0, 1, None, 0, 1, 0, 1, 0, 0) == 5
     # row offset beyond the cache capacity
-    assert L.sda_scramble(None, 0, 0, 1, 0, 1, 1, 4, 64, 1, 0, 1, None, 0, 1, 0, 3, 0) == 1
+    assert L.sda_scramble(None, 0, 0, 1, 0, 1, 1, 4, 64, 1, 0, 1, None, 0, 1, 0, 3, 0, 0) == 1
     # q heads not a multiple of kv heads
     assert L.sda_partial_attention(None, 1, 0, 1, 1, 0, 8, None, 1, 3, 2, 1, 64, 1, 1, 1) == 1
     # merge_shards: empty shard list (attention.cpp:90)
