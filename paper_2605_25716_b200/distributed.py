@@ -90,22 +90,36 @@ def scrambled_decode_step(q: torch.Tensor, compute: RankCompute, bufs: StepBuffe
 
 
 def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = None,
-                     kv_heads: Optional[int] = None) -> RankCompute:
+                     kv_heads: Optional[int] = None, q_first_pos: int = 0) -> RankCompute:
     """RankCompute backed by libsdattn_b200.so. inquirer_keys[dom] = DomainKeys of my requests on
-    domain dom + 1; shard = this rank's protocol.KVShard (all requests' rows of my domain)."""
+    domain dom + 1; shard = this rank's protocol.KVShard (all requests' rows of my domain).
+    q_first_pos: global position of the query span (its rows are shuffled by each domain's
+    span_perm(0, q_first_pos, L_q), identity for single-row decode)."""
     from . import capi, ops
 
     state = {}
     # key sets of my requests for every destination domain, stacked domain-major [W * B_p, bytes]
     keys_all = torch.cat([k.dev for k in inquirer_keys], 0).contiguous()
 
+    def q_perms(lq):
+        """(p_q stacked [W*B_p, L_q] for K1, [p_q^{-1} of domain dom]) -- None for L_q = 1."""
+        if lq == 1:
+            return None, [None] * len(inquirer_keys)
+        if state.get("lq") != lq:
+            fwd, inv = zip(*[k.span_perms(0, q_first_pos, lq) for k in inquirer_keys])
+            state["lq"], state["pq"], state["pq_inv"] = lq, torch.cat(fwd, 0).contiguous(), list(inv)
+        return state["pq"], state["pq_inv"]
+
     def scramble_q_all(q, q_send):
         W = q_send.shape[0]
-        ops.scramble(q, keys_all, capi.PHI_FORWARD, capi.KEYS_KQ, None, out=q_send.view((-1,) + tuple(q_send.shape[2:])),
+        pq, _ = q_perms(q.shape[2])
+        ops.scramble(q, keys_all, capi.PHI_FORWARD, capi.KEYS_KQ, pq, out=q_send.view((-1,) + tuple(q_send.shape[2:])),
                      key_heads=kv_heads or inquirer_keys[0].kv_heads, n_batch=W * q.shape[0])
 
     def scramble_q(q, dom, out):
-        ops.scramble(q, inquirer_keys[dom].dev, capi.PHI_FORWARD, capi.KEYS_KQ, None, out=out,
+        pq, _ = q_perms(q.shape[2])
+        ops.scramble(q, inquirer_keys[dom].dev, capi.PHI_FORWARD, capi.KEYS_KQ,
+                     None if pq is None else pq[dom * q.shape[0]:(dom + 1) * q.shape[0]], out=out,
                      key_heads=kv_heads or inquirer_keys[dom].kv_heads)
 
     def serve(q_all, ret, dims):
@@ -127,7 +141,8 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
     def finish(back, out, dims):
         Hq, Lq, d = dims
         W, Bp, rec = back.shape
-        srcs = [ops.MergeSource(back[dom], back[dom, :, Hq * Lq * d:], inquirer_keys[dom].dev, None,
+        _, pq_inv = q_perms(Lq)
+        srcs = [ops.MergeSource(back[dom], back[dom, :, Hq * Lq * d:], inquirer_keys[dom].dev, pq_inv[dom],
                                 batch_stride=rec, shape=(Bp, Hq, Lq, d)) for dom in range(W)]
         ops.unscramble_merge(srcs, out=out, key_heads=kv_heads or inquirer_keys[0].kv_heads)
 

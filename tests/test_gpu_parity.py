@@ -243,3 +243,20 @@ def test_distributed_step_packed_records_world1():
     got = out.double().cpu().numpy()
     ref = case.oracle()
     assert max_abs_rel(got, ref) < TOL_BF16 and rel_fro(got, ref) < TOL_BF16
+
+
+def test_distributed_step_prefill_rows_world1():
+    """The distributed step with a 200-row query span: p_q permutations on the way out (K1) and
+    their inverses on the way back (K3), tensor-core prefill K2, packed records."""
+    from paper_2605_25716_b200 import distributed as sdist
+    case = Case(B=2, Hq=4, Hkv=4, d=128, lk=1024, n_nodes=1, lq=200, dtype=torch.bfloat16, seed=23)
+    keys = protocol.DomainKeys(case.request_ids(), 0, 1, 4, 128, "cuda")
+    shard = protocol.KVShard(2, 4, 1024, 128, "cuda")
+    shard.ship_segment(dev(case.k[0], torch.bfloat16), dev(case.v[0], torch.bfloat16), keys, first_pos=0)
+    bufs = sdist.StepBuffers.allocate(1, 2, 4, 200, 128, torch.bfloat16, "cuda")
+    comp = sdist.gpu_rank_compute([keys], shard, n_splits=2, q_first_pos=case.q_first_pos)
+    out = torch.empty((2, 4, 200, 128), dtype=torch.float32, device="cuda")
+    sdist.scrambled_decode_step(dev(case.q, torch.bfloat16), comp, bufs, out)
+    got = out.double().cpu().numpy()
+    ref = case.oracle()
+    assert max_abs_rel(got, ref) < TOL_BF16 and rel_fro(got, ref) < TOL_BF16
