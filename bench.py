@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--graph", dest="graph", action="store_true", default=None,
                     help="replay the step (kernels + NCCL all-to-alls) as a CUDA graph (default on)")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1: move Q' and partials over NVLink peer memory (default) or NCCL all-to-all")
     ap.add_argument("--cpu-pairs", type=int, default=128, help="(request, head) pairs in the CPU sample")
     return ap.parse_args()
 
@@ -69,7 +71,7 @@ def workload_config(n):
         "context_per_request": CTX, "kv_rows_per_request_per_gpu": CTX // n, "domains": n,
         "kv_bytes_per_gpu": B_PER * n * H * (CTX // n) * D * 2 * 2,
         "l2": "inputs larger than L2 (2 GiB scrambled KV per GPU vs 126 MB L2), no flush needed",
-        "parallelism": f"kv-sharded x{n} (one domain per GPU), NCCL all-to-all of Q' and partials",
+        "parallelism": f"kv-sharded x{n} (one domain per GPU)",
     }
 
 
@@ -252,8 +254,10 @@ def run_ours(args, ws, rank, local):
                 serve0(q_all, o_out, st_out)
         comp.serve = serve_timed
 
+        exch = sdist.PeerExchange(bufs) if args.exchange == "p2p" else None
+
         def step(qin):
-            return sdist.scrambled_decode_step(qin, comp, bufs, out)
+            return sdist.scrambled_decode_step(qin, comp, bufs, out, exchange=exch)
 
     def barrier():
         if ws > 1:
@@ -366,7 +370,9 @@ def run_ours(args, ws, rank, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (torch.randn Q/K/V, bf16), keys from the reference key-derivation rule",
-            "config": workload_config(ws),
+            "config": dict(workload_config(ws), exchange=("Q' and (O', stats) over NVLink peer memory (exchange.cu)"
+                                                          if args.exchange == "p2p" else "NCCL all-to-all")
+                           if ws > 1 else "none (single domain)"),
             "e2e": {"value": B_tot / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": B_PER * H * D * 2, "d2h_bytes_per_step": B_PER * H * D * 4},
             "gpu_launches": int(launches) * args.steps, "cuda_graph": bool(args.graph),

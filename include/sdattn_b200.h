@@ -202,6 +202,27 @@ sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, i
                                 int64_t out_batch_stride);
 
 /* ------------------------------------------------------------------------------------------
+ * Peer-memory exchange (replaces Simulator::send of SCR_Q / SCR_SHARD, protocol.cpp:892-896,
+ * :1097-1102, inside one NVSwitch box). Receive buffers are mapped into every peer with CUDA
+ * IPC; a push copies each peer's payload over NVLink and raises that peer's per-sender flag
+ * (system-scope release) with the step epoch; a wait spins (acquire) until all of its flags
+ * reached the epoch (traps after ~4 s instead of hanging). All stream-ordered and graph-capturable.
+ * ------------------------------------------------------------------------------------------ */
+/* handle_out: 64 bytes (cudaIpcMemHandle_t of the allocation containing dev_ptr) + offset in it */
+sda_status sda_ipc_get_handle(const void* dev_ptr, void* handle_out, uint64_t* offset_out);
+sda_status sda_ipc_open_handle(const void* handle, uint64_t offset, void** dev_ptr_out);
+sda_status sda_ipc_close_handle(void* dev_ptr, uint64_t offset);
+/* *epoch += 1 (one per step, before the pushes / waits of that step) */
+sda_status sda_exchange_epoch(void* stream, uint32_t* epoch);
+/* for p < n_peers: copy bytes (multiple of 16) src[p] -> dst[p], then *peer_flags[p] = *epoch.
+ * counters: n_peers zero-initialised device u32 (self-resetting). */
+sda_status sda_exchange_push(void* stream, int32_t n_peers, const void* const* src, void* const* dst,
+                             uint32_t* const* peer_flags, uint64_t bytes, const uint32_t* epoch,
+                             uint32_t* counters);
+/* wait until flags[i] >= *epoch for i < n (wrap-around safe) */
+sda_status sda_exchange_wait(void* stream, const uint32_t* flags, int32_t n, const uint32_t* epoch);
+
+/* ------------------------------------------------------------------------------------------
  * Misc
  * ------------------------------------------------------------------------------------------ */
 int32_t sda_abi_version(void);

@@ -28,7 +28,8 @@ STATUS_NAMES = {0: "SDA_OK", 1: "SDA_ERR_INVALID_ARGUMENT", 2: "SDA_ERR_NOT_POW2
 EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_negotiate_keyset",
            "sda_span_perm", "sda_invert_permutation", "sda_keyset_bytes", "sda_pack_keyset", "sda_scramble",
            "sda_partial_attention", "sda_partial_attention_causal", "sda_default_splits", "sda_default_splits_gqa", "sda_unscramble_merge", "sda_abi_version",
-           "sda_status_string", "sda_launch_count")
+           "sda_status_string", "sda_launch_count", "sda_ipc_get_handle", "sda_ipc_open_handle",
+           "sda_ipc_close_handle", "sda_exchange_epoch", "sda_exchange_push", "sda_exchange_wait")
 
 
 class SdaError(RuntimeError):
@@ -90,6 +91,13 @@ def _load() -> ct.CDLL:
     lib.sda_unscramble_merge.argtypes = [_vp, ct.POINTER(MergeSource), ct.c_int32, ct.c_int64, ct.c_int32,
                                          ct.c_int64, ct.c_int64, ct.c_int32, ct.c_int64, ct.c_int32, _vp, ct.c_int32,
                                          _vp, _vp, ct.c_int64]
+    lib.sda_ipc_get_handle.argtypes = [_vp, _vp, ct.POINTER(ct.c_uint64)]
+    lib.sda_ipc_open_handle.argtypes = [_vp, ct.c_uint64, ct.POINTER(ct.c_void_p)]
+    lib.sda_ipc_close_handle.argtypes = [_vp, ct.c_uint64]
+    lib.sda_exchange_epoch.argtypes = [_vp, _vp]
+    lib.sda_exchange_push.argtypes = [_vp, ct.c_int32, ct.POINTER(ct.c_void_p), ct.POINTER(ct.c_void_p),
+                                      ct.POINTER(ct.c_void_p), ct.c_uint64, _vp, _vp]
+    lib.sda_exchange_wait.argtypes = [_vp, _vp, ct.c_int32, _vp]
     lib.sda_abi_version.restype = ct.c_int32
     lib.sda_status_string.restype = ct.c_char_p
     lib.sda_status_string.argtypes = [ct.c_int32]

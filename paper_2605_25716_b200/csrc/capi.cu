@@ -11,6 +11,14 @@ namespace {
 
 std::atomic<uint64_t> g_launches{0};
 
+}  // namespace
+
+namespace sda {
+void count_launch() { ++g_launches; }
+}  // namespace sda
+
+namespace {
+
 bool supported_dim(int d) { return d == 32 || d == 64 || d == 128 || d == 256; }
 bool pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
 // Debug knobs (tests compare kernel variants): SDA_K1_SIMT=1 / SDA_K2_SIMT=1 force the SIMT

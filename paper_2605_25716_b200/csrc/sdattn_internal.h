@@ -18,6 +18,7 @@ enum : int { kInFwd = 0, kInInvT = 1, kOutFwd = 2, kOutInvT = 3, kInvIn = 4, kIn
 enum : int { kP1 = 0, kP2 = 1, kP1Inv = 2, kP2Inv = 3 };
 
 uint64_t derive(uint64_t base, const uint64_t* tags, size_t n);
+void count_launch();   // sda_launch_count() bookkeeping for kernels launched outside capi.cu
 
 // Kernel parameter blocks (passed by value to the kernels).
 struct K1Params {

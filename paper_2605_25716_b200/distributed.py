@@ -63,16 +63,100 @@ class RankCompute:
     scramble_q_all: Optional[Callable[[torch.Tensor, torch.Tensor], None]] = None   # (q, q_send [W, ...]) one launch
 
 
+class PeerExchange:
+    """SCR_Q / SCR_SHARD over NVLink peer memory (exchange.cu) instead of NCCL all-to-alls.
+
+    Setup maps every peer's q_recv / ret_recv / flags (CUDA IPC handles traded once with
+    all_gather_object); each step: epoch += 1, push my Q' slices into the peers' q_recv[my rank]
+    and raise their flags, wait for mine, ... the same for the packed (O', stats) records. Same
+    data placement as all_to_all_single, so the compute is unchanged."""
+
+    def __init__(self, bufs: StepBuffers, group: Optional[dist.ProcessGroup] = None):
+        import ctypes as ct
+
+        from . import capi
+        self.capi, self.ct = capi, ct
+        self.world = bufs.q_send.shape[0]
+        self.rank = dist.get_rank(group)
+        dev = bufs.q_send.device
+        W = self.world
+        self.flags = torch.zeros(2 * W, dtype=torch.int32, device=dev)      # [SCR_Q from r | SCR_SHARD from r]
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.counters = torch.zeros(2 * W, dtype=torch.int32, device=dev)
+        mine = {}
+        for name, t in (("q", bufs.q_recv), ("ret", bufs.ret_recv), ("flags", self.flags)):
+            h = (ct.c_uint8 * 64)()
+            off = ct.c_uint64(0)
+            capi.check(capi.LIB.sda_ipc_get_handle(t.data_ptr(), h, ct.byref(off)), "ipc_get_handle")
+            mine[name] = (bytes(h), int(off.value))
+        everyone = [None] * W
+        dist.all_gather_object(everyone, mine, group=group)
+        self.opened = []
+        base = {}
+        for r in range(W):
+            for name, t in (("q", bufs.q_recv), ("ret", bufs.ret_recv), ("flags", self.flags)):
+                if r == self.rank:
+                    base[(r, name)] = t.data_ptr()
+                    continue
+                hb, off = everyone[r][name]
+                ptr = ct.c_void_p()
+                capi.check(capi.LIB.sda_ipc_open_handle((ct.c_uint8 * 64).from_buffer_copy(hb), off, ct.byref(ptr)),
+                           "ipc_open_handle")
+                self.opened.append((ptr.value, off))
+                base[(r, name)] = ptr.value
+        q_slot = bufs.q_send[0].numel() * bufs.q_send.element_size()
+        r_slot = bufs.ret_send[0].numel() * bufs.ret_send.element_size()
+        arr = lambda xs: (ct.c_void_p * W)(*xs)  # noqa: E731
+        self.q_args = (arr([bufs.q_send[p].data_ptr() for p in range(W)]),
+                       arr([base[(p, "q")] + self.rank * q_slot for p in range(W)]),
+                       arr([base[(p, "flags")] + 4 * self.rank for p in range(W)]), q_slot)
+        self.r_args = (arr([bufs.ret_send[p].data_ptr() for p in range(W)]),
+                       arr([base[(p, "ret")] + self.rank * r_slot for p in range(W)]),
+                       arr([base[(p, "flags")] + 4 * (W + self.rank) for p in range(W)]), r_slot)
+        dist.barrier(group=group)
+
+    def _stream(self):
+        return torch.cuda.current_stream().cuda_stream
+
+    def begin_step(self):
+        self.capi.check(self.capi.LIB.sda_exchange_epoch(self._stream(), self.epoch.data_ptr()), "exchange_epoch")
+
+    def _push(self, args, counters_off):
+        src, dst, flags, nbytes = args
+        self.capi.check(self.capi.LIB.sda_exchange_push(self._stream(), self.world, src, dst, flags, nbytes,
+                                                         self.epoch.data_ptr(),
+                                                         self.counters.data_ptr() + 4 * counters_off), "exchange_push")
+
+    def _wait(self, off):
+        self.capi.check(self.capi.LIB.sda_exchange_wait(self._stream(), self.flags.data_ptr() + 4 * off, self.world,
+                                                         self.epoch.data_ptr()), "exchange_wait")
+
+    def exchange_q(self):
+        self._push(self.q_args, 0)
+        self._wait(0)
+
+    def exchange_ret(self):
+        self._push(self.r_args, self.world)
+        self._wait(self.world)
+
+
 def scrambled_decode_step(q: torch.Tensor, compute: RankCompute, bufs: StepBuffers, out: torch.Tensor,
-                          group: Optional[dist.ProcessGroup] = None) -> torch.Tensor:
-    """One layer step for this rank's requests q [B_p, Hq, Lq, d]; returns out [B_p, Hq, Lq, d]."""
+                          group: Optional[dist.ProcessGroup] = None,
+                          exchange: Optional[PeerExchange] = None) -> torch.Tensor:
+    """One layer step for this rank's requests q [B_p, Hq, Lq, d]; returns out [B_p, Hq, Lq, d].
+    exchange: a PeerExchange to move Q' and the partials over NVLink peer memory (else NCCL)."""
     world = bufs.q_send.shape[0]
+    if exchange is not None:
+        exchange.begin_step()
     if compute.scramble_q_all is not None:                       # span_send_layer, all domains at once
         compute.scramble_q_all(q, bufs.q_send)
     else:
         for dom in range(world):
             compute.scramble_q(q, dom, bufs.q_send[dom])
-    if world > 1:
+    if world > 1 and exchange is not None:
+        exchange.exchange_q()                                         # SCR_Q over peer memory
+        q_all = bufs.q_recv
+    elif world > 1:
         dist.all_to_all_single(bufs.q_recv, bufs.q_send, group=group)   # SCR_Q
         q_all = bufs.q_recv
     else:
@@ -80,7 +164,10 @@ def scrambled_decode_step(q: torch.Tensor, compute: RankCompute, bufs: StepBuffe
     b_tot = q_all.shape[0] * q_all.shape[1]
     compute.serve(q_all.view((b_tot,) + tuple(q_all.shape[2:])),     # try_serve_q on my shard
                   bufs.ret_send.view(b_tot, -1), bufs.dims)
-    if world > 1:
+    if world > 1 and exchange is not None:
+        exchange.exchange_ret()                                       # SCR_SHARD over peer memory
+        back = bufs.ret_recv
+    elif world > 1:
         dist.all_to_all_single(bufs.ret_recv, bufs.ret_send, group=group)   # SCR_SHARD (O' + stats)
         back = bufs.ret_recv
     else:
