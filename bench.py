@@ -50,10 +50,18 @@ def parse():
     ap.add_argument("--graph", dest="graph", action="store_true", default=None,
                     help="replay the step (kernels + NCCL all-to-alls) as a CUDA graph (default on)")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
-    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
-                    help="N>1: move Q' and partials over NVLink peer memory (default) or NCCL all-to-all")
+    ap.add_argument("--exchange", choices=["fused", "p2p", "nccl"], default="fused",
+                    help="N>1: exchange folded into K1/K2/K3 over NVLink peer memory (default), separate "
+                         "peer-memory push/wait kernels, or NCCL all-to-all")
     ap.add_argument("--cpu-pairs", type=int, default=128, help="(request, head) pairs in the CPU sample")
     return ap.parse_args()
+
+
+EXCHANGE_DESC = {
+    "fused": "Q' and (O', stats) written over NVLink peer memory by K1 / K2 themselves, flag-synchronised",
+    "p2p": "Q' and (O', stats) over NVLink peer memory (exchange.cu push / wait kernels)",
+    "nccl": "NCCL all-to-all",
+}
 
 
 def dist_env():
@@ -237,6 +245,7 @@ def run_ours(args, ws, rank, local):
                 e1.record(stream)
                 k2_ev.append((e0, e1))
             return ops.unscramble_merge(srcs, out=out, key_heads=H)
+        step_k2 = step
     else:
         from paper_2605_25716_b200 import distributed as sdist
         bufs = sdist.StepBuffers.allocate(ws, B_PER, H, 1, D, torch.bfloat16, devn)
@@ -254,10 +263,17 @@ def run_ours(args, ws, rank, local):
                 serve0(q_all, o_out, st_out)
         comp.serve = serve_timed
 
-        exch = sdist.PeerExchange(bufs) if args.exchange == "p2p" else None
+        exch = sdist.PeerExchange(bufs) if args.exchange != "nccl" else None
 
         def step(qin):
             return sdist.scrambled_decode_step(qin, comp, bufs, out, exchange=exch)
+        step_k2 = step
+        if args.exchange == "fused":
+            bufs_f = sdist.StepBuffers.allocate(ws, B_PER, H, 1, D, torch.bfloat16, devn)
+            fused = sdist.FusedDecode(sdist.PeerExchange(bufs_f), bufs_f, inq_keys, shard, n_splits=S, kv_heads=H)
+
+            def step(qin):   # noqa: F811
+                return fused.step(qin, out)
 
     def barrier():
         if ws > 1:
@@ -287,7 +303,7 @@ def run_ours(args, ws, rank, local):
     t1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         t0.record(stream)
-        record["on"] = not args.graph
+        record["on"] = not args.graph and step is step_k2
         for _ in range(args.steps):
             run()
         record["on"] = False
@@ -296,11 +312,12 @@ def run_ours(args, ws, rank, local):
     barrier()
     launches = (capi.launch_count() - l0) // args.steps if not args.graph else launches_per_step
     ms = t0.elapsed_time(t1) / args.steps
-    if args.graph:
-        # K2 duration: the same launch, event-bracketed on the same stream, back to back
+    # K2 duration: the same launch, event-bracketed on the same stream, back to back (fused
+    # exchange: the K2 of the unfused step, i.e. the same kernel without the fold tail)
+    if args.graph or step is not step_k2:
         record["on"] = True
         for _ in range(max(10, args.steps // 10)):
-            step(q)
+            step_k2(q)
         record["on"] = False
         torch.cuda.synchronize()
     k2_ms = statistics.mean(a.elapsed_time(b) for a, b in k2_ev)
@@ -370,9 +387,7 @@ def run_ours(args, ws, rank, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (torch.randn Q/K/V, bf16), keys from the reference key-derivation rule",
-            "config": dict(workload_config(ws), exchange=("Q' and (O', stats) over NVLink peer memory (exchange.cu)"
-                                                          if args.exchange == "p2p" else "NCCL all-to-all")
-                           if ws > 1 else "none (single domain)"),
+            "config": dict(workload_config(ws), exchange=EXCHANGE_DESC[args.exchange] if ws > 1 else "none (single domain)"),
             "e2e": {"value": B_tot / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": B_PER * H * D * 2, "d2h_bytes_per_step": B_PER * H * D * 4},
             "gpu_launches": int(launches) * args.steps, "cuda_graph": bool(args.graph),

@@ -182,6 +182,26 @@ __device__ __forceinline__ void fwht_group(float* v, int lane) {
     }
 }
 
+// Cross-GPU signalling for the fused exchange (see exchange.cu): spin (acquire, system scope)
+// until *flag has reached `e` (wrap-around safe), trapping after ~4 s instead of hanging; raise
+// a flag with a release store.
+__device__ __forceinline__ void flag_wait(const uint32_t* flag, uint32_t e) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if ((int32_t)(v - e) >= 0) return;
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 4000000000ull) __trap();
+        __nanosleep(32);
+    }
+}
+__device__ __forceinline__ void flag_raise(uint32_t* flag, uint32_t e) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(e) : "memory");
+}
+
 __host__ __device__ __forceinline__ const uint8_t* scrambler_ptr(const void* keys, int64_t batch_stride,
                                                                  int64_t b, int kh, int d, int which) {
     return static_cast<const uint8_t*>(keys) + b * batch_stride + (int64_t)kh * 64 * d +

@@ -14,13 +14,12 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
 
 namespace sda {
-
-constexpr int kMaxPeers = 16;
 
 struct PushParams {
     const uint4* src[kMaxPeers];     // local payload for peer p
@@ -74,6 +73,12 @@ __global__ void wait_kernel(const uint32_t* flags, int n, const uint32_t* epoch)
         }
     }
     __syncthreads();
+}
+
+__global__ void timestamp_kernel(uint64_t* dst) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *dst = t;
 }
 
 }  // namespace sda
@@ -149,7 +154,11 @@ sda_status sda_exchange_push(void* stream, int32_t n_peers, const void* const* s
     p.n16 = (int64_t)(bytes / 16);
     p.epoch = epoch;
     p.done = counters;
-    int blocks = (int)std::min<int64_t>(16, (p.n16 + 255) / 256);
+    static const int max_blocks = [] {
+        const char* e = getenv("SDA_PUSH_BLOCKS");   // tuning knob (tools/step_timeline.py)
+        return e && atoi(e) > 0 ? atoi(e) : 16;
+    }();
+    int blocks = (int)std::min<int64_t>(max_blocks, (p.n16 + 255) / 256);
     if (blocks < 1) blocks = 1;
     sda::count_launch();
     sda::push_kernel<<<dim3(blocks, n_peers), 256, 0, static_cast<cudaStream_t>(stream)>>>(p);
@@ -160,6 +169,12 @@ sda_status sda_exchange_wait(void* stream, const uint32_t* flags, int32_t n, con
     if (!flags || !epoch || n <= 0 || n > 1024) return SDA_ERR_INVALID_ARGUMENT;
     sda::count_launch();
     sda::wait_kernel<<<1, ((n + 31) / 32) * 32, 0, static_cast<cudaStream_t>(stream)>>>(flags, n, epoch);
+    return from_cuda_x(cudaGetLastError());
+}
+
+sda_status sda_trace_timestamp(void* stream, uint64_t* dst) {
+    if (!dst) return SDA_ERR_INVALID_ARGUMENT;
+    sda::timestamp_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(dst);
     return from_cuda_x(cudaGetLastError());
 }
 

@@ -29,16 +29,31 @@ struct K1Shape {
 
 __device__ __forceinline__ int k1_sidx(int j) { return (j >> 4) * 20 + (j & 15); }
 
-template <int D, typename Tin, typename Tout>
-__global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p) {
+// FLAT (rows == 1, the decode Q): every lane group owns one (request, head) row, so one CTA
+// covers WARPS * R rows of the flattened [n_batch][n_heads] space instead of one (b, h) per CTA
+// with 63 of its 64 row slots idle.
+template <int D, typename Tin, typename Tout, bool FLAT>
+__global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p, const int64_t n_batch) {
     using S = K1Shape<D>;
     constexpr int E = S::E, LPR = S::LPR, R = S::R;
+    constexpr int ITERS = FLAT ? 1 : S::ITERS;
     __shared__ __align__(16) float sbuf[S::WARPS][R * S::RS];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane / LPR, lg = lane % LPR;
-    const int h = blockIdx.y;
-    const int64_t b = blockIdx.z;
+    int64_t b;
+    int h;
+    bool row_ok = true;
+    if constexpr (FLAT) {
+        int64_t f = (int64_t)blockIdx.x * (S::WARPS * R) + warp * R + g;
+        row_ok = f < n_batch * p.n_heads;
+        if (!row_ok) f = 0;
+        b = f / p.n_heads;
+        h = (int)(f % p.n_heads);
+    } else {
+        h = blockIdx.y;
+        b = blockIdx.z;
+    }
     const int kh = h / (p.n_heads / p.key_heads);
     const uint8_t* sc = scrambler_ptr(p.keys, p.keys_bstride, b, kh, D, p.which);
     const float* ftab = reinterpret_cast<const float*>(sc);
@@ -61,13 +76,16 @@ __global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p) {
 
     const int64_t xb = p.x_batch_mod > 0 ? b % p.x_batch_mod : b;
     const Tin* x = static_cast<const Tin*>(p.x) + (xb * p.n_heads + h) * p.rows * D;
-    Tout* out = static_cast<Tout*>(p.out) + ((b * p.n_heads + h) * p.out_rows_cap + p.out_row_offset) * D;
+    const bool fused = p.out_peer[0] != nullptr;   // push straight into the destination's receive slot
+    Tout* out = fused ? static_cast<Tout*>(p.out_peer[b / p.x_batch_mod]) +
+                            ((xb * p.n_heads + h) * p.out_rows_cap + p.out_row_offset) * D
+                      : static_cast<Tout*>(p.out) + ((b * p.n_heads + h) * p.out_rows_cap + p.out_row_offset) * D;
     const uint32_t* perm = p.perm ? p.perm + b * p.perm_bstride : nullptr;
     float* u = &sbuf[warp][g * S::RS];
 
-    for (int it = 0; it < S::ITERS; ++it) {
-        const int64_t r = (int64_t)blockIdx.x * S::ROWS_PER_CTA + (int64_t)it * S::WARPS * R + warp * R + g;
-        const bool valid = r < p.rows;
+    for (int it = 0; it < ITERS; ++it) {
+        const int64_t r = FLAT ? 0 : (int64_t)blockIdx.x * S::ROWS_PER_CTA + (int64_t)it * S::WARPS * R + warp * R + g;
+        const bool valid = row_ok && r < p.rows;
         const int64_t src = valid ? (perm ? (int64_t)perm[r] : r) : 0;
 
         float v[E];
@@ -91,14 +109,48 @@ __global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p) {
         if (valid) store_vec<E>(out + r * D + lg * E, v);
         __syncwarp();
     }
+    if (fused) {   // the CTA completing a destination's rows raises that destination's SCR_Q flag
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // rows of the flattened [n_batch][n_heads][rows] space this CTA wrote, per destination
+            const int64_t per_dest = p.x_batch_mod * p.n_heads * p.rows;
+            int64_t f0, f1;
+            if constexpr (FLAT) {
+                f0 = (int64_t)blockIdx.x * (S::WARPS * R);
+                f1 = f0 + S::WARPS * R;
+                if (f1 > n_batch * p.n_heads) f1 = n_batch * p.n_heads;
+            } else {
+                const int64_t base = (b * p.n_heads + h) * p.rows;
+                f0 = base + (int64_t)blockIdx.x * S::ROWS_PER_CTA;
+                f1 = f0 + S::ROWS_PER_CTA;
+                if (f1 > base + p.rows) f1 = base + p.rows;
+            }
+            for (int64_t d = f0 / per_dest; d * per_dest < f1; ++d) {
+                const int64_t lo = d * per_dest > f0 ? d * per_dest : f0;
+                const int64_t hi = (d + 1) * per_dest < f1 ? (d + 1) * per_dest : f1;
+                const unsigned n = (unsigned)(hi - lo);
+                if (atomicAdd(&p.dest_counters[d], n) + n == (unsigned)per_dest) {
+                    p.dest_counters[d] = 0;
+                    __threadfence_system();
+                    flag_raise(p.peer_flag[d], *p.epoch);
+                }
+            }
+        }
+    }
 }
 
 template <int D, typename Tin, typename Tout>
 static cudaError_t launch_k1_t(const K1Params& p, int64_t n_batch, cudaStream_t st) {
     using S = K1Shape<D>;
+    if (p.rows == 1) {
+        const int64_t n = n_batch * p.n_heads, per = S::WARPS * S::R;
+        k1_scramble_kernel<D, Tin, Tout, true><<<(unsigned)((n + per - 1) / per), 128, 0, st>>>(p, n_batch);
+        return cudaGetLastError();
+    }
     const dim3 grid((unsigned)((p.rows + S::ROWS_PER_CTA - 1) / S::ROWS_PER_CTA), (unsigned)p.n_heads,
                     (unsigned)n_batch);
-    k1_scramble_kernel<D, Tin, Tout><<<grid, 128, 0, st>>>(p);
+    k1_scramble_kernel<D, Tin, Tout, false><<<grid, 128, 0, st>>>(p, n_batch);
     return cudaGetLastError();
 }
 

@@ -40,6 +40,10 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
     const int split = blockIdx.x, h = blockIdx.y;
     const int64_t b = (int64_t)blockIdx.z / p.q_rows, qr = (int64_t)blockIdx.z % p.q_rows;
     const int kvh = h / (p.q_heads / p.kv_heads);
+    if (p.wait_flags) {   // fused exchange: this request's Q' must have arrived from its inquirer
+        if (threadIdx.x == 0) flag_wait(p.wait_flags + b / p.wait_group, *p.epoch);
+        __syncthreads();
+    }
 
     int64_t len = p.kv_len ? (int64_t)p.kv_len[b] : p.kv_cap;
     if (p.causal) {   // keys j <= qr + offset only (AttentionMask::causal, attention.cpp:16-27)
@@ -135,6 +139,58 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
         // back to natural-log units: row_max = max_j q.k_j / sqrt(d)
         p.out_stats[orow * 2 + 0] = S_ > 0.f ? M / kLog2e : -INFINITY;
         p.out_stats[orow * 2 + 1] = S_;
+    }
+    if (!p.fold_counters) return;
+
+    // ---- fused exchange: the last split CTA of this row folds the splits (merge_shards in
+    // scrambled space, attention.cpp:89-123) and pushes the packed (O', stats) record to the
+    // inquirer; the last row of a destination raises its SCR_SHARD flag
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    const int64_t row = (b * p.q_heads + h) * p.q_rows + qr;
+    if (threadIdx.x == 0) last = atomicAdd(&p.fold_counters[row], 1u) == (unsigned)p.n_splits - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int64_t split_stride = p.n_batch * p.q_heads * p.q_rows;
+    float ms = -INFINITY;
+    for (int sp = 0; sp < p.n_splits; ++sp) {
+        const float2 st = __ldcg(reinterpret_cast<const float2*>(p.out_stats) + sp * split_stride + row);
+        if (st.y > 0.f) ms = fmaxf(ms, st.x);
+    }
+    float den = 0.f;
+    const int64_t dest = b / p.wait_group, i = b % p.wait_group;
+    float* rec = p.rec_peer[dest] + i * p.rec_stride;
+    const int64_t hr = (int64_t)h * p.q_rows + qr;
+    for (int dim = threadIdx.x; dim < D; dim += blockDim.x) {
+        float acc = 0.f, dd = 0.f;
+        for (int sp = 0; sp < p.n_splits; ++sp) {
+            const float2 st = __ldcg(reinterpret_cast<const float2*>(p.out_stats) + sp * split_stride + row);
+            if (st.y > 0.f) {
+                const float w = st.y * expf(st.x - ms);
+                dd += w;
+                acc = fmaf(w, __ldcg(p.out_o + (sp * split_stride + row) * D + dim), acc);
+            }
+        }
+        rec[hr * D + dim] = dd > 0.f ? acc / dd : 0.f;
+        den = dd;
+    }
+    if (threadIdx.x == 0) {
+        float* st = rec + (int64_t)p.q_heads * p.q_rows * D + hr * 2;
+        st[0] = den > 0.f ? ms : -INFINITY;
+        st[1] = den;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        p.fold_counters[row] = 0;
+        const unsigned rows_per_dest = (unsigned)(p.wait_group * p.q_heads * p.q_rows);
+        if (atomicAdd(&p.dest_counters[dest], 1u) == rows_per_dest - 1) {
+            p.dest_counters[dest] = 0;
+            __threadfence_system();
+            flag_raise(p.rec_flag[dest], *p.epoch);
+        }
     }
 }
 

@@ -17,25 +17,34 @@
 
 namespace sda {
 
+// Per-lane slice of one source's phi_V^{-1} tables (and its O' row and stats), loaded one
+// source ahead of its use so the dependent HBM / NVLink-written reads of consecutive sources
+// overlap instead of forming one latency chain per source.
+template <int E>
+struct SrcLd {
+    float2 st;
+    float ov[E];
+    float inv_in[E], inv_out[E];
+    int p2[E], p1[E];
+};
+
 template <int D>
-__device__ __forceinline__ void unscramble_acc(const uint8_t* sc, float* acc, float* out, float* sh, int lane) {
+__device__ __forceinline__ void unscramble_acc(const SrcLd<D / 32>& L, float* acc, float* out, float* sh, int lane) {
     constexpr int E = D / 32;
-    const float* ftab = reinterpret_cast<const float*>(sc);
-    const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + 24 * D);
     // t[i] = acc[i] / s2[i] ; u[j] = t[P2[j]] ; w = H u ; y[i] = w[P1[i]] / (s1[i] sqrt(d))
 #pragma unroll
-    for (int e = 0; e < E; ++e) sh[lane * E + e] = acc[e] * ftab[kInvIn * D + lane * E + e];
+    for (int e = 0; e < E; ++e) sh[lane * E + e] = acc[e] * L.inv_in[e];
     __syncwarp();
     float v[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = sh[utab[kP2 * D + lane * E + e]];
+    for (int e = 0; e < E; ++e) v[e] = sh[L.p2[e]];
     fwht_group<E, 32>(v, lane);
     __syncwarp();
 #pragma unroll
     for (int e = 0; e < E; ++e) sh[lane * E + e] = v[e];
     __syncwarp();
 #pragma unroll
-    for (int e = 0; e < E; ++e) out[e] += sh[utab[kP1 * D + lane * E + e]] * ftab[kInvOut * D + lane * E + e];
+    for (int e = 0; e < E; ++e) out[e] += sh[L.p1[e]] * L.inv_out[e];
     __syncwarp();
 }
 
@@ -46,25 +55,60 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* sh = sh_all[warp];
     const int64_t total = p.n_batch * p.q_heads * p.q_rows;
-    const int64_t row = (int64_t)blockIdx.x * 4 + warp;
-    if (row >= total) return;
+    if (p.wait_flags) {   // fused exchange: every domain's SCR_SHARD records must have arrived
+        if (threadIdx.x < p.n_wait) flag_wait(p.wait_flags + threadIdx.x, *p.epoch);
+        __syncthreads();
+    }
+    const int64_t row_raw = (int64_t)blockIdx.x * 4 + warp;
+    const bool active = row_raw < total;
+    const int64_t row = active ? row_raw : total - 1;   // inactive warps compute a dummy row, store nothing
     const int64_t r = row % p.q_rows;
     const int64_t bh = row / p.q_rows;
     const int h = (int)(bh % p.q_heads);
     const int64_t b = bh / p.q_heads;
     const int kh = h / (p.q_heads / p.key_heads);
 
-    // pass 1: M* over sources with exp_sum > 0 (attention.cpp:103-105); lanes stride sources
-    float mstar = -INFINITY;
-    for (int s = lane; s < p.n_src; s += 32) {
-        const K3Source& src = p.src[s];
+    auto offsets = [&](const K3Source& src, int64_t& st_off, int64_t& o_off) {
         const int64_t ri = src.pq_inv ? (int64_t)src.pq_inv[b * p.pq_bstride + r] : r;
-        const int64_t st_off = src.bstride ? b * src.bstride + ((int64_t)h * p.q_rows + ri) * 2 : (bh * p.q_rows + ri) * 2;
-        const float2 st = *reinterpret_cast<const float2*>(src.stats + st_off);
+        st_off = src.bstride ? b * src.bstride + ((int64_t)h * p.q_rows + ri) * 2 : (bh * p.q_rows + ri) * 2;
+        o_off = src.bstride ? b * src.bstride + ((int64_t)h * p.q_rows + ri) * D : (bh * p.q_rows + ri) * D;
+    };
+
+    // pass 1: M* over sources with exp_sum > 0 (attention.cpp:103-105); lanes stride sources,
+    // lane s keeps source s's stats for pass 2 (n_src <= 32)
+    float mstar = -INFINITY;
+    float2 st_lane = make_float2(-INFINITY, 0.f);
+    for (int s = lane; s < p.n_src; s += 32) {
+        int64_t st_off, o_off;
+        offsets(p.src[s], st_off, o_off);
+        const float2 st = *reinterpret_cast<const float2*>(p.src[s].stats + st_off);
+        if (s == lane) st_lane = st;
         if (st.y > 0.f) mstar = fmaxf(mstar, st.x);
     }
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) mstar = fmaxf(mstar, __shfl_xor_sync(0xffffffffu, mstar, m));
+
+    auto load_src = [&](int s, SrcLd<E>& L) {
+        const K3Source& src = p.src[s];
+        int64_t st_off, o_off;
+        offsets(src, st_off, o_off);
+        const float sx = __shfl_sync(0xffffffffu, st_lane.x, s & 31);
+        const float sy = __shfl_sync(0xffffffffu, st_lane.y, s & 31);
+        L.st = p.n_src <= 32 ? make_float2(sx, sy) : *reinterpret_cast<const float2*>(src.stats + st_off);
+        load_vec_any<E>(src.o + o_off + lane * E, L.ov);
+        if (src.keys) {
+            const uint8_t* sc = scrambler_ptr(src.keys, p.keys_bstride, b, kh, D, 1);
+            const float* ftab = reinterpret_cast<const float*>(sc);
+            const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + 24 * D);
+            load_vec_any<E>(ftab + kInvIn * D + lane * E, L.inv_in);
+            load_vec_any<E>(ftab + kInvOut * D + lane * E, L.inv_out);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                L.p2[e] = utab[kP2 * D + lane * E + e];
+                L.p1[e] = utab[kP1 * D + lane * E + e];
+            }
+        }
+    };
 
     float out[E], acc[E];
 #pragma unroll
@@ -72,25 +116,22 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
     float denom = 0.f;
     const bool single = p.n_src == 1;
     bool pending = false;
+    SrcLd<E> cur, nxt;
+    load_src(0, cur);
     for (int s = 0; s < p.n_src; ++s) {
+        if (s + 1 < p.n_src) load_src(s + 1, nxt);
         const K3Source& src = p.src[s];
-        const int64_t ri = src.pq_inv ? (int64_t)src.pq_inv[b * p.pq_bstride + r] : r;
-        const int64_t st_off = src.bstride ? b * src.bstride + ((int64_t)h * p.q_rows + ri) * 2 : (bh * p.q_rows + ri) * 2;
-        const int64_t o_off = src.bstride ? b * src.bstride + ((int64_t)h * p.q_rows + ri) * D : (bh * p.q_rows + ri) * D;
-        const float2 st = *reinterpret_cast<const float2*>(src.stats + st_off);
-        if (st.y > 0.f) {
-            const float w = single ? 1.f : st.y * expf(st.x - mstar);
-            denom += single ? st.y : w;
-            float ov[E];
-            load_vec_any<E>(src.o + o_off + lane * E, ov);
+        if (cur.st.y > 0.f) {
+            const float w = single ? 1.f : cur.st.y * expf(cur.st.x - mstar);
+            denom += single ? cur.st.y : w;
 #pragma unroll
-            for (int e = 0; e < E; ++e) acc[e] = fmaf(w, ov[e], acc[e]);
+            for (int e = 0; e < E; ++e) acc[e] = fmaf(w, cur.ov[e], acc[e]);
             pending = true;
         }
         const bool group_end = (s + 1 == p.n_src) || (p.src[s + 1].keys != src.keys);
         if (group_end && pending) {
             if (src.keys) {
-                unscramble_acc<D>(scrambler_ptr(src.keys, p.keys_bstride, b, kh, D, 1), acc, out, sh, lane);
+                unscramble_acc<D>(cur, acc, out, sh, lane);
             } else {
 #pragma unroll
                 for (int e = 0; e < E; ++e) out[e] += acc[e];
@@ -99,18 +140,30 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
             for (int e = 0; e < E; ++e) acc[e] = 0.f;
             pending = false;
         }
+        cur = nxt;
     }
     const bool masked = !(mstar > -INFINITY);
-    if (masked && lane == 0 && p.err) atomicExch(p.err, (int32_t)SDA_ERR_MASKED_ROW);
+    if (masked && lane == 0 && p.err && active) atomicExch(p.err, (int32_t)SDA_ERR_MASKED_ROW);
     const float inv = masked ? __int_as_float(0x7fc00000) : (single ? 1.f : 1.f / denom);
 #pragma unroll
     for (int e = 0; e < E; ++e) out[e] *= inv;
     const int64_t hr = (int64_t)h * p.q_rows + r;
-    store_vec_any<E>(static_cast<TOut*>(p.out) + (p.out_bstride ? b * p.out_bstride + hr * D : row * D) + lane * E, out);
-    if (p.out_stats && lane == 0) {
+    if (active)
+        store_vec_any<E>(static_cast<TOut*>(p.out) + (p.out_bstride ? b * p.out_bstride + hr * D : row * D) + lane * E, out);
+    if (p.out_stats && lane == 0 && active) {
         const int64_t so = p.out_bstride ? b * p.out_bstride + hr * 2 : row * 2;
         p.out_stats[so + 0] = single ? (masked ? -INFINITY : mstar) : mstar;
         p.out_stats[so + 1] = masked ? 0.f : denom;
+    }
+    if (p.epoch && p.done_counter) {   // fused exchange: the last CTA opens the next step's epoch
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(p.done_counter, 1u) == gridDim.x - 1) {
+                *p.done_counter = 0;
+                *p.epoch += 1;
+            }
+        }
     }
 }
 

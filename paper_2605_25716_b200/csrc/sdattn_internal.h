@@ -7,6 +7,8 @@
 
 namespace sda {
 
+constexpr int kMaxPeers = 16;
+
 // Packed device scrambler for head dim d (SDA_SCRAMBLER_BYTES(d) = 32 d bytes):
 //   f32 tables [6][d] then u16 tables [4][d].
 // With R = 1/sqrt(d) (the normalised FWHT scale, fwht.cpp:24) and the raw +-1 butterfly H:
@@ -36,6 +38,13 @@ struct K1Params {
     int which;    // 0 phi_kq, 1 phi_v
     int inv_t;    // 1: phi^{-T}
     int64_t x_batch_mod;   // > 0: request b reads x[b % x_batch_mod] (one Q, many key sets)
+    // fused peer push (exchange): request b's rows go to out_peer[b / x_batch_mod] (a peer's
+    // receive slot, row layout as `out` with batch x_batch_mod); the last CTA of a destination
+    // raises *peer_flag[dest] = *epoch (system-scope release)
+    void* out_peer[kMaxPeers];
+    uint32_t* peer_flag[kMaxPeers];
+    const uint32_t* epoch;
+    uint32_t* dest_counters;   // [n_dest] zeroed, self-resetting
 };
 
 struct K2Params {
@@ -54,6 +63,17 @@ struct K2Params {
     float scale;   // 1/sqrt(d) (attention.cpp:45)
     int causal;            // 1: key j visible to query row i iff j <= i + causal_offset (attention.hpp:25-27)
     int64_t causal_offset;
+    // fused exchange (decode): wait for this request's SCR_Q (flag of sender b / wait_group),
+    // fold the splits in the last CTA of a row, push the packed (O', stats) record to the
+    // inquirer's receive slot and raise its flag once all of its rows are in
+    const uint32_t* wait_flags;
+    int64_t wait_group;
+    const uint32_t* epoch;
+    uint32_t* fold_counters;   // [n_batch * q_heads * q_rows] zeroed, self-resetting
+    float* rec_peer[kMaxPeers];
+    uint32_t* rec_flag[kMaxPeers];
+    int64_t rec_stride;        // floats per request record (q_heads * q_rows * (d + 2))
+    uint32_t* dest_counters;   // [n_dest] zeroed, self-resetting
 };
 
 struct K3Source {
@@ -77,6 +97,11 @@ struct K3Params {
     float* out_stats;
     int32_t* err;
     int64_t out_bstride;   // elements between requests (out and out_stats); 0 = dense
+    // fused exchange: wait until wait_flags[0..n_wait) >= *epoch; the last CTA bumps *epoch
+    const uint32_t* wait_flags;
+    int n_wait;
+    uint32_t* epoch;
+    uint32_t* done_counter;
 };
 
 }  // namespace sda

@@ -104,6 +104,7 @@ class PeerExchange:
                            "ipc_open_handle")
                 self.opened.append((ptr.value, off))
                 base[(r, name)] = ptr.value
+        self.base = base
         q_slot = bufs.q_send[0].numel() * bufs.q_send.element_size()
         r_slot = bufs.ret_send[0].numel() * bufs.ret_send.element_size()
         arr = lambda xs: (ct.c_void_p * W)(*xs)  # noqa: E731
@@ -138,6 +139,71 @@ class PeerExchange:
     def exchange_ret(self):
         self._push(self.r_args, self.world)
         self._wait(self.world)
+
+
+class FusedDecode:
+    """The decode step (L_q = 1) with the exchange folded into the kernels themselves: K1 writes
+    each destination's Q' straight into its receive slot over NVLink and raises its SCR_Q flag, K2
+    waits for its Q', folds its splits and pushes the packed (O', stats) record back to the
+    inquirer, K3 waits for every domain's record and opens the next epoch -- 3 launches per step
+    instead of 9, same data placement as PeerExchange / all_to_all_single (which stay the
+    reference-shaped form). GPU only."""
+
+    def __init__(self, exchange: PeerExchange, bufs: StepBuffers, inquirer_keys: Sequence, shard,
+                 n_splits: Optional[int] = None, kv_heads: Optional[int] = None):
+        from . import capi, ops
+        ct = exchange.ct
+        self.capi, self.ops, self.ex, self.bufs = capi, ops, exchange, bufs
+        W, rank = exchange.world, exchange.rank
+        Hq, Lq, d = bufs.dims
+        if Lq != 1:
+            raise ValueError("FusedDecode handles single-row decode (L_q = 1)")
+        self.W, self.Bp, self.Hq, self.d = W, bufs.q_send.shape[1], Hq, d
+        dev = bufs.q_send.device
+        self.kv_heads = kv_heads or inquirer_keys[0].kv_heads
+        self.keys_all = torch.cat([k.dev for k in inquirer_keys], 0).contiguous()
+        self.shard = shard
+        B = W * self.Bp
+        self.S = n_splits or capi.default_splits(B, Hq, 1, shard.capacity, kv_heads=shard.k.shape[1], head_dim=d)
+        self.work_o = torch.empty((self.S, B, Hq, 1, d), dtype=torch.float32, device=dev)
+        self.work_st = torch.empty((self.S, B, Hq, 1, 2), dtype=torch.float32, device=dev)
+        # [K1 dest counters W | K2 dest counters W | K3 done 1 | K2 per-row fold counters B*Hq]
+        self.counters = torch.zeros(2 * W + 1 + B * Hq, dtype=torch.int32, device=dev)
+        exchange.epoch.fill_(1)
+        self.q_dst, self.q_flag = exchange.q_args[1], exchange.q_args[2]
+        self.r_dst, self.r_flag = exchange.r_args[1], exchange.r_args[2]
+        rec = bufs.ret_recv.shape[-1]
+        srcs = [ops.MergeSource(bufs.ret_recv[dom], bufs.ret_recv[dom, :, Hq * d:], inquirer_keys[dom].dev, None,
+                                batch_stride=rec, shape=(self.Bp, Hq, 1, d)) for dom in range(W)]
+        self.srcs = (capi.MergeSource * W)()
+        for i, s in enumerate(srcs):
+            self.srcs[i].o, self.srcs[i].stats = s.o.data_ptr(), s.stats.data_ptr()
+            self.srcs[i].keys, self.srcs[i].pq_inv, self.srcs[i].batch_stride = s.keys.data_ptr(), None, rec
+        self.kstride = inquirer_keys[0].dev.stride(0) if inquirer_keys[0].dev.dim() > 1 else 0
+        self.ct = ct
+
+    def step(self, q: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        capi, ops, L = self.capi, self.ops, self.capi.LIB
+        st = torch.cuda.current_stream().cuda_stream
+        W, Bp, Hq, d, S = self.W, self.Bp, self.Hq, self.d, self.S
+        ep, cnt = self.ex.epoch.data_ptr(), self.counters.data_ptr()
+        flags = self.ex.flags.data_ptr()
+        sh = self.shard
+        capi.check(L.sda_fused_scramble_q(st, q.data_ptr(), ops._dtype_code(q), W, Bp, Hq, d, self.keys_all.data_ptr(),
+                                          self.keys_all.stride(0), self.kv_heads, self.q_dst,
+                                          ops._dtype_code(self.bufs.q_recv), self.q_flag, ep, cnt),
+                   "sda_fused_scramble_q")
+        capi.check(L.sda_fused_partial_attention(st, self.bufs.q_recv.data_ptr(), ops._dtype_code(self.bufs.q_recv),
+                                                 sh.k.data_ptr(), sh.v.data_ptr(), ops._dtype_code(sh.k), sh.capacity,
+                                                 sh.kv_len.data_ptr(), W, Bp, Hq, sh.k.shape[1], d, S,
+                                                 self.work_o.data_ptr(), self.work_st.data_ptr(), flags, ep,
+                                                 cnt + 4 * (2 * W + 1), self.r_dst, self.r_flag, cnt + 4 * W),
+                   "sda_fused_partial_attention")
+        capi.check(L.sda_fused_unscramble_merge(st, self.srcs, W, self.kstride, self.kv_heads, 0, Bp, Hq, 1, d,
+                                                out.data_ptr(), ops._dtype_code(out), flags + 4 * W, W, ep,
+                                                cnt + 4 * 2 * W),
+                   "sda_fused_unscramble_merge")
+        return out
 
 
 def scrambled_decode_step(q: torch.Tensor, compute: RankCompute, bufs: StepBuffers, out: torch.Tensor,

@@ -30,28 +30,43 @@ def main():
     bufs = sdist.StepBuffers.allocate(world, BP, H, 1, D, torch.bfloat16, dev)
     comp = sdist.gpu_rank_compute(inq, shard, kv_heads=H)
     exch = sdist.PeerExchange(bufs)
+    bufs_f = sdist.StepBuffers.allocate(world, BP, H, 1, D, torch.bfloat16, dev)
+    fused = sdist.FusedDecode(sdist.PeerExchange(bufs_f), bufs_f, inq, shard, kv_heads=H)
     out_n = torch.empty((BP, H, 1, D), dtype=torch.float32, device=dev)
     out_p = torch.empty_like(out_n)
+    out_f = torch.empty_like(out_n)
     ok = True
+    worst_f = 0.0
     for it in range(20):
         q = torch.randn((BP, H, 1, D), generator=g, device=dev).to(torch.bfloat16)
         sdist.scrambled_decode_step(q, comp, bufs, out_n)
         sdist.scrambled_decode_step(q, comp, bufs, out_p, exchange=exch)
+        fused.step(q, out_f)
         torch.cuda.synchronize()
         ok &= bool(torch.equal(out_n, out_p)) and bool(torch.isfinite(out_p).all())
+        # the fused split fold uses expf + a division, K3's fold exp2 + a reciprocal: ~1 ulp apart
+        worst_f = max(worst_f, float((out_f - out_n).abs().max() / out_n.abs().max()))
     # inside a CUDA graph, replayed
     q_static = torch.randn((BP, H, 1, D), generator=g, device=dev).to(torch.bfloat16)
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph):
         sdist.scrambled_decode_step(q_static, comp, bufs, out_p, exchange=exch)
+    graph_f = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph_f):
+        fused.step(q_static, out_f)
     for it in range(10):
         q_static.copy_(torch.randn((BP, H, 1, D), generator=g, device=dev).to(torch.bfloat16))
         graph.replay()
+        graph_f.replay()
         torch.cuda.synchronize()
         sdist.scrambled_decode_step(q_static, comp, bufs, out_n)
         torch.cuda.synchronize()
         ok &= bool(torch.equal(out_n, out_p))
-    print(f"rank {rank}: peer exchange == NCCL over 30 steps (eager + graph): {ok}", flush=True)
+        worst_f = max(worst_f, float((out_f - out_n).abs().max() / out_n.abs().max()))
+    ok_f = worst_f < 1e-5
+    print(f"rank {rank}: peer exchange == NCCL over 30 steps (eager + graph): {ok}; "
+          f"fused exchange max rel diff {worst_f:.2e} ({'ok' if ok_f else 'FAIL'})", flush=True)
+    ok &= ok_f
     torch.cuda.synchronize()
     dist.barrier(device_ids=[local])
     sys.stdout.flush()

@@ -59,5 +59,45 @@ def main():
     print("multi-GPU path (world 1):", {k: round(v, 1) for k, v in r2.items()}, "total us", round(sum(r2.values()), 1))
 
 
-if __name__ == "__main__":
+def multi():
+    """Under torchrun: per-phase device time of the peer-exchange step on every rank."""
+    import torch.distributed as dist
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    Lr = L // world
+    Bt = B * world
+    keys_own = protocol.DomainKeys(list(range(1, Bt + 1)), 0, rank + 1, H, D, dev)
+    shard = protocol.KVShard(Bt, H, Lr, D, dev)
+    g = torch.Generator(device=dev).manual_seed(rank)
+    shard.ship_segment(torch.randn((Bt, H, Lr, D), generator=g, device=dev).to(torch.bfloat16),
+                       torch.randn((Bt, H, Lr, D), generator=g, device=dev).to(torch.bfloat16), keys_own, rank * Lr)
+    inq = [protocol.DomainKeys(list(range(rank * B + 1, rank * B + B + 1)), 0, d + 1, H, D, dev) for d in range(world)]
+    bufs = sdist.StepBuffers.allocate(world, B, H, 1, D, torch.bfloat16, dev)
+    comp = sdist.gpu_rank_compute(inq, shard, kv_heads=H)
+    ex = sdist.PeerExchange(bufs)
+    q = torch.randn((B, H, 1, D), generator=g, device=dev).to(torch.bfloat16)
+    out = torch.empty((B, H, 1, D), dtype=torch.float32, device=dev)
+    qa = bufs.q_recv.view(Bt, H, 1, D)
+    ret = bufs.ret_send.view(Bt, -1)
+    phases = [("epoch", ex.begin_step), ("K1", lambda: comp.scramble_q_all(q, bufs.q_send)),
+              ("push Q", lambda: ex._push(ex.q_args, 0)), ("wait Q", lambda: ex._wait(0)),
+              ("K2+fold", lambda: comp.serve(qa, ret, bufs.dims)), ("push ret", lambda: ex._push(ex.r_args, world)),
+              ("wait ret", lambda: ex._wait(world)), ("K3", lambda: comp.finish(bufs.ret_recv, out, bufs.dims))]
+    for _ in range(5):
+        for _, fn in phases:
+            fn()
+    torch.cuda.synchronize()
+    dist.barrier(device_ids=[local])
+    r = timed(phases, 50)
+    print(f"rank {rank}:", {k: round(v, 1) for k, v in r.items()}, "sum", round(sum(r.values()), 1), flush=True)
+    torch.cuda.synchronize()
+    dist.barrier(device_ids=[local])
+    os._exit(0)
+
+
+if __name__ == "__main__" and "RANK" in os.environ:
+    multi()
+elif __name__ == "__main__":
     main()
