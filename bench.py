@@ -50,9 +50,9 @@ def parse():
     ap.add_argument("--graph", dest="graph", action="store_true", default=None,
                     help="replay the step (kernels + NCCL all-to-alls) as a CUDA graph (default on)")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
-    ap.add_argument("--exchange", choices=["fused", "p2p", "nccl"], default="fused",
-                    help="N>1: exchange folded into K1/K2/K3 over NVLink peer memory (default), separate "
-                         "peer-memory push/wait kernels, or NCCL all-to-all")
+    ap.add_argument("--exchange", choices=["fused", "p2p", "nccl"], default="p2p",
+                    help="N>1: peer-memory push/wait kernels (default), the exchange folded into K1/K2/K3 "
+                         "(fewer launches, measured no faster), or NCCL all-to-all")
     ap.add_argument("--cpu-pairs", type=int, default=128, help="(request, head) pairs in the CPU sample")
     return ap.parse_args()
 
