@@ -50,15 +50,16 @@ def parse():
     ap.add_argument("--graph", dest="graph", action="store_true", default=None,
                     help="replay the step (kernels + NCCL all-to-alls) as a CUDA graph (default on)")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
-    ap.add_argument("--exchange", choices=["fused", "p2p", "nccl"], default="p2p",
-                    help="N>1: peer-memory push/wait kernels (default), the exchange folded into K1/K2/K3 "
-                         "(fewer launches, measured no faster), or NCCL all-to-all")
+    ap.add_argument("--exchange", choices=["ll", "p2p", "nccl"], default="ll",
+                    help="N>1: the exchange carried by K1/K2/K3 themselves in LL format over NVLink peer "
+                         "memory (default), separate peer-memory push/wait kernels, or NCCL all-to-all")
+    ap.add_argument("--ll-single", action="store_true", help="N=1: run the LL-chained step too (measured no faster)")
     ap.add_argument("--cpu-pairs", type=int, default=128, help="(request, head) pairs in the CPU sample")
     return ap.parse_args()
 
 
 EXCHANGE_DESC = {
-    "fused": "Q' and (O', stats) written over NVLink peer memory by K1 / K2 themselves, flag-synchronised",
+    "ll": "Q' and every split's (O', stats) written over NVLink peer memory by K1 / K2 themselves, epoch-tagged (LL)",
     "p2p": "Q' and (O', stats) over NVLink peer memory (exchange.cu push / wait kernels)",
     "nccl": "NCCL all-to-all",
 }
@@ -246,6 +247,12 @@ def run_ours(args, ws, rank, local):
                 k2_ev.append((e0, e1))
             return ops.unscramble_merge(srcs, out=out, key_heads=H)
         step_k2 = step
+        if args.exchange == "ll" and args.ll_single:   # the same kernels LL-chained (W = 1): no faster
+            from paper_2605_25716_b200 import distributed as sdist
+            lld = sdist.LLDecode(B_PER, H, D, inq_keys, shard, n_splits=S, kv_heads=H)
+
+            def step(qin):   # noqa: F811
+                return lld.step(qin, out)
     else:
         from paper_2605_25716_b200 import distributed as sdist
         bufs = sdist.StepBuffers.allocate(ws, B_PER, H, 1, D, torch.bfloat16, devn)
@@ -268,12 +275,11 @@ def run_ours(args, ws, rank, local):
         def step(qin):
             return sdist.scrambled_decode_step(qin, comp, bufs, out, exchange=exch)
         step_k2 = step
-        if args.exchange == "fused":
-            bufs_f = sdist.StepBuffers.allocate(ws, B_PER, H, 1, D, torch.bfloat16, devn)
-            fused = sdist.FusedDecode(sdist.PeerExchange(bufs_f), bufs_f, inq_keys, shard, n_splits=S, kv_heads=H)
+        if args.exchange == "ll":
+            lld = sdist.LLDecode(B_PER, H, D, inq_keys, shard, n_splits=S, kv_heads=H)
 
             def step(qin):   # noqa: F811
-                return fused.step(qin, out)
+                return lld.step(qin, out)
 
     def barrier():
         if ws > 1:
@@ -312,8 +318,8 @@ def run_ours(args, ws, rank, local):
     barrier()
     launches = (capi.launch_count() - l0) // args.steps if not args.graph else launches_per_step
     ms = t0.elapsed_time(t1) / args.steps
-    # K2 duration: the same launch, event-bracketed on the same stream, back to back (fused
-    # exchange: the K2 of the unfused step, i.e. the same kernel without the fold tail)
+    # K2 duration: the same launch, event-bracketed on the same stream, back to back (LL
+    # exchange: the K2 of the reference-shaped step, the same kernel without the LL epilogue)
     if args.graph or step is not step_k2:
         record["on"] = True
         for _ in range(max(10, args.steps // 10)):

@@ -222,39 +222,37 @@ sda_status sda_exchange_push(void* stream, int32_t n_peers, const void* const* s
 /* wait until flags[i] >= *epoch for i < n (wrap-around safe) */
 sda_status sda_exchange_wait(void* stream, const uint32_t* flags, int32_t n, const uint32_t* epoch);
 
-/* Fused exchange for single-row decode (L_q = 1): the three kernels of a step carry the
- * exchange themselves, so a step is 3 launches instead of K1, push, wait, K2, fold, push, wait, K3.
- * Flags layout on every rank: [W SCR_Q flags, one per sender | W SCR_SHARD flags, one per sender];
- * *epoch starts at 1 and flags at 0; sda_fused_unscramble_merge bumps *epoch when it finishes.
+/* LL exchange for single-row decode (L_q = 1, head_dim >= 64): the three kernels of a step carry
+ * the exchange themselves over peer memory (buffers mapped with sda_ipc_*), so a step is 3
+ * launches with no copy kernel, fence or flag: every 4-byte data word travels next to the 4-byte
+ * step epoch ("LL" format, 16-byte stores of two (word, epoch) pairs) and readers spin until their
+ * words carry the current *epoch (trap after ~4 s instead of hanging). *epoch starts at 1 with
+ * all receive buffers zeroed; sda_ll_unscramble_merge bumps it when it finishes.
  *
- * sda_fused_scramble_q: like sda_scramble(FORWARD, KQ, n_batch = n_dest * b_per, x_batch_mod = b_per)
- *   but batch b goes to out_peer[b / b_per] (the destination's receive slot for this sender,
- *   [b_per][n_heads][1][d]); the last CTA of each destination raises *peer_flag[dest] = *epoch.
- *   dest_counters: n_dest zeroed u32 (self-resetting). */
-sda_status sda_fused_scramble_q(void* stream, const void* q, int32_t q_dtype, int32_t n_dest, int64_t b_per,
-                                int32_t n_heads, int32_t head_dim, const void* keys, int64_t keys_batch_stride,
-                                int32_t key_heads, void* const* out_peer, int32_t out_dtype,
-                                uint32_t* const* peer_flag, const uint32_t* epoch, uint32_t* dest_counters);
-/* sda_fused_partial_attention: sda_partial_attention over q [n_dest * b_per][q_heads][1][d] where
- *   the CTAs of batch b first wait for wait_flags[b / b_per] >= *epoch; work_o / work_stats hold
- *   the splits; the last split of a row folds them (scrambled-space merge) into the packed record
- *   rec_peer[b / b_per] + (b % b_per) * q_heads * (d + 2) floats ([q_heads][d] O' | [q_heads][2]
- *   stats), and the last row of a destination raises *rec_flag[dest] = *epoch.
- *   fold_counters: n_dest * b_per * q_heads zeroed u32, dest_counters: n_dest zeroed u32. */
-sda_status sda_fused_partial_attention(void* stream, const void* q, int32_t q_dtype, const void* k, const void* v,
-                                       int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int32_t n_dest,
-                                       int64_t b_per, int32_t q_heads, int32_t kv_heads, int32_t head_dim,
-                                       int32_t n_splits, float* work_o, float* work_stats, const uint32_t* wait_flags,
-                                       const uint32_t* epoch, uint32_t* fold_counters, float* const* rec_peer,
-                                       uint32_t* const* rec_flag, uint32_t* dest_counters);
-/* sda_fused_unscramble_merge: sda_unscramble_merge (no out_stats / err) that first waits for
- *   wait_flags[0 .. n_wait) >= *epoch and whose last CTA then does *epoch += 1.
- *   done_counter: one zeroed u32 (self-resetting). */
-sda_status sda_fused_unscramble_merge(void* stream, const sda_merge_source* sources, int32_t n_sources,
-                                      int64_t keys_batch_stride, int32_t key_heads, int64_t pq_batch_stride,
-                                      int64_t n_batch, int32_t q_heads, int64_t q_rows, int32_t head_dim, void* out,
-                                      int32_t out_dtype, const uint32_t* wait_flags, int32_t n_wait, uint32_t* epoch,
-                                      uint32_t* done_counter);
+ * Receive buffers on every rank (W = ranks, B_p = requests per inquirer, H = q heads, d):
+ *   Q' slots     [W senders][B_p][H][d]      LL: bf16 wire 4 B per element, f32 wire 8 B per element
+ *   record slots [W senders][S splits][B_p][H][d + 2]   LL f32: 8 B per float ([d O' | row_max, exp_sum])
+ *
+ * sda_ll_scramble_q: K1 (phi_KQ forward) of q [B_p][H][1][d] with the key set of request
+ *   dest * B_p + b (keys stacked destination-major) into ll_q[dest] = destination's Q' slot for
+ *   this sender. */
+sda_status sda_ll_scramble_q(void* stream, const void* q, int32_t q_dtype, int32_t n_dest, int64_t b_per,
+                             int32_t n_heads, int32_t head_dim, const void* keys, int64_t keys_batch_stride,
+                             int32_t key_heads, void* const* ll_q, int32_t wire_dtype, const uint32_t* epoch);
+/* sda_ll_partial_attention: K2 over this rank's Q' slots (ll_q = [W][B_p][H][d] LL) and its KV
+ *   shard (requests sender-major, kv_len / k / v as sda_partial_attention); split s of request
+ *   (sender, i) goes to ll_rec[sender] = the sender's record slot for this domain. */
+sda_status sda_ll_partial_attention(void* stream, const void* ll_q, int32_t wire_dtype, const void* k, const void* v,
+                                    int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int32_t n_dest,
+                                    int64_t b_per, int32_t q_heads, int32_t kv_heads, int32_t head_dim,
+                                    int32_t n_splits, void* const* ll_rec, const uint32_t* epoch);
+/* sda_ll_unscramble_merge: K3 over this rank's record slots (n_domains * n_splits sources, each
+ *   domain unscrambled with its phi_V^-1 from keys[(domain * B_p + b)]) into out [B_p][H][1][d];
+ *   then *epoch += 1. done_counter: one zeroed u32 (self-resetting). */
+sda_status sda_ll_unscramble_merge(void* stream, const void* ll_rec, int32_t n_domains, int32_t n_splits,
+                                   const void* keys, int64_t keys_batch_stride, int32_t key_heads, int64_t b_per,
+                                   int32_t q_heads, int32_t head_dim, void* out, int32_t out_dtype, uint32_t* epoch,
+                                   uint32_t* done_counter);
 
 /* Step tracing: *dst = the GPU's %globaltimer (ns) when this 1-thread kernel runs, in stream
  * order. Not counted by sda_launch_count (instrumentation, not part of a step). */

@@ -30,7 +30,7 @@ EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_
            "sda_partial_attention", "sda_partial_attention_causal", "sda_default_splits", "sda_default_splits_gqa", "sda_unscramble_merge", "sda_abi_version",
            "sda_status_string", "sda_launch_count", "sda_ipc_get_handle", "sda_ipc_open_handle",
            "sda_ipc_close_handle", "sda_exchange_epoch", "sda_exchange_push", "sda_exchange_wait",
-           "sda_fused_scramble_q", "sda_fused_partial_attention", "sda_fused_unscramble_merge", "sda_trace_timestamp")
+           "sda_ll_scramble_q", "sda_ll_partial_attention", "sda_ll_unscramble_merge", "sda_trace_timestamp")
 
 
 class SdaError(RuntimeError):
@@ -100,14 +100,12 @@ def _load() -> ct.CDLL:
                                       ct.POINTER(ct.c_void_p), ct.c_uint64, _vp, _vp]
     lib.sda_exchange_wait.argtypes = [_vp, _vp, ct.c_int32, _vp]
     _pp = ct.POINTER(ct.c_void_p)
-    lib.sda_fused_scramble_q.argtypes = [_vp, _vp, ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int32, _vp,
-                                         ct.c_int64, ct.c_int32, _pp, ct.c_int32, _pp, _vp, _vp]
-    lib.sda_fused_partial_attention.argtypes = [_vp, _vp, ct.c_int32, _vp, _vp, ct.c_int32, ct.c_int64, _vp,
-                                                ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int32,
-                                                ct.c_int32, _vp, _vp, _vp, _vp, _vp, _pp, _pp, _vp]
-    lib.sda_fused_unscramble_merge.argtypes = [_vp, ct.POINTER(MergeSource), ct.c_int32, ct.c_int64, ct.c_int32,
-                                               ct.c_int64, ct.c_int64, ct.c_int32, ct.c_int64, ct.c_int32, _vp,
-                                               ct.c_int32, _vp, ct.c_int32, _vp, _vp]
+    lib.sda_ll_scramble_q.argtypes = [_vp, _vp, ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int32, _vp,
+                                      ct.c_int64, ct.c_int32, _pp, ct.c_int32, _vp]
+    lib.sda_ll_partial_attention.argtypes = [_vp, _vp, ct.c_int32, _vp, _vp, ct.c_int32, ct.c_int64, _vp, ct.c_int32,
+                                             ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32, _pp, _vp]
+    lib.sda_ll_unscramble_merge.argtypes = [_vp, _vp, ct.c_int32, ct.c_int32, _vp, ct.c_int64, ct.c_int32, ct.c_int64,
+                                            ct.c_int32, ct.c_int32, _vp, ct.c_int32, _vp, _vp]
     lib.sda_trace_timestamp.argtypes = [_vp, _vp]
     lib.sda_abi_version.restype = ct.c_int32
     lib.sda_status_string.restype = ct.c_char_p

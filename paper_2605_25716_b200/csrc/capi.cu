@@ -18,14 +18,6 @@ void count_launch() { ++g_launches; }
 }  // namespace sda
 
 namespace {
-// fused-K3 options, set only for the duration of one sda_fused_unscramble_merge call
-thread_local const uint32_t* g_k3_wait_flags = nullptr;
-thread_local int g_k3_n_wait = 0;
-thread_local uint32_t* g_k3_epoch = nullptr;
-thread_local uint32_t* g_k3_done = nullptr;
-}  // namespace
-
-namespace {
 
 bool supported_dim(int d) { return d == 32 || d == 64 || d == 128 || d == 256; }
 bool pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
@@ -190,19 +182,20 @@ sda_status sda_partial_attention_causal(void* stream, const void* q, int32_t q_d
 }
 
 // ------------------------------------------------------------------------------------------
-// Fused exchange (decode): K1 pushes Q' into the destinations' receive slots, K2 waits for its
-// Q', folds its splits and pushes the packed records back, K3 waits for all records.
+// LL exchange (decode): K1 writes Q' into the destinations' receive slots, K2 reads it from its
+// own slot and writes every split's record into the inquirer's slot, K3 merges the records --
+// all epoch-tagged (ll_store / ll_load in common.cuh), no separate copy, fence or flag.
 // ------------------------------------------------------------------------------------------
-sda_status sda_fused_scramble_q(void* stream, const void* q, int32_t q_dtype, int32_t n_dest, int64_t b_per,
-                                int32_t n_heads, int32_t head_dim, const void* keys, int64_t keys_batch_stride,
-                                int32_t key_heads, void* const* out_peer, int32_t out_dtype, uint32_t* const* peer_flag,
-                                const uint32_t* epoch, uint32_t* dest_counters) {
+sda_status sda_ll_scramble_q(void* stream, const void* q, int32_t q_dtype, int32_t n_dest, int64_t b_per,
+                             int32_t n_heads, int32_t head_dim, const void* keys, int64_t keys_batch_stride,
+                             int32_t key_heads, void* const* ll_q, int32_t wire_dtype, const uint32_t* epoch) {
     if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
-    if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
-    if (!q || !keys || !out_peer || !peer_flag || !epoch || !dest_counters || n_dest <= 0 ||
-        n_dest > sda::kMaxPeers || b_per <= 0 || n_heads <= 0 || key_heads <= 0 || n_heads % key_heads != 0 ||
-        !valid_dtype(q_dtype) || !valid_dtype(out_dtype))
+    if (!supported_dim(head_dim) || head_dim < 64) return SDA_ERR_UNSUPPORTED;
+    if (!q || !keys || !ll_q || !epoch || n_dest <= 0 || n_dest > sda::kMaxPeers || b_per <= 0 || n_heads <= 0 ||
+        key_heads <= 0 || n_heads % key_heads != 0 || !valid_dtype(q_dtype) || !valid_dtype(wire_dtype))
         return SDA_ERR_INVALID_ARGUMENT;
+    for (int i = 0; i < n_dest; ++i)
+        if (!ll_q[i]) return SDA_ERR_INVALID_ARGUMENT;
     sda::K1Params p{};
     p.x = q;
     p.keys = keys;
@@ -213,45 +206,68 @@ sda_status sda_fused_scramble_q(void* stream, const void* q, int32_t q_dtype, in
     p.key_heads = key_heads;
     p.which = SDA_KEYS_KQ;
     p.x_batch_mod = b_per;
-    for (int i = 0; i < n_dest; ++i) {
-        p.out_peer[i] = out_peer[i];
-        p.peer_flag[i] = peer_flag[i];
-    }
+    for (int i = 0; i < n_dest; ++i) p.ll_out[i] = ll_q[i];
     p.epoch = epoch;
-    p.dest_counters = dest_counters;
     ++g_launches;
-    return from_cuda(sda::launch_k1(p, head_dim, q_dtype, out_dtype, (int64_t)n_dest * b_per,
+    return from_cuda(sda::launch_k1(p, head_dim, q_dtype, wire_dtype, (int64_t)n_dest * b_per,
                                     static_cast<cudaStream_t>(stream)));
 }
 
-sda_status sda_fused_partial_attention(void* stream, const void* q, int32_t q_dtype, const void* k, const void* v,
-                                       int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int32_t n_dest,
-                                       int64_t b_per, int32_t q_heads, int32_t kv_heads, int32_t head_dim,
-                                       int32_t n_splits, float* work_o, float* work_stats, const uint32_t* wait_flags,
-                                       const uint32_t* epoch, uint32_t* fold_counters, float* const* rec_peer,
-                                       uint32_t* const* rec_flag, uint32_t* dest_counters) {
+sda_status sda_ll_partial_attention(void* stream, const void* ll_q, int32_t wire_dtype, const void* k, const void* v,
+                                    int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int32_t n_dest,
+                                    int64_t b_per, int32_t q_heads, int32_t kv_heads, int32_t head_dim,
+                                    int32_t n_splits, void* const* ll_rec, const uint32_t* epoch) {
     if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
-    if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
-    if (!q || !k || !v || !work_o || !work_stats || !wait_flags || !epoch || !fold_counters || !rec_peer ||
-        !rec_flag || !dest_counters || n_dest <= 0 || n_dest > sda::kMaxPeers || b_per <= 0 || q_heads <= 0 ||
-        kv_heads <= 0 || q_heads % kv_heads != 0 || n_splits <= 0 || !valid_dtype(q_dtype) || !valid_dtype(kv_dtype))
+    if (!supported_dim(head_dim) || head_dim < 64) return SDA_ERR_UNSUPPORTED;
+    if (!ll_q || !k || !v || !ll_rec || !epoch || n_dest <= 0 || n_dest > sda::kMaxPeers || b_per <= 0 ||
+        q_heads <= 0 || kv_heads <= 0 || q_heads % kv_heads != 0 || n_splits <= 0 || kv_cap < 0 ||
+        !valid_dtype(wire_dtype) || !valid_dtype(kv_dtype))
         return SDA_ERR_INVALID_ARGUMENT;
+    for (int i = 0; i < n_dest; ++i)
+        if (!ll_rec[i]) return SDA_ERR_INVALID_ARGUMENT;
     const int64_t n_batch = (int64_t)n_dest * b_per;
     if (n_batch > 65535 || q_heads > 65535 || n_splits > 65535) return SDA_ERR_UNSUPPORTED;
-    sda::K2Params p{q, k, v, kv_len, work_o, work_stats, kv_cap, n_batch, 1, q_heads, kv_heads, n_splits,
+    sda::K2Params p{ll_q, k, v, kv_len, nullptr, nullptr, kv_cap, n_batch, 1, q_heads, kv_heads, n_splits,
                     (float)(1.0 / std::sqrt((double)head_dim)), 0, 0};
-    p.wait_flags = wait_flags;
-    p.wait_group = b_per;
     p.epoch = epoch;
-    p.fold_counters = fold_counters;
-    for (int i = 0; i < n_dest; ++i) {
-        p.rec_peer[i] = rec_peer[i];
-        p.rec_flag[i] = rec_flag[i];
-    }
-    p.rec_stride = (int64_t)q_heads * (head_dim + 2);
-    p.dest_counters = dest_counters;
+    p.b_per = b_per;
+    for (int i = 0; i < n_dest; ++i) p.ll_rec[i] = ll_rec[i];
     ++g_launches;
-    return from_cuda(sda::launch_k2_decode(p, head_dim, q_dtype, kv_dtype, static_cast<cudaStream_t>(stream)));
+    return from_cuda(sda::launch_k2_decode(p, head_dim, wire_dtype, kv_dtype, static_cast<cudaStream_t>(stream)));
+}
+
+sda_status sda_ll_unscramble_merge(void* stream, const void* ll_rec, int32_t n_domains, int32_t n_splits,
+                                   const void* keys, int64_t keys_batch_stride, int32_t key_heads, int64_t b_per,
+                                   int32_t q_heads, int32_t head_dim, void* out, int32_t out_dtype, uint32_t* epoch,
+                                   uint32_t* done_counter) {
+    if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
+    if (!supported_dim(head_dim) || head_dim < 64) return SDA_ERR_UNSUPPORTED;
+    if (!ll_rec || !keys || !out || !epoch || !done_counter || n_domains <= 0 || n_splits <= 0 || b_per <= 0 ||
+        q_heads <= 0 || key_heads <= 0 || q_heads % key_heads != 0 || !valid_dtype(out_dtype))
+        return SDA_ERR_INVALID_ARGUMENT;
+    if ((int64_t)n_domains * n_splits > SDA_MAX_SOURCES) return SDA_ERR_UNSUPPORTED;
+    sda::K3Params p{};
+    const int64_t row = (int64_t)q_heads * (head_dim + 2);   // logical floats per request
+    const uint8_t* base = static_cast<const uint8_t*>(ll_rec);
+    for (int w = 0; w < n_domains; ++w)
+        for (int s = 0; s < n_splits; ++s) {
+            const uint8_t* blk = base + 8 * ((int64_t)(w * n_splits + s) * b_per * row);
+            p.src[w * n_splits + s] = {reinterpret_cast<const float*>(blk), reinterpret_cast<const float*>(blk),
+                                       static_cast<const uint8_t*>(keys) + (int64_t)w * b_per * keys_batch_stride,
+                                       nullptr, row};
+        }
+    p.n_src = n_domains * n_splits;
+    p.keys_bstride = keys_batch_stride;
+    p.key_heads = key_heads;
+    p.n_batch = b_per;
+    p.q_heads = q_heads;
+    p.q_rows = 1;
+    p.out = out;
+    p.ll = 1;
+    p.epoch = epoch;
+    p.done_counter = done_counter;
+    ++g_launches;
+    return from_cuda(sda::launch_k3(p, head_dim, out_dtype, static_cast<cudaStream_t>(stream)));
 }
 
 sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, int32_t n_sources,
@@ -285,32 +301,8 @@ sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, i
     p.out_stats = out_stats;
     p.err = err_flag;
     p.out_bstride = out_batch_stride;
-    p.wait_flags = g_k3_wait_flags;
-    p.n_wait = g_k3_n_wait;
-    p.epoch = g_k3_epoch;
-    p.done_counter = g_k3_done;
     ++g_launches;
     return from_cuda(sda::launch_k3(p, head_dim, out_dtype, static_cast<cudaStream_t>(stream)));
-}
-
-sda_status sda_fused_unscramble_merge(void* stream, const sda_merge_source* sources, int32_t n_sources,
-                                      int64_t keys_batch_stride, int32_t key_heads, int64_t pq_batch_stride,
-                                      int64_t n_batch, int32_t q_heads, int64_t q_rows, int32_t head_dim, void* out,
-                                      int32_t out_dtype, const uint32_t* wait_flags, int32_t n_wait, uint32_t* epoch,
-                                      uint32_t* done_counter) {
-    if (!wait_flags || !epoch || !done_counter || n_wait <= 0 || n_wait > 128) return SDA_ERR_INVALID_ARGUMENT;
-    // thread-local hand-off of the fused options to the shared validation / launch path
-    g_k3_wait_flags = wait_flags;
-    g_k3_n_wait = n_wait;
-    g_k3_epoch = epoch;
-    g_k3_done = done_counter;
-    const sda_status st = sda_unscramble_merge(stream, sources, n_sources, keys_batch_stride, key_heads, pq_batch_stride,
-                                               n_batch, q_heads, q_rows, head_dim, out, out_dtype, nullptr, nullptr, 0);
-    g_k3_wait_flags = nullptr;
-    g_k3_n_wait = 0;
-    g_k3_epoch = nullptr;
-    g_k3_done = nullptr;
-    return st;
 }
 
 }  // extern "C"

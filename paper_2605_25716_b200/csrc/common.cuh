@@ -182,24 +182,52 @@ __device__ __forceinline__ void fwht_group(float* v, int lane) {
     }
 }
 
-// Cross-GPU signalling for the fused exchange (see exchange.cu): spin (acquire, system scope)
-// until *flag has reached `e` (wrap-around safe), trapping after ~4 s instead of hanging; raise
-// a flag with a release store.
-__device__ __forceinline__ void flag_wait(const uint32_t* flag, uint32_t e) {
-    uint64_t t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    for (;;) {
-        uint32_t v;
-        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-        if ((int32_t)(v - e) >= 0) return;
-        uint64_t t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > 4000000000ull) __trap();
-        __nanosleep(32);
-    }
+// Programmatic dependent launch (the LL decode chain K1 -> K2 -> K3): a kernel launched with
+// pdl_launch may start once every CTA of its predecessor has called pdl_trigger (or exited), so
+// it overlaps the predecessor's tail instead of waiting for the grid to drain; pdl_wait blocks
+// until the predecessor grid has completed and its writes are visible (no-op without PDL).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename Kern, typename... Args>
+inline cudaError_t pdl_launch(Kern kernel, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
-__device__ __forceinline__ void flag_raise(uint32_t* flag, uint32_t e) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(e) : "memory");
+
+// LL ("low-latency") peer-memory format for the decode exchange: every 4-byte data word is
+// stored next to the 4-byte step epoch, two (data, epoch) pairs per 16-byte store. An aligned
+// 8-byte half is written as one unit, so a reader that polls its words until both epochs match
+// sees the data without any fence or separate flag: one NVLink write latency per exchange
+// instead of store + system fence + flag store + flag poll.
+__device__ __forceinline__ void ll_store(void* p, uint32_t a, uint32_t b, uint32_t e) {
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(e), "r"(b), "r"(e)
+                 : "memory");
+}
+// spin until both epochs of the 16-byte word at p equal e; traps after ~4 s instead of hanging
+__device__ __forceinline__ uint2 ll_load(const void* p, uint32_t e) {
+    uint32_t a, fa, b, fb;
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(fa), "=r"(b), "=r"(fb) : "l"(p) : "memory");
+    if (fa != e || fb != e) {
+        uint64_t t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do {
+            asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(a), "=r"(fa), "=r"(b), "=r"(fb) : "l"(p) : "memory");
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 4000000000ull) __trap();
+        } while (fa != e || fb != e);
+    }
+    return make_uint2(a, b);
 }
 
 __host__ __device__ __forceinline__ const uint8_t* scrambler_ptr(const void* keys, int64_t batch_stride,

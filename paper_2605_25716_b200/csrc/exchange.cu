@@ -29,6 +29,7 @@ struct PushParams {
     int64_t n16;                     // payload size in 16-byte units (same for every peer)
     const uint32_t* epoch;           // local step epoch
     unsigned int* done;              // local per-peer block counters (zeroed, self-resetting)
+    int fence_one;                   // 1: thread 0 fences after the CTA barrier instead of every thread
 };
 
 __global__ void step_epoch_kernel(uint32_t* epoch) {
@@ -42,9 +43,11 @@ __global__ void __launch_bounds__(256) push_kernel(const PushParams p) {
     uint4* d = p.dst[peer];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n16; i += (int64_t)gridDim.x * blockDim.x)
         d[i] = s[i];
-    __threadfence_system();
+    if (!p.fence_one) __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
+        // one fence after the barrier covers the whole CTA's stores (fence cumulativity)
+        if (p.fence_one) __threadfence_system();
         const unsigned int prev = atomicAdd(&p.done[peer], 1u);
         if (prev == gridDim.x - 1) {
             p.done[peer] = 0;
@@ -158,6 +161,11 @@ sda_status sda_exchange_push(void* stream, int32_t n_peers, const void* const* s
         const char* e = getenv("SDA_PUSH_BLOCKS");   // tuning knob (tools/step_timeline.py)
         return e && atoi(e) > 0 ? atoi(e) : 16;
     }();
+    static const int fence_one = [] {
+        const char* e = getenv("SDA_PUSH_FENCE_ONE");   // tuning knob (tools/step_timeline.py)
+        return e && atoi(e) > 0 ? 1 : 0;
+    }();
+    p.fence_one = fence_one;
     int blocks = (int)std::min<int64_t>(max_blocks, (p.n16 + 255) / 256);
     if (blocks < 1) blocks = 1;
     sda::count_launch();

@@ -11,6 +11,8 @@
 // memory, the Walsh-Hadamard butterflies run 4 stages in registers plus log2(LPR) shuffle
 // stages, and P2 is applied as a gather from shared memory. Row permutation is a gather on
 // the input side (output rows are written in order), so stores stay contiguous.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace sda {
@@ -26,6 +28,25 @@ struct K1Shape {
     static constexpr int ROWS_PER_CTA = 64 > WARPS * R ? 64 : WARPS * R;
     static constexpr int ITERS = ROWS_PER_CTA / (WARPS * R);
 };
+
+// E consecutive logical elements starting at `elem` (a multiple of 4) of an LL buffer:
+// bf16 -> one u32 of two values per 8 bytes, f32 -> one value per 8 bytes (ll_store).
+template <int E, typename T>
+__device__ __forceinline__ void ll_store_row(void* base, int64_t elem, const float* v, uint32_t ep) {
+    uint8_t* b = static_cast<uint8_t*>(base);
+    if constexpr (std::is_same<T, float>::value) {
+#pragma unroll
+        for (int m = 0; m < E / 2; ++m)
+            ll_store(b + 8 * (elem + 2 * m), __float_as_uint(v[2 * m]), __float_as_uint(v[2 * m + 1]), ep);
+    } else {
+#pragma unroll
+        for (int m = 0; m < E / 4; ++m) {
+            __nv_bfloat162 x = __floats2bfloat162_rn(v[4 * m], v[4 * m + 1]);
+            __nv_bfloat162 y = __floats2bfloat162_rn(v[4 * m + 2], v[4 * m + 3]);
+            ll_store(b + 8 * ((elem >> 1) + 2 * m), *reinterpret_cast<uint32_t*>(&x), *reinterpret_cast<uint32_t*>(&y), ep);
+        }
+    }
+}
 
 __device__ __forceinline__ int k1_sidx(int j) { return (j >> 4) * 20 + (j & 15); }
 
@@ -76,10 +97,12 @@ __global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p, cons
 
     const int64_t xb = p.x_batch_mod > 0 ? b % p.x_batch_mod : b;
     const Tin* x = static_cast<const Tin*>(p.x) + (xb * p.n_heads + h) * p.rows * D;
-    const bool fused = p.out_peer[0] != nullptr;   // push straight into the destination's receive slot
-    Tout* out = fused ? static_cast<Tout*>(p.out_peer[b / p.x_batch_mod]) +
-                            ((xb * p.n_heads + h) * p.out_rows_cap + p.out_row_offset) * D
-                      : static_cast<Tout*>(p.out) + ((b * p.n_heads + h) * p.out_rows_cap + p.out_row_offset) * D;
+    // LL exchange: write straight into the destination's receive slot, epoch-tagged
+    const bool ll = FLAT && p.epoch != nullptr;
+    const uint32_t ep = ll ? *p.epoch : 0u;
+    if (ll) pdl_trigger();   // K2 may launch right away: it spins on the LL words, not on K1
+    const int64_t out_elem = ((ll ? xb : b) * p.n_heads + h) * p.out_rows_cap * D + p.out_row_offset * D;
+    Tout* out = ll ? nullptr : static_cast<Tout*>(p.out) + out_elem;
     const uint32_t* perm = p.perm ? p.perm + b * p.perm_bstride : nullptr;
     float* u = &sbuf[warp][g * S::RS];
 
@@ -106,37 +129,13 @@ __global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p, cons
         __syncwarp();
 #pragma unroll
         for (int e = 0; e < E; ++e) v[e] = u[p2i[e]] * kout[e];  // y[k] = H(u)[P2inv[k]] * s2^{+-1}[k]/sqrt(d)
-        if (valid) store_vec<E>(out + r * D + lg * E, v);
-        __syncwarp();
-    }
-    if (fused) {   // the CTA completing a destination's rows raises that destination's SCR_Q flag
-        __threadfence_system();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            // rows of the flattened [n_batch][n_heads][rows] space this CTA wrote, per destination
-            const int64_t per_dest = p.x_batch_mod * p.n_heads * p.rows;
-            int64_t f0, f1;
-            if constexpr (FLAT) {
-                f0 = (int64_t)blockIdx.x * (S::WARPS * R);
-                f1 = f0 + S::WARPS * R;
-                if (f1 > n_batch * p.n_heads) f1 = n_batch * p.n_heads;
-            } else {
-                const int64_t base = (b * p.n_heads + h) * p.rows;
-                f0 = base + (int64_t)blockIdx.x * S::ROWS_PER_CTA;
-                f1 = f0 + S::ROWS_PER_CTA;
-                if (f1 > base + p.rows) f1 = base + p.rows;
-            }
-            for (int64_t d = f0 / per_dest; d * per_dest < f1; ++d) {
-                const int64_t lo = d * per_dest > f0 ? d * per_dest : f0;
-                const int64_t hi = (d + 1) * per_dest < f1 ? (d + 1) * per_dest : f1;
-                const unsigned n = (unsigned)(hi - lo);
-                if (atomicAdd(&p.dest_counters[d], n) + n == (unsigned)per_dest) {
-                    p.dest_counters[d] = 0;
-                    __threadfence_system();
-                    flag_raise(p.peer_flag[d], *p.epoch);
-                }
-            }
+        if (valid) {
+            if (ll)
+                ll_store_row<E, Tout>(p.ll_out[b / p.x_batch_mod], out_elem + r * D + lg * E, v, ep);
+            else
+                store_vec<E>(out + r * D + lg * E, v);
         }
+        __syncwarp();
     }
 }
 

@@ -12,6 +12,7 @@
 // shared-memory merge of the CTA's lane groups. Emits the split's locally normalised O'
 // and (row_max, exp_sum) exactly as ShardStats defines them (attention.hpp:34-41).
 #include <cmath>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -40,10 +41,9 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
     const int split = blockIdx.x, h = blockIdx.y;
     const int64_t b = (int64_t)blockIdx.z / p.q_rows, qr = (int64_t)blockIdx.z % p.q_rows;
     const int kvh = h / (p.q_heads / p.kv_heads);
-    if (p.wait_flags) {   // fused exchange: this request's Q' must have arrived from its inquirer
-        if (threadIdx.x == 0) flag_wait(p.wait_flags + b / p.wait_group, *p.epoch);
-        __syncthreads();
-    }
+    const bool ll = p.epoch != nullptr;   // LL exchange (decode): Q' in, the split's record out
+    const uint32_t ep = ll ? *p.epoch : 0u;
+    if (ll) pdl_trigger();   // K3 may launch as soon as every K2 CTA has read the epoch
 
     int64_t len = p.kv_len ? (int64_t)p.kv_len[b] : p.kv_cap;
     if (p.causal) {   // keys j <= qr + offset only (AttentionMask::causal, attention.cpp:16-27)
@@ -57,7 +57,29 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
     const int64_t k1 = min(len, k0 + chunk);
 
     float qv[VEC];
-    load_vec<VEC>(static_cast<const TQ*>(p.q) + ((b * p.q_heads + h) * p.q_rows + qr) * D + lg * VEC, qv);
+    const int64_t q_elem = ((b * p.q_heads + h) * p.q_rows + qr) * D + lg * VEC;
+    if (ll) {   // spin until this request's Q' has arrived from its inquirer
+        const uint8_t* qb = static_cast<const uint8_t*>(p.q);
+        if constexpr (std::is_same<TQ, float>::value) {
+#pragma unroll
+            for (int m = 0; m < VEC / 2; ++m) {
+                const uint2 w = ll_load(qb + 8 * (q_elem + 2 * m), ep);
+                qv[2 * m] = __uint_as_float(w.x);
+                qv[2 * m + 1] = __uint_as_float(w.y);
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < VEC / 4; ++m) {
+                const uint2 w = ll_load(qb + 8 * ((q_elem >> 1) + 2 * m), ep);
+                qv[4 * m] = __uint_as_float(w.x << 16);
+                qv[4 * m + 1] = __uint_as_float(w.x & 0xFFFF0000u);
+                qv[4 * m + 2] = __uint_as_float(w.y << 16);
+                qv[4 * m + 3] = __uint_as_float(w.y & 0xFFFF0000u);
+            }
+        }
+    } else {
+        load_vec<VEC>(static_cast<const TQ*>(p.q) + q_elem, qv);
+    }
 #pragma unroll
     for (int i = 0; i < VEC; ++i) qv[i] *= p.scale * kLog2e;   // logits in log2 units
 
@@ -127,8 +149,26 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
         wgt[i] = (M == -INFINITY) ? 0.f : ex2(sm_m[i] - M);
         S_ = fmaf(sm_s[i], wgt[i], S_);
     }
-    const int64_t orow = ((int64_t)split * p.n_batch * p.q_heads + b * p.q_heads + h) * p.q_rows + qr;
     const float inv = S_ > 0.f ? 1.f / S_ : 0.f;
+    // back to natural-log units: row_max = max_j q.k_j / sqrt(d)
+    const float row_max = S_ > 0.f ? M / kLog2e : -INFINITY;
+    if (ll) {   // the split's record row, straight into the inquirer's receive slot
+        const int64_t dest = b / p.b_per, i = b % p.b_per;
+        uint8_t* rb = static_cast<uint8_t*>(p.ll_rec[dest]) + 8 * (((split * p.b_per + i) * p.q_heads + h) * (D + 2));
+        for (int pr = threadIdx.x; pr < D / 2; pr += blockDim.x) {
+            float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+            for (int g2 = 0; g2 < NG; ++g2) {
+                a0 = fmaf(sm_o[g2][2 * pr], wgt[g2], a0);
+                a1 = fmaf(sm_o[g2][2 * pr + 1], wgt[g2], a1);
+            }
+            ll_store(rb + 16 * pr, __float_as_uint(a0 * inv), __float_as_uint(a1 * inv), ep);
+        }
+        if (threadIdx.x == 0) ll_store(rb + 8 * D, __float_as_uint(row_max), __float_as_uint(S_), ep);
+        pdl_wait();   // K2 completes only after K1 has (stream order for the next step)
+        return;
+    }
+    const int64_t orow = ((int64_t)split * p.n_batch * p.q_heads + b * p.q_heads + h) * p.q_rows + qr;
     for (int dim = threadIdx.x; dim < D; dim += blockDim.x) {
         float acc = 0.f;
 #pragma unroll
@@ -136,67 +176,15 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
         p.out_o[orow * D + dim] = acc * inv;
     }
     if (threadIdx.x == 0) {
-        // back to natural-log units: row_max = max_j q.k_j / sqrt(d)
-        p.out_stats[orow * 2 + 0] = S_ > 0.f ? M / kLog2e : -INFINITY;
+        p.out_stats[orow * 2 + 0] = row_max;
         p.out_stats[orow * 2 + 1] = S_;
-    }
-    if (!p.fold_counters) return;
-
-    // ---- fused exchange: the last split CTA of this row folds the splits (merge_shards in
-    // scrambled space, attention.cpp:89-123) and pushes the packed (O', stats) record to the
-    // inquirer; the last row of a destination raises its SCR_SHARD flag
-    __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    const int64_t row = (b * p.q_heads + h) * p.q_rows + qr;
-    if (threadIdx.x == 0) last = atomicAdd(&p.fold_counters[row], 1u) == (unsigned)p.n_splits - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    const int64_t split_stride = p.n_batch * p.q_heads * p.q_rows;
-    float ms = -INFINITY;
-    for (int sp = 0; sp < p.n_splits; ++sp) {
-        const float2 st = __ldcg(reinterpret_cast<const float2*>(p.out_stats) + sp * split_stride + row);
-        if (st.y > 0.f) ms = fmaxf(ms, st.x);
-    }
-    float den = 0.f;
-    const int64_t dest = b / p.wait_group, i = b % p.wait_group;
-    float* rec = p.rec_peer[dest] + i * p.rec_stride;
-    const int64_t hr = (int64_t)h * p.q_rows + qr;
-    for (int dim = threadIdx.x; dim < D; dim += blockDim.x) {
-        float acc = 0.f, dd = 0.f;
-        for (int sp = 0; sp < p.n_splits; ++sp) {
-            const float2 st = __ldcg(reinterpret_cast<const float2*>(p.out_stats) + sp * split_stride + row);
-            if (st.y > 0.f) {
-                const float w = st.y * expf(st.x - ms);
-                dd += w;
-                acc = fmaf(w, __ldcg(p.out_o + (sp * split_stride + row) * D + dim), acc);
-            }
-        }
-        rec[hr * D + dim] = dd > 0.f ? acc / dd : 0.f;
-        den = dd;
-    }
-    if (threadIdx.x == 0) {
-        float* st = rec + (int64_t)p.q_heads * p.q_rows * D + hr * 2;
-        st[0] = den > 0.f ? ms : -INFINITY;
-        st[1] = den;
-    }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        p.fold_counters[row] = 0;
-        const unsigned rows_per_dest = (unsigned)(p.wait_group * p.q_heads * p.q_rows);
-        if (atomicAdd(&p.dest_counters[dest], 1u) == rows_per_dest - 1) {
-            p.dest_counters[dest] = 0;
-            __threadfence_system();
-            flag_raise(p.rec_flag[dest], *p.epoch);
-        }
     }
 }
 
 template <int D, typename TQ, typename TKV>
 static cudaError_t launch_k2_t(const K2Params& p, cudaStream_t st) {
     const dim3 grid((unsigned)p.n_splits, (unsigned)p.q_heads, (unsigned)(p.n_batch * p.q_rows));
+    if (p.epoch) return pdl_launch(k2_decode_kernel<D, TQ, TKV>, grid, dim3(128), st, p);
     k2_decode_kernel<D, TQ, TKV><<<grid, 128, 0, st>>>(p);
     return cudaGetLastError();
 }

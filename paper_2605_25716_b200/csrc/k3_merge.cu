@@ -55,10 +55,8 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* sh = sh_all[warp];
     const int64_t total = p.n_batch * p.q_heads * p.q_rows;
-    if (p.wait_flags) {   // fused exchange: every domain's SCR_SHARD records must have arrived
-        if (threadIdx.x < p.n_wait) flag_wait(p.wait_flags + threadIdx.x, *p.epoch);
-        __syncthreads();
-    }
+    const bool ll = p.ll != 0;   // LL exchange: records arrive epoch-tagged in peer memory
+    const uint32_t ep = ll ? *p.epoch : 0u;
     const int64_t row_raw = (int64_t)blockIdx.x * 4 + warp;
     const bool active = row_raw < total;
     const int64_t row = active ? row_raw : total - 1;   // inactive warps compute a dummy row, store nothing
@@ -69,6 +67,11 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
     const int kh = h / (p.q_heads / p.key_heads);
 
     auto offsets = [&](const K3Source& src, int64_t& st_off, int64_t& o_off) {
+        if (ll) {   // logical floats of the record row (b, h): [d O' | row_max, exp_sum]
+            o_off = b * src.bstride + (int64_t)h * (D + 2);
+            st_off = o_off + D;
+            return;
+        }
         const int64_t ri = src.pq_inv ? (int64_t)src.pq_inv[b * p.pq_bstride + r] : r;
         st_off = src.bstride ? b * src.bstride + ((int64_t)h * p.q_rows + ri) * 2 : (bh * p.q_rows + ri) * 2;
         o_off = src.bstride ? b * src.bstride + ((int64_t)h * p.q_rows + ri) * D : (bh * p.q_rows + ri) * D;
@@ -81,7 +84,13 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
     for (int s = lane; s < p.n_src; s += 32) {
         int64_t st_off, o_off;
         offsets(p.src[s], st_off, o_off);
-        const float2 st = *reinterpret_cast<const float2*>(p.src[s].stats + st_off);
+        float2 st;
+        if (ll) {
+            const uint2 w = ll_load(reinterpret_cast<const uint8_t*>(p.src[s].o) + 8 * st_off, ep);
+            st = make_float2(__uint_as_float(w.x), __uint_as_float(w.y));
+        } else {
+            st = *reinterpret_cast<const float2*>(p.src[s].stats + st_off);
+        }
         if (s == lane) st_lane = st;
         if (st.y > 0.f) mstar = fmaxf(mstar, st.x);
     }
@@ -94,8 +103,24 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
         offsets(src, st_off, o_off);
         const float sx = __shfl_sync(0xffffffffu, st_lane.x, s & 31);
         const float sy = __shfl_sync(0xffffffffu, st_lane.y, s & 31);
-        L.st = p.n_src <= 32 ? make_float2(sx, sy) : *reinterpret_cast<const float2*>(src.stats + st_off);
-        load_vec_any<E>(src.o + o_off + lane * E, L.ov);
+        if (ll) {
+            const uint8_t* rb = reinterpret_cast<const uint8_t*>(src.o);
+            if (p.n_src <= 32) {
+                L.st = make_float2(sx, sy);
+            } else {
+                const uint2 w = ll_load(rb + 8 * st_off, ep);
+                L.st = make_float2(__uint_as_float(w.x), __uint_as_float(w.y));
+            }
+#pragma unroll
+            for (int m = 0; m < E / 2; ++m) {
+                const uint2 w = ll_load(rb + 8 * (o_off + lane * E + 2 * m), ep);
+                L.ov[2 * m] = __uint_as_float(w.x);
+                L.ov[2 * m + 1] = __uint_as_float(w.y);
+            }
+        } else {
+            L.st = p.n_src <= 32 ? make_float2(sx, sy) : *reinterpret_cast<const float2*>(src.stats + st_off);
+            load_vec_any<E>(src.o + o_off + lane * E, L.ov);
+        }
         if (src.keys) {
             const uint8_t* sc = scrambler_ptr(src.keys, p.keys_bstride, b, kh, D, 1);
             const float* ftab = reinterpret_cast<const float*>(sc);
@@ -155,7 +180,8 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
         p.out_stats[so + 0] = single ? (masked ? -INFINITY : mstar) : mstar;
         p.out_stats[so + 1] = masked ? 0.f : denom;
     }
-    if (p.epoch && p.done_counter) {   // fused exchange: the last CTA opens the next step's epoch
+    if (ll && p.done_counter) {   // LL exchange: the last CTA opens the next step's epoch
+        pdl_wait();   // ... once K2 (still serving other inquirers) has completed too
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
@@ -170,6 +196,7 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
 template <int D, typename TOut>
 static cudaError_t launch_k3_t(const K3Params& p, cudaStream_t st) {
     const int64_t total = p.n_batch * p.q_heads * p.q_rows;
+    if (p.ll) return pdl_launch(k3_merge_kernel<D, TOut>, dim3((unsigned)((total + 3) / 4)), dim3(128), st, p);
     k3_merge_kernel<D, TOut><<<(unsigned)((total + 3) / 4), 128, 0, st>>>(p);
     return cudaGetLastError();
 }

@@ -38,13 +38,11 @@ struct K1Params {
     int which;    // 0 phi_kq, 1 phi_v
     int inv_t;    // 1: phi^{-T}
     int64_t x_batch_mod;   // > 0: request b reads x[b % x_batch_mod] (one Q, many key sets)
-    // fused peer push (exchange): request b's rows go to out_peer[b / x_batch_mod] (a peer's
-    // receive slot, row layout as `out` with batch x_batch_mod); the last CTA of a destination
-    // raises *peer_flag[dest] = *epoch (system-scope release)
-    void* out_peer[kMaxPeers];
-    uint32_t* peer_flag[kMaxPeers];
+    // LL exchange (decode, rows == 1; epoch != nullptr): request b's Q' row goes to
+    // ll_out[b / x_batch_mod] (a peer's receive slot, [x_batch_mod][n_heads][d] in LL format:
+    // every 4-byte data word is followed by the 4-byte step epoch, see ll_store)
+    void* ll_out[kMaxPeers];
     const uint32_t* epoch;
-    uint32_t* dest_counters;   // [n_dest] zeroed, self-resetting
 };
 
 struct K2Params {
@@ -63,17 +61,13 @@ struct K2Params {
     float scale;   // 1/sqrt(d) (attention.cpp:45)
     int causal;            // 1: key j visible to query row i iff j <= i + causal_offset (attention.hpp:25-27)
     int64_t causal_offset;
-    // fused exchange (decode): wait for this request's SCR_Q (flag of sender b / wait_group),
-    // fold the splits in the last CTA of a row, push the packed (O', stats) record to the
-    // inquirer's receive slot and raise its flag once all of its rows are in
-    const uint32_t* wait_flags;
-    int64_t wait_group;
+    // LL exchange (decode, q_rows == 1; epoch != nullptr): q is in LL format (spin until its
+    // words carry *epoch); split `split` of request b = (dest, i) = (b / b_per, b % b_per) is
+    // written as an LL record row [d O' | row_max, exp_sum] at logical float
+    // ((split * b_per + i) * q_heads + h) * (d + 2) of ll_rec[dest] (8 bytes per float)
     const uint32_t* epoch;
-    uint32_t* fold_counters;   // [n_batch * q_heads * q_rows] zeroed, self-resetting
-    float* rec_peer[kMaxPeers];
-    uint32_t* rec_flag[kMaxPeers];
-    int64_t rec_stride;        // floats per request record (q_heads * q_rows * (d + 2))
-    uint32_t* dest_counters;   // [n_dest] zeroed, self-resetting
+    int64_t b_per;
+    void* ll_rec[kMaxPeers];
 };
 
 struct K3Source {
@@ -97,9 +91,10 @@ struct K3Params {
     float* out_stats;
     int32_t* err;
     int64_t out_bstride;   // elements between requests (out and out_stats); 0 = dense
-    // fused exchange: wait until wait_flags[0..n_wait) >= *epoch; the last CTA bumps *epoch
-    const uint32_t* wait_flags;
-    int n_wait;
+    // LL exchange: sources are LL record rows (src.o = byte base, row (b, h) at logical float
+    // b * bstride + h * (d + 2), stats at + d; q_rows == 1), read by spinning until they carry
+    // *epoch; the last CTA then bumps *epoch (done_counter: one zeroed u32, self-resetting)
+    int ll;
     uint32_t* epoch;
     uint32_t* done_counter;
 };

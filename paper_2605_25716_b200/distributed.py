@@ -63,6 +63,38 @@ class RankCompute:
     scramble_q_all: Optional[Callable[[torch.Tensor, torch.Tensor], None]] = None   # (q, q_send [W, ...]) one launch
 
 
+def map_peer_buffers(bufs: dict, group: Optional[dist.ProcessGroup] = None):
+    """CUDA-IPC map every rank's buffers {name: tensor} into this process (handles traded once
+    with all_gather_object). Returns ({name: [device address on rank r]}, [opened mappings])."""
+    import ctypes as ct
+
+    from . import capi
+    if not dist.is_initialized():   # one process, one domain: nothing to map
+        return {name: [t.data_ptr()] for name, t in bufs.items()}, []
+    W, rank = dist.get_world_size(group), dist.get_rank(group)
+    mine = {}
+    for name, t in bufs.items():
+        h = (ct.c_uint8 * 64)()
+        off = ct.c_uint64(0)
+        capi.check(capi.LIB.sda_ipc_get_handle(t.data_ptr(), h, ct.byref(off)), "ipc_get_handle")
+        mine[name] = (bytes(h), int(off.value))
+    everyone = [None] * W
+    dist.all_gather_object(everyone, mine, group=group)
+    ptrs, opened = {name: [0] * W for name in bufs}, []
+    for r in range(W):
+        for name, t in bufs.items():
+            if r == rank:
+                ptrs[name][r] = t.data_ptr()
+                continue
+            hb, off = everyone[r][name]
+            ptr = ct.c_void_p()
+            capi.check(capi.LIB.sda_ipc_open_handle((ct.c_uint8 * 64).from_buffer_copy(hb), off, ct.byref(ptr)),
+                       "ipc_open_handle")
+            opened.append((ptr.value, off))
+            ptrs[name][r] = ptr.value
+    return ptrs, opened
+
+
 class PeerExchange:
     """SCR_Q / SCR_SHARD over NVLink peer memory (exchange.cu) instead of NCCL all-to-alls.
 
@@ -83,27 +115,9 @@ class PeerExchange:
         self.flags = torch.zeros(2 * W, dtype=torch.int32, device=dev)      # [SCR_Q from r | SCR_SHARD from r]
         self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)
         self.counters = torch.zeros(2 * W, dtype=torch.int32, device=dev)
-        mine = {}
-        for name, t in (("q", bufs.q_recv), ("ret", bufs.ret_recv), ("flags", self.flags)):
-            h = (ct.c_uint8 * 64)()
-            off = ct.c_uint64(0)
-            capi.check(capi.LIB.sda_ipc_get_handle(t.data_ptr(), h, ct.byref(off)), "ipc_get_handle")
-            mine[name] = (bytes(h), int(off.value))
-        everyone = [None] * W
-        dist.all_gather_object(everyone, mine, group=group)
-        self.opened = []
-        base = {}
-        for r in range(W):
-            for name, t in (("q", bufs.q_recv), ("ret", bufs.ret_recv), ("flags", self.flags)):
-                if r == self.rank:
-                    base[(r, name)] = t.data_ptr()
-                    continue
-                hb, off = everyone[r][name]
-                ptr = ct.c_void_p()
-                capi.check(capi.LIB.sda_ipc_open_handle((ct.c_uint8 * 64).from_buffer_copy(hb), off, ct.byref(ptr)),
-                           "ipc_open_handle")
-                self.opened.append((ptr.value, off))
-                base[(r, name)] = ptr.value
+        torch.cuda.synchronize()
+        ptrs, self.opened = map_peer_buffers({"q": bufs.q_recv, "ret": bufs.ret_recv, "flags": self.flags}, group)
+        base = {(r, name): ptrs[name][r] for name in ptrs for r in range(W)}
         self.base = base
         q_slot = bufs.q_send[0].numel() * bufs.q_send.element_size()
         r_slot = bufs.ret_send[0].numel() * bufs.ret_send.element_size()
@@ -141,68 +155,72 @@ class PeerExchange:
         self._wait(self.world)
 
 
-class FusedDecode:
-    """The decode step (L_q = 1) with the exchange folded into the kernels themselves: K1 writes
-    each destination's Q' straight into its receive slot over NVLink and raises its SCR_Q flag, K2
-    waits for its Q', folds its splits and pushes the packed (O', stats) record back to the
-    inquirer, K3 waits for every domain's record and opens the next epoch -- 3 launches per step
-    instead of 9, same data placement as PeerExchange / all_to_all_single (which stay the
-    reference-shaped form). GPU only."""
+class LLDecode:
+    """The decode step (L_q = 1) with the exchange carried by the kernels themselves (LL format,
+    see include/sdattn_b200.h): K1 writes each destination's Q' straight into its receive slot
+    over NVLink, K2 spins on its own slot and writes every split's (O', stats) record straight
+    into the inquirer's slot, K3 spins on its slots, merges + unscrambles and opens the next
+    epoch. 3 launches, no copy kernel, fence or flag; same results as scrambled_decode_step
+    (which stays the reference-shaped form: NCCL all-to-all or PeerExchange). GPU only."""
 
-    def __init__(self, exchange: PeerExchange, bufs: StepBuffers, inquirer_keys: Sequence, shard,
-                 n_splits: Optional[int] = None, kv_heads: Optional[int] = None):
+    def __init__(self, b_per: int, q_heads: int, head_dim: int, inquirer_keys: Sequence, shard,
+                 n_splits: Optional[int] = None, kv_heads: Optional[int] = None,
+                 wire_dtype: torch.dtype = torch.bfloat16, group: Optional[dist.ProcessGroup] = None):
+        import ctypes as ct
+
         from . import capi, ops
-        ct = exchange.ct
-        self.capi, self.ops, self.ex, self.bufs = capi, ops, exchange, bufs
-        W, rank = exchange.world, exchange.rank
-        Hq, Lq, d = bufs.dims
-        if Lq != 1:
-            raise ValueError("FusedDecode handles single-row decode (L_q = 1)")
-        self.W, self.Bp, self.Hq, self.d = W, bufs.q_send.shape[1], Hq, d
-        dev = bufs.q_send.device
+        self.capi, self.ops = capi, ops
+        W, rank = (dist.get_world_size(group), dist.get_rank(group)) if dist.is_initialized() else (1, 0)
+        dev = shard.k.device
+        self.W, self.Bp, self.Hq, self.d = W, b_per, q_heads, head_dim
         self.kv_heads = kv_heads or inquirer_keys[0].kv_heads
-        self.keys_all = torch.cat([k.dev for k in inquirer_keys], 0).contiguous()
+        self.keys_all = torch.cat([k.dev for k in inquirer_keys], 0).contiguous()   # [W * B_p, bytes]
         self.shard = shard
-        B = W * self.Bp
-        self.S = n_splits or capi.default_splits(B, Hq, 1, shard.capacity, kv_heads=shard.k.shape[1], head_dim=d)
-        self.work_o = torch.empty((self.S, B, Hq, 1, d), dtype=torch.float32, device=dev)
-        self.work_st = torch.empty((self.S, B, Hq, 1, 2), dtype=torch.float32, device=dev)
-        # [K1 dest counters W | K2 dest counters W | K3 done 1 | K2 per-row fold counters B*Hq]
-        self.counters = torch.zeros(2 * W + 1 + B * Hq, dtype=torch.int32, device=dev)
-        exchange.epoch.fill_(1)
-        self.q_dst, self.q_flag = exchange.q_args[1], exchange.q_args[2]
-        self.r_dst, self.r_flag = exchange.r_args[1], exchange.r_args[2]
-        rec = bufs.ret_recv.shape[-1]
-        srcs = [ops.MergeSource(bufs.ret_recv[dom], bufs.ret_recv[dom, :, Hq * d:], inquirer_keys[dom].dev, None,
-                                batch_stride=rec, shape=(self.Bp, Hq, 1, d)) for dom in range(W)]
-        self.srcs = (capi.MergeSource * W)()
-        for i, s in enumerate(srcs):
-            self.srcs[i].o, self.srcs[i].stats = s.o.data_ptr(), s.stats.data_ptr()
-            self.srcs[i].keys, self.srcs[i].pq_inv, self.srcs[i].batch_stride = s.keys.data_ptr(), None, rec
-        self.kstride = inquirer_keys[0].dev.stride(0) if inquirer_keys[0].dev.dim() > 1 else 0
-        self.ct = ct
+        self.S = n_splits or capi.default_splits(W * b_per, q_heads, 1, shard.capacity, kv_heads=shard.k.shape[1],
+                                                 head_dim=head_dim)
+        self.wire = ops._DT[wire_dtype]
+        q_slot = b_per * q_heads * head_dim * (4 if wire_dtype == torch.bfloat16 else 8)
+        r_slot = self.S * b_per * q_heads * (head_dim + 2) * 8
+        self.q_ll = torch.zeros(W * q_slot, dtype=torch.uint8, device=dev)
+        self.rec_ll = torch.zeros(W * r_slot, dtype=torch.uint8, device=dev)
+        self.epoch = torch.ones(1, dtype=torch.int32, device=dev)
+        self.done = torch.zeros(1, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize()
+        ptrs, self.opened = map_peer_buffers({"q": self.q_ll, "rec": self.rec_ll}, group)
+        arr = lambda xs: (ct.c_void_p * W)(*xs)  # noqa: E731
+        self.ll_q = arr([ptrs["q"][r] + rank * q_slot for r in range(W)])       # my slot on every destination
+        self.ll_rec = arr([ptrs["rec"][r] + rank * r_slot for r in range(W)])   # my slot on every inquirer
+        if dist.is_initialized():
+            dist.barrier(group=group)
+
+    def scramble_q(self, q: torch.Tensor):
+        """K1: span_send_layer for every domain, Q' written into the destinations' slots."""
+        st = torch.cuda.current_stream().cuda_stream
+        self.capi.check(self.capi.LIB.sda_ll_scramble_q(
+            st, q.data_ptr(), self.ops._dtype_code(q), self.W, self.Bp, self.Hq, self.d, self.keys_all.data_ptr(),
+            self.keys_all.stride(0), self.kv_heads, self.ll_q, self.wire, self.epoch.data_ptr()), "sda_ll_scramble_q")
+
+    def serve(self):
+        """K2: try_serve_q on this domain's shard, every split's record into its inquirer's slot."""
+        st, sh = torch.cuda.current_stream().cuda_stream, self.shard
+        self.capi.check(self.capi.LIB.sda_ll_partial_attention(
+            st, self.q_ll.data_ptr(), self.wire, sh.k.data_ptr(), sh.v.data_ptr(), self.ops._dtype_code(sh.k),
+            sh.capacity, sh.kv_len.data_ptr(), self.W, self.Bp, self.Hq, sh.k.shape[1], self.d, self.S, self.ll_rec,
+            self.epoch.data_ptr()), "sda_ll_partial_attention")
+
+    def finish(self, out: torch.Tensor):
+        """K3: span_finish_layer over every domain's split records; opens the next epoch."""
+        st = torch.cuda.current_stream().cuda_stream
+        self.capi.check(self.capi.LIB.sda_ll_unscramble_merge(
+            st, self.rec_ll.data_ptr(), self.W, self.S, self.keys_all.data_ptr(), self.keys_all.stride(0),
+            self.kv_heads, self.Bp, self.Hq, self.d, out.data_ptr(), self.ops._dtype_code(out),
+            self.epoch.data_ptr(), self.done.data_ptr()), "sda_ll_unscramble_merge")
 
     def step(self, q: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
-        capi, ops, L = self.capi, self.ops, self.capi.LIB
-        st = torch.cuda.current_stream().cuda_stream
-        W, Bp, Hq, d, S = self.W, self.Bp, self.Hq, self.d, self.S
-        ep, cnt = self.ex.epoch.data_ptr(), self.counters.data_ptr()
-        flags = self.ex.flags.data_ptr()
-        sh = self.shard
-        capi.check(L.sda_fused_scramble_q(st, q.data_ptr(), ops._dtype_code(q), W, Bp, Hq, d, self.keys_all.data_ptr(),
-                                          self.keys_all.stride(0), self.kv_heads, self.q_dst,
-                                          ops._dtype_code(self.bufs.q_recv), self.q_flag, ep, cnt),
-                   "sda_fused_scramble_q")
-        capi.check(L.sda_fused_partial_attention(st, self.bufs.q_recv.data_ptr(), ops._dtype_code(self.bufs.q_recv),
-                                                 sh.k.data_ptr(), sh.v.data_ptr(), ops._dtype_code(sh.k), sh.capacity,
-                                                 sh.kv_len.data_ptr(), W, Bp, Hq, sh.k.shape[1], d, S,
-                                                 self.work_o.data_ptr(), self.work_st.data_ptr(), flags, ep,
-                                                 cnt + 4 * (2 * W + 1), self.r_dst, self.r_flag, cnt + 4 * W),
-                   "sda_fused_partial_attention")
-        capi.check(L.sda_fused_unscramble_merge(st, self.srcs, W, self.kstride, self.kv_heads, 0, Bp, Hq, 1, d,
-                                                out.data_ptr(), ops._dtype_code(out), flags + 4 * W, W, ep,
-                                                cnt + 4 * 2 * W),
-                   "sda_fused_unscramble_merge")
+        """q [B_p, Hq, 1, d] (this rank's requests) -> out [B_p, Hq, 1, d]."""
+        self.scramble_q(q)
+        self.serve()
+        self.finish(out)
         return out
 
 

@@ -260,3 +260,51 @@ def test_distributed_step_prefill_rows_world1():
     got = out.double().cpu().numpy()
     ref = case.oracle()
     assert max_abs_rel(got, ref) < TOL_BF16 and rel_fro(got, ref) < TOL_BF16
+
+
+@pytest.mark.parametrize("wire", [torch.bfloat16, torch.float32])
+def test_ll_decode_world1_steps_and_graph(wire):
+    """The LL-chained decode step (K1 -> K2 -> K3 carrying the exchange in epoch-tagged words,
+    PDL-launched) at world 1: several steps (the epoch advances; stale words of the previous step
+    must never be taken) eager and replayed from a CUDA graph, each against the oracle."""
+    from paper_2605_25716_b200 import distributed as sdist
+    B, H, D, LK = 3, 4, 128, 2048
+    shard = protocol.KVShard(B, H, LK, D, "cuda")
+    tol = TOL_BF16   # bf16 KV (and the oracle's bf16 wire) either way
+    cases = [Case(B=B, Hq=H, Hkv=H, d=D, lk=LK, n_nodes=1, lq=1, dtype=torch.bfloat16, seed=31 + i) for i in range(4)]
+    # one shard (the KV of case 0), four different queries against it
+    keys = protocol.DomainKeys(cases[0].request_ids(), 0, 1, H, D, "cuda")
+    shard.ship_segment(dev(cases[0].k[0], torch.bfloat16), dev(cases[0].v[0], torch.bfloat16), keys, first_pos=0)
+    lld = sdist.LLDecode(B, H, D, [keys], shard, n_splits=3, wire_dtype=wire)
+    out = torch.empty((B, H, 1, D), dtype=torch.float32, device="cuda")
+
+    # references: the oracle (bf16 wire: rounding-matched) and, for either wire, the
+    # reference-shaped device step (K1 -> K2 -> split fold -> K3) with Q' in the same dtype
+    bufs = sdist.StepBuffers.allocate(1, B, H, 1, D, wire, "cuda")
+    comp = sdist.gpu_rank_compute([keys], shard, n_splits=3)
+    plain_out = torch.empty_like(out)
+
+    def check(i):
+        got = out.double().cpu().numpy()
+        sdist.scrambled_decode_step(dev(cases[i].q, torch.bfloat16), comp, bufs, plain_out)
+        same = plain_out.double().cpu().numpy()
+        assert max_abs_rel(got, same) < 1e-5, i
+        if wire == torch.bfloat16:
+            c = cases[i]
+            c.k, c.v = cases[0].k, cases[0].v
+            ref = c.oracle()
+            assert max_abs_rel(got, ref) < tol and rel_fro(got, ref) < tol, i
+
+    for i in range(3):   # eager steps
+        lld.step(dev(cases[i].q, torch.bfloat16), out)
+        check(i)
+    q_static = dev(cases[0].q, torch.bfloat16)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        lld.step(q_static, out)
+    for i in (3, 1, 2):
+        q_static.copy_(dev(cases[i].q, torch.bfloat16))
+        g.replay()
+        torch.cuda.synchronize()
+        check(i)
+    assert int(lld.epoch.item()) == 1 + 3 + 3   # K3 opened one epoch per step

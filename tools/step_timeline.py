@@ -4,7 +4,7 @@ A 1-thread %globaltimer kernel (sda_trace_timestamp) is placed between the phase
 STEPS steps are captured unrolled in one CUDA graph (distinct stamp slots) and replayed. Rank 0
 prints, per rank, the median duration of every phase and the median offset of each rank's step
 start from rank 0's (the globaltimers of the GPUs of one box agree to ~1 us).
-  python -m torch.distributed.run --nproc-per-node 4 tools/step_timeline.py [fused|p2p|nccl]"""
+  python -m torch.distributed.run --nproc-per-node 4 tools/step_timeline.py [ll|p2p|nccl]"""
 import os
 import sys
 
@@ -20,7 +20,7 @@ STEPS, REPS = 20, 10
 
 
 def main():
-    mode = sys.argv[1] if len(sys.argv) > 1 else "fused"
+    mode = sys.argv[1] if len(sys.argv) > 1 else "ll"
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -40,34 +40,10 @@ def main():
     st = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
     qa, ret = bufs.q_recv.view(Bt, H, 1, D), bufs.ret_send.view(Bt, -1)
 
-    if mode == "fused":
-        fused = sdist.FusedDecode(sdist.PeerExchange(bufs), bufs, inq, shard, kv_heads=H)
-        names = ["K1 (+push Q)", "K2 (+wait Q, fold, push ret)", "K3 (+wait ret)"]
-        ex = fused.ex
-
-        def k_calls():
-            from paper_2605_25716_b200 import ops
-            W, Bp, S = fused.W, fused.Bp, fused.S
-            ep, cnt, flags = ex.epoch.data_ptr(), fused.counters.data_ptr(), ex.flags.data_ptr()
-            Li = capi.LIB
-            sh = fused.shard
-            return [
-                lambda: capi.check(Li.sda_fused_scramble_q(st(), q.data_ptr(), ops._dtype_code(q), W, Bp, H, D,
-                                                           fused.keys_all.data_ptr(), fused.keys_all.stride(0), H,
-                                                           fused.q_dst, ops._dtype_code(bufs.q_recv), fused.q_flag,
-                                                           ep, cnt), "k1"),
-                lambda: capi.check(Li.sda_fused_partial_attention(st(), bufs.q_recv.data_ptr(),
-                                                                  ops._dtype_code(bufs.q_recv), sh.k.data_ptr(),
-                                                                  sh.v.data_ptr(), ops._dtype_code(sh.k),
-                                                                  sh.capacity, sh.kv_len.data_ptr(), W, Bp, H,
-                                                                  sh.k.shape[1], D, S, fused.work_o.data_ptr(),
-                                                                  fused.work_st.data_ptr(), flags, ep,
-                                                                  cnt + 4 * (2 * W + 1), fused.r_dst, fused.r_flag,
-                                                                  cnt + 4 * W), "k2"),
-                lambda: capi.check(Li.sda_fused_unscramble_merge(st(), fused.srcs, W, fused.kstride, H, 0, Bp, H, 1,
-                                                                 D, out.data_ptr(), ops._dtype_code(out),
-                                                                 flags + 4 * W, W, ep, cnt + 8 * W), "k3")]
-        fns = k_calls()
+    if mode == "ll":
+        lld = sdist.LLDecode(B, H, D, inq, shard, kv_heads=H)
+        names = ["K1 (+Q' out)", "K2 (+Q' in, records out)", "K3 (+records in)"]
+        fns = [lambda: lld.scramble_q(q), lld.serve, lambda: lld.finish(out)]
     elif mode == "p2p":
         ex = sdist.PeerExchange(bufs)
         names = ["epoch", "K1", "push Q", "wait Q", "K2+fold", "push ret", "wait ret", "K3"]
