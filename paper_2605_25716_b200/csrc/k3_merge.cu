@@ -12,6 +12,7 @@
 // once per domain: one 128-point FWHT per (row, domain) instead of per split.
 // HBM-bound: reads (4d + 8) B per (row, source), writes d * sizeof(out) B per row.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -193,11 +194,162 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
     }
 }
 
+// Few sources (n_src <= kSmallSrc, plain memory): every source's stats and O' row are loaded up
+// front, so a row costs ~2 dependent memory latencies (p_q^-1 index, then all data at once)
+// instead of one per source -- the prefill merge (65K rows x 4 splits) is latency-bound on the
+// per-row chain, not on bytes.
+constexpr int kSmallSrc = 8;
+
+template <int D, typename TOut, int NS, int RPW, bool EXACT>
+__global__ void __launch_bounds__(128) k3_merge_small_kernel(const K3Params p) {
+    constexpr int E = D / 32;
+    __shared__ __align__(16) float sh_all[4][D];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* sh = sh_all[warp];
+    const int64_t total = p.n_batch * p.q_heads * p.q_rows;
+    const int n = EXACT ? NS : p.n_src;   // !EXACT: n_src <= NS, guarded
+
+    // RPW rows per warp, all of their sources' stats and O' rows in flight at once (NS = n_src
+    // exactly; rows and their (b, h, r) decomposition fit 32 bits, checked by the launcher)
+    int64_t rows[RPW], bs[RPW], rs[RPW];
+    int hs[RPW];
+    bool act[RPW];
+    float2 st[RPW][NS];
+    float ov[RPW][NS][E];
+    const uint32_t qrows = (uint32_t)p.q_rows, qheads = (uint32_t)p.q_heads;
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) {
+        const uint32_t row_raw = ((uint32_t)blockIdx.x * 4 + warp) * RPW + q;
+        act[q] = row_raw < (uint32_t)total;
+        const uint32_t row32 = act[q] ? row_raw : (uint32_t)total - 1;
+        rows[q] = row32;
+        const uint32_t bh = row32 / qrows;
+        rs[q] = row32 - bh * qrows;
+        const uint32_t b32 = bh / qheads;
+        hs[q] = (int)(bh - b32 * qheads);
+        bs[q] = b32;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            if (EXACT || s < n) {
+                const K3Source& src = p.src[s];
+                const int64_t ri = src.pq_inv ? (int64_t)src.pq_inv[bs[q] * p.pq_bstride + rs[q]] : rs[q];
+                const int64_t hr = (int64_t)hs[q] * p.q_rows + ri;
+                const int64_t st_off = src.bstride ? bs[q] * src.bstride + hr * 2 : (bh * p.q_rows + ri) * 2;
+                const int64_t o_off = src.bstride ? bs[q] * src.bstride + hr * D : (bh * p.q_rows + ri) * D;
+                st[q][s] = *reinterpret_cast<const float2*>(src.stats + st_off);
+                load_vec_any<E>(src.o + o_off + lane * E, ov[q][s]);
+            } else {
+                st[q][s] = make_float2(-INFINITY, 0.f);
+            }
+        }
+    }
+
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) {
+        const int64_t b = bs[q], r = rs[q];
+        const int h = hs[q];
+        const int kh = h / (p.q_heads / p.key_heads);
+        SrcLd<E> kt;
+        auto load_tables = [&](const uint8_t* keys) {
+            const uint8_t* sc = scrambler_ptr(keys, p.keys_bstride, b, kh, D, 1);
+            const float* ftab = reinterpret_cast<const float*>(sc);
+            const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + 24 * D);
+            load_vec_any<E>(ftab + kInvIn * D + lane * E, kt.inv_in);
+            load_vec_any<E>(ftab + kInvOut * D + lane * E, kt.inv_out);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                kt.p2[e] = utab[kP2 * D + lane * E + e];
+                kt.p1[e] = utab[kP1 * D + lane * E + e];
+            }
+        };
+        if (p.src[0].keys) load_tables(p.src[0].keys);
+
+        float mstar = -INFINITY;   // attention.cpp:103-105
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+            if ((EXACT || s < n) && st[q][s].y > 0.f) mstar = fmaxf(mstar, st[q][s].x);
+
+        float out[E], acc[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) out[e] = acc[e] = 0.f;
+        float denom = 0.f;
+        const bool single = n == 1;
+        bool pending = false;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            if (EXACT || s < n) {
+                const K3Source& src = p.src[s];
+                if (s > 0 && src.keys && src.keys != p.src[s - 1].keys) load_tables(src.keys);   // new group
+                if (st[q][s].y > 0.f) {
+                    const float w = single ? 1.f : st[q][s].y * expf(st[q][s].x - mstar);
+                    denom += single ? st[q][s].y : w;
+#pragma unroll
+                    for (int e = 0; e < E; ++e) acc[e] = fmaf(w, ov[q][s][e], acc[e]);
+                    pending = true;
+                }
+                const bool group_end = (s + 1 == n) || (p.src[s + 1].keys != src.keys);
+                if (group_end && pending) {
+                    if (src.keys) {
+                        unscramble_acc<D>(kt, acc, out, sh, lane);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < E; ++e) out[e] += acc[e];
+                    }
+#pragma unroll
+                    for (int e = 0; e < E; ++e) acc[e] = 0.f;
+                    pending = false;
+                }
+            }
+        }
+        const bool masked = !(mstar > -INFINITY);
+        if (masked && lane == 0 && p.err && act[q]) atomicExch(p.err, (int32_t)SDA_ERR_MASKED_ROW);
+        const float inv = masked ? __int_as_float(0x7fc00000) : (single ? 1.f : 1.f / denom);
+#pragma unroll
+        for (int e = 0; e < E; ++e) out[e] *= inv;
+        const int64_t hr = (int64_t)h * p.q_rows + r;
+        if (act[q])
+            store_vec_any<E>(static_cast<TOut*>(p.out) + (p.out_bstride ? b * p.out_bstride + hr * D : rows[q] * D) +
+                                 lane * E, out);
+        if (p.out_stats && lane == 0 && act[q]) {
+            const int64_t so = p.out_bstride ? b * p.out_bstride + hr * 2 : rows[q] * 2;
+            p.out_stats[so + 0] = single ? (masked ? -INFINITY : mstar) : mstar;
+            p.out_stats[so + 1] = masked ? 0.f : denom;
+        }
+    }
+}
+
+template <int D, typename TOut, int NS, bool EXACT = true>
+static void launch_k3_small(const K3Params& p, int64_t total, cudaStream_t st) {
+    constexpr int RPW = NS * (D / 32) <= 16 ? 2 : 1;   // in-flight rows per warp (4 measured slower)
+    const int64_t per_cta = 4 * RPW;
+    k3_merge_small_kernel<D, TOut, NS, RPW, EXACT><<<(unsigned)((total + per_cta - 1) / per_cta), 128, 0, st>>>(p);
+}
+
 template <int D, typename TOut>
 static cudaError_t launch_k3_t(const K3Params& p, cudaStream_t st) {
     const int64_t total = p.n_batch * p.q_heads * p.q_rows;
     if (p.ll) return pdl_launch(k3_merge_kernel<D, TOut>, dim3((unsigned)((total + 3) / 4)), dim3(128), st, p);
-    k3_merge_kernel<D, TOut><<<(unsigned)((total + 3) / 4), 128, 0, st>>>(p);
+    const bool small_ok = total < (int64_t(1) << 30) && !getenv("SDA_K3_PIPELINED");
+    if constexpr (D <= 128) {   // 9..16 sources (the decode split fold): all in flight, one row per warp
+        if (small_ok && p.n_src > kSmallSrc && p.n_src <= 16) {
+            launch_k3_small<D, TOut, 16, false>(p, total, st);
+            return cudaGetLastError();
+        }
+    }
+    if (p.n_src <= kSmallSrc && small_ok) {
+        switch (p.n_src) {
+            case 1: launch_k3_small<D, TOut, 1>(p, total, st); break;
+            case 2: launch_k3_small<D, TOut, 2>(p, total, st); break;
+            case 3: launch_k3_small<D, TOut, 3>(p, total, st); break;
+            case 4: launch_k3_small<D, TOut, 4>(p, total, st); break;
+            case 5: launch_k3_small<D, TOut, 5>(p, total, st); break;
+            case 6: launch_k3_small<D, TOut, 6>(p, total, st); break;
+            case 7: launch_k3_small<D, TOut, 7>(p, total, st); break;
+            default: launch_k3_small<D, TOut, 8>(p, total, st); break;
+        }
+    } else {
+        k3_merge_kernel<D, TOut><<<(unsigned)((total + 3) / 4), 128, 0, st>>>(p);
+    }
     return cudaGetLastError();
 }
 
