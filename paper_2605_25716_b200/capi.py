@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsdattn_b200.so")
+LIB_PATH = os.environ.get("SDA_LIB_PATH") or os.path.join(HERE, "libsdattn_b200.so")   # override: kernel-variant experiments
 
 SDA_OK = 0
 SDA_BF16, SDA_F32 = 0, 1

@@ -42,6 +42,28 @@ struct K2TcParams {
     float scale_log2;      // log2(e) / sqrt(d)
 };
 
+#ifdef SDA_K2_TRACE
+// debug build only (tools/k2_trace.py): globaltimer stamps of CTA (0,0,0) -- [kind][j], kinds:
+// 0/1 softmax g got S, 2/3 softmax g arrives with P, 4/5 PV0/PV1 issue, 6/7 MMA loop top / V ready,
+// 8 before the P1 wait, 9/10 before / after the K(j+1) wait
+__device__ uint64_t g_k2_trace[16][64];
+__device__ __forceinline__ void k2_stamp(int kind, int64_t j) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < 64) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_k2_trace[kind][j] = t;
+    }
+}
+#define K2_STAMP(k, j) k2_stamp(k, j)
+#else
+#define K2_STAMP(k, j)
+#endif
+
+// The MMA warp's waits for P sit on the S -> softmax -> PV -> S chain of each Q tile: it spins
+// (test_wait) instead of suspending (try_wait), which trims ~100 ns of wake-up per hand-off
+// (tools/k2_trace.py; +2 % on C3).
+#define K2_WAIT_P(b, ph) tc::mbar_wait_spin(b, ph)
+
 namespace k2tc {
 constexpr int D = 128;
 constexpr int TILE = 128;
@@ -56,6 +78,13 @@ constexpr int NBAR = 15;
 constexpr int SMEM = OFF_BAR + NBAR * 8 + 16;
 constexpr int THREADS = 320;
 constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 384;
+// Exponentials per 4 pairs computed on the FMA pipe (tc::exp2_fma2) instead of MUFU.EX2. Measured
+// on C3 with the single-pass softmax: 0 -> 484 us, 1 -> 492 us, 2 -> 526 us (the added FMA-pipe
+// instructions cost more issue time than the MUFU time they free), so it stays off by default.
+#ifndef SDA_K2_EMU_OF4
+#define SDA_K2_EMU_OF4 0
+#endif
+constexpr int kEmuOf4 = SDA_K2_EMU_OF4;
 }  // namespace k2tc
 
 __global__ void __launch_bounds__(320, 1)
@@ -143,7 +172,9 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
         }
     } else if (warp == 9) {
         // ------------------------------------------------------------------ MMA issuer
-        if (lane == 0 && nkv > 0) {
+        // the whole warp runs the loop (warp-uniform descriptors); the elected lane issues
+        if (nkv > 0) {
+            const bool leader = tc::elect_one();
             constexpr uint32_t IDESC_S = tc::idesc_bf16_f32(128, 128, false, false);   // Q K^T, both K-major
             constexpr uint32_t IDESC_O = tc::idesc_bf16_f32(128, 128, false, true);    // P V, V MN-major
             const uint32_t q0 = tc::smem_u32(smem + OFF_Q0), q1 = tc::smem_u32(smem + OFF_Q1);
@@ -156,10 +187,10 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
 #pragma unroll
                 for (int k = 0; k < D / 16; ++k) {
                     const uint32_t off = (k >> 2) * BLK + (k & 3) * 32;
-                    tc::mma_bf16_ss(d_tmem, tc::sw128_desc(qa + off, 16, 1024), tc::sw128_desc(kb + off, 16, 1024), IDESC_S,
-                                    k > 0 ? 1u : 0u);
+                    const uint64_t da = tc::sw128_desc(qa + off, 16, 1024), db = tc::sw128_desc(kb + off, 16, 1024);
+                    if (leader) tc::mma_bf16_ss(d_tmem, da, db, IDESC_S, k > 0 ? 1u : 0u);
                 }
-                tc::mma_commit(&s_full[g]);
+                if (leader) tc::mma_commit(&s_full[g]);
             };
             auto issue_pv = [&](int g, int64_t j) {
                 const int st = (int)(j & 1);
@@ -167,41 +198,49 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 const uint32_t d_tmem = tmem + (g ? COL_O1 : COL_O0);
                 const uint32_t p_tmem = tmem + (g ? COL_S1 : COL_S0);
 #pragma unroll
-                for (int k = 0; k < TILE / 16; ++k)   // 16 keys per step: P columns 8k.., V rows 16k..
-                    tc::mma_bf16_ts(d_tmem, p_tmem + k * 8, tc::sw128_desc(vb + k * 2048, BLK, 1024), IDESC_O,
-                                    (j > 0 || k > 0) ? 1u : 0u);
+                for (int k = 0; k < TILE / 16; ++k) {   // 16 keys per step: P columns 8k.., V rows 16k..
+                    const uint64_t db = tc::sw128_desc(vb + k * 2048, BLK, 1024);
+                    if (leader) tc::mma_bf16_ts(d_tmem, p_tmem + k * 8, db, IDESC_O, (j > 0 || k > 0) ? 1u : 0u);
+                }
             };
             tc::mbar_wait(q_full, 0);
             tc::mbar_wait(&k_full[0], 0);
             tc::tc_fence_after();
             issue_s(0, 0);
             if (two) issue_s(1, 0);
-            tc::mma_commit(&k_empty[0]);
+            if (leader) tc::mma_commit(&k_empty[0]);
             for (int64_t j = 0; j < nkv; ++j) {
                 const int st = (int)(j & 1);
                 const uint32_t ph = (uint32_t)((j >> 1) & 1);
+                K2_STAMP(6, j);
                 tc::mbar_wait(&v_full[st], ph);
-                tc::mbar_wait(&p_full[0], (uint32_t)(j & 1));
+                K2_STAMP(7, j);
+                K2_WAIT_P(&p_full[0], (uint32_t)(j & 1));
                 tc::tc_fence_after();
+                K2_STAMP(4, j);
                 issue_pv(0, j);
-                if (!two) tc::mma_commit(&v_empty[st]);
-                if (j + 1 == nkv) tc::mma_commit(&o_final[0]);
+                if (!two && leader) tc::mma_commit(&v_empty[st]);
+                if (j + 1 == nkv && leader) tc::mma_commit(&o_final[0]);
                 if (j + 1 < nkv) {
                     const int sn = (int)((j + 1) & 1);
+                    K2_STAMP(9, j);
                     tc::mbar_wait(&k_full[sn], (uint32_t)(((j + 1) >> 1) & 1));
+                    K2_STAMP(10, j);
                     tc::tc_fence_after();
                     issue_s(0, j + 1);
-                    if (!two) tc::mma_commit(&k_empty[sn]);
+                    if (!two && leader) tc::mma_commit(&k_empty[sn]);
                 }
                 if (!two) continue;
-                tc::mbar_wait(&p_full[1], (uint32_t)(j & 1));
+                K2_STAMP(8, j);
+                K2_WAIT_P(&p_full[1], (uint32_t)(j & 1));
                 tc::tc_fence_after();
+                K2_STAMP(5, j);
                 issue_pv(1, j);
-                tc::mma_commit(&v_empty[st]);
-                if (j + 1 == nkv) tc::mma_commit(&o_final[1]);
+                if (leader) tc::mma_commit(&v_empty[st]);
+                if (j + 1 == nkv && leader) tc::mma_commit(&o_final[1]);
                 if (j + 1 < nkv) {
                     issue_s(1, j + 1);
-                    tc::mma_commit(&k_empty[(j + 1) & 1]);
+                    if (leader) tc::mma_commit(&k_empty[(j + 1) & 1]);
                 }
             }
         }
@@ -220,6 +259,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
         for (int64_t j = 0; group_live && j < nkv; ++j) {
             tc::mbar_wait(&s_full[g], (uint32_t)(j & 1));
             tc::tc_fence_after();
+            if ((warp & 3) == 0 && lane == 0) K2_STAMP(g, j);
             if (!warp_live) {
                 tc::tc_fence_before();
                 tc::mbar_arrive(&p_full[g]);
@@ -268,14 +308,21 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 m_use = m_new;
             }
             const float mu = (m_use == -INFINITY) ? 0.f : m_use;
-            // p = exp2(s * scale - mu): one packed FFMA2 per two logits, packed FADD2 row sums
+            // p = exp2(s * scale - mu): one packed FFMA2 per two logits (a share of the exponentials
+            // on the FMA pipe, exp2_fma2), packed FADD2 row sums
             const uint64_t sc2 = tc::f2(p.scale_log2, p.scale_log2), nmu2 = tc::f2(-mu, -mu);
             uint64_t acc0 = tc::f2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
             for (int i = 0; i < 64; ++i) {   // P packed in place: s[i] <- bf16x2(p[2i], p[2i+1])
                 float x0, x1;
                 tc::f2_split(tc::ffma2(tc::f2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sc2, nmu2), x0, x1);
-                const float p0 = ex2(x0), p1 = ex2(x1);
+                float p0, p1;
+                if ((i & 3) < kEmuOf4) {
+                    tc::exp2_fma2(x0, x1, p0, p1);
+                } else {
+                    p0 = ex2(x0);
+                    p1 = ex2(x1);
+                }
                 if (i & 1)
                     acc1 = tc::fadd2(acc1, tc::f2(p0, p1));
                 else
@@ -290,6 +337,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             for (int c = 0; c < 8; ++c) tc::tmem_st8(s_col + c * 8, s + c * 8);
             tc::tmem_st_wait();
             tc::tc_fence_before();
+            if ((warp & 3) == 0 && lane == 0) K2_STAMP(2 + g, j);
             tc::mbar_arrive(&p_full[g]);
         }
         // epilogue: O / l, (row_max, exp_sum) in natural units
@@ -381,3 +429,9 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
 }
 
 }  // namespace sda
+
+#ifdef SDA_K2_TRACE
+extern "C" int sda_debug_k2_trace(void* host) {
+    return (int)cudaMemcpyFromSymbol(host, sda::g_k2_trace, sizeof(sda::g_k2_trace));
+}
+#endif

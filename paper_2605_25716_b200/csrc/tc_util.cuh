@@ -35,6 +35,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Spinning variant (test_wait: never suspends): lower wake-up latency for a lone issuer warp whose
+// waits sit on the critical path, at the price of issue slots on its SMSP.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 // 16-byte async copy global -> shared (LDGSTS), L2-only caching.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
@@ -118,6 +129,18 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// One lane of a fully active warp (the lowest): the MMA issuer runs its loop with the whole warp
+// so the operand descriptors stay warp-uniform (uniform registers, no R2UR per instruction) and
+// only the tcgen05.mma / commit instructions are predicated on the elected lane.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
 // Arrive on `bar` once every previously issued tcgen05.mma of this thread has completed.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -197,6 +220,31 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
     float d;
     asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
     return d;
+}
+
+// 2^x for two values x <= 0 on the FMA pipe instead of the MUFU (XU) pipe, which on B200 is the
+// softmax's bottleneck (16 MUFU ops per clock per SM vs 128 FMA lanes). x = n + f with
+// n = round(x) (magic-number add), 2^f by a degree-3 minimax polynomial on [-1/2, 1/2]
+// (max relative error 7.5e-5, far below the bf16 rounding P gets next), 2^n by adding n to the
+// exponent field. x is clamped at -125 so the exponent never underflows (2^-125 ~ 2e-38 where
+// the MUFU would return 0 or a denormal: negligible in any row sum).
+__device__ __forceinline__ float exp2_fma(float x) {
+    // scalar FADD / FFMA with immediate operands: no registers tied up in constants
+    constexpr float kMagic = 12582912.f;   // 1.5 * 2^23
+    x = fmaxf(x, -125.f);
+    const float t = __fadd_rn(x, kMagic);                 // round(x) in the low mantissa bits
+    const float n = __fadd_rn(t, -kMagic);                // round(x) as a float
+    const float f = __fadd_rn(x, -n);                     // x - round(x) in [-1/2, 1/2]
+    float p = __fmaf_rn(0.05517143f, f, 0.24261081f);
+    p = __fmaf_rn(p, f, 0.69326097f);
+    p = __fmaf_rn(p, f, 0.9999281f);
+    uint32_t r;   // bits(2^f) + (n << 23): the low bits of t hold n (two's complement)
+    asm("mad.lo.u32 %0, %1, 8388608, %2;" : "=r"(r) : "r"(__float_as_uint(t)), "r"(__float_as_uint(p)));
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ void exp2_fma2(float x0, float x1, float& p0, float& p1) {
+    p0 = exp2_fma(x0);
+    p1 = exp2_fma(x1);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {

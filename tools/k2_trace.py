@@ -1,0 +1,44 @@
+"""Per-iteration timeline of one prefill K2 CTA from a trace build of the library (compile
+k2_prefill_tc.cu with -DSDA_K2_TRACE, link it into a copy of the .so, point SDA_LIB_PATH at it):
+softmax wait / arrive and MMA issue times per KV tile j, in ns. This is how the S -> softmax ->
+PV -> S chain of each Q tile was found to set the period (K2 prefill).
+  SDA_LIB_PATH=_variants/trace/libsdattn_b200.so python tools/k2_trace.py"""
+import ctypes as ct
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_25716_b200 import capi, ops  # noqa: E402
+
+
+def main():
+    Lq, Lk, H, S, D = 2048, 16384, 32, 4, 128
+    dev = torch.device("cuda")
+    q = torch.randn((1, H, Lq, D), device=dev).to(torch.bfloat16)
+    k = torch.randn((1, H, Lk, D), device=dev).to(torch.bfloat16)
+    v = torch.randn((1, H, Lk, D), device=dev).to(torch.bfloat16)
+    for _ in range(3):
+        ops.partial_attention(q, k, v, n_splits=S)
+    torch.cuda.synchronize()
+    buf = np.zeros((16, 64), dtype=np.uint64)
+    capi.LIB.sda_debug_k2_trace.argtypes = [ct.c_void_p]
+    assert capi.LIB.sda_debug_k2_trace(buf.ctypes.data) == 0
+    t = buf.astype(np.int64)
+    n = int((t[0] > 0).sum())
+    base = t[0][0]
+    print("MMA warp, ns relative to sm0_wait(j): top, v_full ok, pv0 issue, before k_full, k_full ok, s0 issued, pv1 issue")
+    for j in range(2, 10):
+        b = t[0][j]
+        print(j, [int(t[k][j] - b) for k in (6, 7, 4, 9, 10, 8, 5)], "sm0_arr", int(t[2][j] - b), "sm1_arr", int(t[3][j] - b))
+    print("j  sm0_wait  sm0_arr  X0   sm1_wait sm1_arr  X1   pv0_iss pv1_iss  period")
+    for j in range(n):
+        per = t[0][j + 1] - t[0][j] if j + 1 < n else 0
+        print(f"{j:2d} {t[0][j]-base:8d} {t[2][j]-base:8d} {t[2][j]-t[0][j]:5d} {t[1][j]-base:8d} {t[3][j]-base:8d} "
+              f"{t[3][j]-t[1][j]:5d} {t[4][j]-base:8d} {t[5][j]-base:8d} {per:6d}")
+
+
+if __name__ == "__main__":
+    main()
