@@ -466,12 +466,14 @@ def run_prefill(devn, steps: int, warmup: int, peaks: dict):
     srcs = ops.sources_from_splits(o, st, keys.dev, pq_inv)
     stream = torch.cuda.current_stream()
     ev = []
+    k1_jobs = [ops.scramble_job(kn, keys.dev, capi.PHI_INV_T, capi.KEYS_KQ, pkv, out=shard.k, out_row_offset=LK, key_heads=H),
+               ops.scramble_job(vn, keys.dev, capi.PHI_FORWARD, capi.KEYS_V, pkv, out=shard.v, out_row_offset=LK, key_heads=H),
+               ops.scramble_job(q, keys.dev, capi.PHI_FORWARD, capi.KEYS_KQ, pq, out=qs, key_heads=H)]
 
     def step(rec):
         # the span's K/V go into the cache rows after the shard (scramble + permute fused into the write)
-        ops.scramble(kn, keys.dev, capi.PHI_INV_T, capi.KEYS_KQ, pkv, out=shard.k, out_row_offset=LK, key_heads=H)
-        ops.scramble(vn, keys.dev, capi.PHI_FORWARD, capi.KEYS_V, pkv, out=shard.v, out_row_offset=LK, key_heads=H)
-        ops.scramble(q, keys.dev, capi.PHI_FORWARD, capi.KEYS_KQ, pq, out=qs, key_heads=H)
+        # ... and the span's Q into Q' (p_q), all three K1 jobs in one launch
+        ops.scramble_batch(k1_jobs, D)
         if rec:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -564,12 +566,13 @@ def run_gqa_mixed(devn, steps: int, warmup: int, peaks: dict):
             ev.append((e0, e1))
         ops.unscramble_merge(srcd, out=outd, key_heads=HKV)
 
+    pkv_p = pkv_new[BD:].contiguous()
+    k1_jobs = [ops.scramble_job(knew, keys_p, capi.PHI_INV_T, capi.KEYS_KQ, pkv_p, out=kp, out_row_offset=L, key_heads=HKV),
+               ops.scramble_job(vnew, keys_p, capi.PHI_FORWARD, capi.KEYS_V, pkv_p, out=vp, out_row_offset=L, key_heads=HKV),
+               ops.scramble_job(qp, keys_p, capi.PHI_FORWARD, capi.KEYS_KQ, pq_p, out=qp_s, key_heads=HKV)]
+
     def prefill():
-        ops.scramble(knew, keys_p, capi.PHI_INV_T, capi.KEYS_KQ, pkv_new[BD:].contiguous(), out=kp,
-                     out_row_offset=L, key_heads=HKV)
-        ops.scramble(vnew, keys_p, capi.PHI_FORWARD, capi.KEYS_V, pkv_new[BD:].contiguous(), out=vp,
-                     out_row_offset=L, key_heads=HKV)
-        ops.scramble(qp, keys_p, capi.PHI_FORWARD, capi.KEYS_KQ, pq_p, out=qp_s, key_heads=HKV)
+        ops.scramble_batch(k1_jobs, D)   # the chunk's K, V into the cache and its Q, one K1 launch
         ops.partial_attention(qp_s, kp, vp, lp, n_splits=Sp, out_o=op_, out_stats=sp_)
         ops.unscramble_merge(srcp, out=outp, key_heads=HKV)
 

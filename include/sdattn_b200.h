@@ -131,6 +131,30 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys,
                         void* out, int32_t out_dtype, int64_t out_rows_cap, int64_t out_row_offset,
                         int64_t x_batch_mod);
 
+/* Several K1 jobs in one launch (up to SDA_MAX_SCRAMBLE_JOBS; e.g. a prefill step's span K -> K
+ * cache, span V -> V cache and Q -> Q'): each job has exactly the meaning of one sda_scramble call
+ * with the same fields. When every job takes the tensor-core form (bf16 in/out, head_dim 64 or
+ * 128, >= 128 rows) they share one persistent grid, so small spans do not each pay a pipeline
+ * fill and a partial last wave; otherwise the jobs run one sda_scramble after another. */
+#define SDA_MAX_SCRAMBLE_JOBS 3
+typedef struct {
+    int32_t variant, which_keys;
+    const void* x;
+    int32_t x_dtype;
+    int64_t n_batch;
+    int32_t n_heads;
+    int64_t rows;
+    const void* keys;
+    int64_t keys_batch_stride;
+    int32_t key_heads;
+    const uint32_t* perm;
+    int64_t perm_batch_stride;
+    void* out;
+    int32_t out_dtype;
+    int64_t out_rows_cap, out_row_offset, x_batch_mod;
+} sda_scramble_job;
+sda_status sda_scramble_batch(void* stream, int32_t head_dim, const sda_scramble_job* jobs, int32_t n_jobs);
+
 /* ------------------------------------------------------------------------------------------
  * K2  keyless delegated partial attention over the scrambled KV shard.
  *   replaces shard_attention(q', K', V', none) as run by try_serve_q (attention.cpp:42-78;

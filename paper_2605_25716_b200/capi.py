@@ -30,7 +30,7 @@ EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_
            "sda_partial_attention", "sda_partial_attention_causal", "sda_default_splits", "sda_default_splits_gqa", "sda_unscramble_merge", "sda_abi_version",
            "sda_status_string", "sda_launch_count", "sda_ipc_get_handle", "sda_ipc_open_handle",
            "sda_ipc_close_handle", "sda_exchange_epoch", "sda_exchange_push", "sda_exchange_wait",
-           "sda_ll_scramble_q", "sda_ll_partial_attention", "sda_ll_unscramble_merge", "sda_trace_timestamp")
+           "sda_ll_scramble_q", "sda_ll_partial_attention", "sda_ll_unscramble_merge", "sda_trace_timestamp", "sda_scramble_batch")
 
 
 class SdaError(RuntimeError):
@@ -55,6 +55,18 @@ class HostKeysetC(ct.Structure):
     _fields_ = [("kq_s1", _pd), ("kq_p1", _pu32), ("kq_p2", _pu32), ("kq_s2", _pd),
                 ("v_s1", _pd), ("v_p1", _pu32), ("v_p2", _pu32), ("v_s2", _pd),
                 ("token_perm_seed", ct.c_uint64)]
+
+
+class ScrambleJob(ct.Structure):
+    """sda_scramble_job: the arguments of one sda_scramble call."""
+    _fields_ = [("variant", ct.c_int32), ("which_keys", ct.c_int32), ("x", _vp), ("x_dtype", ct.c_int32),
+                ("n_batch", ct.c_int64), ("n_heads", ct.c_int32), ("rows", ct.c_int64), ("keys", _vp),
+                ("keys_batch_stride", ct.c_int64), ("key_heads", ct.c_int32), ("perm", _vp),
+                ("perm_batch_stride", ct.c_int64), ("out", _vp), ("out_dtype", ct.c_int32),
+                ("out_rows_cap", ct.c_int64), ("out_row_offset", ct.c_int64), ("x_batch_mod", ct.c_int64)]
+
+
+MAX_SCRAMBLE_JOBS = 3
 
 
 class MergeSource(ct.Structure):
@@ -107,6 +119,7 @@ def _load() -> ct.CDLL:
     lib.sda_ll_unscramble_merge.argtypes = [_vp, _vp, ct.c_int32, ct.c_int32, _vp, ct.c_int64, ct.c_int32, ct.c_int64,
                                             ct.c_int32, ct.c_int32, _vp, ct.c_int32, _vp, _vp]
     lib.sda_trace_timestamp.argtypes = [_vp, _vp]
+    lib.sda_scramble_batch.argtypes = [_vp, ct.c_int32, ct.POINTER(ScrambleJob), ct.c_int32]
     lib.sda_abi_version.restype = ct.c_int32
     lib.sda_status_string.restype = ct.c_char_p
     lib.sda_status_string.argtypes = [ct.c_int32]

@@ -82,6 +82,50 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys, const
     return from_cuda(sda::launch_k1(p, head_dim, x_dtype, out_dtype, n_batch, static_cast<cudaStream_t>(stream)));
 }
 
+sda_status sda_scramble_batch(void* stream, int32_t head_dim, const sda_scramble_job* jobs, int32_t n_jobs) {
+    if (!jobs || n_jobs < 0 || n_jobs > SDA_MAX_SCRAMBLE_JOBS) return SDA_ERR_INVALID_ARGUMENT;
+    if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
+    if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
+    sda::K1Params ps[SDA_MAX_SCRAMBLE_JOBS];
+    int64_t nb[SDA_MAX_SCRAMBLE_JOBS];
+    int n_live = 0;
+    bool all_tc = !env_flag("SDA_K1_SIMT");
+    for (int i = 0; i < n_jobs; ++i) {   // same validation as sda_scramble, per job
+        const sda_scramble_job& j = jobs[i];
+        if (j.variant != SDA_PHI_FORWARD && j.variant != SDA_PHI_INV_T) return SDA_ERR_INVALID_ARGUMENT;
+        if (j.which_keys != SDA_KEYS_KQ && j.which_keys != SDA_KEYS_V) return SDA_ERR_INVALID_ARGUMENT;
+        if (!j.x || !j.out || !j.keys || !valid_dtype(j.x_dtype) || !valid_dtype(j.out_dtype))
+            return SDA_ERR_INVALID_ARGUMENT;
+        if (j.n_batch < 0 || j.n_heads <= 0 || j.key_heads <= 0 || j.n_heads % j.key_heads != 0 || j.rows < 0)
+            return SDA_ERR_INVALID_ARGUMENT;
+        if (j.out_row_offset < 0 || j.out_row_offset + j.rows > j.out_rows_cap || j.x_batch_mod < 0)
+            return SDA_ERR_INVALID_ARGUMENT;
+        if (j.n_batch > 65535 || j.n_heads > 65535) return SDA_ERR_UNSUPPORTED;
+        if (j.rows == 0 || j.n_batch == 0) continue;
+        sda::K1Params p{j.x, j.out, j.keys, j.perm, j.keys_batch_stride, j.perm_batch_stride, j.rows, j.out_rows_cap,
+                        j.out_row_offset, j.n_heads, j.key_heads, j.which_keys, j.variant == SDA_PHI_INV_T ? 1 : 0,
+                        j.x_batch_mod};
+        all_tc = all_tc && sda::k1_tc_eligible(p, head_dim, j.x_dtype, j.out_dtype);
+        ps[n_live] = p;
+        nb[n_live] = j.n_batch;
+        ++n_live;
+    }
+    if (n_live == 0) return SDA_OK;
+    if (all_tc) {
+        ++g_launches;
+        return from_cuda(sda::launch_k1_tc_multi(ps, nb, n_live, head_dim, static_cast<cudaStream_t>(stream)));
+    }
+    for (int i = 0; i < n_jobs; ++i) {
+        const sda_scramble_job& j = jobs[i];
+        const sda_status st = sda_scramble(stream, j.variant, j.which_keys, j.x, j.x_dtype, j.n_batch, j.n_heads, j.rows,
+                                           head_dim, j.keys, j.keys_batch_stride, j.key_heads, j.perm,
+                                           j.perm_batch_stride, j.out, j.out_dtype, j.out_rows_cap, j.out_row_offset,
+                                           j.x_batch_mod);
+        if (st != SDA_OK) return st;
+    }
+    return SDA_OK;
+}
+
 int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int64_t kv_cap) {
     if (n_batch <= 0 || q_heads <= 0 || q_rows <= 0 || kv_cap <= 0) return 1;
     if (q_rows >= 64) {

@@ -36,7 +36,9 @@
 
 namespace sda {
 
-struct K1TcParams {
+// One scramble job (the arguments of one sda_scramble call); a launch runs up to kK1Jobs of them
+// back to back in one persistent grid (e.g. the span's K, V and Q of a prefill step).
+struct K1TcJob {
     const __nv_bfloat16* x;
     __nv_bfloat16* out;
     const uint8_t* keys;
@@ -51,9 +53,16 @@ struct K1TcParams {
     int which;
     int inv_t;
     int64_t tiles_per_slab;
+    int64_t x_batch_mod;
+};
+constexpr int kK1Jobs = 3;
+
+struct K1TcParams {
+    K1TcJob job[kK1Jobs];
+    int64_t job_tile0[kK1Jobs + 1];   // first global tile of each job (prefix sums)
+    int n_jobs;
     int64_t total_tiles;
     int64_t tiles_per_cta;
-    int64_t x_batch_mod;
 };
 
 template <int D>
@@ -78,7 +87,9 @@ struct K1TcShape {
 };
 
 template <int D>
-__global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const __grid_constant__ CUtensorMap out_map) {
+__global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const __grid_constant__ CUtensorMap out_map0,
+                                                       const __grid_constant__ CUtensorMap out_map1,
+                                                       const __grid_constant__ CUtensorMap out_map2) {
     using S = K1TcShape<D>;
     constexpr int ST = S::STAGES;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -99,8 +110,10 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
     const int64_t last = min(first + p.tiles_per_cta, p.total_tiles);
     if (first >= last) return;
     const int64_t ntiles = last - first;
-    const int H = p.n_heads;
-    const int G = H / p.key_heads;
+    // global tile id -> (job, tile id within the job)
+    auto job_of = [&](int64_t id) -> int {
+        return id >= p.job_tile0[2] ? 2 : (id >= p.job_tile0[1] ? 1 : 0);
+    };
 
     if (tid == 0) {
 #pragma unroll
@@ -115,7 +128,9 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
         tc::mbar_init(bfree, 1);
         tc::mbar_init(bready, 128);
         tc::fence_mbar_init();
-        tc::prefetch_tmap(&out_map);
+        tc::prefetch_tmap(&out_map0);
+        if (p.n_jobs > 1) tc::prefetch_tmap(&out_map1);
+        if (p.n_jobs > 2) tc::prefetch_tmap(&out_map2);
     }
     if (warp == 0) tc::tmem_alloc<S::TMEM_COLS>(tmem_slot);
     tc::tc_fence_before();
@@ -123,13 +138,17 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    auto tile_rows = [&](int64_t id) -> int {
-        const int64_t rem = p.rows - (id % p.tiles_per_slab) * S::TILE;
+    auto tile_rows = [&](const K1TcJob& jb, int64_t lid) -> int {
+        const int64_t rem = jb.rows - (lid % jb.tiles_per_slab) * S::TILE;
         return (int)(rem < S::TILE ? rem : (int64_t)S::TILE);
     };
+    // key slab (request, key head) of a tile, tagged with its job: B is rebuilt when it changes
     auto kslab_of = [&](int64_t id) -> int64_t {
-        const int64_t slab = id / p.tiles_per_slab;
-        return (slab / H) * p.key_heads + (slab % H) / G;
+        const int j = job_of(id);
+        const K1TcJob& jb = p.job[j];
+        const int64_t slab = (id - p.job_tile0[j]) / jb.tiles_per_slab;
+        const int G = jb.n_heads / jb.key_heads;
+        return ((int64_t)j << 48) + (slab / jb.n_heads) * jb.key_heads + (slab % jb.n_heads) / G;
     };
     constexpr int CPR = D / 8;   // 16-byte chunks per row
 
@@ -142,9 +161,11 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
         // ahead so the perm-load latency overlaps earlier tiles' copies
         auto fetch_src = [&](int64_t it, int32_t* src) {
             const int64_t id = first + it;
-            const int64_t slab = id / p.tiles_per_slab, t = id % p.tiles_per_slab;
-            const int nrows = tile_rows(id);
-            const uint32_t* pm = p.perm ? p.perm + (slab / H) * p.perm_bstride + t * S::TILE : nullptr;
+            const K1TcJob& jb = p.job[job_of(id)];
+            const int64_t lid = id - p.job_tile0[job_of(id)];
+            const int64_t slab = lid / jb.tiles_per_slab, t = lid % jb.tiles_per_slab;
+            const int nrows = tile_rows(jb, lid);
+            const uint32_t* pm = jb.perm ? jb.perm + (slab / jb.n_heads) * jb.perm_bstride + t * S::TILE : nullptr;
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
                 const int r = r0 + k * RSTEP;
@@ -158,9 +179,12 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
             const int st = (int)(it % ST);
             if (it + 2 < ntiles) fetch_src(it + 2, nxt2);
             if (it >= ST) tc::mbar_wait(&empty[st], (uint32_t)(((it / ST) - 1) & 1));
-            const int64_t slab = (first + it) / p.tiles_per_slab;
-            const int64_t xslab = p.x_batch_mod > 0 ? ((slab / H) % p.x_batch_mod) * H + slab % H : slab;
-            const __nv_bfloat16* xs = p.x + xslab * p.rows * D + c * 8;
+            const int jj = job_of(first + it);
+            const K1TcJob& jb = p.job[jj];
+            const int64_t slab = (first + it - p.job_tile0[jj]) / jb.tiles_per_slab;
+            const int H = jb.n_heads;
+            const int64_t xslab = jb.x_batch_mod > 0 ? ((slab / H) % jb.x_batch_mod) * H + slab % H : slab;
+            const __nv_bfloat16* xs = jb.x + xslab * jb.rows * D + c * 8;
             uint8_t* a = a_base + st * S::TILE_BYTES + (c >> 3) * S::BLK_BYTES;
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
@@ -221,12 +245,15 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
             const int64_t ks = kslab_of(id);
             if (ks != cur) {
                 if (it > 0) tc::mbar_wait(bfree, (nbuild - 1) & 1);
-                const int64_t slab = id / p.tiles_per_slab;
+                const int jj = job_of(id);
+                const K1TcJob& jb = p.job[jj];
+                const int64_t slab = (id - p.job_tile0[jj]) / jb.tiles_per_slab;
+                const int H = jb.n_heads, G = H / jb.key_heads;
                 const int64_t b = slab / H;
-                const uint8_t* sc = p.keys + b * p.keys_bstride + (int64_t)((slab % H) / G) * 64 * D +
-                                    (int64_t)p.which * 32 * D;
-                const float* fin = reinterpret_cast<const float*>(sc) + (p.inv_t ? kInInvT : kInFwd) * D;
-                const float* fout = reinterpret_cast<const float*>(sc) + (p.inv_t ? kOutInvT : kOutFwd) * D;
+                const uint8_t* sc = jb.keys + b * jb.keys_bstride + (int64_t)((slab % H) / G) * 64 * D +
+                                    (int64_t)jb.which * 32 * D;
+                const float* fin = reinterpret_cast<const float*>(sc) + (jb.inv_t ? kInInvT : kInFwd) * D;
+                const float* fout = reinterpret_cast<const float*>(sc) + (jb.inv_t ? kOutInvT : kOutFwd) * D;
                 const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + 24 * D);
                 for (int e = tid; e < D * CPR; e += 128) {
                     const int n = e / CPR, c = e % CPR;   // B row n (output column), K chunk c
@@ -280,20 +307,24 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
             tc::mbar_arrive(&tempty[acc]);          // accumulator may be overwritten
             tc::fence_proxy_async_smem();
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            const int64_t slab = id / p.tiles_per_slab, t = id % p.tiles_per_slab;
-            const int nrows = tile_rows(id);
-            const int64_t orow0 = slab * p.out_rows_cap + p.out_row_offset + t * S::TILE;
+            const int jj = job_of(id);
+            const K1TcJob& jb = p.job[jj];
+            const int64_t lid = id - p.job_tile0[jj];
+            const int64_t slab = lid / jb.tiles_per_slab, t = lid % jb.tiles_per_slab;
+            const int nrows = tile_rows(jb, lid);
+            const int64_t orow0 = slab * jb.out_rows_cap + jb.out_row_offset + t * S::TILE;
             if (nrows == S::TILE) {
                 if (tid == 0) {
+                    const CUtensorMap* om = jj == 0 ? &out_map0 : (jj == 1 ? &out_map1 : &out_map2);
 #pragma unroll
                     for (int cb = 0; cb < S::KB; ++cb)
-                        tc::tma_store_2d(&out_map, o + cb * S::BLK_BYTES, cb * 64, (int)orow0);
+                        tc::tma_store_2d(om, o + cb * S::BLK_BYTES, cb * 64, (int)orow0);
                     tc::bulk_commit();
                 }
             } else if (tid < nrows) {  // partial tile: never write past the segment
 #pragma unroll
                 for (int c8 = 0; c8 < CPR; ++c8)
-                    *reinterpret_cast<uint4*>(p.out + (orow0 + tid) * D + c8 * 8) =
+                    *reinterpret_cast<uint4*>(jb.out + (orow0 + tid) * D + c8 * 8) =
                         *reinterpret_cast<const uint4*>(o + (c8 >> 3) * S::BLK_BYTES + tc::sw128_off(tid, c8 & 7));
             }
         }
@@ -347,7 +378,7 @@ static int num_sms() {
 }
 
 template <int D>
-static cudaError_t launch_k1_tc_d(const K1Params& q, int64_t n_batch, cudaStream_t st) {
+static cudaError_t launch_k1_tc_d(const K1Params* qs, const int64_t* n_batch, int n_jobs, cudaStream_t st) {
     using S = K1TcShape<D>;
     static bool attr = false;
     if (!attr) {
@@ -355,29 +386,43 @@ static cudaError_t launch_k1_tc_d(const K1Params& q, int64_t n_batch, cudaStream
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    K1TcParams p;
-    p.x = static_cast<const __nv_bfloat16*>(q.x);
-    p.out = static_cast<__nv_bfloat16*>(q.out);
-    p.keys = static_cast<const uint8_t*>(q.keys);
-    p.perm = q.perm;
-    p.keys_bstride = q.keys_bstride;
-    p.perm_bstride = q.perm_bstride;
-    p.rows = q.rows;
-    p.out_rows_cap = q.out_rows_cap;
-    p.out_row_offset = q.out_row_offset;
-    p.n_heads = q.n_heads;
-    p.key_heads = q.key_heads;
-    p.which = q.which;
-    p.inv_t = q.inv_t;
-    p.x_batch_mod = q.x_batch_mod;
-    p.tiles_per_slab = (q.rows + 127) / 128;
-    p.total_tiles = p.tiles_per_slab * n_batch * q.n_heads;
+    if (n_jobs < 1 || n_jobs > kK1Jobs) return cudaErrorInvalidValue;
+    K1TcParams p{};
+    CUtensorMap maps[kK1Jobs];
+    p.n_jobs = n_jobs;
+    int64_t tile0 = 0;
+    for (int j = 0; j < kK1Jobs; ++j) {
+        p.job_tile0[j] = tile0;
+        if (j >= n_jobs) continue;
+        const K1Params& q = qs[j];
+        K1TcJob& jb = p.job[j];
+        jb.x = static_cast<const __nv_bfloat16*>(q.x);
+        jb.out = static_cast<__nv_bfloat16*>(q.out);
+        jb.keys = static_cast<const uint8_t*>(q.keys);
+        jb.perm = q.perm;
+        jb.keys_bstride = q.keys_bstride;
+        jb.perm_bstride = q.perm_bstride;
+        jb.rows = q.rows;
+        jb.out_rows_cap = q.out_rows_cap;
+        jb.out_row_offset = q.out_row_offset;
+        jb.n_heads = q.n_heads;
+        jb.key_heads = q.key_heads;
+        jb.which = q.which;
+        jb.inv_t = q.inv_t;
+        jb.x_batch_mod = q.x_batch_mod;
+        jb.tiles_per_slab = (q.rows + 127) / 128;
+        tile0 += jb.tiles_per_slab * n_batch[j] * q.n_heads;
+        if (!make_tmap_bf16_2d(&maps[j], q.out, n_batch[j] * q.n_heads * q.out_rows_cap, D, 128))
+            return cudaErrorInvalidValue;
+    }
+    p.job_tile0[kK1Jobs] = tile0;
+    for (int j = n_jobs; j < kK1Jobs; ++j) maps[j] = maps[0];
+    p.total_tiles = tile0;
+    if (p.total_tiles == 0) return cudaSuccess;
     const int64_t grid = std::min<int64_t>(p.total_tiles, num_sms());
     p.tiles_per_cta = (p.total_tiles + grid - 1) / grid;
     const int64_t ngrid = (p.total_tiles + p.tiles_per_cta - 1) / p.tiles_per_cta;
-    CUtensorMap map;
-    if (!make_tmap_bf16_2d(&map, q.out, n_batch * q.n_heads * q.out_rows_cap, D, 128)) return cudaErrorInvalidValue;
-    k1_tc_kernel<D><<<(unsigned)ngrid, S::THREADS, S::SMEM, st>>>(p, map);
+    k1_tc_kernel<D><<<(unsigned)ngrid, S::THREADS, S::SMEM, st>>>(p, maps[0], maps[1], maps[2]);
     return cudaGetLastError();
 }
 
@@ -386,8 +431,12 @@ bool k1_tc_eligible(const K1Params& p, int d, int xdt, int odt) {
 }
 
 cudaError_t launch_k1_tc(const K1Params& p, int d, int64_t n_batch, cudaStream_t st) {
-    if (d == 64) return launch_k1_tc_d<64>(p, n_batch, st);
-    if (d == 128) return launch_k1_tc_d<128>(p, n_batch, st);
+    return launch_k1_tc_multi(&p, &n_batch, 1, d, st);
+}
+
+cudaError_t launch_k1_tc_multi(const K1Params* p, const int64_t* n_batch, int n_jobs, int d, cudaStream_t st) {
+    if (d == 64) return launch_k1_tc_d<64>(p, n_batch, n_jobs, st);
+    if (d == 128) return launch_k1_tc_d<128>(p, n_batch, n_jobs, st);
     return cudaErrorInvalidValue;
 }
 

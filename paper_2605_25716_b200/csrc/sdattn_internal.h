@@ -106,6 +106,7 @@ namespace sda {
 cudaError_t launch_k1(const K1Params& p, int d, int xdt, int odt, int64_t n_batch, cudaStream_t st);
 bool k1_tc_eligible(const K1Params& p, int d, int xdt, int odt);
 cudaError_t launch_k1_tc(const K1Params& p, int d, int64_t n_batch, cudaStream_t st);
+cudaError_t launch_k1_tc_multi(const K1Params* p, const int64_t* n_batch, int n_jobs, int d, cudaStream_t st);
 cudaError_t launch_k2_decode(const K2Params& p, int d, int qdt, int kvdt, cudaStream_t st);
 bool k2_prefill_tc_eligible(const K2Params& p, int d, int qdt, int kvdt);
 cudaError_t launch_k2_prefill_tc(const K2Params& p, cudaStream_t st);

@@ -86,6 +86,29 @@ def scramble(x: torch.Tensor, keys: torch.Tensor, variant: int, which: int, perm
     return out
 
 
+def scramble_job(x: torch.Tensor, keys: torch.Tensor, variant: int, which: int, perm: Optional[torch.Tensor] = None,
+                 out: torch.Tensor = None, out_row_offset: int = 0, key_heads: Optional[int] = None,
+                 n_batch: Optional[int] = None) -> capi.ScrambleJob:
+    """One K1 job for scramble_batch, with the meaning of the same scramble() call."""
+    _cuda(x, "x"), _cuda(out, "out"), _cuda(keys, "keys")
+    if perm is not None:
+        _cuda(perm, "perm")
+    Bx, H, rows, d = x.shape
+    B = n_batch or Bx
+    return capi.ScrambleJob(variant, which, x.data_ptr(), _dtype_code(x), B, H, rows, keys.data_ptr(),
+                            keys.stride(0) if keys.dim() > 1 else 0, key_heads if key_heads is not None else H,
+                            _ptr(perm), perm.stride(0) if perm is not None and perm.dim() > 1 else 0, out.data_ptr(),
+                            _dtype_code(out), out.shape[2], out_row_offset, Bx if B != Bx else 0)
+
+
+def scramble_batch(jobs: Sequence[capi.ScrambleJob], head_dim: int, stream=None) -> None:
+    """K1 for several jobs in one launch (the span's K and V of ship_segment, + its Q in prefill)."""
+    if len(jobs) > capi.MAX_SCRAMBLE_JOBS:
+        raise ValueError(f"at most {capi.MAX_SCRAMBLE_JOBS} jobs")
+    arr = (capi.ScrambleJob * len(jobs))(*jobs)
+    check(capi.LIB.sda_scramble_batch(_stream(stream), head_dim, arr, len(jobs)), "sda_scramble_batch")
+
+
 def partial_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, kv_len: Optional[torch.Tensor] = None,
                       n_splits: Optional[int] = None, out_o: Optional[torch.Tensor] = None,
                       out_stats: Optional[torch.Tensor] = None, stream=None):

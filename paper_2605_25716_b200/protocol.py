@@ -88,10 +88,12 @@ class KVShard:
         if self.rows + L > self.capacity:
             raise ValueError("KV shard capacity exceeded")
         p, _ = keys.span_perms(1, first_pos, L)
-        ops.scramble(k_plain, keys.dev, capi.PHI_INV_T, capi.KEYS_KQ, p, out=self.k, out_row_offset=self.rows,
-                     key_heads=keys.kv_heads, stream=stream)
-        ops.scramble(v_plain, keys.dev, capi.PHI_FORWARD, capi.KEYS_V, p, out=self.v, out_row_offset=self.rows,
-                     key_heads=keys.kv_heads, stream=stream)
+        # K' = K phi_KQ^{-T} and V' = V phi_V, both permuted by p, in one K1 launch
+        ops.scramble_batch([ops.scramble_job(k_plain, keys.dev, capi.PHI_INV_T, capi.KEYS_KQ, p, out=self.k,
+                                             out_row_offset=self.rows, key_heads=keys.kv_heads),
+                            ops.scramble_job(v_plain, keys.dev, capi.PHI_FORWARD, capi.KEYS_V, p, out=self.v,
+                                             out_row_offset=self.rows, key_heads=keys.kv_heads)],
+                           k_plain.shape[3], stream=stream)
         self.rows += L
         self.kv_len.fill_(self.rows)
 

@@ -69,3 +69,30 @@ def test_k1_tc_matches_simt_and_gqa():
     s = _run(x, kd, capi.PHI_FORWARD, capi.KEYS_KQ, perms, rows, 0, simt=True, key_heads=Hkv)
     assert (a == s).mean() > 0.99
     assert np.all(np.abs(a - s) <= 2.0**-7 * np.abs(s) + 1e-5 * np.abs(s).max())
+
+
+def test_scramble_batch_matches_single_jobs():
+    """sda_scramble_batch (three tensor-core jobs sharing one persistent grid: K with phi^-T and
+    V with phi into a cache at a row offset, Q with phi into its own buffer, different row counts
+    and head counts) is bit-identical to the same three sda_scramble calls."""
+    from paper_2605_25716_b200 import capi, ops, protocol
+    H, D, L, LQ, CAP = 4, 128, 640, 384, 1024
+    keys = protocol.DomainKeys([1, 2], 0, 1, H, D, "cuda")
+    g = torch.Generator(device="cuda").manual_seed(5)
+    kx = torch.randn((2, H, L, D), generator=g, device="cuda").to(torch.bfloat16)
+    vx = torch.randn((2, H, L, D), generator=g, device="cuda").to(torch.bfloat16)
+    qx = torch.randn((2, 2 * H, LQ, D), generator=g, device="cuda").to(torch.bfloat16)
+    pkv, _ = keys.span_perms(1, 100, L)
+    pq, _ = keys.span_perms(0, 100 + L, LQ)
+    outs = [torch.zeros((2, H, CAP, D), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    outs += [torch.zeros((2, 2 * H, LQ, D), dtype=torch.bfloat16, device="cuda")]
+    ref = [t.clone() for t in outs]
+    ops.scramble(kx, keys.dev, capi.PHI_INV_T, capi.KEYS_KQ, pkv, out=ref[0], out_row_offset=200, key_heads=H)
+    ops.scramble(vx, keys.dev, capi.PHI_FORWARD, capi.KEYS_V, pkv, out=ref[1], out_row_offset=200, key_heads=H)
+    ops.scramble(qx, keys.dev, capi.PHI_FORWARD, capi.KEYS_KQ, pq, out=ref[2], key_heads=H)
+    ops.scramble_batch([ops.scramble_job(kx, keys.dev, capi.PHI_INV_T, capi.KEYS_KQ, pkv, out=outs[0], out_row_offset=200, key_heads=H),
+                        ops.scramble_job(vx, keys.dev, capi.PHI_FORWARD, capi.KEYS_V, pkv, out=outs[1], out_row_offset=200, key_heads=H),
+                        ops.scramble_job(qx, keys.dev, capi.PHI_FORWARD, capi.KEYS_KQ, pq, out=outs[2], key_heads=H)], D)
+    torch.cuda.synchronize()
+    for a, b in zip(outs, ref):
+        assert torch.equal(a, b)
