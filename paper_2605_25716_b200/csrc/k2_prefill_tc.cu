@@ -79,10 +79,10 @@ constexpr int SMEM = OFF_BAR + NBAR * 8 + 16;
 constexpr int THREADS = 320;
 constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 384;
 // Exponentials per 4 pairs computed on the FMA pipe (tc::exp2_fma2) instead of MUFU.EX2. Measured
-// on C3 with the single-pass softmax: 0 -> 484 us, 1 -> 492 us, 2 -> 526 us (the added FMA-pipe
-// instructions cost more issue time than the MUFU time they free), so it stays off by default.
+// on C3 (exps batched ahead of the packing): 0 -> 489 us, 1 -> 485 us, 2 -> 547 us -- past one in
+// four the added FMA-pipe instructions cost more issue time than the MUFU time they free.
 #ifndef SDA_K2_EMU_OF4
-#define SDA_K2_EMU_OF4 0
+#define SDA_K2_EMU_OF4 1
 #endif
 constexpr int kEmuOf4 = SDA_K2_EMU_OF4;
 }  // namespace k2tc
@@ -275,7 +275,8 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 for (int i = 0; i < 128; ++i)
                     if (i >= valid) s[i] = 0xFF800000u;           // -inf
             }
-            // row max on the raw logits (scale > 0), two new values per 3-input max
+            // row max on the raw logits (scale > 0), two new values per 3-input max (splitting the
+            // TMEM load to overlap the max measured slower)
             float mr0 = -INFINITY, mr1 = -INFINITY;
 #pragma unroll
             for (int i = 0; i < 64; i += 2) {
@@ -308,12 +309,12 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 m_use = m_new;
             }
             const float mu = (m_use == -INFINITY) ? 0.f : m_use;
-            // p = exp2(s * scale - mu): one packed FFMA2 per two logits (a share of the exponentials
-            // on the FMA pipe, exp2_fma2), packed FADD2 row sums
+            // p = exp2(s * scale - mu) in place (one packed FFMA2 per two logits), all 128 first:
+            // the MUFU ops issue back to back instead of each waiting on its consumer; then the row
+            // sum (4 packed FADD2 chains) and the bf16x2 packing of P in place (s[i] <- p[2i], p[2i+1])
             const uint64_t sc2 = tc::f2(p.scale_log2, p.scale_log2), nmu2 = tc::f2(-mu, -mu);
-            uint64_t acc0 = tc::f2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
-            for (int i = 0; i < 64; ++i) {   // P packed in place: s[i] <- bf16x2(p[2i], p[2i+1])
+            for (int i = 0; i < 64; ++i) {
                 float x0, x1;
                 tc::f2_split(tc::ffma2(tc::f2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sc2, nmu2), x0, x1);
                 float p0, p1;
@@ -323,16 +324,24 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                     p0 = ex2(x0);
                     p1 = ex2(x1);
                 }
-                if (i & 1)
-                    acc1 = tc::fadd2(acc1, tc::f2(p0, p1));
-                else
-                    acc0 = tc::fadd2(acc0, tc::f2(p0, p1));
+                s[2 * i] = __float_as_uint(p0);
+                s[2 * i + 1] = __float_as_uint(p1);
+            }
+            uint64_t acc[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) acc[a] = tc::f2(0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                const float p0 = __uint_as_float(s[2 * i]), p1 = __uint_as_float(s[2 * i + 1]);
+                acc[i & 3] = tc::fadd2(acc[i & 3], tc::f2(p0, p1));
                 s[i] = tc::pack_bf16(p0, p1);
             }
-            float a0, a1, b0, b1;
-            tc::f2_split(acc0, a0, a1);
-            tc::f2_split(acc1, b0, b1);
-            l += (a0 + a1) + (b0 + b1);
+            float a0, a1, b0, b1, c0, c1, d0, d1;
+            tc::f2_split(acc[0], a0, a1);
+            tc::f2_split(acc[1], b0, b1);
+            tc::f2_split(acc[2], c0, c1);
+            tc::f2_split(acc[3], d0, d1);
+            l += ((a0 + a1) + (b0 + b1)) + ((c0 + c1) + (d0 + d1));
 #pragma unroll
             for (int c = 0; c < 8; ++c) tc::tmem_st8(s_col + c * 8, s + c * 8);
             tc::tmem_st_wait();
