@@ -47,7 +47,7 @@ typedef enum {
     SDA_ERR_ROLE_VIOLATION = 8    /* protocol.cpp:215-216: compute node asked for its own domain's keys */
 } sda_status;
 
-typedef enum { SDA_BF16 = 0, SDA_F32 = 1 } sda_dtype;
+typedef enum { SDA_BF16 = 0, SDA_F32 = 1, SDA_F64 = 2 /* quantised-wire entry points only */ } sda_dtype;
 
 /* Which transform of phi a scramble applies (scrambler.cpp:75-85). */
 typedef enum {
@@ -281,6 +281,26 @@ sda_status sda_ll_unscramble_merge(void* stream, const void* ll_rec, int32_t n_d
 /* Step tracing: *dst = the GPU's %globaltimer (ns) when this 1-thread kernel runs, in stream
  * order. Not counted by sda_launch_count (instrumentation, not part of a step). */
 sda_status sda_trace_timestamp(void* stream, uint64_t* dst);
+
+/* ------------------------------------------------------------------------------------------
+ * Quantised wire (quant.cpp:26-67; wire_round model.cpp:338-341; gen_quant_bits
+ * protocol.hpp:25-26): per-tensor affine min-max quantisation, 2..8-bit codes packed LSB-first,
+ * bit-exact with quantize_affine / dequantize on the same input values. n_tensors contiguous
+ * tensors of `count` elements each (x, out: [n_tensors][count]); x / out dtype SDA_F32, SDA_F64
+ * or SDA_BF16. scratch: 2 * n_tensors u64 device words. err: optional device i32, set to
+ * SDA_ERR_INVALID_ARGUMENT on a non-finite input value (the reference throws).
+ * ------------------------------------------------------------------------------------------ */
+/* codes of tensor t at codes + t * codes_stride (>= ceil(count * bits / 8) bytes, unused bits 0);
+ * scale[t], zero_point[t] as the reference's QTensor (f32) */
+sda_status sda_quantize_affine(void* stream, const void* x, int32_t x_dtype, int64_t n_tensors, int64_t count,
+                               int32_t bits, uint8_t* codes, int64_t codes_stride, float* scale, float* zero_point,
+                               uint64_t* scratch, int32_t* err);
+sda_status sda_dequantize(void* stream, const uint8_t* codes, int64_t codes_stride, const float* scale,
+                          const float* zero_point, int64_t n_tensors, int64_t count, int32_t bits, void* out,
+                          int32_t out_dtype);
+/* x <- dequantize(quantize_affine(x, bits)) per tensor, in place (the wire emulation) */
+sda_status sda_quant_roundtrip(void* stream, void* x, int32_t dtype, int64_t n_tensors, int64_t count, int32_t bits,
+                               uint64_t* scratch, int32_t* err);
 
 /* ------------------------------------------------------------------------------------------
  * Misc

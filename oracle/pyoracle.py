@@ -205,6 +205,26 @@ class Oracle:
         return merged
 
 
+    # --- quantised wire (quant.cpp:26-67) ---------------------------------------
+    def quantize_affine(self, v, bits: int):
+        """-> (codes uint8 [ceil(n*bits/8)], scale f32, zero_point f32)."""
+        v = np.ascontiguousarray(v, np.float64).ravel()
+        codes = np.zeros((v.size * bits + 7) // 8, np.uint8)
+        sc, zp = ct.c_float(0.0), ct.c_float(0.0)
+        fn = self.lib.ref_quantize_affine if self.is_ref else self.lib.or_quantize_affine
+        if fn(_pd_(v), _sz(v.size), ct.c_int(bits), codes.ctypes.data_as(ct.POINTER(ct.c_uint8)), ct.byref(sc),
+              ct.byref(zp)):
+            raise OracleError("quantize_affine")
+        return codes, np.float32(sc.value), np.float32(zp.value)
+
+    def dequantize(self, codes, n: int, bits: int, scale, zero_point) -> np.ndarray:
+        codes = np.ascontiguousarray(codes, np.uint8)
+        out = np.zeros(n, np.float64)
+        fn = self.lib.ref_dequantize if self.is_ref else self.lib.or_dequantize
+        fn(codes.ctypes.data_as(ct.POINTER(ct.c_uint8)), _sz(n), ct.c_int(bits), ct.c_float(float(scale)),
+           ct.c_float(float(zero_point)), _pd_(out))
+        return out
+
     # --- composition ----------------------------------------------------------
     def scrambled_step(self, shared_seed_: int, request_id: int, layer: int, n_heads: int, head: int, q,
                        q_first_pos: int, k_nodes, v_nodes, wire_fmt: int = FMT_F64, lo: float = 0.125,

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "sdattn/attention.hpp"
+#include "sdattn/quant.hpp"
 #include "sdattn/float_format.hpp"
 #include "sdattn/fwht.hpp"
 #include "sdattn/model.hpp"
@@ -346,6 +347,31 @@ double ref_bench_decode(std::size_t n_pairs, std::size_t n_nodes, std::size_t lk
     }
     std::sort(times.begin(), times.end());
     return times[times.size() / 2];
+}
+
+// quant.cpp:26-67 through the reference's own quantize_affine / dequantize
+int ref_quantize_affine(const double* v, std::size_t n, int bits, std::uint8_t* codes, float* scale,
+                        float* zero_point) {
+    try {
+        const QTensor q = quantize_affine(std::span<const double>(v, n), bits);
+        std::memcpy(codes, q.codes.data(), q.codes.size());
+        *scale = q.scale;
+        *zero_point = q.zero_point;
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+void ref_dequantize(const std::uint8_t* codes, std::size_t n, int bits, float scale, float zero_point, double* out) {
+    QTensor q;
+    q.bits = bits;
+    q.count = n;
+    q.codes.assign(codes, codes + (n * static_cast<std::size_t>(bits) + 7) / 8);
+    q.scale = scale;
+    q.zero_point = zero_point;
+    const std::vector<double> r = dequantize(q);
+    std::memcpy(out, r.data(), n * sizeof(double));
 }
 
 }  // extern "C"

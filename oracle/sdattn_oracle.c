@@ -360,3 +360,46 @@ int or_dec_output(const double* o_s, const double* rmax_s, const double* esum_s,
     free(tmp);
     return 0;
 }
+
+/* quant.cpp:26-51 -- per-tensor affine min-max quantisation, codes packed LSB-first.
+ * codes: ceil(n * bits / 8) zero-initialised bytes. Returns -1 for bits outside [2, 8]
+ * (quant.cpp:27) or a non-finite value (quant.cpp:35). */
+int or_quantize_affine(const double* v, size_t n, int bits, uint8_t* codes, float* scale, float* zero_point) {
+    if (bits < 2 || bits > 8) return -1;
+    memset(codes, 0, (n * (size_t)bits + 7) / 8);
+    *scale = 0.0f;
+    *zero_point = 0.0f;
+    if (n == 0) return 0;
+    double lo = v[0], hi = v[0];
+    for (size_t i = 0; i < n; ++i) {
+        if (!isfinite(v[i])) return -1;
+        if (v[i] < lo) lo = v[i];
+        if (v[i] > hi) hi = v[i];
+    }
+    const uint32_t levels = (1u << bits) - 1u;
+    *zero_point = (float)lo;
+    *scale = (float)((hi - lo) / (double)levels);
+    if (*scale == 0.0f) return 0;   /* constant tensor: all codes 0 */
+    const double inv = 1.0 / (double)*scale;
+    for (size_t i = 0; i < n; ++i) {
+        double c = nearbyint((v[i] - (double)*zero_point) * inv);
+        if (c < 0.0) c = 0.0;
+        if (c > (double)levels) c = (double)levels;
+        const uint32_t code = (uint32_t)c;
+        uint64_t bit = (uint64_t)i * (uint64_t)bits;
+        for (int b = 0; b < bits; ++b, ++bit)
+            if (code & (1u << b)) codes[bit / 8] |= (uint8_t)(1u << (bit % 8));
+    }
+    return 0;
+}
+
+/* quant.cpp:55-61 -- value = code * scale + zero_point in f64 */
+void or_dequantize(const uint8_t* codes, size_t n, int bits, float scale, float zero_point, double* out) {
+    for (size_t i = 0; i < n; ++i) {
+        uint32_t code = 0;
+        uint64_t bit = (uint64_t)i * (uint64_t)bits;
+        for (int b = 0; b < bits; ++b, ++bit)
+            if (codes[bit / 8] & (1u << (bit % 8))) code |= 1u << b;
+        out[i] = (double)code * (double)scale + (double)zero_point;
+    }
+}

@@ -122,6 +122,10 @@ int or_dec_output(const double* o_s, const double* row_max_s, const double* exp_
                   size_t lq, const or_scrambler* phi_v, const uint32_t* p_q, double* out,
                   double* row_max, double* exp_sum);
 
+/* quant.cpp:26-67 */
+int or_quantize_affine(const double* v, size_t n, int bits, uint8_t* codes, float* scale, float* zero_point);
+void or_dequantize(const uint8_t* codes, size_t n, int bits, float scale, float zero_point, double* out);
+
 #ifdef __cplusplus
 }
 #endif

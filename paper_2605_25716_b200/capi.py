@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SDA_LIB_PATH") or os.path.join(HERE, "libsdattn_b200.so")   # override: kernel-variant experiments
 
 SDA_OK = 0
-SDA_BF16, SDA_F32 = 0, 1
+SDA_BF16, SDA_F32, SDA_F64 = 0, 1, 2
 PHI_FORWARD, PHI_INV_T, PHI_INV = 0, 1, 2
 KEYS_KQ, KEYS_V = 0, 1
 MODE_S1_AND_S2, MODE_S1_ONLY = 0, 1
@@ -30,7 +30,8 @@ EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_
            "sda_partial_attention", "sda_partial_attention_causal", "sda_default_splits", "sda_default_splits_gqa", "sda_unscramble_merge", "sda_abi_version",
            "sda_status_string", "sda_launch_count", "sda_ipc_get_handle", "sda_ipc_open_handle",
            "sda_ipc_close_handle", "sda_exchange_epoch", "sda_exchange_push", "sda_exchange_wait",
-           "sda_ll_scramble_q", "sda_ll_partial_attention", "sda_ll_unscramble_merge", "sda_trace_timestamp", "sda_scramble_batch")
+           "sda_ll_scramble_q", "sda_ll_partial_attention", "sda_ll_unscramble_merge", "sda_trace_timestamp", "sda_scramble_batch",
+           "sda_quantize_affine", "sda_dequantize", "sda_quant_roundtrip")
 
 
 class SdaError(RuntimeError):
@@ -120,6 +121,10 @@ def _load() -> ct.CDLL:
                                             ct.c_int32, ct.c_int32, _vp, ct.c_int32, _vp, _vp]
     lib.sda_trace_timestamp.argtypes = [_vp, _vp]
     lib.sda_scramble_batch.argtypes = [_vp, ct.c_int32, ct.POINTER(ScrambleJob), ct.c_int32]
+    lib.sda_quantize_affine.argtypes = [_vp, _vp, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32, _vp, ct.c_int64,
+                                        _vp, _vp, _vp, _vp]
+    lib.sda_dequantize.argtypes = [_vp, _vp, ct.c_int64, _vp, _vp, ct.c_int64, ct.c_int64, ct.c_int32, _vp, ct.c_int32]
+    lib.sda_quant_roundtrip.argtypes = [_vp, _vp, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32, _vp, _vp]
     lib.sda_abi_version.restype = ct.c_int32
     lib.sda_status_string.restype = ct.c_char_p
     lib.sda_status_string.argtypes = [ct.c_int32]

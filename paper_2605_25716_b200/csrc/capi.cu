@@ -126,6 +126,52 @@ sda_status sda_scramble_batch(void* stream, int32_t head_dim, const sda_scramble
     return SDA_OK;
 }
 
+// ------------------------------------------------------------------------------------------ quant wire
+static bool quant_dtype_ok(int t) { return t == SDA_BF16 || t == SDA_F32 || t == SDA_F64; }
+
+sda_status sda_quantize_affine(void* stream, const void* x, int32_t x_dtype, int64_t n_tensors, int64_t count,
+                               int32_t bits, uint8_t* codes, int64_t codes_stride, float* scale, float* zero_point,
+                               uint64_t* scratch, int32_t* err) {
+    if (bits < 2 || bits > 8) return SDA_ERR_INVALID_ARGUMENT;   // quant.cpp:27
+    if (n_tensors < 0 || count < 0 || !quant_dtype_ok(x_dtype) || n_tensors > 65535) return SDA_ERR_INVALID_ARGUMENT;
+    if (n_tensors == 0) return SDA_OK;
+    if (!x || !codes || !scale || !zero_point || !scratch || codes_stride < (count * bits + 7) / 8)
+        return SDA_ERR_INVALID_ARGUMENT;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (count == 0) {   // empty tensor: scale 0, zero point 0, no codes (quant.cpp:33)
+        cudaError_t e = cudaMemsetAsync(scale, 0, n_tensors * 4, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(zero_point, 0, n_tensors * 4, st);
+        return from_cuda(e);
+    }
+    g_launches += 2;
+    return from_cuda(sda::launch_quantize(x, x_dtype, n_tensors, count, bits, codes, codes_stride, scale, zero_point,
+                                          reinterpret_cast<unsigned long long*>(scratch), err, st));
+}
+
+sda_status sda_dequantize(void* stream, const uint8_t* codes, int64_t codes_stride, const float* scale,
+                          const float* zero_point, int64_t n_tensors, int64_t count, int32_t bits, void* out,
+                          int32_t out_dtype) {
+    if (bits < 2 || bits > 8) return SDA_ERR_INVALID_ARGUMENT;
+    if (n_tensors < 0 || count < 0 || !quant_dtype_ok(out_dtype) || n_tensors > 65535) return SDA_ERR_INVALID_ARGUMENT;
+    if (n_tensors == 0 || count == 0) return SDA_OK;
+    if (!codes || !scale || !zero_point || !out || codes_stride < (count * bits + 7) / 8) return SDA_ERR_INVALID_ARGUMENT;
+    ++g_launches;
+    return from_cuda(sda::launch_dequantize(codes, codes_stride, scale, zero_point, n_tensors, count, bits, out,
+                                            out_dtype, static_cast<cudaStream_t>(stream)));
+}
+
+sda_status sda_quant_roundtrip(void* stream, void* x, int32_t dtype, int64_t n_tensors, int64_t count, int32_t bits,
+                               uint64_t* scratch, int32_t* err) {
+    if (bits < 2 || bits > 8) return SDA_ERR_INVALID_ARGUMENT;
+    if (n_tensors < 0 || count < 0 || !quant_dtype_ok(dtype) || n_tensors > 65535) return SDA_ERR_INVALID_ARGUMENT;
+    if (n_tensors == 0 || count == 0) return SDA_OK;
+    if (!x || !scratch) return SDA_ERR_INVALID_ARGUMENT;
+    g_launches += 2;
+    return from_cuda(sda::launch_quant_roundtrip(x, dtype, n_tensors, count, bits,
+                                                 reinterpret_cast<unsigned long long*>(scratch), err,
+                                                 static_cast<cudaStream_t>(stream)));
+}
+
 int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int64_t kv_cap) {
     if (n_batch <= 0 || q_heads <= 0 || q_rows <= 0 || kv_cap <= 0) return 1;
     if (q_rows >= 64) {

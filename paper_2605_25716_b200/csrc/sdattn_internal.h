@@ -106,6 +106,13 @@ namespace sda {
 cudaError_t launch_k1(const K1Params& p, int d, int xdt, int odt, int64_t n_batch, cudaStream_t st);
 bool k1_tc_eligible(const K1Params& p, int d, int xdt, int odt);
 cudaError_t launch_k1_tc(const K1Params& p, int d, int64_t n_batch, cudaStream_t st);
+cudaError_t launch_quantize(const void* x, int dt, int64_t n, int64_t count, int bits, uint8_t* codes,
+                            int64_t codes_stride, float* scale, float* zero, unsigned long long* scratch, int32_t* err,
+                            cudaStream_t st);
+cudaError_t launch_dequantize(const uint8_t* codes, int64_t codes_stride, const float* scale, const float* zero,
+                              int64_t n, int64_t count, int bits, void* out, int dt, cudaStream_t st);
+cudaError_t launch_quant_roundtrip(void* x, int dt, int64_t n, int64_t count, int bits, unsigned long long* scratch,
+                                   int32_t* err, cudaStream_t st);
 cudaError_t launch_k1_tc_multi(const K1Params* p, const int64_t* n_batch, int n_jobs, int d, cudaStream_t st);
 cudaError_t launch_k2_decode(const K2Params& p, int d, int qdt, int kvdt, cudaStream_t st);
 bool k2_prefill_tc_eligible(const K2Params& p, int d, int qdt, int kvdt);

@@ -20,6 +20,7 @@ from . import capi
 from .capi import check
 
 _DT = {torch.bfloat16: capi.SDA_BF16, torch.float32: capi.SDA_F32}
+_DT_Q = {**_DT, torch.float64: capi.SDA_F64}   # f64: quantised-wire entry points only
 
 
 def _dtype_code(t: torch.Tensor) -> int:
@@ -200,3 +201,48 @@ def unscramble_merge(sources: Sequence[MergeSource], out: Optional[torch.Tensor]
                                         out_batch_stride),
           "sda_unscramble_merge")
     return out
+
+
+# --- quantised wire (quant.cpp:26-67) -------------------------------------------------------------
+def quantize_affine(x: torch.Tensor, bits: int, err: Optional[torch.Tensor] = None, stream=None):
+    """x [n, count] (f32 / f64 / bf16; each row one tensor) -> (codes uint8 [n, ceil(count*bits/8)],
+    scale f32 [n], zero_point f32 [n]); bit-exact with quantize_affine on the same values."""
+    _cuda(x, "x")
+    if x.dim() != 2 or x.dtype not in _DT_Q:
+        raise ValueError("x must be [n_tensors, count] f32 / f64 / bf16")
+    x = x.contiguous()
+    n, count = x.shape
+    nb = (count * bits + 7) // 8
+    codes = torch.zeros((n, max(nb, 1)), dtype=torch.uint8, device=x.device)
+    scale = torch.empty(n, dtype=torch.float32, device=x.device)
+    zp = torch.empty(n, dtype=torch.float32, device=x.device)
+    scratch = torch.empty(2 * max(n, 1), dtype=torch.int64, device=x.device)
+    check(capi.LIB.sda_quantize_affine(_stream(stream), x.data_ptr(), _DT_Q[x.dtype], n, count, bits, codes.data_ptr(),
+                                       codes.stride(0), scale.data_ptr(), zp.data_ptr(), scratch.data_ptr(), _ptr(err)),
+          "sda_quantize_affine")
+    return codes[:, :nb], scale, zp
+
+
+def dequantize(codes: torch.Tensor, scale: torch.Tensor, zero_point: torch.Tensor, count: int, bits: int,
+               out_dtype: torch.dtype = torch.float64, stream=None) -> torch.Tensor:
+    """codes uint8 [n, >= ceil(count*bits/8)] -> values [n, count] (value = code * scale + zero_point)."""
+    _cuda(codes, "codes")
+    n = codes.shape[0]
+    out = torch.empty((n, count), dtype=out_dtype, device=codes.device)
+    check(capi.LIB.sda_dequantize(_stream(stream), codes.data_ptr(), codes.stride(0), scale.data_ptr(),
+                                  zero_point.data_ptr(), n, count, bits, out.data_ptr(), _DT_Q[out_dtype]),
+          "sda_dequantize")
+    return out
+
+
+def quant_roundtrip(x: torch.Tensor, bits: int, err: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """In place: x[t] <- dequantize(quantize_affine(x[t], bits)) for every row t of x [n, count]
+    (the quantised-wire emulation of wire_round, model.cpp:338-341)."""
+    _cuda(x, "x")
+    if x.dim() != 2 or not x.is_contiguous() or x.dtype not in _DT_Q:
+        raise ValueError("x must be a contiguous [n_tensors, count] f32 / f64 / bf16 tensor")
+    n, count = x.shape
+    scratch = torch.empty(2 * max(n, 1), dtype=torch.int64, device=x.device)
+    check(capi.LIB.sda_quant_roundtrip(_stream(stream), x.data_ptr(), _DT_Q[x.dtype], n, count, bits,
+                                       scratch.data_ptr(), _ptr(err)), "sda_quant_roundtrip")
+    return x
