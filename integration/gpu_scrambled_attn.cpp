@@ -83,12 +83,18 @@ std::vector<uint32_t> span_perm(uint64_t tps, uint64_t tag, uint64_t first, size
 }  // namespace
 
 sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt) {
-    if (opt.quant_bits > 0 || opt.wire_fmt == sdattn::FloatFormat::f16)
-        throw std::invalid_argument("gpu_scrambled_attn: f16 / quantised wire not supported");
-    const int dt = opt.wire_fmt == sdattn::FloatFormat::bf16 ? SDA_BF16 : SDA_F32;
+    if (opt.wire_fmt == sdattn::FloatFormat::f16 && opt.quant_bits <= 0)
+        throw std::invalid_argument("gpu_scrambled_attn: f16 wire not supported");
+    if (opt.quant_bits > 0 && (opt.quant_bits < 2 || opt.quant_bits > 8))
+        throw std::invalid_argument("quantize_affine: bits must be in [2, 8]");
+    // quantised wire (wire_round, model.cpp:338-341): Q', K', V', O' travel as per-tensor affine
+    // codes -> scrambled in f32, then quantised and dequantised in place on the device; the
+    // normalisation scalars ride at f32 (wire_round_stat, model.cpp:343-348)
+    const int qbits = opt.quant_bits > 0 ? opt.quant_bits : 0;
+    const int dt = (opt.wire_fmt == sdattn::FloatFormat::bf16 && !qbits) ? SDA_BF16 : SDA_F32;
     const size_t esz = dt == SDA_BF16 ? 2 : 4;
     auto keys = std::make_shared<std::map<std::pair<size_t, size_t>, HeadKeys>>();
-    return [opt, dt, esz, keys](const sdattn::AttnRequest& req) -> sdattn::Matrix {
+    return [opt, dt, esz, keys, qbits](const sdattn::AttnRequest& req) -> sdattn::Matrix {
         const size_t d = req.q->cols, lq = req.q->rows, lk = req.k->rows;
         if (d != 32 && d != 64 && d != 128 && d != 256)
             throw std::invalid_argument("gpu_scrambled_attn: head dim must be 32, 64, 128 or 256");
@@ -106,6 +112,15 @@ sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt) {
         ck(sda_scramble(st, SDA_PHI_FORWARD, SDA_KEYS_KQ, q32->p, SDA_F32, 1, 1, (int64_t)lq, (int)d, hk.image->p, 0, 1,
                         pq_d->as<uint32_t>(), 0, q_s.p, dt, (int64_t)lq, 0, 0),
            "scramble Q");
+        DevBuf qscratch(16), qerr(4);
+        ckc(cudaMemset(qerr.p, 0, 4), "memset");
+        auto wire = [&](void* x, size_t count) {   // the quantised wire, one tensor
+            if (qbits)
+                ck(sda_quant_roundtrip(st, x, SDA_F32, 1, (int64_t)count, qbits, qscratch.as<uint64_t>(),
+                                       qerr.as<int32_t>()),
+                   "quant roundtrip");
+        };
+        wire(q_s.p, lq * d);
 
         std::vector<std::unique_ptr<DevBuf>> keep;
         std::vector<sda_merge_source> src;
@@ -122,10 +137,13 @@ sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt) {
             ck(sda_scramble(st, SDA_PHI_FORWARD, SDA_KEYS_V, v32->p, SDA_F32, 1, 1, (int64_t)L, (int)d, hk.image->p, 0, 1,
                             pkv->as<uint32_t>(), 0, vs->p, dt, (int64_t)L, 0, 0),
                "scramble V");
+            wire(ks->p, L * d);
+            wire(vs->p, L * d);
             auto o = std::make_unique<DevBuf>(lq * d * 4), s = std::make_unique<DevBuf>(lq * 2 * 4);
             ck(sda_partial_attention(st, q_s.p, dt, ks->p, vs->p, dt, (int64_t)L, nullptr, 1, 1, 1, (int64_t)lq, (int)d, 1,
                                      o->as<float>(), s->as<float>()),
                "partial attention");
+            wire(o->p, lq * d);   // O' of the shard (one split); stats stay f32
             src.push_back({o->as<float>(), s->as<float>(), hk.image->p, pq_inv_d->as<uint32_t>(), 0});
             keep.push_back(std::move(ks));
             keep.push_back(std::move(vs));
@@ -158,6 +176,8 @@ sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt) {
         ckc(cudaMemcpy(h.data(), out.p, h.size() * 4, cudaMemcpyDeviceToHost), "D2H");
         ckc(cudaMemcpy(&e, err.p, 4, cudaMemcpyDeviceToHost), "D2H");
         if (e == SDA_ERR_MASKED_ROW) throw std::invalid_argument("merge_shards: row masked in every shard");
+        ckc(cudaMemcpy(&e, qerr.p, 4, cudaMemcpyDeviceToHost), "D2H");
+        if (e != 0) throw std::invalid_argument("quantize_affine: non-finite value");
         return sdattn::Matrix(lq, d, std::vector<double>(h.begin(), h.end()));
     };
 }

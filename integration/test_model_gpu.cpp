@@ -67,6 +67,24 @@ int main() {
         const Matrix ref_b = run(scrambled_attn(bopt));   // the reference's own bf16-wire emulation
         const double dev_b = max_abs_diff(gpu_b, ref_b) / std::max(1e-12, frobenius_norm(ref_b) / std::sqrt((double)ref_b.data.size()));
         check(dev_b < 0.5, "gpu (BF16 mode) vs reference scrambled_attn(bf16 wire), max|diff|/rms", dev_b);
+        // quantised wire (8 and 4 bits): Q', K', V', O' quantised per tensor on the device
+        for (int qb : {8, 4}) {
+            ScrambledAttnOptions qopt;
+            qopt.quant_bits = qb;
+            const Matrix gpu_q = run(sdattn_b200::gpu_scrambled_attn(qopt));
+            const Matrix ref_q = run(scrambled_attn(qopt));
+            const double rms = std::max(1e-12, frobenius_norm(ref_q) / std::sqrt((double)ref_q.data.size()));
+            const double dev_q = max_abs_diff(gpu_q, ref_q) / rms;
+            const double dev_qc = max_abs_diff(ref_q, want) / rms;   // the quantisation error itself
+            char what[128];
+            std::snprintf(what, sizeof what, "gpu vs reference scrambled_attn(quant %d), max|diff|/rms (quant error %.3g)",
+                          qb, dev_qc);
+            // the quantisation itself is bit-exact on identical values (tests/test_gpu_quant.py);
+            // here Q', K', V' reach it as f32 device values rather than the oracle's f64, so a
+            // value on a code boundary can land one step away -- the end-to-end difference must
+            // stay well inside the wire's own error
+            check(dev_q < 0.5 * dev_qc, what, dev_q);
+        }
 
         // test_model.cpp:112-129 -- greedy decode is token-identical
         const Model m2 = init_model(decoder(10, hd));
