@@ -44,7 +44,8 @@ typedef enum {
     SDA_ERR_UNSUPPORTED = 5,      /* valid for the reference but not compiled for the device (e.g. d not in {32,64,128,256}) */
     SDA_ERR_CUDA = 6,             /* a CUDA runtime error (launch / config) */
     SDA_ERR_NO_DEVICE = 7,        /* no sm_100 device visible */
-    SDA_ERR_ROLE_VIOLATION = 8    /* protocol.cpp:215-216: compute node asked for its own domain's keys */
+    SDA_ERR_ROLE_VIOLATION = 8,   /* protocol.cpp:215-216: compute node asked for its own domain's keys */
+    SDA_ERR_FRAME = 9             /* FrameError: bad magic / truncated / inconsistent length / CRC mismatch (frame.cpp:138-164) */
 } sda_status;
 
 typedef enum { SDA_BF16 = 0, SDA_F32 = 1, SDA_F64 = 2 /* quantised-wire entry points only */ } sda_dtype;
@@ -301,6 +302,44 @@ sda_status sda_dequantize(void* stream, const uint8_t* codes, int64_t codes_stri
 /* x <- dequantize(quantize_affine(x, bits)) per tensor, in place (the wire emulation) */
 sda_status sda_quant_roundtrip(void* stream, void* x, int32_t dtype, int64_t n_tensors, int64_t count, int32_t bits,
                                uint64_t* scratch, int32_t* err);
+
+/* ------------------------------------------------------------------------------------------
+ * Wire frames on the device ("FATN", frame.hpp:48-92): encode a device tensor into the
+ * reference's bit-exact frame bytes, CRC-32 included, and decode one back.
+ *   dtype: the reference's DtypeCode -- 0 f64, 1 f32, 2 bf16, 3 f16, 16+N quantN (N = 2..8).
+ *   Tensor frames (make_tensor_frame) carry dims {n_tensors, rows, cols}; any dims (<= 8) work.
+ * ------------------------------------------------------------------------------------------ */
+#define SDA_FRAME_MAX_DIMS 8
+typedef struct {
+    uint8_t version;      /* 1 */
+    uint8_t msg_type;     /* MsgType: 2 SCR_KV, 3 SCR_Q, 4 SCR_SHARD, ... */
+    uint64_t request_id;
+    uint16_t layer, head, domain;
+    uint8_t dtype;        /* DtypeCode */
+    uint32_t n_dims;
+    uint32_t dims[SDA_FRAME_MAX_DIMS];
+} sda_frame_header;
+/* element count (0 without dims), payload bytes (dtype_payload_size, frame.cpp:63-75), whole frame
+ * (encoded_size, frame.cpp:134-136), device scratch for sda_frame_encode / _decode / sda_crc32 */
+uint64_t sda_frame_elements(const sda_frame_header* h);
+uint64_t sda_frame_payload_bytes(const sda_frame_header* h);
+uint64_t sda_frame_bytes(const sda_frame_header* h);
+uint64_t sda_frame_scratch_bytes(uint64_t frame_bytes);
+/* payload_from_values + encode_frame: x (device, x_dtype SDA_F32 / SDA_F64 / SDA_BF16, the
+ * frame's elements in order) -> out (device, sda_frame_bytes(h) bytes). err: optional device
+ * i32, SDA_ERR_INVALID_ARGUMENT on a non-finite value for a quantN frame. */
+sda_status sda_frame_encode(void* stream, const sda_frame_header* h, const void* x, int32_t x_dtype, uint8_t* out,
+                            void* scratch, int32_t* err);
+/* host: the header fields and length checks of decode_frame (magic, truncation, payload length,
+ * frame.cpp:138-158) from the first bytes of a frame (size = the whole frame's length) */
+sda_status sda_frame_parse_header(const uint8_t* host_bytes, uint64_t host_len, uint64_t frame_size,
+                                  sda_frame_header* out);
+/* decode_frame's CRC check + values_from_payload: frame (device, frame_size bytes, header h as
+ * parsed) -> out (device, out_dtype). A CRC mismatch sets *err = SDA_ERR_FRAME. */
+sda_status sda_frame_decode(void* stream, const uint8_t* frame, uint64_t frame_size, const sda_frame_header* h,
+                            void* out, int32_t out_dtype, void* scratch, int32_t* err);
+/* CRC-32/IEEE of len device bytes (crc32, frame.cpp:78-83) -> out4 (device, little-endian) */
+sda_status sda_crc32(void* stream, const uint8_t* bytes, uint64_t len, void* scratch, uint8_t* out4);
 
 /* ------------------------------------------------------------------------------------------
  * Misc

@@ -225,6 +225,39 @@ class Oracle:
            ct.c_float(float(zero_point)), _pd_(out))
         return out
 
+    # --- wire frames (frame.cpp) ------------------------------------------------------
+    def crc32(self, b) -> int:
+        b = np.ascontiguousarray(b, np.uint8)
+        fn = self.lib.ref_crc32 if self.is_ref else self.lib.or_crc32
+        fn.restype = ct.c_uint32
+        return int(fn(b.ctypes.data_as(ct.POINTER(ct.c_uint8)), _sz(b.size)))
+
+    def encode_frame(self, msg_type: int, request_id: int, layer: int, head: int, domain: int, dtype: int, dims,
+                     values) -> np.ndarray:
+        """make_tensor_frame-style frame of `values` (reference only)."""
+        v = np.ascontiguousarray(values, np.float64).ravel()
+        d = np.ascontiguousarray(dims, np.uint32)
+        cap = 64 + 4 * d.size + 8 * max(v.size, 1) + 16
+        out = np.zeros(cap, np.uint8)
+        n = ct.c_uint64(0)
+        rc = self.lib.ref_encode_frame(ct.c_uint8(msg_type), _u64(request_id), ct.c_uint16(layer), ct.c_uint16(head),
+                                       ct.c_uint16(domain), ct.c_uint8(dtype), d.ctypes.data_as(ct.POINTER(ct.c_uint32)),
+                                       ct.c_uint32(d.size), _pd_(v), out.ctypes.data_as(ct.POINTER(ct.c_uint8)),
+                                       _u64(cap), ct.byref(n))
+        if rc:
+            raise OracleError(f"encode_frame rc={rc}")
+        return out[:n.value].copy()
+
+    def decode_frame(self, b, cap: int) -> np.ndarray:
+        """decode_frame + values_from_payload (reference only); raises on FrameError."""
+        b = np.ascontiguousarray(b, np.uint8)
+        out = np.zeros(max(cap, 1), np.float64)
+        self.lib.ref_decode_frame.restype = ct.c_longlong
+        n = self.lib.ref_decode_frame(b.ctypes.data_as(ct.POINTER(ct.c_uint8)), _u64(b.size), _pd_(out), _u64(cap))
+        if n < 0:
+            raise OracleError(f"decode_frame rc={n}")
+        return out[:n]
+
     # --- composition ----------------------------------------------------------
     def scrambled_step(self, shared_seed_: int, request_id: int, layer: int, n_heads: int, head: int, q,
                        q_first_pos: int, k_nodes, v_nodes, wire_fmt: int = FMT_F64, lo: float = 0.125,

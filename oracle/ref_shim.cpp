@@ -19,6 +19,7 @@
 
 #include "sdattn/attention.hpp"
 #include "sdattn/quant.hpp"
+#include "sdattn/frame.hpp"
 #include "sdattn/float_format.hpp"
 #include "sdattn/fwht.hpp"
 #include "sdattn/model.hpp"
@@ -372,6 +373,47 @@ void ref_dequantize(const std::uint8_t* codes, std::size_t n, int bits, float sc
     q.zero_point = zero_point;
     const std::vector<double> r = dequantize(q);
     std::memcpy(out, r.data(), n * sizeof(double));
+}
+
+// frame.cpp: make a tensor frame from values (payload_from_values) and encode it
+int ref_encode_frame(std::uint8_t msg_type, std::uint64_t request_id, std::uint16_t layer, std::uint16_t head,
+                     std::uint16_t domain, std::uint8_t dtype, const std::uint32_t* dims, std::uint32_t n_dims,
+                     const double* values, std::uint8_t* out, std::uint64_t cap, std::uint64_t* out_len) {
+    try {
+        Frame f;
+        f.msg_type = static_cast<MsgType>(msg_type);
+        f.request_id = request_id;
+        f.layer = layer;
+        f.head = head;
+        f.domain = domain;
+        f.dtype = static_cast<DtypeCode>(dtype);
+        f.dims.assign(dims, dims + n_dims);
+        f.payload = payload_from_values(std::span<const double>(values, f.element_count()), f.dtype);
+        const std::vector<std::uint8_t> b = encode_frame(f);
+        *out_len = b.size();
+        if (b.size() > cap) return -2;
+        std::memcpy(out, b.data(), b.size());
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// frame.cpp: decode_frame + values_from_payload; returns the element count or -1 (FrameError)
+long long ref_decode_frame(const std::uint8_t* bytes, std::uint64_t n, double* values, std::uint64_t cap) {
+    try {
+        const Frame f = decode_frame(std::span<const std::uint8_t>(bytes, n));
+        const std::vector<double> v = values_from_payload(f.payload, f.element_count(), f.dtype);
+        if (v.size() > cap) return -2;
+        std::memcpy(values, v.data(), v.size() * sizeof(double));
+        return static_cast<long long>(v.size());
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+std::uint32_t ref_crc32(const std::uint8_t* bytes, std::uint64_t n) {
+    return crc32(std::span<const std::uint8_t>(bytes, n));
 }
 
 }  // extern "C"

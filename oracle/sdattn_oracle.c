@@ -403,3 +403,13 @@ void or_dequantize(const uint8_t* codes, size_t n, int bits, float scale, float 
         out[i] = (double)code * (double)scale + (double)zero_point;
     }
 }
+
+/* frame.cpp:17-25, :78-83 -- CRC-32/IEEE (reflected, poly 0xEDB88320, init and final xor ~0) */
+uint32_t or_crc32(const uint8_t* b, size_t n) {
+    uint32_t c = 0xFFFFFFFFu;
+    for (size_t i = 0; i < n; ++i) {
+        c ^= b[i];
+        for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+    }
+    return c ^ 0xFFFFFFFFu;
+}

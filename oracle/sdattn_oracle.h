@@ -126,6 +126,9 @@ int or_dec_output(const double* o_s, const double* row_max_s, const double* exp_
 int or_quantize_affine(const double* v, size_t n, int bits, uint8_t* codes, float* scale, float* zero_point);
 void or_dequantize(const uint8_t* codes, size_t n, int bits, float scale, float zero_point, double* out);
 
+/* frame.cpp:78-83 */
+uint32_t or_crc32(const uint8_t* b, size_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,7 +31,9 @@ EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_
            "sda_status_string", "sda_launch_count", "sda_ipc_get_handle", "sda_ipc_open_handle",
            "sda_ipc_close_handle", "sda_exchange_epoch", "sda_exchange_push", "sda_exchange_wait",
            "sda_ll_scramble_q", "sda_ll_partial_attention", "sda_ll_unscramble_merge", "sda_trace_timestamp", "sda_scramble_batch",
-           "sda_quantize_affine", "sda_dequantize", "sda_quant_roundtrip")
+           "sda_quantize_affine", "sda_dequantize", "sda_quant_roundtrip",
+           "sda_frame_elements", "sda_frame_payload_bytes", "sda_frame_bytes", "sda_frame_scratch_bytes",
+           "sda_frame_encode", "sda_frame_parse_header", "sda_frame_decode", "sda_crc32")
 
 
 class SdaError(RuntimeError):
@@ -68,6 +70,15 @@ class ScrambleJob(ct.Structure):
 
 
 MAX_SCRAMBLE_JOBS = 3
+SDA_ERR_FRAME = 9
+FRAME_MAX_DIMS = 8
+
+
+class FrameHeader(ct.Structure):
+    """sda_frame_header (frame.hpp:48-66)."""
+    _fields_ = [("version", ct.c_uint8), ("msg_type", ct.c_uint8), ("request_id", ct.c_uint64), ("layer", ct.c_uint16),
+                ("head", ct.c_uint16), ("domain", ct.c_uint16), ("dtype", ct.c_uint8), ("n_dims", ct.c_uint32),
+                ("dims", ct.c_uint32 * FRAME_MAX_DIMS)]
 
 
 class MergeSource(ct.Structure):
@@ -121,6 +132,16 @@ def _load() -> ct.CDLL:
                                             ct.c_int32, ct.c_int32, _vp, ct.c_int32, _vp, _vp]
     lib.sda_trace_timestamp.argtypes = [_vp, _vp]
     lib.sda_scramble_batch.argtypes = [_vp, ct.c_int32, ct.POINTER(ScrambleJob), ct.c_int32]
+    _ph = ct.POINTER(FrameHeader)
+    for f in ("sda_frame_elements", "sda_frame_payload_bytes", "sda_frame_bytes"):
+        getattr(lib, f).restype = ct.c_uint64
+        getattr(lib, f).argtypes = [_ph]
+    lib.sda_frame_scratch_bytes.restype = ct.c_uint64
+    lib.sda_frame_scratch_bytes.argtypes = [ct.c_uint64]
+    lib.sda_frame_encode.argtypes = [_vp, _ph, _vp, ct.c_int32, _vp, _vp, _vp]
+    lib.sda_frame_parse_header.argtypes = [_vp, ct.c_uint64, ct.c_uint64, _ph]
+    lib.sda_frame_decode.argtypes = [_vp, _vp, ct.c_uint64, _ph, _vp, ct.c_int32, _vp, _vp]
+    lib.sda_crc32.argtypes = [_vp, _vp, ct.c_uint64, _vp, _vp]
     lib.sda_quantize_affine.argtypes = [_vp, _vp, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32, _vp, ct.c_int64,
                                         _vp, _vp, _vp, _vp]
     lib.sda_dequantize.argtypes = [_vp, _vp, ct.c_int64, _vp, _vp, ct.c_int64, ct.c_int64, ct.c_int32, _vp, ct.c_int32]

@@ -55,6 +55,7 @@ const char* sda_status_string(int32_t s) {
         case SDA_ERR_CUDA: return "CUDA error";
         case SDA_ERR_NO_DEVICE: return "no CUDA device";
         case SDA_ERR_ROLE_VIOLATION: return "role violation";
+        case SDA_ERR_FRAME: return "frame error (magic / length / dtype / CRC)";
         default: return "unknown status";
     }
 }
@@ -170,6 +171,135 @@ sda_status sda_quant_roundtrip(void* stream, void* x, int32_t dtype, int64_t n_t
     return from_cuda(sda::launch_quant_roundtrip(x, dtype, n_tensors, count, bits,
                                                  reinterpret_cast<unsigned long long*>(scratch), err,
                                                  static_cast<cudaStream_t>(stream)));
+}
+
+// ------------------------------------------------------------------------------------------ frames
+static bool frame_dtype_ok(int d) { return (d >= 0 && d <= 3) || (d >= 18 && d <= 24); }
+
+uint64_t sda_frame_elements(const sda_frame_header* h) {
+    if (!h || h->n_dims == 0 || h->n_dims > SDA_FRAME_MAX_DIMS) return 0;
+    uint64_t n = 1;
+    for (uint32_t i = 0; i < h->n_dims; ++i) n *= h->dims[i];
+    return n;
+}
+
+uint64_t sda_frame_payload_bytes(const sda_frame_header* h) {
+    if (!h || !frame_dtype_ok(h->dtype)) return 0;
+    const uint64_t n = sda_frame_elements(h);
+    switch (h->dtype) {
+        case 0: return n * 8;
+        case 1: return n * 4;
+        case 2:
+        case 3: return n * 2;
+        default: return (n * (uint64_t)(h->dtype - 16) + 7) / 8 + 8;
+    }
+}
+
+static uint64_t frame_header_bytes(const sda_frame_header* h) { return 25 + 4ull * h->n_dims; }
+
+uint64_t sda_frame_bytes(const sda_frame_header* h) {
+    if (!h || h->n_dims > SDA_FRAME_MAX_DIMS) return 0;
+    return frame_header_bytes(h) + sda_frame_payload_bytes(h) + 4;
+}
+
+uint64_t sda_frame_scratch_bytes(uint64_t frame_bytes) {
+    return ((sda::crc_scratch_words(frame_bytes) * 4 + 255) / 256) * 256 + 256;
+}
+
+static void scratch_parts(void* scratch, uint64_t frame_bytes, uint32_t** crc, uint64_t** q, float** sz) {
+    uint8_t* s = static_cast<uint8_t*>(scratch);
+    const uint64_t off = ((sda::crc_scratch_words(frame_bytes) * 4 + 255) / 256) * 256;
+    *crc = reinterpret_cast<uint32_t*>(s);
+    *q = reinterpret_cast<uint64_t*>(s + off);
+    *sz = reinterpret_cast<float*>(s + off + 64);
+}
+
+sda_status sda_frame_encode(void* stream, const sda_frame_header* h, const void* x, int32_t x_dtype, uint8_t* out,
+                            void* scratch, int32_t* err) {
+    if (!h || !out || !scratch || h->n_dims > SDA_FRAME_MAX_DIMS || !frame_dtype_ok(h->dtype) || !quant_dtype_ok(x_dtype))
+        return SDA_ERR_INVALID_ARGUMENT;
+    const uint64_t count = sda_frame_elements(h);
+    if (count > 0 && !x) return SDA_ERR_INVALID_ARGUMENT;
+    uint8_t hdr[128];
+    int n = 0;
+    auto put = [&](uint64_t v, int bytes) {
+        for (int i = 0; i < bytes; ++i) hdr[n++] = (uint8_t)(v >> (8 * i));
+    };
+    hdr[n++] = 'F'; hdr[n++] = 'A'; hdr[n++] = 'T'; hdr[n++] = 'N';   // frame.cpp:119-131
+    put(h->version, 1);
+    put(h->msg_type, 1);
+    put(h->request_id, 8);
+    put(h->layer, 2);
+    put(h->head, 2);
+    put(h->domain, 2);
+    put(h->dtype, 1);
+    put(h->n_dims, 4);
+    for (uint32_t i = 0; i < h->n_dims; ++i) put(h->dims[i], 4);
+    uint32_t* crc;
+    uint64_t* q;
+    float* sz;
+    const uint64_t total = sda_frame_bytes(h);
+    scratch_parts(scratch, total, &crc, &q, &sz);
+    g_launches += 3;
+    return from_cuda(sda::launch_frame_encode(x, x_dtype, (int64_t)count, h->dtype, hdr, n, out,
+                                              sda_frame_payload_bytes(h), crc, q, sz, err,
+                                              static_cast<cudaStream_t>(stream)));
+}
+
+sda_status sda_frame_parse_header(const uint8_t* b, uint64_t host_len, uint64_t frame_size, sda_frame_header* out) {
+    if (!b || !out) return SDA_ERR_INVALID_ARGUMENT;
+    if (frame_size < 29 || host_len < 25) return SDA_ERR_FRAME;                       // frame too short
+    if (b[0] != 'F' || b[1] != 'A' || b[2] != 'T' || b[3] != 'N') return SDA_ERR_FRAME;   // bad magic
+    auto get = [&](uint64_t pos, int bytes) {
+        uint64_t v = 0;
+        for (int i = 0; i < bytes; ++i) v |= (uint64_t)b[pos + i] << (8 * i);
+        return v;
+    };
+    sda_frame_header h{};
+    h.version = (uint8_t)get(4, 1);
+    h.msg_type = (uint8_t)get(5, 1);
+    h.request_id = get(6, 8);
+    h.layer = (uint16_t)get(14, 2);
+    h.head = (uint16_t)get(16, 2);
+    h.domain = (uint16_t)get(18, 2);
+    h.dtype = (uint8_t)get(20, 1);
+    const uint64_t nd = get(21, 4);
+    if (25 + 4 * nd + 4 > frame_size) return SDA_ERR_FRAME;                            // truncated
+    if (nd > SDA_FRAME_MAX_DIMS) return SDA_ERR_UNSUPPORTED;
+    if (host_len < 25 + 4 * nd) return SDA_ERR_INVALID_ARGUMENT;                       // pass the whole header
+    h.n_dims = (uint32_t)nd;
+    for (uint32_t i = 0; i < h.n_dims; ++i) h.dims[i] = (uint32_t)get(25 + 4 * i, 4);
+    if (!frame_dtype_ok(h.dtype)) return SDA_ERR_FRAME;                                // unknown dtype
+    if (frame_header_bytes(&h) + sda_frame_payload_bytes(&h) + 4 != frame_size) return SDA_ERR_FRAME;
+    *out = h;
+    return SDA_OK;
+}
+
+sda_status sda_frame_decode(void* stream, const uint8_t* frame, uint64_t frame_size, const sda_frame_header* h,
+                            void* out, int32_t out_dtype, void* scratch, int32_t* err) {
+    if (!h || !frame || !scratch || h->n_dims > SDA_FRAME_MAX_DIMS || !frame_dtype_ok(h->dtype) || !quant_dtype_ok(out_dtype))
+        return SDA_ERR_INVALID_ARGUMENT;
+    if (sda_frame_bytes(h) != frame_size) return SDA_ERR_FRAME;
+    const uint64_t count = sda_frame_elements(h);
+    if (count > 0 && !out) return SDA_ERR_INVALID_ARGUMENT;
+    uint32_t* crc;
+    uint64_t* q;
+    float* sz;
+    scratch_parts(scratch, frame_size, &crc, &q, &sz);
+    g_launches += 3;
+    return from_cuda(sda::launch_frame_decode(frame, (int)frame_header_bytes(h), sda_frame_payload_bytes(h),
+                                              (int64_t)count, h->dtype, out, out_dtype, crc, sz, err,
+                                              static_cast<cudaStream_t>(stream)));
+}
+
+sda_status sda_crc32(void* stream, const uint8_t* bytes, uint64_t len, void* scratch, uint8_t* out4) {
+    if ((!bytes && len) || !scratch || !out4) return SDA_ERR_INVALID_ARGUMENT;
+    uint32_t* crc;
+    uint64_t* q;
+    float* sz;
+    scratch_parts(scratch, len, &crc, &q, &sz);
+    g_launches += 2;
+    return from_cuda(sda::launch_crc32(bytes, len, crc, out4, static_cast<cudaStream_t>(stream)));
 }
 
 int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int64_t kv_cap) {

@@ -246,3 +246,57 @@ def quant_roundtrip(x: torch.Tensor, bits: int, err: Optional[torch.Tensor] = No
     check(capi.LIB.sda_quant_roundtrip(_stream(stream), x.data_ptr(), _DT_Q[x.dtype], n, count, bits,
                                        scratch.data_ptr(), _ptr(err)), "sda_quant_roundtrip")
     return x
+
+
+# --- wire frames (frame.cpp) --------------------------------------------------------------------
+def frame_header(msg_type: int, request_id: int, layer: int, head: int, domain: int, dtype: int, dims,
+                 version: int = 1) -> capi.FrameHeader:
+    h = capi.FrameHeader()
+    h.version, h.msg_type, h.request_id, h.layer, h.head, h.domain, h.dtype = (version, msg_type, request_id, layer,
+                                                                               head, domain, dtype)
+    h.n_dims = len(dims)
+    for i, d in enumerate(dims):
+        h.dims[i] = d
+    return h
+
+
+def frame_encode(h: capi.FrameHeader, x: torch.Tensor, err: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """payload_from_values + encode_frame on the device: x (f32 / f64 / bf16, the frame's elements
+    in order) -> uint8 frame bytes (bit-exact with the reference's encoder on the same values)."""
+    _cuda(x, "x")
+    x = x.contiguous()
+    n = capi.LIB.sda_frame_bytes(ct.byref(h))
+    out = torch.empty(n, dtype=torch.uint8, device=x.device)
+    scratch = torch.empty(capi.LIB.sda_frame_scratch_bytes(n), dtype=torch.uint8, device=x.device)
+    check(capi.LIB.sda_frame_encode(_stream(stream), ct.byref(h), x.data_ptr(), _DT_Q[x.dtype], out.data_ptr(),
+                                    scratch.data_ptr(), _ptr(err)), "sda_frame_encode")
+    return out
+
+
+def frame_parse_header(head_bytes: bytes, frame_size: int) -> capi.FrameHeader:
+    """decode_frame's header checks on the host from the frame's first bytes."""
+    h = capi.FrameHeader()
+    buf = (ct.c_uint8 * len(head_bytes)).from_buffer_copy(head_bytes)
+    check(capi.LIB.sda_frame_parse_header(buf, len(head_bytes), frame_size, ct.byref(h)), "sda_frame_parse_header")
+    return h
+
+
+def frame_decode(frame: torch.Tensor, h: capi.FrameHeader, out_dtype: torch.dtype = torch.float64,
+                 err: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """decode_frame's CRC check (-> err = SDA_ERR_FRAME) + values_from_payload on the device."""
+    _cuda(frame, "frame")
+    n = capi.LIB.sda_frame_elements(ct.byref(h))
+    out = torch.empty(n, dtype=out_dtype, device=frame.device)
+    scratch = torch.empty(capi.LIB.sda_frame_scratch_bytes(frame.numel()), dtype=torch.uint8, device=frame.device)
+    check(capi.LIB.sda_frame_decode(_stream(stream), frame.data_ptr(), frame.numel(), ct.byref(h), out.data_ptr(),
+                                    _DT_Q[out_dtype], scratch.data_ptr(), _ptr(err)), "sda_frame_decode")
+    return out
+
+
+def crc32(b: torch.Tensor, stream=None) -> int:
+    """CRC-32/IEEE of a device byte tensor (synchronises to read the result)."""
+    _cuda(b, "bytes")
+    out = torch.zeros(4, dtype=torch.uint8, device=b.device)
+    scratch = torch.empty(capi.LIB.sda_frame_scratch_bytes(b.numel()), dtype=torch.uint8, device=b.device)
+    check(capi.LIB.sda_crc32(_stream(stream), b.data_ptr(), b.numel(), scratch.data_ptr(), out.data_ptr()), "sda_crc32")
+    return int.from_bytes(bytes(out.cpu().numpy()), "little")
