@@ -321,17 +321,27 @@ int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int
         }
         return best;
     }
-    // Decode is HBM-bound: give the grid >= ~4 full waves of the 148 SMs (at ~8 resident CTAs
-    // per SM) so the last partial wave is a small fraction of the launch, while keeping every
-    // split >= 256 keys.
+    // Decode is HBM-bound and every CTA streams the same number of keys, so the last partial
+    // wave of the grid runs the memory pipe at a fraction of its width: pick the split count
+    // (>= 2 tiles of 128 keys per split) whose grid fills whole waves best, among grids of at
+    // least 2 waves; ties go to fewer splits (C2: 13 splits = 4.99 waves of 148 x 9 CTAs).
     const int64_t ctas = n_batch * q_heads * q_rows;
-    const int64_t target = 148 * 8 * 4;
-    const int64_t want = (target + ctas - 1) / ctas;
-    const int64_t max_by_len = kv_cap / 256 > 0 ? kv_cap / 256 : 1;
-    int64_t s = want < max_by_len ? want : max_by_len;
-    if (s < 1) s = 1;
-    if (s > 1024) s = 1024;
-    return (int32_t)s;
+    const int64_t slots = 148LL * sda::k2_decode_ctas_per_sm();
+    const int64_t max_by_len = std::max<int64_t>(1, kv_cap / 256);
+    const int64_t s_max = std::min<int64_t>(max_by_len, SDA_MAX_SOURCES);   // K3 merges <= 64 sources
+    int64_t best = 1;
+    double best_eff = -1.0;
+    for (int64_t s = 1; s <= s_max; ++s) {
+        const double waves = (double)(s * ctas) / (double)slots;
+        if (waves < 2.0 && s < s_max) continue;
+        const double eff = waves / std::ceil(waves);
+        if (eff > best_eff + 1e-3) {
+            best_eff = eff;
+            best = s;
+        }
+        if (waves > 16.0) break;   // enough waves: the tail no longer matters
+    }
+    return (int32_t)best;
 }
 
 int32_t sda_default_splits_gqa(int64_t n_batch, int32_t q_heads, int32_t kv_heads, int64_t q_rows, int64_t kv_cap,
