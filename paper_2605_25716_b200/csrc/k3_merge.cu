@@ -142,31 +142,112 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
     float denom = 0.f;
     const bool single = p.n_src == 1;
     bool pending = false;
-    SrcLd<E> cur, nxt;
-    load_src(0, cur);
-    for (int s = 0; s < p.n_src; ++s) {
-        if (s + 1 < p.n_src) load_src(s + 1, nxt);
-        const K3Source& src = p.src[s];
-        if (cur.st.y > 0.f) {
-            const float w = single ? 1.f : cur.st.y * expf(cur.st.x - mstar);
-            denom += single ? cur.st.y : w;
+    auto load_tables = [&](const uint8_t* keys, SrcLd<E>& L) {
+        const uint8_t* sc = scrambler_ptr(keys, p.keys_bstride, b, kh, D, 1);
+        const float* ftab = reinterpret_cast<const float*>(sc);
+        const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + 24 * D);
+        load_vec_any<E>(ftab + kInvIn * D + lane * E, L.inv_in);
+        load_vec_any<E>(ftab + kInvOut * D + lane * E, L.inv_out);
 #pragma unroll
-            for (int e = 0; e < E; ++e) acc[e] = fmaf(w, cur.ov[e], acc[e]);
-            pending = true;
+        for (int e = 0; e < E; ++e) {
+            L.p2[e] = utab[kP2 * D + lane * E + e];
+            L.p1[e] = utab[kP1 * D + lane * E + e];
         }
-        const bool group_end = (s + 1 == p.n_src) || (p.src[s + 1].keys != src.keys);
-        if (group_end && pending) {
-            if (src.keys) {
-                unscramble_acc<D>(cur, acc, out, sh, lane);
-            } else {
+    };
+    bool done_ll = false;
+    if constexpr (E >= 2) {
+    if (ll && p.n_src <= 32) {
+        done_ll = true;
+        // LL records: the words of up to 8 sources are requested at once and validated after,
+        // instead of one blocking poll per word (the records are normally all there by now)
+        constexpr int NB = 8, W = E / 2;   // 16-byte LL words per lane per source
+        SrcLd<E> kt;
+        for (int s0 = 0; s0 < p.n_src; s0 += NB) {
+            uint4 raw[NB][W];
 #pragma unroll
-                for (int e = 0; e < E; ++e) out[e] += acc[e];
+            for (int k = 0; k < NB; ++k) {
+                if (s0 + k < p.n_src) {
+                    int64_t st_off, o_off;
+                    offsets(p.src[s0 + k], st_off, o_off);
+                    const uint8_t* rb = reinterpret_cast<const uint8_t*>(p.src[s0 + k].o) + 8 * (o_off + lane * E);
+#pragma unroll
+                    for (int m = 0; m < W; ++m)
+                        asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(raw[k][m].x), "=r"(raw[k][m].y), "=r"(raw[k][m].z), "=r"(raw[k][m].w)
+                                     : "l"(rb + 16 * m) : "memory");
+                }
             }
 #pragma unroll
-            for (int e = 0; e < E; ++e) acc[e] = 0.f;
-            pending = false;
+            for (int k = 0; k < NB; ++k) {
+                const int s = s0 + k;
+                if (s >= p.n_src) break;
+                const K3Source& src = p.src[s];
+                float ov[E];
+#pragma unroll
+                for (int m = 0; m < W; ++m) {
+                    if (raw[k][m].y != ep || raw[k][m].w != ep) {   // not there yet: poll this word
+                        int64_t st_off, o_off;
+                        offsets(src, st_off, o_off);
+                        const uint2 w2 = ll_load(reinterpret_cast<const uint8_t*>(src.o) + 8 * (o_off + lane * E) + 16 * m, ep);
+                        raw[k][m].x = w2.x;
+                        raw[k][m].z = w2.y;
+                    }
+                    ov[2 * m] = __uint_as_float(raw[k][m].x);
+                    ov[2 * m + 1] = __uint_as_float(raw[k][m].z);
+                }
+                const float sx = __shfl_sync(0xffffffffu, st_lane.x, s & 31);
+                const float sy = __shfl_sync(0xffffffffu, st_lane.y, s & 31);
+                if (sy > 0.f) {
+                    const float w = single ? 1.f : sy * expf(sx - mstar);
+                    denom += single ? sy : w;
+#pragma unroll
+                    for (int e = 0; e < E; ++e) acc[e] = fmaf(w, ov[e], acc[e]);
+                    pending = true;
+                }
+                const bool group_end = (s + 1 == p.n_src) || (p.src[s + 1].keys != src.keys);
+                if (group_end && pending) {
+                    if (src.keys) {
+                        load_tables(src.keys, kt);
+                        unscramble_acc<D>(kt, acc, out, sh, lane);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < E; ++e) out[e] += acc[e];
+                    }
+#pragma unroll
+                    for (int e = 0; e < E; ++e) acc[e] = 0.f;
+                    pending = false;
+                }
+            }
         }
-        cur = nxt;
+    }
+    }
+    if (!done_ll) {
+        SrcLd<E> cur, nxt;
+        load_src(0, cur);
+        for (int s = 0; s < p.n_src; ++s) {
+            if (s + 1 < p.n_src) load_src(s + 1, nxt);
+            const K3Source& src = p.src[s];
+            if (cur.st.y > 0.f) {
+                const float w = single ? 1.f : cur.st.y * expf(cur.st.x - mstar);
+                denom += single ? cur.st.y : w;
+    #pragma unroll
+                for (int e = 0; e < E; ++e) acc[e] = fmaf(w, cur.ov[e], acc[e]);
+                pending = true;
+            }
+            const bool group_end = (s + 1 == p.n_src) || (p.src[s + 1].keys != src.keys);
+            if (group_end && pending) {
+                if (src.keys) {
+                    unscramble_acc<D>(cur, acc, out, sh, lane);
+                } else {
+    #pragma unroll
+                    for (int e = 0; e < E; ++e) out[e] += acc[e];
+                }
+    #pragma unroll
+                for (int e = 0; e < E; ++e) acc[e] = 0.f;
+                pending = false;
+            }
+            cur = nxt;
+        }
     }
     const bool masked = !(mstar > -INFINITY);
     if (masked && lane == 0 && p.err && active) atomicExch(p.err, (int32_t)SDA_ERR_MASKED_ROW);

@@ -3,6 +3,7 @@ torchrun -- the decode step through NCCL all-to-all, through the peer-memory pus
 (bit-identical) and through the LL-chained kernels (same math, <= 1e-5 relative), eager and from
 a CUDA graph, over 30 steps."""
 import os
+import re
 import socket
 import subprocess
 import sys
@@ -29,6 +30,7 @@ def test_exchange_check_two_gpus():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tools", "exchange_check.py")]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=500)
-    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("rank ")]
+    # the two ranks print concurrently: their lines can interleave without a newline
+    lines = re.findall(r"rank \d+: .*?\((?:ok|FAIL)\)", r.stdout)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert len(lines) == 2 and all("True" in ln and "(ok)" in ln for ln in lines), lines
