@@ -28,6 +28,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 H, D, CTX, B_PER = 32, 128, 8192, 16
+CONFIG = 2   # BASELINE config of the decode line: 2 (default) or 4 (--config 4)
 METRIC = "scrambled-attn decode tokens/s"
 
 
@@ -54,6 +55,8 @@ def parse():
                     help="N>1: the exchange carried by K1/K2/K3 themselves in LL format over NVLink peer "
                          "memory (default), separate peer-memory push/wait kernels, or NCCL all-to-all")
     ap.add_argument("--ll-single", action="store_true", help="N=1: run the LL-chained step too (measured no faster)")
+    ap.add_argument("--config", type=int, choices=[2, 4], default=2,
+                    help="decode workload: BASELINE config 2 (default, the headline) or 4 (32K-token shard per GPU, batch 64)")
     ap.add_argument("--cpu-pairs", type=int, default=128, help="(request, head) pairs in the CPU sample")
     return ap.parse_args()
 
@@ -72,14 +75,30 @@ def dist_env():
     return ws, rank, local
 
 
+def set_config(cfg: int, ws: int) -> None:
+    """cfg 2: 16 requests per GPU, each request's 8K context sharded over the N GPUs (weak scaling
+    in requests). cfg 4 (BASELINE: 8 nodes x 32K-token shard per node, batch-64 decode): 64
+    requests in total, every GPU holds a 32K-token shard of each (weak scaling in context)."""
+    global CONFIG, CTX, B_PER
+    CONFIG = cfg
+    if cfg == 4:
+        if 64 % ws:
+            raise SystemExit("config 4 needs N dividing 64")
+        CTX, B_PER = 32768 * ws, 64 // ws
+
+
 def workload_config(n):
+    desc = ("BASELINE cfg2 per GPU: scrambled decode, 32 heads x d128, 8K-token context per request "
+            "sharded over N domains (one per GPU), 16 requests per GPU, bf16 KV") if CONFIG == 2 else (
+        "BASELINE cfg4: scrambled decode, 32 heads x d128, batch 64 (64/N inquirer requests per GPU), "
+        "a 32K-token scrambled KV shard of every request on each of the N domains, bf16 KV")
     return {
-        "workload": "BASELINE cfg2 per GPU: scrambled decode, 32 heads x d128, 8K-token context per request "
-                    "sharded over N domains (one per GPU), 16 requests per GPU, bf16 KV",
+        "workload": desc,
         "requests_per_gpu": B_PER, "global_batch": B_PER * n, "q_heads": H, "kv_heads": H, "head_dim": D,
         "context_per_request": CTX, "kv_rows_per_request_per_gpu": CTX // n, "domains": n,
         "kv_bytes_per_gpu": B_PER * n * H * (CTX // n) * D * 2 * 2,
-        "l2": "inputs larger than L2 (2 GiB scrambled KV per GPU vs 126 MB L2), no flush needed",
+        "l2": f"inputs larger than L2 ({B_PER * n * H * (CTX // n) * D * 4 / 2**30:.0f} GiB scrambled KV per GPU vs "
+              "126 MB L2), no flush needed",
         "parallelism": f"kv-sharded x{n} (one domain per GPU)",
     }
 
@@ -205,8 +224,9 @@ def run_ours(args, ws, rank, local):
     owner_keys = protocol.DomainKeys([rid(b) for b in range(B_tot)], 0, rank + 1, H, D, devn)
     shard = protocol.KVShard(B_tot, H, L, D, devn, torch.bfloat16)
     g = torch.Generator(device=devn).manual_seed(1000 + rank)
-    for b0 in range(0, B_tot, 16):  # context owners ship their segments (K1 into the cache)
-        b1 = min(B_tot, b0 + 16)
+    chunk = 16 if L <= 8192 else 4
+    for b0 in range(0, B_tot, chunk):  # context owners ship their segments (K1 into the cache)
+        b1 = min(B_tot, b0 + chunk)
         kp = torch.randn((b1 - b0, H, L, D), generator=g, device=devn).to(torch.bfloat16)
         vp = torch.randn((b1 - b0, H, L, D), generator=g, device=devn).to(torch.bfloat16)
         p, _ = owner_keys.span_perms(1, rank * L, L)
@@ -620,6 +640,7 @@ def main():
     os.dup2(2, 1)
     if args.gpus != ws and ws > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {ws}", file=sys.stderr)
+    set_config(args.config, ws)
     if args.impl == "reference":
         run_reference_arm(args, ws, rank)
     else:
