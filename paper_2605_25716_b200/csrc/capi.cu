@@ -324,7 +324,8 @@ int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int
     // Decode is HBM-bound and every CTA streams the same number of keys, so the last partial
     // wave of the grid runs the memory pipe at a fraction of its width: pick the split count
     // (>= 2 tiles of 128 keys per split) whose grid fills whole waves best, among grids of at
-    // least 2 waves; ties go to fewer splits (C2: 13 splits = 4.99 waves of 148 x 9 CTAs).
+    // least 2 and at most ~12 waves (beyond that more splits only add partials and per-CTA
+    // overhead); ties go to fewer splits (C2: 13 splits = 4.99 waves of 148 x 9 CTAs).
     const int64_t ctas = n_batch * q_heads * q_rows;
     const int64_t slots = 148LL * sda::k2_decode_ctas_per_sm();
     const int64_t max_by_len = std::max<int64_t>(1, kv_cap / 256);
@@ -333,13 +334,13 @@ int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int
     double best_eff = -1.0;
     for (int64_t s = 1; s <= s_max; ++s) {
         const double waves = (double)(s * ctas) / (double)slots;
+        if (waves > 12.0 && best_eff > 0.0) break;
         if (waves < 2.0 && s < s_max) continue;
         const double eff = waves / std::ceil(waves);
         if (eff > best_eff + 1e-3) {
             best_eff = eff;
             best = s;
         }
-        if (waves > 16.0) break;   // enough waves: the tail no longer matters
     }
     return (int32_t)best;
 }
