@@ -300,3 +300,35 @@ def crc32(b: torch.Tensor, stream=None) -> int:
     scratch = torch.empty(capi.LIB.sda_frame_scratch_bytes(b.numel()), dtype=torch.uint8, device=b.device)
     check(capi.LIB.sda_crc32(_stream(stream), b.data_ptr(), b.numel(), scratch.data_ptr(), out.data_ptr()), "sda_crc32")
     return int.from_bytes(bytes(out.cpu().numpy()), "little")
+
+
+# --- K1 folded into the QKV projection (SURVEY 8(f) "next" row 2) --------------------------------
+def project_scrambled(x: torch.Tensor, w: torch.Tensor, keys: torch.Tensor, variant: int, which: int,
+                      perm: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None, out_row_offset: int = 0,
+                      key_heads: Optional[int] = None, stream=None) -> torch.Tensor:
+    """Scrambled projection with no K1 pass over the activations: out[b, h, off + r] =
+    (x[b, perm_b[r]] @ W_h) phi_{b,h} for the projection x @ W_h of project_qkv (model.cpp:124-133)
+    followed by enc_qkv's scramble (scrambler.cpp:126-136). Because phi is linear,
+    (x W_h) phi = x (W_h phi): K1 runs once over the d_model rows of each W_h with request b's key
+    set (W'_{b,h} = W_h phi_{b,h}), and one batched GEMM (cuBLAS: a plain library GEMM) emits the
+    scrambled rows directly; the token permutation is a row gather of x.
+    x [B, rows, d_model] bf16; w [H, d_model, d] bf16 (GQA: H q heads on key_heads key sets).
+    Worth it when rows per request exceed ~d_model / 2 (prefill spans, KV shipping): W' costs
+    d_model x H x d per (request, layer, domain)."""
+    _cuda(x, "x"), _cuda(w, "w"), _cuda(keys, "keys")
+    B, rows, dm = x.shape
+    H, dm2, d = w.shape
+    if dm2 != dm:
+        raise ValueError("x and w disagree on d_model")
+    wp = torch.empty((B, H, dm, d), dtype=w.dtype, device=w.device)
+    # request b reads W (x_batch_mod = 1) and scrambles it with its own key set
+    scramble(w.unsqueeze(0).contiguous(), keys, variant, which, None, out=wp, key_heads=key_heads, n_batch=B,
+             stream=stream)
+    xg = x if perm is None else torch.gather(x, 1, perm.long().unsqueeze(-1).expand(B, rows, dm))
+    res = torch.matmul(xg.unsqueeze(1), wp)   # [B, H, rows, d], f32 accumulation
+    if out is None:
+        if out_row_offset:
+            raise ValueError("out_row_offset needs out")
+        return res
+    out[:, :, out_row_offset:out_row_offset + rows].copy_(res)
+    return out

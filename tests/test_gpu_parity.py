@@ -308,3 +308,25 @@ def test_ll_decode_world1_steps_and_graph(wire):
         torch.cuda.synchronize()
         check(i)
     assert int(lld.epoch.item()) == 1 + 3 + 3   # K3 opened one epoch per step
+
+
+@pytest.mark.parametrize("variant,which", [(0, 0), (1, 0), (0, 1)])
+def test_project_scrambled_folds_k1_into_the_projection(variant, which):
+    """ops.project_scrambled: (x[perm] @ W_h) phi_h computed as x[perm] @ (W_h phi_h) -- K1 over
+    the weights, one GEMM -- against the oracle's projection followed by apply_phi in f64."""
+    B, rows, dm, H, d = 2, 96, 256, 4, 64
+    keys = protocol.DomainKeys([1, 2], 0, 1, H, d, "cuda")
+    x = gauss(71, (B, rows, dm)) * 0.25
+    w = gauss(72, (H, dm, d)) * 0.0625
+    xd, wd = dev(x, torch.bfloat16), dev(w, torch.bfloat16)
+    xr, wr = xd.double().cpu().numpy(), wd.double().cpu().numpy()   # the values the device sees
+    perm, _ = keys.span_perms(1, 40, rows)
+    got = ops.project_scrambled(xd, wd, keys.dev, variant, which, perm).double().cpu().numpy()
+    p = perm.cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            ks = keys.host[b]
+            pre = "kq" if which == 0 else "v"
+            sc = tuple(getattr(ks, pre + f)[h] for f in ("_s1", "_p1", "_p2", "_s2"))
+            ref = C.apply_phi(xr[b][p[b]] @ wr[h], *sc, variant)
+            assert max_abs_rel(got[b, h], ref) < TOL_BF16 and rel_fro(got[b, h], ref) < 1e-2, (b, h)
