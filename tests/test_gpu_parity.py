@@ -330,3 +330,54 @@ def test_project_scrambled_folds_k1_into_the_projection(variant, which):
             sc = tuple(getattr(ks, pre + f)[h] for f in ("_s1", "_p1", "_p2", "_s2"))
             ref = C.apply_phi(xr[b][p[b]] @ wr[h], *sc, variant)
             assert max_abs_rel(got[b, h], ref) < TOL_BF16 and rel_fro(got[b, h], ref) < 1e-2, (b, h)
+
+
+def test_full_size_c5_gqa_decode_sampled_parity():
+    """BASELINE config 5 decode at full size (32 requests, 64 q / 8 kv heads x d128, 64K-token
+    shard, BF16; tensor-core GQA kernel with the default 4 splits): the rounding-matched oracle on
+    sampled (request, q head) pairs, and all pairs against plain attention (f32)."""
+    B, Hq, Hkv, d, L = 32, 64, 8, 128, 65536
+    G = Hq // Hkv
+    g = torch.Generator(device="cuda").manual_seed(55)
+    q = torch.randn((B, Hq, 1, d), generator=g, device="cuda").to(torch.bfloat16)
+    k = torch.randn((B, Hkv, L, d), generator=g, device="cuda").to(torch.bfloat16)
+    v = torch.randn((B, Hkv, L, d), generator=g, device="cuda").to(torch.bfloat16)
+    keys = protocol.DomainKeys([b + 1 for b in range(B)], 0, 1, Hkv, d, "cuda")
+    shard = protocol.KVShard(B, Hkv, L, d, "cuda")
+    shard.ship_segment(k, v, keys, first_pos=0)
+    got = protocol.scrambled_attention(q, [(keys, shard)], q_first_pos=L).double().cpu().numpy()
+    qf = q.float()
+    for b in (0, 13, 31):   # plain attention on a few requests (all heads)
+        kf, vf = k[b].float().repeat_interleave(G, 0), v[b].float().repeat_interleave(G, 0)
+        plain = (torch.softmax((qf[b] @ kf.transpose(-1, -2)) / np.sqrt(d), -1) @ vf).double().cpu().numpy()
+        assert rel_fro(got[b], plain) < 4e-2, b
+    for b, h in [(0, 0), (13, 37), (31, 63)]:
+        ss = C.derive_seed(1, [b + 1, 0x7365656B])
+        ref = C.scrambled_step(ss, b + 1, 0, Hkv, h // G, qf[b, h].double().cpu().numpy(), L,
+                               [k[b, h // G].float().double().cpu().numpy()],
+                               [v[b, h // G].float().double().cpu().numpy()], wire_fmt=2, shard_first_pos=[0])
+        assert max_abs_rel(got[b, h], ref) < TOL_BF16 and rel_fro(got[b, h], ref) < TOL_BF16, (b, h)
+
+
+def test_full_size_c3_prefill_sampled_parity():
+    """BASELINE config 3 per GPU at full size (2048-row span vs a 16K-token shard, 32 heads x
+    d128, BF16; tensor-core prefill K2 with its default splits, p_q permutations): the
+    rounding-matched oracle on one head and plain attention on sampled rows of every head."""
+    H, d, L, LQ = 32, 128, 16384, 2048
+    g = torch.Generator(device="cuda").manual_seed(77)
+    q = torch.randn((1, H, LQ, d), generator=g, device="cuda").to(torch.bfloat16)
+    k = torch.randn((1, H, L, d), generator=g, device="cuda").to(torch.bfloat16)
+    v = torch.randn((1, H, L, d), generator=g, device="cuda").to(torch.bfloat16)
+    keys = protocol.DomainKeys([1], 0, 1, H, d, "cuda")
+    shard = protocol.KVShard(1, H, L, d, "cuda")
+    shard.ship_segment(k, v, keys, first_pos=0)
+    got = protocol.scrambled_attention(q, [(keys, shard)], q_first_pos=L).double().cpu().numpy()[0]
+    rows = torch.tensor([0, 1, 777, 2047], device="cuda")
+    qf, kf, vf = q[0].float(), k[0].float(), v[0].float()
+    plain = (torch.softmax((qf[:, rows] @ kf.transpose(-1, -2)) / np.sqrt(d), -1) @ vf).double().cpu().numpy()
+    assert rel_fro(got[:, rows.cpu().numpy()], plain) < 4e-2
+    h = 5
+    ss = C.derive_seed(1, [1, 0x7365656B])
+    ref = C.scrambled_step(ss, 1, 0, H, h, qf[h].double().cpu().numpy(), L, [kf[h].double().cpu().numpy()],
+                           [vf[h].double().cpu().numpy()], wire_fmt=2, shard_first_pos=[0])
+    assert max_abs_rel(got[h], ref) < TOL_BF16 and rel_fro(got[h], ref) < TOL_BF16

@@ -29,6 +29,8 @@ __global__ void __launch_bounds__(512) kern(float* out, float seed) {
             if (OP == 4) asm volatile("mad.lo.u32 %0, %0, 8388608, %1;" : "+r"(u[k]) : "r"(u[(k + 1) & 7]));
             if (OP == 5) asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(a[k]));
             if (OP == 6) asm volatile("add.rn.f32x2 %0, %0, %0;" : "+l"(d[k]));
+            if (OP == 7) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(u[k]));
+            if (OP == 8) asm volatile("cvt.rn.f16x2.f32 %0, %1, %0;" : "+r"(u[k]) : "f"(a[k]));
         }
     }
     float s = 0.f;
@@ -48,8 +50,9 @@ int main() {
     float* out;
     cudaMalloc(&out, 4);
     const char* names[] = {"MUFU.EX2 (ex2.approx)", "F2FP (cvt.rn.bf16x2.f32)", "FFMA2 (fma.rn.f32x2)", "FMNMX3 (max.f32 x3)",
-                           "IMAD (mad.lo.u32)", "FFMA (fma.rn.f32)", "FADD2 (add.rn.f32x2)"};
-    for (int op = 0; op < 7; ++op) {
+                           "IMAD (mad.lo.u32)", "FFMA (fma.rn.f32)", "FADD2 (add.rn.f32x2)",
+                           "MUFU.EX2 f16x2", "F2FP f16x2 (cvt.rn.f16x2.f32)"};
+    for (int op = 0; op < 9; ++op) {
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
@@ -64,6 +67,8 @@ int main() {
                 case 4: kern<4><<<blocks, threads>>>(out, 1.f); break;
                 case 5: kern<5><<<blocks, threads>>>(out, 1.f); break;
                 case 6: kern<6><<<blocks, threads>>>(out, 1.f); break;
+                case 7: kern<7><<<blocks, threads>>>(out, 1.f); break;
+                case 8: kern<8><<<blocks, threads>>>(out, 1.f); break;
             }
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
