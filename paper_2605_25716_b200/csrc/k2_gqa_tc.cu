@@ -137,7 +137,9 @@ k2_gqa_tc_kernel(const K2GqaParams p, const __grid_constant__ CUtensorMap qmap, 
         }
     } else if (warp == 5) {
         // ------------------------------------------------------------------ MMA issuer
-        if (lane == 0 && nkv > 0) {
+        // the whole warp runs the loop (warp-uniform descriptors); the elected lane issues
+        if (nkv > 0) {
+            const bool leader = tc::elect_one();
             constexpr uint32_t IDESC_S = tc::idesc_bf16_f32(128, N, false, false);  // K . Q^T
             constexpr uint32_t IDESC_O = tc::idesc_bf16_f32(128, N, true, false);   // V^T (MN-major) . P^T
             const uint32_t qb = tc::smem_u32(smem + S::OFF_Q);
@@ -146,11 +148,12 @@ k2_gqa_tc_kernel(const K2GqaParams p, const __grid_constant__ CUtensorMap qmap, 
                 const uint32_t kb = tc::smem_u32(smem + S::OFF_K + st * TILE_BYTES);
                 const uint32_t d_tmem = tmem + COL_S + (uint32_t)((j & 1) * N);
 #pragma unroll
-                for (int k = 0; k < D / 16; ++k)
-                    tc::mma_bf16_ss(d_tmem, tc::sw128_desc(kb + (k >> 2) * BLK + (k & 3) * 32, 16, 1024),
-                                    tc::sw128_desc(qb + (k >> 2) * S::QBLK + (k & 3) * 32, 16, 1024), IDESC_S,
-                                    k > 0 ? 1u : 0u);
-                tc::mma_commit(&s_full[j & 1]);
+                for (int k = 0; k < D / 16; ++k) {
+                    const uint64_t da = tc::sw128_desc(kb + (k >> 2) * BLK + (k & 3) * 32, 16, 1024);
+                    const uint64_t db = tc::sw128_desc(qb + (k >> 2) * S::QBLK + (k & 3) * 32, 16, 1024);
+                    if (leader) tc::mma_bf16_ss(d_tmem, da, db, IDESC_S, k > 0 ? 1u : 0u);
+                }
+                if (leader) tc::mma_commit(&s_full[j & 1]);
             };
             tc::mbar_wait(q_full, 0);
             for (int64_t j = 0; j < nkv && j < 2; ++j) {
@@ -165,14 +168,17 @@ k2_gqa_tc_kernel(const K2GqaParams p, const __grid_constant__ CUtensorMap qmap, 
                 const uint32_t vb = tc::smem_u32(smem + S::OFF_V + st * TILE_BYTES);
                 const uint32_t pb = tc::smem_u32(smem + S::OFF_P + (j & 1) * S::P_BYTES);
 #pragma unroll
-                for (int k = 0; k < TILE / 16; ++k)   // 16 keys per step
-                    tc::mma_bf16_ss(tmem + COL_O, tc::sw128_desc(vb + k * 2048, BLK, 1024),
-                                    tc::sw128_desc(pb + (k >> 2) * (N * 128) + (k & 3) * 32, 16, 1024), IDESC_O,
-                                    (j > 0 || k > 0) ? 1u : 0u);
-                tc::mma_commit(&kv_empty[st]);
-                tc::mma_commit(&p_free[j & 1]);
-                tc::mma_commit(pv_done);
-                if (j + 1 == nkv) tc::mma_commit(o_final);
+                for (int k = 0; k < TILE / 16; ++k) {   // 16 keys per step
+                    const uint64_t da = tc::sw128_desc(vb + k * 2048, BLK, 1024);
+                    const uint64_t db = tc::sw128_desc(pb + (k >> 2) * (N * 128) + (k & 3) * 32, 16, 1024);
+                    if (leader) tc::mma_bf16_ss(tmem + COL_O, da, db, IDESC_O, (j > 0 || k > 0) ? 1u : 0u);
+                }
+                if (leader) {
+                    tc::mma_commit(&kv_empty[st]);
+                    tc::mma_commit(&p_free[j & 1]);
+                    tc::mma_commit(pv_done);
+                    if (j + 1 == nkv) tc::mma_commit(o_final);
+                }
                 if (j + 2 < nkv) {
                     tc::mbar_wait(&kv_full[(j + 2) % ST], (uint32_t)(((j + 2) / ST) & 1));
                     tc::tc_fence_after();
