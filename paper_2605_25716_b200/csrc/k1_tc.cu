@@ -18,7 +18,7 @@
 //   warps 4-7 (loaders) : cp.async 16-byte chunks of the gathered input rows perm[r] straight
 //                         into a SWIZZLE_128B K-major A stage (4 stages); completion is signalled
 //                         with cp.async.mbarrier.arrive.noinc on the stage's `full` barrier;
-//   warp 8     (MMA)    : one lane issues 2 x d/16 tcgen05.mma (M=128, N=d, K=16) into one of
+//   warp 8     (MMA)    : the elected lane issues 2 x d/16 tcgen05.mma (M=128, N=d, K=16) into one of
 //                         two TMEM accumulators; tcgen05.commit frees the A stage and hands the
 //                         accumulator to the epilogue;
 //   warps 0-3 (epilogue): tcgen05.ld -> bf16 -> swizzled SMEM -> TMA tensor
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
     uint64_t* const bready = bfree + 1;
     uint32_t* const tmem_slot = reinterpret_cast<uint32_t*>(bready + 1);
 
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = tid >> 5;
     const int64_t first = (int64_t)blockIdx.x * p.tiles_per_cta;
     const int64_t last = min(first + p.tiles_per_cta, p.total_tiles);
     if (first >= last) return;
@@ -204,11 +204,12 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
         const uint32_t bh = tc::smem_u32(b_hi), bl = tc::smem_u32(b_lo);
         int64_t cur = -1;
         uint32_t nbuild = 0;
+        const bool leader = tc::elect_one();   // the warp runs the loop; descriptors stay warp-uniform
         for (int64_t it = 0; it < ntiles; ++it) {
             const int st = (int)(it % ST), acc = (int)(it & 1);
             const int64_t ks = kslab_of(first + it);
             if (ks != cur) {
-                if (it > 0 && lane == 0) tc::mma_commit(bfree);   // old B free once prior MMAs finish
+                if (it > 0 && leader) tc::mma_commit(bfree);   // old B free once prior MMAs finish
                 tc::mbar_wait(bready, nbuild & 1);
                 ++nbuild;
                 cur = ks;
@@ -217,20 +218,24 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
             if (it >= 2) tc::mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) - 1) & 1));
             tc::fence_proxy_async_smem();          // cp.async (generic proxy) -> tcgen05 (async proxy)
             tc::tc_fence_after();
-            if (lane == 0) {
+            {
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * D);
                 const uint32_t a = tc::smem_u32(a_base + st * S::TILE_BYTES);
 #pragma unroll
                 for (int k = 0; k < D / 16; ++k) {
                     const uint32_t aoff = (k >> 2) * S::BLK_BYTES + (k & 3) * 32;   // 64-wide K block, 16-elem step
                     const uint32_t boff = (k >> 2) * S::BBLK_BYTES + (k & 3) * 32;
-                    tc::mma_bf16_ss(d_tmem, tc::sw128_desc(a + aoff, 16, 1024), tc::sw128_desc(bh + boff, 16, 1024),
-                                    IDESC, k > 0 ? 1u : 0u);
-                    tc::mma_bf16_ss(d_tmem, tc::sw128_desc(a + aoff, 16, 1024), tc::sw128_desc(bl + boff, 16, 1024),
-                                    IDESC, 1u);
+                    const uint64_t da = tc::sw128_desc(a + aoff, 16, 1024);
+                    const uint64_t dh = tc::sw128_desc(bh + boff, 16, 1024), dl = tc::sw128_desc(bl + boff, 16, 1024);
+                    if (leader) {
+                        tc::mma_bf16_ss(d_tmem, da, dh, IDESC, k > 0 ? 1u : 0u);
+                        tc::mma_bf16_ss(d_tmem, da, dl, IDESC, 1u);
+                    }
                 }
-                tc::mma_commit(&empty[st]);
-                tc::mma_commit(&tfull[acc]);
+                if (leader) {
+                    tc::mma_commit(&empty[st]);
+                    tc::mma_commit(&tfull[acc]);
+                }
             }
             __syncwarp();
         }
