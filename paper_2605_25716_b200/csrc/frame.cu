@@ -20,6 +20,8 @@
 // conditioning is one more term: crc = ~(Z^N 0xFFFFFFFF xor raw(M)); the sub-chunk tail is fed
 // byte by byte into the combined register. Z^n matrices are built on the host by squaring.
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cmath>
 #include <cstring>
 #include <type_traits>
@@ -288,7 +290,7 @@ Gf2Mat zeros_op(uint64_t n) {   // Z^n by square-and-multiply
     return r;
 }
 
-bool tables_ready[64] = {};   // per device
+std::atomic<bool> tables_ready[64] = {};   // per device
 
 cudaError_t crc_launch(const uint8_t* msg, uint64_t len, uint32_t* scratch, uint8_t* write_to, const uint8_t* check,
                        int32_t* err, int32_t err_code, cudaStream_t st) {
@@ -305,16 +307,17 @@ cudaError_t crc_launch(const uint8_t* msg, uint64_t len, uint32_t* scratch, uint
     int levels = 0;
     while (((int64_t)1 << levels) < n_chunks) ++levels;
     const int64_t n2 = (int64_t)1 << levels;
-    static CrcPlan plan;   // host copy: matrices depend only on the level (cached)
-    static int built = -1;
-    if (built < levels) {
+    static Gf2Mat level_ops[kMaxLevels];   // Z^(256 * 2^k), built once per process
+    static std::once_flag once;
+    std::call_once(once, [] {
         Gf2Mat m = zeros_op(kCrcChunk);
         for (int k = 0; k < kMaxLevels; ++k) {
-            plan.level[k] = m;
+            level_ops[k] = m;
             m = gf2_mul(m, m);
         }
-        built = kMaxLevels;
-    }
+    });
+    CrcPlan plan;   // per call (kernel parameter): reentrant
+    memcpy(plan.level, level_ops, sizeof(level_ops));
     plan.levels = n_chunks > 0 ? levels : 0;
     plan.k_prefix = gf2_apply_h(zeros_op((uint64_t)n_chunks * kCrcChunk), 0xFFFFFFFFu);
     cudaError_t e = cudaMemsetAsync(scratch, 0, (size_t)n2 * 4, st);

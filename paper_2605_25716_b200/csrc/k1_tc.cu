@@ -385,11 +385,9 @@ static int num_sms() {
 template <int D>
 static cudaError_t launch_k1_tc_d(const K1Params* qs, const int64_t* n_batch, int n_jobs, cudaStream_t st) {
     using S = K1TcShape<D>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k1_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+    {
+        const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k1_tc_kernel<D>), S::SMEM);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     if (n_jobs < 1 || n_jobs > kK1Jobs) return cudaErrorInvalidValue;
     K1TcParams p{};

@@ -329,11 +329,9 @@ template <int N>
 static cudaError_t launch_gqa_n(const K2Params& q, cudaStream_t st) {
     using namespace k2g;
     using S = Shape<N>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k2_gqa_tc_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+    {
+        const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k2_gqa_tc_kernel<N>), S::SMEM);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     K2GqaParams p;
     p.q_rows = q.q_rows;

@@ -407,11 +407,9 @@ bool k2_prefill_tc_eligible(const K2Params& p, int d, int qdt, int kvdt) {
 
 cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
     using namespace k2tc;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k2_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    {
+        const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k2_prefill_tc_kernel), SMEM);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     K2TcParams p;
     p.q_rows = q.q_rows;
