@@ -312,7 +312,7 @@ int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int
         int32_t best = 1;
         double best_eff = -1.0;
         for (int64_t s = 1; s <= max_s; ++s) {
-            const double waves = (double)(units * s) / 148.0;
+            const double waves = (double)(units * s) / (double)sda::device_sms();
             const double eff = waves / std::ceil(waves) - (s > 1 ? 0.01 * (double)s : 0.0);  // small merge cost
             if (eff > best_eff + 1e-9) {
                 best_eff = eff;
@@ -327,7 +327,7 @@ int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int
     // least 2 and at most ~12 waves (beyond that more splits only add partials and per-CTA
     // overhead); ties go to fewer splits (C2: 13 splits = 4.99 waves of 148 x 9 CTAs).
     const int64_t ctas = n_batch * q_heads * q_rows;
-    const int64_t slots = 148LL * sda::k2_decode_ctas_per_sm();
+    const int64_t slots = (int64_t)sda::device_sms() * sda::k2_decode_ctas_per_sm();
     const int64_t max_by_len = std::max<int64_t>(1, kv_cap / 256);
     const int64_t s_max = std::min<int64_t>(max_by_len, SDA_MAX_SOURCES);   // K3 merges <= 64 sources
     int64_t best = 1;
@@ -360,7 +360,7 @@ int32_t sda_default_splits_gqa(int64_t n_batch, int32_t q_heads, int32_t kv_head
         int32_t best = 1;
         double best_cost = 1e300;
         for (int64_t s = 1; s <= max_s; ++s) {
-            const double waves = std::ceil((double)(units * s) / 148.0);
+            const double waves = std::ceil((double)(units * s) / (double)sda::device_sms());
             const double cost = waves * ((double)((tiles + s - 1) / s) + 2.6);
             if (cost < best_cost - 1e-9) {
                 best_cost = cost;

@@ -12,6 +12,26 @@
 
 namespace sda {
 
+// SM count of the current device (grid sizing and the split heuristics); 148 on B200, also the
+// answer without a device (host-side callers of the heuristics)
+inline int device_sms() {
+    static int cache[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        cudaGetLastError();
+        return 148;
+    }
+    if (!cache[dev]) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = 148;
+        }
+        cache[dev] = n;
+    }
+    return cache[dev];
+}
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute is
 // per device, so a process driving several GPUs must set it on each of them
 inline cudaError_t ensure_smem_attr(const void* kernel, int bytes) {

@@ -323,7 +323,7 @@ cudaError_t crc_launch(const uint8_t* msg, uint64_t len, uint32_t* scratch, uint
     cudaError_t e = cudaMemsetAsync(scratch, 0, (size_t)n2 * 4, st);
     if (e != cudaSuccess) return e;
     if (n_chunks > 0) {
-        const int64_t blocks = std::min<int64_t>((n_chunks + 255) / 256, 148 * 8);
+        const int64_t blocks = std::min<int64_t>((n_chunks + 255) / 256, (int64_t)device_sms() * 8);
         crc_chunks_kernel<<<(unsigned)blocks, 256, 0, st>>>(msg, n_chunks, scratch, n2 - n_chunks);
     }
     crc_combine_kernel<<<1, 1024, 0, st>>>(scratch, plan, msg + (uint64_t)n_chunks * kCrcChunk,
@@ -350,7 +350,7 @@ cudaError_t launch_frame_encode(const void* x, int x_dt, int64_t count, int wire
     HeaderBytes h;
     memcpy(h.b, header, hlen);
     h.len = hlen;
-    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, 148 * 8));
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)device_sms() * 8));
     cudaError_t e = cudaSuccess;
     if (wire <= 3) {
         switch (x_dt) {
@@ -389,7 +389,7 @@ cudaError_t launch_frame_decode(const uint8_t* frame, int hlen, uint64_t payload
                                err, SDA_ERR_FRAME, st);
     if (e != cudaSuccess || count == 0) return e;
     const uint8_t* pl = frame + hlen;
-    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, 148 * 8));
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)device_sms() * 8));
     if (wire <= 3) {
         switch (out_dt) {
             case SDA_F32: frame_decode_kernel<float><<<blocks, 256, 0, st>>>(pl, count, wire, static_cast<float*>(out)); break;

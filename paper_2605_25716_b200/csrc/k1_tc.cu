@@ -371,16 +371,7 @@ bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+static int num_sms() { return device_sms(); }
 
 template <int D>
 static cudaError_t launch_k1_tc_d(const K1Params* qs, const int64_t* n_batch, int n_jobs, cudaStream_t st) {
