@@ -266,11 +266,13 @@ sda_status sda_ll_scramble_q(void* stream, const void* q, int32_t q_dtype, int32
                              int32_t key_heads, void* const* ll_q, int32_t wire_dtype, const uint32_t* epoch);
 /* sda_ll_partial_attention: K2 over this rank's Q' slots (ll_q = [W][B_p][H][d] LL) and its KV
  *   shard (requests sender-major, kv_len / k / v as sda_partial_attention); split s of request
- *   (sender, i) goes to ll_rec[sender] = the sender's record slot for this domain. */
+ *   (sender, i) goes to ll_rec[sender] = the sender's record slot for this domain.
+ *   gqa_work: optional device buffer of W * B_p * H * d bf16; with it, GQA shards (bf16, d 128,
+ *   2 <= H / kv_heads <= 32) run the tensor-core GQA kernel (Q' unpacked from LL first). */
 sda_status sda_ll_partial_attention(void* stream, const void* ll_q, int32_t wire_dtype, const void* k, const void* v,
                                     int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int32_t n_dest,
                                     int64_t b_per, int32_t q_heads, int32_t kv_heads, int32_t head_dim,
-                                    int32_t n_splits, void* const* ll_rec, const uint32_t* epoch);
+                                    int32_t n_splits, void* const* ll_rec, const uint32_t* epoch, void* gqa_work);
 /* sda_ll_unscramble_merge: K3 over this rank's record slots (n_domains * n_splits sources, each
  *   domain unscrambled with its phi_V^-1 from keys[(domain * B_p + b)]) into out [B_p][H][1][d];
  *   then *epoch += 1. done_counter: one zeroed u32 (self-resetting). */

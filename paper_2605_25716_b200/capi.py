@@ -127,7 +127,7 @@ def _load() -> ct.CDLL:
     lib.sda_ll_scramble_q.argtypes = [_vp, _vp, ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int32, _vp,
                                       ct.c_int64, ct.c_int32, _pp, ct.c_int32, _vp]
     lib.sda_ll_partial_attention.argtypes = [_vp, _vp, ct.c_int32, _vp, _vp, ct.c_int32, ct.c_int64, _vp, ct.c_int32,
-                                             ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32, _pp, _vp]
+                                             ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32, _pp, _vp, _vp]
     lib.sda_ll_unscramble_merge.argtypes = [_vp, _vp, ct.c_int32, ct.c_int32, _vp, ct.c_int64, ct.c_int32, ct.c_int64,
                                             ct.c_int32, ct.c_int32, _vp, ct.c_int32, _vp, _vp]
     lib.sda_trace_timestamp.argtypes = [_vp, _vp]

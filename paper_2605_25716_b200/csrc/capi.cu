@@ -450,7 +450,7 @@ sda_status sda_ll_scramble_q(void* stream, const void* q, int32_t q_dtype, int32
 sda_status sda_ll_partial_attention(void* stream, const void* ll_q, int32_t wire_dtype, const void* k, const void* v,
                                     int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int32_t n_dest,
                                     int64_t b_per, int32_t q_heads, int32_t kv_heads, int32_t head_dim,
-                                    int32_t n_splits, void* const* ll_rec, const uint32_t* epoch) {
+                                    int32_t n_splits, void* const* ll_rec, const uint32_t* epoch, void* gqa_work) {
     if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
     if (!supported_dim(head_dim) || head_dim < 64) return SDA_ERR_UNSUPPORTED;
     if (!ll_q || !k || !v || !ll_rec || !epoch || n_dest <= 0 || n_dest > sda::kMaxPeers || b_per <= 0 ||
@@ -466,8 +466,18 @@ sda_status sda_ll_partial_attention(void* stream, const void* ll_q, int32_t wire
     p.epoch = epoch;
     p.b_per = b_per;
     for (int i = 0; i < n_dest; ++i) p.ll_rec[i] = ll_rec[i];
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (gqa_work && sda::k2_gqa_tc_eligible(p, head_dim, wire_dtype, kv_dtype) && !env_flag("SDA_K2_SIMT")) {
+        // GQA: unpack Q' out of its LL words (spins on the epoch), then the tensor-core GQA
+        // kernel reads it through TMA and writes its split records in LL form
+        g_launches += 2;
+        cudaError_t e = sda::launch_ll_unpack_q(ll_q, n_batch * q_heads * head_dim, gqa_work, epoch, st);
+        if (e != cudaSuccess) return from_cuda(e);
+        p.q = gqa_work;
+        return from_cuda(sda::launch_k2_gqa_tc(p, st));
+    }
     ++g_launches;
-    return from_cuda(sda::launch_k2_decode(p, head_dim, wire_dtype, kv_dtype, static_cast<cudaStream_t>(stream)));
+    return from_cuda(sda::launch_k2_decode(p, head_dim, wire_dtype, kv_dtype, st));
 }
 
 sda_status sda_ll_unscramble_merge(void* stream, const void* ll_rec, int32_t n_domains, int32_t n_splits,

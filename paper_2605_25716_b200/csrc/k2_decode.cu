@@ -11,6 +11,7 @@
 // warp-shuffle dot-product reduction; per-lane-group online softmax in f32; a final
 // shared-memory merge of the CTA's lane groups. Emits the split's locally normalised O'
 // and (row_max, exp_sum) exactly as ShardStats defines them (attention.hpp:34-41).
+#include <algorithm>
 #include <cmath>
 #include <type_traits>
 
@@ -198,6 +199,23 @@ static cudaError_t launch_k2_d(const K2Params& p, int qdt, int kvdt, cudaStream_
     if (qdt == SDA_F32 && kvdt == SDA_BF16) return launch_k2_t<D, float, __nv_bfloat16>(p, st);
     if (qdt == SDA_BF16 && kvdt == SDA_F32) return launch_k2_t<D, __nv_bfloat16, float>(p, st);
     return launch_k2_t<D, float, float>(p, st);
+}
+
+// LL Q' (bf16 wire: 4 values per 16-byte word) -> plain bf16 rows for the TMA-fed tensor-core
+// GQA kernel; spins until the words carry the step's epoch
+__global__ void __launch_bounds__(256) ll_unpack_q_kernel(const uint8_t* __restrict__ ll, int64_t words, uint2* out,
+                                                          const uint32_t* epoch) {
+    const uint32_t ep = *epoch;
+    pdl_trigger();
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x)
+        out[w] = ll_load(ll + 16 * w, ep);
+}
+
+cudaError_t launch_ll_unpack_q(const void* ll_q, int64_t elems, void* out, const uint32_t* epoch, cudaStream_t st) {
+    const int64_t words = elems / 4;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((words + 255) / 256, 1184));
+    return pdl_launch(ll_unpack_q_kernel, dim3(blocks), dim3(256), st, static_cast<const uint8_t*>(ll_q), words,
+                      static_cast<uint2*>(out), epoch);
 }
 
 int k2_decode_ctas_per_sm() {   // resident CTAs per SM of the C2 instantiation (split heuristic)

@@ -35,6 +35,12 @@ struct K2GqaParams {
     int n_splits;
     int rows;              // R = G * q_rows (real rows of the N dimension)
     float scale_log2;
+    // LL exchange (decode, q_rows == 1; epoch != nullptr): split `split` of request b = (dest, i)
+    // is written as LL record rows [d O' | row_max, exp_sum] at logical float
+    // ((split * b_per + i) * q_heads + head) * (d + 2) of ll_rec[dest] (as k2_decode.cu)
+    const uint32_t* epoch;
+    int64_t b_per;
+    void* ll_rec[kMaxPeers];
 };
 
 namespace k2g {
@@ -90,6 +96,8 @@ k2_gqa_tc_kernel(const K2GqaParams p, const __grid_constant__ CUtensorMap qmap, 
     const int64_t nkv = t1 > t0 ? t1 - t0 : 0;
     const int64_t k_end = min(len, t1 * TILE);
     const int64_t qrow0 = (b * p.q_heads + (int64_t)kvh * G) * p.q_rows;   // first of the R Q rows
+    const uint32_t ep = p.epoch ? *p.epoch : 0u;
+    if (p.epoch) pdl_trigger();   // K3 may launch once every CTA has read the epoch
     const int64_t kvrow0 = (b * p.kv_heads + kvh) * p.kv_cap + t0 * TILE;
 
     if (tid == 0) {
@@ -298,9 +306,29 @@ k2_gqa_tc_kernel(const K2GqaParams p, const __grid_constant__ CUtensorMap qmap, 
 #pragma unroll
             for (int h = 0; h < N; ++h) ov[h] = 0u;
         }
+        if (p.epoch) {   // LL records straight into the inquirer's slot (q_rows == 1: row = q head)
+            const int64_t dest = b / p.b_per, i = b % p.b_per;
+            uint8_t* rb = static_cast<uint8_t*>(p.ll_rec[dest]) +
+                          8 * (((int64_t)split * p.b_per + i) * p.q_heads + (int64_t)kvh * G) * (D + 2);
+#pragma unroll
+            for (int h = 0; h < N; ++h) {
+                const float inv = lt[h] > 0.f ? 1.f / lt[h] : 0.f;
+                const float o_here = __uint_as_float(ov[h]) * inv;               // d = tid
+                const float o_next = __shfl_down_sync(0xffffffffu, o_here, 1);  // d = tid + 1
+                if (h < R) {
+                    uint8_t* row = rb + 8 * ((int64_t)h * (D + 2));
+                    if ((tid & 1) == 0) ll_store(row + 8 * tid, __float_as_uint(o_here), __float_as_uint(o_next), ep);
+                    if (tid == 0) {
+                        const bool any = lt[h] > 0.f;
+                        ll_store(row + 8 * D, __float_as_uint(any ? m_run[h] / kLog2e : -INFINITY),
+                                 __float_as_uint(any ? lt[h] * ex2(m_use[h] - m_run[h]) : 0.f), ep);
+                    }
+                }
+            }
+        }
         const int64_t orow0 = (int64_t)split * p.n_batch * p.q_heads * p.q_rows + qrow0;
 #pragma unroll
-        for (int h = 0; h < N; ++h) {
+        for (int h = 0; h < N && !p.epoch; ++h) {
             if (h < R) {
                 const float inv = lt[h] > 0.f ? 1.f / lt[h] : 0.f;
                 p.out_o[(orow0 + h) * D + tid] = __uint_as_float(ov[h]) * inv;   // d = tid: coalesced
@@ -345,6 +373,9 @@ static cudaError_t launch_gqa_n(const K2Params& q, cudaStream_t st) {
     p.n_splits = q.n_splits;
     p.rows = (int)((q.q_heads / q.kv_heads) * q.q_rows);
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+    p.epoch = q.epoch;
+    p.b_per = q.b_per;
+    for (int i = 0; i < kMaxPeers; ++i) p.ll_rec[i] = q.ll_rec[i];
     CUtensorMap qm, km, vm;
     if (!make_tmap_bf16_2d(&qm, q.q, q.n_batch * q.q_heads * q.q_rows, D, N) ||
         !make_tmap_bf16_2d(&km, q.k, q.n_batch * q.kv_heads * q.kv_cap, D, TILE) ||

@@ -113,6 +113,7 @@ cudaError_t launch_dequantize(const uint8_t* codes, int64_t codes_stride, const 
                               int64_t n, int64_t count, int bits, void* out, int dt, cudaStream_t st);
 uint64_t crc_scratch_words(uint64_t len);
 int k2_decode_ctas_per_sm();
+cudaError_t launch_ll_unpack_q(const void* ll_q, int64_t elems, void* out, const uint32_t* epoch, cudaStream_t st);
 cudaError_t launch_crc32(const uint8_t* msg, uint64_t len, uint32_t* scratch, uint8_t* out4, cudaStream_t st);
 cudaError_t launch_frame_encode(const void* x, int x_dt, int64_t count, int wire, const uint8_t* header, int hlen,
                                 uint8_t* out, uint64_t payload_bytes, uint32_t* crc_scratch, uint64_t* q_scratch,

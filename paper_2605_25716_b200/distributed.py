@@ -185,6 +185,9 @@ class LLDecode:
         self.rec_ll = torch.zeros(W * r_slot, dtype=torch.uint8, device=dev)
         self.epoch = torch.ones(1, dtype=torch.int32, device=dev)
         self.done = torch.zeros(1, dtype=torch.int32, device=dev)
+        # GQA shards: Q' is unpacked from its LL words into this buffer for the tensor-core kernel
+        self.gqa_work = (torch.empty((W * b_per, q_heads, 1, head_dim), dtype=torch.bfloat16, device=dev)
+                         if shard.k.shape[1] < q_heads else None)
         torch.cuda.synchronize()
         ptrs, self.opened = map_peer_buffers({"q": self.q_ll, "rec": self.rec_ll}, group)
         arr = lambda xs: (ct.c_void_p * W)(*xs)  # noqa: E731
@@ -206,7 +209,8 @@ class LLDecode:
         self.capi.check(self.capi.LIB.sda_ll_partial_attention(
             st, self.q_ll.data_ptr(), self.wire, sh.k.data_ptr(), sh.v.data_ptr(), self.ops._dtype_code(sh.k),
             sh.capacity, sh.kv_len.data_ptr(), self.W, self.Bp, self.Hq, sh.k.shape[1], self.d, self.S, self.ll_rec,
-            self.epoch.data_ptr()), "sda_ll_partial_attention")
+            self.epoch.data_ptr(), None if self.gqa_work is None else self.gqa_work.data_ptr()),
+            "sda_ll_partial_attention")
 
     def finish(self, out: torch.Tensor):
         """K3: span_finish_layer over every domain's split records; opens the next epoch."""

@@ -381,3 +381,31 @@ def test_full_size_c3_prefill_sampled_parity():
     ref = C.scrambled_step(ss, 1, 0, H, h, qf[h].double().cpu().numpy(), L, [kf[h].double().cpu().numpy()],
                            [vf[h].double().cpu().numpy()], wire_fmt=2, shard_first_pos=[0])
     assert max_abs_rel(got[h], ref) < TOL_BF16 and rel_fro(got[h], ref) < TOL_BF16
+
+
+def test_ll_decode_world1_gqa_tensor_core():
+    """The LL-chained step on a GQA shard (16 q / 2 kv heads): Q' unpacked from its LL words, the
+    tensor-core GQA kernel writing LL split records, K3 over them -- against the oracle and the
+    reference-shaped step, over several epochs."""
+    from paper_2605_25716_b200 import distributed as sdist
+    B, Hq, Hkv, D, LK = 3, 16, 2, 128, 2048
+    cases = [Case(B=B, Hq=Hq, Hkv=Hkv, d=D, lk=LK, n_nodes=1, lq=1, dtype=torch.bfloat16, seed=91 + i) for i in range(3)]
+    keys = protocol.DomainKeys(cases[0].request_ids(), 0, 1, Hkv, D, "cuda")
+    shard = protocol.KVShard(B, Hkv, LK, D, "cuda")
+    shard.ship_segment(dev(cases[0].k[0], torch.bfloat16), dev(cases[0].v[0], torch.bfloat16), keys, first_pos=0)
+    lld = sdist.LLDecode(B, Hq, D, [keys], shard, kv_heads=Hkv)
+    assert lld.gqa_work is not None
+    bufs = sdist.StepBuffers.allocate(1, B, Hq, 1, D, torch.bfloat16, "cuda")
+    comp = sdist.gpu_rank_compute([keys], shard, n_splits=lld.S, kv_heads=Hkv)
+    out = torch.empty((B, Hq, 1, D), dtype=torch.float32, device="cuda")
+    plain_out = torch.empty_like(out)
+    for i in range(3):
+        q = dev(cases[i].q, torch.bfloat16)
+        lld.step(q, out)
+        sdist.scrambled_decode_step(q, comp, bufs, plain_out)
+        got, same = out.double().cpu().numpy(), plain_out.double().cpu().numpy()
+        assert max_abs_rel(got, same) < 1e-5, i
+        c = cases[i]
+        c.k, c.v = cases[0].k, cases[0].v
+        ref = c.oracle()
+        assert max_abs_rel(got, ref) < TOL_BF16 and rel_fro(got, ref) < TOL_BF16, i
