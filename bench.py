@@ -28,6 +28,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 H, D, CTX, B_PER = 32, 128, 8192, 16
+HQ, HKV = H, H   # decode line's q / kv heads (config 5: GQA 64 / 8)
 CONFIG = 2   # BASELINE config of the decode line: 2 (default) or 4 (--config 4)
 METRIC = "scrambled-attn decode tokens/s"
 
@@ -55,8 +56,9 @@ def parse():
                     help="N>1: the exchange carried by K1/K2/K3 themselves in LL format over NVLink peer "
                          "memory (default), separate peer-memory push/wait kernels, or NCCL all-to-all")
     ap.add_argument("--ll-single", action="store_true", help="N=1: run the LL-chained step too (measured no faster)")
-    ap.add_argument("--config", type=int, choices=[2, 4], default=2,
-                    help="decode workload: BASELINE config 2 (default, the headline) or 4 (32K-token shard per GPU, batch 64)")
+    ap.add_argument("--config", type=int, choices=[2, 4, 5], default=2,
+                    help="decode workload: BASELINE config 2 (default, the headline), 4 (32K-token shard per GPU, "
+                         "batch 64) or 5 (GQA 64/8 heads, 64K-token shard per GPU, batch 32)")
     ap.add_argument("--cpu-pairs", type=int, default=128, help="(request, head) pairs in the CPU sample")
     return ap.parse_args()
 
@@ -79,25 +81,31 @@ def set_config(cfg: int, ws: int) -> None:
     """cfg 2: 16 requests per GPU, each request's 8K context sharded over the N GPUs (weak scaling
     in requests). cfg 4 (BASELINE: 8 nodes x 32K-token shard per node, batch-64 decode): 64
     requests in total, every GPU holds a 32K-token shard of each (weak scaling in context)."""
-    global CONFIG, CTX, B_PER
+    global CONFIG, CTX, B_PER, HQ, HKV
     CONFIG = cfg
     if cfg == 4:
         if 64 % ws:
             raise SystemExit("config 4 needs N dividing 64")
         CTX, B_PER = 32768 * ws, 64 // ws
+    if cfg == 5:   # GQA decode: 32 requests in total, a 64K-token shard of each per GPU
+        if 32 % ws:
+            raise SystemExit("config 5 needs N dividing 32")
+        CTX, B_PER, HQ, HKV = 65536 * ws, 32 // ws, 64, 8
 
 
 def workload_config(n):
-    desc = ("BASELINE cfg2 per GPU: scrambled decode, 32 heads x d128, 8K-token context per request "
-            "sharded over N domains (one per GPU), 16 requests per GPU, bf16 KV") if CONFIG == 2 else (
-        "BASELINE cfg4: scrambled decode, 32 heads x d128, batch 64 (64/N inquirer requests per GPU), "
-        "a 32K-token scrambled KV shard of every request on each of the N domains, bf16 KV")
+    desc = {2: "BASELINE cfg2 per GPU: scrambled decode, 32 heads x d128, 8K-token context per request "
+               "sharded over N domains (one per GPU), 16 requests per GPU, bf16 KV",
+            4: "BASELINE cfg4: scrambled decode, 32 heads x d128, batch 64 (64/N inquirer requests per GPU), "
+               "a 32K-token scrambled KV shard of every request on each of the N domains, bf16 KV",
+            5: "BASELINE cfg5 (decode part): GQA 64 q / 8 kv heads x d128, batch 32 (32/N inquirer requests per "
+               "GPU), a 64K-token scrambled KV shard of every request on each of the N domains, bf16 KV"}[CONFIG]
     return {
         "workload": desc,
-        "requests_per_gpu": B_PER, "global_batch": B_PER * n, "q_heads": H, "kv_heads": H, "head_dim": D,
+        "requests_per_gpu": B_PER, "global_batch": B_PER * n, "q_heads": HQ, "kv_heads": HKV, "head_dim": D,
         "context_per_request": CTX, "kv_rows_per_request_per_gpu": CTX // n, "domains": n,
-        "kv_bytes_per_gpu": B_PER * n * H * (CTX // n) * D * 2 * 2,
-        "l2": f"inputs larger than L2 ({B_PER * n * H * (CTX // n) * D * 4 / 2**30:.0f} GiB scrambled KV per GPU vs "
+        "kv_bytes_per_gpu": B_PER * n * HKV * (CTX // n) * D * 2 * 2,
+        "l2": f"inputs larger than L2 ({B_PER * n * HKV * (CTX // n) * D * 4 / 2**30:.0f} GiB scrambled KV per GPU vs "
               "126 MB L2), no flush needed",
         "parallelism": f"kv-sharded x{n} (one domain per GPU)",
     }
@@ -174,9 +182,11 @@ def cpu_reference(n_nodes: int, pairs: int, threads: int, steps: int = 3):
     if REF is None:
         raise RuntimeError("oracle/_ref/libsdattn_ref.so not built")
     secs = np.zeros(max(steps, 1))
-    REF.lib.ref_bench_decode(pairs, n_nodes, CTX // n_nodes, D, H, threads, 2, max(steps, 1),
+    # a (request, q head) pair costs one shard attention on its kv head's keys (GQA: HQ / HKV q
+    # heads share a key set; the reference itself has no GQA)
+    REF.lib.ref_bench_decode(pairs, n_nodes, CTX // n_nodes, D, HKV, threads, 2, max(steps, 1),
                              secs.ctypes.data_as(__import__("ctypes").POINTER(__import__("ctypes").c_double)))
-    return [(pairs / t) / H for t in secs], list(secs)
+    return [(pairs / t) / HQ for t in secs], list(secs)
 
 
 def run_reference_arm(args, ws, rank):
@@ -189,7 +199,7 @@ def run_reference_arm(args, ws, rank):
     vals, walls = vals[args.warmup:], walls[args.warmup:]
     value = statistics.median(vals)
     sample = (f"{args.cpu_pairs} (request, head) pairs of the workload per step ({ws} shard(s) x {CTX // ws} keys, "
-              f"d{D}, bf16 wire, f64 math), {threads} threads; tokens/s = pairs/s / {H} heads")
+              f"d{D}, bf16 wire, f64 math), {threads} threads; tokens/s = pairs/s / {HQ} heads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(walls),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -221,42 +231,42 @@ def run_ours(args, ws, rank, local):
     rid = lambda b: b + 1  # noqa: E731
 
     # --- compute-node state: this rank's domain (rank + 1) shard for all requests -------------
-    owner_keys = protocol.DomainKeys([rid(b) for b in range(B_tot)], 0, rank + 1, H, D, devn)
-    shard = protocol.KVShard(B_tot, H, L, D, devn, torch.bfloat16)
+    owner_keys = protocol.DomainKeys([rid(b) for b in range(B_tot)], 0, rank + 1, HKV, D, devn)
+    shard = protocol.KVShard(B_tot, HKV, L, D, devn, torch.bfloat16)
     g = torch.Generator(device=devn).manual_seed(1000 + rank)
     chunk = 16 if L <= 8192 else 4
     for b0 in range(0, B_tot, chunk):  # context owners ship their segments (K1 into the cache)
         b1 = min(B_tot, b0 + chunk)
-        kp = torch.randn((b1 - b0, H, L, D), generator=g, device=devn).to(torch.bfloat16)
-        vp = torch.randn((b1 - b0, H, L, D), generator=g, device=devn).to(torch.bfloat16)
+        kp = torch.randn((b1 - b0, HKV, L, D), generator=g, device=devn).to(torch.bfloat16)
+        vp = torch.randn((b1 - b0, HKV, L, D), generator=g, device=devn).to(torch.bfloat16)
         p, _ = owner_keys.span_perms(1, rank * L, L)
         ops.scramble(kp, owner_keys.dev[b0:b1], capi.PHI_INV_T, capi.KEYS_KQ, p[b0:b1].contiguous(),
-                     out=shard.k[b0:b1], key_heads=H)
+                     out=shard.k[b0:b1], key_heads=HKV)
         ops.scramble(vp, owner_keys.dev[b0:b1], capi.PHI_FORWARD, capi.KEYS_V, p[b0:b1].contiguous(),
-                     out=shard.v[b0:b1], key_heads=H)
+                     out=shard.v[b0:b1], key_heads=HKV)
         del kp, vp
     shard.rows = L
     shard.kv_len.fill_(L)
     del owner_keys
 
     # --- inquirer state: keys for my requests on every domain ---------------------------------
-    inq_keys = [protocol.DomainKeys([rid(b) for b in my_reqs], 0, dom + 1, H, D, devn) for dom in range(ws)]
-    q = torch.randn((B_PER, H, 1, D), generator=g, device=devn).to(torch.bfloat16)
-    S = capi.default_splits(B_tot, H, 1, L)
-    out = torch.empty((B_PER, H, 1, D), dtype=torch.float32, device=devn)
+    inq_keys = [protocol.DomainKeys([rid(b) for b in my_reqs], 0, dom + 1, HKV, D, devn) for dom in range(ws)]
+    q = torch.randn((B_PER, HQ, 1, D), generator=g, device=devn).to(torch.bfloat16)
+    S = capi.default_splits(B_tot, HQ, 1, L, kv_heads=HKV, head_dim=D)
+    out = torch.empty((B_PER, HQ, 1, D), dtype=torch.float32, device=devn)
     stream = torch.cuda.current_stream()
     k2_ev = []
     record = {"on": False}
 
     if ws == 1:
-        q_s = torch.empty((B_PER, H, 1, D), dtype=torch.bfloat16, device=devn)
-        o_parts = torch.empty((S, B_tot, H, 1, D), dtype=torch.float32, device=devn)
-        st_parts = torch.empty((S, B_tot, H, 1, 2), dtype=torch.float32, device=devn)
+        q_s = torch.empty((B_PER, HQ, 1, D), dtype=torch.bfloat16, device=devn)
+        o_parts = torch.empty((S, B_tot, HQ, 1, D), dtype=torch.float32, device=devn)
+        st_parts = torch.empty((S, B_tot, HQ, 1, 2), dtype=torch.float32, device=devn)
         srcs = ops.sources_from_splits(o_parts, st_parts, inq_keys[0].dev, None)
 
         def step(qin):
             # K1 (Q', span_perm over one row is the identity) -> K2 -> K3 (fold splits + unscramble)
-            ops.scramble(qin, inq_keys[0].dev, capi.PHI_FORWARD, capi.KEYS_KQ, None, out=q_s, key_heads=H)
+            ops.scramble(qin, inq_keys[0].dev, capi.PHI_FORWARD, capi.KEYS_KQ, None, out=q_s, key_heads=HKV)
             if record["on"]:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -265,18 +275,18 @@ def run_ours(args, ws, rank, local):
             if record["on"]:
                 e1.record(stream)
                 k2_ev.append((e0, e1))
-            return ops.unscramble_merge(srcs, out=out, key_heads=H)
+            return ops.unscramble_merge(srcs, out=out, key_heads=HKV)
         step_k2 = step
         if args.exchange == "ll" and args.ll_single:   # the same kernels LL-chained (W = 1): no faster
             from paper_2605_25716_b200 import distributed as sdist
-            lld = sdist.LLDecode(B_PER, H, D, inq_keys, shard, n_splits=S, kv_heads=H)
+            lld = sdist.LLDecode(B_PER, HQ, D, inq_keys, shard, n_splits=S, kv_heads=HKV)
 
             def step(qin):   # noqa: F811
                 return lld.step(qin, out)
     else:
         from paper_2605_25716_b200 import distributed as sdist
-        bufs = sdist.StepBuffers.allocate(ws, B_PER, H, 1, D, torch.bfloat16, devn)
-        comp = sdist.gpu_rank_compute(inq_keys, shard, n_splits=S, kv_heads=H)
+        bufs = sdist.StepBuffers.allocate(ws, B_PER, HQ, 1, D, torch.bfloat16, devn)
+        comp = sdist.gpu_rank_compute(inq_keys, shard, n_splits=S, kv_heads=HKV)
         serve0 = comp.serve
 
         def serve_timed(q_all, o_out, st_out):
@@ -296,7 +306,7 @@ def run_ours(args, ws, rank, local):
             return sdist.scrambled_decode_step(qin, comp, bufs, out, exchange=exch)
         step_k2 = step
         if args.exchange == "ll":
-            lld = sdist.LLDecode(B_PER, H, D, inq_keys, shard, n_splits=S, kv_heads=H)
+            lld = sdist.LLDecode(B_PER, HQ, D, inq_keys, shard, n_splits=S, kv_heads=HKV)
 
             def step(qin):   # noqa: F811
                 return lld.step(qin, out)
@@ -355,7 +365,7 @@ def run_ours(args, ws, rank, local):
 
     # ---- end to end through the public API with host buffers -----------------------------------
     q_host = q.cpu().pin_memory()
-    out_host = torch.empty((B_PER, H, 1, D), dtype=torch.float32).pin_memory()
+    out_host = torch.empty((B_PER, HQ, 1, D), dtype=torch.float32).pin_memory()
     q_dev = torch.empty_like(q)
 
     def e2e_step():
@@ -396,8 +406,8 @@ def run_ours(args, ws, rank, local):
     except (OSError, ValueError):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    kv_bytes = B_tot * H * L * D * 2 * 2
-    k2_bytes = kv_bytes + B_tot * H * D * 2 + B_tot * H * (4 * D + 8)
+    kv_bytes = B_tot * HKV * L * D * 2 * 2
+    k2_bytes = kv_bytes + B_tot * HQ * D * 2 + B_tot * HQ * (4 * D + 8)
     achieved = k2_bytes / (k2_ms * 1e-3) / 1e9
     traffic = None
     try:
@@ -415,9 +425,10 @@ def run_ours(args, ws, rank, local):
             "data": "synthetic (torch.randn Q/K/V, bf16), keys from the reference key-derivation rule",
             "config": dict(workload_config(ws), exchange=EXCHANGE_DESC[args.exchange] if ws > 1 else "none (single domain)"),
             "e2e": {"value": B_tot / (e2e_ms * 1e-3), "unit": "tokens/s",
-                    "h2d_bytes_per_step": B_PER * H * D * 2, "d2h_bytes_per_step": B_PER * H * D * 4},
+                    "h2d_bytes_per_step": B_PER * HQ * D * 2, "d2h_bytes_per_step": B_PER * HQ * D * 4},
             "gpu_launches": int(launches) * args.steps, "cuda_graph": bool(args.graph),
-            "roofline": {"bound": "hbm", "kernel": "k2_decode_kernel<128,bf16,bf16>" + ("" if ws == 1 else " + split fold"), "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": ("k2_gqa_tc_kernel<16>" if HKV < HQ else "k2_decode_kernel<128,bf16,bf16>")
+                         + ("" if ws == 1 else " + split fold"), "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": k2_bytes, "k2_ms": k2_ms,
                          "k2_share_of_step": k2_ms / ms_max, "peak_source": "MEASURED_PEAKS.json hbm_gbs"
