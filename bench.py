@@ -56,9 +56,10 @@ def parse():
                     help="N>1: the exchange carried by K1/K2/K3 themselves in LL format over NVLink peer "
                          "memory (default), separate peer-memory push/wait kernels, or NCCL all-to-all")
     ap.add_argument("--ll-single", action="store_true", help="N=1: run the LL-chained step too (measured no faster)")
-    ap.add_argument("--config", type=int, choices=[2, 4, 5], default=2,
-                    help="decode workload: BASELINE config 2 (default, the headline), 4 (32K-token shard per GPU, "
-                         "batch 64) or 5 (GQA 64/8 heads, 64K-token shard per GPU, batch 32)")
+    ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2,
+                    help="BASELINE config: 2 (default: the decode headline), 3 (prefill across GPUs: a 2K-token span "
+                         "per GPU vs a 16K-token shard per domain), 4 (decode, 32K-token shard per GPU, batch 64) or "
+                         "5 (GQA decode, 64K-token shard per GPU, batch 32)")
     ap.add_argument("--cpu-pairs", type=int, default=128, help="(request, head) pairs in the CPU sample")
     return ap.parse_args()
 
@@ -451,7 +452,7 @@ def run_ours(args, ws, rank, local):
                 vals, secs = cpu_reference(1, args.cpu_pairs, threads, 5)
                 line["cpu_baseline"] = {"value": statistics.median(vals), "unit": "tokens/s", "cores": threads,
                                         "kind": "reference",
-                                        "sample": f"{args.cpu_pairs} (request, head) pairs x 8192 keys x d128 of "
+                                        "sample": f"{args.cpu_pairs} (request, head) pairs x {CTX} keys x d128 of "
                                                   f"the workload through the reference's own enc->shard_attention->"
                                                   f"dec->merge (oracle/_ref, f64), median of 5 steps of "
                                                   f"{statistics.median(secs):.3f} s wall on {threads} threads"}
@@ -462,6 +463,124 @@ def run_ours(args, ws, rank, local):
         torch.cuda.synchronize()
         dist.barrier(device_ids=[local])
         # leave without tearing NCCL down (communicator teardown can stall at exit); all work is done
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
+
+
+def run_prefill_dist(args, ws, rank, local):
+    """--config 3 (BASELINE: 4 nodes x 16K-token KV shard, 2K-token prefill with the scramble +
+    permutation fused into the KV write) on N GPUs: every rank is the inquirer for one 2K-token
+    span and holds a 16K-token scrambled shard of every span's earlier context. One step = the
+    span's own K/V scrambled into the local cache + K1 of Q' for every domain (p_q), the Q'
+    exchange, tensor-core prefill K2 of every span against this rank's shard, the (O', stats)
+    exchange and K3. Reference-shaped exchange (peer-memory push/wait kernels, or NCCL with
+    --exchange nccl): the LL form covers decode only. Prints one prefill TFLOP/s line."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_25716_b200 import capi, ops, protocol
+    from paper_2605_25716_b200 import distributed as sdist
+
+    torch.cuda.set_device(local)
+    devn = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=devn)
+    LQ, LK = 2048, 16384
+    rid = lambda b: b + 1  # noqa: E731
+    stream = torch.cuda.current_stream()
+    # this rank's domain shard of every span's context (+ room for its own span's rows)
+    owner = protocol.DomainKeys([rid(b) for b in range(ws)], 0, rank + 1, H, D, devn)
+    shard = protocol.KVShard(ws, H, LK + LQ, D, devn, torch.bfloat16)
+    g = torch.Generator(device=devn).manual_seed(3000 + rank)
+    kp = torch.randn((ws, H, LK, D), generator=g, device=devn).to(torch.bfloat16)
+    vp = torch.randn((ws, H, LK, D), generator=g, device=devn).to(torch.bfloat16)
+    shard.ship_segment(kp, vp, owner, first_pos=rank * LK)
+    del kp, vp
+    inq = [protocol.DomainKeys([rid(rank)], 0, dom + 1, H, D, devn) for dom in range(ws)]
+    q_first = ws * LK
+    q = torch.randn((1, H, LQ, D), generator=g, device=devn).to(torch.bfloat16)
+    kn = torch.randn((1, H, LQ, D), generator=g, device=devn).to(torch.bfloat16)
+    vn = torch.randn((1, H, LQ, D), generator=g, device=devn).to(torch.bfloat16)
+    own_shard = protocol.KVShard(1, H, LQ, D, devn, torch.bfloat16)   # the span's own K/V (local cache)
+    pkv, _ = inq[rank].span_perms(1, q_first, LQ)
+    k1_jobs = [ops.scramble_job(kn, inq[rank].dev, capi.PHI_INV_T, capi.KEYS_KQ, pkv, out=own_shard.k, key_heads=H),
+               ops.scramble_job(vn, inq[rank].dev, capi.PHI_FORWARD, capi.KEYS_V, pkv, out=own_shard.v, key_heads=H)]
+    S = capi.default_splits(ws, H, LQ, LK)
+    comp = sdist.gpu_rank_compute(inq, shard, n_splits=S, kv_heads=H, q_first_pos=q_first)
+    bufs = sdist.StepBuffers.allocate(ws, 1, H, LQ, D, torch.bfloat16, devn)
+    exch = sdist.PeerExchange(bufs) if ws > 1 and args.exchange != "nccl" else None
+    out = torch.empty((1, H, LQ, D), dtype=torch.float32, device=devn)
+
+    def step(qin):
+        ops.scramble_batch(k1_jobs, D)   # the span's K/V into the cache, scramble + permute fused
+        return sdist.scrambled_decode_step(qin, comp, bufs, out, exchange=exch)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        step(q)
+    torch.cuda.synchronize()
+    c0 = capi.launch_count()
+    step(q)
+    launches = capi.launch_count() - c0
+    barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(q)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    # end to end: Q span from pinned host memory in, O back out
+    q_host, out_host, q_dev = q.cpu().pin_memory(), torch.empty((1, H, LQ, D)).pin_memory(), torch.empty_like(q)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        q_dev.copy_(q_host, non_blocking=True)
+        out_host.copy_(step(q_dev), non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        tt = torch.tensor([ms, e2e_ms], device=devn)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, e2e_ms = float(tt[0]), float(tt[1])
+    flops = 4.0 * LQ * LK * H * D * ws * ws   # every span against every domain's shard
+    if rank == 0:
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except (OSError, ValueError):
+            pass
+        peak = float(peaks.get("bf16_tflops", 1590.0)) * ws
+        value = flops / (ms * 1e-3) / 1e12
+        emit({"metric": "scrambled-attn prefill TFLOP/s", "value": value, "unit": "TFLOP/s", "n_gpus": ws,
+              "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+              "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+              "data": "synthetic (torch.randn Q/K/V, bf16), keys from the reference key-derivation rule",
+              "config": {"workload": "BASELINE cfg3: one 2K-token prefill span per GPU against a 16K-token scrambled "
+                                     "KV shard of every span on each of the N domains (+ the span's own K/V scrambled "
+                                     "into the cache), 32 heads x d128, bf16",
+                         "q_rows": LQ, "kv_rows_per_domain": LK, "domains": ws, "splits": S,
+                         "exchange": ("none (single domain)" if ws == 1 else EXCHANGE_DESC[args.exchange if args.exchange != "ll" else "p2p"]),
+                         "l2": "inputs larger than L2, no flush needed"},
+              "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                      "h2d_bytes_per_step": LQ * H * D * 2, "d2h_bytes_per_step": LQ * H * D * 4},
+              "gpu_launches": int(launches) * args.steps, "cuda_graph": False,
+              "roofline": {"bound": "tensor", "kernel": "k2_prefill_tc_kernel (whole step)", "achieved": value,
+                           "peak": peak, "unit": "TFLOP/s", "frac": value / peak,
+                           "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) x N"},
+              "clocks": clk.summary()})
+    if ws > 1:
+        torch.cuda.synchronize()
+        dist.barrier(device_ids=[local])
         sys.stdout.flush()
         sys.stderr.flush()
         os._exit(0)
@@ -652,8 +771,16 @@ def main():
     if args.gpus != ws and ws > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {ws}", file=sys.stderr)
     set_config(args.config, ws)
+    if args.impl == "reference" and args.config == 3:
+        if rank == 0:
+            emit({"impl": "reference", "unavailable": "config 3 (multi-GPU prefill) has no reference arm here: the "
+                                                      "reference's f64 prefill takes minutes per step; see the N=1 "
+                                                      "prefill line of the default run"})
+        return
     if args.impl == "reference":
         run_reference_arm(args, ws, rank)
+    elif args.config == 3:
+        run_prefill_dist(args, ws, rank, local)
     else:
         run_ours(args, ws, rank, local)
 
