@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p, cons
     // LL exchange: write straight into the destination's receive slot, epoch-tagged
     const bool ll = FLAT && p.epoch != nullptr;
     const uint32_t ep = ll ? *p.epoch : 0u;
-    if (ll) pdl_trigger();   // K2 may launch right away: it spins on the LL words, not on K1
+    pdl_trigger();   // K2 may launch right away (it waits on K1's grid, or spins on the LL words)
     const int64_t out_elem = ((ll ? xb : b) * p.n_heads + h) * p.out_rows_cap * D + p.out_row_offset * D;
     Tout* out = ll ? nullptr : static_cast<Tout*>(p.out) + out_elem;
     const uint32_t* perm = p.perm ? p.perm + b * p.perm_bstride : nullptr;

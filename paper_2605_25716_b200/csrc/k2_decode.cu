@@ -47,7 +47,8 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
     const int kvh = h / (p.q_heads / p.kv_heads);
     const bool ll = p.epoch != nullptr;   // LL exchange (decode): Q' in, the split's record out
     const uint32_t ep = ll ? *p.epoch : 0u;
-    if (ll) pdl_trigger();   // K3 may launch as soon as every K2 CTA has read the epoch
+    if (!ll) pdl_wait();   // launched early behind K1 (PDL): its Q' must be complete; LL spins instead
+    pdl_trigger();         // K3 may launch once every K2 CTA is running (it waits on this grid or on LL)
 
     int64_t len = p.kv_len ? (int64_t)p.kv_len[b] : p.kv_cap;
     if (p.causal) {   // keys j <= qr + offset only (AttentionMask::causal, attention.cpp:16-27)
@@ -188,9 +189,7 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
 template <int D, typename TQ, typename TKV>
 static cudaError_t launch_k2_t(const K2Params& p, cudaStream_t st) {
     const dim3 grid((unsigned)p.n_splits, (unsigned)p.q_heads, (unsigned)(p.n_batch * p.q_rows));
-    if (p.epoch) return pdl_launch(k2_decode_kernel<D, TQ, TKV>, grid, dim3(128), st, p);
-    k2_decode_kernel<D, TQ, TKV><<<grid, 128, 0, st>>>(p);
-    return cudaGetLastError();
+    return pdl_launch(k2_decode_kernel<D, TQ, TKV>, grid, dim3(128), st, p);
 }
 
 template <int D>

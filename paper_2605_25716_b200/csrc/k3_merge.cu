@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
     const int64_t total = p.n_batch * p.q_heads * p.q_rows;
     const bool ll = p.ll != 0;   // LL exchange: records arrive epoch-tagged in peer memory
     const uint32_t ep = ll ? *p.epoch : 0u;
+    if (!ll) pdl_wait();         // launched early behind K2 (PDL): its partials must be complete
     const int64_t row_raw = (int64_t)blockIdx.x * 4 + warp;
     const bool active = row_raw < total;
     const int64_t row = active ? row_raw : total - 1;   // inactive warps compute a dummy row, store nothing
@@ -289,6 +290,7 @@ __global__ void __launch_bounds__(128) k3_merge_small_kernel(const K3Params p) {
     float* sh = sh_all[warp];
     const int64_t total = p.n_batch * p.q_heads * p.q_rows;
     const int n = EXACT ? NS : p.n_src;   // !EXACT: n_src <= NS, guarded
+    pdl_wait();   // launched early behind K2 (PDL): its partials must be complete
 
     // RPW rows per warp, all of their sources' stats and O' rows in flight at once (NS = n_src
     // exactly; rows and their (b, h, r) decomposition fit 32 bits, checked by the launcher)
@@ -403,7 +405,8 @@ template <int D, typename TOut, int NS, bool EXACT = true>
 static void launch_k3_small(const K3Params& p, int64_t total, cudaStream_t st) {
     constexpr int RPW = NS * (D / 32) <= 16 ? 2 : 1;   // in-flight rows per warp (4 measured slower)
     const int64_t per_cta = 4 * RPW;
-    k3_merge_small_kernel<D, TOut, NS, RPW, EXACT><<<(unsigned)((total + per_cta - 1) / per_cta), 128, 0, st>>>(p);
+    pdl_launch(k3_merge_small_kernel<D, TOut, NS, RPW, EXACT>, dim3((unsigned)((total + per_cta - 1) / per_cta)), dim3(128),
+               st, p);
 }
 
 template <int D, typename TOut>
@@ -429,7 +432,7 @@ static cudaError_t launch_k3_t(const K3Params& p, cudaStream_t st) {
             default: launch_k3_small<D, TOut, 8>(p, total, st); break;
         }
     } else {
-        k3_merge_kernel<D, TOut><<<(unsigned)((total + 3) / 4), 128, 0, st>>>(p);
+        return pdl_launch(k3_merge_kernel<D, TOut>, dim3((unsigned)((total + 3) / 4)), dim3(128), st, p);
     }
     return cudaGetLastError();
 }
