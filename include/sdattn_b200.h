@@ -273,6 +273,18 @@ sda_status sda_ll_partial_attention(void* stream, const void* ll_q, int32_t wire
                                     int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int32_t n_dest,
                                     int64_t b_per, int32_t q_heads, int32_t kv_heads, int32_t head_dim,
                                     int32_t n_splits, void* const* ll_rec, const uint32_t* epoch, void* gqa_work);
+/* Remote records for prefill spans (q_rows >= 64, tensor-core form, one split): K2 over
+ *   q [n_dest * b_per][q_heads][q_rows][d] (requests sender-major) writing request (dest, i)'s
+ *   packed record [q_heads * q_rows * d O' | q_heads * q_rows * 2 stats] straight into
+ *   rec_peer[dest] + i * rec_stride floats (the inquirer's receive slot, peer memory); the CTA
+ *   completing a destination raises *peer_flag[dest] = *epoch (system-scope release), which the
+ *   inquirer's sda_exchange_wait consumes. Replaces K2 + split fold + sda_exchange_push on the
+ *   return path. dest_counters: n_dest zeroed u32 (self-resetting). */
+sda_status sda_partial_attention_remote(void* stream, const void* q, int32_t q_dtype, const void* k, const void* v,
+                                        int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int32_t n_dest,
+                                        int64_t b_per, int32_t q_heads, int32_t kv_heads, int64_t q_rows,
+                                        int32_t head_dim, float* const* rec_peer, int64_t rec_stride,
+                                        uint32_t* const* peer_flag, const uint32_t* epoch, uint32_t* dest_counters);
 /* sda_ll_unscramble_merge: K3 over this rank's record slots (n_domains * n_splits sources, each
  *   domain unscrambled with its phi_V^-1 from keys[(domain * B_p + b)]) into out [B_p][H][1][d];
  *   then *epoch += 1. done_counter: one zeroed u32 (self-resetting). */

@@ -33,7 +33,8 @@ EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_
            "sda_ll_scramble_q", "sda_ll_partial_attention", "sda_ll_unscramble_merge", "sda_trace_timestamp", "sda_scramble_batch",
            "sda_quantize_affine", "sda_dequantize", "sda_quant_roundtrip",
            "sda_frame_elements", "sda_frame_payload_bytes", "sda_frame_bytes", "sda_frame_scratch_bytes",
-           "sda_frame_encode", "sda_frame_parse_header", "sda_frame_decode", "sda_crc32")
+           "sda_frame_encode", "sda_frame_parse_header", "sda_frame_decode", "sda_crc32",
+           "sda_partial_attention_remote")
 
 
 class SdaError(RuntimeError):
@@ -142,6 +143,9 @@ def _load() -> ct.CDLL:
     lib.sda_frame_parse_header.argtypes = [_vp, ct.c_uint64, ct.c_uint64, _ph]
     lib.sda_frame_decode.argtypes = [_vp, _vp, ct.c_uint64, _ph, _vp, ct.c_int32, _vp, _vp]
     lib.sda_crc32.argtypes = [_vp, _vp, ct.c_uint64, _vp, _vp]
+    lib.sda_partial_attention_remote.argtypes = [_vp, _vp, ct.c_int32, _vp, _vp, ct.c_int32, ct.c_int64, _vp,
+                                                 ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32,
+                                                 _pp, ct.c_int64, _pp, _vp, _vp]
     lib.sda_quantize_affine.argtypes = [_vp, _vp, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32, _vp, ct.c_int64,
                                         _vp, _vp, _vp, _vp]
     lib.sda_dequantize.argtypes = [_vp, _vp, ct.c_int64, _vp, _vp, ct.c_int64, ct.c_int64, ct.c_int32, _vp, ct.c_int32]

@@ -480,6 +480,38 @@ sda_status sda_ll_partial_attention(void* stream, const void* ll_q, int32_t wire
     return from_cuda(sda::launch_k2_decode(p, head_dim, wire_dtype, kv_dtype, st));
 }
 
+sda_status sda_partial_attention_remote(void* stream, const void* q, int32_t q_dtype, const void* k, const void* v,
+                                        int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int32_t n_dest,
+                                        int64_t b_per, int32_t q_heads, int32_t kv_heads, int64_t q_rows,
+                                        int32_t head_dim, float* const* rec_peer, int64_t rec_stride,
+                                        uint32_t* const* peer_flag, const uint32_t* epoch, uint32_t* dest_counters) {
+    if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
+    if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
+    if (!q || !k || !v || !rec_peer || !peer_flag || !epoch || !dest_counters || n_dest <= 0 ||
+        n_dest > sda::kMaxPeers || b_per <= 0 || q_heads <= 0 || kv_heads <= 0 || q_heads % kv_heads != 0 ||
+        q_rows <= 0 || !valid_dtype(q_dtype) || !valid_dtype(kv_dtype) || rec_stride < (int64_t)q_heads * q_rows * (head_dim + 2))
+        return SDA_ERR_INVALID_ARGUMENT;
+    for (int i = 0; i < n_dest; ++i)
+        if (!rec_peer[i] || !peer_flag[i]) return SDA_ERR_INVALID_ARGUMENT;
+    const int64_t n_batch = (int64_t)n_dest * b_per;
+    if (n_batch * q_rows > 65535 || q_heads > 65535) return SDA_ERR_UNSUPPORTED;
+    sda::K2Params p{q, k, v, kv_len, nullptr, nullptr, kv_cap, n_batch, q_rows, q_heads, kv_heads, 1,
+                    (float)(1.0 / std::sqrt((double)head_dim)), 0, 0};
+    if (!sda::k2_prefill_tc_eligible(p, head_dim, q_dtype, kv_dtype) || (q_heads / kv_heads > 1 && q_rows < 64))
+        return SDA_ERR_UNSUPPORTED;   // the tensor-core prefill form only (one split per request)
+    p.remote_rec = 1;
+    p.epoch = epoch;
+    p.b_per = b_per;
+    p.rec_stride = rec_stride;
+    for (int i = 0; i < n_dest; ++i) {
+        p.ll_rec[i] = rec_peer[i];
+        p.peer_flag[i] = peer_flag[i];
+    }
+    p.dest_counters = dest_counters;
+    ++g_launches;
+    return from_cuda(sda::launch_k2_prefill_tc(p, static_cast<cudaStream_t>(stream)));
+}
+
 sda_status sda_ll_unscramble_merge(void* stream, const void* ll_rec, int32_t n_domains, int32_t n_splits,
                                    const void* keys, int64_t keys_batch_stride, int32_t key_heads, int64_t b_per,
                                    int32_t q_heads, int32_t head_dim, void* out, int32_t out_dtype, uint32_t* epoch,

@@ -243,6 +243,12 @@ inline cudaError_t pdl_launch(Kern kernel, dim3 grid, dim3 block, cudaStream_t s
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+// raise a peer's flag to the step epoch with a system-scope release store (the waiting side
+// polls it with acquire loads: exchange.cu wait_kernel)
+__device__ __forceinline__ void flag_raise(uint32_t* flag, uint32_t e) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(e) : "memory");
+}
+
 // LL ("low-latency") peer-memory format for the decode exchange: every 4-byte data word is
 // stored next to the 4-byte step epoch, two (data, epoch) pairs per 16-byte store. An aligned
 // 8-byte half is written as one unit, so a reader that polls its words until both epochs match

@@ -40,6 +40,14 @@ struct K2TcParams {
     int grouped;           // 1: GQA decode mode, one CTA per (request, kv head): its G = Hq/Hkv
                            //    q heads x Lq rows (contiguous in Q) form the Q tile
     float scale_log2;      // log2(e) / sqrt(d)
+    // remote records (K2Params): O' / stats of request b straight into peer dest = b / b_per
+    int remote;
+    int64_t b_per;
+    int64_t rec_stride;
+    float* rec_peer[kMaxPeers];
+    uint32_t* peer_flag[kMaxPeers];
+    uint32_t* dest_counters;
+    const uint32_t* epoch;
 };
 
 #ifdef SDA_K2_TRACE
@@ -354,13 +362,28 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
         const bool store = r_in < nrows;
         // output rows mirror the Q rows ([split][request][q head][q row]); head_row already holds
         // request, head and row-tile offsets
-        const int64_t orow = (int64_t)split * p.n_batch * p.q_heads * p.q_rows + head_row + r_in;
+        int64_t orow = (int64_t)split * p.n_batch * p.q_heads * p.q_rows + head_row + r_in;
+        float* out_o = p.out_o;
+        float* out_stats = p.out_stats;
+        if (p.remote) {   // the packed record of request b in its inquirer's receive slot (one split)
+            const int64_t dest = b / p.b_per, i = b % p.b_per;
+            float* rec = p.rec_peer[dest] + i * p.rec_stride;
+            orow = head_row - b * p.q_heads * p.q_rows + r_in;   // (head, row) within the request
+            out_o = rec;
+            out_stats = rec + (int64_t)p.q_heads * p.q_rows * D;
+        }
         if (group_live && warp_live) {
             if (nkv > 0) {
                 tc::mbar_wait(&o_final[g], 0);
                 tc::tc_fence_after();
             }
             const float inv = l > 0.f ? 1.f / l : 0.f;
+            // remote records: stage the warp's 32 rows in SMEM (group 0 reuses the K ring, whose
+            // last reader has completed; group 1 the V ring) and write them as one contiguous
+            // 16 KB run -- whole 512-byte rows per warp store instead of 32 scattered 16-byte
+            // pieces, which NVLink carries far less efficiently
+            // (rows of 512 B, 16-byte chunks XOR-swizzled by row & 7 against bank conflicts)
+            float* stg = reinterpret_cast<float*>(smem + (g ? OFF_V : OFF_K) + (warp & 3) * 32 * 128 * 4);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 uint32_t o[16];
@@ -371,24 +394,50 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
 #pragma unroll
                     for (int e = 0; e < 16; ++e) o[e] = 0u;
                 }
-                if (store) {
-                    float4* dst = reinterpret_cast<float4*>(p.out_o + orow * D + c * 16);
+                if (p.remote) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        *reinterpret_cast<float4*>(stg + lane * 128 + (((c * 4 + e) ^ (lane & 7)) * 4)) =
+                            make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                        __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+                } else if (store) {
+                    float4* dst = reinterpret_cast<float4*>(out_o + orow * D + c * 16);
 #pragma unroll
                     for (int e = 0; e < 4; ++e)
                         dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
                                              __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
                 }
             }
+            if (p.remote) {
+                __syncwarp();
+                // rows orow(lane 0) .. +31 are consecutive: 32 x 512 B contiguous (the tail of a
+                // partial tile stops at nrows)
+                const int64_t row0 = orow - lane;
+                const int nvalid = (int)min((int64_t)32, nrows - (r_in - lane));
+                for (int r = 0; r < nvalid; ++r)
+                    reinterpret_cast<float4*>(out_o + (row0 + r) * D)[lane] =
+                        *reinterpret_cast<const float4*>(stg + r * 128 + ((lane ^ (r & 7)) * 4));
+            }
             if (store) {
                 const bool any = l > 0.f;
-                p.out_stats[orow * 2 + 0] = any ? m_run / kLog2e : -INFINITY;
-                p.out_stats[orow * 2 + 1] = any ? l * ex2(m_use - m_run) : 0.f;
+                out_stats[orow * 2 + 0] = any ? m_run / kLog2e : -INFINITY;
+                out_stats[orow * 2 + 1] = any ? l * ex2(m_use - m_run) : 0.f;
             }
         }
     }
+    if (p.remote) __threadfence_system();   // this CTA's record stores visible system-wide
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
+    if (p.remote && tid == 0) {   // the CTA completing a destination's records raises its flag
+        const int64_t dest = b / p.b_per;
+        const unsigned per_dest = gridDim.x * gridDim.y * (unsigned)(p.b_per * p.n_splits);
+        if (atomicAdd(&p.dest_counters[dest], 1u) == per_dest - 1) {
+            p.dest_counters[dest] = 0;
+            __threadfence_system();
+            flag_raise(p.peer_flag[dest], *p.epoch);
+        }
+    }
     if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
@@ -424,6 +473,15 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
     p.grouped = k2_grouped(q) ? 1 : 0;
     p.n_qpairs = p.grouped ? 1 : (int)((q.q_rows + 2 * TILE - 1) / (2 * TILE));
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+    p.remote = q.remote_rec;
+    p.b_per = q.b_per;
+    p.rec_stride = q.rec_stride;
+    for (int i = 0; i < kMaxPeers; ++i) {
+        p.rec_peer[i] = static_cast<float*>(q.ll_rec[i]);
+        p.peer_flag[i] = q.peer_flag[i];
+    }
+    p.dest_counters = q.dest_counters;
+    p.epoch = q.epoch;
     CUtensorMap qm, km, vm;
     if (!make_tmap_bf16_2d(&qm, q.q, q.n_batch * q.q_heads * q.q_rows, D, TILE) ||
         !make_tmap_bf16_2d(&km, q.k, q.n_batch * q.kv_heads * q.kv_cap, D, TILE) ||

@@ -68,6 +68,14 @@ struct K2Params {
     const uint32_t* epoch;
     int64_t b_per;
     void* ll_rec[kMaxPeers];
+    // remote records (prefill, one split): request b = (dest, i) writes its packed record
+    // [q_heads * q_rows * d O' | q_heads * q_rows * 2 stats] straight into ll_rec[dest] +
+    // i * rec_stride floats (a peer's receive slot, plain stores); the CTA completing a
+    // destination raises *peer_flag[dest] = *epoch (system-scope release)
+    int remote_rec;
+    int64_t rec_stride;
+    uint32_t* peer_flag[kMaxPeers];
+    uint32_t* dest_counters;   // [n_dest] zeroed, self-resetting
 };
 
 struct K3Source {

@@ -61,6 +61,9 @@ class RankCompute:
     serve: Callable[[torch.Tensor, torch.Tensor, tuple], None]       # (q_all, ret [B_tot, rec], dims): K2 + fold
     finish: Callable[[torch.Tensor, torch.Tensor, tuple], None]      # (ret_back [W, B_p, rec], out, dims): K3
     scramble_q_all: Optional[Callable[[torch.Tensor, torch.Tensor], None]] = None   # (q, q_send [W, ...]) one launch
+    # (q_all, dims, exchange) -> bool: K2 writing every request's record straight into its
+    # inquirer's receive slot and raising the return flags (False: not eligible, use serve)
+    serve_remote: Optional[Callable[[torch.Tensor, tuple, "PeerExchange"], bool]] = None
 
 
 def map_peer_buffers(bufs: dict, group: Optional[dist.ProcessGroup] = None):
@@ -244,6 +247,12 @@ def scrambled_decode_step(q: torch.Tensor, compute: RankCompute, bufs: StepBuffe
     if world > 1 and exchange is not None:
         exchange.exchange_q()                                         # SCR_Q over peer memory
         q_all = bufs.q_recv
+        b_tot = q_all.shape[0] * q_all.shape[1]
+        if compute.serve_remote is not None and compute.serve_remote(
+                q_all.view((b_tot,) + tuple(q_all.shape[2:])), bufs.dims, exchange):
+            exchange._wait(world)                                     # SCR_SHARD written by K2 itself
+            compute.finish(bufs.ret_recv, out, bufs.dims)
+            return out
     elif world > 1:
         dist.all_to_all_single(bufs.q_recv, bufs.q_send, group=group)   # SCR_Q
         q_all = bufs.q_recv
@@ -313,6 +322,20 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
         ops.unscramble_merge(ops.sources_from_splits(state["o"], state["st"]), out=ret,
                              out_stats=ret[:, Hq * Lq * d:], out_batch_stride=rec)
 
+    def serve_remote(q_all, dims, ex):
+        B, Hq, Lq, d = q_all.shape
+        if Lq < 64 or d != 128 or q_all.dtype != torch.bfloat16 or shard.k.dtype != torch.bfloat16:
+            return False
+        import ctypes as ct
+        L = capi.LIB
+        capi.check(L.sda_partial_attention_remote(
+            torch.cuda.current_stream().cuda_stream, q_all.data_ptr(), capi.SDA_BF16, shard.k.data_ptr(),
+            shard.v.data_ptr(), capi.SDA_BF16, shard.capacity, shard.kv_len.data_ptr(), ex.world, B // ex.world, Hq,
+            shard.k.shape[1], Lq, d, ct.cast(ex.r_args[1], ct.POINTER(ct.c_void_p)), Hq * Lq * (d + 2),
+            ct.cast(ex.r_args[2], ct.POINTER(ct.c_void_p)), ex.epoch.data_ptr(),
+            ex.counters.data_ptr() + 4 * ex.world), "sda_partial_attention_remote")
+        return True
+
     def finish(back, out, dims):
         Hq, Lq, d = dims
         W, Bp, rec = back.shape
@@ -321,4 +344,4 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
                                 batch_stride=rec, shape=(Bp, Hq, Lq, d)) for dom in range(W)]
         ops.unscramble_merge(srcs, out=out, key_heads=kv_heads or inquirer_keys[0].kv_heads)
 
-    return RankCompute(scramble_q, serve, finish, scramble_q_all)
+    return RankCompute(scramble_q, serve, finish, scramble_q_all, serve_remote)

@@ -64,8 +64,34 @@ def main():
         ok &= bool(torch.equal(out_n, out_p))
         worst_f = max(worst_f, float((out_f - out_n).abs().max() / out_n.abs().max()))
     ok_f = worst_f < 1e-5
+    # prefill spans (256 rows): the return path written by K2 itself into the inquirers' slots
+    # (sda_partial_attention_remote, one split) against the NCCL form with the same single split
+    # (different split counts round P to bf16 against different bases: ~1e-3 apart)
+    LQ, BQ = 256, 1
+    inq_p = [protocol.DomainKeys(list(range(rank * BQ + 1, rank * BQ + BQ + 1)), 0, d + 1, H, D, dev) for d in range(world)]
+    keys_p = protocol.DomainKeys(list(range(1, world * BQ + 1)), 0, rank + 1, H, D, dev)
+    shard_p = protocol.KVShard(world * BQ, H, L, D, dev)
+    shard_p.ship_segment(torch.randn((world * BQ, H, L, D), generator=g, device=dev).to(torch.bfloat16),
+                         torch.randn((world * BQ, H, L, D), generator=g, device=dev).to(torch.bfloat16), keys_p,
+                         first_pos=rank * L)
+    comp_p = sdist.gpu_rank_compute(inq_p, shard_p, n_splits=1, kv_heads=H, q_first_pos=world * L)
+    bufs_n = sdist.StepBuffers.allocate(world, BQ, H, LQ, D, torch.bfloat16, dev)
+    bufs_r = sdist.StepBuffers.allocate(world, BQ, H, LQ, D, torch.bfloat16, dev)
+    exch_r = sdist.PeerExchange(bufs_r)
+    pn = torch.empty((BQ, H, LQ, D), dtype=torch.float32, device=dev)
+    pr = torch.empty_like(pn)
+    worst_p = 0.0
+    for it in range(5):
+        q = torch.randn((BQ, H, LQ, D), generator=g, device=dev).to(torch.bfloat16)
+        sdist.scrambled_decode_step(q, comp_p, bufs_n, pn)
+        sdist.scrambled_decode_step(q, comp_p, bufs_r, pr, exchange=exch_r)
+        torch.cuda.synchronize()
+        worst_p = max(worst_p, float((pr - pn).abs().max() / pn.abs().max()))
+    ok_p = worst_p < 1e-5
+    ok &= ok_p
     print(f"rank {rank}: peer exchange == NCCL over 30 steps (eager + graph): {ok}; "
-          f"LL exchange max rel diff {worst_f:.2e} ({'ok' if ok_f else 'FAIL'})", flush=True)
+          f"LL exchange max rel diff {worst_f:.2e}; prefill remote records max rel diff {worst_p:.2e} "
+          f"({'ok' if ok_f and ok_p else 'FAIL'})", flush=True)
     ok &= ok_f
     torch.cuda.synchronize()
     dist.barrier(device_ids=[local])
