@@ -409,3 +409,36 @@ def test_ll_decode_world1_gqa_tensor_core():
         c.k, c.v = cases[0].k, cases[0].v
         ref = c.oracle()
         assert max_abs_rel(got, ref) < TOL_BF16 and rel_fro(got, ref) < TOL_BF16, i
+
+
+def test_many_splits_pipelined_merge_and_ragged_ll():
+    """K3's pipelined form (> 16 sources: 40 splits of a 8K-key shard) against the oracle, and the
+    LL step on a shard with ragged per-request lengths (kv_len < capacity, a split past the end of
+    a short request) against the reference-shaped step."""
+    from paper_2605_25716_b200 import distributed as sdist
+    case = Case(B=3, Hq=4, Hkv=4, d=128, lk=8192, n_nodes=1, lq=1, dtype=torch.bfloat16, seed=303)
+    got = case.run_device(n_splits=40)
+    ref = case.oracle()
+    assert max_abs_rel(got, ref) < TOL_BF16 and rel_fro(got, ref) < TOL_BF16
+    keys = protocol.DomainKeys(case.request_ids(), 0, 1, 4, 128, "cuda")
+    shard = protocol.KVShard(3, 4, 8192, 128, "cuda")
+    shard.ship_segment(dev(case.k[0], torch.bfloat16), dev(case.v[0], torch.bfloat16), keys, first_pos=0)
+    shard.kv_len.copy_(torch.tensor([8192, 300, 4100], dtype=torch.int32, device="cuda"))
+    lld = sdist.LLDecode(3, 4, 128, [keys], shard, n_splits=6)
+    bufs = sdist.StepBuffers.allocate(1, 3, 4, 1, 128, torch.bfloat16, "cuda")
+    comp = sdist.gpu_rank_compute([keys], shard, n_splits=6)
+    out = torch.empty((3, 4, 1, 128), dtype=torch.float32, device="cuda")
+    same = torch.empty_like(out)
+    q = dev(case.q, torch.bfloat16)
+    for _ in range(2):
+        lld.step(q, out)
+        sdist.scrambled_decode_step(q, comp, bufs, same)
+        assert max_abs_rel(out.double().cpu().numpy(), same.double().cpu().numpy()) < 1e-5
+    # the short request against plain attention over the 300 keys now live: the first 300 cache rows
+    # hold the plaintext rows perm[0:300] of the segment (span_perm(1, 0, 8192), enc_qkv's gather)
+    perm = keys.span_perms(1, 0, 8192)[0][1, :300].long()
+    kf, vf = dev(case.k[0], torch.bfloat16)[1].float(), dev(case.v[0], torch.bfloat16)[1].float()
+    qf = q[1].float()
+    kl, vl = kf[:, perm], vf[:, perm]
+    plain = (torch.softmax((qf @ kl.transpose(-1, -2)) / np.sqrt(128), -1) @ vl).double().cpu().numpy()
+    assert rel_fro(out[1].double().cpu().numpy(), plain) < 4e-2
