@@ -656,7 +656,9 @@ def run_prefill(devn, steps: int, warmup: int, peaks: dict):
             "flops_per_step": flops,
             "roofline": {"bound": "tensor", "kernel": "k2_prefill_tc_kernel", "achieved": tf_k2, "peak": peak,
                          "unit": "TFLOP/s", "frac": tf_k2 / peak, "k2_ms": k2_ms, "k2_share_of_step": k2_ms / ms,
-                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"}}
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)",
+                         "frac_of_sustained": tf_k2 / float(peaks.get("bf16_tflops_sustained", peak)),
+                         "frac_of_mma_issue_rate": tf_k2 / (8192 * 148 * 1.965e9 / 1e12)}}
 
 
 def run_gqa_mixed(devn, steps: int, warmup: int, peaks: dict):
