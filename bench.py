@@ -638,11 +638,12 @@ def run_prefill(devn, steps: int, warmup: int, peaks: dict):
         step(False)
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for _ in range(steps):
-        step(True)
-    t1.record(stream)
-    torch.cuda.synchronize()
+    with ClockSampler(devn.index or 0) as clk:
+        t0.record(stream)
+        for _ in range(steps):
+            step(True)
+        t1.record(stream)
+        torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / steps
     k2_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
     flops = 4.0 * LQ * LK * H * D
@@ -653,7 +654,7 @@ def run_prefill(devn, steps: int, warmup: int, peaks: dict):
             "config": {"workload": "BASELINE cfg3 per GPU: 2K-token prefill span vs 16K-token scrambled KV shard "
                                    "(+ the span's own 2K K/V rows scrambled into the cache), 32 heads x d128, bf16",
                        "q_rows": LQ, "kv_rows": LK, "kv_rows_written": LQ, "heads": H, "head_dim": D, "splits": S},
-            "flops_per_step": flops,
+            "flops_per_step": flops, "clocks": clk.summary(),
             "roofline": {"bound": "tensor", "kernel": "k2_prefill_tc_kernel", "achieved": tf_k2, "peak": peak,
                          "unit": "TFLOP/s", "frac": tf_k2 / peak, "k2_ms": k2_ms, "k2_share_of_step": k2_ms / ms,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)",
