@@ -137,7 +137,7 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys,
  * with the same fields. When every job takes the tensor-core form (bf16 in/out, head_dim 64 or
  * 128, >= 128 rows) they share one persistent grid, so small spans do not each pay a pipeline
  * fill and a partial last wave; otherwise the jobs run one sda_scramble after another. */
-#define SDA_MAX_SCRAMBLE_JOBS 3
+#define SDA_MAX_SCRAMBLE_JOBS 16
 typedef struct {
     int32_t variant, which_keys;
     const void* x;
@@ -155,6 +155,14 @@ typedef struct {
     int64_t out_rows_cap, out_row_offset, x_batch_mod;
 } sda_scramble_job;
 sda_status sda_scramble_batch(void* stream, int32_t head_dim, const sda_scramble_job* jobs, int32_t n_jobs);
+/* The same with jobs whose `out` lies in a peer's memory (a receive slot mapped with sda_ipc_*):
+ * when all of job j's rows are stored, the CTA completing it raises *peer_flag[j] = *epoch
+ * (system-scope release; peer_flag[j] = NULL for a local job). All jobs must take the
+ * tensor-core form (else SDA_ERR_UNSUPPORTED). counters: 16 zeroed u32 (self-resetting). This is
+ * the prefill SCR_Q send folded into K1 (the span's Q' for every domain written straight into
+ * the domains' receive slots, no copy kernel). */
+sda_status sda_scramble_batch_remote(void* stream, int32_t head_dim, const sda_scramble_job* jobs, int32_t n_jobs,
+                                     uint32_t* const* peer_flag, const uint32_t* epoch, uint32_t* counters);
 
 /* ------------------------------------------------------------------------------------------
  * K2  keyless delegated partial attention over the scrambled KV shard.

@@ -34,7 +34,7 @@ EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_
            "sda_quantize_affine", "sda_dequantize", "sda_quant_roundtrip",
            "sda_frame_elements", "sda_frame_payload_bytes", "sda_frame_bytes", "sda_frame_scratch_bytes",
            "sda_frame_encode", "sda_frame_parse_header", "sda_frame_decode", "sda_crc32",
-           "sda_partial_attention_remote")
+           "sda_partial_attention_remote", "sda_scramble_batch_remote")
 
 
 class SdaError(RuntimeError):
@@ -70,7 +70,7 @@ class ScrambleJob(ct.Structure):
                 ("out_rows_cap", ct.c_int64), ("out_row_offset", ct.c_int64), ("x_batch_mod", ct.c_int64)]
 
 
-MAX_SCRAMBLE_JOBS = 3
+MAX_SCRAMBLE_JOBS = 16
 SDA_ERR_FRAME = 9
 FRAME_MAX_DIMS = 8
 
@@ -133,6 +133,8 @@ def _load() -> ct.CDLL:
                                             ct.c_int32, ct.c_int32, _vp, ct.c_int32, _vp, _vp]
     lib.sda_trace_timestamp.argtypes = [_vp, _vp]
     lib.sda_scramble_batch.argtypes = [_vp, ct.c_int32, ct.POINTER(ScrambleJob), ct.c_int32]
+    lib.sda_scramble_batch_remote.argtypes = [_vp, ct.c_int32, ct.POINTER(ScrambleJob), ct.c_int32,
+                                              ct.POINTER(ct.c_void_p), _vp, _vp]
     _ph = ct.POINTER(FrameHeader)
     for f in ("sda_frame_elements", "sda_frame_payload_bytes", "sda_frame_bytes"):
         getattr(lib, f).restype = ct.c_uint64

@@ -83,12 +83,16 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys, const
     return from_cuda(sda::launch_k1(p, head_dim, x_dtype, out_dtype, n_batch, static_cast<cudaStream_t>(stream)));
 }
 
-sda_status sda_scramble_batch(void* stream, int32_t head_dim, const sda_scramble_job* jobs, int32_t n_jobs) {
+static sda_status scramble_batch_impl(void* stream, int32_t head_dim, const sda_scramble_job* jobs, int32_t n_jobs,
+                                      uint32_t* const* peer_flag, const uint32_t* epoch, uint32_t* counters) {
     if (!jobs || n_jobs < 0 || n_jobs > SDA_MAX_SCRAMBLE_JOBS) return SDA_ERR_INVALID_ARGUMENT;
     if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
     if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
+    const bool remote = peer_flag != nullptr;
+    if (remote && (!epoch || !counters)) return SDA_ERR_INVALID_ARGUMENT;
     sda::K1Params ps[SDA_MAX_SCRAMBLE_JOBS];
     int64_t nb[SDA_MAX_SCRAMBLE_JOBS];
+    uint32_t* flags[SDA_MAX_SCRAMBLE_JOBS];
     int n_live = 0;
     bool all_tc = !env_flag("SDA_K1_SIMT");
     for (int i = 0; i < n_jobs; ++i) {   // same validation as sda_scramble, per job
@@ -102,20 +106,27 @@ sda_status sda_scramble_batch(void* stream, int32_t head_dim, const sda_scramble
         if (j.out_row_offset < 0 || j.out_row_offset + j.rows > j.out_rows_cap || j.x_batch_mod < 0)
             return SDA_ERR_INVALID_ARGUMENT;
         if (j.n_batch > 65535 || j.n_heads > 65535) return SDA_ERR_UNSUPPORTED;
-        if (j.rows == 0 || j.n_batch == 0) continue;
+        if (j.rows == 0 || j.n_batch == 0) {
+            if (remote && peer_flag[i]) return SDA_ERR_INVALID_ARGUMENT;   // an empty remote job would never signal
+            continue;
+        }
         sda::K1Params p{j.x, j.out, j.keys, j.perm, j.keys_batch_stride, j.perm_batch_stride, j.rows, j.out_rows_cap,
                         j.out_row_offset, j.n_heads, j.key_heads, j.which_keys, j.variant == SDA_PHI_INV_T ? 1 : 0,
                         j.x_batch_mod};
         all_tc = all_tc && sda::k1_tc_eligible(p, head_dim, j.x_dtype, j.out_dtype);
         ps[n_live] = p;
         nb[n_live] = j.n_batch;
+        flags[n_live] = remote ? peer_flag[i] : nullptr;
         ++n_live;
     }
     if (n_live == 0) return SDA_OK;
     if (all_tc) {
         ++g_launches;
-        return from_cuda(sda::launch_k1_tc_multi(ps, nb, n_live, head_dim, static_cast<cudaStream_t>(stream)));
+        return from_cuda(sda::launch_k1_tc_multi(ps, nb, n_live, head_dim, static_cast<cudaStream_t>(stream),
+                                                 remote ? flags : nullptr, remote ? epoch : nullptr,
+                                                 remote ? counters : nullptr));
     }
+    if (remote) return SDA_ERR_UNSUPPORTED;
     for (int i = 0; i < n_jobs; ++i) {
         const sda_scramble_job& j = jobs[i];
         const sda_status st = sda_scramble(stream, j.variant, j.which_keys, j.x, j.x_dtype, j.n_batch, j.n_heads, j.rows,
@@ -125,6 +136,16 @@ sda_status sda_scramble_batch(void* stream, int32_t head_dim, const sda_scramble
         if (st != SDA_OK) return st;
     }
     return SDA_OK;
+}
+
+sda_status sda_scramble_batch(void* stream, int32_t head_dim, const sda_scramble_job* jobs, int32_t n_jobs) {
+    return scramble_batch_impl(stream, head_dim, jobs, n_jobs, nullptr, nullptr, nullptr);
+}
+
+sda_status sda_scramble_batch_remote(void* stream, int32_t head_dim, const sda_scramble_job* jobs, int32_t n_jobs,
+                                     uint32_t* const* peer_flag, const uint32_t* epoch, uint32_t* counters) {
+    if (!peer_flag) return SDA_ERR_INVALID_ARGUMENT;
+    return scramble_batch_impl(stream, head_dim, jobs, n_jobs, peer_flag, epoch, counters);
 }
 
 // ------------------------------------------------------------------------------------------ quant wire

@@ -55,7 +55,7 @@ struct K1TcJob {
     int64_t tiles_per_slab;
     int64_t x_batch_mod;
 };
-constexpr int kK1Jobs = 3;
+constexpr int kK1Jobs = 16;
 
 struct K1TcParams {
     K1TcJob job[kK1Jobs];
@@ -63,6 +63,15 @@ struct K1TcParams {
     int n_jobs;
     int64_t total_tiles;
     int64_t tiles_per_cta;
+    // remote jobs (out in a peer's memory): once all of a job's tiles are stored, the CTA that
+    // completes it raises *peer_flag[job] = *epoch (system-scope release); null = local job
+    uint32_t* peer_flag[kK1Jobs];
+    uint32_t* job_counters;           // [kK1Jobs] zeroed, self-resetting
+    const uint32_t* epoch;
+};
+
+struct K1OutMaps {                    // one TMA store map per job (kernel parameter, 64-byte aligned)
+    CUtensorMap m[kK1Jobs];
 };
 
 template <int D>
@@ -87,9 +96,7 @@ struct K1TcShape {
 };
 
 template <int D>
-__global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const __grid_constant__ CUtensorMap out_map0,
-                                                       const __grid_constant__ CUtensorMap out_map1,
-                                                       const __grid_constant__ CUtensorMap out_map2) {
+__global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const __grid_constant__ K1OutMaps maps) {
     using S = K1TcShape<D>;
     constexpr int ST = S::STAGES;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -112,7 +119,9 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
     const int64_t ntiles = last - first;
     // global tile id -> (job, tile id within the job)
     auto job_of = [&](int64_t id) -> int {
-        return id >= p.job_tile0[2] ? 2 : (id >= p.job_tile0[1] ? 1 : 0);
+        int j = 0;
+        while (j + 1 < p.n_jobs && id >= p.job_tile0[j + 1]) ++j;
+        return j;
     };
 
     if (tid == 0) {
@@ -128,9 +137,7 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
         tc::mbar_init(bfree, 1);
         tc::mbar_init(bready, 128);
         tc::fence_mbar_init();
-        tc::prefetch_tmap(&out_map0);
-        if (p.n_jobs > 1) tc::prefetch_tmap(&out_map1);
-        if (p.n_jobs > 2) tc::prefetch_tmap(&out_map2);
+        for (int j = 0; j < p.n_jobs; ++j) tc::prefetch_tmap(&maps.m[j]);
     }
     if (warp == 0) tc::tmem_alloc<S::TMEM_COLS>(tmem_slot);
     tc::tc_fence_before();
@@ -320,7 +327,7 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
             const int64_t orow0 = slab * jb.out_rows_cap + jb.out_row_offset + t * S::TILE;
             if (nrows == S::TILE) {
                 if (tid == 0) {
-                    const CUtensorMap* om = jj == 0 ? &out_map0 : (jj == 1 ? &out_map1 : &out_map2);
+                    const CUtensorMap* om = &maps.m[jj];
 #pragma unroll
                     for (int cb = 0; cb < S::KB; ++cb)
                         tc::tma_store_2d(om, o + cb * S::BLK_BYTES, cb * 64, (int)orow0);
@@ -333,7 +340,26 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
                         *reinterpret_cast<const uint4*>(o + (c8 >> 3) * S::BLK_BYTES + tc::sw128_off(tid, c8 & 7));
             }
         }
-        if (tid == 0) tc::bulk_wait0();
+        if (tid == 0) tc::bulk_wait0();   // this CTA's TMA stores have completed
+        if (p.epoch) {
+            // remote jobs: make this CTA's stores (TMA and the masked tail) visible system-wide,
+            // then count its tiles per job; the CTA completing a job raises the job's flag
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __threadfence_system();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (tid == 0) {
+                for (int jj = job_of(first); jj < p.n_jobs && p.job_tile0[jj] < last; ++jj) {
+                    if (!p.peer_flag[jj]) continue;
+                    const int64_t lo = max(first, p.job_tile0[jj]), hi = min(last, p.job_tile0[jj + 1]);
+                    const unsigned n = (unsigned)(hi - lo), total = (unsigned)(p.job_tile0[jj + 1] - p.job_tile0[jj]);
+                    if (n && atomicAdd(&p.job_counters[jj], n) + n == total) {
+                        p.job_counters[jj] = 0;
+                        __threadfence_system();
+                        flag_raise(p.peer_flag[jj], *p.epoch);
+                    }
+                }
+            }
+        }
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -374,7 +400,8 @@ bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t
 static int num_sms() { return device_sms(); }
 
 template <int D>
-static cudaError_t launch_k1_tc_d(const K1Params* qs, const int64_t* n_batch, int n_jobs, cudaStream_t st) {
+static cudaError_t launch_k1_tc_d(const K1Params* qs, const int64_t* n_batch, int n_jobs, cudaStream_t st,
+                                  uint32_t* const* peer_flag, const uint32_t* epoch, uint32_t* counters) {
     using S = K1TcShape<D>;
     {
         const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k1_tc_kernel<D>), S::SMEM);
@@ -382,8 +409,10 @@ static cudaError_t launch_k1_tc_d(const K1Params* qs, const int64_t* n_batch, in
     }
     if (n_jobs < 1 || n_jobs > kK1Jobs) return cudaErrorInvalidValue;
     K1TcParams p{};
-    CUtensorMap maps[kK1Jobs];
+    K1OutMaps maps;
     p.n_jobs = n_jobs;
+    p.epoch = epoch;
+    p.job_counters = counters;
     int64_t tile0 = 0;
     for (int j = 0; j < kK1Jobs; ++j) {
         p.job_tile0[j] = tile0;
@@ -406,17 +435,18 @@ static cudaError_t launch_k1_tc_d(const K1Params* qs, const int64_t* n_batch, in
         jb.x_batch_mod = q.x_batch_mod;
         jb.tiles_per_slab = (q.rows + 127) / 128;
         tile0 += jb.tiles_per_slab * n_batch[j] * q.n_heads;
-        if (!make_tmap_bf16_2d(&maps[j], q.out, n_batch[j] * q.n_heads * q.out_rows_cap, D, 128))
+        if (!make_tmap_bf16_2d(&maps.m[j], q.out, n_batch[j] * q.n_heads * q.out_rows_cap, D, 128))
             return cudaErrorInvalidValue;
+        p.peer_flag[j] = peer_flag ? peer_flag[j] : nullptr;
     }
     p.job_tile0[kK1Jobs] = tile0;
-    for (int j = n_jobs; j < kK1Jobs; ++j) maps[j] = maps[0];
+    for (int j = n_jobs; j < kK1Jobs; ++j) maps.m[j] = maps.m[0];
     p.total_tiles = tile0;
     if (p.total_tiles == 0) return cudaSuccess;
     const int64_t grid = std::min<int64_t>(p.total_tiles, num_sms());
     p.tiles_per_cta = (p.total_tiles + grid - 1) / grid;
     const int64_t ngrid = (p.total_tiles + p.tiles_per_cta - 1) / p.tiles_per_cta;
-    k1_tc_kernel<D><<<(unsigned)ngrid, S::THREADS, S::SMEM, st>>>(p, maps[0], maps[1], maps[2]);
+    k1_tc_kernel<D><<<(unsigned)ngrid, S::THREADS, S::SMEM, st>>>(p, maps);
     return cudaGetLastError();
 }
 
@@ -425,12 +455,13 @@ bool k1_tc_eligible(const K1Params& p, int d, int xdt, int odt) {
 }
 
 cudaError_t launch_k1_tc(const K1Params& p, int d, int64_t n_batch, cudaStream_t st) {
-    return launch_k1_tc_multi(&p, &n_batch, 1, d, st);
+    return launch_k1_tc_multi(&p, &n_batch, 1, d, st, nullptr, nullptr, nullptr);
 }
 
-cudaError_t launch_k1_tc_multi(const K1Params* p, const int64_t* n_batch, int n_jobs, int d, cudaStream_t st) {
-    if (d == 64) return launch_k1_tc_d<64>(p, n_batch, n_jobs, st);
-    if (d == 128) return launch_k1_tc_d<128>(p, n_batch, n_jobs, st);
+cudaError_t launch_k1_tc_multi(const K1Params* p, const int64_t* n_batch, int n_jobs, int d, cudaStream_t st,
+                               uint32_t* const* peer_flag, const uint32_t* epoch, uint32_t* counters) {
+    if (d == 64) return launch_k1_tc_d<64>(p, n_batch, n_jobs, st, peer_flag, epoch, counters);
+    if (d == 128) return launch_k1_tc_d<128>(p, n_batch, n_jobs, st, peer_flag, epoch, counters);
     return cudaErrorInvalidValue;
 }
 

@@ -131,7 +131,9 @@ cudaError_t launch_frame_decode(const uint8_t* frame, int hlen, uint64_t payload
                                 cudaStream_t st);
 cudaError_t launch_quant_roundtrip(void* x, int dt, int64_t n, int64_t count, int bits, unsigned long long* scratch,
                                    int32_t* err, cudaStream_t st);
-cudaError_t launch_k1_tc_multi(const K1Params* p, const int64_t* n_batch, int n_jobs, int d, cudaStream_t st);
+cudaError_t launch_k1_tc_multi(const K1Params* p, const int64_t* n_batch, int n_jobs, int d, cudaStream_t st,
+                               uint32_t* const* peer_flag = nullptr, const uint32_t* epoch = nullptr,
+                               uint32_t* counters = nullptr);
 cudaError_t launch_k2_decode(const K2Params& p, int d, int qdt, int kvdt, cudaStream_t st);
 bool k2_prefill_tc_eligible(const K2Params& p, int d, int qdt, int kvdt);
 cudaError_t launch_k2_prefill_tc(const K2Params& p, cudaStream_t st);

@@ -16,6 +16,7 @@ on CPU with the oracle standing in for the kernels.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Callable, Optional, Sequence
 
@@ -64,6 +65,9 @@ class RankCompute:
     # (q_all, dims, exchange) -> bool: K2 writing every request's record straight into its
     # inquirer's receive slot and raising the return flags (False: not eligible, use serve)
     serve_remote: Optional[Callable[[torch.Tensor, tuple, "PeerExchange"], bool]] = None
+    # (q, exchange) -> bool: K1 writing every domain's Q' straight into that domain's receive
+    # slot and raising its SCR_Q flag (False: not eligible, use scramble_q_all + exchange_q)
+    scramble_q_remote: Optional[Callable[[torch.Tensor, "PeerExchange"], bool]] = None
 
 
 def map_peer_buffers(bufs: dict, group: Optional[dist.ProcessGroup] = None):
@@ -118,6 +122,7 @@ class PeerExchange:
         self.flags = torch.zeros(2 * W, dtype=torch.int32, device=dev)      # [SCR_Q from r | SCR_SHARD from r]
         self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)
         self.counters = torch.zeros(2 * W, dtype=torch.int32, device=dev)
+        self.k1_counters = torch.zeros(16, dtype=torch.int32, device=dev)   # sda_scramble_batch_remote
         torch.cuda.synchronize()
         ptrs, self.opened = map_peer_buffers({"q": bufs.q_recv, "ret": bufs.ret_recv, "flags": self.flags}, group)
         base = {(r, name): ptrs[name][r] for name in ptrs for r in range(W)}
@@ -239,13 +244,19 @@ def scrambled_decode_step(q: torch.Tensor, compute: RankCompute, bufs: StepBuffe
     world = bufs.q_send.shape[0]
     if exchange is not None:
         exchange.begin_step()
-    if compute.scramble_q_all is not None:                       # span_send_layer, all domains at once
-        compute.scramble_q_all(q, bufs.q_send)
-    else:
-        for dom in range(world):
-            compute.scramble_q(q, dom, bufs.q_send[dom])
+    q_sent = (world > 1 and exchange is not None and compute.scramble_q_remote is not None
+              and compute.scramble_q_remote(q, exchange))            # K1 wrote Q' into the peers' slots
+    if not q_sent:
+        if compute.scramble_q_all is not None:                   # span_send_layer, all domains at once
+            compute.scramble_q_all(q, bufs.q_send)
+        else:
+            for dom in range(world):
+                compute.scramble_q(q, dom, bufs.q_send[dom])
     if world > 1 and exchange is not None:
-        exchange.exchange_q()                                         # SCR_Q over peer memory
+        if q_sent:
+            exchange._wait(0)                                         # SCR_Q written by K1 itself
+        else:
+            exchange.exchange_q()                                     # SCR_Q over peer memory
         q_all = bufs.q_recv
         b_tot = q_all.shape[0] * q_all.shape[1]
         if compute.serve_remote is not None and compute.serve_remote(
@@ -336,6 +347,31 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
             ex.counters.data_ptr() + 4 * ex.world), "sda_partial_attention_remote")
         return True
 
+    def scramble_q_remote(q, ex):
+        # opt-in (SDA_K1_REMOTE=1): TMA stores into peer memory measured +3 % at N=2 but -21 % at
+        # N=4 on C3 against K1 into q_send + the push kernel, so the push stays the default
+        Bp, Hq, Lq, d = q.shape
+        if os.environ.get("SDA_K1_REMOTE") != "1":
+            return False
+        if Lq < 128 or d not in (64, 128) or q.dtype != torch.bfloat16 or ex.world > 16:
+            return False
+        import ctypes as ct
+        pq, _ = q_perms(Lq)
+        kh = kv_heads or inquirer_keys[0].kv_heads
+        q = q.contiguous()
+        jobs = (capi.ScrambleJob * ex.world)()
+        for dom in range(ex.world):
+            kd = inquirer_keys[dom].dev
+            perm = pq[dom * Bp:(dom + 1) * Bp]
+            jobs[dom] = capi.ScrambleJob(capi.PHI_FORWARD, capi.KEYS_KQ, q.data_ptr(), capi.SDA_BF16, Bp, Hq, Lq,
+                                         kd.data_ptr(), kd.stride(0) if kd.dim() > 1 else 0, kh, perm.data_ptr(),
+                                         perm.stride(0), ex.q_args[1][dom], capi.SDA_BF16, Lq, 0, 0)
+        flags = (ct.c_void_p * ex.world)(*[ex.q_args[2][dom] for dom in range(ex.world)])
+        capi.check(capi.LIB.sda_scramble_batch_remote(torch.cuda.current_stream().cuda_stream, d, jobs, ex.world,
+                                                      flags, ex.epoch.data_ptr(), ex.k1_counters.data_ptr()),
+                   "sda_scramble_batch_remote")
+        return True
+
     def finish(back, out, dims):
         Hq, Lq, d = dims
         W, Bp, rec = back.shape
@@ -344,4 +380,4 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
                                 batch_stride=rec, shape=(Bp, Hq, Lq, d)) for dom in range(W)]
         ops.unscramble_merge(srcs, out=out, key_heads=kv_heads or inquirer_keys[0].kv_heads)
 
-    return RankCompute(scramble_q, serve, finish, scramble_q_all, serve_remote)
+    return RankCompute(scramble_q, serve, finish, scramble_q_all, serve_remote, scramble_q_remote)
