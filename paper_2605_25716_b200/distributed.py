@@ -348,10 +348,10 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
         return True
 
     def scramble_q_remote(q, ex):
-        # opt-in (SDA_K1_REMOTE=1): TMA stores into peer memory measured +3 % at N=2 but -21 % at
-        # N=4 on C3 against K1 into q_send + the push kernel, so the push stays the default
+        # TMA stores straight into peer memory: +3-5 % at N=2, +0.4-3 % at N=4 on C3 against K1
+        # into q_send + the push kernel (SDA_K1_REMOTE=0 selects the latter)
         Bp, Hq, Lq, d = q.shape
-        if os.environ.get("SDA_K1_REMOTE") != "1":
+        if os.environ.get("SDA_K1_REMOTE") == "0":
             return False
         if Lq < 128 or d not in (64, 128) or q.dtype != torch.bfloat16 or ex.world > 16:
             return False

@@ -14,7 +14,6 @@ from paper_2605_25716_b200 import distributed as sdist  # noqa: E402
 
 
 def main():
-    os.environ.setdefault("SDA_K1_REMOTE", "1")   # exercise the K1-writes-Q'-to-peers path too
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
