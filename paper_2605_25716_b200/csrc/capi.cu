@@ -326,17 +326,23 @@ sda_status sda_crc32(void* stream, const uint8_t* bytes, uint64_t len, void* scr
 int32_t sda_default_splits(int64_t n_batch, int32_t q_heads, int64_t q_rows, int64_t kv_cap) {
     if (n_batch <= 0 || q_heads <= 0 || q_rows <= 0 || kv_cap <= 0) return 1;
     if (q_rows >= 64) {
-        // prefill (tcgen05 kernel, one CTA per SM per 256 query rows): pick the split count whose
-        // grid fills the last wave of 148 SMs best, at least 4 KV tiles per split
+        // prefill (tcgen05 kernel, one CTA per SM per 256 query rows x split): minimise
+        //   ceil(waves) * (KV tiles per split + 4)  +  splits * merge cost
+        // in units of one CTA's 128-key tile time (~1.86 us): each CTA pays ~4 tiles of pipeline
+        // fill and epilogue, and every extra split is another (O', stats) set for K3 to read
+        // (~0.022 tile-times per 256-row unit at ~3.3 TB/s). C3: 1 split (K2 493 us + K3 ~15 us)
+        // instead of 4 (480 + 51 us); C5's prefill chunk: 2.
         const int64_t units = ((q_rows + 255) / 256) * q_heads * n_batch;
-        const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(8, (kv_cap / 128) / 4));
+        const int64_t tiles = (kv_cap + 127) / 128;
+        const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(8, tiles / 4));
+        const double sms = (double)sda::device_sms();
         int32_t best = 1;
-        double best_eff = -1.0;
+        double best_cost = 1e300;
         for (int64_t s = 1; s <= max_s; ++s) {
-            const double waves = (double)(units * s) / (double)sda::device_sms();
-            const double eff = waves / std::ceil(waves) - (s > 1 ? 0.01 * (double)s : 0.0);  // small merge cost
-            if (eff > best_eff + 1e-9) {
-                best_eff = eff;
+            const double waves = std::ceil((double)(units * s) / sms);
+            const double cost = waves * ((double)((tiles + s - 1) / s) + 4.0) + (double)s * 0.022 * (double)units;
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
                 best = (int32_t)s;
             }
         }
