@@ -396,6 +396,9 @@ int32_t sda_default_splits_gqa(int64_t n_batch, int32_t q_heads, int32_t kv_head
         }
         return best;
     }
+    // prefill rows on the tensor-core form: one split, which runs stream-K (persistent CTAs over
+    // the linear tile order, k2_prefill_tc.cu) -- full waves without partials for K3 to merge
+    if (head_dim == 128 && q_rows >= 64) return 1;
     return sda_default_splits(n_batch, q_heads, q_rows, kv_cap);
 }
 

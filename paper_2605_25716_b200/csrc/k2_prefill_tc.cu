@@ -20,6 +20,10 @@
 // groups so the tensor pipe always has the other tile's work queued. TMEM: S0|S1|O0|O1 =
 // 4 x 128 columns (P_g aliases the first 64 columns of S_g).
 #include <cmath>
+#include <climits>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "tc_util.cuh"
@@ -48,6 +52,12 @@ struct K2TcParams {
     uint32_t* peer_flag[kMaxPeers];
     uint32_t* dest_counters;
     const uint32_t* epoch;
+    // stream-K mode (one split): persistent CTAs over the linear tile order, pieces of a unit
+    // merged by its last finisher through sk_buf (3 slots x 256 rows per CTA) and sk_tick
+    // (one zeroed, self-resetting u32 per unit)
+    int sk;
+    float* sk_buf;
+    uint32_t* sk_tick;
 };
 
 #ifdef SDA_K2_TRACE
@@ -55,6 +65,15 @@ struct K2TcParams {
 // 0/1 softmax g got S, 2/3 softmax g arrives with P, 4/5 PV0/PV1 issue, 6/7 MMA loop top / V ready,
 // 8 before the P1 wait, 9/10 before / after the K(j+1) wait
 __device__ uint64_t g_k2_trace[16][64];
+__device__ uint64_t g_k2_cta[1024][2];   // every CTA's (start, end) globaltimer
+__device__ __forceinline__ void k2_cta_stamp(int which) {
+    if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && blockIdx.x < 1024) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_k2_cta[blockIdx.x][which] = t;
+    }
+}
+#define K2_CTA_STAMP(w) k2_cta_stamp(w)
 __device__ __forceinline__ void k2_stamp(int kind, int64_t j) {
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < 64) {
         uint64_t t;
@@ -65,6 +84,7 @@ __device__ __forceinline__ void k2_stamp(int kind, int64_t j) {
 #define K2_STAMP(k, j) k2_stamp(k, j)
 #else
 #define K2_STAMP(k, j)
+#define K2_CTA_STAMP(w)
 #endif
 
 // The MMA warp's waits for P sit on the S -> softmax -> PV -> S chain of each Q tile: it spins
@@ -81,10 +101,15 @@ constexpr int OFF_Q0 = 0, OFF_Q1 = OFF_Q0 + TILE_BYTES;
 constexpr int OFF_K = OFF_Q1 + TILE_BYTES;        // 2 stages
 constexpr int OFF_V = OFF_K + 2 * TILE_BYTES;     // 2 stages
 constexpr int OFF_BAR = OFF_V + 2 * TILE_BYTES;
-// barriers: q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], o_final[2]
-constexpr int NBAR = 15;
-constexpr int SMEM = OFF_BAR + NBAR * 8 + 16;
-constexpr int THREADS = 320;
+// barriers: q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], o_final[2],
+// q_empty, o_empty[2]
+constexpr int NBAR = 18;
+constexpr int OFF_SEG = OFF_BAR + NBAR * 8 + 16;   // per softmax warp: segment state (SoftKeep)
+constexpr int SMEM = OFF_SEG + 8 * 128;
+// 12 warps = 3 warpgroups so registers can move between them (setmaxnreg): softmax warps 0-7
+// grow to 224, the TMA / MMA warpgroup (warps 8-9; 10-11 idle) shrinks to 56
+constexpr int THREADS = 384;
+constexpr int kSoftmaxRegs = 224, kIssueRegs = 56;
 constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 384;
 // Exponentials per 4 pairs computed on the FMA pipe (tc::exp2_fma2) instead of MUFU.EX2. Measured
 // on C3 (exps batched ahead of the packing): 0 -> 489 us, 1 -> 485 us, 2 -> 547 us -- past one in
@@ -93,9 +118,150 @@ constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 384;
 #define SDA_K2_EMU_OF4 1
 #endif
 constexpr int kEmuOf4 = SDA_K2_EMU_OF4;
+#ifndef SDA_K2_SUM_AFTER
+#define SDA_K2_SUM_AFTER 1
+#endif
 }  // namespace k2tc
 
-__global__ void __launch_bounds__(320, 1)
+namespace k2tc {
+// One unit of work = (request, q head, pair of 128-row Q tiles) over a range of 128-key tiles.
+struct Seg {
+    int64_t head_row;    // global Q row of the unit's first row
+    int b;               // request
+    int kvh;             // kv head (key set)
+    int nrows;           // rows of the unit (<= 256)
+    int len;             // keys of request b
+    int t0, nkv;         // first unit-local key tile, tiles in this segment
+    int split;           // split mode: output slot
+    int unit, ub, nt;    // stream-K: unit index, its first tile in its group's linear order, its tiles
+    bool two;            // second Q tile in use
+    bool first;          // stream-K: the segment starts the CTA's range
+};
+
+
+__device__ __forceinline__ int len_of(const K2TcParams& p, int64_t b) {
+    return p.kv_len ? p.kv_len[b] : (int)p.kv_cap;
+}
+__device__ __forceinline__ int ntile_of(const K2TcParams& p, int64_t b) { return (len_of(p, b) + TILE - 1) / TILE; }
+
+// unit (request b, q head, Q-tile pair qp)
+__device__ __forceinline__ void fill_unit(const K2TcParams& p, int b, int head, int qp, Seg& s) {
+    s.b = b;
+    s.kvh = head / (p.q_heads / p.kv_heads);
+    s.head_row = ((int64_t)b * p.q_heads + head) * p.q_rows + (int64_t)qp * 2 * TILE;
+    s.nrows = (int)min((int64_t)2 * TILE, p.q_rows - (int64_t)qp * 2 * TILE);
+    s.two = s.nrows > TILE;
+    s.len = len_of(p, b);
+}
+
+// split mode: the CTA's one segment -- blockIdx.z = request * n_splits + split;
+//   normal : blockIdx.x = 256-row pair of Q tiles, blockIdx.y = q head
+//   grouped: blockIdx.y = kv head; the tile rows are its G q heads x Lq rows
+__device__ __forceinline__ void split_seg(const K2TcParams& p, Seg& s) {
+    const int64_t b = blockIdx.z / p.n_splits;
+    const int split = blockIdx.z % p.n_splits;
+    const int G = p.q_heads / p.kv_heads;
+    s.b = (int)b;
+    s.split = split;
+    s.kvh = p.grouped ? (int)blockIdx.y : (int)blockIdx.y / G;
+    s.head_row = p.grouped ? (b * p.q_heads + (int64_t)s.kvh * G) * p.q_rows
+                           : (b * p.q_heads + blockIdx.y) * p.q_rows + (int64_t)blockIdx.x * 2 * TILE;
+    s.nrows = (int)(p.grouped ? (int64_t)G * p.q_rows : min((int64_t)2 * TILE, p.q_rows - (int64_t)blockIdx.x * 2 * TILE));
+    s.two = s.nrows > TILE;
+    s.len = len_of(p, b);
+    // split ranges aligned to whole 128-key tiles
+    const int ntile_all = (s.len + TILE - 1) / TILE;
+    const int tps = (ntile_all + p.n_splits - 1) / p.n_splits;
+    const int t0 = split * tps;
+    const int t1 = min(ntile_all, t0 + tps);
+    s.t0 = t0;
+    s.nkv = t1 > t0 ? t1 - t0 : 0;
+    s.unit = s.ub = s.nt = 0;
+    s.first = true;
+}
+
+// Stream-K: the (request, q head) key tiles laid end to end = T tiles. The grid is NG groups of
+// n_qpairs CTAs; CTA (group g, pair qp) takes the Q-tile pair qp of every (request, head) over
+// tiles [T g / NG, T (g+1) / NG) -- so a group's CTAs walk the same keys in lockstep and read
+// each K/V tile from HBM once (the L2 serves the others), as the split-mode grid does. A range
+// covers the tail of one (request, head), whole ones, the head of another.
+__device__ __forceinline__ int sk_lo(int T, int NG, int g) { return (int)((int64_t)T * g / NG); }
+
+struct SkCursor {
+    int lo, hi, pos, b, head, off, acc, nt;
+};
+
+__device__ __forceinline__ void sk_init(const K2TcParams& p, int T, int NG, int g, SkCursor& k) {
+    k.lo = g < NG ? sk_lo(T, NG, g) : 0;
+    k.hi = g < NG ? sk_lo(T, NG, g + 1) : 0;
+    k.pos = k.lo;
+    k.acc = k.b = k.nt = k.head = k.off = 0;
+    if (k.pos >= k.hi) return;
+    for (;; ++k.b) {
+        k.nt = ntile_of(p, k.b);
+        if (k.pos < k.acc + p.q_heads * k.nt) break;
+        k.acc += p.q_heads * k.nt;
+    }
+    k.head = (k.pos - k.acc) / k.nt;
+    k.off = (k.pos - k.acc) % k.nt;
+}
+
+__device__ __forceinline__ bool sk_next(const K2TcParams& p, int qp, SkCursor& k, Seg& s) {
+    if (k.pos >= k.hi) return false;
+    fill_unit(p, k.b, k.head, qp, s);
+    s.t0 = k.off;
+    s.nkv = min(k.nt - k.off, k.hi - k.pos);
+    s.split = 0;
+    s.unit = (k.b * p.q_heads + k.head) * p.n_qpairs + qp;
+    s.ub = k.acc + k.head * k.nt;
+    s.nt = k.nt;
+    s.first = k.pos == k.lo;
+    k.pos += s.nkv;
+    k.off += s.nkv;
+    if (k.off == k.nt) {
+        k.off = 0;
+        if (++k.head == p.q_heads) {
+            k.head = 0;
+            k.acc += p.q_heads * k.nt;
+            ++k.b;
+            while (k.pos < k.hi && (k.nt = ntile_of(p, k.b)) == 0) ++k.b;   // requests with no keys
+        }
+    }
+    return true;
+}
+
+// A softmax warp's segment state waits out the tile loop in SMEM, so it holds no registers
+// next to the 128 logits of a row (re-read through an opaque pointer).
+struct SoftKeep {
+    Seg seg;
+    SkCursor cur;
+    int T, NG;
+};
+static_assert(sizeof(SoftKeep) <= 128, "one 128-byte SMEM slot per softmax warp");
+__device__ __forceinline__ SoftKeep* opaque(SoftKeep* k) {
+    SoftKeep* r;
+    asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(k));
+    return r;
+}
+
+// group whose range holds linear tile x
+__device__ __forceinline__ int sk_group_of(int x, int T, int NG) {
+    int g = (int)min((int64_t)NG - 1, (int64_t)x * NG / T);
+    while (g + 1 < NG && sk_lo(T, NG, g + 1) <= x) ++g;
+    while (g > 0 && sk_lo(T, NG, g) > x) --g;
+    return g;
+}
+
+// scratch slot (CTA, k): k = 0 the CTA's first segment, 1 its last, 2 whole units; O rows then stats
+constexpr int64_t SK_SLOT = 2 * TILE * D + 2 * TILE * 2;
+__device__ __forceinline__ float* sk_slot(const K2TcParams& p, int cta, int k) {
+    return p.sk_buf + ((int64_t)cta * 3 + k) * SK_SLOT;
+}
+
+__device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+}  // namespace k2tc
+
+__global__ void __launch_bounds__(384, 1)
 k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                      const __grid_constant__ CUtensorMap vmap) {
     using namespace k2tc;
@@ -109,32 +275,41 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
     uint64_t* const s_full = bars + 9;
     uint64_t* const p_full = bars + 11;
     uint64_t* const o_final = bars + 13;
+    uint64_t* const q_empty = bars + 15;
+    uint64_t* const o_empty = bars + 16;
     uint32_t* const tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
+    uint32_t* const sk_ticket = tmem_slot + 1;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // work unit: blockIdx.z = request * n_splits + split;
+    // Work: split mode -- one segment per CTA: blockIdx.z = request * n_splits + split;
     //   normal : blockIdx.x = 256-row pair of Q tiles, blockIdx.y = q head
     //   grouped: blockIdx.y = kv head; the tile rows are its G q heads x Lq rows
-    const int64_t b = blockIdx.z / p.n_splits;
-    const int split = blockIdx.z % p.n_splits;
-    const int G = p.q_heads / p.kv_heads;
-    const int kvh = p.grouped ? (int)blockIdx.y : (int)blockIdx.y / G;
-    const int64_t head_row = p.grouped ? (b * p.q_heads + (int64_t)kvh * G) * p.q_rows
-                                       : (b * p.q_heads + blockIdx.y) * p.q_rows + (int64_t)blockIdx.x * 2 * TILE;
-    const int64_t nrows = p.grouped ? (int64_t)G * p.q_rows
-                                    : min((int64_t)2 * TILE, p.q_rows - (int64_t)blockIdx.x * 2 * TILE);
-    const bool two = nrows > TILE;                  // second Q tile in use
-    const int64_t len = p.kv_len ? (int64_t)p.kv_len[b] : p.kv_cap;
-    // split ranges aligned to whole 128-key tiles
-    const int64_t ntile_all = (len + TILE - 1) / TILE;
-    const int64_t tps = (ntile_all + p.n_splits - 1) / p.n_splits;
-    const int64_t t0 = (int64_t)split * tps;
-    const int64_t t1 = min(ntile_all, t0 + tps);
-    const int64_t nkv = t1 > t0 ? t1 - t0 : 0;
-    const int64_t k_end = min(len, t1 * TILE);      // keys >= k_end are masked
+    // stream-K mode (p.sk) -- a persistent CTA per SM walking its range of the linear tile order.
+    int T_sk = 0, NG = 1;
+    const int nq = p.n_qpairs;
+    const int grp = (int)blockIdx.x / nq, qp_sk = (int)blockIdx.x % nq;
+    if (p.sk) {
+        for (int64_t b = 0; b < p.n_batch; ++b) T_sk += ntile_of(p, b);
+        T_sk *= p.q_heads;
+        // groups that take part in the range split: every range then holds >= 1 tile (ragged
+        // kv_len can leave fewer tiles than groups; the other CTAs only serve empty requests)
+        NG = max(1, min((int)gridDim.x / nq, T_sk));
+    }
+    // the CTA's segments, the same sequence in every warp role
+    SkCursor cur;
+    if (p.sk) sk_init(p, T_sk, NG, grp, cur);
+    bool lpending = true;
+    auto next_seg = [&](Seg& sg) -> bool {
+        if (p.sk) return sk_next(p, qp_sk, cur, sg);
+        if (!lpending) return false;
+        lpending = false;
+        split_seg(p, sg);
+        return true;
+    };
 
     if (tid == 0) {
         tc::mbar_init(q_full, 1);
+        tc::mbar_init(q_empty, 1);
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&k_full[i], 1);
             tc::mbar_init(&k_empty[i], 1);
@@ -143,6 +318,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             tc::mbar_init(&s_full[i], 1);
             tc::mbar_init(&p_full[i], 128);
             tc::mbar_init(&o_final[i], 1);
+            tc::mbar_init(&o_empty[i], 128);
         }
         tc::fence_mbar_init();
     }
@@ -151,286 +327,579 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    K2_CTA_STAMP(0);
 
-    const int64_t qrow0 = head_row;                       // global row of this CTA's first Q row
-    const int64_t kvrow0 = ((b * p.kv_heads + kvh) * p.kv_cap) + t0 * TILE;
-
-    if (warp == 8) {
+    if (warp >= 8) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kIssueRegs));
+      if (warp == 8) {
         // ------------------------------------------------------------------ TMA producer
-        if (lane == 0 && nkv > 0) {
+        // K/V tiles run through the 2-stage rings continuously across segments (jj counts all
+        // tiles of the CTA); a segment's Q is loaded after its first K/V tile is queued, once the
+        // previous segment's MMAs have released the Q buffers
+        if (lane == 0) {
             tc::prefetch_tmap(&qmap);
             tc::prefetch_tmap(&kmap);
             tc::prefetch_tmap(&vmap);
-            tc::mbar_arrive_expect_tx(q_full, (two ? 2 : 1) * TILE_BYTES);
-            for (int g = 0; g < (two ? 2 : 1); ++g)
-                for (int kb = 0; kb < 2; ++kb)
-                    tc::tma_load_2d(smem + (g ? OFF_Q1 : OFF_Q0) + kb * BLK, &qmap, kb * 64, (int)(qrow0 + g * TILE), q_full);
-            for (int64_t j = 0; j < nkv; ++j) {
-                const int st = (int)(j & 1);
-                const uint32_t ph = (uint32_t)(((j >> 1) - 1) & 1);
-                if (j >= 2) tc::mbar_wait(&k_empty[st], ph);
-                tc::mbar_arrive_expect_tx(&k_full[st], TILE_BYTES);
-                for (int kb = 0; kb < 2; ++kb)
-                    tc::tma_load_2d(smem + OFF_K + st * TILE_BYTES + kb * BLK, &kmap, kb * 64, (int)(kvrow0 + j * TILE), &k_full[st]);
-                if (j >= 2) tc::mbar_wait(&v_empty[st], ph);
-                tc::mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
-                for (int kb = 0; kb < 2; ++kb)
-                    tc::tma_load_2d(smem + OFF_V + st * TILE_BYTES + kb * BLK, &vmap, kb * 64, (int)(kvrow0 + j * TILE), &v_full[st]);
+            int64_t jj = 0;
+            int si = 0;
+            Seg sg;
+            while (next_seg(sg)) {
+                if (sg.nkv == 0) continue;
+                const int64_t kvrow0 = (((int64_t)sg.b * p.kv_heads + sg.kvh) * p.kv_cap) + (int64_t)sg.t0 * TILE;
+                for (int64_t j = 0; j < sg.nkv; ++j, ++jj) {
+                    const int st = (int)(jj & 1);
+                    const uint32_t ph = (uint32_t)(((jj >> 1) - 1) & 1);
+                    if (jj >= 2) tc::mbar_wait(&k_empty[st], ph);
+                    tc::mbar_arrive_expect_tx(&k_full[st], TILE_BYTES);
+                    for (int kb = 0; kb < 2; ++kb)
+                        tc::tma_load_2d(smem + OFF_K + st * TILE_BYTES + kb * BLK, &kmap, kb * 64, (int)(kvrow0 + j * TILE), &k_full[st]);
+                    if (jj >= 2) tc::mbar_wait(&v_empty[st], ph);
+                    tc::mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
+                    for (int kb = 0; kb < 2; ++kb)
+                        tc::tma_load_2d(smem + OFF_V + st * TILE_BYTES + kb * BLK, &vmap, kb * 64, (int)(kvrow0 + j * TILE), &v_full[st]);
+                    if (j == 0) {
+                        if (si > 0) tc::mbar_wait(q_empty, (uint32_t)((si - 1) & 1));
+                        tc::mbar_arrive_expect_tx(q_full, (sg.two ? 2 : 1) * TILE_BYTES);
+                        for (int g = 0; g < (sg.two ? 2 : 1); ++g)
+                            for (int kb = 0; kb < 2; ++kb)
+                                tc::tma_load_2d(smem + (g ? OFF_Q1 : OFF_Q0) + kb * BLK, &qmap, kb * 64,
+                                                (int)(sg.head_row + g * TILE), q_full);
+                    }
+                }
+                ++si;
             }
         }
-    } else if (warp == 9) {
+      } else if (warp == 9) {
         // ------------------------------------------------------------------ MMA issuer
         // the whole warp runs the loop (warp-uniform descriptors); the elected lane issues
-        if (nkv > 0) {
-            const bool leader = tc::elect_one();
-            constexpr uint32_t IDESC_S = tc::idesc_bf16_f32(128, 128, false, false);   // Q K^T, both K-major
-            constexpr uint32_t IDESC_O = tc::idesc_bf16_f32(128, 128, false, true);    // P V, V MN-major
-            const uint32_t q0 = tc::smem_u32(smem + OFF_Q0), q1 = tc::smem_u32(smem + OFF_Q1);
-            const uint32_t kbase = tc::smem_u32(smem + OFF_K), vbase = tc::smem_u32(smem + OFF_V);
-            auto issue_s = [&](int g, int64_t j) {
-                const int st = (int)(j & 1);
-                const uint32_t qa = g ? q1 : q0;
-                const uint32_t kb = kbase + st * TILE_BYTES;
-                const uint32_t d_tmem = tmem + (g ? COL_S1 : COL_S0);
+        const bool leader = tc::elect_one();
+        constexpr uint32_t IDESC_S = tc::idesc_bf16_f32(128, 128, false, false);   // Q K^T, both K-major
+        constexpr uint32_t IDESC_O = tc::idesc_bf16_f32(128, 128, false, true);    // P V, V MN-major
+        const uint32_t q0 = tc::smem_u32(smem + OFF_Q0), q1 = tc::smem_u32(smem + OFF_Q1);
+        const uint32_t kbase = tc::smem_u32(smem + OFF_K), vbase = tc::smem_u32(smem + OFF_V);
+        auto issue_s = [&](int g, int st) {
+            const uint32_t qa = g ? q1 : q0;
+            const uint32_t kb = kbase + st * TILE_BYTES;
+            const uint32_t d_tmem = tmem + (g ? COL_S1 : COL_S0);
 #pragma unroll
-                for (int k = 0; k < D / 16; ++k) {
-                    const uint32_t off = (k >> 2) * BLK + (k & 3) * 32;
-                    const uint64_t da = tc::sw128_desc(qa + off, 16, 1024), db = tc::sw128_desc(kb + off, 16, 1024);
-                    if (leader) tc::mma_bf16_ss(d_tmem, da, db, IDESC_S, k > 0 ? 1u : 0u);
-                }
-                if (leader) tc::mma_commit(&s_full[g]);
-            };
-            auto issue_pv = [&](int g, int64_t j) {
-                const int st = (int)(j & 1);
-                const uint32_t vb = vbase + st * TILE_BYTES;
-                const uint32_t d_tmem = tmem + (g ? COL_O1 : COL_O0);
-                const uint32_t p_tmem = tmem + (g ? COL_S1 : COL_S0);
+            for (int k = 0; k < D / 16; ++k) {
+                const uint32_t off = (k >> 2) * BLK + (k & 3) * 32;
+                const uint64_t da = tc::sw128_desc(qa + off, 16, 1024), db = tc::sw128_desc(kb + off, 16, 1024);
+                if (leader) tc::mma_bf16_ss(d_tmem, da, db, IDESC_S, k > 0 ? 1u : 0u);
+            }
+            if (leader) tc::mma_commit(&s_full[g]);
+        };
+        auto issue_pv = [&](int g, int st, bool acc) {
+            const uint32_t vb = vbase + st * TILE_BYTES;
+            const uint32_t d_tmem = tmem + (g ? COL_O1 : COL_O0);
+            const uint32_t p_tmem = tmem + (g ? COL_S1 : COL_S0);
 #pragma unroll
-                for (int k = 0; k < TILE / 16; ++k) {   // 16 keys per step: P columns 8k.., V rows 16k..
-                    const uint64_t db = tc::sw128_desc(vb + k * 2048, BLK, 1024);
-                    if (leader) tc::mma_bf16_ts(d_tmem, p_tmem + k * 8, db, IDESC_O, (j > 0 || k > 0) ? 1u : 0u);
-                }
-            };
-            tc::mbar_wait(q_full, 0);
-            tc::mbar_wait(&k_full[0], 0);
+            for (int k = 0; k < TILE / 16; ++k) {   // 16 keys per step: P columns 8k.., V rows 16k..
+                const uint64_t db = tc::sw128_desc(vb + k * 2048, BLK, 1024);
+                if (leader) tc::mma_bf16_ts(d_tmem, p_tmem + k * 8, db, IDESC_O, (acc || k > 0) ? 1u : 0u);
+            }
+        };
+        int64_t jj = 0;
+        int si = 0;
+        uint32_t pc[2] = {0u, 0u}, ou[2] = {0u, 0u};   // P tiles consumed / segments accumulated, per Q tile
+        Seg sg;
+        while (next_seg(sg)) {
+            if (sg.nkv == 0) continue;
+            const bool two = sg.two;
+            tc::mbar_wait(q_full, (uint32_t)(si & 1));
+            tc::mbar_wait(&k_full[jj & 1], (uint32_t)((jj >> 1) & 1));
             tc::tc_fence_after();
-            issue_s(0, 0);
-            if (two) issue_s(1, 0);
-            if (leader) tc::mma_commit(&k_empty[0]);
-            for (int64_t j = 0; j < nkv; ++j) {
-                const int st = (int)(j & 1);
-                const uint32_t ph = (uint32_t)((j >> 1) & 1);
-                K2_STAMP(6, j);
+            issue_s(0, (int)(jj & 1));
+            if (two) issue_s(1, (int)(jj & 1));
+            if (leader) tc::mma_commit(&k_empty[jj & 1]);
+            for (int64_t j = 0; j < sg.nkv; ++j) {
+                const int64_t J = jj + j;
+                const int st = (int)(J & 1);
+                const uint32_t ph = (uint32_t)((J >> 1) & 1);
+                K2_STAMP(6, J);
                 tc::mbar_wait(&v_full[st], ph);
-                K2_STAMP(7, j);
-                K2_WAIT_P(&p_full[0], (uint32_t)(j & 1));
+                K2_STAMP(7, J);
+                K2_WAIT_P(&p_full[0], pc[0] & 1);
+                ++pc[0];
+                // O0 is reused from the previous segment once its epilogue has read it
+                if (j == 0 && ou[0] > 0) tc::mbar_wait(&o_empty[0], (ou[0] - 1) & 1);
                 tc::tc_fence_after();
-                K2_STAMP(4, j);
-                issue_pv(0, j);
+                K2_STAMP(4, J);
+                issue_pv(0, st, j > 0);
                 if (!two && leader) tc::mma_commit(&v_empty[st]);
-                if (j + 1 == nkv && leader) tc::mma_commit(&o_final[0]);
-                if (j + 1 < nkv) {
-                    const int sn = (int)((j + 1) & 1);
-                    K2_STAMP(9, j);
-                    tc::mbar_wait(&k_full[sn], (uint32_t)(((j + 1) >> 1) & 1));
-                    K2_STAMP(10, j);
+                if (j + 1 == sg.nkv && leader) tc::mma_commit(&o_final[0]);
+                const int sn = (int)((J + 1) & 1);
+                if (j + 1 < sg.nkv) {
+                    K2_STAMP(9, J);
+                    tc::mbar_wait(&k_full[sn], (uint32_t)(((J + 1) >> 1) & 1));
+                    K2_STAMP(10, J);
                     tc::tc_fence_after();
-                    issue_s(0, j + 1);
+                    issue_s(0, sn);
                     if (!two && leader) tc::mma_commit(&k_empty[sn]);
                 }
                 if (!two) continue;
-                K2_STAMP(8, j);
-                K2_WAIT_P(&p_full[1], (uint32_t)(j & 1));
+                K2_STAMP(8, J);
+                K2_WAIT_P(&p_full[1], pc[1] & 1);
+                ++pc[1];
+                if (j == 0 && ou[1] > 0) tc::mbar_wait(&o_empty[1], (ou[1] - 1) & 1);
                 tc::tc_fence_after();
-                K2_STAMP(5, j);
-                issue_pv(1, j);
+                K2_STAMP(5, J);
+                issue_pv(1, st, j > 0);
                 if (leader) tc::mma_commit(&v_empty[st]);
-                if (j + 1 == nkv && leader) tc::mma_commit(&o_final[1]);
-                if (j + 1 < nkv) {
-                    issue_s(1, j + 1);
-                    if (leader) tc::mma_commit(&k_empty[(j + 1) & 1]);
+                if (j + 1 == sg.nkv && leader) tc::mma_commit(&o_final[1]);
+                if (j + 1 < sg.nkv) {
+                    issue_s(1, sn);
+                    if (leader) tc::mma_commit(&k_empty[sn]);
                 }
             }
+            ++ou[0];
+            if (two) ++ou[1];
+            if (leader) tc::mma_commit(q_empty);   // Q buffers free once this segment's MMAs are done
+            jj += sg.nkv;
+            ++si;
         }
+      }
     } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
         // ------------------------------------------------------------------ softmax groups
         const int g = warp >> 2;                               // Q tile
         const int row = (warp & 3) * 32 + lane;                // TMEM lane = tile row
-        const int64_t tile_row0 = (int64_t)g * TILE + (warp & 3) * 32;
-        const bool group_live = g == 0 || two;
-        // warps whose 32 rows are all past the CTA's rows only keep the barrier protocol going
-        const bool warp_live = tile_row0 < nrows;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const uint32_t s_col = tmem + (g ? COL_S1 : COL_S0) + lane_off;
         const uint32_t o_col = tmem + (g ? COL_O1 : COL_O0) + lane_off;
-        float m_run = -INFINITY, m_use = -INFINITY, l = 0.f;
-        for (int64_t j = 0; group_live && j < nkv; ++j) {
-            tc::mbar_wait(&s_full[g], (uint32_t)(j & 1));
-            tc::tc_fence_after();
-            if ((warp & 3) == 0 && lane == 0) K2_STAMP(g, j);
-            if (!warp_live) {
-                tc::tc_fence_before();
-                tc::mbar_arrive(&p_full[g]);
-                continue;
+        uint32_t sc = 0, oc = 0;                               // S tiles / segments seen by this group
+        SoftKeep* const keep = reinterpret_cast<SoftKeep*>(smem + OFF_SEG) + warp;
+        if (lane == 0) {
+            keep->cur = cur;
+            keep->T = T_sk;
+            keep->NG = NG;
+        }
+        __syncwarp();
+        auto soft_next = [&](Seg& sg) -> bool {
+            if (!p.sk) {
+                if (!lpending) return false;
+                lpending = false;
+                split_seg(p, sg);
+                return true;
             }
-            uint32_t s[128];
+            SoftKeep* const k = opaque(keep);
+            SkCursor c = k->cur;
+            const bool ok = sk_next(p, (int)blockIdx.x % p.n_qpairs, c, sg);
+            __syncwarp();
+            if (lane == 0) k->cur = c;
+            __syncwarp();
+            return ok;
+        };
+        Seg sg0;
+        int si_tr = 0;   // segment index (trace builds only)
+        (void)si_tr;
+        while (soft_next(sg0)) {
+            if (tid == 0) K2_STAMP(11, si_tr);
+            const int nkv = sg0.nkv;
+            const bool group_live = g == 0 || sg0.two;
+            // warps whose 32 rows are all past the unit's rows only keep the barrier protocol going
+            const bool warp_live = g * TILE + (warp & 3) * 32 < sg0.nrows;
+            const int kv_left = sg0.len - sg0.t0 * TILE;             // keys from the segment's first tile
+            if (lane == 0) keep->seg = sg0;
+            __syncwarp();
+            float m_run = -INFINITY, m_use = -INFINITY, l = 0.f;
+            for (int j = 0; group_live && j < nkv; ++j) {
+                tc::mbar_wait(&s_full[g], sc & 1);
+                ++sc;
+                tc::tc_fence_after();
+                if ((warp & 3) == 0 && lane == 0) K2_STAMP(g, j);
+                if (!warp_live) {
+                    tc::tc_fence_before();
+                    tc::mbar_arrive(&p_full[g]);
+                    continue;
+                }
+                uint32_t s[128];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) tc::tmem_ld16(s_col + c * 16, s + c * 16);
-            tc::tmem_ld_wait();
-            const int64_t valid = k_end - (t0 + j) * TILE;      // keys of this tile still in range
-            if (valid < TILE) {                                   // only the split's last tile
+                for (int c = 0; c < 8; ++c) tc::tmem_ld16(s_col + c * 16, s + c * 16);
+                tc::tmem_ld_wait();
+                const int valid = kv_left - (int)j * TILE;            // keys of this tile still in range
+                if (valid < TILE) {                                   // only the unit's last tile
 #pragma unroll
-                for (int i = 0; i < 128; ++i)
-                    if (i >= valid) s[i] = 0xFF800000u;           // -inf
-            }
-            // row max on the raw logits (scale > 0), two new values per 3-input max (splitting the
-            // TMEM load to overlap the max measured slower)
-            float mr0 = -INFINITY, mr1 = -INFINITY;
+                    for (int i = 0; i < 128; ++i)
+                        if (i >= valid) s[i] = 0xFF800000u;           // -inf
+                }
+                // row max on the raw logits (scale > 0), two new values per 3-input max (splitting the
+                // TMEM load to overlap the max measured slower)
+                float mr0 = -INFINITY, mr1 = -INFINITY;
 #pragma unroll
-            for (int i = 0; i < 64; i += 2) {
-                mr0 = tc::fmax3(mr0, __uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
-                mr1 = tc::fmax3(mr1, __uint_as_float(s[2 * i + 2]), __uint_as_float(s[2 * i + 3]));
-            }
-            const float mt = fmaxf(mr0, mr1) * p.scale_log2;
-            const float m_new = fmaxf(m_run, mt);
-            m_run = m_new;
-            // lazy rescale: keep the exponent base unless the max grew by more than 8 (x256)
-            const bool need = m_new > m_use + 8.f;
-            if (__any_sync(0xffffffffu, need && j > 0 && m_use > -INFINITY)) {
-                const float alpha = (need && m_use > -INFINITY) ? ex2(m_use - m_new) : 1.f;
+                for (int i = 0; i < 64; i += 2) {
+                    mr0 = tc::fmax3(mr0, __uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
+                    mr1 = tc::fmax3(mr1, __uint_as_float(s[2 * i + 2]), __uint_as_float(s[2 * i + 3]));
+                }
+                const float mt = fmaxf(mr0, mr1) * p.scale_log2;
+                const float m_new = fmaxf(m_run, mt);
+                m_run = m_new;
+                // lazy rescale: keep the exponent base unless the max grew by more than 8 (x256)
+                const bool need = m_new > m_use + 8.f;
+                if (__any_sync(0xffffffffu, need && j > 0 && m_use > -INFINITY)) {
+                    const float alpha = (need && m_use > -INFINITY) ? ex2(m_use - m_new) : 1.f;
 #pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    uint32_t o[8];
-                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                                 : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(o[6]),
-                                   "=r"(o[7])
-                                 : "r"(o_col + c * 8));
-                    tc::tmem_ld_wait();
+                    for (int c = 0; c < 16; ++c) {
+                        uint32_t o[8];
+                        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                                     : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(o[6]),
+                                       "=r"(o[7])
+                                     : "r"(o_col + c * 8));
+                        tc::tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                    tc::tmem_st8(o_col + c * 8, o);
+                        for (int e = 0; e < 8; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                        tc::tmem_st8(o_col + c * 8, o);
+                    }
+                    tc::tmem_st_wait();
+                }
+                if (need) {
+                    if (m_use > -INFINITY) l *= ex2(m_use - m_new);
+                    m_use = m_new;
+                }
+                const float mu = (m_use == -INFINITY) ? 0.f : m_use;
+                // p = exp2(s * scale - mu) in place (one packed FFMA2 per two logits), all 128 first:
+                // the MUFU ops issue back to back instead of each waiting on its consumer; then the row
+                // sum (4 packed FADD2 chains) and the bf16x2 packing of P in place (s[i] <- p[2i], p[2i+1])
+                const uint64_t sc2 = tc::f2(p.scale_log2, p.scale_log2), nmu2 = tc::f2(-mu, -mu);
+#pragma unroll
+                for (int i = 0; i < 64; ++i) {
+                    float x0, x1;
+                    tc::f2_split(tc::ffma2(tc::f2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sc2, nmu2), x0, x1);
+                    float p0, p1;
+                    if ((i & 3) < kEmuOf4) {
+                        tc::exp2_fma2(x0, x1, p0, p1);
+                    } else {
+                        p0 = ex2(x0);
+                        p1 = ex2(x1);
+                    }
+                    s[2 * i] = __float_as_uint(p0);
+                    s[2 * i + 1] = __float_as_uint(p1);
+                }
+                uint64_t acc[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) acc[a] = tc::f2(0.f, 0.f);
+#if SDA_K2_SUM_AFTER
+                // P to TMEM first (packed 16 at a time; the fp32 values stay in s[]), the row sum
+                // after the arrive: the FADD2 chains leave the softmax -> PV -> S chain
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t pk[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        pk[e] = tc::pack_bf16(__uint_as_float(s[16 * c + 2 * e]), __uint_as_float(s[16 * c + 2 * e + 1]));
+                    tc::tmem_st8(s_col + c * 8, pk);
                 }
                 tc::tmem_st_wait();
-            }
-            if (need) {
-                if (m_use > -INFINITY) l *= ex2(m_use - m_new);
-                m_use = m_new;
-            }
-            const float mu = (m_use == -INFINITY) ? 0.f : m_use;
-            // p = exp2(s * scale - mu) in place (one packed FFMA2 per two logits), all 128 first:
-            // the MUFU ops issue back to back instead of each waiting on its consumer; then the row
-            // sum (4 packed FADD2 chains) and the bf16x2 packing of P in place (s[i] <- p[2i], p[2i+1])
-            const uint64_t sc2 = tc::f2(p.scale_log2, p.scale_log2), nmu2 = tc::f2(-mu, -mu);
+                tc::tc_fence_before();
+                if ((warp & 3) == 0 && lane == 0) K2_STAMP(2 + g, j);
+                tc::mbar_arrive(&p_full[g]);
 #pragma unroll
-            for (int i = 0; i < 64; ++i) {
-                float x0, x1;
-                tc::f2_split(tc::ffma2(tc::f2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sc2, nmu2), x0, x1);
-                float p0, p1;
-                if ((i & 3) < kEmuOf4) {
-                    tc::exp2_fma2(x0, x1, p0, p1);
-                } else {
-                    p0 = ex2(x0);
-                    p1 = ex2(x1);
+                for (int i = 0; i < 64; ++i)
+                    acc[i & 3] = tc::fadd2(acc[i & 3], tc::f2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])));
+#else
+#pragma unroll
+                for (int i = 0; i < 64; ++i) {
+                    const float p0 = __uint_as_float(s[2 * i]), p1 = __uint_as_float(s[2 * i + 1]);
+                    acc[i & 3] = tc::fadd2(acc[i & 3], tc::f2(p0, p1));
+                    s[i] = tc::pack_bf16(p0, p1);
                 }
-                s[2 * i] = __float_as_uint(p0);
-                s[2 * i + 1] = __float_as_uint(p1);
-            }
-            uint64_t acc[4];
+#endif
+                float a0, a1, b0, b1, c0, c1, d0, d1;
+                tc::f2_split(acc[0], a0, a1);
+                tc::f2_split(acc[1], b0, b1);
+                tc::f2_split(acc[2], c0, c1);
+                tc::f2_split(acc[3], d0, d1);
+                l += ((a0 + a1) + (b0 + b1)) + ((c0 + c1) + (d0 + d1));
+#if !SDA_K2_SUM_AFTER
 #pragma unroll
-            for (int a = 0; a < 4; ++a) acc[a] = tc::f2(0.f, 0.f);
-#pragma unroll
-            for (int i = 0; i < 64; ++i) {
-                const float p0 = __uint_as_float(s[2 * i]), p1 = __uint_as_float(s[2 * i + 1]);
-                acc[i & 3] = tc::fadd2(acc[i & 3], tc::f2(p0, p1));
-                s[i] = tc::pack_bf16(p0, p1);
+                for (int c = 0; c < 8; ++c) tc::tmem_st8(s_col + c * 8, s + c * 8);
+                tc::tmem_st_wait();
+                tc::tc_fence_before();
+                if ((warp & 3) == 0 && lane == 0) K2_STAMP(2 + g, j);
+                tc::mbar_arrive(&p_full[g]);
+#endif
             }
-            float a0, a1, b0, b1, c0, c1, d0, d1;
-            tc::f2_split(acc[0], a0, a1);
-            tc::f2_split(acc[1], b0, b1);
-            tc::f2_split(acc[2], c0, c1);
-            tc::f2_split(acc[3], d0, d1);
-            l += ((a0 + a1) + (b0 + b1)) + ((c0 + c1) + (d0 + d1));
-#pragma unroll
-            for (int c = 0; c < 8; ++c) tc::tmem_st8(s_col + c * 8, s + c * 8);
-            tc::tmem_st_wait();
-            tc::tc_fence_before();
-            if ((warp & 3) == 0 && lane == 0) K2_STAMP(2 + g, j);
-            tc::mbar_arrive(&p_full[g]);
-        }
-        // epilogue: O / l, (row_max, exp_sum) in natural units
-        const int64_t r_in = (int64_t)g * TILE + row;          // row within this CTA's rows
-        const bool store = r_in < nrows;
-        // output rows mirror the Q rows ([split][request][q head][q row]); head_row already holds
-        // request, head and row-tile offsets
-        int64_t orow = (int64_t)split * p.n_batch * p.q_heads * p.q_rows + head_row + r_in;
-        float* out_o = p.out_o;
-        float* out_stats = p.out_stats;
-        if (p.remote) {   // the packed record of request b in its inquirer's receive slot (one split)
-            const int64_t dest = b / p.b_per, i = b % p.b_per;
-            float* rec = p.rec_peer[dest] + i * p.rec_stride;
-            orow = head_row - b * p.q_heads * p.q_rows + r_in;   // (head, row) within the request
-            out_o = rec;
-            out_stats = rec + (int64_t)p.q_heads * p.q_rows * D;
-        }
-        if (group_live && warp_live) {
-            if (nkv > 0) {
-                tc::mbar_wait(&o_final[g], 0);
-                tc::tc_fence_after();
-            }
+            // epilogue: O / l, (row_max, exp_sum) in natural units
+            if (tid == 0) K2_STAMP(12, si_tr);
+            const SoftKeep* const kk = opaque(keep);
+            const Seg sg = kk->seg;
+            const int64_t r_in = (int64_t)g * TILE + row;          // row within the unit
+            const bool store = r_in < sg.nrows;
             const float inv = l > 0.f ? 1.f / l : 0.f;
-            // remote records: stage the warp's 32 rows in SMEM (group 0 reuses the K ring, whose
-            // last reader has completed; group 1 the V ring) and write them as one contiguous
-            // 16 KB run -- whole 512-byte rows per warp store instead of 32 scattered 16-byte
-            // pieces, which NVLink carries far less efficiently
-            // (rows of 512 B, 16-byte chunks XOR-swizzled by row & 7 against bank conflicts)
-            float* stg = reinterpret_cast<float*>(smem + (g ? OFF_V : OFF_K) + (warp & 3) * 32 * 128 * 4);
+            const float st_max = l > 0.f ? m_run / kLog2e : -INFINITY;
+            const float st_sum = l > 0.f ? l * ex2(m_use - m_run) : 0.f;
+            if (p.sk) {
+                // stream-K: a unit held whole by this CTA is written straight from TMEM (as in split
+                // mode); a piece goes to this CTA's scratch slot, and the last of the unit's pieces
+                // to finish merges them into the output
+                const int T_sk = kk->T, NG = kk->NG, nq = p.n_qpairs, qp_sk = (int)blockIdx.x % nq;
+                const int g_a = sk_group_of(sg.ub, T_sk, NG);
+                const int P = 1 + sk_group_of(sg.ub + sg.nt - 1, T_sk, NG) - g_a;   // pieces of the unit
+                float* out_o = p.out_o;
+                float* out_stats = p.out_stats;
+                int64_t orow0 = sg.head_row;   // one split: output rows mirror the Q rows
+                if (p.remote) {
+                    float* rec = p.rec_peer[sg.b / p.b_per] + (sg.b % p.b_per) * p.rec_stride;
+                    orow0 = sg.head_row - (int64_t)sg.b * p.q_heads * p.q_rows;
+                    out_o = rec;
+                    out_stats = rec + (int64_t)p.q_heads * p.q_rows * D;
+                }
+                // remote records are staged in slot 2 and copied out as whole 512-byte rows
+                const bool direct = P == 1 && !p.remote;
+                float* const slot2 = sk_slot(p, (int)blockIdx.x, 2);
+                float* const slot = P == 1 ? slot2 : sk_slot(p, (int)blockIdx.x, sg.first ? 0 : 1);
+                float* const dst_o = direct ? out_o + orow0 * D : slot;
+                float* const dst_st = direct ? out_stats + orow0 * 2 : slot + 2 * TILE * D;
+                if (group_live) {
+                    if (warp_live) {
+                        tc::mbar_wait(&o_final[g], oc & 1);
+                        tc::tc_fence_after();
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                uint32_t o[16];
+                        for (int c = 0; c < 8; ++c) {
+                            uint32_t o[16];
+                            tc::tmem_ld16(o_col + c * 16, o);
+                            tc::tmem_ld_wait();
+                            if (store) {
+                                float4* dst = reinterpret_cast<float4*>(dst_o + r_in * D + c * 16);
+#pragma unroll
+                                for (int e = 0; e < 4; ++e)
+                                    dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                                         __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+                            }
+                        }
+                    }
+                    ++oc;
+                    tc::tc_fence_before();
+                    tc::mbar_arrive(&o_empty[g]);   // O_g may be overwritten by the next segment
+                    if (store) *reinterpret_cast<float2*>(dst_st + r_in * 2) = make_float2(st_max, st_sum);
+                }
+                if (tid == 0) K2_STAMP(13, si_tr);
+                if (direct) {
+                    ++si_tr;
+                    continue;
+                }
+                __threadfence();
+                softmax_bar();
+                if (tid == 0) {
+                    uint32_t t = 0;
+                    if (P > 1) {
+                        t = atomicAdd(&p.sk_tick[sg.unit], 1u);
+                        __threadfence();
+                    }
+                    *sk_ticket = t;
+                }
+                softmax_bar();
+                if (tid == 0) K2_STAMP(14, si_tr);
+                if ((int)*sk_ticket == P - 1) {
+                    if (P > 1) {
+                        // warp w merges rows 32w .. 32w+31: lane = row for the weights (from each
+                        // piece's stats), then lanes across a row's 512 bytes for O' -- 16 rows
+                        // (8 KB) in flight per warp, coalesced reads and writes. Piece k lives in
+                        // CTA (group g_a + k, this pair): its first segment's slot unless that
+                        // group's range starts before the unit.
+                        __threadfence();
+                        auto piece = [&](int k) -> const float* {
+                            const int gk = g_a + k;
+                            return sk_slot(p, gk * nq + qp_sk, sk_lo(T_sk, NG, gk) < sg.ub ? 1 : 0);
+                        };
+                        const int r_l = warp * 32 + lane;
+                        const bool live_l = r_l < sg.nrows;
+                        float mx = -INFINITY, L = 0.f;
+                        for (int k = 0; k < P && live_l; ++k) {
+                            const float2 stt = __ldcg(reinterpret_cast<const float2*>(piece(k) + 2 * TILE * D + r_l * 2));
+                            if (stt.y > 0.f) mx = fmaxf(mx, stt.x);
+                        }
+                        for (int k = 0; k < P && live_l; ++k) {
+                            const float2 stt = __ldcg(reinterpret_cast<const float2*>(piece(k) + 2 * TILE * D + r_l * 2));
+                            if (stt.y > 0.f) L += stt.y * ex2((stt.x - mx) * kLog2e);
+                        }
+                        const float iv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll 1
+                        for (int h = 0; h < 2; ++h) {
+                            const int rb = warp * 32 + h * 16;     // first row of this batch
+                            float4 acc[16];
+#pragma unroll
+                            for (int u = 0; u < 16; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            for (int k = 0; k < P; ++k) {
+                                const float* pk = piece(k);
+                                float wl = 0.f;
+                                if (live_l) {
+                                    const float2 stt = __ldcg(reinterpret_cast<const float2*>(pk + 2 * TILE * D + r_l * 2));
+                                    wl = stt.y > 0.f ? stt.y * ex2((stt.x - mx) * kLog2e) * iv : 0.f;
+                                }
+                                float4 v[16];
+#pragma unroll
+                                for (int u = 0; u < 16; ++u)
+                                    v[u] = rb + u < sg.nrows ? __ldcg(reinterpret_cast<const float4*>(pk + (rb + u) * D) + lane)
+                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                                for (int u = 0; u < 16; ++u) {
+                                    const float w = __shfl_sync(0xffffffffu, wl, h * 16 + u);
+                                    acc[u].x += w * v[u].x;
+                                    acc[u].y += w * v[u].y;
+                                    acc[u].z += w * v[u].z;
+                                    acc[u].w += w * v[u].w;
+                                }
+                            }
+#pragma unroll
+                            for (int u = 0; u < 16; ++u)
+                                if (rb + u < sg.nrows) reinterpret_cast<float4*>(out_o + (orow0 + rb + u) * D)[lane] = acc[u];
+                        }
+                        if (live_l) *reinterpret_cast<float2*>(out_stats + (orow0 + r_l) * 2) = make_float2(L > 0.f ? mx : -INFINITY, L);
+                        if (p.remote) __threadfence_system();
+                    } else if (p.remote) {
+                        // one piece: slot 2 -> the inquirer's record, a warp per row, 4 rows in flight
+                        softmax_bar();
+                        for (int r = warp; r < sg.nrows; r += 32) {
+                            float4 v[4];
+                            float2 sv[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int rr = r + u * 8;
+                                if (rr < sg.nrows) {
+                                    v[u] = __ldcg(reinterpret_cast<const float4*>(slot2 + rr * D) + lane);
+                                    sv[u] = __ldcg(reinterpret_cast<const float2*>(slot2 + 2 * TILE * D + rr * 2));
+                                }
+                            }
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int rr = r + u * 8;
+                                if (rr < sg.nrows) {
+                                    reinterpret_cast<float4*>(out_o + (orow0 + rr) * D)[lane] = v[u];
+                                    if (lane == 0) *reinterpret_cast<float2*>(out_stats + (orow0 + rr) * 2) = sv[u];
+                                }
+                            }
+                        }
+                        __threadfence_system();
+                    }
+                    softmax_bar();
+                    if (tid == 0) {
+                        if (P > 1) p.sk_tick[sg.unit] = 0u;   // self-resetting for the next launch
+                        if (p.remote) {   // the unit completing a destination's records raises its flag
+                            const int64_t dest = sg.b / p.b_per;
+                            const unsigned per_dest = (unsigned)((int64_t)p.q_heads * nq * p.b_per);
+                            if (atomicAdd(&p.dest_counters[dest], 1u) == per_dest - 1) {
+                                p.dest_counters[dest] = 0;
+                                __threadfence_system();
+                                flag_raise(p.peer_flag[dest], *p.epoch);
+                            }
+                        }
+                    }
+                }
+                softmax_bar();   // scratch slot 2 and the ticket are reused by the next segment
+                if (tid == 0) K2_STAMP(15, si_tr);
+                ++si_tr;
+                continue;
+            }
+            // split mode: output rows mirror the Q rows ([split][request][q head][q row])
+            int64_t orow = (int64_t)sg.split * p.n_batch * p.q_heads * p.q_rows + sg.head_row + r_in;
+            float* out_o = p.out_o;
+            float* out_stats = p.out_stats;
+            if (p.remote) {   // the packed record of request b in its inquirer's receive slot (one split)
+                const int64_t dest = sg.b / p.b_per, i = sg.b % p.b_per;
+                float* rec = p.rec_peer[dest] + i * p.rec_stride;
+                orow = sg.head_row - (int64_t)sg.b * p.q_heads * p.q_rows + r_in;   // (head, row) within the request
+                out_o = rec;
+                out_stats = rec + (int64_t)p.q_heads * p.q_rows * D;
+            }
+            if (group_live && warp_live) {
                 if (nkv > 0) {
-                    tc::tmem_ld16(o_col + c * 16, o);
-                    tc::tmem_ld_wait();
-                } else {
+                    tc::mbar_wait(&o_final[g], 0);
+                    tc::tc_fence_after();
+                }
+                // remote records: stage the warp's 32 rows in SMEM (group 0 reuses the K ring, whose
+                // last reader has completed; group 1 the V ring) and write them as one contiguous
+                // 16 KB run -- whole 512-byte rows per warp store instead of 32 scattered 16-byte
+                // pieces, which NVLink carries far less efficiently
+                // (rows of 512 B, 16-byte chunks XOR-swizzled by row & 7 against bank conflicts)
+                float* stg = reinterpret_cast<float*>(smem + (g ? OFF_V : OFF_K) + (warp & 3) * 32 * 128 * 4);
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) o[e] = 0u;
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t o[16];
+                    if (nkv > 0) {
+                        tc::tmem_ld16(o_col + c * 16, o);
+                        tc::tmem_ld_wait();
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) o[e] = 0u;
+                    }
+                    if (p.remote) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            *reinterpret_cast<float4*>(stg + lane * 128 + (((c * 4 + e) ^ (lane & 7)) * 4)) =
+                                make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                            __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+                    } else if (store) {
+                        float4* dst = reinterpret_cast<float4*>(out_o + orow * D + c * 16);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                                 __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+                    }
                 }
                 if (p.remote) {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        *reinterpret_cast<float4*>(stg + lane * 128 + (((c * 4 + e) ^ (lane & 7)) * 4)) =
-                            make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
-                                        __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
-                } else if (store) {
-                    float4* dst = reinterpret_cast<float4*>(out_o + orow * D + c * 16);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
-                                             __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+                    __syncwarp();
+                    // rows orow(lane 0) .. +31 are consecutive: 32 x 512 B contiguous (the tail of a
+                    // partial tile stops at nrows)
+                    const int64_t row0 = orow - lane;
+                    const int nvalid = (int)min((int64_t)32, sg.nrows - (r_in - lane));
+                    for (int r = 0; r < nvalid; ++r)
+                        reinterpret_cast<float4*>(out_o + (row0 + r) * D)[lane] =
+                            *reinterpret_cast<const float4*>(stg + r * 128 + ((lane ^ (r & 7)) * 4));
+                }
+                if (store) {
+                    out_stats[orow * 2 + 0] = st_max;
+                    out_stats[orow * 2 + 1] = st_sum;
                 }
             }
-            if (p.remote) {
-                __syncwarp();
-                // rows orow(lane 0) .. +31 are consecutive: 32 x 512 B contiguous (the tail of a
-                // partial tile stops at nrows)
-                const int64_t row0 = orow - lane;
-                const int nvalid = (int)min((int64_t)32, nrows - (r_in - lane));
-                for (int r = 0; r < nvalid; ++r)
-                    reinterpret_cast<float4*>(out_o + (row0 + r) * D)[lane] =
-                        *reinterpret_cast<const float4*>(stg + r * 128 + ((lane ^ (r & 7)) * 4));
-            }
-            if (store) {
-                const bool any = l > 0.f;
-                out_stats[orow * 2 + 0] = any ? m_run / kLog2e : -INFINITY;
-                out_stats[orow * 2 + 1] = any ? l * ex2(m_use - m_run) : 0.f;
+        }
+        if (p.sk) {
+            // requests with no keys contribute no tiles: their units (zero O', stats (-inf, 0)) go
+            // round-robin over the CTAs
+            const int64_t upr = (int64_t)p.q_heads * nq;
+            for (int64_t b = 0; b < p.n_batch; ++b) {
+                if (ntile_of(p, b) != 0) continue;
+                for (int64_t ui = 0; ui < upr; ++ui) {
+                    if ((b * upr + ui) % gridDim.x != blockIdx.x) continue;
+                    Seg z;
+                    fill_unit(p, (int)b, (int)(ui / nq), (int)(ui % nq), z);
+                    float* out_o = p.out_o;
+                    float* out_stats = p.out_stats;
+                    int64_t orow0 = z.head_row;
+                    if (p.remote) {
+                        float* rec = p.rec_peer[b / p.b_per] + (b % p.b_per) * p.rec_stride;
+                        orow0 = z.head_row - b * p.q_heads * p.q_rows;
+                        out_o = rec;
+                        out_stats = rec + (int64_t)p.q_heads * p.q_rows * D;
+                    }
+                    for (int64_t r = warp; r < z.nrows; r += 8) {
+                        reinterpret_cast<float4*>(out_o + (orow0 + r) * D)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (lane == 0) *reinterpret_cast<float2*>(out_stats + (orow0 + r) * 2) = make_float2(-INFINITY, 0.f);
+                    }
+                    if (p.remote) {
+                        __threadfence_system();
+                        softmax_bar();
+                        if (tid == 0) {
+                            const int64_t dest = b / p.b_per;
+                            const unsigned per_dest = (unsigned)(upr * p.b_per);
+                            if (atomicAdd(&p.dest_counters[dest], 1u) == per_dest - 1) {
+                                p.dest_counters[dest] = 0;
+                                __threadfence_system();
+                                flag_raise(p.peer_flag[dest], *p.epoch);
+                            }
+                        }
+                    }
+                }
             }
         }
     }
-    if (p.remote) __threadfence_system();   // this CTA's record stores visible system-wide
+    if (warp == 0) K2_CTA_STAMP(1);
+    if (p.remote && !p.sk) __threadfence_system();   // this CTA's record stores visible system-wide
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
-    if (p.remote && tid == 0) {   // the CTA completing a destination's records raises its flag
-        const int64_t dest = b / p.b_per;
+    if (p.remote && !p.sk && tid == 0) {   // the CTA completing a destination's records raises its flag
+        const int64_t dest = (int64_t)(blockIdx.z / p.n_splits) / p.b_per;
         const unsigned per_dest = gridDim.x * gridDim.y * (unsigned)(p.b_per * p.n_splits);
         if (atomicAdd(&p.dest_counters[dest], 1u) == per_dest - 1) {
             p.dest_counters[dest] = 0;
@@ -453,6 +922,77 @@ static bool k2_grouped(const K2Params& p) {
 bool k2_prefill_tc_eligible(const K2Params& p, int d, int qdt, int kvdt) {
     return d == 128 && qdt == SDA_BF16 && kvdt == SDA_BF16 && (p.q_rows >= 64 || k2_grouped(p));
 }
+
+// Stream-K scratch, one per (device, stream): launches on one stream are ordered, so they can
+// share it; a stream being captured into a graph gets no new allocation (split mode instead).
+namespace {
+struct SkScratch {
+    int dev;
+    cudaStream_t st;
+    float* buf;
+    size_t buf_floats;
+    uint32_t* tick;
+    size_t n_tick;
+    uint64_t used;
+};
+std::mutex g_sk_mu;
+std::vector<SkScratch> g_sk;
+uint64_t g_sk_clock = 0;
+constexpr size_t kSkMaxPerDevice = 8;
+
+bool sk_scratch(cudaStream_t st, size_t need_floats, size_t need_tick, float** buf, uint32_t** tick) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    std::lock_guard<std::mutex> lk(g_sk_mu);
+    SkScratch* e = nullptr;
+    size_t on_dev = 0;
+    for (auto& x : g_sk)
+        if (x.dev == dev) {
+            ++on_dev;
+            if (x.st == st) e = &x;
+        }
+    if (e && e->buf_floats >= need_floats && e->n_tick >= need_tick) {
+        e->used = ++g_sk_clock;
+        *buf = e->buf;
+        *tick = e->tick;
+        return true;
+    }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+    if (!e && on_dev >= kSkMaxPerDevice) {   // evict the least recently used entry of this device
+        for (auto& x : g_sk)
+            if (x.dev == dev && (!e || x.used < e->used)) e = &x;
+    }
+    if (e) {   // grow or recycle: nothing may still read the old buffers
+        if (cudaDeviceSynchronize() != cudaSuccess) return false;
+        cudaFree(e->buf);
+        cudaFree(e->tick);
+    } else {
+        g_sk.push_back(SkScratch{dev, st, nullptr, 0, nullptr, 0, 0});
+        e = &g_sk.back();
+    }
+    e->st = st;
+    e->buf = nullptr;
+    e->tick = nullptr;
+    e->buf_floats = e->n_tick = 0;
+    if (cudaMalloc(&e->buf, need_floats * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&e->tick, need_tick * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMemsetAsync(e->tick, 0, need_tick * sizeof(uint32_t), st) != cudaSuccess) {
+        cudaFree(e->buf);
+        cudaFree(e->tick);
+        e->buf = nullptr;
+        e->tick = nullptr;
+        cudaGetLastError();
+        return false;
+    }
+    e->buf_floats = need_floats;
+    e->n_tick = need_tick;
+    e->used = ++g_sk_clock;
+    *buf = e->buf;
+    *tick = e->tick;
+    return true;
+}
+}  // namespace
 
 cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
     using namespace k2tc;
@@ -482,11 +1022,34 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
     }
     p.dest_counters = q.dest_counters;
     p.epoch = q.epoch;
+    p.sk = 0;
+    p.sk_buf = nullptr;
+    p.sk_tick = nullptr;
     CUtensorMap qm, km, vm;
     if (!make_tmap_bf16_2d(&qm, q.q, q.n_batch * q.q_heads * q.q_rows, D, TILE) ||
         !make_tmap_bf16_2d(&km, q.k, q.n_batch * q.kv_heads * q.kv_cap, D, TILE) ||
         !make_tmap_bf16_2d(&vm, q.v, q.n_batch * q.kv_heads * q.kv_cap, D, TILE))
         return cudaErrorInvalidValue;
+    // One split (not grouped): stream-K over a persistent grid of groups of n_qpairs CTAs, one
+    // CTA per SM, so the last wave is never partial (C3: 256 units on 148 SMs ran as 2 waves, the
+    // second 73 % full). Its tile count is bounded with every request at kv_cap.
+    const int64_t sms = device_sms();
+    const int64_t units = q.n_batch * q.q_heads * (int64_t)p.n_qpairs;
+    const int64_t tiles_max = q.n_batch * q.q_heads * ((q.kv_cap + TILE - 1) / TILE);
+    if (!p.grouped && q.n_splits == 1 && p.n_qpairs <= sms && tiles_max < (int64_t)INT32_MAX && units < (int64_t)INT32_MAX &&
+        !std::getenv("SDA_K2_NO_SK")) {
+        const int64_t NG = std::max<int64_t>(1, std::min<int64_t>(sms / p.n_qpairs, tiles_max));
+        const int64_t G = NG * p.n_qpairs;
+        float* buf = nullptr;
+        uint32_t* tick = nullptr;
+        if (sk_scratch(st, (size_t)G * 3 * (size_t)SK_SLOT, (size_t)std::max<int64_t>(1, units), &buf, &tick)) {
+            p.sk = 1;
+            p.sk_buf = buf;
+            p.sk_tick = tick;
+            k2_prefill_tc_kernel<<<dim3((unsigned)G), THREADS, SMEM, st>>>(p, qm, km, vm);
+            return cudaGetLastError();
+        }
+    }
     const dim3 grid((unsigned)p.n_qpairs, (unsigned)(p.grouped ? q.kv_heads : q.q_heads),
                     (unsigned)(q.n_batch * q.n_splits));
     k2_prefill_tc_kernel<<<grid, THREADS, SMEM, st>>>(p, qm, km, vm);
@@ -498,5 +1061,8 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
 #ifdef SDA_K2_TRACE
 extern "C" int sda_debug_k2_trace(void* host) {
     return (int)cudaMemcpyFromSymbol(host, sda::g_k2_trace, sizeof(sda::g_k2_trace));
+}
+extern "C" int sda_debug_k2_cta(void* host) {
+    return (int)cudaMemcpyFromSymbol(host, sda::g_k2_cta, sizeof(sda::g_k2_cta));
 }
 #endif

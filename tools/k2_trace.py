@@ -40,5 +40,42 @@ def main():
               f"{t[3][j]-t[1][j]:5d} {t[4][j]-base:8d} {t[5][j]-base:8d} {per:6d}")
 
 
+
+
+def main_sk():
+    """stream-K mode (one split): CTA 0's segments -- start, tile loop done, O read, ticket, end (us)."""
+    Lq, Lk, H, D = 2048, 16384, int(os.environ.get("H", "32")), 128
+    dev = torch.device("cuda")
+    q = torch.randn((1, H, Lq, D), device=dev).to(torch.bfloat16)
+    k = torch.randn((1, H, Lk, D), device=dev).to(torch.bfloat16)
+    v = torch.randn((1, H, Lk, D), device=dev).to(torch.bfloat16)
+    for _ in range(3):
+        ops.partial_attention(q, k, v, n_splits=1)
+    torch.cuda.synchronize()
+    buf = np.zeros((16, 64), dtype=np.uint64)
+    capi.LIB.sda_debug_k2_trace.argtypes = [ct.c_void_p]
+    assert capi.LIB.sda_debug_k2_trace(buf.ctypes.data) == 0
+    t = buf.astype(np.int64)
+    base = t[11][0]
+    print("seg  start  loop_done  O_read  ticket  end   (us from segment 0 start)")
+    for si in range(8):
+        if t[11][si] == 0:
+            break
+        print(si, [round((t[kk][si] - base) / 1e3, 2) if t[kk][si] else None for kk in (11, 12, 13, 14, 15)])
+    cta = np.zeros((1024, 2), dtype=np.uint64)
+    capi.LIB.sda_debug_k2_cta.argtypes = [ct.c_void_p]
+    assert capi.LIB.sda_debug_k2_cta(cta.ctypes.data) == 0
+    c = cta.astype(np.int64)
+    n = int((c[:, 0] > 0).sum())
+    c = c[:n]
+    t0 = c[:, 0].min()
+    end = (c[:, 1] - t0) / 1e3
+    print(f"{n} CTAs: start spread {(c[:, 0].max() - t0) / 1e3:.2f} us; end min {end.min():.1f} median "
+          f"{np.median(end):.1f} max {end.max():.1f} us")
+    nq = 8
+    for g in range(n // nq):
+        print(f"group {g:2d}: end {end[g * nq:(g + 1) * nq].min():6.1f} .. {end[g * nq:(g + 1) * nq].max():6.1f}")
+
+
 if __name__ == "__main__":
-    main()
+    main_sk() if os.environ.get("SK") else main()
