@@ -8,7 +8,8 @@
 //
 // One CTA = up to two 128-row Q tiles of one (request, q head) x one KV split -- or, for GQA
 // decode ("grouped" mode), the G q heads x L_q rows of one (request, kv head), so K/V stream
-// from HBM once per group instead of once per q head; 10 warps:
+// from HBM once per group instead of once per q head. With one split the CTAs are persistent
+// and walk ranges of key tiles instead (stream-K, below). 12 warps (10, 11 idle; setmaxnreg):
 //   warp 8      TMA producer: Q0/Q1 once, then K_j / V_j tiles (128 keys) into 2-stage rings
 //   warp 9      MMA issuer (one lane): S_g = Q_g K_j^T (SS, K-major) into TMEM, and
 //               O_g += P_g V_j with P_g read straight from TMEM (TS form; V as an MN-major B)
@@ -256,6 +257,27 @@ __device__ __forceinline__ int sk_group_of(int x, int T, int NG) {
 constexpr int64_t SK_SLOT = 2 * TILE * D + 2 * TILE * 2;
 __device__ __forceinline__ float* sk_slot(const K2TcParams& p, int cta, int k) {
     return p.sk_buf + ((int64_t)cta * 3 + k) * SK_SLOT;
+}
+
+// 16 f32 of a thread's own output row (x inv) as two 256-bit stores: whole 32-byte sectors per
+// lane instead of the half sectors of 16-byte stores (the thread-per-row epilogue)
+__device__ __forceinline__ void store_row16(float* dst, const uint32_t (&o)[16], float inv) {
+    if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 8 * h),
+                         "f"(__uint_as_float(o[8 * h + 0]) * inv), "f"(__uint_as_float(o[8 * h + 1]) * inv),
+                         "f"(__uint_as_float(o[8 * h + 2]) * inv), "f"(__uint_as_float(o[8 * h + 3]) * inv),
+                         "f"(__uint_as_float(o[8 * h + 4]) * inv), "f"(__uint_as_float(o[8 * h + 5]) * inv),
+                         "f"(__uint_as_float(o[8 * h + 6]) * inv), "f"(__uint_as_float(o[8 * h + 7]) * inv)
+                         : "memory");
+    } else {   // a caller's output view only 16-byte aligned
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            reinterpret_cast<float4*>(dst)[e] =
+                make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                            __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+    }
 }
 
 __device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
@@ -659,13 +681,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                             uint32_t o[16];
                             tc::tmem_ld16(o_col + c * 16, o);
                             tc::tmem_ld_wait();
-                            if (store) {
-                                float4* dst = reinterpret_cast<float4*>(dst_o + r_in * D + c * 16);
-#pragma unroll
-                                for (int e = 0; e < 4; ++e)
-                                    dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
-                                                         __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
-                            }
+                            if (store) store_row16(dst_o + r_in * D + c * 16, o, inv);
                         }
                     }
                     ++oc;
@@ -830,11 +846,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                                 make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
                                             __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
                     } else if (store) {
-                        float4* dst = reinterpret_cast<float4*>(out_o + orow * D + c * 16);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
-                                                 __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+                        store_row16(out_o + orow * D + c * 16, o, inv);
                     }
                 }
                 if (p.remote) {
