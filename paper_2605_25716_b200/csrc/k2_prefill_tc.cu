@@ -122,6 +122,9 @@ constexpr int kEmuOf4 = SDA_K2_EMU_OF4;
 #ifndef SDA_K2_SUM_AFTER
 #define SDA_K2_SUM_AFTER 1
 #endif
+#ifndef SDA_K2_SPEC
+#define SDA_K2_SPEC 0
+#endif
 }  // namespace k2tc
 
 namespace k2tc {
@@ -536,22 +539,61 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                     continue;
                 }
                 uint32_t s[128];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) tc::tmem_ld16(s_col + c * 16, s + c * 16);
-                tc::tmem_ld_wait();
                 const int valid = kv_left - (int)j * TILE;            // keys of this tile still in range
-                if (valid < TILE) {                                   // only the unit's last tile
+                auto load_s = [&]() {
 #pragma unroll
-                    for (int i = 0; i < 128; ++i)
-                        if (i >= valid) s[i] = 0xFF800000u;           // -inf
-                }
-                // row max on the raw logits (scale > 0), two new values per 3-input max (splitting the
-                // TMEM load to overlap the max measured slower)
+                    for (int c = 0; c < 8; ++c) tc::tmem_ld16(s_col + c * 16, s + c * 16);
+                    tc::tmem_ld_wait();
+                    if (valid < TILE) {                               // only the unit's last tile
+#pragma unroll
+                        for (int i = 0; i < 128; ++i)
+                            if (i >= valid) s[i] = 0xFF800000u;       // -inf
+                    }
+                };
+                // p = exp2(s * scale - mu) in place (one packed FFMA2 per two logits), all 128 first:
+                // the MUFU ops issue back to back instead of each waiting on its consumer. With
+                // `with_max` the row max of the raw logits is taken in the same pass.
+                auto exp_pass = [&](float mu, bool with_max, float& mr0, float& mr1) {
+                    const uint64_t sc2 = tc::f2(p.scale_log2, p.scale_log2), nmu2 = tc::f2(-mu, -mu);
+#pragma unroll
+                    for (int i = 0; i < 64; ++i) {
+                        const float r0 = __uint_as_float(s[2 * i]), r1 = __uint_as_float(s[2 * i + 1]);
+                        if (with_max) {
+                            if (i & 1) mr1 = tc::fmax3(mr1, r0, r1);
+                            else mr0 = tc::fmax3(mr0, r0, r1);
+                        }
+                        float x0, x1;
+                        tc::f2_split(tc::ffma2(tc::f2(r0, r1), sc2, nmu2), x0, x1);
+                        float p0, p1;
+                        if ((i & 3) < kEmuOf4) {
+                            tc::exp2_fma2(x0, x1, p0, p1);
+                        } else {
+                            p0 = ex2(x0);
+                            p1 = ex2(x1);
+                        }
+                        s[2 * i] = __float_as_uint(p0);
+                        s[2 * i + 1] = __float_as_uint(p1);
+                    }
+                };
+                load_s();
                 float mr0 = -INFINITY, mr1 = -INFINITY;
+#if SDA_K2_SPEC
+                // speculative: once every row of the warp has a base, exponentiate against it with
+                // the tile max in the same pass (the max no longer sits between the S load and the
+                // exponentials); a row whose max grew by more than 8 re-reads S from TMEM below
+                const bool spec = __all_sync(0xffffffffu, m_use > -INFINITY);
+#else
+                constexpr bool spec = false;
+#endif
+                if (spec) {
+                    exp_pass(m_use, true, mr0, mr1);
+                } else {
+                    // row max on the raw logits (scale > 0), two new values per 3-input max
 #pragma unroll
-                for (int i = 0; i < 64; i += 2) {
-                    mr0 = tc::fmax3(mr0, __uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
-                    mr1 = tc::fmax3(mr1, __uint_as_float(s[2 * i + 2]), __uint_as_float(s[2 * i + 3]));
+                    for (int i = 0; i < 64; i += 2) {
+                        mr0 = tc::fmax3(mr0, __uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
+                        mr1 = tc::fmax3(mr1, __uint_as_float(s[2 * i + 2]), __uint_as_float(s[2 * i + 3]));
+                    }
                 }
                 const float mt = fmaxf(mr0, mr1) * p.scale_log2;
                 const float m_new = fmaxf(m_run, mt);
@@ -578,24 +620,11 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                     if (m_use > -INFINITY) l *= ex2(m_use - m_new);
                     m_use = m_new;
                 }
-                const float mu = (m_use == -INFINITY) ? 0.f : m_use;
-                // p = exp2(s * scale - mu) in place (one packed FFMA2 per two logits), all 128 first:
-                // the MUFU ops issue back to back instead of each waiting on its consumer; then the row
-                // sum (4 packed FADD2 chains) and the bf16x2 packing of P in place (s[i] <- p[2i], p[2i+1])
-                const uint64_t sc2 = tc::f2(p.scale_log2, p.scale_log2), nmu2 = tc::f2(-mu, -mu);
-#pragma unroll
-                for (int i = 0; i < 64; ++i) {
-                    float x0, x1;
-                    tc::f2_split(tc::ffma2(tc::f2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sc2, nmu2), x0, x1);
-                    float p0, p1;
-                    if ((i & 3) < kEmuOf4) {
-                        tc::exp2_fma2(x0, x1, p0, p1);
-                    } else {
-                        p0 = ex2(x0);
-                        p1 = ex2(x1);
-                    }
-                    s[2 * i] = __float_as_uint(p0);
-                    s[2 * i + 1] = __float_as_uint(p1);
+                if (!spec) {
+                    exp_pass((m_use == -INFINITY) ? 0.f : m_use, false, mr0, mr1);
+                } else if (__any_sync(0xffffffffu, need)) {
+                    load_s();   // S is still in TMEM (P has not been written over it)
+                    exp_pass(m_use, false, mr0, mr1);
                 }
                 uint64_t acc[4];
 #pragma unroll
