@@ -396,9 +396,32 @@ int32_t sda_default_splits_gqa(int64_t n_batch, int32_t q_heads, int32_t kv_head
         }
         return best;
     }
-    // prefill rows on the tensor-core form: one split, which runs stream-K (persistent CTAs over
-    // the linear tile order, k2_prefill_tc.cu) -- full waves without partials for K3 to merge
-    if (head_dim == 128 && q_rows >= 64) return 1;
+    if (head_dim == 128 && q_rows >= 64) {
+        // prefill rows on the tensor-core form: one split runs stream-K (persistent groups of
+        // n_qpairs CTAs over the linear tile order, k2_prefill_tc.cu): ~tiles / CTA + ~8 tiles of
+        // segment fill / drain, x1.09 measured against the split grid's per-tile cost (static
+        // ranges wait for the slowest SM; C3 471 vs 482 us, 27 heads 419 vs 512 us) -- against
+        // the split grid's waves x (tiles per split + 4) + merge cost for S >= 2 (C5's prefill
+        // chunk, 1024 CTAs = 6.9 full waves at S = 2, stays on the split grid: 3.60 vs 3.86 ms)
+        const int64_t qpairs = (q_rows + 255) / 256;
+        const int64_t units = qpairs * q_heads * n_batch;
+        const int64_t tiles = (kv_cap + 127) / 128;
+        const int64_t sms = sda::device_sms();
+        const int64_t ctas = std::max<int64_t>(1, sms / qpairs) * qpairs;
+        const double sk = qpairs <= sms ? 1.09 * ((double)(units * tiles) / (double)ctas + 8.0) : 1e300;
+        const int64_t max_s = std::max<int64_t>(2, std::min<int64_t>(8, tiles / 4));
+        int32_t best = 1;
+        double best_cost = sk;
+        for (int64_t s2 = 2; s2 <= max_s; ++s2) {
+            const double waves = std::ceil((double)(units * s2) / (double)sms);
+            const double cost = waves * ((double)((tiles + s2 - 1) / s2) + 4.0) + (double)s2 * 0.022 * (double)units;
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                best = (int32_t)s2;
+            }
+        }
+        return best;
+    }
     return sda_default_splits(n_batch, q_heads, q_rows, kv_cap);
 }
 

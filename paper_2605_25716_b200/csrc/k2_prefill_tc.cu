@@ -109,7 +109,14 @@ constexpr int OFF_SEG = OFF_BAR + NBAR * 8 + 16;   // per softmax warp: segment 
 constexpr int SMEM = OFF_SEG + 8 * 128;
 // 12 warps = 3 warpgroups so registers can move between them (setmaxnreg): softmax warps 0-7
 // grow to 224, the TMA / MMA warpgroup (warps 8-9; 10-11 idle) shrinks to 56
+#ifndef SDA_K2_SETMAXNREG
+#define SDA_K2_SETMAXNREG 1
+#endif
+#if SDA_K2_SETMAXNREG
 constexpr int THREADS = 384;
+#else
+constexpr int THREADS = 320;
+#endif
 constexpr int kSoftmaxRegs = 224, kIssueRegs = 56;
 constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 384;
 // Exponentials per 4 pairs computed on the FMA pipe (tc::exp2_fma2) instead of MUFU.EX2. Measured
@@ -286,7 +293,7 @@ __device__ __forceinline__ void store_row16(float* dst, const uint32_t (&o)[16],
 __device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 }  // namespace k2tc
 
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(k2tc::THREADS, 1)
 k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                      const __grid_constant__ CUtensorMap vmap) {
     using namespace k2tc;
@@ -355,7 +362,9 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
     K2_CTA_STAMP(0);
 
     if (warp >= 8) {
+#if SDA_K2_SETMAXNREG
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kIssueRegs));
+#endif
       if (warp == 8) {
         // ------------------------------------------------------------------ TMA producer
         // K/V tiles run through the 2-stage rings continuously across segments (jj counts all
@@ -368,8 +377,16 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             int64_t jj = 0;
             int si = 0;
             Seg sg;
+            auto load_q = [&]() {
+                tc::mbar_arrive_expect_tx(q_full, (sg.two ? 2 : 1) * TILE_BYTES);
+                for (int g = 0; g < (sg.two ? 2 : 1); ++g)
+                    for (int kb = 0; kb < 2; ++kb)
+                        tc::tma_load_2d(smem + (g ? OFF_Q1 : OFF_Q0) + kb * BLK, &qmap, kb * 64, (int)(sg.head_row + g * TILE),
+                                        q_full);
+            };
             while (next_seg(sg)) {
                 if (sg.nkv == 0) continue;
+                if (si == 0) load_q();   // the first segment's Q ahead of its K/V (nothing to wait for)
                 const int64_t kvrow0 = (((int64_t)sg.b * p.kv_heads + sg.kvh) * p.kv_cap) + (int64_t)sg.t0 * TILE;
                 for (int64_t j = 0; j < sg.nkv; ++j, ++jj) {
                     const int st = (int)(jj & 1);
@@ -382,13 +399,9 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                     tc::mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
                     for (int kb = 0; kb < 2; ++kb)
                         tc::tma_load_2d(smem + OFF_V + st * TILE_BYTES + kb * BLK, &vmap, kb * 64, (int)(kvrow0 + j * TILE), &v_full[st]);
-                    if (j == 0) {
-                        if (si > 0) tc::mbar_wait(q_empty, (uint32_t)((si - 1) & 1));
-                        tc::mbar_arrive_expect_tx(q_full, (sg.two ? 2 : 1) * TILE_BYTES);
-                        for (int g = 0; g < (sg.two ? 2 : 1); ++g)
-                            for (int kb = 0; kb < 2; ++kb)
-                                tc::tma_load_2d(smem + (g ? OFF_Q1 : OFF_Q0) + kb * BLK, &qmap, kb * 64,
-                                                (int)(sg.head_row + g * TILE), q_full);
+                    if (j == 0 && si > 0) {   // later segments: once the previous one's MMAs release Q
+                        tc::mbar_wait(q_empty, (uint32_t)((si - 1) & 1));
+                        load_q();
                     }
                 }
                 ++si;
@@ -485,7 +498,9 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
         }
       }
     } else {
+#if SDA_K2_SETMAXNREG
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
+#endif
         // ------------------------------------------------------------------ softmax groups
         const int g = warp >> 2;                               // Q tile
         const int row = (warp & 3) * 32 + lane;                // TMEM lane = tile row

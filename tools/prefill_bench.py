@@ -1,6 +1,6 @@
 """Micro-benchmark of the tcgen05 prefill partial attention (K2) at BASELINE config 3 per GPU:
 2048-row prefill span x 16K-key scrambled shard x 32 heads x d128 (bf16), CUDA-event timed.
-  python tools/prefill_bench.py [Lq Lk H splits...]"""
+  [HKV=kv_heads] python tools/prefill_bench.py [Lq Lk H splits...]"""
 import os
 import sys
 
@@ -17,9 +17,10 @@ def main():
     splits = a[3:] or [1, 2, 3, 4, 6, 8]
     D = 128
     dev = torch.device("cuda")
+    HKV = int(os.environ.get("HKV", H))   # GQA: kv heads (default = H)
     q = torch.randn((1, H, Lq, D), device=dev).to(torch.bfloat16)
-    k = torch.randn((1, H, Lk, D), device=dev).to(torch.bfloat16)
-    v = torch.randn((1, H, Lk, D), device=dev).to(torch.bfloat16)
+    k = torch.randn((1, HKV, Lk, D), device=dev).to(torch.bfloat16)
+    v = torch.randn((1, HKV, Lk, D), device=dev).to(torch.bfloat16)
     flops = 4.0 * Lq * Lk * H * D
     for S in splits:
         ts = []
