@@ -186,6 +186,22 @@ sda_status sda_partial_attention(void* stream, const void* q, int32_t q_dtype,
                                  const int32_t* kv_len, int64_t n_batch, int32_t q_heads,
                                  int32_t kv_heads, int64_t q_rows, int32_t head_dim, int32_t n_splits,
                                  float* out_o, float* out_stats);
+/* Same, with a workspace for the stream-K form of the tensor-core prefill kernel (n_splits == 1,
+ * bf16, d 128, >= 64 query rows): persistent CTAs, one per SM, walk ranges of the key tiles and the
+ * pieces of a (request, head, 256-row) unit are merged in the kernel -- full waves without extra
+ * partials for K3. workspace: sda_prefill_workspace_bytes() bytes; its first
+ * 4 * n_batch * q_heads * ceil(q_rows / 256) bytes are per-unit tickets that must be zero before a
+ * launch -- every launch leaves them zero, so a buffer needs zeroing only when it is new or was last
+ * used for a larger shape's scratch; the rest is scratch. One workspace serves one launch at a time
+ * (e.g. one per stream). workspace == NULL or too small: the split grid, as sda_partial_attention. */
+sda_status sda_partial_attention_ws(void* stream, const void* q, int32_t q_dtype,
+                                    const void* k, const void* v, int32_t kv_dtype, int64_t kv_cap,
+                                    const int32_t* kv_len, int64_t n_batch, int32_t q_heads,
+                                    int32_t kv_heads, int64_t q_rows, int32_t head_dim, int32_t n_splits,
+                                    float* out_o, float* out_stats, void* workspace, size_t workspace_bytes);
+/* Workspace bytes sda_partial_attention_ws needs for this shape; 0 when it does not run stream-K. */
+size_t sda_prefill_workspace_bytes(int64_t n_batch, int32_t q_heads, int32_t kv_heads, int64_t q_rows,
+                                   int64_t kv_cap, int32_t head_dim, int32_t q_dtype, int32_t kv_dtype);
 /* The inquirer's own span is attended in plaintext with a causal mask (protocol.cpp:944-947,
  * AttentionMask::causal(offset), attention.hpp:25-27): key j is visible to query row i iff
  * j <= i + causal_offset. Same layouts and outputs as sda_partial_attention (SIMT kernel). */
@@ -287,12 +303,14 @@ sda_status sda_ll_partial_attention(void* stream, const void* ll_q, int32_t wire
  *   rec_peer[dest] + i * rec_stride floats (the inquirer's receive slot, peer memory); the CTA
  *   completing a destination raises *peer_flag[dest] = *epoch (system-scope release), which the
  *   inquirer's sda_exchange_wait consumes. Replaces K2 + split fold + sda_exchange_push on the
- *   return path. dest_counters: n_dest zeroed u32 (self-resetting). */
+ *   return path. dest_counters: n_dest zeroed u32 (self-resetting). workspace / workspace_bytes:
+ *   as sda_partial_attention_ws (stream-K; NULL -> the split grid). */
 sda_status sda_partial_attention_remote(void* stream, const void* q, int32_t q_dtype, const void* k, const void* v,
                                         int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int32_t n_dest,
                                         int64_t b_per, int32_t q_heads, int32_t kv_heads, int64_t q_rows,
                                         int32_t head_dim, float* const* rec_peer, int64_t rec_stride,
-                                        uint32_t* const* peer_flag, const uint32_t* epoch, uint32_t* dest_counters);
+                                        uint32_t* const* peer_flag, const uint32_t* epoch, uint32_t* dest_counters,
+                                        void* workspace, size_t workspace_bytes);
 /* sda_ll_unscramble_merge: K3 over this rank's record slots (n_domains * n_splits sources, each
  *   domain unscrambled with its phi_V^-1 from keys[(domain * B_p + b)]) into out [B_p][H][1][d];
  *   then *epoch += 1. done_counter: one zeroed u32 (self-resetting). */

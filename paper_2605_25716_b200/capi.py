@@ -34,7 +34,8 @@ EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_
            "sda_quantize_affine", "sda_dequantize", "sda_quant_roundtrip",
            "sda_frame_elements", "sda_frame_payload_bytes", "sda_frame_bytes", "sda_frame_scratch_bytes",
            "sda_frame_encode", "sda_frame_parse_header", "sda_frame_decode", "sda_crc32",
-           "sda_partial_attention_remote", "sda_scramble_batch_remote")
+           "sda_partial_attention_remote", "sda_scramble_batch_remote", "sda_partial_attention_ws",
+           "sda_prefill_workspace_bytes")
 
 
 class SdaError(RuntimeError):
@@ -107,6 +108,12 @@ def _load() -> ct.CDLL:
                                  ct.c_int64, ct.c_int64, ct.c_int64]
     lib.sda_partial_attention.argtypes = [_vp, _vp, ct.c_int32, _vp, _vp, ct.c_int32, ct.c_int64, _vp, ct.c_int64,
                                           ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int32, _vp, _vp]
+    lib.sda_partial_attention_ws.argtypes = [_vp, _vp, ct.c_int32, _vp, _vp, ct.c_int32, ct.c_int64, _vp, ct.c_int64,
+                                             ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int32, _vp, _vp, _vp,
+                                             ct.c_size_t]
+    lib.sda_prefill_workspace_bytes.restype = ct.c_size_t
+    lib.sda_prefill_workspace_bytes.argtypes = [ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32,
+                                                ct.c_int32, ct.c_int32]
     lib.sda_partial_attention_causal.argtypes = [_vp, _vp, ct.c_int32, _vp, _vp, ct.c_int32, ct.c_int64, _vp,
                                                  ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32,
                                                  ct.c_int32, ct.c_int64, _vp, _vp]
@@ -147,7 +154,7 @@ def _load() -> ct.CDLL:
     lib.sda_crc32.argtypes = [_vp, _vp, ct.c_uint64, _vp, _vp]
     lib.sda_partial_attention_remote.argtypes = [_vp, _vp, ct.c_int32, _vp, _vp, ct.c_int32, ct.c_int64, _vp,
                                                  ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32,
-                                                 _pp, ct.c_int64, _pp, _vp, _vp]
+                                                 _pp, ct.c_int64, _pp, _vp, _vp, _vp, ct.c_size_t]
     lib.sda_quantize_affine.argtypes = [_vp, _vp, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32, _vp, ct.c_int64,
                                         _vp, _vp, _vp, _vp]
     lib.sda_dequantize.argtypes = [_vp, _vp, ct.c_int64, _vp, _vp, ct.c_int64, ct.c_int64, ct.c_int32, _vp, ct.c_int32]

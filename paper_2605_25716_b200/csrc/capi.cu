@@ -425,10 +425,30 @@ int32_t sda_default_splits_gqa(int64_t n_batch, int32_t q_heads, int32_t kv_head
     return sda_default_splits(n_batch, q_heads, q_rows, kv_cap);
 }
 
+size_t sda_prefill_workspace_bytes(int64_t n_batch, int32_t q_heads, int32_t kv_heads, int64_t q_rows, int64_t kv_cap,
+                                   int32_t head_dim, int32_t q_dtype, int32_t kv_dtype) {
+    if (n_batch <= 0 || q_rows <= 0 || kv_cap <= 0 || q_heads <= 0 || kv_heads <= 0 || q_heads % kv_heads != 0)
+        return 0;
+    sda::K2Params p{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, kv_cap, n_batch, q_rows, q_heads, kv_heads, 1,
+                    0.f, 0, 0};
+    if (!sda::k2_prefill_tc_eligible(p, head_dim, q_dtype, kv_dtype) || sda::k2_gqa_tc_eligible(p, head_dim, q_dtype, kv_dtype))
+        return 0;
+    return sda::k2_prefill_sk_workspace_bytes(p);
+}
+
 sda_status sda_partial_attention(void* stream, const void* q, int32_t q_dtype, const void* k, const void* v,
                                  int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int64_t n_batch,
                                  int32_t q_heads, int32_t kv_heads, int64_t q_rows, int32_t head_dim,
                                  int32_t n_splits, float* out_o, float* out_stats) {
+    return sda_partial_attention_ws(stream, q, q_dtype, k, v, kv_dtype, kv_cap, kv_len, n_batch, q_heads, kv_heads, q_rows,
+                                    head_dim, n_splits, out_o, out_stats, nullptr, 0);
+}
+
+sda_status sda_partial_attention_ws(void* stream, const void* q, int32_t q_dtype, const void* k, const void* v,
+                                    int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int64_t n_batch,
+                                    int32_t q_heads, int32_t kv_heads, int64_t q_rows, int32_t head_dim,
+                                    int32_t n_splits, float* out_o, float* out_stats, void* workspace,
+                                    size_t workspace_bytes) {
     if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
     if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
     if (!q || !k || !v || !out_o || !out_stats || !valid_dtype(q_dtype) || !valid_dtype(kv_dtype))
@@ -440,6 +460,8 @@ sda_status sda_partial_attention(void* stream, const void* q, int32_t q_dtype, c
     if (n_batch == 0 || q_rows == 0) return SDA_OK;
     sda::K2Params p{q, k, v, kv_len, out_o, out_stats, kv_cap, n_batch, q_rows, q_heads, kv_heads, n_splits,
                     (float)(1.0 / std::sqrt((double)head_dim)), 0, 0};
+    p.sk_work = workspace;
+    p.sk_work_bytes = workspace ? workspace_bytes : 0;
     ++g_launches;
     if (sda::k2_gqa_tc_eligible(p, head_dim, q_dtype, kv_dtype) && !env_flag("SDA_K2_SIMT") &&
         !env_flag("SDA_K2_GROUPED"))
@@ -537,7 +559,8 @@ sda_status sda_partial_attention_remote(void* stream, const void* q, int32_t q_d
                                         int32_t kv_dtype, int64_t kv_cap, const int32_t* kv_len, int32_t n_dest,
                                         int64_t b_per, int32_t q_heads, int32_t kv_heads, int64_t q_rows,
                                         int32_t head_dim, float* const* rec_peer, int64_t rec_stride,
-                                        uint32_t* const* peer_flag, const uint32_t* epoch, uint32_t* dest_counters) {
+                                        uint32_t* const* peer_flag, const uint32_t* epoch, uint32_t* dest_counters,
+                                        void* workspace, size_t workspace_bytes) {
     if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
     if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
     if (!q || !k || !v || !rec_peer || !peer_flag || !epoch || !dest_counters || n_dest <= 0 ||
@@ -561,6 +584,8 @@ sda_status sda_partial_attention_remote(void* stream, const void* q, int32_t q_d
         p.peer_flag[i] = peer_flag[i];
     }
     p.dest_counters = dest_counters;
+    p.sk_work = workspace;
+    p.sk_work_bytes = workspace ? workspace_bytes : 0;
     ++g_launches;
     return from_cuda(sda::launch_k2_prefill_tc(p, static_cast<cudaStream_t>(stream)));
 }

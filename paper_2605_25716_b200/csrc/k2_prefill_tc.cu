@@ -23,8 +23,6 @@
 #include <cmath>
 #include <climits>
 #include <cstdlib>
-#include <mutex>
-#include <vector>
 
 #include "common.cuh"
 #include "tc_util.cuh"
@@ -53,9 +51,9 @@ struct K2TcParams {
     uint32_t* peer_flag[kMaxPeers];
     uint32_t* dest_counters;
     const uint32_t* epoch;
-    // stream-K mode (one split): persistent CTAs over the linear tile order, pieces of a unit
-    // merged by its last finisher through sk_buf (3 slots x 256 rows per CTA) and sk_tick
-    // (one zeroed, self-resetting u32 per unit)
+    // stream-K mode (one split, the caller's workspace): persistent CTAs over the linear tile
+    // order, pieces of a unit merged by its last finisher through sk_buf (3 slots x 256 rows per
+    // CTA) and sk_tick (one zeroed, self-resetting u32 per unit)
     int sk;
     float* sk_buf;
     uint32_t* sk_tick;
@@ -979,76 +977,34 @@ bool k2_prefill_tc_eligible(const K2Params& p, int d, int qdt, int kvdt) {
     return d == 128 && qdt == SDA_BF16 && kvdt == SDA_BF16 && (p.q_rows >= 64 || k2_grouped(p));
 }
 
-// Stream-K scratch, one per (device, stream): launches on one stream are ordered, so they can
-// share it; a stream being captured into a graph gets no new allocation (split mode instead).
+// Stream-K layout of the caller's workspace: one ticket per unit first (the only part that must
+// be zero; a launch leaves it zeroed), then 3 scratch slots per CTA from a 256-byte boundary.
 namespace {
-struct SkScratch {
-    int dev;
-    cudaStream_t st;
-    float* buf;
-    size_t buf_floats;
-    uint32_t* tick;
-    size_t n_tick;
-    uint64_t used;
+struct SkShape {
+    int64_t ctas;      // grid: groups x n_qpairs
+    int64_t units;
+    size_t tick_bytes;
+    size_t bytes;      // 0: this shape does not run stream-K
 };
-std::mutex g_sk_mu;
-std::vector<SkScratch> g_sk;
-uint64_t g_sk_clock = 0;
-constexpr size_t kSkMaxPerDevice = 8;
-
-bool sk_scratch(cudaStream_t st, size_t need_floats, size_t need_tick, float** buf, uint32_t** tick) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return false;
-    std::lock_guard<std::mutex> lk(g_sk_mu);
-    SkScratch* e = nullptr;
-    size_t on_dev = 0;
-    for (auto& x : g_sk)
-        if (x.dev == dev) {
-            ++on_dev;
-            if (x.st == st) e = &x;
-        }
-    if (e && e->buf_floats >= need_floats && e->n_tick >= need_tick) {
-        e->used = ++g_sk_clock;
-        *buf = e->buf;
-        *tick = e->tick;
-        return true;
-    }
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
-    if (!e && on_dev >= kSkMaxPerDevice) {   // evict the least recently used entry of this device
-        for (auto& x : g_sk)
-            if (x.dev == dev && (!e || x.used < e->used)) e = &x;
-    }
-    if (e) {   // grow or recycle: nothing may still read the old buffers
-        if (cudaDeviceSynchronize() != cudaSuccess) return false;
-        cudaFree(e->buf);
-        cudaFree(e->tick);
-    } else {
-        g_sk.push_back(SkScratch{dev, st, nullptr, 0, nullptr, 0, 0});
-        e = &g_sk.back();
-    }
-    e->st = st;
-    e->buf = nullptr;
-    e->tick = nullptr;
-    e->buf_floats = e->n_tick = 0;
-    if (cudaMalloc(&e->buf, need_floats * sizeof(float)) != cudaSuccess ||
-        cudaMalloc(&e->tick, need_tick * sizeof(uint32_t)) != cudaSuccess ||
-        cudaMemsetAsync(e->tick, 0, need_tick * sizeof(uint32_t), st) != cudaSuccess) {
-        cudaFree(e->buf);
-        cudaFree(e->tick);
-        e->buf = nullptr;
-        e->tick = nullptr;
-        cudaGetLastError();
-        return false;
-    }
-    e->buf_floats = need_floats;
-    e->n_tick = need_tick;
-    e->used = ++g_sk_clock;
-    *buf = e->buf;
-    *tick = e->tick;
-    return true;
+SkShape sk_shape(int64_t n_batch, int q_heads, int64_t q_rows, int64_t kv_cap) {
+    using namespace k2tc;
+    SkShape s{0, 0, 0, 0};
+    const int64_t sms = device_sms();
+    const int64_t nq = (q_rows + 2 * TILE - 1) / (2 * TILE);
+    s.units = n_batch * q_heads * nq;
+    const int64_t tiles_max = n_batch * q_heads * ((kv_cap + TILE - 1) / TILE);
+    if (nq > sms || tiles_max >= (int64_t)INT32_MAX || s.units >= (int64_t)INT32_MAX || s.units == 0) return s;
+    s.ctas = std::max<int64_t>(1, std::min<int64_t>(sms / nq, tiles_max)) * nq;
+    s.tick_bytes = ((size_t)s.units * sizeof(uint32_t) + 255) / 256 * 256;
+    s.bytes = s.tick_bytes + (size_t)s.ctas * 3 * (size_t)SK_SLOT * sizeof(float);
+    return s;
 }
 }  // namespace
+
+size_t k2_prefill_sk_workspace_bytes(const K2Params& q) {
+    if (k2_grouped(q)) return 0;
+    return sk_shape(q.n_batch, q.q_heads, q.q_rows, q.kv_cap).bytes;
+}
 
 cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
     using namespace k2tc;
@@ -1086,23 +1042,16 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
         !make_tmap_bf16_2d(&km, q.k, q.n_batch * q.kv_heads * q.kv_cap, D, TILE) ||
         !make_tmap_bf16_2d(&vm, q.v, q.n_batch * q.kv_heads * q.kv_cap, D, TILE))
         return cudaErrorInvalidValue;
-    // One split (not grouped): stream-K over a persistent grid of groups of n_qpairs CTAs, one
-    // CTA per SM, so the last wave is never partial (C3: 256 units on 148 SMs ran as 2 waves, the
-    // second 73 % full). Its tile count is bounded with every request at kv_cap.
-    const int64_t sms = device_sms();
-    const int64_t units = q.n_batch * q.q_heads * (int64_t)p.n_qpairs;
-    const int64_t tiles_max = q.n_batch * q.q_heads * ((q.kv_cap + TILE - 1) / TILE);
-    if (!p.grouped && q.n_splits == 1 && p.n_qpairs <= sms && tiles_max < (int64_t)INT32_MAX && units < (int64_t)INT32_MAX &&
-        !std::getenv("SDA_K2_NO_SK")) {
-        const int64_t NG = std::max<int64_t>(1, std::min<int64_t>(sms / p.n_qpairs, tiles_max));
-        const int64_t G = NG * p.n_qpairs;
-        float* buf = nullptr;
-        uint32_t* tick = nullptr;
-        if (sk_scratch(st, (size_t)G * 3 * (size_t)SK_SLOT, (size_t)std::max<int64_t>(1, units), &buf, &tick)) {
+    // One split (not grouped) with the caller's workspace: stream-K over a persistent grid of
+    // groups of n_qpairs CTAs, one CTA per SM, so the last wave is never partial (C3: 256 units
+    // on 148 SMs ran as 2 waves, the second 73 % full).
+    if (!p.grouped && q.n_splits == 1 && q.sk_work && !std::getenv("SDA_K2_NO_SK")) {
+        const SkShape sh = sk_shape(q.n_batch, q.q_heads, q.q_rows, q.kv_cap);
+        if (sh.bytes && q.sk_work_bytes >= sh.bytes) {
             p.sk = 1;
-            p.sk_buf = buf;
-            p.sk_tick = tick;
-            k2_prefill_tc_kernel<<<dim3((unsigned)G), THREADS, SMEM, st>>>(p, qm, km, vm);
+            p.sk_tick = static_cast<uint32_t*>(q.sk_work);
+            p.sk_buf = reinterpret_cast<float*>(static_cast<char*>(q.sk_work) + sh.tick_bytes);
+            k2_prefill_tc_kernel<<<dim3((unsigned)sh.ctas), THREADS, SMEM, st>>>(p, qm, km, vm);
             return cudaGetLastError();
         }
     }

@@ -76,6 +76,10 @@ struct K2Params {
     int64_t rec_stride;
     uint32_t* peer_flag[kMaxPeers];
     uint32_t* dest_counters;   // [n_dest] zeroed, self-resetting
+    // stream-K workspace of the tensor-core prefill form (one split): caller-owned, zeroed once,
+    // left zeroed by every launch; null -> split grid
+    void* sk_work;
+    size_t sk_work_bytes;
 };
 
 struct K3Source {
@@ -137,6 +141,8 @@ cudaError_t launch_k1_tc_multi(const K1Params* p, const int64_t* n_batch, int n_
 cudaError_t launch_k2_decode(const K2Params& p, int d, int qdt, int kvdt, cudaStream_t st);
 bool k2_prefill_tc_eligible(const K2Params& p, int d, int qdt, int kvdt);
 cudaError_t launch_k2_prefill_tc(const K2Params& p, cudaStream_t st);
+// bytes of the stream-K workspace for this shape (one split), 0 when it does not run stream-K
+size_t k2_prefill_sk_workspace_bytes(const K2Params& p);
 bool k2_gqa_tc_eligible(const K2Params& p, int d, int qdt, int kvdt);
 cudaError_t launch_k2_gqa_tc(const K2Params& p, cudaStream_t st);
 cudaError_t launch_k3(const K3Params& p, int d, int odt, cudaStream_t st);

@@ -339,12 +339,15 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
             return False
         import ctypes as ct
         L = capi.LIB
+        ws, ws_bytes = ops.prefill_workspace(B, Hq, shard.k.shape[1], Lq, shard.capacity, d, capi.SDA_BF16,
+                                             capi.SDA_BF16, q_all.device)
         capi.check(L.sda_partial_attention_remote(
             torch.cuda.current_stream().cuda_stream, q_all.data_ptr(), capi.SDA_BF16, shard.k.data_ptr(),
             shard.v.data_ptr(), capi.SDA_BF16, shard.capacity, shard.kv_len.data_ptr(), ex.world, B // ex.world, Hq,
             shard.k.shape[1], Lq, d, ct.cast(ex.r_args[1], ct.POINTER(ct.c_void_p)), Hq * Lq * (d + 2),
             ct.cast(ex.r_args[2], ct.POINTER(ct.c_void_p)), ex.epoch.data_ptr(),
-            ex.counters.data_ptr() + 4 * ex.world), "sda_partial_attention_remote")
+            ex.counters.data_ptr() + 4 * ex.world, 0 if ws is None else ws.data_ptr(), ws_bytes),
+            "sda_partial_attention_remote")
         return True
 
     def scramble_q_remote(q, ex):

@@ -128,10 +128,37 @@ def partial_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, kv_len:
         _cuda(kv_len, "kv_len")
         if kv_len.dtype != torch.int32:
             raise TypeError("kv_len must be int32")
-    check(capi.LIB.sda_partial_attention(_stream(stream), q.data_ptr(), _dtype_code(q), k.data_ptr(), v.data_ptr(),
-                                         _dtype_code(k), cap, _ptr(kv_len), B, Hq, Hkv, Lq, d, S,
-                                         out_o.data_ptr(), out_stats.data_ptr()), "sda_partial_attention")
+    ws, ws_bytes = (prefill_workspace(B, Hq, Hkv, Lq, cap, d, _dtype_code(q), _dtype_code(k), q.device, stream)
+                    if S == 1 else (None, 0))
+    check(capi.LIB.sda_partial_attention_ws(_stream(stream), q.data_ptr(), _dtype_code(q), k.data_ptr(), v.data_ptr(),
+                                            _dtype_code(k), cap, _ptr(kv_len), B, Hq, Hkv, Lq, d, S,
+                                            out_o.data_ptr(), out_stats.data_ptr(), _ptr(ws), ws_bytes),
+          "sda_partial_attention_ws")
     return out_o, out_stats
+
+
+_WORKSPACES = {}
+
+
+def prefill_workspace(B: int, Hq: int, Hkv: int, Lq: int, cap: int, d: int, q_code: int, kv_code: int,
+                      device: torch.device, stream=None):
+    """The stream-K workspace of sda_partial_attention_ws for this shape: one buffer per (device,
+    stream), grown on demand (launches on one stream are ordered). Its leading per-unit tickets
+    must be zero; every launch leaves them zero, so they are re-zeroed only when the shape changes
+    (another shape's scratch may lie there). Returns (tensor or None, bytes)."""
+    nbytes = int(capi.LIB.sda_prefill_workspace_bytes(B, Hq, Hkv, Lq, cap, d, q_code, kv_code))
+    if nbytes == 0:
+        return None, 0
+    st = _stream(stream)
+    key = (device.index if device.index is not None else torch.cuda.current_device(), st)
+    shape = (B, Hq, Lq, cap)
+    buf, last = _WORKSPACES.get(key, (None, None))
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+    elif last != shape:
+        buf[:4 * B * Hq * ((Lq + 255) // 256)].zero_()
+    _WORKSPACES[key] = (buf, shape)
+    return buf, nbytes
 
 
 def partial_attention_causal(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal_offset: int = 0,

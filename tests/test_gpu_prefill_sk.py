@@ -86,3 +86,34 @@ def test_prefill_sk_whole_units_bit_identical():
     a_o, a_s = _k2(q, k, v, [512])
     b_o, b_s = _k2(q, k, v, [512], sk=False)
     assert np.array_equal(a_o, b_o) and np.array_equal(a_s, b_s)
+
+
+def test_prefill_workspace_abi():
+    """The C ABI: sda_prefill_workspace_bytes sizes the stream-K workspace (0 for shapes that do not
+    run it); sda_partial_attention_ws with it, without it (split grid) and with a too-small one
+    (split grid) agree, and the workspace is left zeroed."""
+    from paper_2605_25716_b200 import capi
+    B, hq, hkv, lq, cap = 1, 4, 4, 512, 2048
+    n = int(capi.LIB.sda_prefill_workspace_bytes(B, hq, hkv, lq, cap, 128, capi.SDA_BF16, capi.SDA_BF16))
+    assert n > 0
+    assert capi.LIB.sda_prefill_workspace_bytes(B, hq, hkv, 1, cap, 128, capi.SDA_BF16, capi.SDA_BF16) == 0
+    assert capi.LIB.sda_prefill_workspace_bytes(B, hq, hkv, lq, cap, 64, capi.SDA_BF16, capi.SDA_BF16) == 0
+    q, k, v = (dev(x, torch.bfloat16) for x in _inputs(91, B, hq, hkv, lq, cap))
+    ws = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    outs = []
+    for w, nb in ((ws, n), (None, 0), (ws, n - 1)):
+        o = torch.empty((1, B, hq, lq, 128), dtype=torch.float32, device="cuda")
+        st = torch.empty((1, B, hq, lq, 2), dtype=torch.float32, device="cuda")
+        rc = capi.LIB.sda_partial_attention_ws(torch.cuda.current_stream().cuda_stream, q.data_ptr(), capi.SDA_BF16,
+                                               k.data_ptr(), v.data_ptr(), capi.SDA_BF16, cap, None, B, hq, hkv, lq,
+                                               128, 1, o.data_ptr(), st.data_ptr(),
+                                               None if w is None else w.data_ptr(), nb)
+        assert rc == 0
+        torch.cuda.synchronize()
+        outs.append((o.double().cpu().numpy(), st.double().cpu().numpy()))
+    # the scratch slots keep the last partials; the leading per-unit tickets must be back at zero
+    tick = ws[:4 * (B * hq * ((lq + 255) // 256))].view(torch.int32)
+    assert int(tick.abs().sum()) == 0
+    for o, st in outs[1:]:
+        assert max_abs_rel(outs[0][0], o) < 1e-2 and rel_fro(outs[0][0], o) < 5e-3
+        assert np.allclose(outs[0][1][..., 0], st[..., 0], atol=1e-5)
