@@ -89,7 +89,8 @@ struct K1TcShape {
     static constexpr int OFF_OUT = OFF_BLO + D * D * 2;      // output staging
     static constexpr int OFF_BAR = OFF_OUT + TILE_BYTES;
     static constexpr int NBAR = 2 * STAGES + 4 + 2;          // full, empty, tmem_full, tmem_empty, bfree, bready
-    static constexpr int SMEM = OFF_BAR + 8 * NBAR + 16;
+    static constexpr int OFF_KT = OFF_BAR + 8 * NBAR + 16;   // key tables of the B being built
+    static constexpr int SMEM = OFF_KT + D * (4 + 4 + 2 + 2);
     static constexpr uint32_t TMEM_COLS = 2 * D;
     static constexpr int THREADS = 288;
     static constexpr int LOADERS = 128;                      // warps 4-7
@@ -264,21 +265,37 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
                 const int64_t b = slab / H;
                 const uint8_t* sc = jb.keys + b * jb.keys_bstride + (int64_t)((slab % H) / G) * 64 * D +
                                     (int64_t)jb.which * 32 * D;
-                const float* fin = reinterpret_cast<const float*>(sc) + (jb.inv_t ? kInInvT : kInFwd) * D;
-                const float* fout = reinterpret_cast<const float*>(sc) + (jb.inv_t ? kOutInvT : kOutFwd) * D;
-                const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + 24 * D);
+                // the four tables (s_in, s_out, P1, P2^-1) into SMEM once, then B from SMEM: the
+                // 16 K-chunks per thread no longer wait on global loads
+                float* const kt_in = reinterpret_cast<float*>(smem + S::OFF_KT);
+                float* const kt_out = kt_in + D;
+                uint16_t* const kt_p1 = reinterpret_cast<uint16_t*>(kt_out + D);
+                uint16_t* const kt_p2 = kt_p1 + D;
+                {
+                    const float* fin_g = reinterpret_cast<const float*>(sc) + (jb.inv_t ? kInInvT : kInFwd) * D;
+                    const float* fout_g = reinterpret_cast<const float*>(sc) + (jb.inv_t ? kOutInvT : kOutFwd) * D;
+                    const uint16_t* utab_g = reinterpret_cast<const uint16_t*>(sc + 24 * D);
+                    for (int i = tid; i < D; i += 128) {
+                        kt_in[i] = fin_g[i];
+                        kt_out[i] = fout_g[i];
+                        kt_p1[i] = utab_g[kP1 * D + i];
+                        kt_p2[i] = utab_g[kP2Inv * D + i];
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                }
+                const float* fin = kt_in;
                 for (int e = tid; e < D * CPR; e += 128) {
                     const int n = e / CPR, c = e % CPR;   // B row n (output column), K chunk c
-                    const uint32_t pn = utab[kP2Inv * D + n];
-                    const float on = fout[n];
+                    const uint32_t pn = kt_p2[n];
+                    const float on = kt_out[n];
                     uint4 hv, lv;
                     uint32_t* hw = reinterpret_cast<uint32_t*>(&hv);
                     uint32_t* lw = reinterpret_cast<uint32_t*>(&lv);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         const int i0 = 8 * c + 2 * j, i1 = i0 + 1;
-                        const float v0 = ((__popc(utab[kP1 * D + i0] & pn) & 1) ? -fin[i0] : fin[i0]) * on;
-                        const float v1 = ((__popc(utab[kP1 * D + i1] & pn) & 1) ? -fin[i1] : fin[i1]) * on;
+                        const float v0 = ((__popc(kt_p1[i0] & pn) & 1) ? -fin[i0] : fin[i0]) * on;
+                        const float v1 = ((__popc(kt_p1[i1] & pn) & 1) ? -fin[i1] : fin[i1]) * on;
                         hw[j] = tc::pack_bf16(v0, v1);
                         float h0, h1;
                         bf16x2_to_f2(hw[j], h0, h1);
