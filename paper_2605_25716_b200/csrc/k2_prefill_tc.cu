@@ -375,16 +375,16 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             int64_t jj = 0;
             int si = 0;
             Seg sg;
-            auto load_q = [&]() {
-                tc::mbar_arrive_expect_tx(q_full, (sg.two ? 2 : 1) * TILE_BYTES);
-                for (int g = 0; g < (sg.two ? 2 : 1); ++g)
+            auto load_q = [&](const Seg& s) {
+                tc::mbar_arrive_expect_tx(q_full, (s.two ? 2 : 1) * TILE_BYTES);
+                for (int g = 0; g < (s.two ? 2 : 1); ++g)
                     for (int kb = 0; kb < 2; ++kb)
-                        tc::tma_load_2d(smem + (g ? OFF_Q1 : OFF_Q0) + kb * BLK, &qmap, kb * 64, (int)(sg.head_row + g * TILE),
+                        tc::tma_load_2d(smem + (g ? OFF_Q1 : OFF_Q0) + kb * BLK, &qmap, kb * 64, (int)(s.head_row + g * TILE),
                                         q_full);
             };
             while (next_seg(sg)) {
                 if (sg.nkv == 0) continue;
-                if (si == 0) load_q();   // the first segment's Q ahead of its K/V (nothing to wait for)
+                if (si == 0) load_q(sg);   // the first segment's Q ahead of its K/V (nothing to wait for)
                 const int64_t kvrow0 = (((int64_t)sg.b * p.kv_heads + sg.kvh) * p.kv_cap) + (int64_t)sg.t0 * TILE;
                 for (int64_t j = 0; j < sg.nkv; ++j, ++jj) {
                     const int st = (int)(jj & 1);
@@ -399,7 +399,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                         tc::tma_load_2d(smem + OFF_V + st * TILE_BYTES + kb * BLK, &vmap, kb * 64, (int)(kvrow0 + j * TILE), &v_full[st]);
                     if (j == 0 && si > 0) {   // later segments: once the previous one's MMAs release Q
                         tc::mbar_wait(q_empty, (uint32_t)((si - 1) & 1));
-                        load_q();
+                        load_q(sg);
                     }
                 }
                 ++si;

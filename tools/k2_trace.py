@@ -74,7 +74,10 @@ def main_sk():
           f"{np.median(end):.1f} max {end.max():.1f} us")
     nq = 8
     for g in range(n // nq):
-        print(f"group {g:2d}: end {end[g * nq:(g + 1) * nq].min():6.1f} .. {end[g * nq:(g + 1) * nq].max():6.1f}")
+        e = end[g * nq:(g + 1) * nq]
+        print(f"group {g:2d}: end {e.min():6.1f} .. {e.max():6.1f}  per pair: " + " ".join(f"{x:5.0f}" for x in e))
+    if os.environ.get("SMID"):
+        pass
 
 
 if __name__ == "__main__":
