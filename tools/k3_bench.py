@@ -49,6 +49,7 @@ def run(B, H, Lq, S, D=128, reps=20):
 
 if __name__ == "__main__":
     run(1, 32, 2048, 4)
+    run(1, 32, 2048, 1)
     run(16, 32, 1, 10)
     run(16, 32, 1, 4)
     run(2, 64, 2048, 2)
