@@ -97,12 +97,16 @@ constexpr int TILE = 128;
 constexpr int TILE_BYTES = TILE * D * 2;          // 32 KB bf16 tile
 constexpr int BLK = TILE * 128;                   // [128 x 64] swizzled block (16 KB)
 constexpr int OFF_Q0 = 0, OFF_Q1 = OFF_Q0 + TILE_BYTES;
-constexpr int OFF_K = OFF_Q1 + TILE_BYTES;        // 2 stages
-constexpr int OFF_V = OFF_K + 2 * TILE_BYTES;     // 2 stages
+#ifndef SDA_K2_KSTAGES
+#define SDA_K2_KSTAGES 2
+#endif
+constexpr int KST = SDA_K2_KSTAGES;               // K ring stages (V: 2)
+constexpr int OFF_K = OFF_Q1 + TILE_BYTES;
+constexpr int OFF_V = OFF_K + KST * TILE_BYTES;   // 2 stages
 constexpr int OFF_BAR = OFF_V + 2 * TILE_BYTES;
-// barriers: q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], o_final[2],
-// q_empty, o_empty[2]
-constexpr int NBAR = 18;
+// barriers: q_full, k_full[KST], k_empty[KST], v_full[2], v_empty[2], s_full[2], p_full[2],
+// o_final[2], q_empty, o_empty[2]
+constexpr int NBAR = 14 + 2 * KST;
 constexpr int OFF_SEG = OFF_BAR + NBAR * 8 + 16;   // per softmax warp: segment state (SoftKeep)
 constexpr int SMEM = OFF_SEG + 8 * 128;
 // 12 warps = 3 warpgroups so registers can move between them (setmaxnreg): softmax warps 0-7
@@ -299,14 +303,14 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
     uint64_t* const bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
     uint64_t* const q_full = bars;
     uint64_t* const k_full = bars + 1;
-    uint64_t* const k_empty = bars + 3;
-    uint64_t* const v_full = bars + 5;
-    uint64_t* const v_empty = bars + 7;
-    uint64_t* const s_full = bars + 9;
-    uint64_t* const p_full = bars + 11;
-    uint64_t* const o_final = bars + 13;
-    uint64_t* const q_empty = bars + 15;
-    uint64_t* const o_empty = bars + 16;
+    uint64_t* const k_empty = k_full + KST;
+    uint64_t* const v_full = k_empty + KST;
+    uint64_t* const v_empty = v_full + 2;
+    uint64_t* const s_full = v_empty + 2;
+    uint64_t* const p_full = s_full + 2;
+    uint64_t* const o_final = p_full + 2;
+    uint64_t* const q_empty = o_final + 2;
+    uint64_t* const o_empty = q_empty + 1;
     uint32_t* const tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
     uint32_t* const sk_ticket = tmem_slot + 1;
 
@@ -340,9 +344,11 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
     if (tid == 0) {
         tc::mbar_init(q_full, 1);
         tc::mbar_init(q_empty, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < KST; ++i) {
             tc::mbar_init(&k_full[i], 1);
             tc::mbar_init(&k_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&v_full[i], 1);
             tc::mbar_init(&v_empty[i], 1);
             tc::mbar_init(&s_full[i], 1);
@@ -389,10 +395,11 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 for (int64_t j = 0; j < sg.nkv; ++j, ++jj) {
                     const int st = (int)(jj & 1);
                     const uint32_t ph = (uint32_t)(((jj >> 1) - 1) & 1);
-                    if (jj >= 2) tc::mbar_wait(&k_empty[st], ph);
-                    tc::mbar_arrive_expect_tx(&k_full[st], TILE_BYTES);
+                    const int sk = (int)(jj % KST);
+                    if (jj >= KST) tc::mbar_wait(&k_empty[sk], (uint32_t)((jj / KST - 1) & 1));
+                    tc::mbar_arrive_expect_tx(&k_full[sk], TILE_BYTES);
                     for (int kb = 0; kb < 2; ++kb)
-                        tc::tma_load_2d(smem + OFF_K + st * TILE_BYTES + kb * BLK, &kmap, kb * 64, (int)(kvrow0 + j * TILE), &k_full[st]);
+                        tc::tma_load_2d(smem + OFF_K + sk * TILE_BYTES + kb * BLK, &kmap, kb * 64, (int)(kvrow0 + j * TILE), &k_full[sk]);
                     if (jj >= 2) tc::mbar_wait(&v_empty[st], ph);
                     tc::mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
                     for (int kb = 0; kb < 2; ++kb)
@@ -443,11 +450,11 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             if (sg.nkv == 0) continue;
             const bool two = sg.two;
             tc::mbar_wait(q_full, (uint32_t)(si & 1));
-            tc::mbar_wait(&k_full[jj & 1], (uint32_t)((jj >> 1) & 1));
+            tc::mbar_wait(&k_full[jj % KST], (uint32_t)((jj / KST) & 1));
             tc::tc_fence_after();
-            issue_s(0, (int)(jj & 1));
-            if (two) issue_s(1, (int)(jj & 1));
-            if (leader) tc::mma_commit(&k_empty[jj & 1]);
+            issue_s(0, (int)(jj % KST));
+            if (two) issue_s(1, (int)(jj % KST));
+            if (leader) tc::mma_commit(&k_empty[jj % KST]);
             for (int64_t j = 0; j < sg.nkv; ++j) {
                 const int64_t J = jj + j;
                 const int st = (int)(J & 1);
@@ -464,10 +471,10 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 issue_pv(0, st, j > 0);
                 if (!two && leader) tc::mma_commit(&v_empty[st]);
                 if (j + 1 == sg.nkv && leader) tc::mma_commit(&o_final[0]);
-                const int sn = (int)((J + 1) & 1);
+                const int sn = (int)((J + 1) % KST);
                 if (j + 1 < sg.nkv) {
                     K2_STAMP(9, J);
-                    tc::mbar_wait(&k_full[sn], (uint32_t)(((J + 1) >> 1) & 1));
+                    tc::mbar_wait(&k_full[sn], (uint32_t)(((J + 1) / KST) & 1));
                     K2_STAMP(10, J);
                     tc::tc_fence_after();
                     issue_s(0, sn);
