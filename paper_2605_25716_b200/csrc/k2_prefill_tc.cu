@@ -10,7 +10,7 @@
 // decode ("grouped" mode), the G q heads x L_q rows of one (request, kv head), so K/V stream
 // from HBM once per group instead of once per q head. With one split the CTAs are persistent
 // and walk ranges of key tiles instead (stream-K, below). 12 warps (10, 11 idle; setmaxnreg):
-//   warp 8      TMA producer: Q0/Q1 once, then K_j / V_j tiles (128 keys) into 2-stage rings
+//   warp 8      TMA producer: Q0/Q1 per segment, K_j / V_j tiles (128 keys) into rings
 //   warp 9      MMA issuer (one lane): S_g = Q_g K_j^T (SS, K-major) into TMEM, and
 //               O_g += P_g V_j with P_g read straight from TMEM (TS form; V as an MN-major B)
 //   warps 0-3   softmax for Q tile 0, warps 4-7 for Q tile 1 (thread = row = TMEM lane):

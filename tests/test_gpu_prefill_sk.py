@@ -117,3 +117,27 @@ def test_prefill_workspace_abi():
     for o, st in outs[1:]:
         assert max_abs_rel(outs[0][0], o) < 1e-2 and rel_fro(outs[0][0], o) < 5e-3
         assert np.allclose(outs[0][1][..., 0], st[..., 0], atol=1e-5)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_prefill_sk_random_shapes(seed):
+    """Seeded random shapes -- ragged and empty requests, GQA, partial Q tiles, units spread over
+    one to many CTA groups -- stream-K against the split-grid kernel on the same inputs."""
+    rng = np.random.default_rng(1000 + seed)
+    B = int(rng.integers(1, 4))
+    hkv = int(rng.choice([1, 2, 4]))
+    hq = hkv * int(rng.choice([1, 2, 4]))
+    lq = int(rng.choice([64, 100, 128, 200, 256, 300, 512, 777]))
+    cap = int(rng.choice([128, 640, 1000, 2048, 5000]))
+    kv_len = [int(x) for x in rng.integers(0, cap + 1, size=B)]
+    kv_len[int(rng.integers(0, B))] = cap
+    q, k, v = _inputs(2000 + seed, B, hq, hkv, lq, cap)
+    a_o, a_s = _k2(q, k, v, kv_len)
+    b_o, b_s = _k2(q, k, v, kv_len, sk=False)
+    for b in range(B):
+        if kv_len[b] == 0:
+            assert np.all(a_o[b] == 0) and np.all(a_s[b, ..., 1] == 0)
+            continue
+        assert max_abs_rel(a_o[b], b_o[b]) < 1e-2 and rel_fro(a_o[b], b_o[b]) < 5e-3, (b, B, hq, hkv, lq, cap, kv_len)
+        assert np.allclose(a_s[b, ..., 0], b_s[b, ..., 0], atol=1e-5)
+        assert np.allclose(a_s[b, ..., 1], b_s[b, ..., 1], rtol=5e-3)
