@@ -97,6 +97,14 @@ constexpr int TILE = 128;
 constexpr int TILE_BYTES = TILE * D * 2;          // 32 KB bf16 tile
 constexpr int BLK = TILE * 128;                   // [128 x 64] swizzled block (16 KB)
 constexpr int OFF_Q0 = 0, OFF_Q1 = OFF_Q0 + TILE_BYTES;
+// P handed to the MMA in parts: part i's PV issues while the softmax exponentiates part i+1
+// (C3: 1 part 476-480 us, 2 parts 460-467 us, 4 parts 531 us -- the extra waits and stores
+// cost more than the overlap gains)
+#ifndef SDA_K2_PPARTS
+#define SDA_K2_PPARTS 2
+#endif
+#define SDA_K2_PSPLIT (SDA_K2_PPARTS > 1)
+constexpr int kPParts = SDA_K2_PPARTS;
 #ifndef SDA_K2_KSTAGES
 #define SDA_K2_KSTAGES 2
 #endif
@@ -105,8 +113,8 @@ constexpr int OFF_K = OFF_Q1 + TILE_BYTES;
 constexpr int OFF_V = OFF_K + KST * TILE_BYTES;   // 2 stages
 constexpr int OFF_BAR = OFF_V + 2 * TILE_BYTES;
 // barriers: q_full, k_full[KST], k_empty[KST], v_full[2], v_empty[2], s_full[2], p_full[2],
-// o_final[2], q_empty, o_empty[2]
-constexpr int NBAR = 14 + 2 * KST;
+// o_final[2], q_empty, o_empty[2], p_part[2][kPParts - 1]
+constexpr int NBAR = 14 + 2 * KST + 2 * (SDA_K2_PPARTS > 1 ? SDA_K2_PPARTS - 1 : 0);
 constexpr int OFF_SEG = OFF_BAR + NBAR * 8 + 16;   // per softmax warp: segment state (SoftKeep)
 constexpr int SMEM = OFF_SEG + 8 * 128;
 // 12 warps = 3 warpgroups so registers can move between them (setmaxnreg): softmax warps 0-7
@@ -311,6 +319,10 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
     uint64_t* const o_final = p_full + 2;
     uint64_t* const q_empty = o_final + 2;
     uint64_t* const o_empty = q_empty + 1;
+    // PSPLIT: part i (< kPParts - 1) of tile g's P is in TMEM -- one barrier per part, so each
+    // completes once per tile (a barrier completing several phases ahead of its waiter would
+    // leave the waiter's parity ambiguous)
+    uint64_t* const p_part = o_empty + 2;
     uint32_t* const tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
     uint32_t* const sk_ticket = tmem_slot + 1;
 
@@ -353,6 +365,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             tc::mbar_init(&v_empty[i], 1);
             tc::mbar_init(&s_full[i], 1);
             tc::mbar_init(&p_full[i], 128);
+            for (int part = 0; part + 1 < kPParts; ++part) tc::mbar_init(&p_part[i * (kPParts - 1) + part], 128);
             tc::mbar_init(&o_final[i], 1);
             tc::mbar_init(&o_empty[i], 128);
         }
@@ -432,15 +445,35 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             }
             if (leader) tc::mma_commit(&s_full[g]);
         };
-        auto issue_pv = [&](int g, int st, bool acc) {
+        auto issue_pv = [&](int g, int st, bool acc, int k0, int k1) {
             const uint32_t vb = vbase + st * TILE_BYTES;
             const uint32_t d_tmem = tmem + (g ? COL_O1 : COL_O0);
             const uint32_t p_tmem = tmem + (g ? COL_S1 : COL_S0);
 #pragma unroll
-            for (int k = 0; k < TILE / 16; ++k) {   // 16 keys per step: P columns 8k.., V rows 16k..
+            for (int k = k0; k < k1; ++k) {   // 16 keys per step: P columns 8k.., V rows 16k..
                 const uint64_t db = tc::sw128_desc(vb + k * 2048, BLK, 1024);
                 if (leader) tc::mma_bf16_ts(d_tmem, p_tmem + k * 8, db, IDESC_O, (acc || k > 0) ? 1u : 0u);
             }
+        };
+        // PV of tile g: with PSPLIT the first 64 keys go as soon as their P is in TMEM
+        auto pv = [&](int g, int st, bool acc, uint32_t n) {   // n: P tiles of Q tile g so far
+            const uint32_t ph = n & 1;
+#if SDA_K2_PSPLIT
+            constexpr int KPP = TILE / 16 / kPParts;   // PV k-steps per part
+#pragma unroll
+            for (int part = 0; part + 1 < kPParts; ++part) {   // one barrier per part
+                K2_WAIT_P(&p_part[g * (kPParts - 1) + part], ph);
+                tc::tc_fence_after();
+                issue_pv(g, st, acc, part * KPP, (part + 1) * KPP);
+            }
+            K2_WAIT_P(&p_full[g], ph);
+            tc::tc_fence_after();
+            issue_pv(g, st, true, (kPParts - 1) * KPP, TILE / 16);
+#else
+            K2_WAIT_P(&p_full[g], ph);
+            tc::tc_fence_after();
+            issue_pv(g, st, acc, 0, TILE / 16);
+#endif
         };
         int64_t jj = 0;
         int si = 0;
@@ -462,13 +495,11 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 K2_STAMP(6, J);
                 tc::mbar_wait(&v_full[st], ph);
                 K2_STAMP(7, J);
-                K2_WAIT_P(&p_full[0], pc[0] & 1);
-                ++pc[0];
                 // O0 is reused from the previous segment once its epilogue has read it
                 if (j == 0 && ou[0] > 0) tc::mbar_wait(&o_empty[0], (ou[0] - 1) & 1);
-                tc::tc_fence_after();
                 K2_STAMP(4, J);
-                issue_pv(0, st, j > 0);
+                pv(0, st, j > 0, pc[0]);
+                ++pc[0];
                 if (!two && leader) tc::mma_commit(&v_empty[st]);
                 if (j + 1 == sg.nkv && leader) tc::mma_commit(&o_final[0]);
                 const int sn = (int)((J + 1) % KST);
@@ -482,12 +513,10 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 }
                 if (!two) continue;
                 K2_STAMP(8, J);
-                K2_WAIT_P(&p_full[1], pc[1] & 1);
-                ++pc[1];
                 if (j == 0 && ou[1] > 0) tc::mbar_wait(&o_empty[1], (ou[1] - 1) & 1);
-                tc::tc_fence_after();
                 K2_STAMP(5, J);
-                issue_pv(1, st, j > 0);
+                pv(1, st, j > 0, pc[1]);
+                ++pc[1];
                 if (leader) tc::mma_commit(&v_empty[st]);
                 if (j + 1 == sg.nkv && leader) tc::mma_commit(&o_final[1]);
                 if (j + 1 < sg.nkv) {
@@ -555,6 +584,9 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 if ((warp & 3) == 0 && lane == 0) K2_STAMP(g, j);
                 if (!warp_live) {
                     tc::tc_fence_before();
+#if SDA_K2_PSPLIT
+                    for (int part = 0; part + 1 < kPParts; ++part) tc::mbar_arrive(&p_part[g * (kPParts - 1) + part]);
+#endif
                     tc::mbar_arrive(&p_full[g]);
                     continue;
                 }
@@ -573,10 +605,10 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 // p = exp2(s * scale - mu) in place (one packed FFMA2 per two logits), all 128 first:
                 // the MUFU ops issue back to back instead of each waiting on its consumer. With
                 // `with_max` the row max of the raw logits is taken in the same pass.
-                auto exp_pass = [&](float mu, bool with_max, float& mr0, float& mr1) {
+                auto exp_range = [&](float mu, bool with_max, float& mr0, float& mr1, int i0, int i1) {
                     const uint64_t sc2 = tc::f2(p.scale_log2, p.scale_log2), nmu2 = tc::f2(-mu, -mu);
 #pragma unroll
-                    for (int i = 0; i < 64; ++i) {
+                    for (int i = i0; i < i1; ++i) {
                         const float r0 = __uint_as_float(s[2 * i]), r1 = __uint_as_float(s[2 * i + 1]);
                         if (with_max) {
                             if (i & 1) mr1 = tc::fmax3(mr1, r0, r1);
@@ -595,6 +627,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                         s[2 * i + 1] = __float_as_uint(p1);
                     }
                 };
+                auto exp_pass = [&](float mu, bool with_max, float& mr0, float& mr1) { exp_range(mu, with_max, mr0, mr1, 0, 64); };
                 load_s();
                 float mr0 = -INFINITY, mr1 = -INFINITY;
 #if SDA_K2_SPEC
@@ -640,7 +673,29 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                     if (m_use > -INFINITY) l *= ex2(m_use - m_new);
                     m_use = m_new;
                 }
-                if (!spec) {
+                const bool psplit = SDA_K2_PSPLIT && !spec;
+                if (psplit) {
+                    // every part but the last: its P into TMEM and announced before the next
+                    // part's exponentials, so its PV overlaps the rest of the softmax
+                    const float mu = (m_use == -INFINITY) ? 0.f : m_use;
+                    constexpr int PP = 64 / kPParts;   // logit pairs per part
+#pragma unroll
+                    for (int part = 0; part < kPParts; ++part) {
+                        exp_range(mu, false, mr0, mr1, part * PP, (part + 1) * PP);
+                        if (part + 1 == kPParts) break;
+#pragma unroll
+                        for (int c = part * PP / 8; c < (part + 1) * PP / 8; ++c) {
+                            uint32_t pk[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e)
+                                pk[e] = tc::pack_bf16(__uint_as_float(s[16 * c + 2 * e]), __uint_as_float(s[16 * c + 2 * e + 1]));
+                            tc::tmem_st8(s_col + c * 8, pk);
+                        }
+                        tc::tmem_st_wait();
+                        tc::tc_fence_before();
+                        tc::mbar_arrive(&p_part[g * (kPParts - 1) + part]);
+                    }
+                } else if (!spec) {
                     exp_pass((m_use == -INFINITY) ? 0.f : m_use, false, mr0, mr1);
                 } else if (__any_sync(0xffffffffu, need)) {
                     load_s();   // S is still in TMEM (P has not been written over it)
@@ -654,6 +709,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 // after the arrive: the FADD2 chains leave the softmax -> PV -> S chain
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
+                    if (psplit && c < (kPParts - 1) * 8 / kPParts) continue;   // already in TMEM
                     uint32_t pk[8];
 #pragma unroll
                     for (int e = 0; e < 8; ++e)
@@ -663,6 +719,10 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 tc::tmem_st_wait();
                 tc::tc_fence_before();
                 if ((warp & 3) == 0 && lane == 0) K2_STAMP(2 + g, j);
+#if SDA_K2_PSPLIT
+                if (!psplit)   // (speculative path: whole P at once)
+                    for (int part = 0; part + 1 < kPParts; ++part) tc::mbar_arrive(&p_part[g * (kPParts - 1) + part]);
+#endif
                 tc::mbar_arrive(&p_full[g]);
 #pragma unroll
                 for (int i = 0; i < 64; ++i)
