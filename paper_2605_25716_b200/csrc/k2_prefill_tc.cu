@@ -55,6 +55,7 @@ struct K2TcParams {
     // order, pieces of a unit merged by its last finisher through sk_buf (3 slots x 256 rows per
     // CTA) and sk_tick (one zeroed, self-resetting u32 per unit)
     int sk;
+    int sk_gq;             // CTAs per group (Q-tile pairs walked in lockstep); divides n_qpairs
     float* sk_buf;
     uint32_t* sk_tick;
 };
@@ -218,10 +219,11 @@ __device__ __forceinline__ void sk_init(const K2TcParams& p, int T, int NG, int 
     k.pos = k.lo;
     k.acc = k.b = k.nt = k.head = k.off = 0;
     if (k.pos >= k.hi) return;
+    const int nhs = p.q_heads * (p.n_qpairs / p.sk_gq);   // (head, pair-subset) sequences per request
     for (;; ++k.b) {
         k.nt = ntile_of(p, k.b);
-        if (k.pos < k.acc + p.q_heads * k.nt) break;
-        k.acc += p.q_heads * k.nt;
+        if (k.pos < k.acc + nhs * k.nt) break;
+        k.acc += nhs * k.nt;
     }
     k.head = (k.pos - k.acc) / k.nt;
     k.off = (k.pos - k.acc) % k.nt;
@@ -229,11 +231,13 @@ __device__ __forceinline__ void sk_init(const K2TcParams& p, int T, int NG, int 
 
 __device__ __forceinline__ bool sk_next(const K2TcParams& p, int qp, SkCursor& k, Seg& s) {
     if (k.pos >= k.hi) return false;
-    fill_unit(p, k.b, k.head, qp, s);
+    const int nsub = p.n_qpairs / p.sk_gq, nhs = p.q_heads * nsub;
+    const int head = k.head / nsub, qpair = (k.head % nsub) * p.sk_gq + qp;
+    fill_unit(p, k.b, head, qpair, s);
     s.t0 = k.off;
     s.nkv = min(k.nt - k.off, k.hi - k.pos);
     s.split = 0;
-    s.unit = (k.b * p.q_heads + k.head) * p.n_qpairs + qp;
+    s.unit = (k.b * p.q_heads + head) * p.n_qpairs + qpair;
     s.ub = k.acc + k.head * k.nt;
     s.nt = k.nt;
     s.first = k.pos == k.lo;
@@ -241,9 +245,9 @@ __device__ __forceinline__ bool sk_next(const K2TcParams& p, int qp, SkCursor& k
     k.off += s.nkv;
     if (k.off == k.nt) {
         k.off = 0;
-        if (++k.head == p.q_heads) {
+        if (++k.head == nhs) {
             k.head = 0;
-            k.acc += p.q_heads * k.nt;
+            k.acc += nhs * k.nt;
             ++k.b;
             while (k.pos < k.hi && (k.nt = ntile_of(p, k.b)) == 0) ++k.b;   // requests with no keys
         }
@@ -332,14 +336,14 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
     //   grouped: blockIdx.y = kv head; the tile rows are its G q heads x Lq rows
     // stream-K mode (p.sk) -- a persistent CTA per SM walking its range of the linear tile order.
     int T_sk = 0, NG = 1;
-    const int nq = p.n_qpairs;
-    const int grp = (int)blockIdx.x / nq, qp_sk = (int)blockIdx.x % nq;
+    const int gq = p.sk ? p.sk_gq : 1;   // stream-K: CTAs per group
+    const int grp = (int)blockIdx.x / gq, qp_sk = (int)blockIdx.x % gq;
     if (p.sk) {
         for (int64_t b = 0; b < p.n_batch; ++b) T_sk += ntile_of(p, b);
-        T_sk *= p.q_heads;
+        T_sk *= p.q_heads * (p.n_qpairs / gq);
         // groups that take part in the range split: every range then holds >= 1 tile (ragged
         // kv_len can leave fewer tiles than groups; the other CTAs only serve empty requests)
-        NG = max(1, min((int)gridDim.x / nq, T_sk));
+        NG = max(1, min((int)gridDim.x / gq, T_sk));
     }
     // the CTA's segments, the same sequence in every warp role
     SkCursor cur;
@@ -558,7 +562,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             }
             SoftKeep* const k = opaque(keep);
             SkCursor c = k->cur;
-            const bool ok = sk_next(p, (int)blockIdx.x % p.n_qpairs, c, sg);
+            const bool ok = sk_next(p, (int)blockIdx.x % p.sk_gq, c, sg);
             __syncwarp();
             if (lane == 0) k->cur = c;
             __syncwarp();
@@ -763,7 +767,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 // stream-K: a unit held whole by this CTA is written straight from TMEM (as in split
                 // mode); a piece goes to this CTA's scratch slot, and the last of the unit's pieces
                 // to finish merges them into the output
-                const int T_sk = kk->T, NG = kk->NG, nq = p.n_qpairs, qp_sk = (int)blockIdx.x % nq;
+                const int T_sk = kk->T, NG = kk->NG, gq = p.sk_gq, qp_sk = (int)blockIdx.x % gq;
                 const int g_a = sk_group_of(sg.ub, T_sk, NG);
                 const int P = 1 + sk_group_of(sg.ub + sg.nt - 1, T_sk, NG) - g_a;   // pieces of the unit
                 float* out_o = p.out_o;
@@ -825,7 +829,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                         __threadfence();
                         auto piece = [&](int k) -> const float* {
                             const int gk = g_a + k;
-                            return sk_slot(p, gk * nq + qp_sk, sk_lo(T_sk, NG, gk) < sg.ub ? 1 : 0);
+                            return sk_slot(p, gk * gq + qp_sk, sk_lo(T_sk, NG, gk) < sg.ub ? 1 : 0);
                         };
                         const int r_l = warp * 32 + lane;
                         const bool live_l = r_l < sg.nrows;
@@ -902,7 +906,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                         if (P > 1) p.sk_tick[sg.unit] = 0u;   // self-resetting for the next launch
                         if (p.remote) {   // the unit completing a destination's records raises its flag
                             const int64_t dest = sg.b / p.b_per;
-                            const unsigned per_dest = (unsigned)((int64_t)p.q_heads * nq * p.b_per);
+                            const unsigned per_dest = (unsigned)((int64_t)p.q_heads * p.n_qpairs * p.b_per);
                             if (atomicAdd(&p.dest_counters[dest], 1u) == per_dest - 1) {
                                 p.dest_counters[dest] = 0;
                                 __threadfence_system();
@@ -977,6 +981,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
         if (p.sk) {
             // requests with no keys contribute no tiles: their units (zero O', stats (-inf, 0)) go
             // round-robin over the CTAs
+            const int nq = p.n_qpairs;
             const int64_t upr = (int64_t)p.q_heads * nq;
             for (int64_t b = 0; b < p.n_batch; ++b) {
                 if (ntile_of(p, b) != 0) continue;
@@ -1048,20 +1053,37 @@ bool k2_prefill_tc_eligible(const K2Params& p, int d, int qdt, int kvdt) {
 // be zero; a launch leaves it zeroed), then 3 scratch slots per CTA from a 256-byte boundary.
 namespace {
 struct SkShape {
-    int64_t ctas;      // grid: groups x n_qpairs
+    int64_t gq;        // CTAs per group
+    int64_t ctas;      // grid: groups x gq
     int64_t units;
     size_t tick_bytes;
     size_t bytes;      // 0: this shape does not run stream-K
 };
 SkShape sk_shape(int64_t n_batch, int q_heads, int64_t q_rows, int64_t kv_cap) {
     using namespace k2tc;
-    SkShape s{0, 0, 0, 0};
+    SkShape s{1, 0, 0, 0, 0};
     const int64_t sms = device_sms();
     const int64_t nq = (q_rows + 2 * TILE - 1) / (2 * TILE);
     s.units = n_batch * q_heads * nq;
     const int64_t tiles_max = n_batch * q_heads * ((kv_cap + TILE - 1) / TILE);
     if (nq > sms || tiles_max >= (int64_t)INT32_MAX || s.units >= (int64_t)INT32_MAX || s.units == 0) return s;
-    s.ctas = std::max<int64_t>(1, std::min<int64_t>(sms / nq, tiles_max)) * nq;
+    // CTAs per group: among the divisors of n_qpairs of at least min(4, n_qpairs) -- smaller
+    // groups share each K/V tile between too few CTAs (C3: groups of 2, 482 us) -- the one that
+    // leaves the fewest SMs idle, ties to the larger (C3: 37 groups of 4 = 148 SMs, 467 us,
+    // against 18 groups of 8 = 144 SMs, 469-472 us)
+    s.gq = nq;
+    for (int64_t d = std::min<int64_t>(4, nq); d <= nq; ++d)
+        if (nq % d == 0 && (sms / d) * d > (sms / s.gq) * s.gq) s.gq = d;
+    if (const char* e = std::getenv("SDA_K2_SK_GQ")) {   // experiment override (must divide n_qpairs)
+        const int64_t d = std::atoll(e);
+        if (d >= 1 && d <= nq && nq % d == 0) s.gq = d;
+    }
+    const int64_t tiles_sub = tiles_max * (nq / s.gq);
+    if (tiles_sub >= (int64_t)INT32_MAX) {
+        s.bytes = 0;
+        return s;
+    }
+    s.ctas = std::max<int64_t>(1, std::min<int64_t>(sms / s.gq, tiles_sub)) * s.gq;
     s.tick_bytes = ((size_t)s.units * sizeof(uint32_t) + 255) / 256 * 256;
     s.bytes = s.tick_bytes + (size_t)s.ctas * 3 * (size_t)SK_SLOT * sizeof(float);
     return s;
@@ -1102,6 +1124,7 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
     p.dest_counters = q.dest_counters;
     p.epoch = q.epoch;
     p.sk = 0;
+    p.sk_gq = 1;
     p.sk_buf = nullptr;
     p.sk_tick = nullptr;
     CUtensorMap qm, km, vm;
@@ -1116,6 +1139,7 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
         const SkShape sh = sk_shape(q.n_batch, q.q_heads, q.q_rows, q.kv_cap);
         if (sh.bytes && q.sk_work_bytes >= sh.bytes) {
             p.sk = 1;
+            p.sk_gq = (int)sh.gq;
             p.sk_tick = static_cast<uint32_t*>(q.sk_work);
             p.sk_buf = reinterpret_cast<float*>(static_cast<char*>(q.sk_work) + sh.tick_bytes);
             k2_prefill_tc_kernel<<<dim3((unsigned)sh.ctas), THREADS, SMEM, st>>>(p, qm, km, vm);
