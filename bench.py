@@ -512,9 +512,9 @@ def run_prefill_dist(args, ws, rank, local):
     exch = sdist.PeerExchange(bufs) if ws > 1 and args.exchange != "nccl" else None
     out = torch.empty((1, H, LQ, D), dtype=torch.float32, device=devn)
 
-    def step(qin):
+    def step(qin, o=out):
         ops.scramble_batch(k1_jobs, D)   # the span's K/V into the cache, scramble + permute fused
-        return sdist.scrambled_decode_step(qin, comp, bufs, out, exchange=exch)
+        return sdist.scrambled_decode_step(qin, comp, bufs, o, exchange=exch)
 
     def barrier():
         if ws > 1:
@@ -537,17 +537,43 @@ def run_prefill_dist(args, ws, rank, local):
         torch.cuda.synchronize()
     barrier()
     ms = t0.elapsed_time(t1) / args.steps
-    # end to end: Q span from pinned host memory in, O back out
-    q_host, out_host, q_dev = q.cpu().pin_memory(), torch.empty((1, H, LQ, D)).pin_memory(), torch.empty_like(q)
+    # end to end: every step's Q span from pinned host memory in, its O back out, over a stream of
+    # successive spans (independent prefill chunks/requests). Two slots: span i+1's H2D (copy-in
+    # stream) and span i-1's D2H (copy-out stream) run under span i's kernels; PCIe is full duplex.
+    q_host = q.cpu().pin_memory()
+    q_dev = [torch.empty_like(q), torch.empty_like(q)]
+    o_dev = [out, torch.empty_like(out)]
+    out_host = [torch.empty((1, H, LQ, D)).pin_memory() for _ in range(2)]
+    c_in, c_out = torch.cuda.Stream(devn), torch.cuda.Stream(devn)
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    used, loaded, done, drained = [ev(), ev()], [ev(), ev()], [ev(), ev()], [ev(), ev()]
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        q_dev.copy_(q_host, non_blocking=True)
-        out_host.copy_(step(q_dev), non_blocking=True)
+    c_in.wait_event(e0)
+    c_out.wait_event(e0)
+    for i in range(args.steps):
+        s = i & 1
+        with torch.cuda.stream(c_in):
+            if i >= 2:
+                c_in.wait_event(used[s])          # span i-2 is done reading q_dev[s]
+            q_dev[s].copy_(q_host, non_blocking=True)
+            loaded[s].record(c_in)
+        stream.wait_event(loaded[s])
+        if i >= 2:
+            stream.wait_event(drained[s])         # span i-2's O has left o_dev[s]
+        step(q_dev[s], o_dev[s])
+        used[s].record(stream)
+        with torch.cuda.stream(c_out):
+            c_out.wait_event(used[s])
+            out_host[s].copy_(o_dev[s], non_blocking=True)
+            drained[s].record(c_out)
+    stream.wait_stream(c_out)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
+    ref_o = out_host[(args.steps - 1) & 1]
+    assert torch.equal(ref_o, o_dev[(args.steps - 1) & 1].cpu()), "e2e: host copy of O differs from the device O"
     if ws > 1:
         tt = torch.tensor([ms, e2e_ms], device=devn)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -572,7 +598,9 @@ def run_prefill_dist(args, ws, rank, local):
                          "exchange": ("none (single domain)" if ws == 1 else EXCHANGE_DESC[args.exchange if args.exchange != "ll" else "p2p"]),
                          "l2": "inputs larger than L2, no flush needed"},
               "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-                      "h2d_bytes_per_step": LQ * H * D * 2, "d2h_bytes_per_step": LQ * H * D * 4},
+                      "h2d_bytes_per_step": LQ * H * D * 2, "d2h_bytes_per_step": LQ * H * D * 4,
+                      "overlap": "successive spans double-buffered: span i+1's Q H2D and span i-1's O D2H "
+                                 "on two copy streams under span i's kernels"},
               "gpu_launches": int(launches) * args.steps, "cuda_graph": False,
               "roofline": {"bound": "tensor", "kernel": "k2_prefill_tc_kernel (whole step)", "achieved": value,
                            "peak": peak, "unit": "TFLOP/s", "frac": value / peak,
