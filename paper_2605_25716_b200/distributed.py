@@ -186,6 +186,7 @@ class LLDecode:
         self.shard = shard
         self.S = n_splits or capi.default_splits(W * b_per, q_heads, 1, shard.capacity, kv_heads=shard.k.shape[1],
                                                  head_dim=head_dim)
+        self.S = max(1, min(self.S, capi.MAX_SOURCES // W))   # K3 merges W x S split records
         self.wire = ops._DT[wire_dtype]
         q_slot = b_per * q_heads * head_dim * (4 if wire_dtype == torch.bfloat16 else 8)
         r_slot = self.S * b_per * q_heads * (head_dim + 2) * 8
