@@ -37,6 +37,16 @@ def _cuda(t: torch.Tensor, name: str) -> torch.Tensor:
     return t
 
 
+def _cuda_or_pinned(t: torch.Tensor, name: str) -> torch.Tensor:
+    """A CUDA tensor, or a pinned host tensor read/written in place by the kernel over PCIe
+    (zero-copy: pinned allocations are device-addressable under UVA)."""
+    if not t.is_cuda and not t.is_pinned():
+        raise ValueError(f"{name} must be a CUDA tensor or pinned host memory")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
 def _stream(stream: Optional[torch.cuda.Stream]) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
@@ -68,8 +78,9 @@ def scramble(x: torch.Tensor, keys: torch.Tensor, variant: int, which: int, perm
     keys: uint8 [B, keyset_bytes] (request b's key set in row b); perm: int32/u32 [B, rows] or None.
     n_batch > B scrambles x once per stacked key set: request b reads x[b % B] (one query batch
     for several destination domains in one launch).
+    x may be pinned host memory (zero-copy read).
     """
-    _cuda(x, "x")
+    _cuda_or_pinned(x, "x")
     Bx, H, rows, d = x.shape
     B = n_batch or Bx
     kh = key_heads if key_heads is not None else H
@@ -223,6 +234,7 @@ def unscramble_merge(sources: Sequence[MergeSource], out: Optional[torch.Tensor]
             pstride = s.pq_inv.stride(0) if s.pq_inv.dim() > 1 else 0
     if out is None:
         out = torch.empty((B, Hq, Lq, d), dtype=out_dtype, device=sources[0].o.device)
+    _cuda_or_pinned(out, "out")   # pinned host memory: O stored straight to the host (zero-copy)
     check(capi.LIB.sda_unscramble_merge(_stream(stream), arr, n, kstride, key_heads or Hq, pstride, B, Hq, Lq, d,
                                         out.data_ptr(), _dtype_code(out), _ptr(out_stats), _ptr(err_flag),
                                         out_batch_stride),
