@@ -230,7 +230,10 @@ class LLDecode:
             self.epoch.data_ptr(), self.done.data_ptr()), "sda_ll_unscramble_merge")
 
     def step(self, q: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
-        """q [B_p, Hq, 1, d] (this rank's requests) -> out [B_p, Hq, 1, d]."""
+        """q [B_p, Hq, 1, d] (this rank's requests) -> out [B_p, Hq, 1, d]. Either may be pinned
+        host memory (K1 reads Q / K3 stores O over PCIe)."""
+        self.ops._cuda_or_pinned(q, "q")
+        self.ops._cuda_or_pinned(out, "out")
         self.scramble_q(q)
         self.serve()
         self.finish(out)
