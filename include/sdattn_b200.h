@@ -45,7 +45,8 @@ typedef enum {
     SDA_ERR_CUDA = 6,             /* a CUDA runtime error (launch / config) */
     SDA_ERR_NO_DEVICE = 7,        /* no sm_100 device visible */
     SDA_ERR_ROLE_VIOLATION = 8,   /* protocol.cpp:215-216: compute node asked for its own domain's keys */
-    SDA_ERR_FRAME = 9             /* FrameError: bad magic / truncated / inconsistent length / CRC mismatch (frame.cpp:138-164) */
+    SDA_ERR_FRAME = 9,            /* FrameError: bad magic / truncated / inconsistent length / CRC mismatch (frame.cpp:138-164) */
+    SDA_ERR_TIMEOUT = 10          /* a peer-memory wait gave up (sda_spin_error): a peer rank is gone or far behind */
 } sda_status;
 
 typedef enum { SDA_BF16 = 0, SDA_F32 = 1, SDA_F64 = 2 /* quantised-wire entry points only */ } sda_dtype;
@@ -255,7 +256,9 @@ sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, i
  * :1097-1102, inside one NVSwitch box). Receive buffers are mapped into every peer with CUDA
  * IPC; a push copies each peer's payload over NVLink and raises that peer's per-sender flag
  * (system-scope release) with the step epoch; a wait spins (acquire) until all of its flags
- * reached the epoch (traps after ~4 s instead of hanging). All stream-ordered and graph-capturable.
+ * reached the epoch. All stream-ordered and graph-capturable. No wait hangs or traps: one that sees
+ * nothing within the spin budget (sda_set_spin_timeout_ns, default 30 s) returns and records
+ * SDA_ERR_TIMEOUT, which sda_spin_error reports; the exchange must then be torn down.
  * ------------------------------------------------------------------------------------------ */
 /* handle_out: 64 bytes (cudaIpcMemHandle_t of the allocation containing dev_ptr) + offset in it */
 sda_status sda_ipc_get_handle(const void* dev_ptr, void* handle_out, uint64_t* offset_out);
@@ -270,12 +273,17 @@ sda_status sda_exchange_push(void* stream, int32_t n_peers, const void* const* s
                              uint32_t* counters);
 /* wait until flags[i] >= *epoch for i < n (wrap-around safe) */
 sda_status sda_exchange_wait(void* stream, const uint32_t* flags, int32_t n, const uint32_t* epoch);
+/* Spin budget (ns) of every peer-memory wait on the current device (synchronous; default 30 s). */
+sda_status sda_set_spin_timeout_ns(uint64_t ns);
+/* *out = SDA_ERR_TIMEOUT if a wait on the current device gave up since the last clear, else SDA_OK
+ * (synchronous: call between steps, e.g. after a stream synchronize); clear != 0 resets it. */
+sda_status sda_spin_error(int32_t* out, int32_t clear);
 
 /* LL exchange for single-row decode (L_q = 1, head_dim >= 64): the three kernels of a step carry
  * the exchange themselves over peer memory (buffers mapped with sda_ipc_*), so a step is 3
  * launches with no copy kernel, fence or flag: every 4-byte data word travels next to the 4-byte
  * step epoch ("LL" format, 16-byte stores of two (word, epoch) pairs) and readers spin until their
- * words carry the current *epoch (trap after ~4 s instead of hanging). *epoch starts at 1 with
+ * words carry the current *epoch (spin budget and error reporting as above). *epoch starts at 1 with
  * all receive buffers zeroed; sda_ll_unscramble_merge bumps it when it finishes.
  *
  * Receive buffers on every rank (W = ranks, B_p = requests per inquirer, H = q heads, d):

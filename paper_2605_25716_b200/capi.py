@@ -22,7 +22,8 @@ MODE_S1_AND_S2, MODE_S1_ONLY = 0, 1
 MAX_SOURCES = 64
 STATUS_NAMES = {0: "SDA_OK", 1: "SDA_ERR_INVALID_ARGUMENT", 2: "SDA_ERR_NOT_POW2", 3: "SDA_ERR_EMPTY_SHARDS",
                 4: "SDA_ERR_MASKED_ROW", 5: "SDA_ERR_UNSUPPORTED", 6: "SDA_ERR_CUDA", 7: "SDA_ERR_NO_DEVICE",
-                8: "SDA_ERR_ROLE_VIOLATION"}
+                8: "SDA_ERR_ROLE_VIOLATION", 9: "SDA_ERR_FRAME", 10: "SDA_ERR_TIMEOUT"}
+SDA_ERR_TIMEOUT = 10
 
 # Every symbol include/sdattn_b200.h declares (checked by tests/test_capi_load.py).
 EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_negotiate_keyset",
@@ -35,7 +36,7 @@ EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_
            "sda_frame_elements", "sda_frame_payload_bytes", "sda_frame_bytes", "sda_frame_scratch_bytes",
            "sda_frame_encode", "sda_frame_parse_header", "sda_frame_decode", "sda_crc32",
            "sda_partial_attention_remote", "sda_scramble_batch_remote", "sda_partial_attention_ws",
-           "sda_prefill_workspace_bytes")
+           "sda_prefill_workspace_bytes", "sda_set_spin_timeout_ns", "sda_spin_error")
 
 
 class SdaError(RuntimeError):
@@ -131,6 +132,8 @@ def _load() -> ct.CDLL:
     lib.sda_exchange_push.argtypes = [_vp, ct.c_int32, ct.POINTER(ct.c_void_p), ct.POINTER(ct.c_void_p),
                                       ct.POINTER(ct.c_void_p), ct.c_uint64, _vp, _vp]
     lib.sda_exchange_wait.argtypes = [_vp, _vp, ct.c_int32, _vp]
+    lib.sda_set_spin_timeout_ns.argtypes = [ct.c_uint64]
+    lib.sda_spin_error.argtypes = [ct.POINTER(ct.c_int32), ct.c_int32]
     _pp = ct.POINTER(ct.c_void_p)
     lib.sda_ll_scramble_q.argtypes = [_vp, _vp, ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int32, _vp,
                                       ct.c_int64, ct.c_int32, _pp, ct.c_int32, _vp]
@@ -180,6 +183,19 @@ def check(status: int, what: str) -> None:
 
 def launch_count() -> int:
     return int(LIB.sda_launch_count())
+
+
+def set_spin_timeout(seconds: float) -> None:
+    """Spin budget of the peer-memory waits on the current device (default 30 s)."""
+    check(LIB.sda_set_spin_timeout_ns(int(seconds * 1e9)), "sda_set_spin_timeout_ns")
+
+
+def check_spin(clear: bool = True) -> None:
+    """Raise SdaError(SDA_ERR_TIMEOUT) if a peer-memory wait on the current device gave up since the
+    last check (synchronous; call between steps)."""
+    v = ct.c_int32(0)
+    check(LIB.sda_spin_error(ct.byref(v), 1 if clear else 0), "sda_spin_error")
+    check(v.value, "peer-memory wait")
 
 
 # ---------------------------------------------------------------------------------------------

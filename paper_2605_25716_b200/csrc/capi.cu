@@ -19,7 +19,8 @@ void count_launch() { ++g_launches; }
 
 namespace {
 
-bool supported_dim(int d) { return d == 32 || d == 64 || d == 128 || d == 256; }
+// 4..16: SIMT forms for the reference's own small-model tests; 32..256: every form
+bool supported_dim(int d) { return d == 4 || d == 8 || d == 16 || d == 32 || d == 64 || d == 128 || d == 256; }
 bool pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
 // Debug knobs (tests compare kernel variants): SDA_K1_SIMT=1 / SDA_K2_SIMT=1 force the SIMT
 // K1 / K2 kernels; SDA_K2_GROUPED=1 routes small GQA groups to the grouped-row kernel.
@@ -51,11 +52,12 @@ const char* sda_status_string(int32_t s) {
         case SDA_ERR_NOT_POW2: return "head dim must be a power of two";
         case SDA_ERR_EMPTY_SHARDS: return "merge: empty shard list";
         case SDA_ERR_MASKED_ROW: return "merge: row masked in every shard";
-        case SDA_ERR_UNSUPPORTED: return "unsupported on device (head dim not in {32,64,128,256})";
+        case SDA_ERR_UNSUPPORTED: return "unsupported on device (head dim not in {4,8,16,32,64,128,256}, or a form that needs d >= 64)";
         case SDA_ERR_CUDA: return "CUDA error";
         case SDA_ERR_NO_DEVICE: return "no CUDA device";
         case SDA_ERR_ROLE_VIOLATION: return "role violation";
         case SDA_ERR_FRAME: return "frame error (magic / length / dtype / CRC)";
+        case SDA_ERR_TIMEOUT: return "peer-memory wait timed out (a peer rank is gone or far behind)";
         default: return "unknown status";
     }
 }

@@ -154,6 +154,49 @@ struct Raw8<float> {
     }
 };
 
+// Four consecutive elements in storage format (the d = 4 decode rows of K2).
+template <typename T>
+struct Raw4;
+
+template <>
+struct Raw4<__nv_bfloat16> {
+    uint2 w;
+    __device__ __forceinline__ void load(const __nv_bfloat16* p) {
+        asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(w.x), "=r"(w.y) : "l"(p));
+    }
+    __device__ __forceinline__ float get(int i) const {
+        const uint32_t x = i < 2 ? w.x : w.y;
+        return (i & 1) ? __uint_as_float(x & 0xFFFF0000u) : __uint_as_float(x << 16);
+    }
+};
+
+template <>
+struct Raw4<float> {
+    uint4 a;
+    __device__ __forceinline__ void load(const float* p) { a = ld_stream(p); }
+    __device__ __forceinline__ float get(int i) const {
+        return __uint_as_float(i == 0 ? a.x : i == 1 ? a.y : i == 2 ? a.z : a.w);
+    }
+};
+
+// N consecutive elements (N a power of two >= 4; 8-byte aligned for bf16 N = 4) into f32: the
+// small head dims (d = 4, 8, 16) of the reference's own model tests
+template <int N>
+__device__ __forceinline__ void load_vec_n(const float* p, float* v) {
+    load_vec<N>(p, v);
+}
+template <int N>
+__device__ __forceinline__ void load_vec_n(const __nv_bfloat16* p, float* v) {
+    if constexpr (N % 8 == 0) {
+        load_vec<N>(p, v);
+    } else {
+        static_assert(N == 4, "");
+        const uint2 w = *reinterpret_cast<const uint2*>(p);
+        bf16x2_to_f2(w.x, v[0], v[1]);
+        bf16x2_to_f2(w.y, v[2], v[3]);
+    }
+}
+
 // Small-vector variants for N in {1, 2, 4, 8, 16, ...} f32 loads / any-typed stores.
 template <int N>
 __device__ __forceinline__ void load_vec_any(const float* p, float* v) {
@@ -258,18 +301,50 @@ __device__ __forceinline__ void ll_store(void* p, uint32_t a, uint32_t b, uint32
     asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(e), "r"(b), "r"(e)
                  : "memory");
 }
-// spin until both epochs of the 16-byte word at p equal e; traps after ~4 s instead of hanging
+// Spin budget of every peer-memory wait (LL words, exchange flags): a wait that sees nothing for
+// g_spin_timeout_ns gives up instead of hanging or trapping -- it records SDA_ERR_TIMEOUT in
+// g_spin_error (read and cleared by sda_spin_error) and returns, so the kernel runs to its end and
+// the CUDA context survives; the host reads the flag and tears the exchange down. Without
+// relocatable device code every translation unit has its own copy of both; the TUs that spin
+// export spin_access_<tu> (SDA_SPIN_ACCESSOR), through which sda_set_spin_timeout_ns and
+// sda_spin_error reach them all.
+static __device__ unsigned long long g_spin_timeout_ns = 30000000000ull;   // 30 s default
+static __device__ int g_spin_error = 0;
+
+// host: set this TU's timeout (set != nullptr), read its error word (err), clear it (clear)
+#define SDA_SPIN_ACCESSOR(name)                                                                   \
+    cudaError_t name(const unsigned long long* set, int* err, int clear) {                        \
+        cudaError_t e = cudaSuccess;                                                              \
+        if (set) e = cudaMemcpyToSymbol(g_spin_timeout_ns, set, sizeof(*set));                    \
+        if (e == cudaSuccess && err) e = cudaMemcpyFromSymbol(err, g_spin_error, sizeof(int));   \
+        if (e == cudaSuccess && clear) {                                                          \
+            const int z = 0;                                                                      \
+            e = cudaMemcpyToSymbol(g_spin_error, &z, sizeof(z));                                  \
+        }                                                                                         \
+        return e;                                                                                 \
+    }
+
+// true once the spin that started at t0 has used up its budget (the error is recorded once)
+__device__ __forceinline__ bool spin_expired(uint64_t t0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 <= *(volatile unsigned long long*)&g_spin_timeout_ns) return false;
+    atomicCAS(&g_spin_error, 0, (int)SDA_ERR_TIMEOUT);
+    return true;
+}
+
+// spin until both epochs of the 16-byte word at p equal e (or the spin budget is used up: the
+// stale words are returned and g_spin_error is set)
 __device__ __forceinline__ uint2 ll_load(const void* p, uint32_t e) {
     uint32_t a, fa, b, fb;
     asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(fa), "=r"(b), "=r"(fb) : "l"(p) : "memory");
     if (fa != e || fb != e) {
-        uint64_t t0, t;
+        uint64_t t0;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
         do {
             asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(a), "=r"(fa), "=r"(b), "=r"(fb) : "l"(p) : "memory");
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > 4000000000ull) __trap();
+            if (spin_expired(t0)) break;
         } while (fa != e || fb != e);
     }
     return make_uint2(a, b);

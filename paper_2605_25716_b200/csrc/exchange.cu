@@ -10,7 +10,8 @@
 // Safety of buffer reuse comes from the protocol itself: a sender's next SCR_Q push into rank r
 // happens only after it has received r's SCR_SHARD for the current step, which r sends only after
 // its K2 has consumed the current Q'; likewise for the return buffers. A spin that does not see
-// its flag within ~4 s traps (a kernel error instead of a hung GPU).
+// its flag within the spin budget (sda_set_spin_timeout_ns, default 30 s) gives up and records
+// SDA_ERR_TIMEOUT for sda_spin_error instead of hanging the GPU or trapping the context.
 #include <cuda.h>
 
 #include <algorithm>
@@ -69,14 +70,14 @@ __global__ void wait_kernel(const uint32_t* flags, int n, const uint32_t* epoch)
             uint32_t v;
             asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
             if ((int32_t)(v - e) >= 0) break;
-            uint64_t t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > 4000000000ull) __trap();   // ~4 s: a peer is gone; fail instead of hanging
+            if (spin_expired(t0)) break;   // a peer is gone: record SDA_ERR_TIMEOUT, do not hang
             __nanosleep(64);
         }
     }
     __syncthreads();
 }
+
+SDA_SPIN_ACCESSOR(spin_access_exchange)
 
 __global__ void timestamp_kernel(uint64_t* dst) {
     uint64_t t;
@@ -178,6 +179,35 @@ sda_status sda_exchange_wait(void* stream, const uint32_t* flags, int32_t n, con
     sda::count_launch();
     sda::wait_kernel<<<1, ((n + 31) / 32) * 32, 0, static_cast<cudaStream_t>(stream)>>>(flags, n, epoch);
     return from_cuda_x(cudaGetLastError());
+}
+
+// every translation unit whose kernels spin on peer memory (common.cuh SDA_SPIN_ACCESSOR)
+static cudaError_t spin_access_all(const unsigned long long* set, int* err, int clear) {
+    cudaError_t (*const tus[])(const unsigned long long*, int*, int) = {
+        sda::spin_access_exchange, sda::spin_access_k2_decode, sda::spin_access_k3_merge};
+    int worst = 0;
+    for (auto fn : tus) {
+        int v = 0;
+        const cudaError_t e = fn(set, err ? &v : nullptr, clear);
+        if (e != cudaSuccess) return e;
+        if (v) worst = v;
+    }
+    if (err) *err = worst;
+    return cudaSuccess;
+}
+
+sda_status sda_set_spin_timeout_ns(uint64_t ns) {
+    if (ns == 0) return SDA_ERR_INVALID_ARGUMENT;
+    const unsigned long long v = ns;
+    return from_cuda_x(spin_access_all(&v, nullptr, 0));
+}
+
+sda_status sda_spin_error(int32_t* out, int32_t clear) {
+    if (!out) return SDA_ERR_INVALID_ARGUMENT;
+    int v = 0;
+    const cudaError_t e = spin_access_all(nullptr, &v, clear);
+    *out = v;
+    return from_cuda_x(e);
 }
 
 sda_status sda_trace_timestamp(void* stream, uint64_t* dst) {

@@ -19,7 +19,7 @@ namespace sda {
 
 template <int D>
 struct K1Shape {
-    static constexpr int E = 16;              // elements per lane
+    static constexpr int E = D < 16 ? D : 16; // elements per lane (d < 16: one lane owns a row)
     static constexpr int LPR = D / E;         // lanes per row
     static constexpr int R = 32 / LPR;        // rows per warp
     static constexpr int CS = E + 4;          // padded chunk stride (conflict-free LDS/STS.128)
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p, cons
         const int64_t src = valid ? (perm ? (int64_t)perm[r] : r) : 0;
 
         float v[E];
-        load_vec<E>(x + src * D + lg * E, v);
+        load_vec_n<E>(x + src * D + lg * E, v);
 #pragma unroll
         for (int e = 0; e < E; ++e) u[p1[e]] = v[e] * kin[e];   // u[P1[i]] = x[i] * s1^{+-1}[i]
         __syncwarp();
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p, cons
             if (ll)
                 ll_store_row<E, Tout>(p.ll_out[b / p.x_batch_mod], out_elem + r * D + lg * E, v, ep);
             else
-                store_vec<E>(out + r * D + lg * E, v);
+                store_vec_any<E>(out + r * D + lg * E, v);
         }
         __syncwarp();
     }
@@ -163,6 +163,9 @@ static cudaError_t launch_k1_d(const K1Params& p, int xdt, int odt, int64_t n_ba
 
 cudaError_t launch_k1(const K1Params& p, int d, int xdt, int odt, int64_t n_batch, cudaStream_t st) {
     switch (d) {
+        case 4: return launch_k1_d<4>(p, xdt, odt, n_batch, st);
+        case 8: return launch_k1_d<8>(p, xdt, odt, n_batch, st);
+        case 16: return launch_k1_d<16>(p, xdt, odt, n_batch, st);
         case 32: return launch_k1_d<32>(p, xdt, odt, n_batch, st);
         case 64: return launch_k1_d<64>(p, xdt, odt, n_batch, st);
         case 128: return launch_k1_d<128>(p, xdt, odt, n_batch, st);

@@ -21,7 +21,7 @@ namespace sda {
 
 template <int D>
 struct K2Shape {
-    static constexpr int VEC = 8;
+    static constexpr int VEC = D < 8 ? D : 8;    // elements per lane (d = 4: one lane per key row)
     static constexpr int LPR = D / VEC;          // lanes per key row
     static constexpr int RW = 32 / LPR;          // key rows per warp step
     static constexpr int WARPS = 4;
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
             }
         }
     } else {
-        load_vec<VEC>(static_cast<const TQ*>(p.q) + q_elem, qv);
+        load_vec_n<VEC>(static_cast<const TQ*>(p.q) + q_elem, qv);
     }
 #pragma unroll
     for (int i = 0; i < VEC; ++i) qv[i] *= p.scale * kLog2e;   // logits in log2 units
@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
     // full-mask shuffles below are always executed by all 32 lanes; rows past k1 are masked.
     for (int64_t jw = k0 + warp * S::RW; jw < k1; jw += (int64_t)NG * U) {
         const int64_t j0 = jw + g;
-        Raw8<TKV> kr[U], vr[U];
+        using Raw = typename std::conditional<VEC == 8, Raw8<TKV>, Raw4<TKV>>::type;
+        Raw kr[U], vr[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t j = j0 + (int64_t)u * NG;
@@ -148,12 +149,26 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
 #pragma unroll
     for (int i = 0; i < NG; ++i) M = fmaxf(M, sm_m[i]);
     float S_ = 0.f;
-    float wgt[NG];
+    // lane-group weights: in registers up to 32 groups (d >= 32); the small head dims (64 / 128
+    // groups) keep them in shared memory instead of spilling a 128-entry array
+    constexpr bool WREG = NG <= 32;
+    float wgt[WREG ? NG : 1];
+    __shared__ float sm_w[WREG ? 1 : NG];
+    if constexpr (WREG) {
 #pragma unroll
-    for (int i = 0; i < NG; ++i) {
-        wgt[i] = (M == -INFINITY) ? 0.f : ex2(sm_m[i] - M);
-        S_ = fmaf(sm_s[i], wgt[i], S_);
+        for (int i = 0; i < NG; ++i) {
+            wgt[i] = (M == -INFINITY) ? 0.f : ex2(sm_m[i] - M);
+            S_ = fmaf(sm_s[i], wgt[i], S_);
+        }
+    } else {
+        for (int i = threadIdx.x; i < NG; i += blockDim.x) sm_w[i] = (M == -INFINITY) ? 0.f : ex2(sm_m[i] - M);
+        __syncthreads();
+        for (int i = 0; i < NG; ++i) S_ = fmaf(sm_s[i], sm_w[i], S_);
     }
+    auto weight = [&](int i) -> float {
+        if constexpr (WREG) return wgt[i];
+        else return sm_w[i];
+    };
     const float inv = S_ > 0.f ? 1.f / S_ : 0.f;
     // back to natural-log units: row_max = max_j q.k_j / sqrt(d)
     const float row_max = S_ > 0.f ? M / kLog2e : -INFINITY;
@@ -164,8 +179,8 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
             float a0 = 0.f, a1 = 0.f;
 #pragma unroll
             for (int g2 = 0; g2 < NG; ++g2) {
-                a0 = fmaf(sm_o[g2][2 * pr], wgt[g2], a0);
-                a1 = fmaf(sm_o[g2][2 * pr + 1], wgt[g2], a1);
+                a0 = fmaf(sm_o[g2][2 * pr], weight(g2), a0);
+                a1 = fmaf(sm_o[g2][2 * pr + 1], weight(g2), a1);
             }
             ll_store(rb + 16 * pr, __float_as_uint(a0 * inv), __float_as_uint(a1 * inv), ep);
         }
@@ -177,7 +192,7 @@ __global__ void __launch_bounds__(128) k2_decode_kernel(const K2Params p) {
     for (int dim = threadIdx.x; dim < D; dim += blockDim.x) {
         float acc = 0.f;
 #pragma unroll
-        for (int i = 0; i < NG; ++i) acc = fmaf(sm_o[i][dim], wgt[i], acc);
+        for (int i = 0; i < NG; ++i) acc = fmaf(sm_o[i][dim], weight(i), acc);
         p.out_o[orow * D + dim] = acc * inv;
     }
     if (threadIdx.x == 0) {
@@ -217,6 +232,8 @@ cudaError_t launch_ll_unpack_q(const void* ll_q, int64_t elems, void* out, const
                       static_cast<uint2*>(out), epoch);
 }
 
+SDA_SPIN_ACCESSOR(spin_access_k2_decode)
+
 int k2_decode_ctas_per_sm() {   // resident CTAs per SM of the C2 instantiation (split heuristic)
     static int n = 0;
     if (!n) {
@@ -234,6 +251,9 @@ int k2_decode_ctas_per_sm() {   // resident CTAs per SM of the C2 instantiation 
 
 cudaError_t launch_k2_decode(const K2Params& p, int d, int qdt, int kvdt, cudaStream_t st) {
     switch (d) {
+        case 4: return launch_k2_d<4>(p, qdt, kvdt, st);
+        case 8: return launch_k2_d<8>(p, qdt, kvdt, st);
+        case 16: return launch_k2_d<16>(p, qdt, kvdt, st);
         case 32: return launch_k2_d<32>(p, qdt, kvdt, st);
         case 64: return launch_k2_d<64>(p, qdt, kvdt, st);
         case 128: return launch_k2_d<128>(p, qdt, kvdt, st);

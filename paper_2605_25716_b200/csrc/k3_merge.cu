@@ -437,9 +437,111 @@ static cudaError_t launch_k3_t(const K3Params& p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+SDA_SPIN_ACCESSOR(spin_access_k3_merge)
+
+// Small head dims (d in {4, 8, 16}: the reference's own model / protocol tests, test_model.cpp:17-19,
+// helpers.hpp:19): one thread per output row, the whole row and the phi_V^-1 of its group in the
+// thread's registers / local memory. Same two passes and the same per-group unscramble as
+// k3_merge_kernel (no LL records: the LL exchange is a d >= 64 decode form).
+template <int D, typename TOut>
+__global__ void __launch_bounds__(128) k3_merge_tiny_kernel(const K3Params p) {
+    pdl_wait();
+    const int64_t total = p.n_batch * p.q_heads * p.q_rows;
+    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= total) return;
+    const int64_t r = row % p.q_rows, bh = row / p.q_rows;
+    const int h = (int)(bh % p.q_heads);
+    const int64_t b = bh / p.q_heads;
+    const int kh = h / (p.q_heads / p.key_heads);
+    auto offs = [&](const K3Source& src, int64_t& st_off, int64_t& o_off) {
+        const int64_t ri = src.pq_inv ? (int64_t)src.pq_inv[b * p.pq_bstride + r] : r;
+        st_off = src.bstride ? b * src.bstride + ((int64_t)h * p.q_rows + ri) * 2 : (bh * p.q_rows + ri) * 2;
+        o_off = src.bstride ? b * src.bstride + ((int64_t)h * p.q_rows + ri) * D : (bh * p.q_rows + ri) * D;
+    };
+    float mstar = -INFINITY;   // attention.cpp:103-105
+    for (int s = 0; s < p.n_src; ++s) {
+        int64_t so, oo;
+        offs(p.src[s], so, oo);
+        const float2 st = *reinterpret_cast<const float2*>(p.src[s].stats + so);
+        if (st.y > 0.f) mstar = fmaxf(mstar, st.x);
+    }
+    const bool single = p.n_src == 1;
+    float out[D], acc[D];
+#pragma unroll
+    for (int e = 0; e < D; ++e) out[e] = acc[e] = 0.f;
+    float denom = 0.f;
+    bool pending = false;
+    for (int s = 0; s < p.n_src; ++s) {
+        const K3Source& src = p.src[s];
+        int64_t so, oo;
+        offs(src, so, oo);
+        const float2 st = *reinterpret_cast<const float2*>(src.stats + so);
+        if (st.y > 0.f) {
+            const float w = single ? 1.f : st.y * expf(st.x - mstar);
+            denom += single ? st.y : w;
+#pragma unroll
+            for (int e = 0; e < D; ++e) acc[e] = fmaf(w, src.o[oo + e], acc[e]);
+            pending = true;
+        }
+        const bool group_end = (s + 1 == p.n_src) || (p.src[s + 1].keys != src.keys);
+        if (group_end && pending) {
+            if (src.keys) {
+                // u[j] = acc[P2[j]] / s2[P2[j]] ; w = H u ; y[i] = w[P1[i]] / (s1[i] sqrt(d))
+                const uint8_t* sc = scrambler_ptr(src.keys, p.keys_bstride, b, kh, D, 1);
+                const float* ftab = reinterpret_cast<const float*>(sc);
+                const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + 24 * D);
+                float t[D], u[D];
+#pragma unroll
+                for (int e = 0; e < D; ++e) t[e] = acc[e] * ftab[kInvIn * D + e];
+                for (int j = 0; j < D; ++j) u[j] = t[utab[kP2 * D + j]];
+#pragma unroll
+                for (int hh = 1; hh < D; hh <<= 1)
+#pragma unroll
+                    for (int i = 0; i < D; ++i)
+                        if ((i & hh) == 0) {
+                            const float a = u[i], c = u[i + hh];
+                            u[i] = a + c;
+                            u[i + hh] = a - c;
+                        }
+                for (int i = 0; i < D; ++i) out[i] += u[utab[kP1 * D + i]] * ftab[kInvOut * D + i];
+            } else {
+#pragma unroll
+                for (int e = 0; e < D; ++e) out[e] += acc[e];
+            }
+#pragma unroll
+            for (int e = 0; e < D; ++e) acc[e] = 0.f;
+            pending = false;
+        }
+    }
+    const bool masked = !(mstar > -INFINITY);
+    if (masked && p.err) atomicExch(p.err, (int32_t)SDA_ERR_MASKED_ROW);
+    const float inv = masked ? __int_as_float(0x7fc00000) : (single ? 1.f : 1.f / denom);
+#pragma unroll
+    for (int e = 0; e < D; ++e) out[e] *= inv;
+    const int64_t hr = (int64_t)h * p.q_rows + r;
+    TOut* o = static_cast<TOut*>(p.out) + (p.out_bstride ? b * p.out_bstride + hr * D : row * D);
+#pragma unroll
+    for (int e = 0; e < D; ++e) o[e] = (TOut)out[e];
+    if (p.out_stats) {
+        const int64_t so = p.out_bstride ? b * p.out_bstride + hr * 2 : row * 2;
+        p.out_stats[so + 0] = single ? (masked ? -INFINITY : mstar) : mstar;
+        p.out_stats[so + 1] = masked ? 0.f : denom;
+    }
+}
+
+template <int D, typename TOut>
+static cudaError_t launch_k3_tiny(const K3Params& p, cudaStream_t st) {
+    if (p.ll) return cudaErrorInvalidValue;
+    const int64_t total = p.n_batch * p.q_heads * p.q_rows;
+    return pdl_launch(k3_merge_tiny_kernel<D, TOut>, dim3((unsigned)((total + 127) / 128)), dim3(128), st, p);
+}
+
 cudaError_t launch_k3(const K3Params& p, int d, int odt, cudaStream_t st) {
     const bool bf = odt == SDA_BF16;
     switch (d) {
+        case 4: return bf ? launch_k3_tiny<4, __nv_bfloat16>(p, st) : launch_k3_tiny<4, float>(p, st);
+        case 8: return bf ? launch_k3_tiny<8, __nv_bfloat16>(p, st) : launch_k3_tiny<8, float>(p, st);
+        case 16: return bf ? launch_k3_tiny<16, __nv_bfloat16>(p, st) : launch_k3_tiny<16, float>(p, st);
         case 32: return bf ? launch_k3_t<32, __nv_bfloat16>(p, st) : launch_k3_t<32, float>(p, st);
         case 64: return bf ? launch_k3_t<64, __nv_bfloat16>(p, st) : launch_k3_t<64, float>(p, st);
         case 128: return bf ? launch_k3_t<128, __nv_bfloat16>(p, st) : launch_k3_t<128, float>(p, st);

@@ -146,5 +146,9 @@ size_t k2_prefill_sk_workspace_bytes(const K2Params& p);
 bool k2_gqa_tc_eligible(const K2Params& p, int d, int qdt, int kvdt);
 cudaError_t launch_k2_gqa_tc(const K2Params& p, cudaStream_t st);
 cudaError_t launch_k3(const K3Params& p, int d, int odt, cudaStream_t st);
+// per-TU spin budget / error word (common.cuh SDA_SPIN_ACCESSOR)
+cudaError_t spin_access_exchange(const unsigned long long* set, int* err, int clear);
+cudaError_t spin_access_k2_decode(const unsigned long long* set, int* err, int clear);
+cudaError_t spin_access_k3_merge(const unsigned long long* set, int* err, int clear);
 
 }  // namespace sda

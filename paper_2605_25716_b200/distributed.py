@@ -110,21 +110,36 @@ class PeerExchange:
     and raise their flags, wait for mine, ... the same for the packed (O', stats) records. Same
     data placement as all_to_all_single, so the compute is unchanged."""
 
-    def __init__(self, bufs: StepBuffers, group: Optional[dist.ProcessGroup] = None):
+    def __init__(self, bufs: StepBuffers, group: Optional[dist.ProcessGroup] = None, rank: Optional[int] = None):
+        """rank: this exchange's logical rank inside an in-process LocalWorld (one GPU emulating W
+        domains; its peers' buffers are then connected by LocalWorld, not over CUDA IPC)."""
         import ctypes as ct
 
         from . import capi
         self.capi, self.ct = capi, ct
         self.world = bufs.q_send.shape[0]
-        self.rank = dist.get_rank(group)
+        self.rank = dist.get_rank(group) if rank is None else rank
+        self.bufs = bufs
         dev = bufs.q_send.device
         W = self.world
         self.flags = torch.zeros(2 * W, dtype=torch.int32, device=dev)      # [SCR_Q from r | SCR_SHARD from r]
         self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)
         self.counters = torch.zeros(2 * W, dtype=torch.int32, device=dev)
         self.k1_counters = torch.zeros(16, dtype=torch.int32, device=dev)   # sda_scramble_batch_remote
-        torch.cuda.synchronize()
-        ptrs, self.opened = map_peer_buffers({"q": bufs.q_recv, "ret": bufs.ret_recv, "flags": self.flags}, group)
+        self.opened = []
+        if rank is None:
+            torch.cuda.synchronize()
+            ptrs, self.opened = map_peer_buffers(self.peer_buffers(), group)
+            self.connect(ptrs)
+            dist.barrier(group=group)
+
+    def peer_buffers(self) -> dict:
+        """The buffers every peer writes into (mapped into the peers' address spaces)."""
+        return {"q": self.bufs.q_recv, "ret": self.bufs.ret_recv, "flags": self.flags}
+
+    def connect(self, ptrs: dict) -> None:
+        """ptrs[name][r]: the address of rank r's peer buffer `name` as this process sees it."""
+        ct, bufs, W = self.ct, self.bufs, self.world
         base = {(r, name): ptrs[name][r] for name in ptrs for r in range(W)}
         self.base = base
         q_slot = bufs.q_send[0].numel() * bufs.q_send.element_size()
@@ -136,7 +151,6 @@ class PeerExchange:
         self.r_args = (arr([bufs.ret_send[p].data_ptr() for p in range(W)]),
                        arr([base[(p, "ret")] + self.rank * r_slot for p in range(W)]),
                        arr([base[(p, "flags")] + 4 * (W + self.rank) for p in range(W)]), r_slot)
-        dist.barrier(group=group)
 
     def _stream(self):
         return torch.cuda.current_stream().cuda_stream
@@ -154,13 +168,25 @@ class PeerExchange:
         self.capi.check(self.capi.LIB.sda_exchange_wait(self._stream(), self.flags.data_ptr() + 4 * off, self.world,
                                                          self.epoch.data_ptr()), "exchange_wait")
 
-    def exchange_q(self):
+    def push_q(self):
         self._push(self.q_args, 0)
+
+    def wait_q(self):
         self._wait(0)
 
-    def exchange_ret(self):
+    def push_ret(self):
         self._push(self.r_args, self.world)
+
+    def wait_ret(self):
         self._wait(self.world)
+
+    def exchange_q(self):
+        self.push_q()
+        self.wait_q()
+
+    def exchange_ret(self):
+        self.push_ret()
+        self.wait_ret()
 
 
 class LLDecode:
@@ -173,12 +199,19 @@ class LLDecode:
 
     def __init__(self, b_per: int, q_heads: int, head_dim: int, inquirer_keys: Sequence, shard,
                  n_splits: Optional[int] = None, kv_heads: Optional[int] = None,
-                 wire_dtype: torch.dtype = torch.bfloat16, group: Optional[dist.ProcessGroup] = None):
+                 wire_dtype: torch.dtype = torch.bfloat16, group: Optional[dist.ProcessGroup] = None,
+                 world: Optional[tuple] = None):
+        """world: (W, rank) of a logical rank inside an in-process LocalWorld (one GPU emulating W
+        domains); its peers' slots are then connected by LocalWorld instead of over CUDA IPC."""
         import ctypes as ct
 
         from . import capi, ops
-        self.capi, self.ops = capi, ops
-        W, rank = (dist.get_world_size(group), dist.get_rank(group)) if dist.is_initialized() else (1, 0)
+        self.capi, self.ops, self.ct = capi, ops, ct
+        if world is not None:
+            W, rank = world
+        else:
+            W, rank = (dist.get_world_size(group), dist.get_rank(group)) if dist.is_initialized() else (1, 0)
+        self.rank = rank
         dev = shard.k.device
         self.W, self.Bp, self.Hq, self.d = W, b_per, q_heads, head_dim
         self.kv_heads = kv_heads or inquirer_keys[0].kv_heads
@@ -197,13 +230,25 @@ class LLDecode:
         # GQA shards: Q' is unpacked from its LL words into this buffer for the tensor-core kernel
         self.gqa_work = (torch.empty((W * b_per, q_heads, 1, head_dim), dtype=torch.bfloat16, device=dev)
                          if shard.k.shape[1] < q_heads else None)
-        torch.cuda.synchronize()
-        ptrs, self.opened = map_peer_buffers({"q": self.q_ll, "rec": self.rec_ll}, group)
-        arr = lambda xs: (ct.c_void_p * W)(*xs)  # noqa: E731
-        self.ll_q = arr([ptrs["q"][r] + rank * q_slot for r in range(W)])       # my slot on every destination
-        self.ll_rec = arr([ptrs["rec"][r] + rank * r_slot for r in range(W)])   # my slot on every inquirer
-        if dist.is_initialized():
-            dist.barrier(group=group)
+        if os.environ.get("SDA_SPIN_TIMEOUT_S"):   # spin budget of the LL waits (default 30 s)
+            capi.set_spin_timeout(float(os.environ["SDA_SPIN_TIMEOUT_S"]))
+        self.q_slot, self.r_slot = q_slot, r_slot
+        self.opened = []
+        if world is None:
+            torch.cuda.synchronize()
+            ptrs, self.opened = map_peer_buffers(self.peer_buffers(), group)
+            self.connect(ptrs)
+            if dist.is_initialized():
+                dist.barrier(group=group)
+
+    def peer_buffers(self) -> dict:
+        return {"q": self.q_ll, "rec": self.rec_ll}
+
+    def connect(self, ptrs: dict) -> None:
+        """ptrs[name][r]: the address of rank r's receive buffer `name` as this process sees it."""
+        arr = lambda xs: (self.ct.c_void_p * self.W)(*xs)  # noqa: E731
+        self.ll_q = arr([ptrs["q"][r] + self.rank * self.q_slot for r in range(self.W)])     # my slot on every destination
+        self.ll_rec = arr([ptrs["rec"][r] + self.rank * self.r_slot for r in range(self.W)])  # my slot on every inquirer
 
     def scramble_q(self, q: torch.Tensor):
         """K1: span_send_layer for every domain, Q' written into the destinations' slots."""
@@ -229,22 +274,43 @@ class LLDecode:
             self.kv_heads, self.Bp, self.Hq, self.d, out.data_ptr(), self.ops._dtype_code(out),
             self.epoch.data_ptr(), self.done.data_ptr()), "sda_ll_unscramble_merge")
 
+    def validate(self, t: torch.Tensor, name: str) -> None:
+        """Every check that can raise, done before the step's first launch: once K1 has written
+        Q' into the peers' slots the step must run to its K3 (which opens the next epoch), or the
+        ranks' epochs go out of step."""
+        self.ops._cuda_or_pinned(t, name)
+        if t.dtype not in (torch.bfloat16, torch.float32):
+            raise TypeError(f"{name} must be bf16 or f32, got {t.dtype}")
+        if tuple(t.shape) != (self.Bp, self.Hq, 1, self.d):
+            raise ValueError(f"{name} must have shape {(self.Bp, self.Hq, 1, self.d)}, got {tuple(t.shape)}")
+        if t.is_cuda and t.device != self.shard.k.device:
+            raise ValueError(f"{name} is on {t.device}, the shard on {self.shard.k.device}")
+
+    def check(self) -> None:
+        """Raise SdaError(SDA_ERR_TIMEOUT) if a spin of this device gave up (a peer is gone)."""
+        self.capi.check_spin()
+
     def step(self, q: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
         """q [B_p, Hq, 1, d] (this rank's requests) -> out [B_p, Hq, 1, d]. Either may be pinned
         host memory (K1 reads Q / K3 stores O over PCIe)."""
-        self.ops._cuda_or_pinned(q, "q")
-        self.ops._cuda_or_pinned(out, "out")
+        self.validate(q, "q")
+        self.validate(out, "out")
         self.scramble_q(q)
         self.serve()
         self.finish(out)
         return out
 
 
-def scrambled_decode_step(q: torch.Tensor, compute: RankCompute, bufs: StepBuffers, out: torch.Tensor,
-                          group: Optional[dist.ProcessGroup] = None,
-                          exchange: Optional[PeerExchange] = None) -> torch.Tensor:
-    """One layer step for this rank's requests q [B_p, Hq, Lq, d]; returns out [B_p, Hq, Lq, d].
-    exchange: a PeerExchange to move Q' and the partials over NVLink peer memory (else NCCL)."""
+A2A_Q, A2A_RET, SYNC = "a2a_q", "a2a_ret", "sync"
+
+
+def decode_step_phases(q: torch.Tensor, compute: RankCompute, bufs: StepBuffers, out: torch.Tensor,
+                       exchange: Optional[PeerExchange] = None):
+    """One layer step of one rank as a generator of its cross-rank points: it yields A2A_Q /
+    A2A_RET where an all-to-all of bufs.q_send -> q_recv / ret_send -> ret_recv is due, and SYNC
+    between a peer-memory push (or a kernel that writes into peers' slots) and the wait on the
+    flags it raises. scrambled_decode_step drives it with NCCL; LocalWorld drives W of them in
+    lockstep on one GPU (every rank's launches of a phase before any rank's next phase)."""
     world = bufs.q_send.shape[0]
     if exchange is not None:
         exchange.begin_step()
@@ -257,19 +323,20 @@ def scrambled_decode_step(q: torch.Tensor, compute: RankCompute, bufs: StepBuffe
             for dom in range(world):
                 compute.scramble_q(q, dom, bufs.q_send[dom])
     if world > 1 and exchange is not None:
-        if q_sent:
-            exchange._wait(0)                                         # SCR_Q written by K1 itself
-        else:
-            exchange.exchange_q()                                     # SCR_Q over peer memory
+        if not q_sent:
+            exchange.push_q()                                         # SCR_Q over peer memory
+        yield SYNC
+        exchange.wait_q()
         q_all = bufs.q_recv
         b_tot = q_all.shape[0] * q_all.shape[1]
         if compute.serve_remote is not None and compute.serve_remote(
                 q_all.view((b_tot,) + tuple(q_all.shape[2:])), bufs.dims, exchange):
-            exchange._wait(world)                                     # SCR_SHARD written by K2 itself
+            yield SYNC                                                # SCR_SHARD written by K2 itself
+            exchange.wait_ret()
             compute.finish(bufs.ret_recv, out, bufs.dims)
-            return out
+            return
     elif world > 1:
-        dist.all_to_all_single(bufs.q_recv, bufs.q_send, group=group)   # SCR_Q
+        yield A2A_Q                                                   # SCR_Q
         q_all = bufs.q_recv
     else:
         q_all = bufs.q_send
@@ -277,15 +344,83 @@ def scrambled_decode_step(q: torch.Tensor, compute: RankCompute, bufs: StepBuffe
     compute.serve(q_all.view((b_tot,) + tuple(q_all.shape[2:])),     # try_serve_q on my shard
                   bufs.ret_send.view(b_tot, -1), bufs.dims)
     if world > 1 and exchange is not None:
-        exchange.exchange_ret()                                       # SCR_SHARD over peer memory
+        exchange.push_ret()                                           # SCR_SHARD over peer memory
+        yield SYNC
+        exchange.wait_ret()
         back = bufs.ret_recv
     elif world > 1:
-        dist.all_to_all_single(bufs.ret_recv, bufs.ret_send, group=group)   # SCR_SHARD (O' + stats)
+        yield A2A_RET                                                 # SCR_SHARD (O' + stats)
         back = bufs.ret_recv
     else:
         back = bufs.ret_send
     compute.finish(back, out, bufs.dims)                          # span_finish_layer
+
+
+def scrambled_decode_step(q: torch.Tensor, compute: RankCompute, bufs: StepBuffers, out: torch.Tensor,
+                          group: Optional[dist.ProcessGroup] = None,
+                          exchange: Optional[PeerExchange] = None) -> torch.Tensor:
+    """One layer step for this rank's requests q [B_p, Hq, Lq, d]; returns out [B_p, Hq, Lq, d].
+    exchange: a PeerExchange to move Q' and the partials over NVLink peer memory (else NCCL)."""
+    for ev in decode_step_phases(q, compute, bufs, out, exchange):
+        if ev == A2A_Q:
+            dist.all_to_all_single(bufs.q_recv, bufs.q_send, group=group)
+        elif ev == A2A_RET:
+            dist.all_to_all_single(bufs.ret_recv, bufs.ret_send, group=group)
     return out
+
+
+class LocalWorld:
+    """W logical ranks (compute domains 1..W and their inquirers) in ONE process on ONE GPU: the
+    multi-GPU step forms with every rank's receive slots in the same device memory, so their
+    cross-rank addressing (which domain's slot, which inquirer's record) runs -- and is checked
+    against the oracle -- on a 1-GPU box, including W = 8, the node count of BASELINE configs
+    4 and 5. Every rank's launches of one phase are issued before any rank's next phase on the
+    one stream, so a wait never precedes the writes it waits for. The all-to-alls of the NCCL
+    form become the same slot-to-slot copies. Not a product path: the LL / push / remote kernels
+    are the ones the multi-GPU step runs, only the peers live in one address space."""
+
+    @staticmethod
+    def connect(objs: Sequence) -> None:
+        """Wire W LLDecode / PeerExchange objects (built with world=(W, r) / rank=r) to each other."""
+        names = objs[0].peer_buffers().keys()
+        ptrs = {n: [o.peer_buffers()[n].data_ptr() for o in objs] for n in names}
+        for o in objs:
+            o.connect(ptrs)
+
+    @staticmethod
+    def ll_step(ranks: Sequence["LLDecode"], qs: Sequence[torch.Tensor], outs: Sequence[torch.Tensor]) -> None:
+        """One LL decode step of every rank: all K1 (Q' into the domains' slots), all K2, all K3."""
+        for r, x in enumerate(ranks):
+            x.validate(qs[r], "q")
+            x.validate(outs[r], "out")
+        for r, x in enumerate(ranks):
+            x.scramble_q(qs[r])
+        for x in ranks:
+            x.serve()
+        for r, x in enumerate(ranks):
+            x.finish(outs[r])
+
+    @staticmethod
+    def decode_step(qs: Sequence[torch.Tensor], computes: Sequence[RankCompute], bufs: Sequence[StepBuffers],
+                    outs: Sequence[torch.Tensor], exchanges: Optional[Sequence[PeerExchange]] = None) -> None:
+        """scrambled_decode_step of every rank, phase by phase (NCCL form: exchanges None)."""
+        W = len(qs)
+        gens = [decode_step_phases(qs[r], computes[r], bufs[r], outs[r], None if exchanges is None else exchanges[r])
+                for r in range(W)]
+        while True:
+            evs = [next(g, None) for g in gens]
+            if all(e is None for e in evs):
+                return
+            if len(set(evs)) != 1:
+                raise RuntimeError(f"ranks out of step: {evs}")
+            if evs[0] == A2A_Q:       # q_recv[r][s] = q_send[s][r] (all_to_all_single)
+                for r in range(W):
+                    for src in range(W):
+                        bufs[r].q_recv[src].copy_(bufs[src].q_send[r])
+            elif evs[0] == A2A_RET:
+                for r in range(W):
+                    for src in range(W):
+                        bufs[r].ret_recv[src].copy_(bufs[src].ret_send[r])
 
 
 def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = None,

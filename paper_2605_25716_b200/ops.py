@@ -84,10 +84,10 @@ def scramble(x: torch.Tensor, keys: torch.Tensor, variant: int, which: int, perm
     Bx, H, rows, d = x.shape
     B = n_batch or Bx
     kh = key_heads if key_heads is not None else H
-    if out is None:
-        out = torch.empty((B, H, rows, d), dtype=out_dtype or x.dtype, device=x.device)
-    _cuda(out, "out")
     _cuda(keys, "keys")
+    if out is None:   # a pinned host x is read in place; its result still lives on the keys' device
+        out = torch.empty((B, H, rows, d), dtype=out_dtype or x.dtype, device=x.device if x.is_cuda else keys.device)
+    _cuda(out, "out")
     if perm is not None:
         _cuda(perm, "perm")
     check(capi.LIB.sda_scramble(_stream(stream), variant, which, x.data_ptr(), _dtype_code(x), B, H, rows, d,

@@ -29,8 +29,10 @@ def test_status_mapping_without_device():
     L = capi.LIB
     # build_scrambler: d must be a power of two (scrambler.cpp:27)
     assert L.sda_scramble(None, 0, 0, 1, 0, 1, 1, 1, 48, 1, 0, 1, None, 0, 1, 0, 1, 0, 0) == 2
-    # d = 16 is valid for the reference but not compiled for the device
-    assert L.sda_scramble(None, 0, 0, 1, 0, 1, 1, 1, 16, 1, 0, 1, None, 0, 1, 0, 1, 0, 0) == 5
+    # d = 2 is valid for the reference but not compiled for the device (4..256 are)
+    assert L.sda_scramble(None, 0, 0, 1, 0, 1, 1, 1, 2, 1, 0, 1, None, 0, 1, 0, 1, 0, 0) == 5
+    # the LL decode exchange is a d >= 64 form
+    assert L.sda_ll_unscramble_merge(None, 1, 1, 1, 1, 0, 1, 1, 1, 16, 1, 0, 1, 1) == 5
     # row offset beyond the cache capacity
     assert L.sda_scramble(None, 0, 0, 1, 0, 1, 1, 4, 64, 1, 0, 1, None, 0, 1, 0, 3, 0, 0) == 1
     # q heads not a multiple of kv heads
