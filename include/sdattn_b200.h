@@ -49,7 +49,10 @@ typedef enum {
     SDA_ERR_TIMEOUT = 10          /* a peer-memory wait gave up (sda_spin_error): a peer rank is gone or far behind */
 } sda_status;
 
-typedef enum { SDA_BF16 = 0, SDA_F32 = 1, SDA_F64 = 2 /* quantised-wire entry points only */ } sda_dtype;
+/* SDA_F64: the FP64 mode (reference arithmetic and operation order on the device, f64 key image,
+ * f64 partials / stats in the float* output slots; SIMT, not a throughput path) of sda_scramble,
+ * sda_partial_attention(_causal) and sda_unscramble_merge, and the quantised-wire / frame entry points. */
+typedef enum { SDA_BF16 = 0, SDA_F32 = 1, SDA_F64 = 2 } sda_dtype;
 
 /* Which transform of phi a scramble applies (scrambler.cpp:75-85). */
 typedef enum {
@@ -105,6 +108,12 @@ sda_status sda_invert_permutation(const uint32_t* forward, size_t n, uint32_t* i
 #define SDA_SCRAMBLER_BYTES(d) ((size_t)32 * (size_t)(d))
 #define SDA_KEYSET_HEAD_BYTES(d) ((size_t)64 * (size_t)(d))
 size_t sda_keyset_bytes(uint32_t n_heads, uint32_t head_dim);
+/* FP64 mode key image (the f64 entry points: x / q / kv / out dtype SDA_F64): raw f64 s1, s2 and
+ * the u16 permutations + inverses, so the device repeats the reference's f64 operations exactly. */
+#define SDA_SCRAMBLER_BYTES_F64(d) ((size_t)24 * (size_t)(d))
+#define SDA_KEYSET_HEAD_BYTES_F64(d) ((size_t)48 * (size_t)(d))
+size_t sda_keyset_bytes_f64(uint32_t n_heads, uint32_t head_dim);
+sda_status sda_pack_keyset_f64(const sda_host_keyset* ks, uint32_t n_heads, uint32_t head_dim, void* out);
 /* Packs a host key set into the device image (f32 factor tables with the 1/sqrt(d) of the
  * normalised FWHT folded in, u16 permutations and their inverses). `out` is host memory of
  * sda_keyset_bytes(); the caller uploads it (cudaMemcpyAsync) next to its other key sets. */
@@ -350,6 +359,12 @@ sda_status sda_dequantize(void* stream, const uint8_t* codes, int64_t codes_stri
 /* x <- dequantize(quantize_affine(x, bits)) per tensor, in place (the wire emulation) */
 sda_status sda_quant_roundtrip(void* stream, void* x, int32_t dtype, int64_t n_tensors, int64_t count, int32_t bits,
                                uint64_t* scratch, int32_t* err);
+
+/* x <- round_to_format(x, wire_fmt) in place, the float-format wire_round (float_format.cpp:26-58,
+ * model.cpp:339-348, protocol.cpp:179): RNE onto the format's grid done in f64, +-inf and overflow
+ * clamped to +-max_finite. x: n device values, x_dtype SDA_F32 or SDA_F64; wire_fmt the reference's
+ * FloatFormat (0 f64 = no-op, 1 f32, 2 bf16, 3 f16). */
+sda_status sda_wire_round(void* stream, void* x, int32_t x_dtype, int64_t n, int32_t wire_fmt);
 
 /* ------------------------------------------------------------------------------------------
  * Wire frames on the device ("FATN", frame.hpp:48-92): encode a device tensor into the

@@ -36,7 +36,8 @@ EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_
            "sda_frame_elements", "sda_frame_payload_bytes", "sda_frame_bytes", "sda_frame_scratch_bytes",
            "sda_frame_encode", "sda_frame_parse_header", "sda_frame_decode", "sda_crc32",
            "sda_partial_attention_remote", "sda_scramble_batch_remote", "sda_partial_attention_ws",
-           "sda_prefill_workspace_bytes", "sda_set_spin_timeout_ns", "sda_spin_error")
+           "sda_prefill_workspace_bytes", "sda_set_spin_timeout_ns", "sda_spin_error",
+           "sda_wire_round", "sda_keyset_bytes_f64", "sda_pack_keyset_f64")
 
 
 class SdaError(RuntimeError):
@@ -104,6 +105,9 @@ def _load() -> ct.CDLL:
     lib.sda_keyset_bytes.restype = ct.c_size_t
     lib.sda_keyset_bytes.argtypes = [ct.c_uint32, ct.c_uint32]
     lib.sda_pack_keyset.argtypes = [ct.POINTER(HostKeysetC), ct.c_uint32, ct.c_uint32, _vp]
+    lib.sda_keyset_bytes_f64.restype = ct.c_size_t
+    lib.sda_keyset_bytes_f64.argtypes = [ct.c_uint32, ct.c_uint32]
+    lib.sda_pack_keyset_f64.argtypes = [ct.POINTER(HostKeysetC), ct.c_uint32, ct.c_uint32, _vp]
     lib.sda_scramble.argtypes = [_vp, ct.c_int32, ct.c_int32, _vp, ct.c_int32, ct.c_int64, ct.c_int32, ct.c_int64,
                                  ct.c_int32, _vp, ct.c_int64, ct.c_int32, _vp, ct.c_int64, _vp, ct.c_int32,
                                  ct.c_int64, ct.c_int64, ct.c_int64]
@@ -161,6 +165,7 @@ def _load() -> ct.CDLL:
     lib.sda_quantize_affine.argtypes = [_vp, _vp, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32, _vp, ct.c_int64,
                                         _vp, _vp, _vp, _vp]
     lib.sda_dequantize.argtypes = [_vp, _vp, ct.c_int64, _vp, _vp, ct.c_int64, ct.c_int64, ct.c_int32, _vp, ct.c_int32]
+    lib.sda_wire_round.argtypes = [_vp, _vp, ct.c_int32, ct.c_int64, ct.c_int32]
     lib.sda_quant_roundtrip.argtypes = [_vp, _vp, ct.c_int32, ct.c_int64, ct.c_int64, ct.c_int32, _vp, _vp]
     lib.sda_abi_version.restype = ct.c_int32
     lib.sda_status_string.restype = ct.c_char_p
@@ -257,6 +262,13 @@ class HostKeyset:
         out = np.zeros(int(LIB.sda_keyset_bytes(self.n_heads, self.head_dim)), np.uint8)
         c = self._c()
         check(LIB.sda_pack_keyset(ct.byref(c), self.n_heads, self.head_dim, out.ctypes.data), "pack_keyset")
+        return out
+
+    def pack_f64(self) -> np.ndarray:
+        """FP64-mode device image (sda_pack_keyset_f64), as a host uint8 array."""
+        out = np.zeros(int(LIB.sda_keyset_bytes_f64(self.n_heads, self.head_dim)), np.uint8)
+        c = self._c()
+        check(LIB.sda_pack_keyset_f64(ct.byref(c), self.n_heads, self.head_dim, out.ctypes.data), "pack_keyset_f64")
         return out
 
 

@@ -30,6 +30,9 @@ bool env_flag(const char* name) {
 }
 
 bool valid_dtype(int t) { return t == SDA_BF16 || t == SDA_F32; }
+// FP64 mode (f64_path.cu): every tensor of the call f64, or none
+bool valid_dtype_f64(int t) { return valid_dtype(t) || t == SDA_F64; }
+bool f64_pair_ok(int a, int b) { return (a == SDA_F64) == (b == SDA_F64); }
 
 sda_status from_cuda(cudaError_t e) {
     if (e == cudaSuccess) return SDA_OK;
@@ -71,7 +74,8 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys, const
     if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
     if (variant != SDA_PHI_FORWARD && variant != SDA_PHI_INV_T) return SDA_ERR_INVALID_ARGUMENT;
     if (which_keys != SDA_KEYS_KQ && which_keys != SDA_KEYS_V) return SDA_ERR_INVALID_ARGUMENT;
-    if (!x || !out || !keys || !valid_dtype(x_dtype) || !valid_dtype(out_dtype)) return SDA_ERR_INVALID_ARGUMENT;
+    if (!x || !out || !keys || !valid_dtype_f64(x_dtype) || !valid_dtype_f64(out_dtype) || !f64_pair_ok(x_dtype, out_dtype))
+        return SDA_ERR_INVALID_ARGUMENT;
     if (n_batch < 0 || n_heads <= 0 || key_heads <= 0 || n_heads % key_heads != 0 || rows < 0)
         return SDA_ERR_INVALID_ARGUMENT;
     if (out_row_offset < 0 || out_row_offset + rows > out_rows_cap || x_batch_mod < 0) return SDA_ERR_INVALID_ARGUMENT;
@@ -80,6 +84,8 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys, const
     sda::K1Params p{x, out, keys, perm, keys_batch_stride, perm_batch_stride, rows, out_rows_cap, out_row_offset,
                     n_heads, key_heads, which_keys, variant == SDA_PHI_INV_T ? 1 : 0, x_batch_mod};
     ++g_launches;
+    if (x_dtype == SDA_F64)
+        return from_cuda(sda::launch_f64_path(1, &p, head_dim, n_batch, static_cast<cudaStream_t>(stream)));
     if (sda::k1_tc_eligible(p, head_dim, x_dtype, out_dtype) && !env_flag("SDA_K1_SIMT"))
         return from_cuda(sda::launch_k1_tc(p, head_dim, n_batch, static_cast<cudaStream_t>(stream)));
     return from_cuda(sda::launch_k1(p, head_dim, x_dtype, out_dtype, n_batch, static_cast<cudaStream_t>(stream)));
@@ -101,7 +107,8 @@ static sda_status scramble_batch_impl(void* stream, int32_t head_dim, const sda_
         const sda_scramble_job& j = jobs[i];
         if (j.variant != SDA_PHI_FORWARD && j.variant != SDA_PHI_INV_T) return SDA_ERR_INVALID_ARGUMENT;
         if (j.which_keys != SDA_KEYS_KQ && j.which_keys != SDA_KEYS_V) return SDA_ERR_INVALID_ARGUMENT;
-        if (!j.x || !j.out || !j.keys || !valid_dtype(j.x_dtype) || !valid_dtype(j.out_dtype))
+        if (!j.x || !j.out || !j.keys || !valid_dtype_f64(j.x_dtype) || !valid_dtype_f64(j.out_dtype) ||
+            !f64_pair_ok(j.x_dtype, j.out_dtype))
             return SDA_ERR_INVALID_ARGUMENT;
         if (j.n_batch < 0 || j.n_heads <= 0 || j.key_heads <= 0 || j.n_heads % j.key_heads != 0 || j.rows < 0)
             return SDA_ERR_INVALID_ARGUMENT;
@@ -194,6 +201,15 @@ sda_status sda_quant_roundtrip(void* stream, void* x, int32_t dtype, int64_t n_t
     return from_cuda(sda::launch_quant_roundtrip(x, dtype, n_tensors, count, bits,
                                                  reinterpret_cast<unsigned long long*>(scratch), err,
                                                  static_cast<cudaStream_t>(stream)));
+}
+
+sda_status sda_wire_round(void* stream, void* x, int32_t x_dtype, int64_t n, int32_t wire_fmt) {
+    if (n < 0 || (x_dtype != SDA_F32 && x_dtype != SDA_F64) || wire_fmt < 0 || wire_fmt > 3)
+        return SDA_ERR_INVALID_ARGUMENT;
+    if (n == 0 || wire_fmt == 0) return SDA_OK;
+    if (!x) return SDA_ERR_INVALID_ARGUMENT;
+    ++g_launches;
+    return from_cuda(sda::launch_wire_round(x, x_dtype, n, wire_fmt, static_cast<cudaStream_t>(stream)));
 }
 
 // ------------------------------------------------------------------------------------------ frames
@@ -453,7 +469,8 @@ sda_status sda_partial_attention_ws(void* stream, const void* q, int32_t q_dtype
                                     size_t workspace_bytes) {
     if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
     if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
-    if (!q || !k || !v || !out_o || !out_stats || !valid_dtype(q_dtype) || !valid_dtype(kv_dtype))
+    if (!q || !k || !v || !out_o || !out_stats || !valid_dtype_f64(q_dtype) || !valid_dtype_f64(kv_dtype) ||
+        !f64_pair_ok(q_dtype, kv_dtype))
         return SDA_ERR_INVALID_ARGUMENT;
     if (n_batch < 0 || q_rows < 0 || kv_cap < 0 || q_heads <= 0 || kv_heads <= 0 || q_heads % kv_heads != 0 ||
         n_splits <= 0)
@@ -462,6 +479,10 @@ sda_status sda_partial_attention_ws(void* stream, const void* q, int32_t q_dtype
     if (n_batch == 0 || q_rows == 0) return SDA_OK;
     sda::K2Params p{q, k, v, kv_len, out_o, out_stats, kv_cap, n_batch, q_rows, q_heads, kv_heads, n_splits,
                     (float)(1.0 / std::sqrt((double)head_dim)), 0, 0};
+    if (q_dtype == SDA_F64) {
+        ++g_launches;
+        return from_cuda(sda::launch_f64_path(2, &p, head_dim, n_batch, static_cast<cudaStream_t>(stream)));
+    }
     p.sk_work = workspace;
     p.sk_work_bytes = workspace ? workspace_bytes : 0;
     ++g_launches;
@@ -479,7 +500,8 @@ sda_status sda_partial_attention_causal(void* stream, const void* q, int32_t q_d
                                         int32_t n_splits, int64_t causal_offset, float* out_o, float* out_stats) {
     if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
     if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
-    if (!q || !k || !v || !out_o || !out_stats || !valid_dtype(q_dtype) || !valid_dtype(kv_dtype))
+    if (!q || !k || !v || !out_o || !out_stats || !valid_dtype_f64(q_dtype) || !valid_dtype_f64(kv_dtype) ||
+        !f64_pair_ok(q_dtype, kv_dtype))
         return SDA_ERR_INVALID_ARGUMENT;
     if (n_batch < 0 || q_rows < 0 || kv_cap < 0 || q_heads <= 0 || kv_heads <= 0 || q_heads % kv_heads != 0 ||
         n_splits <= 0)
@@ -489,6 +511,8 @@ sda_status sda_partial_attention_causal(void* stream, const void* q, int32_t q_d
     sda::K2Params p{q, k, v, kv_len, out_o, out_stats, kv_cap, n_batch, q_rows, q_heads, kv_heads, n_splits,
                     (float)(1.0 / std::sqrt((double)head_dim)), 1, causal_offset};
     ++g_launches;
+    if (q_dtype == SDA_F64)
+        return from_cuda(sda::launch_f64_path(2, &p, head_dim, n_batch, static_cast<cudaStream_t>(stream)));
     return from_cuda(sda::launch_k2_decode(p, head_dim, q_dtype, kv_dtype, static_cast<cudaStream_t>(stream)));
 }
 
@@ -634,7 +658,7 @@ sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, i
     if (n_sources > SDA_MAX_SOURCES || !sources) return SDA_ERR_INVALID_ARGUMENT;
     if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
     if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
-    if (!out || !valid_dtype(out_dtype) || n_batch < 0 || q_rows < 0 || q_heads <= 0) return SDA_ERR_INVALID_ARGUMENT;
+    if (!out || !valid_dtype_f64(out_dtype) || n_batch < 0 || q_rows < 0 || q_heads <= 0) return SDA_ERR_INVALID_ARGUMENT;
     bool any_keys = false;
     for (int i = 0; i < n_sources; ++i) {
         if (!sources[i].o || !sources[i].stats) return SDA_ERR_INVALID_ARGUMENT;
@@ -658,6 +682,8 @@ sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, i
     p.err = err_flag;
     p.out_bstride = out_batch_stride;
     ++g_launches;
+    if (out_dtype == SDA_F64)   // FP64 mode: f64 sources and stats, f64 key images
+        return from_cuda(sda::launch_f64_path(3, &p, head_dim, n_batch, static_cast<cudaStream_t>(stream)));
     return from_cuda(sda::launch_k3(p, head_dim, out_dtype, static_cast<cudaStream_t>(stream)));
 }
 

@@ -382,6 +382,28 @@ cudaError_t launch_frame_encode(const void* x, int x_dt, int64_t count, int wire
                       st);
 }
 
+// x <- round_to_format(x, fmt) in place (float_format.cpp:26-58; the float-format wire_round of
+// model.cpp:339-348 / protocol.cpp:179): fmt 0 f64 (no-op), 1 f32, 2 bf16, 3 f16
+template <typename T>
+__global__ void __launch_bounds__(256) wire_round_kernel(T* x, int64_t n, int fmt) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = (double)x[i];
+        double y;
+        if (fmt == 1) y = (double)(float)v;
+        else if (fmt == 2) y = round_spec(v, 7, -126, 0x1.FEp127);
+        else y = round_spec(v, 10, -14, 65504.0);
+        x[i] = (T)y;
+    }
+}
+
+cudaError_t launch_wire_round(void* x, int dt, int64_t n, int fmt, cudaStream_t st) {
+    if (fmt == 0 || n == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)device_sms() * 8));
+    if (dt == SDA_F32) wire_round_kernel<float><<<blocks, 256, 0, st>>>(static_cast<float*>(x), n, fmt);
+    else wire_round_kernel<double><<<blocks, 256, 0, st>>>(static_cast<double*>(x), n, fmt);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_frame_decode(const uint8_t* frame, int hlen, uint64_t payload_bytes, int64_t count, int wire,
                                 void* out, int out_dt, uint32_t* crc_scratch, float* q_sz, int32_t* err,
                                 cudaStream_t st) {

@@ -99,6 +99,22 @@ static void pack_scrambler(size_t d, const double* s1, const uint32_t* p1, const
     }
 }
 
+// FP64 mode scrambler (SDA_SCRAMBLER_BYTES_F64(d) bytes): f64 [2][d] = {s1, s2}, then the u16
+// tables of pack_scrambler -- the raw factors, so the device repeats the reference's f64 ops
+static void pack_scrambler_f64(size_t d, const double* s1, const uint32_t* p1, const uint32_t* p2,
+                               const double* s2, uint8_t* dst) {
+    double* f = reinterpret_cast<double*>(dst);
+    uint16_t* u = reinterpret_cast<uint16_t*>(dst + 16 * d);
+    for (size_t i = 0; i < d; ++i) {
+        f[i] = s1[i];
+        f[d + i] = s2[i];
+        u[kP1 * d + i] = static_cast<uint16_t>(p1[i]);
+        u[kP2 * d + i] = static_cast<uint16_t>(p2[i]);
+        u[kP1Inv * d + p1[i]] = static_cast<uint16_t>(i);
+        u[kP2Inv * d + p2[i]] = static_cast<uint16_t>(i);
+    }
+}
+
 static bool pow2(uint64_t n) { return n != 0 && (n & (n - 1)) == 0; }
 
 }  // namespace sda
@@ -176,6 +192,25 @@ sda_status sda_pack_keyset(const sda_host_keyset* ks, uint32_t n_heads, uint32_t
         sda::pack_scrambler(d, ks->kq_s1 + h * d, ks->kq_p1 + h * d, ks->kq_p2 + h * d, ks->kq_s2 + h * d, head);
         sda::pack_scrambler(d, ks->v_s1 + h * d, ks->v_p1 + h * d, ks->v_p2 + h * d, ks->v_s2 + h * d,
                             head + SDA_SCRAMBLER_BYTES(d));
+    }
+    return SDA_OK;
+}
+
+size_t sda_keyset_bytes_f64(uint32_t n_heads, uint32_t head_dim) {
+    return static_cast<size_t>(n_heads) * SDA_KEYSET_HEAD_BYTES_F64(head_dim);
+}
+
+sda_status sda_pack_keyset_f64(const sda_host_keyset* ks, uint32_t n_heads, uint32_t head_dim, void* out) {
+    if (!ks || !out) return SDA_ERR_INVALID_ARGUMENT;
+    if (!sda::pow2(head_dim)) return SDA_ERR_NOT_POW2;
+    if (head_dim > 65536) return SDA_ERR_UNSUPPORTED;
+    const size_t d = head_dim;
+    uint8_t* dst = static_cast<uint8_t*>(out);
+    for (uint32_t h = 0; h < n_heads; ++h) {
+        uint8_t* head = dst + h * SDA_KEYSET_HEAD_BYTES_F64(d);
+        sda::pack_scrambler_f64(d, ks->kq_s1 + h * d, ks->kq_p1 + h * d, ks->kq_p2 + h * d, ks->kq_s2 + h * d, head);
+        sda::pack_scrambler_f64(d, ks->v_s1 + h * d, ks->v_p1 + h * d, ks->v_p2 + h * d, ks->v_s2 + h * d,
+                                head + SDA_SCRAMBLER_BYTES_F64(d));
     }
     return SDA_OK;
 }

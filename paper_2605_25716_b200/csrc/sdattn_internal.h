@@ -133,6 +133,7 @@ cudaError_t launch_frame_encode(const void* x, int x_dt, int64_t count, int wire
 cudaError_t launch_frame_decode(const uint8_t* frame, int hlen, uint64_t payload_bytes, int64_t count, int wire,
                                 void* out, int out_dt, uint32_t* crc_scratch, float* q_sz, int32_t* err,
                                 cudaStream_t st);
+cudaError_t launch_wire_round(void* x, int dt, int64_t n, int fmt, cudaStream_t st);
 cudaError_t launch_quant_roundtrip(void* x, int dt, int64_t n, int64_t count, int bits, unsigned long long* scratch,
                                    int32_t* err, cudaStream_t st);
 cudaError_t launch_k1_tc_multi(const K1Params* p, const int64_t* n_batch, int n_jobs, int d, cudaStream_t st,
@@ -146,6 +147,8 @@ size_t k2_prefill_sk_workspace_bytes(const K2Params& p);
 bool k2_gqa_tc_eligible(const K2Params& p, int d, int qdt, int kvdt);
 cudaError_t launch_k2_gqa_tc(const K2Params& p, cudaStream_t st);
 cudaError_t launch_k3(const K3Params& p, int d, int odt, cudaStream_t st);
+// FP64 mode (f64_path.cu): which 1 = K1 (K1Params), 2 = K2 (K2Params), 3 = K3 (K3Params)
+cudaError_t launch_f64_path(int which, const void* params, int d, int64_t n_batch, cudaStream_t st);
 // per-TU spin budget / error word (common.cuh SDA_SPIN_ACCESSOR)
 cudaError_t spin_access_exchange(const unsigned long long* set, int* err, int clear);
 cudaError_t spin_access_k2_decode(const unsigned long long* set, int* err, int clear);

@@ -19,13 +19,15 @@ import torch
 from . import capi
 from .capi import check
 
-_DT = {torch.bfloat16: capi.SDA_BF16, torch.float32: capi.SDA_F32}
-_DT_Q = {**_DT, torch.float64: capi.SDA_F64}   # f64: quantised-wire entry points only
+_DT = {torch.bfloat16: capi.SDA_BF16, torch.float32: capi.SDA_F32, torch.float64: capi.SDA_F64}
+_DT_Q = _DT   # the quantised-wire / frame entry points take the same three
 
 
 def _dtype_code(t: torch.Tensor) -> int:
+    """bf16 / f32, or f64 for the FP64 mode (the reference's arithmetic on the device: f64 key
+    images, f64 partials and stats)."""
     if t.dtype not in _DT:
-        raise TypeError(f"unsupported dtype {t.dtype} (bf16 or f32)")
+        raise TypeError(f"unsupported dtype {t.dtype} (bf16, f32 or f64)")
     return _DT[t.dtype]
 
 
@@ -131,10 +133,11 @@ def partial_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, kv_len:
     if k.dtype != v.dtype or k.shape != v.shape:
         raise ValueError("k and v must have the same shape and dtype")
     S = n_splits or capi.default_splits(B, Hq, Lq, cap, kv_heads=Hkv, head_dim=d)
+    pdt = torch.float64 if q.dtype == torch.float64 else torch.float32   # partials: f64 in the FP64 mode
     if out_o is None:
-        out_o = torch.empty((S, B, Hq, Lq, d), dtype=torch.float32, device=q.device)
+        out_o = torch.empty((S, B, Hq, Lq, d), dtype=pdt, device=q.device)
     if out_stats is None:
-        out_stats = torch.empty((S, B, Hq, Lq, 2), dtype=torch.float32, device=q.device)
+        out_stats = torch.empty((S, B, Hq, Lq, 2), dtype=pdt, device=q.device)
     if kv_len is not None:
         _cuda(kv_len, "kv_len")
         if kv_len.dtype != torch.int32:
@@ -179,8 +182,9 @@ def partial_attention_causal(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, 
     _cuda(q, "q"), _cuda(k, "k"), _cuda(v, "v")
     B, Hq, Lq, d = q.shape
     Hkv, cap = k.shape[1], k.shape[2]
-    out_o = torch.empty((n_splits, B, Hq, Lq, d), dtype=torch.float32, device=q.device)
-    out_stats = torch.empty((n_splits, B, Hq, Lq, 2), dtype=torch.float32, device=q.device)
+    pdt = torch.float64 if q.dtype == torch.float64 else torch.float32
+    out_o = torch.empty((n_splits, B, Hq, Lq, d), dtype=pdt, device=q.device)
+    out_stats = torch.empty((n_splits, B, Hq, Lq, 2), dtype=pdt, device=q.device)
     check(capi.LIB.sda_partial_attention_causal(_stream(stream), q.data_ptr(), _dtype_code(q), k.data_ptr(),
                                                 v.data_ptr(), _dtype_code(k), cap, _ptr(kv_len), B, Hq, Hkv, Lq, d,
                                                 n_splits, causal_offset, out_o.data_ptr(), out_stats.data_ptr()),
@@ -272,6 +276,17 @@ def dequantize(codes: torch.Tensor, scale: torch.Tensor, zero_point: torch.Tenso
                                   zero_point.data_ptr(), n, count, bits, out.data_ptr(), _DT_Q[out_dtype]),
           "sda_dequantize")
     return out
+
+
+def wire_round(x: torch.Tensor, wire_fmt: int, stream=None) -> torch.Tensor:
+    """In place: x <- round_to_format(x, wire_fmt) (float_format.cpp:26-58; wire_fmt 0 f64, 1 f32,
+    2 bf16, 3 f16), the float-format wire_round of model.cpp:339-348. x: contiguous f32 / f64."""
+    _cuda(x, "x")
+    if x.dtype not in (torch.float32, torch.float64):
+        raise ValueError("x must be f32 or f64")
+    check(capi.LIB.sda_wire_round(_stream(stream), x.data_ptr(), _DT_Q[x.dtype], x.numel(), wire_fmt),
+          "sda_wire_round")
+    return x
 
 
 def quant_roundtrip(x: torch.Tensor, bits: int, err: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:

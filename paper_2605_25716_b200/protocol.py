@@ -34,7 +34,9 @@ class DomainKeys:
 
     def __init__(self, request_ids: Sequence[int], layer: int, domain: int, kv_heads: int, head_dim: int,
                  device, master_seed: int = 1, mag_lo: float = 0.125, mag_hi: float = 8.0,
-                 mode: int = capi.MODE_S1_AND_S2, shared_seeds: Optional[Sequence[int]] = None):
+                 mode: int = capi.MODE_S1_AND_S2, shared_seeds: Optional[Sequence[int]] = None,
+                 fp64: bool = False):
+        """fp64: upload the FP64-mode key image (for f64 activations / shards) instead of the f32 one."""
         self.request_ids = list(request_ids)
         self.layer, self.domain = layer, domain
         self.kv_heads, self.head_dim = kv_heads, head_dim
@@ -42,7 +44,8 @@ class DomainKeys:
         seeds = shared_seeds if shared_seeds is not None else [capi.shared_seed(master_seed, r) for r in request_ids]
         self.host = [capi.negotiate_keyset(s, r, layer, domain, kv_heads, head_dim, mag_lo, mag_hi, mode)
                      for s, r in zip(seeds, self.request_ids)]
-        self.dev = ops.upload_keys([ks.pack() for ks in self.host], self.device)
+        self.fp64 = fp64
+        self.dev = ops.upload_keys([ks.pack_f64() if fp64 else ks.pack() for ks in self.host], self.device)
 
     @property
     def batch(self) -> int:

@@ -8,7 +8,26 @@ import torch
 from oracle import C, FMT_BF16, FMT_F32, max_abs_rel, rel_fro
 from paper_2605_25716_b200 import protocol
 
-__all__ = ["gauss", "dev", "Case", "max_abs_rel", "rel_fro", "FMT_BF16", "FMT_F32"]
+__all__ = ["gauss", "dev", "Case", "max_abs_rel", "rel_fro", "FMT_BF16", "FMT_F32", "assert_lse", "LSE_TOL"]
+
+# SURVEY 8(d) metric 4: LSE = row_max + ln(exp_sum) against the rounding-matched oracle (both
+# sides see identical bf16 / f32 Q', K', V', so only the accumulation order differs)
+LSE_TOL = {"bf16": 1e-3, "f32": 1e-5}
+
+
+def assert_lse(st, rm, rs, tol, what=""):
+    """st [..., 2] = device (row_max, exp_sum); rm, rs = the oracle's. Masked rows (exp_sum 0)
+    must be masked on both sides; elsewhere |LSE_dev - LSE_ref| <= tol (absolute, natural log)."""
+    st = np.asarray(st, np.float64)
+    rm, rs = np.asarray(rm, np.float64), np.asarray(rs, np.float64)
+    dead = rs == 0
+    assert np.array_equal(st[..., 1] == 0, dead), ("masked rows differ", what)
+    live = ~dead
+    if live.any():
+        got = st[..., 0][live] + np.log(st[..., 1][live])
+        ref = rm[live] + np.log(rs[live])
+        err = float(np.abs(got - ref).max())
+        assert err <= tol, (f"LSE off by {err:.3e} > {tol:.0e}", what)
 
 
 def gauss(seed: int, shape) -> np.ndarray:
@@ -29,7 +48,7 @@ class Case:
                  q_scale=1.0, kv_lens=None, mag=(0.125, 8.0), mode=0):
         self.B, self.Hq, self.Hkv, self.d, self.lk, self.n, self.lq = B, Hq, Hkv, d, lk, n_nodes, lq
         self.dtype = dtype
-        self.fmt = FMT_BF16 if dtype == torch.bfloat16 else FMT_F32
+        self.fmt = {torch.bfloat16: FMT_BF16, torch.float32: FMT_F32, torch.float64: 0}[dtype]
         self.master = master_seed
         self.mag, self.mode = mag, mode
         self.kv_lens = kv_lens  # optional per-node list of per-request lengths (<= lk)
@@ -47,7 +66,7 @@ class Case:
         domains = []
         for i in range(self.n):
             keys = protocol.DomainKeys(self.request_ids(), 0, i + 1, self.Hkv, self.d, "cuda", self.master,
-                                       self.mag[0], self.mag[1], self.mode)
+                                       self.mag[0], self.mag[1], self.mode, fp64=self.dtype == torch.float64)
             shard = protocol.KVShard(self.B, self.Hkv, self.lk, self.d, "cuda", self.dtype)
             shard.ship_segment(dev(self.k[i], self.dtype), dev(self.v[i], self.dtype), keys, first_pos=i * self.lk)
             domains.append((keys, shard))
@@ -60,7 +79,7 @@ class Case:
                 q_s, pinv = keys.scramble_q(q, self.q_first_pos, out_dtype=shard.k.dtype)
                 o, st = shard.serve(q_s, n_splits=n_splits)
                 bad = protocol.DomainKeys(self.request_ids(), 0, keys.domain, self.Hkv, self.d, "cuda",
-                                          self.master ^ 0xDEADBEEF)  # protocol.cpp:232-243 sabotage
+                                          self.master ^ 0xDEADBEEF, fp64=self.dtype == torch.float64)  # protocol.cpp:232-243 sabotage
                 partials.append((o, st, bad, pinv))
             out = protocol.finish(partials, out_dtype=out_dtype, kv_heads=self.Hkv)
         torch.cuda.synchronize()

@@ -102,7 +102,7 @@ def test_ll_decode_emulated_world_graph_and_f32_wire():
         g.replay()
         torch.cuda.synchronize()
         w.check(outs)
-    assert int(ranks[1].epoch.item()) == 1 + 1 + 1 + 3
+    assert int(ranks[1].epoch.item()) == 1 + 1 + 3   # start 1, one eager step, 3 replays
 
 
 def test_ll_decode_emulated_world_gqa():

@@ -9,6 +9,7 @@ import torch
 
 from oracle import C, REF, OracleError
 from paper_2605_25716_b200 import capi, ops
+from tests.gpu_helpers import gauss
 
 pytestmark = pytest.mark.gpu
 
@@ -69,3 +70,23 @@ def test_frame_corruption_and_malformed_headers():
     for blob, size in ((b"FATX" + bytes(ref[4:64]), ref.size), (bytes(ref[:64]), ref.size - 1), (bytes(ref[:20]), 20)):
         with pytest.raises(capi.SdaError):
             ops.frame_parse_header(blob, size)
+
+
+@pytest.mark.parametrize("fmt", [1, 2, 3])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_wire_round_matches_round_to_format(fmt, dtype):
+    """sda_wire_round == the reference's round_to_format (float_format.cpp:26-58) element for
+    element: ties, subnormals, overflow and +-inf clamped to +-max_finite, signed zeros."""
+    from oracle import REF
+    o = REF or C
+    x = np.concatenate([gauss(7, (4096,)) * 10.0 ** np.linspace(-40, 40, 4096),
+                        [0.0, -0.0, np.inf, -np.inf, 3.4e38, -3.3e38, 1.0 + 2.0**-8, 1.0 + 3 * 2.0**-8,
+                         65504.0, 65520.0, 1e-45, 2.0**-130, 1.00390625, 5.960464477539063e-08]])
+    x = x.astype(np.float32).astype(np.float64) if dtype == torch.float32 else x
+    t = torch.from_numpy(x.copy()).to("cuda").to(dtype)
+    ops.wire_round(t, fmt)
+    got = t.double().cpu().numpy()
+    ref = o.round_to_format(x, fmt)
+    if dtype == torch.float32:
+        ref = ref.astype(np.float32).astype(np.float64)
+    assert np.array_equal(got, ref) and np.array_equal(np.signbit(got), np.signbit(ref))
