@@ -33,6 +33,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -64,10 +65,28 @@ void ckc(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Device buffers come from a per-size free list: these operators are called once per (layer, head,
+// segment) with tiny operands, and cudaMalloc / cudaFree (which synchronises) per call would
+// dominate. Calls are serialised on the legacy default stream, so a buffer released after its
+// result was read back is free for the next call.
+std::map<size_t, std::vector<void*>>& pool() {
+    static std::map<size_t, std::vector<void*>> p;
+    return p;
+}
+
 struct Dev {
     void* p = nullptr;
-    explicit Dev(size_t bytes) { ckc(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc"); }
-    ~Dev() { cudaFree(p); }
+    size_t n = 0;
+    explicit Dev(size_t bytes) : n(((bytes ? bytes : 16) + 255) / 256 * 256) {
+        auto& fl = pool()[n];
+        if (!fl.empty()) {
+            p = fl.back();
+            fl.pop_back();
+        } else {
+            ckc(cudaMalloc(&p, n), "cudaMalloc");
+        }
+    }
+    ~Dev() { pool()[n].push_back(p); }
     Dev(const Dev&) = delete;
     Dev& operator=(const Dev&) = delete;
     template <class T>

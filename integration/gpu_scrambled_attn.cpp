@@ -96,8 +96,8 @@ sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt) {
     auto keys = std::make_shared<std::map<std::pair<size_t, size_t>, HeadKeys>>();
     return [opt, dt, esz, keys, qbits](const sdattn::AttnRequest& req) -> sdattn::Matrix {
         const size_t d = req.q->cols, lq = req.q->rows, lk = req.k->rows;
-        if (d != 32 && d != 64 && d != 128 && d != 256)
-            throw std::invalid_argument("gpu_scrambled_attn: head dim must be 32, 64, 128 or 256");
+        if (d < 4 || d > 256 || (d & (d - 1)))
+            throw std::invalid_argument("gpu_scrambled_attn: head dim must be a power of two in [4, 256]");
         auto it = keys->find({req.layer, req.head});
         if (it == keys->end()) it = keys->emplace(std::make_pair(req.layer, req.head), derive_head(opt, req.layer, req.head, d)).first;
         const HeadKeys& hk = it->second;
@@ -143,7 +143,11 @@ sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt) {
             ck(sda_partial_attention(st, q_s.p, dt, ks->p, vs->p, dt, (int64_t)L, nullptr, 1, 1, 1, (int64_t)lq, (int)d, 1,
                                      o->as<float>(), s->as<float>()),
                "partial attention");
-            wire(o->p, lq * d);   // O' of the shard (one split); stats stay f32
+            wire(o->p, lq * d);   // O' of the shard (one split)
+            if (dt == SDA_BF16) {    // wire_round of O' and wire_round_stat of the stats (model.cpp:392-394)
+                ck(sda_wire_round(st, o->p, SDA_F32, (int64_t)(lq * d), 2), "wire_round O'");
+                ck(sda_wire_round(st, s->p, SDA_F32, (int64_t)(lq * 2), 2), "wire_round stats");
+            }
             src.push_back({o->as<float>(), s->as<float>(), hk.image->p, pq_inv_d->as<uint32_t>(), 0});
             keep.push_back(std::move(ks));
             keep.push_back(std::move(vs));

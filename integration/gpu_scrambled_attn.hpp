@@ -14,9 +14,10 @@
 namespace sdattn_b200 {
 
 // wire_fmt f64 or f32 -> FP32 device mode (Q'/K'/V' kept in f32); bf16 -> BF16 device mode
-// (Q'/K'/V' rounded once to bf16; O' and the stats stay f32, tighter than the reference's
-// wire_round of O' and stats). f16 and quantised wires (quant_bits > 0) are not supported and
-// throw std::invalid_argument, as do head dims outside {32, 64, 128, 256}.
+// (Q'/K'/V' rounded once to bf16, O' and the stats rounded to the bf16 grid as the reference's
+// wire_round / wire_round_stat do, sda_wire_round); quant_bits in [2, 8] -> Q', K', V', O'
+// quantised per tensor on the device (sda_quant_roundtrip), stats at f32. f16 wires throw
+// std::invalid_argument, as do head dims outside {4, 8, ..., 256}.
 sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt);
 
 }  // namespace sdattn_b200

@@ -1,8 +1,8 @@
 // test_model_gpu.cpp -- the reference's own provider-equivalence and greedy-decode tests
 // (proj/tests/test_model.cpp:90-129) run against the B200 path through gpu_scrambled_attn.
 // Built by integration/Makefile against the reference's sources (oracle/_ref) -- test
-// infrastructure; run on a GPU box by tests/test_gpu_adapter.py. The model uses head_dim 32
-// (the device kernels support d in {32, 64, 128, 256}; the reference test's toy model uses 16).
+// infrastructure; run on a GPU box by tests/test_gpu_adapter.py. head_dim 16 is the reference
+// test's own toy model (test_model.cpp:14-23: d_model 64, 4 heads); 32 and 64 as well.
 #include <cmath>
 #include <cstdio>
 #include <vector>
@@ -16,6 +16,12 @@ using namespace sdattn;
 namespace {
 
 int failures = 0;
+
+double max_abs(const Matrix& m) {
+    double a = 0.0;
+    for (double v : m.data) a = std::max(a, std::abs(v));
+    return a;
+}
 
 void check(bool ok, const char* what, double val = 0.0) {
     std::printf("%-72s %s (%.3g)\n", what, ok ? "PASS" : "FAIL", val);
@@ -42,7 +48,7 @@ std::vector<int> random_ids(std::size_t n, std::size_t vocab, RngStream& rng) {
 }  // namespace
 
 int main() {
-    for (std::size_t hd : {32u, 64u}) {
+    for (std::size_t hd : {16u, 32u, 64u}) {
         std::printf("--- head_dim %zu\n", hd);
         // test_model.cpp:90-110 -- providers agree across a cache split
         const Model m = init_model(decoder(9, hd));
@@ -65,8 +71,10 @@ int main() {
         bopt.wire_fmt = FloatFormat::bf16;
         const Matrix gpu_b = run(sdattn_b200::gpu_scrambled_attn(bopt));
         const Matrix ref_b = run(scrambled_attn(bopt));   // the reference's own bf16-wire emulation
-        const double dev_b = max_abs_diff(gpu_b, ref_b) / std::max(1e-12, frobenius_norm(ref_b) / std::sqrt((double)ref_b.data.size()));
-        check(dev_b < 0.5, "gpu (BF16 mode) vs reference scrambled_attn(bf16 wire), max|diff|/rms", dev_b);
+        // O' and the stats are wire-rounded like the reference's (sda_wire_round): what is left is
+        // f32 vs f64 accumulation ahead of the same bf16 roundings -- the BF16-mode bar, 2e-2
+        const double dev_b = max_abs_diff(gpu_b, ref_b) / std::max(1e-12, max_abs(ref_b));
+        check(dev_b < 2e-2, "gpu (BF16 mode) vs reference scrambled_attn(bf16 wire), max|diff|/max|ref|", dev_b);
         // quantised wire (8 and 4 bits): Q', K', V', O' quantised per tensor on the device
         for (int qb : {8, 4}) {
             ScrambledAttnOptions qopt;

@@ -513,6 +513,10 @@ sda_status sda_partial_attention_causal(void* stream, const void* q, int32_t q_d
     ++g_launches;
     if (q_dtype == SDA_F64)
         return from_cuda(sda::launch_f64_path(2, &p, head_dim, n_batch, static_cast<cudaStream_t>(stream)));
+    // prefill-sized spans (bf16, d 128, >= 64 rows): the tensor-core kernel with per-row key limits
+    if (q_rows >= 64 && sda::k2_prefill_tc_eligible(p, head_dim, q_dtype, kv_dtype) &&
+        !sda::k2_gqa_tc_eligible(p, head_dim, q_dtype, kv_dtype) && !env_flag("SDA_K2_SIMT"))
+        return from_cuda(sda::launch_k2_prefill_tc(p, static_cast<cudaStream_t>(stream)));
     return from_cuda(sda::launch_k2_decode(p, head_dim, q_dtype, kv_dtype, static_cast<cudaStream_t>(stream)));
 }
 

@@ -255,11 +255,13 @@ __device__ __forceinline__ void fwht_group(float* v, int lane) {
     }
 #pragma unroll
     for (int m = 1; m < LPR; m <<= 1) {
-        const bool upper = (lane & m) != 0;
+        // lower lane: v + o, upper lane: o - v -- one FFMA with sign +-1 (exact: the product by
+        // +-1 is exact and the FMA rounds once, as the add / subtract does)
+        const float sgn = (lane & m) ? -1.f : 1.f;
 #pragma unroll
         for (int i = 0; i < E; ++i) {
             const float o = __shfl_xor_sync(0xffffffffu, v[i], m);
-            v[i] = upper ? (o - v[i]) : (v[i] + o);
+            v[i] = fmaf(sgn, v[i], o);
         }
     }
 }

@@ -40,6 +40,11 @@ struct K2TcParams {
     int kv_heads;
     int n_splits;
     int n_qpairs;          // ceil(Lq / 256) (normal mode)
+    // causal (the inquirer's local span, AttentionMask::causal(offset), attention.hpp:25-27; split
+    // mode, normal tiles only): key j is visible to span row i iff j <= i + causal_offset. The grid
+    // is then x = q head, y = Q-tile pair from the last (longest key range first)
+    int causal;
+    int64_t causal_offset;
     int grouped;           // 1: GQA decode mode, one CTA per (request, kv head): its G = Hq/Hkv
                            //    q heads x Lq rows (contiguous in Q) form the Q tile
     float scale_log2;      // log2(e) / sqrt(d)
@@ -183,14 +188,20 @@ __device__ __forceinline__ void split_seg(const K2TcParams& p, Seg& s) {
     const int64_t b = blockIdx.z / p.n_splits;
     const int split = blockIdx.z % p.n_splits;
     const int G = p.q_heads / p.kv_heads;
+    const int head = p.causal ? (int)blockIdx.x : (int)blockIdx.y;
+    const int qp = p.causal ? p.n_qpairs - 1 - (int)blockIdx.y : (int)blockIdx.x;
     s.b = (int)b;
     s.split = split;
-    s.kvh = p.grouped ? (int)blockIdx.y : (int)blockIdx.y / G;
+    s.kvh = p.grouped ? head : head / G;
     s.head_row = p.grouped ? (b * p.q_heads + (int64_t)s.kvh * G) * p.q_rows
-                           : (b * p.q_heads + blockIdx.y) * p.q_rows + (int64_t)blockIdx.x * 2 * TILE;
-    s.nrows = (int)(p.grouped ? (int64_t)G * p.q_rows : min((int64_t)2 * TILE, p.q_rows - (int64_t)blockIdx.x * 2 * TILE));
+                           : (b * p.q_heads + head) * p.q_rows + (int64_t)qp * 2 * TILE;
+    s.nrows = (int)(p.grouped ? (int64_t)G * p.q_rows : min((int64_t)2 * TILE, p.q_rows - (int64_t)qp * 2 * TILE));
     s.two = s.nrows > TILE;
     s.len = len_of(p, b);
+    if (p.causal) {   // the pair's last row sees keys < its index + offset + 1: the tiles past are skipped
+        const int64_t lim = (int64_t)qp * 2 * TILE + s.nrows + p.causal_offset;
+        s.len = (int)max((int64_t)0, min((int64_t)s.len, lim));
+    }
     // split ranges aligned to whole 128-key tiles
     const int ntile_all = (s.len + TILE - 1) / TILE;
     const int tps = (ntile_all + p.n_splits - 1) / p.n_splits;
@@ -577,7 +588,12 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             const bool group_live = g == 0 || sg0.two;
             // warps whose 32 rows are all past the unit's rows only keep the barrier protocol going
             const bool warp_live = g * TILE + (warp & 3) * 32 < sg0.nrows;
-            const int kv_left = sg0.len - sg0.t0 * TILE;             // keys from the segment's first tile
+            int kv_left = sg0.len - sg0.t0 * TILE;                   // keys from the segment's first tile
+            if (p.causal) {   // this thread's row: keys <= its span index + offset (and < kv_len)
+                const int64_t qrow = sg0.head_row % p.q_rows + (int64_t)g * TILE + row;
+                const int64_t lim = min((int64_t)len_of(p, sg0.b), qrow + p.causal_offset + 1);
+                kv_left = (int)max((int64_t)-TILE, lim - (int64_t)sg0.t0 * TILE);
+            }
             if (lane == 0) keep->seg = sg0;
             __syncwarp();
             float m_run = -INFINITY, m_use = -INFINITY, l = 0.f;
@@ -1127,6 +1143,9 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
     p.sk_gq = 1;
     p.sk_buf = nullptr;
     p.sk_tick = nullptr;
+    p.causal = q.causal ? 1 : 0;
+    p.causal_offset = q.causal_offset;
+    if (p.causal && p.grouped) return cudaErrorInvalidValue;
     CUtensorMap qm, km, vm;
     if (!make_tmap_bf16_2d(&qm, q.q, q.n_batch * q.q_heads * q.q_rows, D, TILE) ||
         !make_tmap_bf16_2d(&km, q.k, q.n_batch * q.kv_heads * q.kv_cap, D, TILE) ||
@@ -1135,7 +1154,7 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
     // One split (not grouped) with the caller's workspace: stream-K over a persistent grid of
     // groups of n_qpairs CTAs, one CTA per SM, so the last wave is never partial (C3: 256 units
     // on 148 SMs ran as 2 waves, the second 73 % full).
-    if (!p.grouped && q.n_splits == 1 && q.sk_work && !std::getenv("SDA_K2_NO_SK")) {
+    if (!p.grouped && !p.causal && q.n_splits == 1 && q.sk_work && !std::getenv("SDA_K2_NO_SK")) {
         const SkShape sh = sk_shape(q.n_batch, q.q_heads, q.q_rows, q.kv_cap);
         if (sh.bytes && q.sk_work_bytes >= sh.bytes) {
             p.sk = 1;
@@ -1146,8 +1165,9 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
             return cudaGetLastError();
         }
     }
-    const dim3 grid((unsigned)p.n_qpairs, (unsigned)(p.grouped ? q.kv_heads : q.q_heads),
-                    (unsigned)(q.n_batch * q.n_splits));
+    const dim3 grid = p.causal ? dim3((unsigned)q.q_heads, (unsigned)p.n_qpairs, (unsigned)(q.n_batch * q.n_splits))
+                               : dim3((unsigned)p.n_qpairs, (unsigned)(p.grouped ? q.kv_heads : q.q_heads),
+                                      (unsigned)(q.n_batch * q.n_splits));
     k2_prefill_tc_kernel<<<grid, THREADS, SMEM, st>>>(p, qm, km, vm);
     return cudaGetLastError();
 }

@@ -401,6 +401,217 @@ __global__ void __launch_bounds__(128) k3_merge_small_kernel(const K3Params p) {
     }
 }
 
+// fwht_group over U independent rows at once (lane owns elements [lane*E, lane*E+E) of each):
+// every stage runs across all rows before the next, so the shuffle latencies overlap
+template <int U, int E>
+__device__ __forceinline__ void fwht_rows(float (&v)[U][E], int lane) {
+#pragma unroll
+    for (int h = 1; h < E; h <<= 1)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int i = 0; i < E; ++i)
+                if ((i & h) == 0) {
+                    const float a = v[u][i], b = v[u][i + h];
+                    v[u][i] = a + b;
+                    v[u][i + h] = a - b;
+                }
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+        const float sgn = (lane & m) ? -1.f : 1.f;
+        float o[U][E];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int i = 0; i < E; ++i) o[u][i] = __shfl_xor_sync(0xffffffffu, v[u][i], m);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int i = 0; i < E; ++i) v[u][i] = fmaf(sgn, v[u][i], o[u][i]);
+    }
+}
+
+// Prefill-shaped merge (q_rows >= 64, plain memory, <= 8 sources): a CTA owns 64 consecutive
+// rows of one (request, head), so the phi_V^-1 tables of its sources are staged in shared memory
+// once per CTA (k3_merge_small_kernel re-reads them from L1 for every row: the u16 permutation
+// loads alone were most of its L1 traffic). Per row: coalesced 16-byte loads of every source's O'
+// row, the weighted sum in scrambled space per key group, and one unscramble per group through the
+// warp's shared-memory row (P2 gather -> 2 register + 5 shuffle butterfly stages -> P1 gather),
+// then coalesced stores. The p_q^-1 row indices of a warp's 16 rows are fetched in one load per
+// source up front, and U rows' stats and O' of every source are requested before any is used.
+template <int D, typename TOut, int NS, bool EXACT>
+__global__ void __launch_bounds__(128) k3_rows_kernel(const K3Params p) {
+    constexpr int E = D / 32;
+    constexpr int U = NS >= 4 ? 1 : 4 / NS;   // rows in flight per warp
+    constexpr int RPW = 16;                    // rows per warp; 64 per CTA
+    __shared__ __align__(16) float s_in[NS][D];    // InvIn (1 / s2)
+    __shared__ __align__(16) float s_out[NS][D];   // InvOut (1 / (s1 sqrt(d)))
+    __shared__ __align__(16) uint16_t s_p2[NS][D];
+    __shared__ __align__(16) uint16_t s_p1[NS][D];
+    __shared__ __align__(16) float s_row[4][U][D];
+    const int n = EXACT ? NS : p.n_src;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t bh = blockIdx.y;
+    const int h = (int)(bh % p.q_heads);
+    const int64_t b = bh / p.q_heads;
+    const int kh = h / (p.q_heads / p.key_heads);
+    for (int s = 0; s < n; ++s) {
+        if (!p.src[s].keys) continue;
+        const uint8_t* sc = scrambler_ptr(p.src[s].keys, p.keys_bstride, b, kh, D, 1);
+        const float* ftab = reinterpret_cast<const float*>(sc);
+        const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + 24 * D);
+        for (int j = threadIdx.x; j < D; j += blockDim.x) {
+            s_in[s][j] = ftab[kInvIn * D + j];
+            s_out[s][j] = ftab[kInvOut * D + j];
+            s_p2[s][j] = utab[kP2 * D + j];
+            s_p1[s][j] = utab[kP1 * D + j];
+        }
+    }
+    pdl_wait();   // launched early behind K2 (PDL): its partials must be complete
+    __syncthreads();
+
+    const int64_t r_base = (int64_t)blockIdx.x * (4 * RPW) + warp * RPW;
+    uint32_t ridx[NS];   // lane t < RPW: source s's O' row for output row r_base + t
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        ridx[s] = 0;
+        if ((EXACT || s < n) && lane < RPW && r_base + lane < p.q_rows)
+            ridx[s] = p.src[s].pq_inv ? p.src[s].pq_inv[b * p.pq_bstride + r_base + lane] : (uint32_t)(r_base + lane);
+    }
+    // per-source bases of this (request, head): a row is then one 32-bit multiply-add away
+    const float* obase[NS];
+    const float* sbase[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const K3Source& src = p.src[s];
+        const int64_t off = src.bstride ? b * src.bstride + (int64_t)h * p.q_rows * D : bh * p.q_rows * D;
+        const int64_t soff = src.bstride ? b * src.bstride + (int64_t)h * p.q_rows * 2 : bh * p.q_rows * 2;
+        obase[s] = (EXACT || s < n) ? src.o + off : nullptr;
+        sbase[s] = (EXACT || s < n) ? src.stats + soff : nullptr;
+    }
+    TOut* const obh = static_cast<TOut*>(p.out) + (p.out_bstride ? b * p.out_bstride + (int64_t)h * p.q_rows * D : bh * p.q_rows * D);
+    float* const sbh = p.out_stats ? p.out_stats + (p.out_bstride ? b * p.out_bstride + (int64_t)h * p.q_rows * 2 : bh * p.q_rows * 2)
+                                   : nullptr;
+    float* rows[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) rows[u] = s_row[warp][u];
+    const bool single = n == 1;
+    for (int t0 = 0; t0 < RPW; t0 += U) {
+        float2 st[U][NS];
+        float xv[U][NS][E];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool valid = r_base + t0 + u < p.q_rows;
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                const uint32_t ri = __shfl_sync(0xffffffffu, ridx[s], t0 + u);
+                if ((EXACT || s < n) && valid) {
+                    st[u][s] = *reinterpret_cast<const float2*>(sbase[s] + (size_t)ri * 2);
+                    load_vec_any<E>(obase[s] + (size_t)ri * D + lane * E, xv[u][s]);
+                } else {
+                    st[u][s] = make_float2(-INFINITY, 0.f);
+#pragma unroll
+                    for (int e = 0; e < E; ++e) xv[u][s][e] = 0.f;
+                }
+            }
+        }
+        // the U rows go through every step together (one loop nest per step), so their shared-memory
+        // round trips and shuffle stages overlap instead of forming U dependent chains
+        float mstar[U], denom[U], acc[U][E], out[U][E];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            mstar[u] = -INFINITY;   // attention.cpp:103-105
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+                if ((EXACT || s < n) && st[u][s].y > 0.f) mstar[u] = fmaxf(mstar[u], st[u][s].x);
+            denom[u] = 0.f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc[u][e] = out[u][e] = 0.f;
+        }
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            if (!(EXACT || s < n)) continue;
+            const K3Source& src = p.src[s];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                // a source with no visible key (exp_sum 0) adds nothing: a zero weight rather than a
+                // branch, so the unscramble below stays warp-uniform code
+                const bool live = st[u][s].y > 0.f;
+                const float w = live ? (single ? 1.f : st[u][s].y * expf(st[u][s].x - mstar[u])) : 0.f;
+                denom[u] += single ? st[u][s].y : w;
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc[u][e] = live ? fmaf(w, xv[u][s][e], acc[u][e]) : acc[u][e];   // never 0 * NaN
+            }
+            const bool group_end = (s + 1 == n) || (p.src[s + 1].keys != src.keys);
+            if (!group_end) continue;
+            if (src.keys) {   // one unscramble per key group (linearity)
+                // t = acc / s2 ; u[j] = t[P2[j]] ; w = H u ; y[i] = w[P1[i]] / (s1[i] sqrt(d))
+                float tin[E], tout[E], v[U][E];
+                uint16_t p2[E], p1[E];
+                load_vec_any<E>(&s_in[s][lane * E], tin);
+                load_vec_any<E>(&s_out[s][lane * E], tout);
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    p2[e] = s_p2[s][lane * E + e];
+                    p1[e] = s_p1[s][lane * E + e];
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) v[u][e] = acc[u][e] * tin[e];
+                    store_vec_any<E>(rows[u] + lane * E, v[u]);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int e = 0; e < E; ++e) v[u][e] = rows[u][p2[e]];
+                fwht_rows<U, E>(v, lane);
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < U; ++u) store_vec_any<E>(rows[u] + lane * E, v[u]);
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int e = 0; e < E; ++e) out[u][e] = fmaf(rows[u][p1[e]], tout[e], out[u][e]);
+                __syncwarp();
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int e = 0; e < E; ++e) out[u][e] += acc[u][e];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc[u][e] = 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t r = r_base + t0 + u;
+            const bool valid = r < p.q_rows;
+            const bool masked = !(mstar[u] > -INFINITY);
+            if (masked && lane == 0 && p.err && valid) atomicExch(p.err, (int32_t)SDA_ERR_MASKED_ROW);
+            const float inv = masked ? __int_as_float(0x7fc00000) : (single ? 1.f : 1.f / denom[u]);
+#pragma unroll
+            for (int e = 0; e < E; ++e) out[u][e] *= inv;
+            if (valid) {
+                store_vec_any<E>(obh + (size_t)r * D + lane * E, out[u]);
+                if (sbh && lane == 0)
+                    *reinterpret_cast<float2*>(sbh + (size_t)r * 2) =
+                        make_float2(single ? (masked ? -INFINITY : mstar[u]) : mstar[u], masked ? 0.f : denom[u]);
+            }
+        }
+    }
+}
+
+template <int D, typename TOut, int NS, bool EXACT = true>
+static cudaError_t launch_k3_rows(const K3Params& p, cudaStream_t st) {
+    const dim3 grid((unsigned)((p.q_rows + 63) / 64), (unsigned)(p.n_batch * p.q_heads));
+    return pdl_launch(k3_rows_kernel<D, TOut, NS, EXACT>, grid, dim3(128), st, p);
+}
+
 template <int D, typename TOut, int NS, bool EXACT = true>
 static void launch_k3_small(const K3Params& p, int64_t total, cudaStream_t st) {
     constexpr int RPW = NS * (D / 32) <= 16 ? 2 : 1;   // in-flight rows per warp (4 measured slower)
@@ -414,6 +625,15 @@ static cudaError_t launch_k3_t(const K3Params& p, cudaStream_t st) {
     const int64_t total = p.n_batch * p.q_heads * p.q_rows;
     if (p.ll) return pdl_launch(k3_merge_kernel<D, TOut>, dim3((unsigned)((total + 3) / 4)), dim3(128), st, p);
     const bool small_ok = total < (int64_t(1) << 30) && !getenv("SDA_K3_PIPELINED");
+    // prefill-shaped rows (many per (request, head)): the table-staging row kernel
+    if (p.q_rows >= 64 && p.n_src <= kSmallSrc && p.n_batch * p.q_heads < 65536 && !getenv("SDA_K3_NO_ROWS")) {
+        switch (p.n_src) {
+            case 1: return launch_k3_rows<D, TOut, 1>(p, st);
+            case 2: return launch_k3_rows<D, TOut, 2>(p, st);
+            case 3: case 4: return launch_k3_rows<D, TOut, 4, false>(p, st);
+            default: return launch_k3_rows<D, TOut, 8, false>(p, st);
+        }
+    }
     if constexpr (D <= 128) {   // 9..16 sources (the decode split fold): all in flight, one row per warp
         if (small_ok && p.n_src > kSmallSrc && p.n_src <= 16) {
             launch_k3_small<D, TOut, 16, false>(p, total, st);

@@ -485,3 +485,56 @@ def test_many_splits_pipelined_merge_and_ragged_ll():
     kl, vl = kf[:, perm], vf[:, perm]
     plain = (torch.softmax((qf @ kl.transpose(-1, -2)) / np.sqrt(128), -1) @ vl).double().cpu().numpy()
     assert rel_fro(out[1].double().cpu().numpy(), plain) < 4e-2
+
+
+@pytest.mark.parametrize("n_groups,splits,lq,out_dtype", [(1, 1, 300, torch.bfloat16), (1, 2, 128, torch.float32),
+                                                          (3, 2, 200, torch.float32), (2, 1, 64, torch.bfloat16)])
+def test_k3_rows_kernel_prefill_shapes(n_groups, splits, lq, out_dtype):
+    """The prefill-shaped K3 form (q_rows >= 64: tables staged per CTA, P2 gather on load, P1
+    scatter through the warp's row) against dec_output + merge_shards: several domains (key
+    groups) x splits, a plaintext source, a masked row in one source, merged stats, ragged tail."""
+    B, H, d = 2, 3, 128
+    srcs, shards = [], [[] for _ in range(B * H)]
+    for gi in range(n_groups + 1):
+        keyed = gi < n_groups
+        kd = pqi = None
+        if keyed:
+            kh, kd = _keys(B, H, d, domain=gi + 1)
+            pq = [kh[b].span_perm(0, 77, lq) for b in range(B)]
+            pqi = ops.upload_perms([capi.invert_permutation(p) for p in pq], "cuda")
+        for s in range(splits if keyed else 1):
+            seed = 300 + 10 * gi + s
+            o = gauss(seed, (B, H, lq, d))
+            m = gauss(seed + 1, (B, H, lq)) * 2 + (500.0 if (gi, s) == (0, 0) else 0.0)
+            sm = np.abs(gauss(seed + 2, (B, H, lq))) + 0.3
+            if (gi, s) == (n_groups, 0):
+                sm[1, 2, 5] = 0.0   # masked in the plaintext source only
+            st = np.stack([m, sm], -1)
+            srcs.append(ops.MergeSource(dev(o, torch.float32), dev(st, torch.float32), kd, pqi))
+            for b in range(B):
+                for h in range(H):
+                    if keyed:
+                        od = C.apply_phi(o[b, h], *_sc(kh[b], h, 1), 2)
+                        oo, mm, ss = np.zeros_like(od), np.zeros(lq), np.zeros(lq)
+                        oo[pq[b]], mm[pq[b]], ss[pq[b]] = od, m[b, h], sm[b, h]
+                    else:
+                        oo, mm, ss = o[b, h], m[b, h], sm[b, h]
+                    shards[b * H + h].append((oo, mm, ss))
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ost = torch.empty((B, H, lq, 2), dtype=torch.float32, device="cuda")
+    got = ops.unscramble_merge(srcs, out_dtype=out_dtype, err_flag=err, out_stats=ost).double().cpu().numpy()
+    gst = ost.double().cpu().numpy()
+    assert int(err.item()) == 0
+    tol = 1e-2 if out_dtype == torch.bfloat16 else 1e-5
+    for b in range(B):
+        for h in range(H):
+            sh = shards[b * H + h]
+            if len(sh) == 1:
+                ref, rmax, rsum = sh[0]
+            else:
+                ref = C.merge_shards([x[0] for x in sh], [x[1] for x in sh], [x[2] for x in sh])
+                ms = np.stack([x[1] for x in sh]); ss = np.stack([x[2] for x in sh])
+                rmax = np.where(ss > 0, ms, -np.inf).max(0)
+                rsum = (ss * np.exp(np.where(ss > 0, ms, -np.inf) - rmax)).sum(0)
+            assert max_abs_rel(got[b, h], ref) < tol, (b, h)
+            assert np.allclose(gst[b, h, :, 0], rmax, rtol=1e-6) and np.allclose(gst[b, h, :, 1], rsum, rtol=1e-5)

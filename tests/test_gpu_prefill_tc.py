@@ -127,3 +127,48 @@ def test_gqa_grouped_decode_tc(hq, hkv, lq, cap, kv_len, n_splits, grouped):
         return (o_ * w[..., None]).sum(0) / w.sum(0)[..., None]
     a, b_ = merged(o, st), merged(simt_o, simt_st)
     assert max_abs_rel(a, b_) < 1e-2 and rel_fro(a, b_) < 5e-3
+
+
+def _merge_np(o, st):
+    m = np.where(st[..., 1] > 0, st[..., 0], -np.inf)
+    mx = m.max(0)
+    w = np.where(st[..., 1] > 0, st[..., 1] * np.exp(m - np.where(np.isfinite(mx), mx, 0)), 0.0)
+    L = w.sum(0)
+    out = (o * w[..., None]).sum(0) / np.where(L > 0, L, 1)[..., None]
+    return out, mx, L
+
+
+@pytest.mark.parametrize("lq,lk,off,n_splits,hq,hkv", [
+    (300, 300, 0, 1, 2, 2),       # the inquirer's own span (q_first_pos == k_first_pos)
+    (512, 512, 0, 2, 2, 1),       # GQA heads, two splits
+    (256, 1000, 744, 1, 1, 1),    # a span at the end of a longer local context
+    (200, 200, -5, 3, 2, 2),      # negative offset: the first 5 rows see no key
+])
+def test_prefill_tc_causal(lq, lk, off, n_splits, hq, hkv):
+    """AttentionMask::causal(offset) on the tensor-core prefill kernel (per-row key limits in the
+    softmax, tiles past a pair's last visible key skipped) against shard_attention(..., causal)."""
+    d = 128
+    q = C.round_to_format(gauss(81, (1, hq, lq, d)), 2)
+    k = C.round_to_format(gauss(82, (1, hkv, lk, d)), 2)
+    v = C.round_to_format(gauss(83, (1, hkv, lk, d)), 2)
+    o, st = ops.partial_attention_causal(dev(q, torch.bfloat16), dev(k, torch.bfloat16), dev(v, torch.bfloat16),
+                                         causal_offset=off, n_splits=n_splits)
+    o, st = o.double().cpu().numpy(), st.double().cpu().numpy()
+    mo, mm, ml = _merge_np(o, st)
+    G = hq // hkv
+    for h in range(hq):
+        ro, rm, rs = C.shard_attention(q[0, h], k[0, h // G], v[0, h // G], off)
+        live = rs > 0
+        assert np.array_equal(ml[0, h] > 0, live), h
+        assert max_abs_rel(mo[0, h][live], ro[live]) < 1e-2 and rel_fro(mo[0, h][live], ro[live]) < 5e-3, h
+        assert_lse(np.stack([mm[0, h], ml[0, h]], -1), rm, rs, LSE_TOL['bf16'], h)
+    # the tensor-core form against the SIMT form of the same call
+    os.environ["SDA_K2_SIMT"] = "1"
+    try:
+        so, sst = ops.partial_attention_causal(dev(q, torch.bfloat16), dev(k, torch.bfloat16), dev(v, torch.bfloat16),
+                                               causal_offset=off, n_splits=1)
+    finally:
+        os.environ.pop("SDA_K2_SIMT", None)
+    so = so.double().cpu().numpy()[0]
+    live = ml > 0
+    assert max_abs_rel(mo[live], so[live]) < 1e-2

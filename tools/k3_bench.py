@@ -1,6 +1,12 @@
-"""Micro-benchmark of K3 (LSE merge + inverse permutation + unscramble), CUDA-event timed:
-the prefill merge (1 request x 32 heads x 2048 rows, 4 splits, p_q^-1 gather) and the decode
-merge (16 requests x 32 heads x 1 row, 10 splits), for the preloading and the pipelined kernel.
+"""Micro-benchmark of K3 (LSE merge + inverse permutation + unscramble), CUDA-event timed per
+launch with the L2 flushed before each one (a 256 MB read: clean lines, so no write-back lands
+inside the timed launch), and with the inputs L2-resident (as in a step, where K3 reads the
+partials K2 has just written), for the prefill merges (C3: 1 request
+x 32 heads x 2048 rows, 1 or 4 splits; C5's prefill chunk: 64 heads, 2 splits, 2 requests) and
+the decode merges (16 requests x 32 heads x 1 row), per kernel form:
+  rows      k3_rows_kernel (q_rows >= 64: tables staged per CTA, P2 gather on load, P1 scatter)
+  preload   k3_merge_small_kernel (SDA_K3_NO_ROWS=1)
+  pipelined k3_merge_kernel (SDA_K3_PIPELINED=1)
   python tools/k3_bench.py"""
 import os
 import sys
@@ -10,8 +16,10 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_25716_b200 import ops, protocol  # noqa: E402
 
+MODES = {"rows": {}, "preload": {"SDA_K3_NO_ROWS": "1"}, "pipelined": {"SDA_K3_PIPELINED": "1", "SDA_K3_NO_ROWS": "1"}}
 
-def run(B, H, Lq, S, D=128, reps=20):
+
+def run(B, H, Lq, S, D=128, reps=20, out_dtype=torch.bfloat16):
     dev = torch.device("cuda")
     keys = protocol.DomainKeys(list(range(1, B + 1)), 0, 1, H, D, dev)
     o = torch.randn((S, B, H, Lq, D), device=dev)
@@ -20,36 +28,53 @@ def run(B, H, Lq, S, D=128, reps=20):
     if Lq > 1:
         pinv = torch.stack([torch.randperm(Lq, device=dev) for _ in range(B)]).to(torch.int32).contiguous()
     srcs = ops.sources_from_splits(o, st, keys.dev, pinv)
-    out = torch.empty((B, H, Lq, D), device=dev)
+    out = torch.empty((B, H, Lq, D), device=dev, dtype=out_dtype)
+    flush = torch.ones(64 << 20, dtype=torch.float32, device=dev)
     res = {}
-    for mode in ("preload", "pipelined"):
-        if mode == "pipelined":
-            os.environ["SDA_K3_PIPELINED"] = "1"
-        else:
-            os.environ.pop("SDA_K3_PIPELINED", None)
+    for mode, env in MODES.items():
+        for k in ("SDA_K3_NO_ROWS", "SDA_K3_PIPELINED"):
+            os.environ.pop(k, None)
+        os.environ.update(env)
         for _ in range(3):
             ops.unscramble_merge(srcs, out=out, key_heads=H)
         ref = out.clone()
-        g = torch.cuda.CUDAGraph()   # replayed: no host launch overhead in the small cases
+        g = torch.cuda.CUDAGraph()   # one K3 launch, replayed: no host time inside the events
         with torch.cuda.graph(g):
+            ops.unscramble_merge(srcs, out=out, key_heads=H)
+        med = []
+        for cold in (True, False):
+            ts = []
             for _ in range(reps):
-                ops.unscramble_merge(srcs, out=out, key_heads=H)
-        g.replay()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        g.replay()
-        e1.record()
-        torch.cuda.synchronize()
-        res[mode] = (e0.elapsed_time(e1) / reps * 1e3, ref)
-    nbytes = S * B * H * Lq * (D + 2) * 4 + B * H * Lq * D * 4
-    same = torch.equal(res["preload"][1], res["pipelined"][1])
-    print(f"B={B} H={H} Lq={Lq} S={S}: " + ", ".join(f"{m} {t:.1f} us ({nbytes / t / 1e3:.0f} GB/s)"
-                                                     for m, (t, _) in res.items()) + f", identical: {same}")
+                if cold:
+                    flush.sum()
+                else:
+                    g.replay()   # the inputs are in L2 from the previous launch
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                g.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e3)
+            ts.sort()
+            med.append(ts[len(ts) // 2])
+        res[mode] = (med, ref)
+    for k in ("SDA_K3_NO_ROWS", "SDA_K3_PIPELINED"):
+        os.environ.pop(k, None)
+    nbytes = S * B * H * Lq * (D + 2) * 4 + B * H * Lq * D * out.element_size() + (B * Lq * 4 if Lq > 1 else 0)
+    base = res["preload"][1].float()
+    worst = max(float((r.float() - base).abs().max() / base.abs().max()) for _, r in res.values())
+    print(f"B={B} H={H} Lq={Lq} S={S} ({nbytes / 1e6:.1f} MB): " +
+          ", ".join(f"{m} {t[0]:.1f} us cold ({nbytes / t[0] / 1e3:.0f} GB/s) / {t[1]:.1f} us L2-warm"
+                    for m, (t, _) in res.items()) +
+          f"; max rel diff between forms {worst:.1e}")
 
 
 if __name__ == "__main__":
-    run(1, 32, 2048, 4)
+    if len(sys.argv) > 1 and sys.argv[1] == "c3":   # the C3 single-source merge only (ncu captures)
+        run(1, 32, 2048, 1, reps=3)
+        sys.exit(0)
     run(1, 32, 2048, 1)
-    run(16, 32, 1, 10)
-    run(16, 32, 1, 4)
+    run(1, 32, 2048, 4)
     run(2, 64, 2048, 2)
+    run(16, 32, 1, 13)
+    run(16, 32, 1, 4)
