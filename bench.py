@@ -190,6 +190,15 @@ def cpu_reference(n_nodes: int, pairs: int, threads: int, steps: int = 3):
     return [(pairs / t) / HQ for t in secs], list(secs)
 
 
+def single_core_reference(n_nodes: int, pairs: int = 8, steps: int = 3):
+    """The reference as shipped is single-threaded: the same composition on ONE
+    host thread over a smaller bounded sample (8 (request, head) pairs, 3 steps)."""
+    vals, secs = cpu_reference(n_nodes, pairs, 1, steps)
+    return {"value": statistics.median(vals), "unit": "tokens/s", "cores": 1,
+            "sample": f"{pairs} (request, head) pairs per step x {CTX} keys, median of {steps} steps of "
+                      f"{statistics.median(secs):.3f} s on 1 thread"}, secs
+
+
 def run_reference_arm(args, ws, rank):
     """--impl reference: the reference's own C++ hot path (oracle/_ref) on all host cores. Under
     torchrun only rank 0 runs; the others exit without work."""
@@ -206,7 +215,7 @@ def run_reference_arm(args, ws, rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference RngStream gaussians)", "config": workload_config(ws),
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference",
-                             "sample": sample},
+                             "sample": sample, "single_core": single_core_reference(ws)[0]},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
 
@@ -236,10 +245,13 @@ def run_ours(args, ws, rank, local):
     shard = protocol.KVShard(B_tot, HKV, L, D, devn, torch.bfloat16)
     g = torch.Generator(device=devn).manual_seed(1000 + rank)
     chunk = 16 if L <= 8192 else 4
+    plain_kv = None
     for b0 in range(0, B_tot, chunk):  # context owners ship their segments (K1 into the cache)
         b1 = min(B_tot, b0 + chunk)
         kp = torch.randn((b1 - b0, HKV, L, D), generator=g, device=devn).to(torch.bfloat16)
         vp = torch.randn((b1 - b0, HKV, L, D), generator=g, device=devn).to(torch.bfloat16)
+        if ws == 1 and b0 == 0:   # plaintext of the first requests: the vs-plain parity sample below
+            plain_kv = (kp[:4].clone(), vp[:4].clone())
         p, _ = owner_keys.span_perms(1, rank * L, L)
         ops.scramble(kp, owner_keys.dev[b0:b1], capi.PHI_INV_T, capi.KEYS_KQ, p[b0:b1].contiguous(),
                      out=shard.k[b0:b1], key_heads=HKV)
@@ -409,6 +421,28 @@ def run_ours(args, ws, rank, local):
             t = float(tt[0])
         return t
 
+    # ---- parity sample printed with the line: the step's output against plain unscrambled
+    # attention (f32 over the same bf16 plaintext) on 4 requests x all heads -- the BF16-mode floor
+    # of SURVEY 7.4.1 made visible (BASELINE north_star: 2e-2; the test suite's rounding-matched
+    # oracle comparisons are the parity gate)
+    parity = None
+    if plain_kv is not None:
+        kf, vf = plain_kv[0].float(), plain_kv[1].float()
+        G = HQ // HKV
+        qf = q[:4].float()
+        kf, vf = kf.repeat_interleave(G, 1), vf.repeat_interleave(G, 1)
+        ref = torch.softmax((qf @ kf.transpose(-1, -2)) / D ** 0.5, -1) @ vf
+        got = step(q)[:4].float()
+        torch.cuda.synchronize()
+        diff = (got - ref).flatten(2)
+        rel_fro = (diff.norm(dim=-1) / ref.flatten(2).norm(dim=-1)).max().item()
+        mar = (diff.abs().amax(-1) / ref.flatten(2).abs().amax(-1)).max().item()
+        parity = {"vs_plain_rel_fro_max": rel_fro, "vs_plain_max_abs_rel_max": mar, "pairs": 4 * HQ,
+                  "scaling_range": "[1/8, 8] (protocol default)",
+                  "note": "bf16-storage floor of Q', K', V' at the default scaling range (SURVEY 7.4.1); "
+                          "vs the rounding-matched oracle the tests hold 2e-2 (tests/test_gpu_parity.py)"}
+        del plain_kv, kf, vf
+
     e2e_memcpy_ms = time_e2e(e2e_memcpy)
     e2e_zc_ms = time_e2e(e2e_zero_copy)
     assert torch.isfinite(out_host).all()
@@ -453,6 +487,8 @@ def run_ours(args, ws, rank, local):
                          if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"},
             "clocks": clk.summary(),
         }
+        if parity is not None:
+            line["parity"] = parity
         if ws == 1 and not args.no_prefill:
             try:
                 line["prefill"] = run_prefill(devn, 10, 3, peaks)
@@ -467,12 +503,14 @@ def run_ours(args, ws, rank, local):
             try:
                 threads = os.cpu_count() or 1
                 vals, secs = cpu_reference(1, args.cpu_pairs, threads, 5)
+                one, one_s = single_core_reference(1)
                 line["cpu_baseline"] = {"value": statistics.median(vals), "unit": "tokens/s", "cores": threads,
                                         "kind": "reference",
                                         "sample": f"{args.cpu_pairs} (request, head) pairs x {CTX} keys x d128 of "
                                                   f"the workload through the reference's own enc->shard_attention->"
                                                   f"dec->merge (oracle/_ref, f64), median of 5 steps of "
-                                                  f"{statistics.median(secs):.3f} s wall on {threads} threads"}
+                                                  f"{statistics.median(secs):.3f} s wall on {threads} threads",
+                                        "single_core": one}
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "unavailable": str(e)}
         emit(line)
@@ -531,7 +569,8 @@ def run_prefill_dist(args, ws, rank, local):
     k1_jobs = [ops.scramble_job(kn, inq[rank].dev, capi.PHI_INV_T, capi.KEYS_KQ, pkv, out=own_shard.k, key_heads=H),
                ops.scramble_job(vn, inq[rank].dev, capi.PHI_FORWARD, capi.KEYS_V, pkv, out=own_shard.v, key_heads=H)]
     S = capi.default_splits(ws, H, LQ, LK)
-    comp = sdist.gpu_rank_compute(inq, shard, n_splits=S, kv_heads=H, q_first_pos=q_first)
+    # the span also attends its own K/V in plaintext with the causal mask (protocol.cpp:944-947)
+    comp = sdist.gpu_rank_compute(inq, shard, n_splits=S, kv_heads=H, q_first_pos=q_first, local_kv=(kn, vn))
     bufs = sdist.StepBuffers.allocate(ws, 1, H, LQ, D, torch.bfloat16, devn)
     exch = sdist.PeerExchange(bufs) if ws > 1 and args.exchange != "nccl" else None
     out = torch.empty((1, H, LQ, D), dtype=torch.float32, device=devn)
@@ -602,7 +641,8 @@ def run_prefill_dist(args, ws, rank, local):
         tt = torch.tensor([ms, e2e_ms], device=devn)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms, e2e_ms = float(tt[0]), float(tt[1])
-    flops = 4.0 * LQ * LK * H * D * ws * ws   # every span against every domain's shard
+    # every span against every domain's shard, + every span's causal local attention
+    flops = 4.0 * LQ * LK * H * D * ws * ws + 2.0 * LQ * (LQ + 1) * H * D * ws
     if rank == 0:
         peaks = {}
         try:
@@ -617,7 +657,8 @@ def run_prefill_dist(args, ws, rank, local):
               "data": "synthetic (torch.randn Q/K/V, bf16), keys from the reference key-derivation rule",
               "config": {"workload": "BASELINE cfg3: one 2K-token prefill span per GPU against a 16K-token scrambled "
                                      "KV shard of every span on each of the N domains (+ the span's own K/V scrambled "
-                                     "into the cache), 32 heads x d128, bf16",
+                                     "into the cache, + the span attending its own K/V in plaintext with the causal "
+                                     "mask, merged in K3), 32 heads x d128, bf16",
                          "q_rows": LQ, "kv_rows_per_domain": LK, "domains": ws, "splits": S,
                          "exchange": ("none (single domain)" if ws == 1 else EXCHANGE_DESC[args.exchange if args.exchange != "ll" else "p2p"]),
                          "l2": "inputs larger than L2, no flush needed"},
@@ -665,7 +706,11 @@ def run_prefill(devn, steps: int, warmup: int, peaks: dict):
     o = torch.empty((S, 1, H, LQ, D), dtype=torch.float32, device=devn)
     st = torch.empty((S, 1, H, LQ, 2), dtype=torch.float32, device=devn)
     out = torch.empty((1, H, LQ, D), dtype=torch.float32, device=devn)
-    srcs = ops.sources_from_splits(o, st, keys.dev, pq_inv)
+    # the inquirer's own span attended in plaintext with the causal mask (protocol.cpp:944-947),
+    # tensor-core K2 with per-row key limits, merged by K3 as a plaintext source
+    lo = torch.empty((1, 1, H, LQ, D), dtype=torch.float32, device=devn)
+    ls = torch.empty((1, 1, H, LQ, 2), dtype=torch.float32, device=devn)
+    srcs = ops.sources_from_splits(o, st, keys.dev, pq_inv) + ops.sources_from_splits(lo, ls)
     stream = torch.cuda.current_stream()
     ev = []
     k1_jobs = [ops.scramble_job(kn, keys.dev, capi.PHI_INV_T, capi.KEYS_KQ, pkv, out=shard.k, out_row_offset=LK, key_heads=H),
@@ -684,8 +729,14 @@ def run_prefill(devn, steps: int, warmup: int, peaks: dict):
         if rec:
             e1.record(stream)
             ev.append((e0, e1))
+        ops.partial_attention_causal(q, kn, vn, causal_offset=0, n_splits=1, out_o=lo, out_stats=ls)
+        if rec:
+            e2 = torch.cuda.Event(enable_timing=True)
+            e2.record(stream)
+            ev_local.append((e1, e2))
         ops.unscramble_merge(srcs, out=out, key_heads=H)
 
+    ev_local = []
     for _ in range(warmup):
         step(False)
     torch.cuda.synchronize()
@@ -698,15 +749,21 @@ def run_prefill(devn, steps: int, warmup: int, peaks: dict):
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / steps
     k2_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
-    flops = 4.0 * LQ * LK * H * D
+    local_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_local)
+    flops_remote = 4.0 * LQ * LK * H * D
+    flops_local = 2.0 * LQ * (LQ + 1) * H * D   # causal: row i attends i + 1 keys
+    flops = flops_remote + flops_local
     peak = float(peaks.get("bf16_tflops", 1590.0))
-    tf_k2 = flops / (k2_ms * 1e-3) / 1e12
+    tf_k2 = flops_remote / (k2_ms * 1e-3) / 1e12
     return {"metric": "scrambled-attn prefill TFLOP/s", "value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
             "ms_per_step": ms, "steps": steps, "warmup": warmup,
             "config": {"workload": "BASELINE cfg3 per GPU: 2K-token prefill span vs 16K-token scrambled KV shard "
-                                   "(+ the span's own 2K K/V rows scrambled into the cache), 32 heads x d128, bf16",
+                                   "(+ the span's own 2K K/V rows scrambled into the cache, + the span attending its "
+                                   "own K/V in plaintext with the causal mask, merged in K3), 32 heads x d128, bf16",
                        "q_rows": LQ, "kv_rows": LK, "kv_rows_written": LQ, "heads": H, "head_dim": D, "splits": S},
-            "flops_per_step": flops, "clocks": clk.summary(),
+            "flops_per_step": flops, "flops_remote": flops_remote, "flops_local_causal": flops_local,
+            "local_causal_ms": local_ms,
+            "local_causal_tflops": flops_local / (local_ms * 1e-3) / 1e12, "clocks": clk.summary(),
             "roofline": {"bound": "tensor", "kernel": "k2_prefill_tc_kernel", "achieved": tf_k2, "peak": peak,
                          "unit": "TFLOP/s", "frac": tf_k2 / peak, "k2_ms": k2_ms, "k2_share_of_step": k2_ms / ms,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)",
@@ -755,7 +812,9 @@ def run_gqa_mixed(devn, steps: int, warmup: int, peaks: dict):
     outd = torch.empty((BD, HQ, 1, D), dtype=torch.float32, device=devn)
     outp = torch.empty((1, HQ, LP, D), dtype=torch.float32, device=devn)
     srcd = ops.sources_from_splits(od, sd, keys_d, None)
-    srcp = ops.sources_from_splits(op_, sp_, keys_p, pq_inv[BD:].contiguous())
+    lo = torch.empty((1, 1, HQ, LP, D), dtype=torch.float32, device=devn)   # the chunk's own span, causal
+    ls = torch.empty((1, 1, HQ, LP, 2), dtype=torch.float32, device=devn)
+    srcp = ops.sources_from_splits(op_, sp_, keys_p, pq_inv[BD:].contiguous()) + ops.sources_from_splits(lo, ls)
     pq_p = pq[BD:].contiguous()
     stream = torch.cuda.current_stream()
     ev = []
@@ -779,6 +838,7 @@ def run_gqa_mixed(devn, steps: int, warmup: int, peaks: dict):
     def prefill():
         ops.scramble_batch(k1_jobs, D)   # the chunk's K, V into the cache and its Q, one K1 launch
         ops.partial_attention(qp_s, kp, vp, lp, n_splits=Sp, out_o=op_, out_stats=sp_)
+        ops.partial_attention_causal(qp, knew, vnew, causal_offset=0, n_splits=1, out_o=lo, out_stats=ls)
         ops.unscramble_merge(srcp, out=outp, key_heads=HKV)
 
     def timed(fn, n):
@@ -801,13 +861,14 @@ def run_gqa_mixed(devn, steps: int, warmup: int, peaks: dict):
     k2_bytes = kv_bytes + BD * HQ * D * 2 + BD * HQ * (4 * D + 8)
     achieved = k2_bytes / (k2_ms * 1e-3) / 1e9
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    pf_flops = 4.0 * LP * L * HQ * D
+    pf_flops = 4.0 * LP * L * HQ * D + 2.0 * LP * (LP + 1) * HQ * D   # + the chunk's causal local span
     return {"metric": "scrambled-attn GQA decode tokens/s (mixed step also reported)",
             "value": BD / (ms_dec * 1e-3), "unit": "tokens/s", "ms_per_step_decode": ms_dec,
             "ms_per_step_mixed": ms_mix, "mixed_tokens_per_s": (BD + LP) / (ms_mix * 1e-3),
             "mixed_prefill_tflops_incl_decode": pf_flops / ((ms_mix) * 1e-3) / 1e12, "steps": steps,
             "config": {"workload": "BASELINE cfg5 per GPU: GQA 64 q / 8 kv heads x d128, 64K-token scrambled KV "
-                                   "shard per request; mixed step = 32 decode requests + one 2K-token prefill chunk",
+                                   "shard per request; mixed step = 32 decode requests + one 2K-token prefill chunk "
+                                   "(against its 64K shard, and its own 2K K/V in plaintext with the causal mask)",
                        "decode_requests": BD, "prefill_chunk": LP, "kv_rows": L, "splits_decode": Sd,
                        "splits_prefill": Sp},
             "roofline": {"bound": "hbm", "kernel": "k2_gqa_tc_kernel<16>", "achieved": achieved, "peak": peak,

@@ -424,11 +424,15 @@ class LocalWorld:
 
 
 def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = None,
-                     kv_heads: Optional[int] = None, q_first_pos: int = 0) -> RankCompute:
+                     kv_heads: Optional[int] = None, q_first_pos: int = 0,
+                     local_kv: Optional[tuple] = None, local_offset: int = 0) -> RankCompute:
     """RankCompute backed by libsdattn_b200.so. inquirer_keys[dom] = DomainKeys of my requests on
     domain dom + 1; shard = this rank's protocol.KVShard (all requests' rows of my domain).
     q_first_pos: global position of the query span (its rows are shuffled by each domain's
-    span_perm(0, q_first_pos, L_q), identity for single-row decode)."""
+    span_perm(0, q_first_pos, L_q), identity for single-row decode).
+    local_kv: (k, v) plaintext [B_p, Hkv, L_local, d] of the inquirer's own span: attended with the
+    causal mask at local_offset (= q_first_pos - the local keys' first position) and merged by K3
+    as a plaintext source, as span_finish_layer does (protocol.cpp:941-947)."""
     from . import capi, ops
 
     state = {}
@@ -445,12 +449,14 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
         return state["pq"], state["pq_inv"]
 
     def scramble_q_all(q, q_send):
+        state["q_plain"] = q
         W = q_send.shape[0]
         pq, _ = q_perms(q.shape[2])
         ops.scramble(q, keys_all, capi.PHI_FORWARD, capi.KEYS_KQ, pq, out=q_send.view((-1,) + tuple(q_send.shape[2:])),
                      key_heads=kv_heads or inquirer_keys[0].kv_heads, n_batch=W * q.shape[0])
 
     def scramble_q(q, dom, out):
+        state["q_plain"] = q
         pq, _ = q_perms(q.shape[2])
         ops.scramble(q, inquirer_keys[dom].dev, capi.PHI_FORWARD, capi.KEYS_KQ,
                      None if pq is None else pq[dom * q.shape[0]:(dom + 1) * q.shape[0]], out=out,
@@ -492,6 +498,7 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
     def scramble_q_remote(q, ex):
         # TMA stores straight into peer memory: +3-5 % at N=2, +0.4-3 % at N=4 on C3 against K1
         # into q_send + the push kernel (SDA_K1_REMOTE=0 selects the latter)
+        state["q_plain"] = q
         Bp, Hq, Lq, d = q.shape
         if os.environ.get("SDA_K1_REMOTE") == "0":
             return False
@@ -520,6 +527,15 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
         _, pq_inv = q_perms(Lq)
         srcs = [ops.MergeSource(back[dom], back[dom, :, Hq * Lq * d:], inquirer_keys[dom].dev, pq_inv[dom],
                                 batch_stride=rec, shape=(Bp, Hq, Lq, d)) for dom in range(W)]
+        if local_kv is not None:   # the inquirer's own span, plaintext, causal (no keys, no p_q)
+            key = ("local", Bp, Hq, Lq, d)
+            if state.get("lkey") != key:
+                state["lkey"] = key
+                state["lo"] = torch.empty((1, Bp, Hq, Lq, d), dtype=torch.float32, device=out.device)
+                state["ls"] = torch.empty((1, Bp, Hq, Lq, 2), dtype=torch.float32, device=out.device)
+            ops.partial_attention_causal(state["q_plain"], local_kv[0], local_kv[1], causal_offset=local_offset,
+                                         n_splits=1, out_o=state["lo"], out_stats=state["ls"])
+            srcs += ops.sources_from_splits(state["lo"], state["ls"])
         ops.unscramble_merge(srcs, out=out, key_heads=kv_heads or inquirer_keys[0].kv_heads)
 
     return RankCompute(scramble_q, serve, finish, scramble_q_all, serve_remote, scramble_q_remote)

@@ -176,15 +176,20 @@ def prefill_workspace(B: int, Hq: int, Hkv: int, Lq: int, cap: int, d: int, q_co
 
 
 def partial_attention_causal(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal_offset: int = 0,
-                             kv_len: Optional[torch.Tensor] = None, n_splits: int = 1, stream=None):
+                             kv_len: Optional[torch.Tensor] = None, n_splits: int = 1,
+                             out_o: Optional[torch.Tensor] = None, out_stats: Optional[torch.Tensor] = None,
+                             stream=None):
     """Plaintext causal shard (the inquirer's own span, protocol.cpp:944-947): key j is visible to
-    query row i iff j <= i + causal_offset. Returns (o [S,B,Hq,Lq,d], stats [S,B,Hq,Lq,2])."""
+    query row i iff j <= i + causal_offset. Returns (o [S,B,Hq,Lq,d], stats [S,B,Hq,Lq,2]).
+    bf16, d 128, >= 64 rows: the tensor-core prefill kernel with per-row key limits."""
     _cuda(q, "q"), _cuda(k, "k"), _cuda(v, "v")
     B, Hq, Lq, d = q.shape
     Hkv, cap = k.shape[1], k.shape[2]
     pdt = torch.float64 if q.dtype == torch.float64 else torch.float32
-    out_o = torch.empty((n_splits, B, Hq, Lq, d), dtype=pdt, device=q.device)
-    out_stats = torch.empty((n_splits, B, Hq, Lq, 2), dtype=pdt, device=q.device)
+    if out_o is None:
+        out_o = torch.empty((n_splits, B, Hq, Lq, d), dtype=pdt, device=q.device)
+    if out_stats is None:
+        out_stats = torch.empty((n_splits, B, Hq, Lq, 2), dtype=pdt, device=q.device)
     check(capi.LIB.sda_partial_attention_causal(_stream(stream), q.data_ptr(), _dtype_code(q), k.data_ptr(),
                                                 v.data_ptr(), _dtype_code(k), cap, _ptr(kv_len), B, Hq, Hkv, Lq, d,
                                                 n_splits, causal_offset, out_o.data_ptr(), out_stats.data_ptr()),

@@ -179,3 +179,37 @@ def test_prefill_remote_emulated_world(W):
         for h in range(w.Hq):
             assert max_abs_rel(got[b, h], ref[b, h]) < 2e-2 and rel_fro(got[b, h], ref[b, h]) < 2e-2, (b, h)
             assert np.all(np.isfinite(got[b, h, rows]))
+
+
+def test_prefill_with_causal_local_span_emulated_world():
+    """span_finish_layer with the inquirer's own span (protocol.cpp:941-948): every domain's
+    scrambled partial + the span's own K/V attended in plaintext with the causal mask (tensor-core
+    K2 with per-row key limits), all merged by K3 -- against plain attention over [every domain's
+    context ++ the span's own keys, causal] (f32 over the same bf16 plaintext)."""
+    W, LQ = 2, 256
+    w = World(W, 1, 4, 4, 128, 512, LQ, torch.bfloat16, seed=400)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    own = [(torch.randn((1, 4, LQ, 128), generator=g, device="cuda").to(torch.bfloat16),
+            torch.randn((1, 4, LQ, 128), generator=g, device="cuda").to(torch.bfloat16)) for _ in range(W)]
+    bufs = [sdist.StepBuffers.allocate(W, 1, 4, LQ, 128, torch.bfloat16, "cuda") for _ in range(W)]
+    ex = [sdist.PeerExchange(bufs[r], rank=r) for r in range(W)]
+    sdist.LocalWorld.connect(ex)
+    comps = [sdist.gpu_rank_compute(w.inq[r], w.shards[r], n_splits=1, kv_heads=4, q_first_pos=w.case.q_first_pos,
+                                    local_kv=own[r]) for r in range(W)]
+    outs = w.outs()
+    sdist.LocalWorld.decode_step([w.q(r) for r in range(W)], comps, bufs, outs, ex)
+    torch.cuda.synchronize()
+    c = w.case
+    for r in range(W):
+        q = torch.from_numpy(c.q[r]).cuda().float()                                    # [4, LQ, d]
+        k = torch.cat([torch.from_numpy(c.k[dom][r]).cuda().float() for dom in range(W)] + [own[r][0][0].float()], 1)
+        v = torch.cat([torch.from_numpy(c.v[dom][r]).cuda().float() for dom in range(W)] + [own[r][1][0].float()], 1)
+        s = (q @ k.transpose(-1, -2)) / 128 ** 0.5
+        ctx = W * 512
+        j = torch.arange(ctx + LQ, device="cuda")
+        i = torch.arange(LQ, device="cuda")
+        s = s.masked_fill((j[None, :] >= ctx) & (j[None, :] - ctx > i[:, None]), float("-inf"))
+        ref = (torch.softmax(s, -1) @ v).double().cpu().numpy()
+        got = outs[r][0].double().cpu().numpy()
+        for h in range(4):
+            assert rel_fro(got[h], ref[h]) < 4e-2 and max_abs_rel(got[h], ref[h]) < 6e-2, (r, h)
