@@ -142,6 +142,21 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys,
                         void* out, int32_t out_dtype, int64_t out_rows_cap, int64_t out_row_offset,
                         int64_t x_batch_mod);
 
+/* K1 with the quantised wire in its epilogue (wire_round, model.cpp:338-341; gen_quant_bits
+ * frames, protocol.hpp:25-26): the same scramble + gather as sda_scramble, then every
+ * (request, head) tensor of out (rows x d) holds dequantize(quantize_affine(tensor, quant_bits)) of
+ * its f32 scrambled values (quant.cpp:26-67: per-tensor min / max, 2..8-bit codes). Two launches of
+ * the SIMT K1: a min / max pass and the pass that quantises before its one store (no separate
+ * read-modify-write of out). scratch: 2 * n_batch * n_heads u64 device words; err: optional
+ * device i32, SDA_ERR_INVALID_ARGUMENT on a non-finite scrambled value (the reference throws). */
+sda_status sda_scramble_quant(void* stream, int32_t variant, int32_t which_keys,
+                              const void* x, int32_t x_dtype, int64_t n_batch, int32_t n_heads,
+                              int64_t rows, int32_t head_dim,
+                              const void* keys, int64_t keys_batch_stride, int32_t key_heads,
+                              const uint32_t* perm, int64_t perm_batch_stride,
+                              void* out, int32_t out_dtype, int64_t out_rows_cap, int64_t out_row_offset,
+                              int64_t x_batch_mod, int32_t quant_bits, uint64_t* scratch, int32_t* err);
+
 /* Several K1 jobs in one launch (up to SDA_MAX_SCRAMBLE_JOBS; e.g. a prefill step's span K -> K
  * cache, span V -> V cache and Q -> Q'): each job has exactly the meaning of one sda_scramble call
  * with the same fields. When every job takes the tensor-core form (bf16 in/out, head_dim 64 or
@@ -244,6 +259,11 @@ int32_t sda_default_splits_gqa(int64_t n_batch, int32_t q_heads, int32_t kv_head
  *   out_batch_stride : elements between requests in out and out_stats (0 = dense); a packed
  *               per-request record [q_heads*q_rows*d | q_heads*q_rows*2] is what one NCCL
  *               all-to-all carries back to the inquirer (O' and stats together).
+ *   alignment (d >= 32, f32 / bf16 out): every O' and output row is moved as one d/32-element
+ *               vector per lane, so source and output pointers and batch strides must keep rows
+ *               aligned to that vector (min(16, 4 d/32) bytes for O', min(16, d/32 sizeof(out))
+ *               for out) and stats pairs to 8 bytes; otherwise SDA_ERR_INVALID_ARGUMENT. A packed
+ *               record qualifies whenever q_heads * q_rows is even.
  * ------------------------------------------------------------------------------------------ */
 typedef struct {
     const float* o;          /* [n_batch][q_heads][q_rows][d] */
@@ -259,6 +279,19 @@ sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, i
                                 int64_t n_batch, int32_t q_heads, int64_t q_rows, int32_t head_dim,
                                 void* out, int32_t out_dtype, float* out_stats, int32_t* err_flag,
                                 int64_t out_batch_stride);
+
+/* K3 with the quantised O' wire on its input path (SCR_SHARD frames in quantN, protocol.hpp:25-26;
+ * wire_round of O', model.cpp:392): the same merge as sda_unscramble_merge, except that every key
+ * group's O' -- the domain's normalised partial, still scrambled -- is replaced by
+ * dequantize(quantize_affine(O', quant_bits)) per (request, head) tensor (q_rows x d) before its
+ * unscramble; the stats stay f32 (wire_round_stat). One query row: a single launch (the warp holds
+ * the whole tensor); more rows: a min / max pass first, scratch = 2 * groups * n_batch * q_heads
+ * u64 device words (groups = runs of sources sharing a key set). head_dim >= 32, out bf16 / f32. */
+sda_status sda_unscramble_merge_quant(void* stream, const sda_merge_source* sources, int32_t n_sources,
+                                      int64_t keys_batch_stride, int32_t key_heads, int64_t pq_batch_stride,
+                                      int64_t n_batch, int32_t q_heads, int64_t q_rows, int32_t head_dim,
+                                      void* out, int32_t out_dtype, float* out_stats, int32_t* err_flag,
+                                      int64_t out_batch_stride, int32_t quant_bits, uint64_t* scratch);
 
 /* ------------------------------------------------------------------------------------------
  * Peer-memory exchange (replaces Simulator::send of SCR_Q / SCR_SHARD, protocol.cpp:892-896,

@@ -88,8 +88,9 @@ sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt) {
     if (opt.quant_bits > 0 && (opt.quant_bits < 2 || opt.quant_bits > 8))
         throw std::invalid_argument("quantize_affine: bits must be in [2, 8]");
     // quantised wire (wire_round, model.cpp:338-341): Q', K', V', O' travel as per-tensor affine
-    // codes -> scrambled in f32, then quantised and dequantised in place on the device; the
-    // normalisation scalars ride at f32 (wire_round_stat, model.cpp:343-348)
+    // codes -> Q', K', V' quantised and dequantised in K1's epilogue (sda_scramble_quant), O' of
+    // each shard by a round trip after K2; the normalisation scalars ride at f32
+    // (wire_round_stat, model.cpp:343-348)
     const int qbits = opt.quant_bits > 0 ? opt.quant_bits : 0;
     const int dt = (opt.wire_fmt == sdattn::FloatFormat::bf16 && !qbits) ? SDA_BF16 : SDA_F32;
     const size_t esz = dt == SDA_BF16 ? 2 : 4;
@@ -109,18 +110,26 @@ sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt) {
         ck(sda_invert_permutation(pq.data(), lq, pq_inv.data()), "invert");
         auto pq_d = upload_u32(pq), pq_inv_d = upload_u32(pq_inv);
         DevBuf q_s(lq * d * esz);
-        ck(sda_scramble(st, SDA_PHI_FORWARD, SDA_KEYS_KQ, q32->p, SDA_F32, 1, 1, (int64_t)lq, (int)d, hk.image->p, 0, 1,
-                        pq_d->as<uint32_t>(), 0, q_s.p, dt, (int64_t)lq, 0, 0),
-           "scramble Q");
         DevBuf qscratch(16), qerr(4);
         ckc(cudaMemset(qerr.p, 0, 4), "memset");
-        auto wire = [&](void* x, size_t count) {   // the quantised wire, one tensor
+        // K1; on a quantised wire the quantise -> dequantise of the tensor runs in K1's epilogue
+        auto k1 = [&](int variant, int which, const void* x, size_t rows, const uint32_t* perm, void* out, const char* what) {
+            if (qbits)
+                ck(sda_scramble_quant(st, variant, which, x, SDA_F32, 1, 1, (int64_t)rows, (int)d, hk.image->p, 0, 1, perm,
+                                      0, out, dt, (int64_t)rows, 0, 0, qbits, qscratch.as<uint64_t>(), qerr.as<int32_t>()),
+                   what);
+            else
+                ck(sda_scramble(st, variant, which, x, SDA_F32, 1, 1, (int64_t)rows, (int)d, hk.image->p, 0, 1, perm, 0, out,
+                                dt, (int64_t)rows, 0, 0),
+                   what);
+        };
+        auto wire = [&](void* x, size_t count) {   // the quantised wire of O', one tensor per shard
             if (qbits)
                 ck(sda_quant_roundtrip(st, x, SDA_F32, 1, (int64_t)count, qbits, qscratch.as<uint64_t>(),
                                        qerr.as<int32_t>()),
                    "quant roundtrip");
         };
-        wire(q_s.p, lq * d);
+        k1(SDA_PHI_FORWARD, SDA_KEYS_KQ, q32->p, lq, pq_d->as<uint32_t>(), q_s.p, "scramble Q");
 
         std::vector<std::unique_ptr<DevBuf>> keep;
         std::vector<sda_merge_source> src;
@@ -131,14 +140,8 @@ sdattn::AttnFn gpu_scrambled_attn(const sdattn::ScrambledAttnOptions& opt) {
             auto k32 = upload_f32(k), v32 = upload_f32(v);
             auto pkv = upload_u32(span_perm(hk.token_perm_seed, 1, seg->first_pos, L));
             auto ks = std::make_unique<DevBuf>(L * d * esz), vs = std::make_unique<DevBuf>(L * d * esz);
-            ck(sda_scramble(st, SDA_PHI_INV_T, SDA_KEYS_KQ, k32->p, SDA_F32, 1, 1, (int64_t)L, (int)d, hk.image->p, 0, 1,
-                            pkv->as<uint32_t>(), 0, ks->p, dt, (int64_t)L, 0, 0),
-               "scramble K");
-            ck(sda_scramble(st, SDA_PHI_FORWARD, SDA_KEYS_V, v32->p, SDA_F32, 1, 1, (int64_t)L, (int)d, hk.image->p, 0, 1,
-                            pkv->as<uint32_t>(), 0, vs->p, dt, (int64_t)L, 0, 0),
-               "scramble V");
-            wire(ks->p, L * d);
-            wire(vs->p, L * d);
+            k1(SDA_PHI_INV_T, SDA_KEYS_KQ, k32->p, L, pkv->as<uint32_t>(), ks->p, "scramble K");
+            k1(SDA_PHI_FORWARD, SDA_KEYS_V, v32->p, L, pkv->as<uint32_t>(), vs->p, "scramble V");
             auto o = std::make_unique<DevBuf>(lq * d * 4), s = std::make_unique<DevBuf>(lq * 2 * 4);
             ck(sda_partial_attention(st, q_s.p, dt, ks->p, vs->p, dt, (int64_t)L, nullptr, 1, 1, 1, (int64_t)lq, (int)d, 1,
                                      o->as<float>(), s->as<float>()),

@@ -30,6 +30,13 @@ bool env_flag(const char* name) {
 }
 
 bool valid_dtype(int t) { return t == SDA_BF16 || t == SDA_F32; }
+size_t dtype_size(int t) { return t == SDA_BF16 ? 2 : t == SDA_F32 ? 4 : 8; }
+// rows of d elements are moved as vectors of up to 16 bytes: the base pointer must be aligned to
+// min(16, one row) (row strides are whole rows, so every row then is)
+bool row_aligned(const void* ptr, int d, int dt) {
+    const uintptr_t a = std::min<size_t>(16, (size_t)d * dtype_size(dt));
+    return reinterpret_cast<uintptr_t>(ptr) % a == 0;
+}
 // FP64 mode (f64_path.cu): every tensor of the call f64, or none
 bool valid_dtype_f64(int t) { return valid_dtype(t) || t == SDA_F64; }
 bool f64_pair_ok(int a, int b) { return (a == SDA_F64) == (b == SDA_F64); }
@@ -43,6 +50,13 @@ sda_status from_cuda(cudaError_t e) {
 }  // namespace
 
 extern "C" {
+
+static sda_status unscramble_merge_impl(void* stream, const sda_merge_source* sources, int32_t n_sources,
+                                        int64_t keys_batch_stride, int32_t key_heads, int64_t pq_batch_stride,
+                                        int64_t n_batch, int32_t q_heads, int64_t q_rows, int32_t head_dim, void* out,
+                                        int32_t out_dtype, float* out_stats, int32_t* err_flag,
+                                        int64_t out_batch_stride, int quant_bits, int n_groups,
+                                        unsigned long long* qscratch);
 
 int32_t sda_abi_version(void) { return SDA_ABI_VERSION; }
 
@@ -76,6 +90,7 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys, const
     if (which_keys != SDA_KEYS_KQ && which_keys != SDA_KEYS_V) return SDA_ERR_INVALID_ARGUMENT;
     if (!x || !out || !keys || !valid_dtype_f64(x_dtype) || !valid_dtype_f64(out_dtype) || !f64_pair_ok(x_dtype, out_dtype))
         return SDA_ERR_INVALID_ARGUMENT;
+    if (!row_aligned(x, head_dim, x_dtype) || !row_aligned(out, head_dim, out_dtype)) return SDA_ERR_INVALID_ARGUMENT;
     if (n_batch < 0 || n_heads <= 0 || key_heads <= 0 || n_heads % key_heads != 0 || rows < 0)
         return SDA_ERR_INVALID_ARGUMENT;
     if (out_row_offset < 0 || out_row_offset + rows > out_rows_cap || x_batch_mod < 0) return SDA_ERR_INVALID_ARGUMENT;
@@ -88,6 +103,34 @@ sda_status sda_scramble(void* stream, int32_t variant, int32_t which_keys, const
         return from_cuda(sda::launch_f64_path(1, &p, head_dim, n_batch, static_cast<cudaStream_t>(stream)));
     if (sda::k1_tc_eligible(p, head_dim, x_dtype, out_dtype) && !env_flag("SDA_K1_SIMT"))
         return from_cuda(sda::launch_k1_tc(p, head_dim, n_batch, static_cast<cudaStream_t>(stream)));
+    return from_cuda(sda::launch_k1(p, head_dim, x_dtype, out_dtype, n_batch, static_cast<cudaStream_t>(stream)));
+}
+
+sda_status sda_scramble_quant(void* stream, int32_t variant, int32_t which_keys, const void* x, int32_t x_dtype,
+                              int64_t n_batch, int32_t n_heads, int64_t rows, int32_t head_dim, const void* keys,
+                              int64_t keys_batch_stride, int32_t key_heads, const uint32_t* perm,
+                              int64_t perm_batch_stride, void* out, int32_t out_dtype, int64_t out_rows_cap,
+                              int64_t out_row_offset, int64_t x_batch_mod, int32_t quant_bits, uint64_t* scratch,
+                              int32_t* err) {
+    if (quant_bits < 2 || quant_bits > 8) return SDA_ERR_INVALID_ARGUMENT;   // quant.cpp:27
+    if (!scratch) return SDA_ERR_INVALID_ARGUMENT;
+    if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
+    if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
+    if (variant != SDA_PHI_FORWARD && variant != SDA_PHI_INV_T) return SDA_ERR_INVALID_ARGUMENT;
+    if (which_keys != SDA_KEYS_KQ && which_keys != SDA_KEYS_V) return SDA_ERR_INVALID_ARGUMENT;
+    if (!x || !out || !keys || !valid_dtype(x_dtype) || !valid_dtype(out_dtype)) return SDA_ERR_INVALID_ARGUMENT;
+    if (!row_aligned(x, head_dim, x_dtype) || !row_aligned(out, head_dim, out_dtype)) return SDA_ERR_INVALID_ARGUMENT;
+    if (n_batch < 0 || n_heads <= 0 || key_heads <= 0 || n_heads % key_heads != 0 || rows < 0)
+        return SDA_ERR_INVALID_ARGUMENT;
+    if (out_row_offset < 0 || out_row_offset + rows > out_rows_cap || x_batch_mod < 0) return SDA_ERR_INVALID_ARGUMENT;
+    if (n_batch > 65535 || n_heads > 65535) return SDA_ERR_UNSUPPORTED;
+    if (rows == 0 || n_batch == 0) return SDA_OK;
+    sda::K1Params p{x, out, keys, perm, keys_batch_stride, perm_batch_stride, rows, out_rows_cap, out_row_offset,
+                    n_heads, key_heads, which_keys, variant == SDA_PHI_INV_T ? 1 : 0, x_batch_mod};
+    p.quant_bits = quant_bits;
+    p.qscratch = reinterpret_cast<unsigned long long*>(scratch);
+    p.qerr = err;
+    g_launches += 2;
     return from_cuda(sda::launch_k1(p, head_dim, x_dtype, out_dtype, n_batch, static_cast<cudaStream_t>(stream)));
 }
 
@@ -472,6 +515,8 @@ sda_status sda_partial_attention_ws(void* stream, const void* q, int32_t q_dtype
     if (!q || !k || !v || !out_o || !out_stats || !valid_dtype_f64(q_dtype) || !valid_dtype_f64(kv_dtype) ||
         !f64_pair_ok(q_dtype, kv_dtype))
         return SDA_ERR_INVALID_ARGUMENT;
+    if (!row_aligned(q, head_dim, q_dtype) || !row_aligned(k, head_dim, kv_dtype) || !row_aligned(v, head_dim, kv_dtype))
+        return SDA_ERR_INVALID_ARGUMENT;
     if (n_batch < 0 || q_rows < 0 || kv_cap < 0 || q_heads <= 0 || kv_heads <= 0 || q_heads % kv_heads != 0 ||
         n_splits <= 0)
         return SDA_ERR_INVALID_ARGUMENT;
@@ -502,6 +547,8 @@ sda_status sda_partial_attention_causal(void* stream, const void* q, int32_t q_d
     if (!supported_dim(head_dim)) return SDA_ERR_UNSUPPORTED;
     if (!q || !k || !v || !out_o || !out_stats || !valid_dtype_f64(q_dtype) || !valid_dtype_f64(kv_dtype) ||
         !f64_pair_ok(q_dtype, kv_dtype))
+        return SDA_ERR_INVALID_ARGUMENT;
+    if (!row_aligned(q, head_dim, q_dtype) || !row_aligned(k, head_dim, kv_dtype) || !row_aligned(v, head_dim, kv_dtype))
         return SDA_ERR_INVALID_ARGUMENT;
     if (n_batch < 0 || q_rows < 0 || kv_cap < 0 || q_heads <= 0 || kv_heads <= 0 || q_heads % kv_heads != 0 ||
         n_splits <= 0)
@@ -654,10 +701,39 @@ sda_status sda_ll_unscramble_merge(void* stream, const void* ll_rec, int32_t n_d
     return from_cuda(sda::launch_k3(p, head_dim, out_dtype, static_cast<cudaStream_t>(stream)));
 }
 
+sda_status sda_unscramble_merge_quant(void* stream, const sda_merge_source* sources, int32_t n_sources,
+                                      int64_t keys_batch_stride, int32_t key_heads, int64_t pq_batch_stride,
+                                      int64_t n_batch, int32_t q_heads, int64_t q_rows, int32_t head_dim, void* out,
+                                      int32_t out_dtype, float* out_stats, int32_t* err_flag, int64_t out_batch_stride,
+                                      int32_t quant_bits, uint64_t* scratch) {
+    if (quant_bits < 2 || quant_bits > 8) return SDA_ERR_INVALID_ARGUMENT;
+    if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
+    if (head_dim < 32 || !supported_dim(head_dim) || out_dtype == SDA_F64) return SDA_ERR_UNSUPPORTED;
+    if (n_sources <= 0) return SDA_ERR_EMPTY_SHARDS;
+    if (!sources || n_sources > SDA_MAX_SOURCES) return SDA_ERR_INVALID_ARGUMENT;
+    int groups = 1;
+    for (int i = 1; i < n_sources; ++i) groups += sources[i].keys != sources[i - 1].keys;
+    if (q_rows > 1 && !scratch) return SDA_ERR_INVALID_ARGUMENT;
+    return unscramble_merge_impl(stream, sources, n_sources, keys_batch_stride, key_heads, pq_batch_stride, n_batch,
+                                 q_heads, q_rows, head_dim, out, out_dtype, out_stats, err_flag, out_batch_stride,
+                                 quant_bits, groups, reinterpret_cast<unsigned long long*>(scratch));
+}
+
 sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, int32_t n_sources,
                                 int64_t keys_batch_stride, int32_t key_heads, int64_t pq_batch_stride,
                                 int64_t n_batch, int32_t q_heads, int64_t q_rows, int32_t head_dim, void* out,
                                 int32_t out_dtype, float* out_stats, int32_t* err_flag, int64_t out_batch_stride) {
+    return unscramble_merge_impl(stream, sources, n_sources, keys_batch_stride, key_heads, pq_batch_stride, n_batch,
+                                 q_heads, q_rows, head_dim, out, out_dtype, out_stats, err_flag, out_batch_stride, 0,
+                                 0, nullptr);
+}
+
+static sda_status unscramble_merge_impl(void* stream, const sda_merge_source* sources, int32_t n_sources,
+                                        int64_t keys_batch_stride, int32_t key_heads, int64_t pq_batch_stride,
+                                        int64_t n_batch, int32_t q_heads, int64_t q_rows, int32_t head_dim, void* out,
+                                        int32_t out_dtype, float* out_stats, int32_t* err_flag,
+                                        int64_t out_batch_stride, int quant_bits, int n_groups,
+                                        unsigned long long* qscratch) {
     if (n_sources <= 0) return SDA_ERR_EMPTY_SHARDS;  // attention.cpp:90
     if (n_sources > SDA_MAX_SOURCES || !sources) return SDA_ERR_INVALID_ARGUMENT;
     if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
@@ -669,6 +745,23 @@ sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, i
         any_keys |= sources[i].keys != nullptr;
     }
     if (any_keys && (key_heads <= 0 || q_heads % key_heads != 0)) return SDA_ERR_INVALID_ARGUMENT;
+    if (head_dim >= 32 && out_dtype != SDA_F64) {
+        // the warp forms move a row as one d/32-element vector per lane: every O' and output row
+        // must start on that vector's alignment (up to 16 bytes), every stats pair on 8 bytes --
+        // so pointers and batch strides must keep them there (a packed record of q_heads * q_rows
+        // * (d + 2) floats does whenever q_heads * q_rows is even)
+        auto misaligned = [](const void* ptr, int64_t stride_elems, int64_t esz, int64_t align) {
+            return (reinterpret_cast<uintptr_t>(ptr) % align) != 0 || ((stride_elems * esz) % align) != 0;
+        };
+        const int64_t vin = std::min<int64_t>(16, (head_dim / 32) * 4);
+        const int64_t osz = out_dtype == SDA_BF16 ? 2 : 4, vout = std::min<int64_t>(16, (head_dim / 32) * osz);
+        for (int i = 0; i < n_sources; ++i)
+            if (misaligned(sources[i].o, sources[i].batch_stride, 4, vin) ||
+                misaligned(sources[i].stats, sources[i].batch_stride, 4, 8))
+                return SDA_ERR_INVALID_ARGUMENT;
+        if (misaligned(out, out_batch_stride, osz, vout) || (out_stats && misaligned(out_stats, out_batch_stride, 4, 8)))
+            return SDA_ERR_INVALID_ARGUMENT;
+    }
     if (n_batch == 0 || q_rows == 0) return SDA_OK;
     sda::K3Params p{};
     for (int i = 0; i < n_sources; ++i)
@@ -685,7 +778,10 @@ sda_status sda_unscramble_merge(void* stream, const sda_merge_source* sources, i
     p.out_stats = out_stats;
     p.err = err_flag;
     p.out_bstride = out_batch_stride;
-    ++g_launches;
+    p.quant_bits = quant_bits;
+    p.n_groups = n_groups;
+    p.qscratch = qscratch;
+    g_launches += quant_bits > 0 && q_rows > 1 ? 2 : 1;
     if (out_dtype == SDA_F64)   // FP64 mode: f64 sources and stats, f64 key images
         return from_cuda(sda::launch_f64_path(3, &p, head_dim, n_batch, static_cast<cudaStream_t>(stream)));
     return from_cuda(sda::launch_k3(p, head_dim, out_dtype, static_cast<cudaStream_t>(stream)));

@@ -14,6 +14,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "quant.cuh"
 
 namespace sda {
 
@@ -53,7 +54,11 @@ __device__ __forceinline__ int k1_sidx(int j) { return (j >> 4) * 20 + (j & 15);
 // FLAT (rows == 1, the decode Q): every lane group owns one (request, head) row, so one CTA
 // covers WARPS * R rows of the flattened [n_batch][n_heads] space instead of one (b, h) per CTA
 // with 63 of its 64 row slots idle.
-template <int D, typename Tin, typename Tout, bool FLAT>
+// QP (the quantised wire, sda_scramble_quant): 0 none; 1 min / max pass -- the scrambled values of
+// every (request, head) tensor reduced into p.qscratch, nothing stored; 2 -- the scrambled values
+// quantised and dequantised with their tensor's parameters before the one store (wire_round,
+// model.cpp:338-341, on the f32 scrambled values)
+template <int D, typename Tin, typename Tout, bool FLAT, int QP = 0>
 __global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p, const int64_t n_batch) {
     using S = K1Shape<D>;
     constexpr int E = S::E, LPR = S::LPR, R = S::R;
@@ -105,6 +110,12 @@ __global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p, cons
     Tout* out = ll ? nullptr : static_cast<Tout*>(p.out) + out_elem;
     const uint32_t* perm = p.perm ? p.perm + b * p.perm_bstride : nullptr;
     float* u = &sbuf[warp][g * S::RS];
+    const int64_t qt = b * p.n_heads + h;   // quantisation tensor (request, head)
+    const int64_t n_t = n_batch * p.n_heads;
+    double qlo = INFINITY, qhi = -INFINITY;
+    bool qbad = false;
+    QParams qp;
+    if constexpr (QP == 2) qp = qparams(p.qscratch, p.qscratch + n_t, qt, p.quant_bits);
 
     for (int it = 0; it < ITERS; ++it) {
         const int64_t r = FLAT ? 0 : (int64_t)blockIdx.x * S::ROWS_PER_CTA + (int64_t)it * S::WARPS * R + warp * R + g;
@@ -129,6 +140,21 @@ __global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p, cons
         __syncwarp();
 #pragma unroll
         for (int e = 0; e < E; ++e) v[e] = u[p2i[e]] * kout[e];  // y[k] = H(u)[P2inv[k]] * s2^{+-1}[k]/sqrt(d)
+        if constexpr (QP == 1) {
+            if (valid)
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    qbad |= !isfinite(v[e]);
+                    qlo = fmin(qlo, (double)v[e]);
+                    qhi = fmax(qhi, (double)v[e]);
+                }
+            __syncwarp();
+            continue;
+        }
+        if constexpr (QP == 2) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = __double2float_rn(qround((double)v[e], qp));
+        }
         if (valid) {
             if (ll)
                 ll_store_row<E, Tout>(p.ll_out[b / p.x_batch_mod], out_elem + r * D + lg * E, v, ep);
@@ -137,20 +163,44 @@ __global__ void __launch_bounds__(128) k1_scramble_kernel(const K1Params p, cons
         }
         __syncwarp();
     }
+    if constexpr (QP == 1) {   // per lane group (FLAT: one tensor per group) or per warp (one tensor per CTA)
+        if (qbad && p.qerr) atomicExch(p.qerr, (int32_t)SDA_ERR_INVALID_ARGUMENT);
+#pragma unroll
+        for (int m = 1; m < (FLAT ? LPR : 32); m <<= 1) {
+            qlo = fmin(qlo, __shfl_xor_sync(0xffffffffu, qlo, m));
+            qhi = fmax(qhi, __shfl_xor_sync(0xffffffffu, qhi, m));
+        }
+        if ((FLAT ? lg == 0 : lane == 0) && qlo <= qhi) {
+            atomicMin(p.qscratch + qt, dkey(qlo));
+            atomicMax(p.qscratch + n_t + qt, dkey(qhi));
+        }
+    }
 }
 
-template <int D, typename Tin, typename Tout>
-static cudaError_t launch_k1_t(const K1Params& p, int64_t n_batch, cudaStream_t st) {
+template <int D, typename Tin, typename Tout, int QP>
+static cudaError_t launch_k1_q(const K1Params& p, int64_t n_batch, cudaStream_t st) {
     using S = K1Shape<D>;
     if (p.rows == 1) {
         const int64_t n = n_batch * p.n_heads, per = S::WARPS * S::R;
-        k1_scramble_kernel<D, Tin, Tout, true><<<(unsigned)((n + per - 1) / per), 128, 0, st>>>(p, n_batch);
+        k1_scramble_kernel<D, Tin, Tout, true, QP><<<(unsigned)((n + per - 1) / per), 128, 0, st>>>(p, n_batch);
         return cudaGetLastError();
     }
     const dim3 grid((unsigned)((p.rows + S::ROWS_PER_CTA - 1) / S::ROWS_PER_CTA), (unsigned)p.n_heads,
                     (unsigned)n_batch);
-    k1_scramble_kernel<D, Tin, Tout, false><<<grid, 128, 0, st>>>(p, n_batch);
+    k1_scramble_kernel<D, Tin, Tout, false, QP><<<grid, 128, 0, st>>>(p, n_batch);
     return cudaGetLastError();
+}
+
+template <int D, typename Tin, typename Tout>
+static cudaError_t launch_k1_t(const K1Params& p, int64_t n_batch, cudaStream_t st) {
+    if (p.quant_bits <= 0) return launch_k1_q<D, Tin, Tout, 0>(p, n_batch, st);
+    // quantised wire: min / max pass, then the pass that quantises in its epilogue
+    const int64_t n_t = n_batch * p.n_heads;
+    cudaError_t e = cudaMemsetAsync(p.qscratch, 0xFF, n_t * 8, st);          // min keys
+    if (e == cudaSuccess) e = cudaMemsetAsync(p.qscratch + n_t, 0x00, n_t * 8, st);   // max keys
+    if (e == cudaSuccess) e = launch_k1_q<D, Tin, Tout, 1>(p, n_batch, st);
+    if (e == cudaSuccess) e = launch_k1_q<D, Tin, Tout, 2>(p, n_batch, st);
+    return e;
 }
 
 template <int D>

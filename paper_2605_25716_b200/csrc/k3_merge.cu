@@ -15,6 +15,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "quant.cuh"
 
 namespace sda {
 
@@ -155,6 +156,47 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
             L.p1[e] = utab[kP1 * D + lane * E + e];
         }
     };
+    // quantised wire of O' (sda_unscramble_merge_quant): every key group's O' -- the domain's
+    // normalised shard output, acc / its weight, still scrambled -- goes through
+    // dequantize(quantize_affine(.)) before its unscramble (SCR_SHARD frames in quantN,
+    // model.cpp:392, protocol.hpp:25-26). One tensor per (group, request, head): with one query row
+    // the warp holds all of it; with more, a min / max pass (qpass 1) fills p.qscratch first.
+    float gw = 0.f;   // the current group's weight
+    int grp = 0;      // group index
+    const int64_t n_bh = p.n_batch * p.q_heads;
+    auto quant_group = [&](float* a) -> bool {   // false: min / max pass, nothing more to do
+        if (p.quant_bits <= 0) return true;
+        double lo = INFINITY, hi = -INFINITY;
+        float y[E];
+        const float iw = gw > 0.f ? 1.f / gw : 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            y[e] = a[e] * iw;
+            lo = fmin(lo, (double)y[e]);
+            hi = fmax(hi, (double)y[e]);
+        }
+        QParams q;
+        if (p.q_rows == 1 || p.qpass == 1) {
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) {
+                lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, m));
+                hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, m));
+            }
+            if (p.qpass == 1) {
+                if (lane == 0 && active && lo <= hi) {
+                    atomicMin(p.qscratch + grp * n_bh + bh, dkey(lo));
+                    atomicMax(p.qscratch + (p.n_groups + grp) * n_bh + bh, dkey(hi));
+                }
+                return false;
+            }
+            q = qparams_lohi(lo, hi, p.quant_bits);
+        } else {
+            q = qparams(p.qscratch + grp * n_bh, p.qscratch + (p.n_groups + grp) * n_bh, bh, p.quant_bits);
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) a[e] = __double2float_rn(qround((double)y[e], q)) * gw;
+        return true;
+    };
     bool done_ll = false;
     if constexpr (E >= 2) {
     if (ll && p.n_src <= 32) {
@@ -201,12 +243,13 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
                 if (sy > 0.f) {
                     const float w = single ? 1.f : sy * expf(sx - mstar);
                     denom += single ? sy : w;
+                    gw += w;
 #pragma unroll
                     for (int e = 0; e < E; ++e) acc[e] = fmaf(w, ov[e], acc[e]);
                     pending = true;
                 }
                 const bool group_end = (s + 1 == p.n_src) || (p.src[s + 1].keys != src.keys);
-                if (group_end && pending) {
+                if (group_end && pending && quant_group(acc)) {
                     if (src.keys) {
                         load_tables(src.keys, kt);
                         unscramble_acc<D>(kt, acc, out, sh, lane);
@@ -214,9 +257,13 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
 #pragma unroll
                         for (int e = 0; e < E; ++e) out[e] += acc[e];
                     }
+                }
+                if (group_end) {
 #pragma unroll
                     for (int e = 0; e < E; ++e) acc[e] = 0.f;
                     pending = false;
+                    gw = 0.f;
+                    ++grp;
                 }
             }
         }
@@ -231,25 +278,31 @@ __global__ void __launch_bounds__(128) k3_merge_kernel(const K3Params p) {
             if (cur.st.y > 0.f) {
                 const float w = single ? 1.f : cur.st.y * expf(cur.st.x - mstar);
                 denom += single ? cur.st.y : w;
+                gw += w;
     #pragma unroll
                 for (int e = 0; e < E; ++e) acc[e] = fmaf(w, cur.ov[e], acc[e]);
                 pending = true;
             }
             const bool group_end = (s + 1 == p.n_src) || (p.src[s + 1].keys != src.keys);
-            if (group_end && pending) {
+            if (group_end && pending && quant_group(acc)) {
                 if (src.keys) {
                     unscramble_acc<D>(cur, acc, out, sh, lane);
                 } else {
     #pragma unroll
                     for (int e = 0; e < E; ++e) out[e] += acc[e];
                 }
+            }
+            if (group_end) {
     #pragma unroll
                 for (int e = 0; e < E; ++e) acc[e] = 0.f;
                 pending = false;
+                gw = 0.f;
+                ++grp;
             }
             cur = nxt;
         }
     }
+    if (p.qpass == 1) return;   // the quantised wire's min / max pass stores nothing
     const bool masked = !(mstar > -INFINITY);
     if (masked && lane == 0 && p.err && active) atomicExch(p.err, (int32_t)SDA_ERR_MASKED_ROW);
     const float inv = masked ? __int_as_float(0x7fc00000) : (single ? 1.f : 1.f / denom);
@@ -623,6 +676,21 @@ static void launch_k3_small(const K3Params& p, int64_t total, cudaStream_t st) {
 template <int D, typename TOut>
 static cudaError_t launch_k3_t(const K3Params& p, cudaStream_t st) {
     const int64_t total = p.n_batch * p.q_heads * p.q_rows;
+    if (p.quant_bits > 0) {   // quantised O' wire: the general form (min / max pass first for > 1 row)
+        const dim3 grid((unsigned)((total + 3) / 4));
+        if (p.q_rows > 1) {
+            const int64_t n = (int64_t)p.n_groups * p.n_batch * p.q_heads;
+            cudaError_t e = cudaMemsetAsync(p.qscratch, 0xFF, n * 8, st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(p.qscratch + n, 0x00, n * 8, st);
+            if (e != cudaSuccess) return e;
+            K3Params p1 = p;
+            p1.qpass = 1;
+            if ((e = pdl_launch(k3_merge_kernel<D, TOut>, grid, dim3(128), st, p1)) != cudaSuccess) return e;
+        }
+        K3Params p2 = p;
+        p2.qpass = 2;
+        return pdl_launch(k3_merge_kernel<D, TOut>, grid, dim3(128), st, p2);
+    }
     if (p.ll) return pdl_launch(k3_merge_kernel<D, TOut>, dim3((unsigned)((total + 3) / 4)), dim3(128), st, p);
     const bool small_ok = total < (int64_t(1) << 30) && !getenv("SDA_K3_PIPELINED");
     // prefill-shaped rows (many per (request, head)): the table-staging row kernel

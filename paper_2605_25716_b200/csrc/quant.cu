@@ -20,68 +20,11 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "quant.cuh"
 
 namespace sda {
 
 namespace {
-
-// order-preserving u64 key of a double (for atomicMin / atomicMax)
-__device__ __forceinline__ unsigned long long dkey(double v) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-}
-__device__ __forceinline__ double dkey_inv(unsigned long long k) {
-    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k));
-}
-
-template <typename T>
-__device__ __forceinline__ double to_d(T v) {
-    if constexpr (std::is_same<T, __nv_bfloat16>::value)
-        return (double)__bfloat162float(v);
-    else
-        return (double)v;
-}
-template <typename T>
-__device__ __forceinline__ T from_d(double v) {
-    if constexpr (std::is_same<T, __nv_bfloat16>::value)
-        return __float2bfloat16_rn(__double2float_rn(v));
-    else if constexpr (std::is_same<T, float>::value)
-        return __double2float_rn(v);
-    else
-        return v;
-}
-
-struct QParams {
-    double zero, scale, inv;
-    uint32_t levels;
-    bool constant;
-};
-
-__device__ __forceinline__ QParams qparams(const unsigned long long* kmin, const unsigned long long* kmax, int64_t t,
-                                           int bits) {
-    QParams q;
-    const double lo = dkey_inv(kmin[t]), hi = dkey_inv(kmax[t]);
-    q.levels = (1u << bits) - 1u;
-    const float zf = __double2float_rn(lo);
-    const float sf = __double2float_rn(__ddiv_rn(__dsub_rn(hi, lo), (double)q.levels));
-    q.zero = (double)zf;
-    q.scale = (double)sf;
-    q.constant = sf == 0.f;
-    q.inv = q.constant ? 0.0 : __drcp_rn(q.scale);
-    return q;
-}
-
-__device__ __forceinline__ uint32_t qcode(double v, const QParams& q) {
-    if (q.constant) return 0u;
-    double c = rint(__dmul_rn(__dsub_rn(v, q.zero), q.inv));
-    c = c < 0.0 ? 0.0 : c;
-    c = c > (double)q.levels ? (double)q.levels : c;
-    return (uint32_t)c;
-}
-
-__device__ __forceinline__ double qvalue(uint32_t code, const QParams& q) {
-    return __dadd_rn(__dmul_rn((double)code, q.scale), q.zero);
-}
 
 // grid (x, n_tensors): per-tensor min / max of the finite values; any non-finite value -> *err
 template <typename T>

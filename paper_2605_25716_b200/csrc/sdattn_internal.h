@@ -43,6 +43,11 @@ struct K1Params {
     // every 4-byte data word is followed by the 4-byte step epoch, see ll_store)
     void* ll_out[kMaxPeers];
     const uint32_t* epoch;
+    // quantised wire in the epilogue (sda_scramble_quant): out = dequantize(quantize_affine(.))
+    // per (request, head) tensor, from the per-tensor min / max keys of a first pass
+    int quant_bits;
+    unsigned long long* qscratch;   // [2][n_batch * n_heads] order-preserving min / max keys
+    int32_t* qerr;
 };
 
 struct K2Params {
@@ -109,6 +114,12 @@ struct K3Params {
     int ll;
     uint32_t* epoch;
     uint32_t* done_counter;
+    // quantised O' wire (sda_unscramble_merge_quant): every key group's O' quantised + dequantised
+    // before its unscramble; qpass 1 = the min / max pass over (group, request, head) tensors
+    int quant_bits;
+    int qpass;
+    int n_groups;
+    unsigned long long* qscratch;   // [2][n_groups][n_batch * q_heads] min / max keys
 };
 
 }  // namespace sda

@@ -100,6 +100,30 @@ def scramble(x: torch.Tensor, keys: torch.Tensor, variant: int, which: int, perm
     return out
 
 
+def scramble_quant(x: torch.Tensor, keys: torch.Tensor, variant: int, which: int, bits: int,
+                   perm: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                   out_row_offset: int = 0, key_heads: Optional[int] = None, err: Optional[torch.Tensor] = None,
+                   stream=None) -> torch.Tensor:
+    """K1 with the quantised wire in its epilogue: scramble() followed by dequantize(quantize_affine(.,
+    bits)) of every (request, head) tensor (quant.cpp:26-67, wire_round model.cpp:338-341), without a
+    separate pass over the output. out f32 (or bf16)."""
+    _cuda(x, "x"), _cuda(keys, "keys")
+    B, H, rows, d = x.shape
+    kh = key_heads if key_heads is not None else H
+    if out is None:
+        out = torch.empty((B, H, rows, d), dtype=torch.float32, device=x.device)
+    _cuda(out, "out")
+    if perm is not None:
+        _cuda(perm, "perm")
+    scratch = torch.empty(2 * B * H, dtype=torch.int64, device=x.device)
+    check(capi.LIB.sda_scramble_quant(_stream(stream), variant, which, x.data_ptr(), _dtype_code(x), B, H, rows, d,
+                                      keys.data_ptr(), keys.stride(0) if keys.dim() > 1 else 0, kh, _ptr(perm),
+                                      perm.stride(0) if perm is not None and perm.dim() > 1 else 0, out.data_ptr(),
+                                      _dtype_code(out), out.shape[2], out_row_offset, 0, bits, scratch.data_ptr(),
+                                      _ptr(err)), "sda_scramble_quant")
+    return out
+
+
 def scramble_job(x: torch.Tensor, keys: torch.Tensor, variant: int, which: int, perm: Optional[torch.Tensor] = None,
                  out: torch.Tensor = None, out_row_offset: int = 0, key_heads: Optional[int] = None,
                  n_batch: Optional[int] = None) -> capi.ScrambleJob:
@@ -217,7 +241,7 @@ def sources_from_splits(o: torch.Tensor, stats: torch.Tensor, keys: Optional[tor
 def unscramble_merge(sources: Sequence[MergeSource], out: Optional[torch.Tensor] = None,
                      out_dtype: torch.dtype = torch.float32, key_heads: Optional[int] = None,
                      out_stats: Optional[torch.Tensor] = None, err_flag: Optional[torch.Tensor] = None,
-                     out_batch_stride: int = 0, stream=None) -> torch.Tensor:
+                     out_batch_stride: int = 0, quant_bits: int = 0, stream=None) -> torch.Tensor:
     """K3. Merged, unscrambled, inverse-permuted output [B, Hq, Lq, d] (or a packed per-request
     record when out_batch_stride is given: out and out_stats then point into the same buffer)."""
     n = len(sources)
@@ -244,6 +268,14 @@ def unscramble_merge(sources: Sequence[MergeSource], out: Optional[torch.Tensor]
     if out is None:
         out = torch.empty((B, Hq, Lq, d), dtype=out_dtype, device=sources[0].o.device)
     _cuda_or_pinned(out, "out")   # pinned host memory: O stored straight to the host (zero-copy)
+    if quant_bits:   # the quantised O' wire on K3's input path (quantize -> dequantize per group tensor)
+        groups = 1 + sum(1 for i in range(1, n) if arr[i].keys != arr[i - 1].keys)
+        scratch = torch.empty(2 * groups * B * Hq, dtype=torch.int64, device=sources[0].o.device)
+        check(capi.LIB.sda_unscramble_merge_quant(_stream(stream), arr, n, kstride, key_heads or Hq, pstride, B, Hq, Lq,
+                                                  d, out.data_ptr(), _dtype_code(out), _ptr(out_stats),
+                                                  _ptr(err_flag), out_batch_stride, quant_bits, scratch.data_ptr()),
+              "sda_unscramble_merge_quant")
+        return out
     check(capi.LIB.sda_unscramble_merge(_stream(stream), arr, n, kstride, key_heads or Hq, pstride, B, Hq, Lq, d,
                                         out.data_ptr(), _dtype_code(out), _ptr(out_stats), _ptr(err_flag),
                                         out_batch_stride),
