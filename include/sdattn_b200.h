@@ -157,6 +157,21 @@ sda_status sda_scramble_quant(void* stream, int32_t variant, int32_t which_keys,
                               void* out, int32_t out_dtype, int64_t out_rows_cap, int64_t out_row_offset,
                               int64_t x_batch_mod, int32_t quant_bits, uint64_t* scratch, int32_t* err);
 
+/* The QKV projection with K1 fused into it (one tcgen05 kernel: projection GEMM -> TMEM -> the
+ * scramble as a second GEMM in its epilogue -> bf16 TMA store): replaces project_qkv
+ * (model.cpp:124-133) followed by enc_qkv's apply_phi / apply_phi_inv_t + permute_rows_gather
+ * (scrambler.cpp:126-136), so no unscrambled Q / K / V reaches HBM.
+ *   out[b][h][out_row_offset + r][:] = bf16( (x[b][perm_b[r]][:] . W[h*d .. h*d+d-1][:]^T) phi_{b, h / G} )
+ *   x   : bf16 [n_batch][x_rows][d_model]  (the layer input after the norm, model.cpp:124)
+ *   w   : bf16 [n_heads * head_dim][d_model], the projection weight as an nn.Linear stores it
+ *   out : bf16 [n_batch][n_heads][out_rows_cap][head_dim]; perm as sda_scramble (NULL = identity)
+ * head_dim 64 or 128, d_model a multiple of 64; f32 accumulation, one RNE rounding at the store. */
+sda_status sda_project_scramble(void* stream, const void* x, int64_t n_batch, int64_t x_rows, int32_t d_model,
+                                const void* w, int32_t n_heads, int32_t head_dim, const void* keys,
+                                int64_t keys_batch_stride, int32_t key_heads, int32_t variant, int32_t which_keys,
+                                const uint32_t* perm, int64_t perm_batch_stride, int64_t rows, void* out,
+                                int64_t out_rows_cap, int64_t out_row_offset);
+
 /* Several K1 jobs in one launch (up to SDA_MAX_SCRAMBLE_JOBS; e.g. a prefill step's span K -> K
  * cache, span V -> V cache and Q -> Q'): each job has exactly the meaning of one sda_scramble call
  * with the same fields. When every job takes the tensor-core form (bf16 in/out, head_dim 64 or

@@ -38,7 +38,7 @@ EXPORTS = ("sda_derive_seed", "sda_shared_seed", "sda_random_permutation", "sda_
            "sda_partial_attention_remote", "sda_scramble_batch_remote", "sda_partial_attention_ws",
            "sda_prefill_workspace_bytes", "sda_set_spin_timeout_ns", "sda_spin_error",
            "sda_wire_round", "sda_keyset_bytes_f64", "sda_pack_keyset_f64", "sda_scramble_quant",
-           "sda_unscramble_merge_quant")
+           "sda_unscramble_merge_quant", "sda_project_scramble")
 
 
 class SdaError(RuntimeError):
@@ -132,6 +132,9 @@ def _load() -> ct.CDLL:
                                          _vp, _vp, ct.c_int64]
     lib.sda_unscramble_merge_quant.argtypes = lib.sda_unscramble_merge.argtypes + [ct.c_int32, _vp]
     lib.sda_scramble_quant.argtypes = lib.sda_scramble.argtypes + [ct.c_int32, _vp, _vp]
+    lib.sda_project_scramble.argtypes = [_vp, _vp, ct.c_int64, ct.c_int64, ct.c_int32, _vp, ct.c_int32, ct.c_int32,
+                                         _vp, ct.c_int64, ct.c_int32, ct.c_int32, ct.c_int32, _vp, ct.c_int64,
+                                         ct.c_int64, _vp, ct.c_int64, ct.c_int64]
     lib.sda_ipc_get_handle.argtypes = [_vp, _vp, ct.POINTER(ct.c_uint64)]
     lib.sda_ipc_open_handle.argtypes = [_vp, ct.c_uint64, ct.POINTER(ct.c_void_p)]
     lib.sda_ipc_close_handle.argtypes = [_vp, ct.c_uint64]

@@ -134,6 +134,32 @@ sda_status sda_scramble_quant(void* stream, int32_t variant, int32_t which_keys,
     return from_cuda(sda::launch_k1(p, head_dim, x_dtype, out_dtype, n_batch, static_cast<cudaStream_t>(stream)));
 }
 
+sda_status sda_project_scramble(void* stream, const void* x, int64_t n_batch, int64_t x_rows, int32_t d_model,
+                                const void* w, int32_t n_heads, int32_t head_dim, const void* keys,
+                                int64_t keys_batch_stride, int32_t key_heads, int32_t variant, int32_t which_keys,
+                                const uint32_t* perm, int64_t perm_batch_stride, int64_t rows, void* out,
+                                int64_t out_rows_cap, int64_t out_row_offset) {
+    if (!pow2(head_dim)) return SDA_ERR_NOT_POW2;
+    if (head_dim != 64 && head_dim != 128) return SDA_ERR_UNSUPPORTED;
+    if (d_model <= 0 || d_model % 64 != 0) return SDA_ERR_UNSUPPORTED;
+    if (variant != SDA_PHI_FORWARD && variant != SDA_PHI_INV_T) return SDA_ERR_INVALID_ARGUMENT;
+    if (which_keys != SDA_KEYS_KQ && which_keys != SDA_KEYS_V) return SDA_ERR_INVALID_ARGUMENT;
+    if (!x || !w || !keys || !out || n_batch < 0 || x_rows < 0 || rows < 0 || n_heads <= 0 || key_heads <= 0 ||
+        n_heads % key_heads != 0)
+        return SDA_ERR_INVALID_ARGUMENT;
+    if (!perm && rows > x_rows) return SDA_ERR_INVALID_ARGUMENT;
+    if (out_row_offset < 0 || out_row_offset + rows > out_rows_cap) return SDA_ERR_INVALID_ARGUMENT;
+    if (reinterpret_cast<uintptr_t>(x) % 16 || reinterpret_cast<uintptr_t>(w) % 16 || reinterpret_cast<uintptr_t>(out) % 16)
+        return SDA_ERR_INVALID_ARGUMENT;
+    if (n_batch > 65535 || n_heads > 65535) return SDA_ERR_UNSUPPORTED;
+    if (rows == 0 || n_batch == 0) return SDA_OK;
+    ++g_launches;
+    return from_cuda(sda::launch_project_scramble(x, n_batch, x_rows, d_model, w, n_heads, head_dim, keys,
+                                                  keys_batch_stride, key_heads, variant, which_keys, perm,
+                                                  perm_batch_stride, rows, out, out_rows_cap, out_row_offset,
+                                                  static_cast<cudaStream_t>(stream)));
+}
+
 static sda_status scramble_batch_impl(void* stream, int32_t head_dim, const sda_scramble_job* jobs, int32_t n_jobs,
                                       uint32_t* const* peer_flag, const uint32_t* epoch, uint32_t* counters) {
     if (!jobs || n_jobs < 0 || n_jobs > SDA_MAX_SCRAMBLE_JOBS) return SDA_ERR_INVALID_ARGUMENT;

@@ -158,6 +158,10 @@ size_t k2_prefill_sk_workspace_bytes(const K2Params& p);
 bool k2_gqa_tc_eligible(const K2Params& p, int d, int qdt, int kvdt);
 cudaError_t launch_k2_gqa_tc(const K2Params& p, cudaStream_t st);
 cudaError_t launch_k3(const K3Params& p, int d, int odt, cudaStream_t st);
+cudaError_t launch_project_scramble(const void* x, int64_t n_batch, int64_t x_rows, int d_model, const void* w,
+                                    int n_heads, int d, const void* keys, int64_t keys_bstride, int key_heads,
+                                    int variant, int which, const uint32_t* perm, int64_t perm_bstride, int64_t rows,
+                                    void* out, int64_t out_rows_cap, int64_t out_row_offset, cudaStream_t st);
 // FP64 mode (f64_path.cu): which 1 = K1 (K1Params), 2 = K2 (K2Params), 3 = K3 (K3Params)
 cudaError_t launch_f64_path(int which, const void* params, int d, int64_t n_batch, cudaStream_t st);
 // per-TU spin budget / error word (common.cuh SDA_SPIN_ACCESSOR)

@@ -393,33 +393,32 @@ def crc32(b: torch.Tensor, stream=None) -> int:
     return int.from_bytes(bytes(out.cpu().numpy()), "little")
 
 
-# --- K1 folded into the QKV projection (SURVEY 8(f) "next" row 2) --------------------------------
+# --- K1 fused into the QKV projection (SURVEY 8(f) "next" row 2) ---------------------------------
 def project_scrambled(x: torch.Tensor, w: torch.Tensor, keys: torch.Tensor, variant: int, which: int,
                       perm: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None, out_row_offset: int = 0,
-                      key_heads: Optional[int] = None, stream=None) -> torch.Tensor:
-    """Scrambled projection with no K1 pass over the activations: out[b, h, off + r] =
-    (x[b, perm_b[r]] @ W_h) phi_{b,h} for the projection x @ W_h of project_qkv (model.cpp:124-133)
-    followed by enc_qkv's scramble (scrambler.cpp:126-136). Because phi is linear,
-    (x W_h) phi = x (W_h phi): K1 runs once over the d_model rows of each W_h with request b's key
-    set (W'_{b,h} = W_h phi_{b,h}), and one batched GEMM (cuBLAS: a plain library GEMM) emits the
-    scrambled rows directly; the token permutation is a row gather of x.
-    x [B, rows, d_model] bf16; w [H, d_model, d] bf16 (GQA: H q heads on key_heads key sets).
-    Worth it when rows per request exceed ~d_model / 2 (prefill spans, KV shipping): W' costs
-    d_model x H x d per (request, layer, domain)."""
+                      key_heads: Optional[int] = None, rows: Optional[int] = None, stream=None) -> torch.Tensor:
+    """Scrambled projection in one tcgen05 kernel (sda_project_scramble): out[b, h, off + r] =
+    bf16((x[b, perm_b[r]] @ W_h^T) phi_{b,h}) -- project_qkv (model.cpp:124-133) followed by enc_qkv's
+    scramble + row gather (scrambler.cpp:126-136); the projection accumulates in TMEM and the
+    scramble runs as a second GEMM in its epilogue, so no unscrambled Q / K / V reaches HBM.
+    x bf16 [B, x_rows, d_model]; w bf16 [H * d, d_model] (the nn.Linear weight of the head
+    block); keys uint8 [B, keyset_bytes]; perm int32 [B, rows] or None; d 64 or 128."""
     _cuda(x, "x"), _cuda(w, "w"), _cuda(keys, "keys")
-    B, rows, dm = x.shape
-    H, dm2, d = w.shape
-    if dm2 != dm:
-        raise ValueError("x and w disagree on d_model")
-    wp = torch.empty((B, H, dm, d), dtype=w.dtype, device=w.device)
-    # request b reads W (x_batch_mod = 1) and scrambles it with its own key set
-    scramble(w.unsqueeze(0).contiguous(), keys, variant, which, None, out=wp, key_heads=key_heads, n_batch=B,
-             stream=stream)
-    xg = x if perm is None else torch.gather(x, 1, perm.long().unsqueeze(-1).expand(B, rows, dm))
-    res = torch.matmul(xg.unsqueeze(1), wp)   # [B, H, rows, d], f32 accumulation
+    if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
+        raise TypeError("x and w must be bf16")
+    B, x_rows, dm = x.shape
     if out is None:
-        if out_row_offset:
-            raise ValueError("out_row_offset needs out")
-        return res
-    out[:, :, out_row_offset:out_row_offset + rows].copy_(res)
+        raise ValueError("out [B, H, cap, d] is required (the cache / Q' buffer the kernel writes)")
+    _cuda(out, "out")
+    _, H, cap, d = out.shape
+    if w.shape != (H * d, dm):
+        raise ValueError(f"w must be [{H * d}, {dm}]")
+    n = rows if rows is not None else (perm.shape[1] if perm is not None else x_rows)
+    if perm is not None:
+        _cuda(perm, "perm")
+    check(capi.LIB.sda_project_scramble(_stream(stream), x.data_ptr(), B, x_rows, dm, w.data_ptr(), H, d,
+                                        keys.data_ptr(), keys.stride(0) if keys.dim() > 1 else 0,
+                                        key_heads if key_heads is not None else H, variant, which, _ptr(perm),
+                                        perm.stride(0) if perm is not None and perm.dim() > 1 else 0, n,
+                                        out.data_ptr(), cap, out_row_offset), "sda_project_scramble")
     return out

@@ -319,26 +319,36 @@ def test_ll_decode_world1_steps_and_graph(wire):
     assert int(lld.epoch.item()) == 1 + 3 + 3   # K3 opened one epoch per step
 
 
+@pytest.mark.parametrize("d,dm,rows,off", [(64, 256, 96, 0), (128, 512, 300, 17), (128, 4096, 128, 0)])
 @pytest.mark.parametrize("variant,which", [(0, 0), (1, 0), (0, 1)])
-def test_project_scrambled_folds_k1_into_the_projection(variant, which):
-    """ops.project_scrambled: (x[perm] @ W_h) phi_h computed as x[perm] @ (W_h phi_h) -- K1 over
-    the weights, one GEMM -- against the oracle's projection followed by apply_phi in f64."""
-    B, rows, dm, H, d = 2, 96, 256, 4, 64
+def test_project_scrambled_fused_projection_and_k1(d, dm, rows, off, variant, which):
+    """sda_project_scramble (the projection GEMM with K1 as a second GEMM in its epilogue, one
+    tcgen05 kernel): out[b, h, off + r] = (x[b, perm_b[r]] @ W_h^T) phi_h against the oracle's
+    projection (f64, over the bf16 values the device sees) followed by apply_phi and the bf16
+    rounding; rows outside [off, off + rows) of the cache untouched; a partial last tile."""
+    B, H = 2, 3
     keys = protocol.DomainKeys([1, 2], 0, 1, H, d, "cuda")
-    x = gauss(71, (B, rows, dm)) * 0.25
-    w = gauss(72, (H, dm, d)) * 0.0625
+    x = gauss(71, (B, rows, dm)) * 0.5
+    w = gauss(72, (H * d, dm)) / np.sqrt(dm)
     xd, wd = dev(x, torch.bfloat16), dev(w, torch.bfloat16)
     xr, wr = xd.double().cpu().numpy(), wd.double().cpu().numpy()   # the values the device sees
     perm, _ = keys.span_perms(1, 40, rows)
-    got = ops.project_scrambled(xd, wd, keys.dev, variant, which, perm).double().cpu().numpy()
+    cap = off + rows + 5
+    out = torch.zeros((B, H, cap, d), dtype=torch.bfloat16, device="cuda")
+    ops.project_scrambled(xd, wd, keys.dev, variant, which, perm, out=out, out_row_offset=off)
+    got = out.double().cpu().numpy()
+    assert not got[:, :, :off].any() and not got[:, :, off + rows:].any()
     p = perm.cpu().numpy()
     for b in range(B):
         for h in range(H):
             ks = keys.host[b]
             pre = "kq" if which == 0 else "v"
             sc = tuple(getattr(ks, pre + f)[h] for f in ("_s1", "_p1", "_p2", "_s2"))
-            ref = C.apply_phi(xr[b][p[b]] @ wr[h], *sc, variant)
-            assert max_abs_rel(got[b, h], ref) < TOL_BF16 and rel_fro(got[b, h], ref) < 1e-2, (b, h)
+            ref = C.round_to_format(C.apply_phi(xr[b][p[b]] @ wr[h * d:(h + 1) * d].T, *sc, variant), 2)
+            g = got[b, h, off:off + rows]
+            # f32 accumulation of the projection ahead of the one bf16 rounding: 1-ulp flips only
+            assert max_abs_rel(g, ref) < 1e-2 and rel_fro(g, ref) < 5e-3, (b, h)
+            assert (g == ref).mean() > 0.9, (b, h)
 
 
 def test_full_size_c5_gqa_decode_sampled_parity():
