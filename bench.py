@@ -61,6 +61,9 @@ def parse():
                          "per GPU vs a 16K-token shard per domain), 4 (decode, 32K-token shard per GPU, batch 64) or "
                          "5 (GQA decode, 64K-token shard per GPU, batch 32)")
     ap.add_argument("--cpu-pairs", type=int, default=128, help="(request, head) pairs in the CPU sample")
+    ap.add_argument("--domains-per-gpu", type=int, default=1,
+                    help="decode configs: K compute domains per GPU (N GPUs run N*K domains; e.g. BASELINE configs 4 / 5 "
+                         "as written, 8 nodes, on 4 GPUs with K = 2), LL exchange; the line is labelled with both counts")
     return ap.parse_args()
 
 
@@ -523,6 +526,162 @@ def run_ours(args, ws, rank, local):
         os._exit(0)
 
 
+def run_ours_domains(args, ws, rank, local):
+    """Decode with K = --domains-per-gpu compute domains per GPU (W = N * K domains): BASELINE
+    configs 4 / 5 as written (8 nodes) on fewer GPUs, labelled as such. Every GPU holds the K
+    domains' scrambled shards of every request and is the inquirer for K * B_PER requests; a step
+    runs, phase by phase, every local domain's LL K1, then K2, then K3 (the exchange carried by the
+    kernels over NVLink peer memory to the other GPUs' domains and through local memory to the
+    GPU's own). value = all requests decoded per step / step time (max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_25716_b200 import capi, ops, protocol
+    from paper_2605_25716_b200 import distributed as sdist
+
+    K = args.domains_per_gpu
+    W = ws * K
+    torch.cuda.set_device(local)
+    devn = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=devn)
+    B_tot = B_PER * W
+    L = CTX // W
+    rid = lambda b: b + 1  # noqa: E731
+    g = torch.Generator(device=devn).manual_seed(2000 + rank)
+    doms = [rank * K + i for i in range(K)]
+    lls, qs, outs = [], [], []
+    S = None
+    for dom in doms:
+        owner = protocol.DomainKeys([rid(b) for b in range(B_tot)], 0, dom + 1, HKV, D, devn)
+        shard = protocol.KVShard(B_tot, HKV, L, D, devn, torch.bfloat16)
+        p, _ = owner.span_perms(1, dom * L, L)
+        chunk = 16 if L <= 8192 else 4
+        for b0 in range(0, B_tot, chunk):
+            b1 = min(B_tot, b0 + chunk)
+            x = torch.randn((b1 - b0, HKV, L, D), generator=g, device=devn).to(torch.bfloat16)
+            ops.scramble(x, owner.dev[b0:b1], capi.PHI_INV_T, capi.KEYS_KQ, p[b0:b1].contiguous(), out=shard.k[b0:b1],
+                         key_heads=HKV)
+            x = torch.randn((b1 - b0, HKV, L, D), generator=g, device=devn).to(torch.bfloat16)
+            ops.scramble(x, owner.dev[b0:b1], capi.PHI_FORWARD, capi.KEYS_V, p[b0:b1].contiguous(), out=shard.v[b0:b1],
+                         key_heads=HKV)
+            del x
+        shard.rows = L
+        shard.kv_len.fill_(L)
+        del owner
+        my = [dom * B_PER + i for i in range(B_PER)]
+        inq = [protocol.DomainKeys([rid(b) for b in my], 0, d2 + 1, HKV, D, devn) for d2 in range(W)]
+        if S is None:
+            S = capi.default_splits(B_tot, HQ, 1, L, kv_heads=HKV, head_dim=D)
+        lls.append(sdist.LLDecode(B_PER, HQ, D, inq, shard, n_splits=S, kv_heads=HKV, world=(W, dom)))
+        qs.append(torch.randn((B_PER, HQ, 1, D), generator=g, device=devn).to(torch.bfloat16))
+        outs.append(torch.empty((B_PER, HQ, 1, D), dtype=torch.float32, device=devn))
+    opened = sdist.connect_domains(lls)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for i, x in enumerate(lls):
+            x.scramble_q(qs[i])
+        for x in lls:
+            x.serve()
+        for i, x in enumerate(lls):
+            x.finish(outs[i])
+
+    def barrier():
+        if ws > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    c0 = capi.launch_count()
+    step()
+    launches = capi.launch_count() - c0
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    barrier()
+    graph.replay()
+    torch.cuda.synchronize()
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    # e2e: every local domain's Q from pinned host memory in, its O back to pinned host memory
+    q_host = [q.cpu().pin_memory() for q in qs]
+    o_host = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
+
+    def e2e():
+        for i in range(K):
+            qs[i].copy_(q_host[i], non_blocking=True)
+        step()
+        for i in range(K):
+            o_host[i].copy_(outs[i], non_blocking=True)
+    e2e()
+    gr2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr2):
+        e2e()
+    barrier()
+    gr2.replay()
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        gr2.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    for x in lls:
+        x.check()
+    if ws > 1:
+        tt = torch.tensor([ms, e2e_ms], device=devn)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, e2e_ms = float(tt[0]), float(tt[1])
+    assert all(torch.isfinite(o).all() for o in o_host)
+    if rank == 0:
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except (OSError, ValueError):
+            pass
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        kv_bytes = K * B_tot * HKV * L * D * 2 * 2   # per GPU: K domains' shards
+        cfgd = workload_config(W)
+        cfgd.update({"domains": W, "domains_per_gpu": K, "gpus": ws,
+                     "kv_bytes_per_gpu": kv_bytes,
+                     "label": f"{W} compute domains on {ws} GPU(s), {K} per GPU: every GPU streams {K} domains' "
+                              f"shards per step, so per-GPU work is {K}x that of {W} GPUs",
+                     "exchange": EXCHANGE_DESC["ll"]})
+        emit({"metric": METRIC, "value": B_tot / (ms * 1e-3), "unit": "tokens/s", "n_gpus": ws,
+              "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+              "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+              "data": "synthetic (torch.randn Q/K/V, bf16), keys from the reference key-derivation rule",
+              "config": cfgd,
+              "e2e": {"value": B_tot / (e2e_ms * 1e-3), "unit": "tokens/s",
+                      "h2d_bytes_per_step": K * B_PER * HQ * D * 2, "d2h_bytes_per_step": K * B_PER * HQ * D * 4,
+                      "transfer": "pinned Q H2D copies -> step -> O D2H copies, every local domain, serial per step"},
+              "gpu_launches": int(launches) * args.steps, "cuda_graph": True,
+              "roofline": {"bound": "hbm", "kernel": "the step (K domains' K2 dominate)",
+                           "achieved": kv_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                           "frac": kv_bytes / (ms * 1e-3) / 1e9 / peak, "algorithmic_bytes_per_step": kv_bytes,
+                           "note": "KV bytes of the K local shards / step time (an upper bound on K2's share)"},
+              "clocks": clk.summary()})
+    if ws > 1:
+        torch.cuda.synchronize()
+        dist.barrier(device_ids=[local])
+    del opened   # process exit releases the IPC mappings
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os._exit(0)
+
+
 E2E_FORMS = {"memcpy": "pinned Q H2D copy -> step -> O D2H copy into pinned memory, serial per step",
              "zero-copy": "K1 reads Q straight from pinned host memory, K3 stores O straight into pinned host "
                           "memory (UVA), serial per step; the memcpy form is reported beside it. At N>1 the PCIe "
@@ -886,7 +1045,7 @@ def main():
     os.dup2(2, 1)
     if args.gpus != ws and ws > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {ws}", file=sys.stderr)
-    set_config(args.config, ws)
+    set_config(args.config, ws * max(1, args.domains_per_gpu))
     if args.impl == "reference" and args.config == 3:
         if rank == 0:
             emit({"impl": "reference", "unavailable": "config 3 (multi-GPU prefill) has no reference arm here: the "
@@ -897,6 +1056,8 @@ def main():
         run_reference_arm(args, ws, rank)
     elif args.config == 3:
         run_prefill_dist(args, ws, rank, local)
+    elif args.domains_per_gpu > 1:
+        run_ours_domains(args, ws, rank, local)
     else:
         run_ours(args, ws, rank, local)
 

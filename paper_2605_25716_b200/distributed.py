@@ -301,6 +301,55 @@ class LLDecode:
         return out
 
 
+def connect_domains(objs: Sequence, group: Optional[dist.ProcessGroup] = None) -> list:
+    """Several compute domains per process (e.g. BASELINE configs 4 / 5's 8 nodes on 4 GPUs, two
+    domains per GPU): objs = this process's LLDecode objects, built with world=(W, domain) for
+    global domains rank * len(objs) + i. Every object's receive buffers are mapped into every
+    process (CUDA IPC handles traded once) and each object is connected to all W domains' slots --
+    the local ones by address, the remote ones through the mapping. Returns the opened mappings."""
+    import ctypes as ct
+
+    from . import capi
+    names = list(objs[0].peer_buffers().keys())
+    mine = []
+    for o in objs:
+        hs = {}
+        for name, t in o.peer_buffers().items():
+            h = (ct.c_uint8 * 64)()
+            off = ct.c_uint64(0)
+            capi.check(capi.LIB.sda_ipc_get_handle(t.data_ptr(), h, ct.byref(off)), "ipc_get_handle")
+            hs[name] = (bytes(h), int(off.value))
+        mine.append((o.rank, hs))
+    P = dist.get_world_size(group) if dist.is_initialized() else 1
+    me = dist.get_rank(group) if dist.is_initialized() else 0
+    everyone = [None] * P
+    if P > 1:
+        dist.all_gather_object(everyone, mine, group=group)
+    else:
+        everyone = [mine]
+    W = objs[0].W
+    ptrs = {n: [0] * W for n in names}
+    opened = []
+    local = {o.rank: o for o in objs}
+    for r in range(P):
+        for dom, hs in everyone[r]:
+            for n in names:
+                if r == me:
+                    ptrs[n][dom] = local[dom].peer_buffers()[n].data_ptr()
+                    continue
+                hb, off = hs[n]
+                ptr = ct.c_void_p()
+                capi.check(capi.LIB.sda_ipc_open_handle((ct.c_uint8 * 64).from_buffer_copy(hb), off, ct.byref(ptr)),
+                           "ipc_open_handle")
+                opened.append((ptr.value, off))
+                ptrs[n][dom] = ptr.value
+    for o in objs:
+        o.connect(ptrs)
+    if P > 1:
+        dist.barrier(group=group)
+    return opened
+
+
 A2A_Q, A2A_RET, SYNC = "a2a_q", "a2a_ret", "sync"
 
 
