@@ -42,7 +42,8 @@ struct K2TcParams {
     int n_qpairs;          // ceil(Lq / 256) (normal mode)
     // causal (the inquirer's local span, AttentionMask::causal(offset), attention.hpp:25-27; split
     // mode, normal tiles only): key j is visible to span row i iff j <= i + causal_offset. The grid
-    // is then x = q head, y = Q-tile pair from the last (longest key range first)
+    // is then x = q head, y = c < ceil(n_qpairs / 2): the CTA runs Q-tile pair n_qpairs - 1 - c (the
+    // longer key range) and then pair c, so every CTA gets about the same number of key tiles
     int causal;
     int64_t causal_offset;
     int grouped;           // 1: GQA decode mode, one CTA per (request, kv head): its G = Hq/Hkv
@@ -184,12 +185,18 @@ __device__ __forceinline__ void fill_unit(const K2TcParams& p, int b, int head, 
 // split mode: the CTA's one segment -- blockIdx.z = request * n_splits + split;
 //   normal : blockIdx.x = 256-row pair of Q tiles, blockIdx.y = q head
 //   grouped: blockIdx.y = kv head; the tile rows are its G q heads x Lq rows
-__device__ __forceinline__ void split_seg(const K2TcParams& p, Seg& s) {
+// split mode: segments per CTA (causal: the paired Q-tile pairs, 1 for the middle pair of an odd count)
+__device__ __forceinline__ int split_nseg(const K2TcParams& p) {
+    if (!p.causal) return 1;
+    return (int)blockIdx.y == p.n_qpairs - 1 - (int)blockIdx.y ? 1 : 2;
+}
+
+__device__ __forceinline__ void split_seg(const K2TcParams& p, Seg& s, int idx = 0) {
     const int64_t b = blockIdx.z / p.n_splits;
     const int split = blockIdx.z % p.n_splits;
     const int G = p.q_heads / p.kv_heads;
     const int head = p.causal ? (int)blockIdx.x : (int)blockIdx.y;
-    const int qp = p.causal ? p.n_qpairs - 1 - (int)blockIdx.y : (int)blockIdx.x;
+    const int qp = p.causal ? (idx == 0 ? p.n_qpairs - 1 - (int)blockIdx.y : (int)blockIdx.y) : (int)blockIdx.x;
     s.b = (int)b;
     s.split = split;
     s.kvh = p.grouped ? head : head / G;
@@ -359,12 +366,11 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
     // the CTA's segments, the same sequence in every warp role
     SkCursor cur;
     if (p.sk) sk_init(p, T_sk, NG, grp, cur);
-    bool lpending = true;
+    int lseg = 0;   // split mode: segments of this CTA taken so far
     auto next_seg = [&](Seg& sg) -> bool {
         if (p.sk) return sk_next(p, qp_sk, cur, sg);
-        if (!lpending) return false;
-        lpending = false;
-        split_seg(p, sg);
+        if (lseg >= split_nseg(p)) return false;
+        split_seg(p, sg, lseg++);
         return true;
     };
 
@@ -566,9 +572,8 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
         __syncwarp();
         auto soft_next = [&](Seg& sg) -> bool {
             if (!p.sk) {
-                if (!lpending) return false;
-                lpending = false;
-                split_seg(p, sg);
+                if (lseg >= split_nseg(p)) return false;
+                split_seg(p, sg, lseg++);
                 return true;
             }
             SoftKeep* const k = opaque(keep);
@@ -949,7 +954,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             }
             if (group_live && warp_live) {
                 if (nkv > 0) {
-                    tc::mbar_wait(&o_final[g], 0);
+                    tc::mbar_wait(&o_final[g], oc & 1);
                     tc::tc_fence_after();
                 }
                 // remote records: stage the warp's 32 rows in SMEM (group 0 reuses the K ring, whose
@@ -992,6 +997,11 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                     out_stats[orow * 2 + 0] = st_max;
                     out_stats[orow * 2 + 1] = st_sum;
                 }
+            }
+            if (group_live && nkv > 0) {   // O_g may be overwritten by this CTA's next segment (causal pairs)
+                ++oc;
+                tc::tc_fence_before();
+                tc::mbar_arrive(&o_empty[g]);
             }
         }
         if (p.sk) {
@@ -1165,7 +1175,7 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
             return cudaGetLastError();
         }
     }
-    const dim3 grid = p.causal ? dim3((unsigned)q.q_heads, (unsigned)p.n_qpairs, (unsigned)(q.n_batch * q.n_splits))
+    const dim3 grid = p.causal ? dim3((unsigned)q.q_heads, (unsigned)((p.n_qpairs + 1) / 2), (unsigned)(q.n_batch * q.n_splits))
                                : dim3((unsigned)p.n_qpairs, (unsigned)(p.grouped ? q.kv_heads : q.q_heads),
                                       (unsigned)(q.n_batch * q.n_splits));
     k2_prefill_tc_kernel<<<grid, THREADS, SMEM, st>>>(p, qm, km, vm);
