@@ -41,14 +41,19 @@ struct KpParams {
 template <int D>
 struct KpShape {
     static constexpr int TILE = 128;
-    static constexpr int ST = D == 128 ? 3 : 4;               // projection K stages
+    // projection K stages: a stage is only 4 MMAs (256 tensor cycles) of work, so the loads need
+    // many stages in flight to cover their latency (3 stages: 39 % tensor-pipe active, ncu)
+    static constexpr int ST = D == 128 ? 5 : 8;
     static constexpr int A_BYTES = TILE * 128;                // [128 x 64] bf16, one K step of A
     static constexpr int B_BYTES = D * 128;                   // [d x 64] bf16, one K step of W_h
     static constexpr int OFF_STAGE = 0;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int OFF_A2H = ST * STAGE_BYTES;          // Y hi [128 x d] (K-major, d/64 blocks)
+    // Y hi / lo [128 x d] (K-major, d/64 blocks) reuse the stages: they are written after the last
+    // projection MMA has completed (yfull), when no stage is read or loaded any more
+    static constexpr int OFF_A2H = 0;
     static constexpr int OFF_A2L = OFF_A2H + TILE * D * 2;
-    static constexpr int OFF_BH = OFF_A2L + TILE * D * 2;     // B hi [d x d]
+    static_assert(2 * TILE * D * 2 <= ST * STAGE_BYTES, "Y hi / lo must fit in the stages");
+    static constexpr int OFF_BH = ST * STAGE_BYTES;           // B hi [d x d]
     static constexpr int OFF_BL = OFF_BH + D * D * 2;
     static constexpr int OFF_KT = OFF_BL + D * D * 2;         // key tables
     static constexpr int OFF_BAR = OFF_KT + D * 12;
