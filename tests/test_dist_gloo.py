@@ -125,3 +125,31 @@ def test_scrambled_decode_step_gloo(world):
     assert len(ret) == world
     for r in range(world):
         assert ret[r] < 1e-8, (r, ret[r])
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_local_world_decode_step_cpu(world):
+    """distributed.LocalWorld drives W ranks' decode_step_phases in lockstep in one process (the
+    NCCL all-to-alls as slot copies): with the oracle standing in for the kernels, every rank's
+    requests must equal plain attention over their whole context -- the same routing the gloo
+    test checks across processes, and the driver the GPU emulation tests use."""
+    from oracle import C
+    from paper_2605_25716_b200.distributed import LocalWorld
+    q, k, v = _plain_inputs(world)
+    comps = [_oracle_compute(r, world, k, v) for r in range(world)]
+    f64 = dict(dtype=torch.float64)
+    shp = (world, BP, H, 1, D)
+    rec = H * 1 * (D + 2)
+    bufs = [StepBuffers(torch.empty(shp, **f64), torch.empty(shp, **f64), torch.empty((world, BP, rec), **f64),
+                        torch.empty((world, BP, rec), **f64), (H, 1, D)) for _ in range(world)]
+    outs = [torch.empty((BP, H, 1, D), **f64) for _ in range(world)]
+    qs = [torch.from_numpy(q[r * BP:(r + 1) * BP].copy()) for r in range(world)]
+    LocalWorld.decode_step(qs, comps, bufs, outs)
+    for r in range(world):
+        for i in range(BP):
+            b = r * BP + i
+            for h in range(H):
+                kk = np.concatenate([k[dom, b, h] for dom in range(world)])
+                vv = np.concatenate([v[dom, b, h] for dom in range(world)])
+                plain = C.shard_attention(q[b, h], kk, vv)[0]
+                assert np.abs(outs[r][i, h].numpy() - plain).max() < 1e-8, (r, i, h)
