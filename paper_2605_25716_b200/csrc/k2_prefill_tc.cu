@@ -149,6 +149,9 @@ constexpr int kEmuOf4 = SDA_K2_EMU_OF4;
 #ifndef SDA_K2_SPEC
 #define SDA_K2_SPEC 0
 #endif
+#ifndef SDA_K2_MAX4
+#define SDA_K2_MAX4 0
+#endif
 }  // namespace k2tc
 
 namespace k2tc {
@@ -667,11 +670,25 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                     exp_pass(m_use, true, mr0, mr1);
                 } else {
                     // row max on the raw logits (scale > 0), two new values per 3-input max
+#if SDA_K2_MAX4
+                    // four independent chains: half the dependent FMNMX3 latency of two
+                    float mr2 = -INFINITY, mr3 = -INFINITY;
+#pragma unroll
+                    for (int i = 0; i < 64; i += 4) {
+                        mr0 = tc::fmax3(mr0, __uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
+                        mr1 = tc::fmax3(mr1, __uint_as_float(s[2 * i + 2]), __uint_as_float(s[2 * i + 3]));
+                        mr2 = tc::fmax3(mr2, __uint_as_float(s[2 * i + 4]), __uint_as_float(s[2 * i + 5]));
+                        mr3 = tc::fmax3(mr3, __uint_as_float(s[2 * i + 6]), __uint_as_float(s[2 * i + 7]));
+                    }
+                    mr0 = fmaxf(mr0, mr2);
+                    mr1 = fmaxf(mr1, mr3);
+#else
 #pragma unroll
                     for (int i = 0; i < 64; i += 2) {
                         mr0 = tc::fmax3(mr0, __uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
                         mr1 = tc::fmax3(mr1, __uint_as_float(s[2 * i + 2]), __uint_as_float(s[2 * i + 3]));
                     }
+#endif
                 }
                 const float mt = fmaxf(mr0, mr1) * p.scale_log2;
                 const float m_new = fmaxf(m_run, mt);
