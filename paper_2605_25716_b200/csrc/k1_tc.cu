@@ -180,12 +180,14 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
                 src[k] = r < nrows ? (pm ? (int32_t)__ldg(pm + r) : (int32_t)(t * S::TILE + r)) : -1;
             }
         };
-        int32_t cur[NR], nxt[NR], nxt2[NR];
-        fetch_src(0, cur);
-        if (1 < ntiles) fetch_src(1, nxt);
-        for (int64_t it = 0; it < ntiles; ++it) {
+        // three index buffers used in rotation with static names (the loop is unrolled by 3): tile
+        // it's indices were loaded two tiles earlier and nothing copies a register whose load may
+        // still be in flight (a cur = nxt move would stall on that load and cut the look-ahead to
+        // one tile -- the perm loads cost ~12 % of K1's bandwidth that way, tools/k1_bench.py)
+        int32_t ia[NR], ib[NR], ic[NR];
+        auto tile = [&](int64_t it, const int32_t (&use)[NR], int32_t (&fetch)[NR]) {
             const int st = (int)(it % ST);
-            if (it + 2 < ntiles) fetch_src(it + 2, nxt2);
+            if (it + 2 < ntiles) fetch_src(it + 2, fetch);
             if (it >= ST) tc::mbar_wait(&empty[st], (uint32_t)(((it / ST) - 1) & 1));
             const int jj = job_of(first + it);
             const K1TcJob& jb = p.job[jj];
@@ -197,14 +199,16 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
                 const int r = r0 + k * RSTEP;
-                if (cur[k] >= 0) tc::cp_async16(a + tc::sw128_off(r, c & 7), xs + (int64_t)cur[k] * D);
+                if (use[k] >= 0) tc::cp_async16(a + tc::sw128_off(r, c & 7), xs + (int64_t)use[k] * D);
             }
             tc::cp_async_arrive_noinc(&full[st]);
-#pragma unroll
-            for (int k = 0; k < NR; ++k) {
-                cur[k] = nxt[k];
-                nxt[k] = nxt2[k];
-            }
+        };
+        fetch_src(0, ia);
+        if (1 < ntiles) fetch_src(1, ib);
+        for (int64_t it = 0; it < ntiles; it += 3) {
+            tile(it, ia, ic);
+            if (it + 1 < ntiles) tile(it + 1, ib, ia);
+            if (it + 2 < ntiles) tile(it + 2, ic, ib);
         }
     } else if (warp == 8) {
         // ------------------------------------------------------------------ MMA issuer

@@ -1,5 +1,6 @@
 """Micro-benchmark of K1 (scramble + permute into the cache): tcgen05 vs SIMT, random vs
-identity token permutation. CUDA-event timed, L2 flushed between launches.
+identity token permutation. CUDA-event timed, L2 flushed between launches by a 256 MB read
+(clean lines: a write flush would leave dirty lines whose write-back lands in the timed launch).
   python tools/k1_bench.py [B H rows d]"""
 import os
 import sys
@@ -20,7 +21,7 @@ def main():
     out = torch.empty_like(x)
     perm_rand = ops.upload_perms([k.span_perm(1, 0, L) for k in kh], dev)
     perm_id = ops.upload_perms([np.arange(L, dtype=np.uint32)] * B, dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = torch.ones(64 << 20, dtype=torch.float32, device=dev)
     nbytes = 2 * x.numel() * 2
     for impl in ("tc", "simt"):
         if impl == "simt":
@@ -30,7 +31,7 @@ def main():
         for name, perm in (("random", perm_rand), ("identity", perm_id), ("none", None)):
             ts = []
             for i in range(8):
-                flush.zero_()
+                flush.sum()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 ops.scramble(x, kd, capi.PHI_INV_T, capi.KEYS_KQ, perm, out=out, key_heads=H)
