@@ -105,8 +105,8 @@ sda_status sda_span_perm(uint64_t token_perm_seed, uint64_t tag, uint64_t first_
 sda_status sda_invert_permutation(const uint32_t* forward, size_t n, uint32_t* inverse);
 
 /* Bytes of one packed device scrambler / one head (phi_kq + phi_v) / one key set. */
-#define SDA_SCRAMBLER_BYTES(d) ((size_t)32 * (size_t)(d))
-#define SDA_KEYSET_HEAD_BYTES(d) ((size_t)64 * (size_t)(d))
+#define SDA_SCRAMBLER_BYTES(d) ((size_t)34 * (size_t)(d))
+#define SDA_KEYSET_HEAD_BYTES(d) ((size_t)68 * (size_t)(d))
 size_t sda_keyset_bytes(uint32_t n_heads, uint32_t head_dim);
 /* FP64 mode key image (the f64 entry points: x / q / kv / out dtype SDA_F64): raw f64 s1, s2 and
  * the u16 permutations + inverses, so the device repeats the reference's f64 operations exactly. */
@@ -115,7 +115,8 @@ size_t sda_keyset_bytes(uint32_t n_heads, uint32_t head_dim);
 size_t sda_keyset_bytes_f64(uint32_t n_heads, uint32_t head_dim);
 sda_status sda_pack_keyset_f64(const sda_host_keyset* ks, uint32_t n_heads, uint32_t head_dim, void* out);
 /* Packs a host key set into the device image (f32 factor tables with the 1/sqrt(d) of the
- * normalised FWHT folded in, u16 permutations and their inverses). `out` is host memory of
+ * normalised FWHT folded in, u16 permutations and their inverses, and the bank-conflict-free
+ * order in which K3's warp forms gather through P2 and P1). `out` is host memory of
  * sda_keyset_bytes(); the caller uploads it (cudaMemcpyAsync) next to its other key sets. */
 sda_status sda_pack_keyset(const sda_host_keyset* ks, uint32_t n_heads, uint32_t head_dim, void* out);
 

@@ -354,8 +354,8 @@ __device__ __forceinline__ uint2 ll_load(const void* p, uint32_t e) {
 
 __host__ __device__ __forceinline__ const uint8_t* scrambler_ptr(const void* keys, int64_t batch_stride,
                                                                  int64_t b, int kh, int d, int which) {
-    return static_cast<const uint8_t*>(keys) + b * batch_stride + (int64_t)kh * 64 * d +
-           (int64_t)which * 32 * d;
+    return static_cast<const uint8_t*>(keys) + b * batch_stride + (int64_t)kh * SDA_KEYSET_HEAD_BYTES(d) +
+           (int64_t)which * SDA_SCRAMBLER_BYTES(d);
 }
 
 }  // namespace sda

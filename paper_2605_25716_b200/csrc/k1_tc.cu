@@ -267,8 +267,7 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
                 const int64_t slab = (id - p.job_tile0[jj]) / jb.tiles_per_slab;
                 const int H = jb.n_heads, G = H / jb.key_heads;
                 const int64_t b = slab / H;
-                const uint8_t* sc = jb.keys + b * jb.keys_bstride + (int64_t)((slab % H) / G) * 64 * D +
-                                    (int64_t)jb.which * 32 * D;
+                const uint8_t* sc = scrambler_ptr(jb.keys, jb.keys_bstride, b, (int)((slab % H) / G), D, jb.which);
                 // the four tables (s_in, s_out, P1, P2^-1) into SMEM once, then B from SMEM: the
                 // 16 K-chunks per thread no longer wait on global loads
                 float* const kt_in = reinterpret_cast<float*>(smem + S::OFF_KT);

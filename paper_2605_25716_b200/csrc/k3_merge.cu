@@ -484,13 +484,26 @@ __device__ __forceinline__ void fwht_rows(float (&v)[U][E], int lane) {
     }
 }
 
+// x[k & (E-1)] for a run-time k as a tree of E-1 selects on k's bits (keeps x in registers)
+template <int E>
+__device__ __forceinline__ float pick(const float* x, uint32_t k) {
+    if constexpr (E == 1) {
+        return x[0];
+    } else {
+        const float lo = pick<E / 2>(x, k), hi = pick<E / 2>(x + E / 2, k);
+        return (k & (E / 2)) ? hi : lo;
+    }
+}
+
 // Prefill-shaped merge (q_rows >= 64, plain memory, <= 8 sources): a CTA owns 64 consecutive
 // rows of one (request, head), so the phi_V^-1 tables of its sources are staged in shared memory
 // once per CTA (k3_merge_small_kernel re-reads them from L1 for every row: the u16 permutation
 // loads alone were most of its L1 traffic). Per row: coalesced 16-byte loads of every source's O'
 // row, the weighted sum in scrambled space per key group, and one unscramble per group through the
 // warp's shared-memory row (P2 gather -> 2 register + 5 shuffle butterfly stages -> P1 gather),
-// then coalesced stores. The p_q^-1 row indices of a warp's 16 rows are fetched in one load per
+// then coalesced stores. Both gathers follow the key image's schedules (kSchedOff): every load
+// instruction's 32 addresses fall in 32 distinct banks, so a gather costs E wavefronts, not the
+// ~2E a random permutation's collisions cost. The p_q^-1 row indices of a warp's 16 rows are fetched in one load per
 // source up front, and U rows' stats and O' of every source are requested before any is used.
 template <int D, typename TOut, int NS, bool EXACT>
 __global__ void __launch_bounds__(128) k3_rows_kernel(const K3Params p) {
@@ -499,8 +512,11 @@ __global__ void __launch_bounds__(128) k3_rows_kernel(const K3Params p) {
     constexpr int RPW = 16;                    // rows per warp; 64 per CTA
     __shared__ __align__(16) float s_in[NS][D];    // InvIn (1 / s2)
     __shared__ __align__(16) float s_out[NS][D];   // InvOut (1 / (s1 sqrt(d)))
-    __shared__ __align__(16) uint16_t s_p2[NS][D];
-    __shared__ __align__(16) uint16_t s_p1[NS][D];
+    // the two gathers of the unscramble in the key set's bank-conflict-free order (keys.cpp
+    // gather_schedule): load k of lane l reads address s_g2[s][k*32+l] (the 32 addresses of a load
+    // hit 32 different banks); element e of the lane's E is the value of load (s_k2[s][l] >> 4e) & 15
+    __shared__ __align__(16) uint16_t s_g2[NS][D], s_g1[NS][D];
+    __shared__ uint32_t s_k2[NS][32], s_k1[NS][32];
     __shared__ __align__(16) float s_row[4][U][D];
     const int n = EXACT ? NS : p.n_src;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -513,11 +529,22 @@ __global__ void __launch_bounds__(128) k3_rows_kernel(const K3Params p) {
         const uint8_t* sc = scrambler_ptr(p.src[s].keys, p.keys_bstride, b, kh, D, 1);
         const float* ftab = reinterpret_cast<const float*>(sc);
         const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + 24 * D);
+        const uint8_t* sch = sc + kSchedOff * D;
         for (int j = threadIdx.x; j < D; j += blockDim.x) {
             s_in[s][j] = ftab[kInvIn * D + j];
             s_out[s][j] = ftab[kInvOut * D + j];
-            s_p2[s][j] = utab[kP2 * D + j];
-            s_p1[s][j] = utab[kP1 * D + j];
+            const int l = j / E, k = j % E;   // schedule entry (lane l, load k) -> slot k*32 + l
+            s_g2[s][k * 32 + l] = utab[kP2 * D + l * E + sch[kSchedP2 * D + j]];
+            s_g1[s][k * 32 + l] = utab[kP1 * D + l * E + sch[kSchedP1 * D + j]];
+        }
+        for (int l = threadIdx.x; l < 32; l += blockDim.x) {
+            uint32_t k2 = 0, k1 = 0;
+            for (int k = 0; k < E; ++k) {
+                k2 |= (uint32_t)k << (4 * sch[kSchedP2 * D + l * E + k]);
+                k1 |= (uint32_t)k << (4 * sch[kSchedP1 * D + l * E + k]);
+            }
+            s_k2[s][l] = k2;
+            s_k1[s][l] = k1;
         }
     }
     pdl_wait();   // launched early behind K2 (PDL): its partials must be complete
@@ -599,15 +626,16 @@ __global__ void __launch_bounds__(128) k3_rows_kernel(const K3Params p) {
             if (!group_end) continue;
             if (src.keys) {   // one unscramble per key group (linearity)
                 // t = acc / s2 ; u[j] = t[P2[j]] ; w = H u ; y[i] = w[P1[i]] / (s1[i] sqrt(d))
-                float tin[E], tout[E], v[U][E];
-                uint16_t p2[E], p1[E];
+                float tin[E], tout[E], v[U][E], x[E];
+                int g2[E], g1[E];
                 load_vec_any<E>(&s_in[s][lane * E], tin);
                 load_vec_any<E>(&s_out[s][lane * E], tout);
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    p2[e] = s_p2[s][lane * E + e];
-                    p1[e] = s_p1[s][lane * E + e];
+                for (int k = 0; k < E; ++k) {
+                    g2[k] = s_g2[s][k * 32 + lane];
+                    g1[k] = s_g1[s][k * 32 + lane];
                 }
+                const uint32_t k2 = s_k2[s][lane], k1 = s_k1[s][lane];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
 #pragma unroll
@@ -616,18 +644,24 @@ __global__ void __launch_bounds__(128) k3_rows_kernel(const K3Params p) {
                 }
                 __syncwarp();
 #pragma unroll
-                for (int u = 0; u < U; ++u)
+                for (int u = 0; u < U; ++u) {   // u[j] = t[P2[j]] over conflict-free loads
 #pragma unroll
-                    for (int e = 0; e < E; ++e) v[u][e] = rows[u][p2[e]];
+                    for (int k = 0; k < E; ++k) x[k] = rows[u][g2[k]];
+#pragma unroll
+                    for (int e = 0; e < E; ++e) v[u][e] = pick<E>(x, k2 >> (4 * e));
+                }
                 fwht_rows<U, E>(v, lane);
                 __syncwarp();
 #pragma unroll
                 for (int u = 0; u < U; ++u) store_vec_any<E>(rows[u] + lane * E, v[u]);
                 __syncwarp();
 #pragma unroll
-                for (int u = 0; u < U; ++u)
+                for (int u = 0; u < U; ++u) {   // y[i] = w[P1[i]] InvOut[i]
 #pragma unroll
-                    for (int e = 0; e < E; ++e) out[u][e] = fmaf(rows[u][p1[e]], tout[e], out[u][e]);
+                    for (int k = 0; k < E; ++k) x[k] = rows[u][g1[k]];
+#pragma unroll
+                    for (int e = 0; e < E; ++e) out[u][e] = fmaf(pick<E>(x, k1 >> (4 * e)), tout[e], out[u][e]);
+                }
                 __syncwarp();
             } else {
 #pragma unroll

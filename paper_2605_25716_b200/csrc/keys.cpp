@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <vector>
 
 #include "sdattn_b200.h"
@@ -79,6 +80,44 @@ static void draw_scrambler(size_t d, double lo, double hi, int mode, SplitMix64&
     }
 }
 
+// Bank-conflict-free gather order through permutation q (sdattn_internal.h, kSched*): the
+// lanes x banks multigraph with an edge (l, q[l*E+e] % 32) per element is E-regular, so E
+// rounds of Kuhn's augmenting-path matching each find a perfect matching of the edges left.
+static void gather_schedule(size_t d, const uint32_t* q, uint8_t* sched) {
+    const int E = static_cast<int>(d / 32);
+    if (E < 1) return;
+    std::vector<uint8_t> used(d, 0);   // element l*E+e already scheduled
+    for (int k = 0; k < E; ++k) {
+        int bank_of_lane[32], lane_of_bank[32], elem_of_lane[32];
+        for (int i = 0; i < 32; ++i) bank_of_lane[i] = lane_of_bank[i] = elem_of_lane[i] = -1;
+        for (int l = 0; l < 32; ++l) {
+            bool seen[32] = {};
+            std::function<bool(int)> augment = [&](int lane) -> bool {
+                for (int e = 0; e < E; ++e) {
+                    const size_t j = static_cast<size_t>(lane) * E + e;
+                    if (used[j]) continue;
+                    const int bnk = static_cast<int>(q[j] % 32);
+                    if (seen[bnk]) continue;
+                    seen[bnk] = true;
+                    if (lane_of_bank[bnk] < 0 || augment(lane_of_bank[bnk])) {
+                        lane_of_bank[bnk] = lane;
+                        bank_of_lane[lane] = bnk;
+                        elem_of_lane[lane] = e;
+                        return true;
+                    }
+                }
+                return false;
+            };
+            augment(l);   // a perfect matching exists (regular bipartite multigraph): always succeeds
+        }
+        for (int l = 0; l < 32; ++l) {
+            const int e = elem_of_lane[l] < 0 ? 0 : elem_of_lane[l];
+            sched[l * E + k] = static_cast<uint8_t>(e);
+            used[static_cast<size_t>(l) * E + e] = 1;
+        }
+    }
+}
+
 // Packed device scrambler (SDA_SCRAMBLER_BYTES(d) bytes), see sdattn_internal.h.
 static void pack_scrambler(size_t d, const double* s1, const uint32_t* p1, const uint32_t* p2,
                            const double* s2, uint8_t* dst) {
@@ -97,6 +136,10 @@ static void pack_scrambler(size_t d, const double* s1, const uint32_t* p1, const
         u[kP1Inv * d + p1[i]] = static_cast<uint16_t>(i);
         u[kP2Inv * d + p2[i]] = static_cast<uint16_t>(i);
     }
+    uint8_t* sch = dst + kSchedOff * d;
+    std::fill(sch, sch + 2 * d, uint8_t{0});
+    gather_schedule(d, p2, sch + kSchedP2 * d);
+    gather_schedule(d, p1, sch + kSchedP1 * d);
 }
 
 // FP64 mode scrambler (SDA_SCRAMBLER_BYTES_F64(d) bytes): f64 [2][d] = {s1, s2}, then the u16

@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(288, 1) kp_tc_kernel(const KpParams p, const _
         const int row = tid;
         {   // B for (request b, key head of h), as k1_tc.cu builds it
             const int G = p.n_heads / p.key_heads;
-            const uint8_t* sc = p.keys + b * p.keys_bstride + (int64_t)(h / G) * 64 * D + (int64_t)p.which * 32 * D;
+            const uint8_t* sc = scrambler_ptr(p.keys, p.keys_bstride, b, h / G, D, p.which);
             float* const kt_in = reinterpret_cast<float*>(smem + S::OFF_KT);
             float* const kt_out = kt_in + D;
             uint16_t* const kt_p1 = reinterpret_cast<uint16_t*>(kt_out + D);

@@ -9,8 +9,14 @@ namespace sda {
 
 constexpr int kMaxPeers = 16;
 
-// Packed device scrambler for head dim d (SDA_SCRAMBLER_BYTES(d) = 32 d bytes):
-//   f32 tables [6][d] then u16 tables [4][d].
+// Packed device scrambler for head dim d (SDA_SCRAMBLER_BYTES(d) = 34 d bytes):
+//   f32 tables [6][d], u16 tables [4][d], then u8 gather schedules [2][d] (d >= 32; zero below):
+//   a warp that owns elements [lane*E, lane*E+E) (E = d/32) and gathers them through a permutation
+//   Q from a row in shared memory issues E loads; in load k lane l takes its element
+//   e = sched[l*E + k], chosen so that the 32 addresses Q[l*E + e] of every load fall in 32
+//   different banks. Q's values mod 32 put exactly E of a lane's and E of a bank's elements on each
+//   side of a lanes x banks multigraph that is E-regular, so it splits into E perfect matchings
+//   (Konig) -- one per load. kSchedP2: the gather u[j] = t[P2[j]]; kSchedP1: y[i] = w[P1[i]].
 // With R = 1/sqrt(d) (the normalised FWHT scale, fwht.cpp:24) and the raw +-1 butterfly H:
 //   x phi      : y[k] = OutFwd[k]  * H(u)[P2Inv[k]],  u[P1[i]] = x[i] * InFwd[i]
 //   x phi^{-T} : y[k] = OutInvT[k] * H(u)[P2Inv[k]],  u[P1[i]] = x[i] * InInvT[i]
@@ -18,6 +24,9 @@ constexpr int kMaxPeers = 16;
 // (scrambler.cpp:42-63 with the componentwise steps folded into gathers / scatters.)
 enum : int { kInFwd = 0, kInInvT = 1, kOutFwd = 2, kOutInvT = 3, kInvIn = 4, kInvOut = 5 };
 enum : int { kP1 = 0, kP2 = 1, kP1Inv = 2, kP2Inv = 3 };
+enum : int { kSchedP2 = 0, kSchedP1 = 1 };
+constexpr int kU16Off = 24;   // u16 tables at 24 d bytes
+constexpr int kSchedOff = 32; // u8 schedules at 32 d bytes
 
 uint64_t derive(uint64_t base, const uint64_t* tags, size_t n);
 void count_launch();   // sda_launch_count() bookkeeping for kernels launched outside capi.cu
