@@ -274,11 +274,11 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 template <typename Kern, typename... Args>
-inline cudaError_t pdl_launch(Kern kernel, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+inline cudaError_t pdl_launch_smem(Kern kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -286,6 +286,10 @@ inline cudaError_t pdl_launch(Kern kernel, dim3 grid, dim3 block, cudaStream_t s
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+template <typename Kern, typename... Args>
+inline cudaError_t pdl_launch(Kern kernel, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+    return pdl_launch_smem(kernel, grid, block, 0, st, args...);
 }
 
 // raise a peer's flag to the step epoch with a system-scope release store (the waiting side

@@ -136,6 +136,8 @@ struct K3Params {
 #include <cuda_runtime.h>
 namespace sda {
 cudaError_t launch_k1(const K1Params& p, int d, int xdt, int odt, int64_t n_batch, cudaStream_t st);
+// K3 on the tensor cores (k3_tc.cu); cudaErrorNotSupported when the merge is not eligible
+cudaError_t launch_k3_tc(const K3Params& p, int d, int odt, cudaStream_t st);
 bool k1_tc_eligible(const K1Params& p, int d, int xdt, int odt);
 cudaError_t launch_k1_tc(const K1Params& p, int d, int64_t n_batch, cudaStream_t st);
 cudaError_t launch_quantize(const void* x, int dt, int64_t n, int64_t count, int bits, uint8_t* codes,
