@@ -17,7 +17,6 @@
 
 #include "common.cuh"
 #include "quant.cuh"
-#include "tc_util.cuh"
 
 namespace sda {
 
@@ -497,44 +496,31 @@ __device__ __forceinline__ float pick(const float* x, uint32_t k) {
     }
 }
 
-// Prefill-shaped merge (q_rows >= 64, plain memory, <= 8 sources, 16-byte aligned O'): a CTA owns
-// 64 consecutive rows of one (request, head) -- 16 per warp -- so the phi_V^-1 tables of its
-// sources are staged in shared memory once per CTA. Each warp streams its rows' O' (one row of
-// every source per slot) into a private shared-memory ring with 1D bulk copies (TMA engine,
-// mbarrier completion), issued as soon as the p_q^-1 indices are known: up to 16 rows x 4d bytes
-// per warp are in flight from the first cycle instead of U rows per load-compute round trip. Per
-// row, the P2 gather of the unscramble reads the ring directly -- the weighted sum over a key
-// group's sources is formed per gathered element, times InvIn[P2[j]] -- then 2 register + 5
-// shuffle butterfly stages, the P1 gather through a per-warp scratch row, and coalesced stores.
-// Both gathers follow the key image's schedules (kSchedOff): every load instruction's 32
-// addresses fall in 32 distinct banks. Arithmetic per element is the same as k3_merge_small's.
-template <int D, int NS>
-struct K3RowsCfg {
-    static constexpr int E = D / 32;
-    static constexpr int U = NS >= 4 ? 1 : 4 / NS;   // rows in lockstep per warp
-    static constexpr int RPW = 16;                   // rows per warp; 64 per CTA
-    static constexpr int RING = 16 / NS;             // ring slots per warp (a slot = NS rows of O')
-    static constexpr size_t kRing = (size_t)4 * RING * NS * D * 4;
-    static constexpr size_t kSmem = kRing + (size_t)4 * U * D * 4;   // + per-warp scratch rows
-};
-
+// Prefill-shaped merge (q_rows >= 64, plain memory, <= 8 sources): a CTA owns 64 consecutive
+// rows of one (request, head), so the phi_V^-1 tables of its sources are staged in shared memory
+// once per CTA (k3_merge_small_kernel re-reads them from L1 for every row: the u16 permutation
+// loads alone were most of its L1 traffic). Per row: coalesced 16-byte loads of every source's O'
+// row, the weighted sum in scrambled space per key group, and one unscramble per group through the
+// warp's shared-memory row (P2 gather -> 2 register + 5 shuffle butterfly stages -> P1 gather),
+// then coalesced stores. Both gathers follow the key image's schedules (kSchedOff): every load
+// instruction's 32 addresses fall in 32 distinct banks, so a gather costs E wavefronts, not the
+// ~2E a random permutation's collisions cost. The p_q^-1 row indices of a warp's 16 rows are fetched in one load per
+// source up front, and U rows' stats and O' of every source are requested before any is used.
 template <int D, typename TOut, int NS, bool EXACT>
 __global__ void __launch_bounds__(128) k3_rows_kernel(const K3Params p) {
-    using C = K3RowsCfg<D, NS>;
-    constexpr int E = C::E, U = C::U, RPW = C::RPW, RING = C::RING;
-    static_assert(RING % U == 0 && RPW % RING == 0, "ring geometry");
-    __shared__ __align__(16) float s_tin[NS][D];   // InvIn[P2[j]] (1 / s2 at the gathered index)
+    constexpr int E = D / 32;
+    constexpr int U = NS >= 4 ? 1 : 4 / NS;   // rows in flight per warp
+    constexpr int RPW = 16;                    // rows per warp; 64 per CTA
+    __shared__ __align__(16) float s_in[NS][D];    // InvIn (1 / s2)
     __shared__ __align__(16) float s_out[NS][D];   // InvOut (1 / (s1 sqrt(d)))
-    // load k of lane l reads s_g2[s][k*32+l] (32 distinct banks per load, keys.cpp gather_schedule);
-    // element e of the lane's E is the value of load (s_k2[s][l] >> 4e) & 15
+    // the two gathers of the unscramble in the key set's bank-conflict-free order (keys.cpp
+    // gather_schedule): load k of lane l reads address s_g2[s][k*32+l] (the 32 addresses of a load
+    // hit 32 different banks); element e of the lane's E is the value of load (s_k2[s][l] >> 4e) & 15
     __shared__ __align__(16) uint16_t s_g2[NS][D], s_g1[NS][D];
     __shared__ uint32_t s_k2[NS][32], s_k1[NS][32];
-    __shared__ __align__(8) uint64_t s_bar[4][RING];
-    extern __shared__ __align__(128) float k3_dyn[];
+    __shared__ __align__(16) float s_row[4][U][D];
     const int n = EXACT ? NS : p.n_src;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* const ring = k3_dyn + (size_t)warp * RING * NS * D;           // [RING][NS][D]
-    float* const scratch = k3_dyn + (size_t)4 * RING * NS * D + (size_t)warp * U * D;
     const int64_t bh = blockIdx.y;
     const int h = (int)(bh % p.q_heads);
     const int64_t b = bh / p.q_heads;
@@ -543,10 +529,10 @@ __global__ void __launch_bounds__(128) k3_rows_kernel(const K3Params p) {
         if (!p.src[s].keys) continue;
         const uint8_t* sc = scrambler_ptr(p.src[s].keys, p.keys_bstride, b, kh, D, 1);
         const float* ftab = reinterpret_cast<const float*>(sc);
-        const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + kU16Off * D);
+        const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + 24 * D);
         const uint8_t* sch = sc + kSchedOff * D;
         for (int j = threadIdx.x; j < D; j += blockDim.x) {
-            s_tin[s][j] = ftab[kInvIn * D + utab[kP2 * D + j]];
+            s_in[s][j] = ftab[kInvIn * D + j];
             s_out[s][j] = ftab[kInvOut * D + j];
             const int l = j / E, k = j % E;   // schedule entry (lane l, load k) -> slot k*32 + l
             s_g2[s][k * 32 + l] = utab[kP2 * D + l * E + sch[kSchedP2 * D + j]];
@@ -562,179 +548,156 @@ __global__ void __launch_bounds__(128) k3_rows_kernel(const K3Params p) {
             s_k1[s][l] = k1;
         }
     }
-    if (lane == 0)
-        for (int i = 0; i < RING; ++i) tc::mbar_init(&s_bar[warp][i], 1);
-    tc::fence_mbar_init();
     pdl_wait();   // launched early behind K2 (PDL): its partials must be complete
     __syncthreads();
 
     const int64_t r_base = (int64_t)blockIdx.x * (4 * RPW) + warp * RPW;
-    const int nvalid = (int)(p.q_rows - r_base < RPW ? (p.q_rows - r_base > 0 ? p.q_rows - r_base : 0) : RPW);
-    // lane t < RPW: source s's O' row index and stats for output row r_base + t
-    uint32_t ridx[NS];
-    float2 stv[NS];
+    uint32_t ridx[NS];   // lane t < RPW: source s's O' row for output row r_base + t
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        ridx[s] = 0;
+        if ((EXACT || s < n) && lane < RPW && r_base + lane < p.q_rows)
+            ridx[s] = p.src[s].pq_inv ? p.src[s].pq_inv[b * p.pq_bstride + r_base + lane] : (uint32_t)(r_base + lane);
+    }
+    // per-source bases of this (request, head): a row is then one 32-bit multiply-add away
     const float* obase[NS];
+    const float* sbase[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
         const K3Source& src = p.src[s];
         const int64_t off = src.bstride ? b * src.bstride + (int64_t)h * p.q_rows * D : bh * p.q_rows * D;
         const int64_t soff = src.bstride ? b * src.bstride + (int64_t)h * p.q_rows * 2 : bh * p.q_rows * 2;
         obase[s] = (EXACT || s < n) ? src.o + off : nullptr;
-        ridx[s] = 0;
-        stv[s] = make_float2(-INFINITY, 0.f);
-        if ((EXACT || s < n) && lane < nvalid) {
-            ridx[s] = src.pq_inv ? src.pq_inv[b * p.pq_bstride + r_base + lane] : (uint32_t)(r_base + lane);
-            stv[s] = *reinterpret_cast<const float2*>(src.stats + soff + (size_t)ridx[s] * 2);
-        }
+        sbase[s] = (EXACT || s < n) ? src.stats + soff : nullptr;
     }
-    // O' rows of row t into slot t % RING: one bulk copy per source, all on the slot's barrier
-    auto issue = [&](int t) {
-        if (t >= nvalid) return;
-        uint64_t* bar = &s_bar[warp][t % RING];
-        float* dst = ring + (size_t)(t % RING) * NS * D;
-        uint32_t ri[NS];
-#pragma unroll
-        for (int s = 0; s < NS; ++s) ri[s] = __shfl_sync(0xffffffffu, ridx[s], t);
-        if (lane == 0) {
-            tc::mbar_arrive_expect_tx(bar, (uint32_t)(n * D * 4));
-#pragma unroll
-            for (int s = 0; s < NS; ++s)
-                if (EXACT || s < n) tc::bulk_g2s(dst + s * D, obase[s] + (size_t)ri[s] * D, D * 4, bar);
-        }
-    };
-#pragma unroll 1
-    for (int t = 0; t < RING; ++t) issue(t);
-
     TOut* const obh = static_cast<TOut*>(p.out) + (p.out_bstride ? b * p.out_bstride + (int64_t)h * p.q_rows * D : bh * p.q_rows * D);
     float* const sbh = p.out_stats ? p.out_stats + (p.out_bstride ? b * p.out_bstride + (int64_t)h * p.q_rows * 2 : bh * p.q_rows * 2)
                                    : nullptr;
+    float* rows[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) rows[u] = s_row[warp][u];
     const bool single = n == 1;
-#pragma unroll 1
-    for (int t0 = 0; t0 < nvalid; t0 += U) {
+    for (int t0 = 0; t0 < RPW; t0 += U) {
         float2 st[U][NS];
-        const float* slot[U];
-        float mstar[U], denom[U], acc[U][E], out[U][E], v[U][E], x[E];
+        float xv[U][NS][E];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const bool valid = t0 + u < nvalid;
-            slot[u] = ring + (size_t)((t0 + u) % RING) * NS * D;
-            mstar[u] = -INFINITY;   // attention.cpp:103-105
+            const bool valid = r_base + t0 + u < p.q_rows;
 #pragma unroll
             for (int s = 0; s < NS; ++s) {
-                st[u][s].x = __shfl_sync(0xffffffffu, stv[s].x, t0 + u);
-                st[u][s].y = __shfl_sync(0xffffffffu, stv[s].y, t0 + u);
-                if (!valid) st[u][s] = make_float2(-INFINITY, 0.f);
-                if ((EXACT || s < n) && st[u][s].y > 0.f) mstar[u] = fmaxf(mstar[u], st[u][s].x);
+                const uint32_t ri = __shfl_sync(0xffffffffu, ridx[s], t0 + u);
+                if ((EXACT || s < n) && valid) {
+                    st[u][s] = *reinterpret_cast<const float2*>(sbase[s] + (size_t)ri * 2);
+                    load_vec_any<E>(obase[s] + (size_t)ri * D + lane * E, xv[u][s]);
+                } else {
+                    st[u][s] = make_float2(-INFINITY, 0.f);
+#pragma unroll
+                    for (int e = 0; e < E; ++e) xv[u][s][e] = 0.f;
+                }
             }
+        }
+        // the U rows go through every step together (one loop nest per step), so their shared-memory
+        // round trips and shuffle stages overlap instead of forming U dependent chains
+        float mstar[U], denom[U], acc[U][E], out[U][E];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            mstar[u] = -INFINITY;   // attention.cpp:103-105
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+                if ((EXACT || s < n) && st[u][s].y > 0.f) mstar[u] = fmaxf(mstar[u], st[u][s].x);
             denom[u] = 0.f;
 #pragma unroll
             for (int e = 0; e < E; ++e) acc[u][e] = out[u][e] = 0.f;
-            if (valid) tc::mbar_wait(&s_bar[warp][(t0 + u) % RING], ((t0 + u) / RING) & 1);
         }
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
             if (!(EXACT || s < n)) continue;
             const K3Source& src = p.src[s];
-            float w[U];
-            bool live[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 // a source with no visible key (exp_sum 0) adds nothing: a zero weight rather than a
                 // branch, so the unscramble below stays warp-uniform code
-                live[u] = st[u][s].y > 0.f;
-                w[u] = live[u] ? (single ? 1.f : st[u][s].y * expf(st[u][s].x - mstar[u])) : 0.f;
-                denom[u] += single ? st[u][s].y : w[u];
+                const bool live = st[u][s].y > 0.f;
+                const float w = live ? (single ? 1.f : st[u][s].y * expf(st[u][s].x - mstar[u])) : 0.f;
+                denom[u] += single ? st[u][s].y : w;
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc[u][e] = live ? fmaf(w, xv[u][s][e], acc[u][e]) : acc[u][e];   // never 0 * NaN
             }
-            if (!src.keys) {   // plaintext source (the inquirer's own span): natural order
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    load_vec_any<E>(slot[u] + s * D + lane * E, x);
-#pragma unroll
-                    for (int e = 0; e < E; ++e) out[u][e] = live[u] ? fmaf(w[u], x[e], out[u][e]) : out[u][e];
-                }
-                continue;
-            }
-            // acc[u][k] = sum over the group's sources of w * O'[P2[g2[k]]] (gather order k)
-            int g2[E];
-#pragma unroll
-            for (int k = 0; k < E; ++k) g2[k] = s_g2[s][k * 32 + lane];
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-#pragma unroll
-                for (int k = 0; k < E; ++k) {
-                    const float xo = slot[u][s * D + g2[k]];
-                    acc[u][k] = live[u] ? fmaf(w[u], xo, acc[u][k]) : acc[u][k];   // never 0 * NaN
-                }
             const bool group_end = (s + 1 == n) || (p.src[s + 1].keys != src.keys);
             if (!group_end) continue;
-            // one unscramble per key group (linearity):
-            // u[j] = acc[P2[j]] / s2[P2[j]] ; w = H u ; y[i] = w[P1[i]] / (s1[i] sqrt(d))
-            float tin[E], tout[E];
-            int g1[E];
-            load_vec_any<E>(&s_tin[s][lane * E], tin);
-            load_vec_any<E>(&s_out[s][lane * E], tout);
+            if (src.keys) {   // one unscramble per key group (linearity)
+                // t = acc / s2 ; u[j] = t[P2[j]] ; w = H u ; y[i] = w[P1[i]] / (s1[i] sqrt(d))
+                float tin[E], tout[E], v[U][E], x[E];
+                int g2[E], g1[E];
+                load_vec_any<E>(&s_in[s][lane * E], tin);
+                load_vec_any<E>(&s_out[s][lane * E], tout);
 #pragma unroll
-            for (int k = 0; k < E; ++k) g1[k] = s_g1[s][k * 32 + lane];
-            const uint32_t k2 = s_k2[s][lane], k1 = s_k1[s][lane];
+                for (int k = 0; k < E; ++k) {
+                    g2[k] = s_g2[s][k * 32 + lane];
+                    g1[k] = s_g1[s][k * 32 + lane];
+                }
+                const uint32_t k2 = s_k2[s][lane], k1 = s_k1[s][lane];
 #pragma unroll
-            for (int u = 0; u < U; ++u)
+                for (int u = 0; u < U; ++u) {
 #pragma unroll
-                for (int e = 0; e < E; ++e) v[u][e] = __fmul_rn(pick<E>(acc[u], k2 >> (4 * e)), tin[e]);   // not contracted into the FWHT
-            fwht_rows<U, E>(v, lane);
+                    for (int e = 0; e < E; ++e) v[u][e] = acc[u][e] * tin[e];
+                    store_vec_any<E>(rows[u] + lane * E, v[u]);
+                }
+                __syncwarp();
 #pragma unroll
-            for (int u = 0; u < U; ++u) store_vec_any<E>(scratch + u * D + lane * E, v[u]);
-            __syncwarp();
+                for (int u = 0; u < U; ++u) {   // u[j] = t[P2[j]] over conflict-free loads
 #pragma unroll
-            for (int u = 0; u < U; ++u) {   // y[i] = w[P1[i]] InvOut[i]
+                    for (int k = 0; k < E; ++k) x[k] = rows[u][g2[k]];
 #pragma unroll
-                for (int k = 0; k < E; ++k) x[k] = scratch[u * D + g1[k]];
+                    for (int e = 0; e < E; ++e) v[u][e] = pick<E>(x, k2 >> (4 * e));
+                }
+                fwht_rows<U, E>(v, lane);
+                __syncwarp();
 #pragma unroll
-                for (int e = 0; e < E; ++e) out[u][e] = fmaf(pick<E>(x, k1 >> (4 * e)), tout[e], out[u][e]);
+                for (int u = 0; u < U; ++u) store_vec_any<E>(rows[u] + lane * E, v[u]);
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < U; ++u) {   // y[i] = w[P1[i]] InvOut[i]
+#pragma unroll
+                    for (int k = 0; k < E; ++k) x[k] = rows[u][g1[k]];
+#pragma unroll
+                    for (int e = 0; e < E; ++e) out[u][e] = fmaf(pick<E>(x, k1 >> (4 * e)), tout[e], out[u][e]);
+                }
+                __syncwarp();
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int e = 0; e < E; ++e) out[u][e] += acc[u][e];
             }
-            __syncwarp();
 #pragma unroll
             for (int u = 0; u < U; ++u)
 #pragma unroll
                 for (int e = 0; e < E; ++e) acc[u][e] = 0.f;
         }
-        // every lane is done with these slots: refill them with rows t0 + RING ..
-        __syncwarp();
-        if (t0 + RING < nvalid) {
-            tc::fence_proxy_async_smem();
-#pragma unroll
-            for (int u = 0; u < U; ++u) issue(t0 + u + RING);
-        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t r = r_base + t0 + u;
-            if (t0 + u >= nvalid) continue;
+            const bool valid = r < p.q_rows;
             const bool masked = !(mstar[u] > -INFINITY);
-            if (masked && lane == 0 && p.err) atomicExch(p.err, (int32_t)SDA_ERR_MASKED_ROW);
+            if (masked && lane == 0 && p.err && valid) atomicExch(p.err, (int32_t)SDA_ERR_MASKED_ROW);
             const float inv = masked ? __int_as_float(0x7fc00000) : (single ? 1.f : 1.f / denom[u]);
 #pragma unroll
             for (int e = 0; e < E; ++e) out[u][e] *= inv;
-            store_vec_any<E>(obh + (size_t)r * D + lane * E, out[u]);
-            if (sbh && lane == 0)
-                *reinterpret_cast<float2*>(sbh + (size_t)r * 2) =
-                    make_float2(single ? (masked ? -INFINITY : mstar[u]) : mstar[u], masked ? 0.f : denom[u]);
+            if (valid) {
+                store_vec_any<E>(obh + (size_t)r * D + lane * E, out[u]);
+                if (sbh && lane == 0)
+                    *reinterpret_cast<float2*>(sbh + (size_t)r * 2) =
+                        make_float2(single ? (masked ? -INFINITY : mstar[u]) : mstar[u], masked ? 0.f : denom[u]);
+            }
         }
     }
 }
 
 template <int D, typename TOut, int NS, bool EXACT = true>
 static cudaError_t launch_k3_rows(const K3Params& p, cudaStream_t st) {
-    using C = K3RowsCfg<D, NS>;
-    static uint64_t attr_set = 0;   // per device: > 48 KB of dynamic shared memory at d = 256
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return cudaErrorInvalidDevice;
-    if (!(__atomic_load_n(&attr_set, __ATOMIC_ACQUIRE) >> dev & 1)) {
-        const cudaError_t e = cudaFuncSetAttribute(k3_rows_kernel<D, TOut, NS, EXACT>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
-        if (e != cudaSuccess) return e;
-        __atomic_fetch_or(&attr_set, uint64_t(1) << dev, __ATOMIC_ACQ_REL);
-    }
     const dim3 grid((unsigned)((p.q_rows + 63) / 64), (unsigned)(p.n_batch * p.q_heads));
-    return pdl_launch_smem(k3_rows_kernel<D, TOut, NS, EXACT>, grid, dim3(128), C::kSmem, st, p);
+    return pdl_launch(k3_rows_kernel<D, TOut, NS, EXACT>, grid, dim3(128), st, p);
 }
 
 template <int D, typename TOut, int NS, bool EXACT = true>
@@ -765,16 +728,19 @@ static cudaError_t launch_k3_t(const K3Params& p, cudaStream_t st) {
     }
     if (p.ll) return pdl_launch(k3_merge_kernel<D, TOut>, dim3((unsigned)((total + 3) / 4)), dim3(128), st, p);
     const bool small_ok = total < (int64_t(1) << 30) && !getenv("SDA_K3_PIPELINED");
-    // prefill-shaped merges of one key group (+ plaintext): the tensor-core form (k3_tc.cu)
-    if (!getenv("SDA_K3_NO_TC")) {
+    // prefill-shaped merges of one key group (+ plaintext): the tensor-core form (k3_tc.cu) where
+    // it measured faster than the rows kernel -- three or more sources (tools/k3_bench.py: the C5
+    // chunk's 2 splits + own span 82 vs 104 us; with 1-2 sources the rows kernel's 7 CTAs per SM
+    // hide the gathers' latency better than the TC form's single CTA). SDA_K3_TC=1 forces it.
+    if (!getenv("SDA_K3_NO_TC") && (p.n_src >= 3 || getenv("SDA_K3_TC"))) {
         const cudaError_t e = launch_k3_tc(p, D, std::is_same<TOut, float>::value ? SDA_F32 : SDA_BF16, st);
         if (e != cudaErrorNotSupported) return e;
     }
-    // prefill-shaped rows (many per (request, head)): the table-staging, bulk-copy row kernel
-    bool bulk_ok = true;   // its 1D bulk copies need 16-byte aligned O' rows
-    for (int s = 0; s < p.n_src; ++s)
-        bulk_ok = bulk_ok && reinterpret_cast<uintptr_t>(p.src[s].o) % 16 == 0 && p.src[s].bstride * 4 % 16 == 0;
-    if (bulk_ok && p.q_rows >= 64 && p.n_src <= kSmallSrc && p.n_batch * p.q_heads < 65536 && !getenv("SDA_K3_NO_ROWS")) {
+    // prefill-shaped rows (many per (request, head)): the table-staging row kernel
+    // (1-2 sources; with more, a warp's U = 1 row in flight loses to the preload kernel's 2 rows
+    // x all sources in flight: 4 splits 82 vs 55 us, tools/k3_bench.py; SDA_K3_ROWS=1 forces it)
+    if (p.q_rows >= 64 && p.n_batch * p.q_heads < 65536 && !getenv("SDA_K3_NO_ROWS") &&
+        (p.n_src <= 2 || (getenv("SDA_K3_ROWS") && p.n_src <= kSmallSrc))) {
         switch (p.n_src) {
             case 1: return launch_k3_rows<D, TOut, 1>(p, st);
             case 2: return launch_k3_rows<D, TOut, 2>(p, st);

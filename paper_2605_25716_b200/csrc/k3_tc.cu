@@ -34,9 +34,15 @@
 #include "tc_util.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 namespace sda {
+
+// Debug timeline (SDA_K3TC_TRACE=1): clock64 stamps of one split warp and one epilogue warp per
+// CTA, read back with sda_debug_k3tc_trace (tools/k3_trace.py).
+constexpr int kK3TraceSlots = 64;
+__device__ unsigned long long g_k3tc_trace[1024][kK3TraceSlots];
 
 struct K3TcArgs {
     K3Params p;
@@ -46,6 +52,7 @@ struct K3TcArgs {
     int64_t ntr;             // 128-row tiles per (request, head)
     int64_t total_tiles;
     int64_t tiles_per_cta;
+    int trace;
 };
 
 template <int D>
@@ -97,9 +104,9 @@ template <int D, typename TOut, int NK>
 __global__ void __launch_bounds__(384, 1) k3_tc_kernel(const __grid_constant__ K3TcArgs a) {
     using S = K3TcShape<D>;
     constexpr int V = S::V, RPS = S::ROWS_PER_SPLIT;
-    constexpr int RB = 8 / NK;   // rows per split-warp batch (two batches in flight)
-    constexpr int NB = RPS / RB;  // batches per tile (even)
-    static_assert(NK <= 4 && NB % 2 == 0, "batches alternate between two register sets");
+    constexpr int RB = 4 / NK;    // rows per split-warp batch; a ring of four batches, three in flight
+    constexpr int NB = RPS / RB;  // batches per tile (a multiple of 4)
+    static_assert(NK <= 2 && NB % 4 == 0, "batches rotate through four register sets");
     // bf16 parts of t: hi + mid + lo is exact (f32 output); hi + mid carries 16 significant bits
     // (~2^-17 relative), far below the bf16 output's own rounding
     constexpr int NPART = std::is_same<TOut, float>::value ? 3 : 2;
@@ -115,6 +122,9 @@ __global__ void __launch_bounds__(384, 1) k3_tc_kernel(const __grid_constant__ K
     uint32_t* const tmem_slot = reinterpret_cast<uint32_t*>(bready + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    auto stamp = [&](int slot) {
+        if (a.trace && lane == 0 && slot < kK3TraceSlots && blockIdx.x < 1024) g_k3tc_trace[blockIdx.x][slot] = clock64();
+    };
     const int64_t first = (int64_t)blockIdx.x * a.tiles_per_cta;
     const int64_t last = min(first + a.tiles_per_cta, a.total_tiles);
     if (first >= last) return;
@@ -138,6 +148,7 @@ __global__ void __launch_bounds__(384, 1) k3_tc_kernel(const __grid_constant__ K
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_wait();   // launched early behind K2 (PDL): its partials must be complete
+    if (warp == 0) stamp(0);
 
     auto tile_at = [&](int64_t it) {
         K3Tile t;
@@ -301,12 +312,15 @@ __global__ void __launch_bounds__(384, 1) k3_tc_kernel(const __grid_constant__ K
         float2 st_b[NK], stp_b;
         load_ridx(0, tc_, ridx_c);
         load_ridx(1, t1, ridx_b);
+        load_ridx(2, t2, ridx_a);
+        float x0[RB][NK][V], x1[RB][NK][V], x2[RB][NK][V], x3[RB][NK][V];
+        // the first O' rows as soon as their indices arrive (NB >= 4: batches 0-2 are tile 0's)
+        issue(tc_, 0, ridx_c, x0);
+        issue(tc_, 1, ridx_c, x1);
+        issue(tc_, 2, ridx_c, x2);
         load_stats(0, tc_, ridx_c, st_b, stp_b);
         Wts wc = weights(st_b, stp_b);
         load_stats(1, t1, ridx_b, st_b, stp_b);
-        load_ridx(2, t2, ridx_a);
-        float xa[RB][NK][V], xb[RB][NK][V];
-        issue(tc_, 0, ridx_c, xa);
         uint32_t cur = 0xffffffffu, mma_slab = 0xffffffffu, nbuild = 0;
         constexpr uint32_t IDESC = tc::idesc_bf16_f32(128, D, false, false);
 #pragma unroll 1
@@ -320,11 +334,24 @@ __global__ void __launch_bounds__(384, 1) k3_tc_kernel(const __grid_constant__ K
                 cur = tc_.kslab;
             }
             uint8_t* const A = abuf + bi * S::ABUF;
+            // batch q + 3 (this tile's, or the next tile's first ones) into the ring slot batch
+            // q - 1 just left, then batch q
+            // (unconditional -- past the CTA's last tile it re-reads valid rows -- so the loads land
+            // in the ring registers directly, not in temporaries moved over on a branch join)
+            auto ahead = [&](int q, float (&x)[RB][NK][V]) {
+                const bool same = q + 3 < NB || !more;
+                uint32_t r[NK];
+#pragma unroll
+                for (int k = 0; k < NK; ++k) r[k] = same ? ridx_c[k] : ridx_b[k];
+                issue(same ? tc_ : t1, same ? (q + 3) % NB : q + 3 - NB, r, x);
+            };
 #pragma unroll 1
-            for (int q = 0; q < NB; q += 2) {
-                issue(tc_, q + 1, ridx_c, xb);
+            for (int q = 0; q < NB; q += 4) {
+                ahead(q, x3);
                 if (q == 0) {
+                    if (sw == 0 && it < 7) stamp(2 + 8 * (int)it);
                     if (it >= 2) tc::mbar_wait(&afree[bi], (uint32_t)(((it >> 1) - 1) & 1));
+                    if (sw == 0 && it < 7) stamp(3 + 8 * (int)it);
                     // this tile's per-row merge results: for the epilogue, and out_stats / err
                     const int64_t rowj = tc_.row0 + sw * RPS + jr;
                     if (lane < 16 && rowj < p.q_rows) {
@@ -340,20 +367,18 @@ __global__ void __launch_bounds__(384, 1) k3_tc_kernel(const __grid_constant__ K
                         }
                     }
                 }
-                compute(q, wc, xa, A);
-                // next batch into xa: this tile's q + 2, or the next tile's first
-                const bool same = q + 2 < NB;
-                if (same || more) {
-                    uint32_t r[NK];
-#pragma unroll
-                    for (int k = 0; k < NK; ++k) r[k] = same ? ridx_c[k] : ridx_b[k];
-                    issue(same ? tc_ : t1, same ? q + 2 : 0, r, xa);
-                }
-                compute(q + 1, wc, xb, A);
+                compute(q, wc, x0, A);
+                ahead(q + 1, x0);
+                compute(q + 1, wc, x1, A);
+                ahead(q + 2, x1);
+                compute(q + 2, wc, x2, A);
+                ahead(q + 3, x2);
+                compute(q + 3, wc, x3, A);
             }
             tc::fence_proxy_async_smem();   // generic-proxy stores -> tcgen05 (async proxy) reads
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&afull[bi]);
+            if (sw == 0 && it < 7) stamp(4 + 8 * (int)it);
             if (sw == 0) {   // the tile's MMAs, once every split warp has written its rows
                 if (tc_.kslab != mma_slab) {
                     tc::mbar_wait(bready, nbuild & 1);   // the epilogue built this slab's B
@@ -377,6 +402,7 @@ __global__ void __launch_bounds__(384, 1) k3_tc_kernel(const __grid_constant__ K
                     tc::mma_commit(&tfull[bi]);
                 }
                 __syncwarp();
+                if (it < 7) stamp(5 + 8 * (int)it);
             }
             // advance the prep pipeline by one tile
             wc = weights(st_b, stp_b);
@@ -423,14 +449,36 @@ __global__ void __launch_bounds__(384, 1) k3_tc_kernel(const __grid_constant__ K
             }
             tc::fence_proxy_async_smem();   // B (generic stores) -> tcgen05 reads
             tc::mbar_arrive(bready);
+            if (warp == 0) stamp(1);
         };
         auto finish = [&](int64_t it, const K3Tile& t) {
             const int bi = (int)(it & 1);
             const float* pbase = a.np ? p.src[a.pidx].o + src_off(p.src[a.pidx], t, D) + lane * V : nullptr;
             const int64_t prow0 = t.row0 + warp * 32;
+            // plaintext rows (the inquirer's own span, natural order) of this warp's 32, eight at
+            // a time; rows past q_rows read row 0 (their results are not stored)
+            constexpr int RB2 = 8;
+            auto load_plain = [&](int j0, float (&xp)[RB2][V]) {
+                if (a.np) {
+#pragma unroll
+                    for (int j = 0; j < RB2; ++j) {
+                        const int64_t rg = prow0 + j0 + j;
+                        ldg_vec<V>(pbase + (rg < p.q_rows ? rg : 0) * D, xp[j]);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < RB2; ++j)
+#pragma unroll
+                        for (int e = 0; e < V; ++e) xp[j][e] = 0.f;
+                }
+            };
+            float xpa[RB2][V], xpb[RB2][V];
+            load_plain(0, xpa);
             // phase 1: accumulator row (thread per row) -> f32 staging in this tile's A stage
+            if (warp == 0 && it < 7) stamp(6 + 8 * (int)it);
             tc::mbar_wait(&tfull[bi], (uint32_t)((it >> 1) & 1));
             tc::tc_fence_after();
+            if (warp == 0 && it < 7) stamp(7 + 8 * (int)it);
             uint8_t* const stg = abuf + bi * S::ABUF;
             constexpr int LDS_PER_WAIT = D / 16 < 4 ? D / 16 : 4;   // 64 columns per tcgen05.wait
 #pragma unroll
@@ -449,50 +497,53 @@ __global__ void __launch_bounds__(384, 1) k3_tc_kernel(const __grid_constant__ K
             }
             tc::tc_fence_before();
             __syncwarp();
+            if (warp == 0 && it < 7) stamp(9 + 8 * (int)it);
             // phase 2: a warp per row over this warp's 32 rows: o InvOut, + plaintext, / denom
             TOut* const obh = static_cast<TOut*>(p.out) + (p.out_bstride ? (int64_t)t.b * p.out_bstride + (int64_t)t.h * p.q_rows * D
                                                                           : (int64_t)t.bh * p.q_rows * D);
-            constexpr int RB2 = 8;
-#pragma unroll 1
-            for (int j0 = 0; j0 < 32; j0 += RB2) {
-                float xp[RB2][V];
-                if (a.np) {   // rows past q_rows read row 0 (their results are not stored)
-#pragma unroll
-                    for (int j = 0; j < RB2; ++j) {
-                        const int64_t rg = prow0 + j0 + j;
-                        ldg_vec<V>(pbase + (rg < p.q_rows ? rg : 0) * D, xp[j]);
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < RB2; ++j)
-#pragma unroll
-                        for (int e = 0; e < V; ++e) xp[j][e] = 0.f;
-                }
+            // all eight rows' staging reads first, then the arithmetic, then the stores (rows past
+            // q_rows computed but not stored): no per-row branch serialising the loads
+            auto rows8 = [&](int j0, const float (&xp)[RB2][V]) {
+                float2 ri[RB2];
+                float y[RB2][V];
 #pragma unroll
                 for (int j = 0; j < RB2; ++j) {
                     const int r = warp * 32 + j0 + j;
-                    const int64_t rg = t.row0 + r;
-                    if (rg >= p.q_rows) continue;
-                    const float2 ri = rinfo[bi * S::TILE + r];
-                    float y[V];
+                    ri[j] = rinfo[bi * S::TILE + r];
                     if constexpr (V == 4) {
                         const float4 v4 = *reinterpret_cast<const float4*>(stg + stg_off<D>(r, lane));
-                        y[0] = v4.x, y[1] = v4.y, y[2] = v4.z, y[3] = v4.w;
+                        y[j][0] = v4.x, y[j][1] = v4.y, y[j][2] = v4.z, y[j][3] = v4.w;
                     } else {
                         const float2 v2 = *reinterpret_cast<const float2*>(stg + stg_off<D>(r, lane >> 1) + (lane & 1) * 8);
-                        y[0] = v2.x, y[1] = v2.y;
+                        y[j][0] = v2.x, y[j][1] = v2.y;
                     }
+                }
+#pragma unroll
+                for (int j = 0; j < RB2; ++j)
 #pragma unroll
                     for (int e = 0; e < V; ++e) {
-                        y[e] = __fmul_rn(y[e], inout[e]);
-                        if (ri.y >= 0.f) y[e] = fmaf(ri.y, xp[j][e], y[e]);
-                        y[e] *= ri.x;
+                        float v = __fmul_rn(y[j][e], inout[e]);
+                        if (ri[j].y >= 0.f) v = fmaf(ri[j].y, xp[j][e], v);
+                        y[j][e] = v * ri[j].x;
                     }
-                    store_vec_any<V>(obh + rg * D + lane * V, y);
+#pragma unroll
+                for (int j = 0; j < RB2; ++j) {
+                    const int64_t rg = prow0 + j0 + j;
+                    if (rg < p.q_rows) store_vec_any<V>(obh + rg * D + lane * V, y[j]);
                 }
-            }
+            };
+            // the plaintext rows of the next eight in flight while these eight are finished (the
+            // first eight were requested before the accumulator wait)
+            load_plain(8, xpb);
+            rows8(0, xpa);
+            load_plain(16, xpa);
+            rows8(8, xpb);
+            load_plain(24, xpb);
+            rows8(16, xpa);
+            rows8(24, xpb);
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&afree[bi]);
+            if (warp == 0 && it < 7) stamp(8 + 8 * (int)it);
         };
         K3Tile t = tile_at(0);
         uint32_t cur = 0xffffffffu;
@@ -526,8 +577,7 @@ static cudaError_t launch_k3_tc_t(K3TcArgs& a, cudaStream_t st) {
 template <int D, typename TOut>
 static cudaError_t launch_k3_tc_d(K3TcArgs& a, cudaStream_t st) {
     if (a.nk == 1) return launch_k3_tc_t<D, TOut, 1>(a, st);
-    if (a.nk == 2) return launch_k3_tc_t<D, TOut, 2>(a, st);
-    return launch_k3_tc_t<D, TOut, 4>(a, st);
+    return launch_k3_tc_t<D, TOut, 2>(a, st);
 }
 
 // The tensor-core form takes plain-memory, unquantised merges of d 64 / 128 with >= 128 rows per
@@ -551,7 +601,9 @@ cudaError_t launch_k3_tc(const K3Params& p, int d, int odt, cudaStream_t st) {
         }
         // 16-byte row loads (8 at d = 64): the ABI's alignment check guarantees them
     }
-    if (a.nk == 0 || a.nk > 4) return cudaErrorNotSupported;
+    // 3+ splits of the group: the warp forms' preload kernel is as fast (tools/k3_bench.py)
+    if (a.nk == 0 || a.nk > 2) return cudaErrorNotSupported;
+    a.trace = getenv("SDA_K3TC_TRACE") != nullptr;
     a.ntr = (p.q_rows + 127) / 128;
     a.total_tiles = a.ntr * p.n_batch * p.q_heads;
     if (a.total_tiles == 0) return cudaSuccess;
@@ -562,3 +614,12 @@ cudaError_t launch_k3_tc(const K3Params& p, int d, int odt, cudaStream_t st) {
 }
 
 }  // namespace sda
+
+// debug: the last traced launch's per-CTA clock64 stamps (n_cta x 64)
+extern "C" int sda_debug_k3tc_trace(unsigned long long* host, int n_cta) {
+    if (n_cta > 1024) n_cta = 1024;
+    return cudaMemcpyFromSymbol(host, sda::g_k3tc_trace, sizeof(unsigned long long) * sda::kK3TraceSlots * n_cta) ==
+                   cudaSuccess
+               ? 0
+               : 1;
+}

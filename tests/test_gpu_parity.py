@@ -497,12 +497,21 @@ def test_many_splits_pipelined_merge_and_ragged_ll():
     assert rel_fro(out[1].double().cpu().numpy(), plain) < 4e-2
 
 
+@pytest.mark.parametrize("form", ["default", "rows", "tc"])
 @pytest.mark.parametrize("n_groups,splits,lq,out_dtype", [(1, 1, 300, torch.bfloat16), (1, 2, 128, torch.float32),
-                                                          (3, 2, 200, torch.float32), (2, 1, 64, torch.bfloat16)])
-def test_k3_rows_kernel_prefill_shapes(n_groups, splits, lq, out_dtype):
-    """The prefill-shaped K3 form (q_rows >= 64: tables staged per CTA, P2 gather on load, P1
-    scatter through the warp's row) against dec_output + merge_shards: several domains (key
+                                                          (3, 2, 200, torch.float32), (2, 1, 64, torch.bfloat16),
+                                                          (1, 2, 333, torch.bfloat16), (1, 1, 1000, torch.float32)])
+def test_k3_rows_kernel_prefill_shapes(n_groups, splits, lq, out_dtype, form, monkeypatch):
+    """The prefill-shaped K3 forms -- the rows kernel (q_rows >= 64: tables staged per CTA, the key
+    image's conflict-free gathers) and the tensor-core form (k3_tc.cu: one key group of <= 2 splits
+    + the plaintext source, q_rows >= 128, exact 3-way bf16 split x the +-1 sign matrix; forced with
+    SDA_K3_TC=1, where ineligible it falls back) -- against dec_output + merge_shards: several domains (key
     groups) x splits, a plaintext source, a masked row in one source, merged stats, ragged tail."""
+    if form == "rows":
+        monkeypatch.setenv("SDA_K3_NO_TC", "1")
+        monkeypatch.setenv("SDA_K3_ROWS", "1")
+    elif form == "tc":
+        monkeypatch.setenv("SDA_K3_TC", "1")
     B, H, d = 2, 3, 128
     srcs, shards = [], [[] for _ in range(B * H)]
     for gi in range(n_groups + 1):

@@ -4,7 +4,8 @@ inside the timed launch), and with the inputs L2-resident (as in a step, where K
 partials K2 has just written), for the prefill merges (C3: 1 request
 x 32 heads x 2048 rows, 1 or 4 splits; C5's prefill chunk: 64 heads, 2 splits, 2 requests) and
 the decode merges (16 requests x 32 heads x 1 row), per kernel form:
-  tc        k3_tc_kernel (tcgen05 GEMM against the +-1 sign matrix; one key group, q_rows >= 128)
+  tc        k3_tc_kernel (SDA_K3_TC=1; tcgen05 GEMM against the +-1 sign matrix; one key group of
+            <= 2 splits + <= 1 plaintext source, q_rows >= 128; the default for >= 3 sources)
   rows      k3_rows_kernel (SDA_K3_NO_TC=1; q_rows >= 64: tables staged per CTA, scheduled gathers)
   preload   k3_merge_small_kernel (SDA_K3_NO_ROWS=1)
   pipelined k3_merge_kernel (SDA_K3_PIPELINED=1)
@@ -17,9 +18,9 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_25716_b200 import ops, protocol  # noqa: E402
 
-MODES = {"tc": {}, "rows": {"SDA_K3_NO_TC": "1"}, "preload": {"SDA_K3_NO_TC": "1", "SDA_K3_NO_ROWS": "1"},
+MODES = {"default": {}, "tc": {"SDA_K3_TC": "1"}, "rows": {"SDA_K3_NO_TC": "1", "SDA_K3_ROWS": "1"}, "preload": {"SDA_K3_NO_TC": "1", "SDA_K3_NO_ROWS": "1"},
          "pipelined": {"SDA_K3_NO_TC": "1", "SDA_K3_PIPELINED": "1", "SDA_K3_NO_ROWS": "1"}}
-ENVS = ("SDA_K3_NO_TC", "SDA_K3_NO_ROWS", "SDA_K3_PIPELINED")
+ENVS = ("SDA_K3_TC", "SDA_K3_NO_TC", "SDA_K3_ROWS", "SDA_K3_NO_ROWS", "SDA_K3_PIPELINED")
 
 
 def run(B, H, Lq, S, D=128, reps=20, out_dtype=torch.bfloat16, plain=0, kv_heads=None):
