@@ -40,6 +40,38 @@ def main():
               f"{t[3][j]-t[1][j]:5d} {t[4][j]-base:8d} {t[5][j]-base:8d} {per:6d}")
 
 
+def main_causal():
+    """causal mode (the inquirer's local span, C3): CTA (0,0,0)'s per-KV-tile stamps over its two
+    segments (Q-tile pairs 7 and 0) and the (start, end) of the 32 CTAs with blockIdx.y = 0."""
+    Lq, H, D = 2048, 32, 128
+    dev = torch.device("cuda")
+    q = torch.randn((1, H, Lq, D), device=dev).to(torch.bfloat16)
+    k = torch.randn((1, H, Lq, D), device=dev).to(torch.bfloat16)
+    v = torch.randn((1, H, Lq, D), device=dev).to(torch.bfloat16)
+    for _ in range(3):
+        ops.partial_attention_causal(q, k, v, causal_offset=0, n_splits=1)
+    torch.cuda.synchronize()
+    buf = np.zeros((16, 64), dtype=np.uint64)
+    capi.LIB.sda_debug_k2_trace.argtypes = [ct.c_void_p]
+    assert capi.LIB.sda_debug_k2_trace(buf.ctypes.data) == 0
+    t = buf.astype(np.int64)
+    n = int((t[0] > 0).sum())
+    base = t[0][0]
+    print("j  sm0_wait  sm0_arr  X0   sm1_wait sm1_arr  X1   pv0_iss pv1_iss  period (ns)")
+    for j in range(n):
+        per = t[0][j + 1] - t[0][j] if j + 1 < n else 0
+        print(f"{j:2d} {t[0][j]-base:8d} {t[2][j]-base:8d} {t[2][j]-t[0][j]:5d} {t[1][j]-base:8d} {t[3][j]-base:8d} "
+              f"{t[3][j]-t[1][j]:5d} {t[4][j]-base:8d} {t[5][j]-base:8d} {per:6d}")
+    print("epilogue stamps (kind 12, per segment):", [int(t[12][i] - base) for i in range(4) if t[12][i]])
+    cta = np.zeros((1024, 2), dtype=np.uint64)
+    capi.LIB.sda_debug_k2_cta.argtypes = [ct.c_void_p]
+    assert capi.LIB.sda_debug_k2_cta(cta.ctypes.data) == 0
+    c = cta.astype(np.int64)
+    n = int((c[:, 0] > 0).sum())
+    c = c[:n]
+    t0 = c[:, 0].min()
+    print(f"{n} CTAs (y = 0): start spread {(c[:, 0].max() - t0) / 1e3:.2f} us; durations (us): "
+          + " ".join(f"{(e - s) / 1e3:.1f}" for s, e in c[:8]) + f"; end max {(c[:, 1].max() - t0) / 1e3:.1f}")
 
 
 def main_sk():
@@ -81,4 +113,4 @@ def main_sk():
 
 
 if __name__ == "__main__":
-    main_sk() if os.environ.get("SK") else main()
+    main_causal() if os.environ.get("CAUSAL") else (main_sk() if os.environ.get("SK") else main())
