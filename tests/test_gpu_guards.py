@@ -105,13 +105,18 @@ def test_k2_guards(case):
     assert torch.isfinite(o.t).all()
 
 
-@pytest.mark.parametrize("case", ["decode", "rows", "rows_multi", "tiny", "quant_rows", "fp64", "packed"])
-def test_k3_guards(case):
+@pytest.mark.parametrize("case", ["decode", "rows", "rows_multi", "tiny", "quant_rows", "fp64", "packed", "tc", "tc_d64"])
+def test_k3_guards(case, monkeypatch):
     g = torch.Generator(device="cuda").manual_seed(11)
     B, H, lq, d, S = 2, 3, 1, 128, 4
     dt = torch.float32
     if case.startswith("rows") or case == "quant_rows":
         lq = 130
+    if case.startswith("tc"):   # the tensor-core form: 2 splits + the plaintext source, a ragged last tile
+        monkeypatch.setenv("SDA_K3_TC", "1")
+        lq, S = 300, 3
+        if case == "tc_d64":
+            d = 64
     if case == "rows_multi":
         S = 6
     if case == "tiny":
