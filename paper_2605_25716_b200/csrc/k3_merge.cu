@@ -344,7 +344,6 @@ __global__ void __launch_bounds__(128) k3_merge_small_kernel(const K3Params p) {
     float* sh = sh_all[warp];
     const int64_t total = p.n_batch * p.q_heads * p.q_rows;
     const int n = EXACT ? NS : p.n_src;   // !EXACT: n_src <= NS, guarded
-    pdl_wait();   // launched early behind K2 (PDL): its partials must be complete
 
     // RPW rows per warp, all of their sources' stats and O' rows in flight at once (NS = n_src
     // exactly; rows and their (b, h, r) decomposition fit 32 bits, checked by the launcher)
@@ -354,6 +353,7 @@ __global__ void __launch_bounds__(128) k3_merge_small_kernel(const K3Params p) {
     float2 st[RPW][NS];
     float ov[RPW][NS][E];
     const uint32_t qrows = (uint32_t)p.q_rows, qheads = (uint32_t)p.q_heads;
+    SrcLd<E> kt0[RPW];   // the first key group's phi_V tables: inputs, read before the wait on K2
 #pragma unroll
     for (int q = 0; q < RPW; ++q) {
         const uint32_t row_raw = ((uint32_t)blockIdx.x * 4 + warp) * RPW + q;
@@ -365,6 +365,23 @@ __global__ void __launch_bounds__(128) k3_merge_small_kernel(const K3Params p) {
         const uint32_t b32 = bh / qheads;
         hs[q] = (int)(bh - b32 * qheads);
         bs[q] = b32;
+        if (p.src[0].keys) {
+            const uint8_t* sc = scrambler_ptr(p.src[0].keys, p.keys_bstride, bs[q], hs[q] / (p.q_heads / p.key_heads), D, 1);
+            const float* ftab = reinterpret_cast<const float*>(sc);
+            const uint16_t* utab = reinterpret_cast<const uint16_t*>(sc + kU16Off * D);
+            load_vec_any<E>(ftab + kInvIn * D + lane * E, kt0[q].inv_in);
+            load_vec_any<E>(ftab + kInvOut * D + lane * E, kt0[q].inv_out);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                kt0[q].p2[e] = utab[kP2 * D + lane * E + e];
+                kt0[q].p1[e] = utab[kP1 * D + lane * E + e];
+            }
+        }
+    }
+    pdl_wait();   // launched early behind K2 (PDL): its partials must be complete
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) {
+        const int64_t bh = bs[q] * p.q_heads + hs[q];
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
             if (EXACT || s < n) {
@@ -386,7 +403,7 @@ __global__ void __launch_bounds__(128) k3_merge_small_kernel(const K3Params p) {
         const int64_t b = bs[q], r = rs[q];
         const int h = hs[q];
         const int kh = h / (p.q_heads / p.key_heads);
-        SrcLd<E> kt;
+        SrcLd<E> kt = kt0[q];
         auto load_tables = [&](const uint8_t* keys) {
             const uint8_t* sc = scrambler_ptr(keys, p.keys_bstride, b, kh, D, 1);
             const float* ftab = reinterpret_cast<const float*>(sc);
@@ -399,7 +416,6 @@ __global__ void __launch_bounds__(128) k3_merge_small_kernel(const K3Params p) {
                 kt.p1[e] = utab[kP1 * D + lane * E + e];
             }
         };
-        if (p.src[0].keys) load_tables(p.src[0].keys);
 
         float mstar = -INFINITY;   // attention.cpp:103-105
 #pragma unroll
