@@ -33,6 +33,7 @@
 #include "tc_util.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace sda {
 
@@ -63,12 +64,20 @@ struct K1TcParams {
     int n_jobs;
     int64_t total_tiles;
     int64_t tiles_per_cta;
+    int trace;
     // remote jobs (out in a peer's memory): once all of a job's tiles are stored, the CTA that
     // completes it raises *peer_flag[job] = *epoch (system-scope release); null = local job
     uint32_t* peer_flag[kK1Jobs];
     uint32_t* job_counters;           // [kK1Jobs] zeroed, self-resetting
     const uint32_t* epoch;
 };
+
+// Debug timeline (SDA_K1TC_TRACE=1): clock64 stamps per CTA -- [0] start, [1] first B built, and
+// per tile it < 10: [2+5it] loader issues the gather, [3+5it] MMA warp sees the stage full,
+// [4+5it] MMAs issued, [5+5it] epilogue sees the accumulator, [6+5it] its store issued.
+// Read back with sda_debug_k1tc_trace (tools/k1_trace.py).
+constexpr int kK1TraceSlots = 64;
+__device__ unsigned long long g_k1tc_trace[1024][kK1TraceSlots];
 
 struct K1OutMaps {                    // one TMA store map per job (kernel parameter, 64-byte aligned)
     CUtensorMap m[kK1Jobs];
@@ -114,6 +123,10 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
     uint32_t* const tmem_slot = reinterpret_cast<uint32_t*>(bready + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5;
+    auto stamp = [&](int slot) {
+        if (p.trace && (tid & 31) == 0 && slot < kK1TraceSlots && blockIdx.x < 1024)
+            g_k1tc_trace[blockIdx.x][slot] = clock64();
+    };
     const int64_t first = (int64_t)blockIdx.x * p.tiles_per_cta;
     const int64_t last = min(first + p.tiles_per_cta, p.total_tiles);
     if (first >= last) return;
@@ -145,6 +158,7 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (warp == 0) stamp(0);
 
     auto tile_rows = [&](const K1TcJob& jb, int64_t lid) -> int {
         const int64_t rem = jb.rows - (lid % jb.tiles_per_slab) * S::TILE;
@@ -189,6 +203,7 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
             const int st = (int)(it % ST);
             if (it + 2 < ntiles) fetch_src(it + 2, fetch);
             if (it >= ST) tc::mbar_wait(&empty[st], (uint32_t)(((it / ST) - 1) & 1));
+            if (warp == 4 && it < 10) stamp(2 + 5 * (int)it);
             const int jj = job_of(first + it);
             const K1TcJob& jb = p.job[jj];
             const int64_t slab = (first + it - p.job_tile0[jj]) / jb.tiles_per_slab;
@@ -227,6 +242,7 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
                 cur = ks;
             }
             tc::mbar_wait(&full[st], (uint32_t)((it / ST) & 1));
+            if (it < 10) stamp(3 + 5 * (int)it);
             if (it >= 2) tc::mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) - 1) & 1));
             tc::fence_proxy_async_smem();          // cp.async (generic proxy) -> tcgen05 (async proxy)
             tc::tc_fence_after();
@@ -248,6 +264,7 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
                     tc::mma_commit(&empty[st]);
                     tc::mma_commit(&tfull[acc]);
                 }
+                if (it < 10) stamp(4 + 5 * (int)it);
             }
             __syncwarp();
         }
@@ -310,6 +327,7 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
                 }
                 tc::fence_proxy_async_smem();
                 tc::mbar_arrive(bready);
+                if (warp == 0 && nbuild == 0) stamp(1);
                 ++nbuild;
                 cur = ks;
             }
@@ -318,6 +336,7 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
             asm volatile("bar.sync 1, 128;" ::: "memory");
             tc::mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
             tc::tc_fence_after();
+            if (warp == 0 && it < 10) stamp(5 + 5 * (int)it);
             uint8_t* o = ostg;
 #pragma unroll
             for (int cc = 0; cc < D / 16; ++cc) {
@@ -352,6 +371,7 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
                     for (int cb = 0; cb < S::KB; ++cb)
                         tc::tma_store_2d(om, o + cb * S::BLK_BYTES, cb * 64, (int)orow0);
                     tc::bulk_commit();
+                    if (it < 10) stamp(6 + 5 * (int)it);
                 }
             } else if (tid < nrows) {  // partial tile: never write past the segment
 #pragma unroll
@@ -462,6 +482,7 @@ static cudaError_t launch_k1_tc_d(const K1Params* qs, const int64_t* n_batch, in
     p.job_tile0[kK1Jobs] = tile0;
     for (int j = n_jobs; j < kK1Jobs; ++j) maps.m[j] = maps.m[0];
     p.total_tiles = tile0;
+    p.trace = getenv("SDA_K1TC_TRACE") != nullptr;
     if (p.total_tiles == 0) return cudaSuccess;
     const int64_t grid = std::min<int64_t>(p.total_tiles, num_sms());
     p.tiles_per_cta = (p.total_tiles + grid - 1) / grid;
@@ -486,3 +507,12 @@ cudaError_t launch_k1_tc_multi(const K1Params* p, const int64_t* n_batch, int n_
 }
 
 }  // namespace sda
+
+// debug: the last traced K1 launch's per-CTA clock64 stamps (n_cta x 64)
+extern "C" int sda_debug_k1tc_trace(unsigned long long* host, int n_cta) {
+    if (n_cta > 1024) n_cta = 1024;
+    return cudaMemcpyFromSymbol(host, sda::g_k1tc_trace, sizeof(unsigned long long) * sda::kK1TraceSlots * n_cta) ==
+                   cudaSuccess
+               ? 0
+               : 1;
+}
