@@ -23,7 +23,7 @@ MODES = {"default": {}, "tc": {"SDA_K3_TC": "1"}, "rows": {"SDA_K3_NO_TC": "1", 
 ENVS = ("SDA_K3_TC", "SDA_K3_NO_TC", "SDA_K3_ROWS", "SDA_K3_NO_ROWS", "SDA_K3_PIPELINED")
 
 
-def run(B, H, Lq, S, D=128, reps=20, out_dtype=torch.bfloat16, plain=0, kv_heads=None):
+def run(B, H, Lq, S, D=128, reps=20, out_dtype=torch.bfloat16, plain=0, kv_heads=None, identity=False):
     dev = torch.device("cuda")
     HKV = kv_heads or H
     keys = protocol.DomainKeys(list(range(1, B + 1)), 0, 1, HKV, D, dev)
@@ -31,7 +31,8 @@ def run(B, H, Lq, S, D=128, reps=20, out_dtype=torch.bfloat16, plain=0, kv_heads
     st = torch.stack([torch.randn((S, B, H, Lq), device=dev), torch.rand((S, B, H, Lq), device=dev) + 0.5], -1)
     pinv = None
     if Lq > 1:
-        pinv = torch.stack([torch.randperm(Lq, device=dev) for _ in range(B)]).to(torch.int32).contiguous()
+        pinv = torch.stack([torch.arange(Lq, device=dev) if identity else torch.randperm(Lq, device=dev)
+                            for _ in range(B)]).to(torch.int32).contiguous()
     srcs = ops.sources_from_splits(o, st, keys.dev, pinv)
     if plain:   # the inquirer's own span (plaintext, natural row order), as bench.py's C3 / C5 steps
         lo = torch.randn((plain, B, H, Lq, D), device=dev)
@@ -79,6 +80,12 @@ def run(B, H, Lq, S, D=128, reps=20, out_dtype=torch.bfloat16, plain=0, kv_heads
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "perm":   # random vs identity p_q^-1 (the gather's cost)
+        for ident in (False, True):
+            print("identity p_q^-1" if ident else "random p_q^-1")
+            run(1, 32, 2048, 1, out_dtype=torch.float32, identity=ident)
+            run(1, 32, 2048, 1, out_dtype=torch.float32, plain=1, identity=ident)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "c3":   # the C3 single-source merge only (ncu captures)
         run(1, 32, 2048, 1, reps=3)
         sys.exit(0)
