@@ -101,12 +101,17 @@ struct K1TcShape {
     static constexpr int OFF_KT = OFF_BAR + 8 * NBAR + 16;   // key tables of the B being built
     static constexpr int SMEM = OFF_KT + D * (4 + 4 + 2 + 2);
     static constexpr uint32_t TMEM_COLS = 2 * D;
-    static constexpr int THREADS = 288;
-    static constexpr int LOADERS = 128;                      // warps 4-7
+#ifndef SDA_K1_LOADER_WARPS
+#define SDA_K1_LOADER_WARPS 8   // measured: 4 -> 8 warps 391 -> 368 us on the 2 GiB fill, 12 no better
+#endif
+    static constexpr int LOADER_WARPS = SDA_K1_LOADER_WARPS;
+    static constexpr int LOADERS = 32 * LOADER_WARPS;       // warps 4 .. 4 + LOADER_WARPS - 1
+    static constexpr int MMA_WARP = 4 + LOADER_WARPS;
+    static constexpr int THREADS = 32 * (MMA_WARP + 1);
 };
 
 template <int D>
-__global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const __grid_constant__ K1OutMaps maps) {
+__global__ void __launch_bounds__(K1TcShape<D>::THREADS, 1) k1_tc_kernel(const K1TcParams p, const __grid_constant__ K1OutMaps maps) {
     using S = K1TcShape<D>;
     constexpr int ST = S::STAGES;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -174,9 +179,9 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
     };
     constexpr int CPR = D / 8;   // 16-byte chunks per row
 
-    if (warp >= 4 && warp < 8) {
+    if (warp >= 4 && warp < S::MMA_WARP) {
         // ------------------------------------------------------------------ loaders
-        const int lt = tid - 128;                  // 0..127
+        const int lt = tid - 128;                  // 0 .. LOADERS - 1
         constexpr int RSTEP = S::LOADERS / CPR, NR = S::TILE / RSTEP;
         const int c = lt % CPR, r0 = lt / CPR;
         // source rows of a tile for this thread (-1: past the segment end); fetched two tiles
@@ -225,7 +230,7 @@ __global__ void __launch_bounds__(288, 1) k1_tc_kernel(const K1TcParams p, const
             if (it + 1 < ntiles) tile(it + 1, ib, ia);
             if (it + 2 < ntiles) tile(it + 2, ic, ib);
         }
-    } else if (warp == 8) {
+    } else if (warp == S::MMA_WARP) {
         // ------------------------------------------------------------------ MMA issuer
         constexpr uint32_t IDESC = tc::idesc_bf16_f32(128, D, false, false);
         const uint32_t bh = tc::smem_u32(b_hi), bl = tc::smem_u32(b_lo);
