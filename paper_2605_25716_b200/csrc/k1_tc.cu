@@ -77,7 +77,7 @@ struct K1TcParams {
 // [4+5it] MMAs issued, [5+5it] epilogue sees the accumulator, [6+5it] its store issued.
 // Read back with sda_debug_k1tc_trace (tools/k1_trace.py).
 constexpr int kK1TraceSlots = 64;
-__device__ unsigned long long g_k1tc_trace[1024][kK1TraceSlots];
+__device__ unsigned long long g_k1tc_trace[256][kK1TraceSlots];
 
 struct K1OutMaps {                    // one TMA store map per job (kernel parameter, 64-byte aligned)
     CUtensorMap m[kK1Jobs];
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(K1TcShape<D>::THREADS, 1) k1_tc_kernel(const K
 
     const int tid = threadIdx.x, warp = tid >> 5;
     auto stamp = [&](int slot) {
-        if (p.trace && (tid & 31) == 0 && slot < kK1TraceSlots && blockIdx.x < 1024)
+        if (p.trace && (tid & 31) == 0 && slot < kK1TraceSlots && blockIdx.x < 256)
             g_k1tc_trace[blockIdx.x][slot] = clock64();
     };
     const int64_t first = (int64_t)blockIdx.x * p.tiles_per_cta;
@@ -515,7 +515,7 @@ cudaError_t launch_k1_tc_multi(const K1Params* p, const int64_t* n_batch, int n_
 
 // debug: the last traced K1 launch's per-CTA clock64 stamps (n_cta x 64)
 extern "C" int sda_debug_k1tc_trace(unsigned long long* host, int n_cta) {
-    if (n_cta > 1024) n_cta = 1024;
+    if (n_cta > 256) n_cta = 256;
     return cudaMemcpyFromSymbol(host, sda::g_k1tc_trace, sizeof(unsigned long long) * sda::kK1TraceSlots * n_cta) ==
                    cudaSuccess
                ? 0

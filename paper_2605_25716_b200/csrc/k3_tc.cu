@@ -42,7 +42,7 @@ namespace sda {
 // Debug timeline (SDA_K3TC_TRACE=1): clock64 stamps of one split warp and one epilogue warp per
 // CTA, read back with sda_debug_k3tc_trace (tools/k3_trace.py).
 constexpr int kK3TraceSlots = 64;
-__device__ unsigned long long g_k3tc_trace[1024][kK3TraceSlots];
+__device__ unsigned long long g_k3tc_trace[256][kK3TraceSlots];   // persistent grids: <= one CTA per SM
 
 struct K3TcArgs {
     K3Params p;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(384, 1) k3_tc_kernel(const __grid_constant__ K
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     auto stamp = [&](int slot) {
-        if (a.trace && lane == 0 && slot < kK3TraceSlots && blockIdx.x < 1024) g_k3tc_trace[blockIdx.x][slot] = clock64();
+        if (a.trace && lane == 0 && slot < kK3TraceSlots && blockIdx.x < 256) g_k3tc_trace[blockIdx.x][slot] = clock64();
     };
     const int64_t first = (int64_t)blockIdx.x * a.tiles_per_cta;
     const int64_t last = min(first + a.tiles_per_cta, a.total_tiles);
@@ -617,7 +617,7 @@ cudaError_t launch_k3_tc(const K3Params& p, int d, int odt, cudaStream_t st) {
 
 // debug: the last traced launch's per-CTA clock64 stamps (n_cta x 64)
 extern "C" int sda_debug_k3tc_trace(unsigned long long* host, int n_cta) {
-    if (n_cta > 1024) n_cta = 1024;
+    if (n_cta > 256) n_cta = 256;
     return cudaMemcpyFromSymbol(host, sda::g_k3tc_trace, sizeof(unsigned long long) * sda::kK3TraceSlots * n_cta) ==
                    cudaSuccess
                ? 0
