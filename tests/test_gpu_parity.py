@@ -512,13 +512,31 @@ def test_k3_rows_kernel_prefill_shapes(n_groups, splits, lq, out_dtype, form, mo
         monkeypatch.setenv("SDA_K3_ROWS", "1")
     elif form == "tc":
         monkeypatch.setenv("SDA_K3_TC", "1")
-    B, H, d = 2, 3, 128
+    _k3_prefill_case(n_groups, splits, lq, out_dtype)
+
+
+@pytest.mark.parametrize("form", ["default", "tc", "rows"])
+@pytest.mark.parametrize("splits,lq,out_dtype", [(2, 300, torch.float32), (1, 256, torch.bfloat16)])
+def test_k3_prefill_gqa_key_heads(splits, lq, out_dtype, form, monkeypatch):
+    """GQA merges (the C5 prefill chunk's shape: q head h unscrambles with key head h // G): one
+    key group of splits + the plaintext source, q_heads 4 / key_heads 2, every K3 prefill form."""
+    if form == "rows":
+        monkeypatch.setenv("SDA_K3_NO_TC", "1")
+        monkeypatch.setenv("SDA_K3_ROWS", "1")
+    elif form == "tc":
+        monkeypatch.setenv("SDA_K3_TC", "1")
+    _k3_prefill_case(1, splits, lq, out_dtype, G=2)
+
+
+def _k3_prefill_case(n_groups, splits, lq, out_dtype, G=1):
+    B, H, d = 2, (3 if G == 1 else 4), 128
+    Hk = H // G
     srcs, shards = [], [[] for _ in range(B * H)]
     for gi in range(n_groups + 1):
         keyed = gi < n_groups
         kd = pqi = None
         if keyed:
-            kh, kd = _keys(B, H, d, domain=gi + 1)
+            kh, kd = _keys(B, Hk, d, domain=gi + 1)
             pq = [kh[b].span_perm(0, 77, lq) for b in range(B)]
             pqi = ops.upload_perms([capi.invert_permutation(p) for p in pq], "cuda")
         for s in range(splits if keyed else 1):
@@ -533,7 +551,7 @@ def test_k3_rows_kernel_prefill_shapes(n_groups, splits, lq, out_dtype, form, mo
             for b in range(B):
                 for h in range(H):
                     if keyed:
-                        od = C.apply_phi(o[b, h], *_sc(kh[b], h, 1), 2)
+                        od = C.apply_phi(o[b, h], *_sc(kh[b], h // G, 1), 2)
                         oo, mm, ss = np.zeros_like(od), np.zeros(lq), np.zeros(lq)
                         oo[pq[b]], mm[pq[b]], ss[pq[b]] = od, m[b, h], sm[b, h]
                     else:
@@ -541,7 +559,8 @@ def test_k3_rows_kernel_prefill_shapes(n_groups, splits, lq, out_dtype, form, mo
                     shards[b * H + h].append((oo, mm, ss))
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
     ost = torch.empty((B, H, lq, 2), dtype=torch.float32, device="cuda")
-    got = ops.unscramble_merge(srcs, out_dtype=out_dtype, err_flag=err, out_stats=ost).double().cpu().numpy()
+    got = ops.unscramble_merge(srcs, out_dtype=out_dtype, err_flag=err, out_stats=ost,
+                               key_heads=Hk).double().cpu().numpy()
     gst = ost.double().cpu().numpy()
     assert int(err.item()) == 0
     tol = 1e-2 if out_dtype == torch.bfloat16 else 1e-5
