@@ -12,6 +12,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["SDA_K3TC_TRACE"] = "1"
+os.environ["SDA_K3_TC"] = "1"   # the tensor-core form for every eligible merge (the default takes it for >= 3 sources)
 from paper_2605_25716_b200 import capi, ops, protocol  # noqa: E402
 
 
@@ -48,6 +49,9 @@ def main(show=4, B=1, H=32, Lq=2048, S=1, D=128, plain=0, out_dtype=torch.float3
         items.sort(key=lambda x: x[1])
         print(f"CTA {c}: " + "  ".join(f"{k}={v:.1f}" for k, v in items))
     ends = [max(r[r > 0]) - r[0] for r in t if r[0] > 0]
+    if not ends:
+        print("no trace (the merge did not run on the tensor-core form)")
+        return
     print(f"CTA span (kcycles): median {np.median(ends) / 1000:.1f}, max {max(ends) / 1000:.1f}")
 
 
