@@ -733,6 +733,11 @@ def run_prefill_dist(args, ws, rank, local):
     bufs = sdist.StepBuffers.allocate(ws, 1, H, LQ, D, torch.bfloat16, devn)
     exch = sdist.PeerExchange(bufs) if ws > 1 and args.exchange != "nccl" else None
     out = torch.empty((1, H, LQ, D), dtype=torch.float32, device=devn)
+    # the step runs on a high-priority stream: the span's causal local attention goes to a
+    # lowest-priority side stream after K1 (distributed.gpu_rank_compute), behind K2's CTAs
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream(device=devn, priority=-1)
+    torch.cuda.set_stream(stream)
 
     def step(qin, o=out):
         ops.scramble_batch(k1_jobs, D)   # the span's K/V into the cache, scramble + permute fused
@@ -870,16 +875,27 @@ def run_prefill(devn, steps: int, warmup: int, peaks: dict):
     lo = torch.empty((1, 1, H, LQ, D), dtype=torch.float32, device=devn)
     ls = torch.empty((1, 1, H, LQ, 2), dtype=torch.float32, device=devn)
     srcs = ops.sources_from_splits(o, st, keys.dev, pq_inv) + ops.sources_from_splits(lo, ls)
-    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()   # the setup ran on the default stream
+    stream = torch.cuda.Stream(device=devn, priority=-1)   # the step's stream (high priority, see below)
     ev = []
     k1_jobs = [ops.scramble_job(kn, keys.dev, capi.PHI_INV_T, capi.KEYS_KQ, pkv, out=shard.k, out_row_offset=LK, key_heads=H),
                ops.scramble_job(vn, keys.dev, capi.PHI_FORWARD, capi.KEYS_V, pkv, out=shard.v, out_row_offset=LK, key_heads=H),
                ops.scramble_job(q, keys.dev, capi.PHI_FORWARD, capi.KEYS_KQ, pq, out=qs, key_heads=H)]
 
+    # the span's causal local attention is independent of K1's Q' and of the remote K2: it runs on a
+    # second, lower-priority stream once K1 is done, so its CTAs take the SMs the stream-K K2 frees
+    # in its tail instead of starting after it (SDA_BENCH_C3_SERIAL=1: one stream, as before)
+    serial = bool(os.environ.get("SDA_BENCH_C3_SERIAL"))
+    side = torch.cuda.Stream(device=devn, priority=0)
+    k1_done = torch.cuda.Event()
+    local_done = torch.cuda.Event()
+
     def step(rec):
         # the span's K/V go into the cache rows after the shard (scramble + permute fused into the write)
         # ... and the span's Q into Q' (p_q), all three K1 jobs in one launch
         ops.scramble_batch(k1_jobs, D)
+        if not serial:
+            k1_done.record(stream)
         if rec:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -888,24 +904,39 @@ def run_prefill(devn, steps: int, warmup: int, peaks: dict):
         if rec:
             e1.record(stream)
             ev.append((e0, e1))
-        ops.partial_attention_causal(q, kn, vn, causal_offset=0, n_splits=1, out_o=lo, out_stats=ls)
-        if rec:
-            e2 = torch.cuda.Event(enable_timing=True)
-            e2.record(stream)
-            ev_local.append((e1, e2))
+        if serial:
+            ops.partial_attention_causal(q, kn, vn, causal_offset=0, n_splits=1, out_o=lo, out_stats=ls)
+            if rec:
+                e2 = torch.cuda.Event(enable_timing=True)
+                e2.record(stream)
+                ev_local.append((e1, e2))
+        else:
+            side.wait_event(k1_done)   # (also orders it after the previous step's K3, which read lo / ls)
+            with torch.cuda.stream(side):
+                if rec:
+                    s0 = torch.cuda.Event(enable_timing=True)
+                    s0.record(side)
+                ops.partial_attention_causal(q, kn, vn, causal_offset=0, n_splits=1, out_o=lo, out_stats=ls)
+                if rec:
+                    s1 = torch.cuda.Event(enable_timing=True)
+                    s1.record(side)
+                    ev_local.append((s0, s1))
+                local_done.record(side)
+            stream.wait_event(local_done)
         ops.unscramble_merge(srcs, out=out, key_heads=H)
 
     ev_local = []
-    for _ in range(warmup):
-        step(False)
-    torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(devn.index or 0) as clk:
-        t0.record(stream)
-        for _ in range(steps):
-            step(True)
-        t1.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            step(False)
         torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(devn.index or 0) as clk:
+            t0.record(stream)
+            for _ in range(steps):
+                step(True)
+            t1.record(stream)
+            torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / steps
     k2_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
     local_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_local)

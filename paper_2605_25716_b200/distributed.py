@@ -497,19 +497,52 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
             state["lq"], state["pq"], state["pq_inv"] = lq, torch.cat(fwd, 0).contiguous(), list(inv)
         return state["pq"], state["pq_inv"]
 
-    def scramble_q_all(q, q_send):
+    def start_local(q):
+        """Launch the span's causal local attention (plaintext Q, K, V: independent of K1's Q', of
+        the exchange and of K2) on a side stream once this step's K1 is queued, so it fills the SMs
+        the exchange waits and K2's stream-K tail leave idle; finish joins it before K3. The side
+        stream has the lowest priority: on a higher-priority step stream (bench.py) K2's CTAs go
+        first. SDA_LOCAL_SERIAL=1 runs it in finish on the step stream instead."""
         state["q_plain"] = q
+        state["local_ev"] = None
+        if local_kv is None or os.environ.get("SDA_LOCAL_SERIAL"):
+            return
+        cur = torch.cuda.current_stream(q.device)
+        if state.get("side") is None:
+            state["side"] = torch.cuda.Stream(device=q.device, priority=0)
+            state["fork"], state["join"] = torch.cuda.Event(), torch.cuda.Event()
+        side = state["side"]
+        state["fork"].record(cur)          # after K1 and after the previous step's K3 (it read lo / ls)
+        side.wait_event(state["fork"])
+        with torch.cuda.stream(side):
+            run_local(q)
+            state["join"].record(side)
+        state["local_ev"] = state["join"]
+
+    def run_local(q):
+        Bp, Hq, Lq, d = q.shape
+        key = ("local", Bp, Hq, Lq, d)
+        if state.get("lkey") != key:
+            state["lkey"] = key
+            state["lo"] = torch.empty((1, Bp, Hq, Lq, d), dtype=torch.float32, device=q.device)
+            state["ls"] = torch.empty((1, Bp, Hq, Lq, 2), dtype=torch.float32, device=q.device)
+        ops.partial_attention_causal(q, local_kv[0], local_kv[1], causal_offset=local_offset,
+                                     n_splits=1, out_o=state["lo"], out_stats=state["ls"])
+
+    def scramble_q_all(q, q_send):
         W = q_send.shape[0]
         pq, _ = q_perms(q.shape[2])
         ops.scramble(q, keys_all, capi.PHI_FORWARD, capi.KEYS_KQ, pq, out=q_send.view((-1,) + tuple(q_send.shape[2:])),
                      key_heads=kv_heads or inquirer_keys[0].kv_heads, n_batch=W * q.shape[0])
+        start_local(q)
 
     def scramble_q(q, dom, out):
-        state["q_plain"] = q
         pq, _ = q_perms(q.shape[2])
         ops.scramble(q, inquirer_keys[dom].dev, capi.PHI_FORWARD, capi.KEYS_KQ,
                      None if pq is None else pq[dom * q.shape[0]:(dom + 1) * q.shape[0]], out=out,
                      key_heads=kv_heads or inquirer_keys[dom].kv_heads)
+        if dom == len(inquirer_keys) - 1:
+            start_local(q)
 
     def serve(q_all, ret, dims):
         B, Hq, Lq, d = q_all.shape
@@ -547,7 +580,6 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
     def scramble_q_remote(q, ex):
         # TMA stores straight into peer memory: +3-5 % at N=2, +0.4-3 % at N=4 on C3 against K1
         # into q_send + the push kernel (SDA_K1_REMOTE=0 selects the latter)
-        state["q_plain"] = q
         Bp, Hq, Lq, d = q.shape
         if os.environ.get("SDA_K1_REMOTE") == "0":
             return False
@@ -568,6 +600,7 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
         capi.check(capi.LIB.sda_scramble_batch_remote(torch.cuda.current_stream().cuda_stream, d, jobs, ex.world,
                                                       flags, ex.epoch.data_ptr(), ex.k1_counters.data_ptr()),
                    "sda_scramble_batch_remote")
+        start_local(q)
         return True
 
     def finish(back, out, dims):
@@ -577,13 +610,11 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
         srcs = [ops.MergeSource(back[dom], back[dom, :, Hq * Lq * d:], inquirer_keys[dom].dev, pq_inv[dom],
                                 batch_stride=rec, shape=(Bp, Hq, Lq, d)) for dom in range(W)]
         if local_kv is not None:   # the inquirer's own span, plaintext, causal (no keys, no p_q)
-            key = ("local", Bp, Hq, Lq, d)
-            if state.get("lkey") != key:
-                state["lkey"] = key
-                state["lo"] = torch.empty((1, Bp, Hq, Lq, d), dtype=torch.float32, device=out.device)
-                state["ls"] = torch.empty((1, Bp, Hq, Lq, 2), dtype=torch.float32, device=out.device)
-            ops.partial_attention_causal(state["q_plain"], local_kv[0], local_kv[1], causal_offset=local_offset,
-                                         n_splits=1, out_o=state["lo"], out_stats=state["ls"])
+            if state.get("local_ev") is not None:
+                torch.cuda.current_stream(out.device).wait_event(state["local_ev"])
+                state["local_ev"] = None
+            else:
+                run_local(state["q_plain"])
             srcs += ops.sources_from_splits(state["lo"], state["ls"])
         ops.unscramble_merge(srcs, out=out, key_heads=kv_heads or inquirer_keys[0].kv_heads)
 

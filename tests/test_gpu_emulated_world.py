@@ -181,11 +181,14 @@ def test_prefill_remote_emulated_world(W):
             assert np.all(np.isfinite(got[b, h, rows]))
 
 
-def test_prefill_with_causal_local_span_emulated_world():
+@pytest.mark.parametrize("serial", [False, True], ids=["side_stream", "serial"])
+def test_prefill_with_causal_local_span_emulated_world(serial, monkeypatch):
     """span_finish_layer with the inquirer's own span (protocol.cpp:941-948): every domain's
     scrambled partial + the span's own K/V attended in plaintext with the causal mask (tensor-core
     K2 with per-row key limits), all merged by K3 -- against plain attention over [every domain's
     context ++ the span's own keys, causal] (f32 over the same bf16 plaintext)."""
+    if serial:   # the local span in finish on the step stream, not on the side stream after K1
+        monkeypatch.setenv("SDA_LOCAL_SERIAL", "1")
     W, LQ = 2, 256
     w = World(W, 1, 4, 4, 128, 512, LQ, torch.bfloat16, seed=400)
     g = torch.Generator(device="cuda").manual_seed(5)
