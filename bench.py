@@ -729,7 +729,10 @@ def run_prefill_dist(args, ws, rank, local):
                ops.scramble_job(vn, inq[rank].dev, capi.PHI_FORWARD, capi.KEYS_V, pkv, out=own_shard.v, key_heads=H)]
     S = capi.default_splits(ws, H, LQ, LK)
     # the span also attends its own K/V in plaintext with the causal mask (protocol.cpp:944-947)
-    comp = sdist.gpu_rank_compute(inq, shard, n_splits=S, kv_heads=H, q_first_pos=q_first, local_kv=(kn, vn))
+    # the span's own K/V into the local cache is off the step's path: it runs on the side stream
+    # with the causal span, after this step's Q' scramble
+    comp = sdist.gpu_rank_compute(inq, shard, n_splits=S, kv_heads=H, q_first_pos=q_first, local_kv=(kn, vn),
+                                  side_work=lambda: ops.scramble_batch(k1_jobs, D))
     bufs = sdist.StepBuffers.allocate(ws, 1, H, LQ, D, torch.bfloat16, devn)
     exch = sdist.PeerExchange(bufs) if ws > 1 and args.exchange != "nccl" else None
     out = torch.empty((1, H, LQ, D), dtype=torch.float32, device=devn)
@@ -740,7 +743,7 @@ def run_prefill_dist(args, ws, rank, local):
     torch.cuda.set_stream(stream)
 
     def step(qin, o=out):
-        ops.scramble_batch(k1_jobs, D)   # the span's K/V into the cache, scramble + permute fused
+        # the span's K/V into the cache (scramble + permute fused) runs inside as comp's side work
         return sdist.scrambled_decode_step(qin, comp, bufs, o, exchange=exch)
 
     def barrier():
@@ -892,9 +895,13 @@ def run_prefill(devn, steps: int, warmup: int, peaks: dict):
 
     def step(rec):
         # the span's K/V go into the cache rows after the shard (scramble + permute fused into the write)
-        # ... and the span's Q into Q' (p_q), all three K1 jobs in one launch
-        ops.scramble_batch(k1_jobs, D)
-        if not serial:
+        # ... and the span's Q into Q' (p_q). Serial: all three K1 jobs in one launch. Otherwise only
+        # Q' is on the path to K2; the K/V jobs (written past the 16K rows K2 reads) go to the side
+        # stream with the causal span
+        if serial:
+            ops.scramble_batch(k1_jobs, D)
+        else:
+            ops.scramble_batch(k1_jobs[2:], D)
             k1_done.record(stream)
         if rec:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -913,6 +920,7 @@ def run_prefill(devn, steps: int, warmup: int, peaks: dict):
         else:
             side.wait_event(k1_done)   # (also orders it after the previous step's K3, which read lo / ls)
             with torch.cuda.stream(side):
+                ops.scramble_batch(k1_jobs[:2], D)
                 if rec:
                     s0 = torch.cuda.Event(enable_timing=True)
                     s0.record(side)

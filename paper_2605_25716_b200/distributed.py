@@ -474,14 +474,17 @@ class LocalWorld:
 
 def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = None,
                      kv_heads: Optional[int] = None, q_first_pos: int = 0,
-                     local_kv: Optional[tuple] = None, local_offset: int = 0) -> RankCompute:
+                     local_kv: Optional[tuple] = None, local_offset: int = 0,
+                     side_work: Optional[Callable[[], None]] = None) -> RankCompute:
     """RankCompute backed by libsdattn_b200.so. inquirer_keys[dom] = DomainKeys of my requests on
     domain dom + 1; shard = this rank's protocol.KVShard (all requests' rows of my domain).
     q_first_pos: global position of the query span (its rows are shuffled by each domain's
     span_perm(0, q_first_pos, L_q), identity for single-row decode).
     local_kv: (k, v) plaintext [B_p, Hkv, L_local, d] of the inquirer's own span: attended with the
     causal mask at local_offset (= q_first_pos - the local keys' first position) and merged by K3
-    as a plaintext source, as span_finish_layer does (protocol.cpp:941-947)."""
+    as a plaintext source, as span_finish_layer does (protocol.cpp:941-947).
+    side_work: launches off the step's path (e.g. the span's own K/V scrambled into the local
+    cache, protocol.cpp:885-891), run on the side stream ahead of the local span."""
     from . import capi, ops
 
     state = {}
@@ -505,7 +508,9 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
         first. SDA_LOCAL_SERIAL=1 runs it in finish on the step stream instead."""
         state["q_plain"] = q
         state["local_ev"] = None
-        if local_kv is None or os.environ.get("SDA_LOCAL_SERIAL"):
+        if (local_kv is None and side_work is None) or os.environ.get("SDA_LOCAL_SERIAL"):
+            if side_work is not None:
+                side_work()
             return
         cur = torch.cuda.current_stream(q.device)
         if state.get("side") is None:
@@ -515,7 +520,10 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
         state["fork"].record(cur)          # after K1 and after the previous step's K3 (it read lo / ls)
         side.wait_event(state["fork"])
         with torch.cuda.stream(side):
-            run_local(q)
+            if side_work is not None:
+                side_work()
+            if local_kv is not None:
+                run_local(q)
             state["join"].record(side)
         state["local_ev"] = state["join"]
 
@@ -609,11 +617,12 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
         _, pq_inv = q_perms(Lq)
         srcs = [ops.MergeSource(back[dom], back[dom, :, Hq * Lq * d:], inquirer_keys[dom].dev, pq_inv[dom],
                                 batch_stride=rec, shape=(Bp, Hq, Lq, d)) for dom in range(W)]
+        joined = state.get("local_ev") is not None
+        if joined:
+            torch.cuda.current_stream(out.device).wait_event(state["local_ev"])
+            state["local_ev"] = None
         if local_kv is not None:   # the inquirer's own span, plaintext, causal (no keys, no p_q)
-            if state.get("local_ev") is not None:
-                torch.cuda.current_stream(out.device).wait_event(state["local_ev"])
-                state["local_ev"] = None
-            else:
+            if not joined:
                 run_local(state["q_plain"])
             srcs += ops.sources_from_splits(state["lo"], state["ls"])
         ops.unscramble_merge(srcs, out=out, key_heads=kv_heads or inquirer_keys[0].kv_heads)
