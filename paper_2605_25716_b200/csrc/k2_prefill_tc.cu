@@ -70,7 +70,7 @@ struct K2TcParams {
 // debug build only (tools/k2_trace.py): globaltimer stamps of CTA (0,0,0) -- [kind][j], kinds:
 // 0/1 softmax g got S, 2/3 softmax g arrives with P, 4/5 PV0/PV1 issue, 6/7 MMA loop top / V ready,
 // 8 before the P1 wait, 9/10 before / after the K(j+1) wait
-__device__ uint64_t g_k2_trace[16][64];
+__device__ uint64_t g_k2_trace[24][64];
 __device__ uint64_t g_k2_cta[1024][2];   // every CTA's (start, end) globaltimer
 __device__ __forceinline__ void k2_cta_stamp(int which) {
     if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && blockIdx.x < 1024) {
@@ -88,7 +88,17 @@ __device__ __forceinline__ void k2_stamp(int kind, int64_t j) {
     }
 }
 #define K2_STAMP(k, j) k2_stamp(k, j)
+// the pair's rank-1 CTA (blockIdx.x == 1)
+__device__ __forceinline__ void k2_stamp1(int kind, int64_t j) {
+    if (blockIdx.x == 1 && blockIdx.y == 0 && blockIdx.z == 0 && j < 64) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_k2_trace[kind][j] = t;
+    }
+}
+#define K2_STAMP1(k, j) k2_stamp1(k, j)
 #else
+#define K2_STAMP1(k, j)
 #define K2_STAMP(k, j)
 #define K2_CTA_STAMP(w)
 #endif
@@ -124,6 +134,32 @@ constexpr int OFF_BAR = OFF_V + 2 * TILE_BYTES;
 constexpr int NBAR = 14 + 2 * KST + 2 * (SDA_K2_PPARTS > 1 ? SDA_K2_PPARTS - 1 : 0);
 constexpr int OFF_SEG = OFF_BAR + NBAR * 8 + 16;   // per softmax warp: segment state (SoftKeep)
 constexpr int SMEM = OFF_SEG + 8 * 128;
+// The CTA-pair form (PAIR; opt-in, SDA_K2_PAIR=1 -- parity-green but 495-505 us on C3 against
+// 445-454 us for the form above: with the chain decoupled both softmax groups run at once and
+// each takes 1.5-1.8 us per tile instead of 1.05, so the SM's softmax throughput, not the chain,
+// bounds the step): a cluster of two CTAs issues every MMA as one M = 256 tcgen05.mma
+// (cta_group::2; rank 0 issues): each CTA keeps its own two Q tiles, S and O in its TMEM, and only
+// HALF of every K tile (64 keys) and V tile (64 of the d columns) in its shared memory. That halves
+// each SM's shared-memory operand traffic, and the room it frees holds P_g in SMEM (a SW128 K-major
+// A operand) instead of over S_g in TMEM -- so S_g(j+1) goes into TMEM as soon as the softmax has
+// S_g(j) in registers, and the S -> softmax -> PV -> S chain of a Q tile becomes softmax ->
+// softmax. K and V half tiles share one 6-slot ring in the order the MMAs consume them (K(j+1) for
+// S(j+1), then V(j) for PV(j)). (One CTA with P in SMEM was measured SMEM-bound: DESIGN.md.)
+template <bool PAIR>
+struct Lay {
+    static constexpr int KST = PAIR ? 6 : k2tc::KST;                      // K ring (PAIR: K/V half-tile ring)
+    static constexpr int SLOT = PAIR ? TILE_BYTES / 2 : TILE_BYTES;
+    static constexpr int OFF_P = OFF_Q1 + TILE_BYTES;                     // PAIR: P0 | P1
+    static constexpr int OFF_K = PAIR ? OFF_P + 2 * TILE_BYTES : OFF_Q1 + TILE_BYTES;
+    static constexpr int OFF_V = PAIR ? OFF_K : OFF_K + KST * TILE_BYTES;
+    static constexpr int OFF_BAR = PAIR ? OFF_K + KST * SLOT : OFF_V + 2 * TILE_BYTES;
+    // + PAIR: s_free[2] (softmax holds S_g in registers), p_empty[2] (PV_g done: P_g reusable)
+    static constexpr int NBAR = 14 + 2 * KST + 2 * (SDA_K2_PPARTS > 1 ? SDA_K2_PPARTS - 1 : 0) + (PAIR ? 4 : 0);
+    static constexpr int OFF_SEG = OFF_BAR + NBAR * 8 + 16;
+    static constexpr int SMEM = OFF_SEG + 8 * 128;
+};
+static_assert(Lay<true>::SMEM <= 232448, "pair form exceeds the 227 KB opt-in SMEM");
+static_assert(Lay<false>::SMEM == SMEM, "layouts");
 // 12 warps = 3 warpgroups so registers can move between them (setmaxnreg): softmax warps 0-7
 // grow to 224, the TMA / MMA warpgroup (warps 8-9; 10-11 idle) shrinks to 56
 #ifndef SDA_K2_SETMAXNREG
@@ -328,12 +364,15 @@ __device__ __forceinline__ void store_row16(float* dst, const uint32_t (&o)[16],
 __device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 }  // namespace k2tc
 
+template <bool PAIR>
 __global__ void __launch_bounds__(k2tc::THREADS, 1)
 k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                      const __grid_constant__ CUtensorMap vmap) {
     using namespace k2tc;
+    using L = Lay<PAIR>;
+    constexpr int KST = L::KST;
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint64_t* const bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* const bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
     uint64_t* const q_full = bars;
     uint64_t* const k_full = bars + 1;
     uint64_t* const k_empty = k_full + KST;
@@ -348,7 +387,26 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
     // completes once per tile (a barrier completing several phases ahead of its waiter would
     // leave the waiter's parity ambiguous)
     uint64_t* const p_part = o_empty + 2;
-    uint32_t* const tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
+    uint64_t* const s_free = p_part + 2 * (kPParts > 1 ? kPParts - 1 : 0);   // PAIR only
+    uint64_t* const p_empty = s_free + 2;                                     // PAIR only
+    uint32_t* const tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NBAR);
+    // PAIR: rank 0 issues the MMAs and owns the barriers the pair's TMA bytes and softmax
+    // arrivals complete on (both CTAs arrive there; commits multicast to both CTAs' copies)
+    const uint32_t crank = PAIR ? tc::cluster_rank() : 0u;
+    // softmax -> MMA hand-off. PAIR: one arrive per warp (its lanes ordered before it by
+    // __syncwarp) on this CTA's barrier; rank 1's are forwarded to rank 0 by its relay warps
+    auto arrive0 = [&](uint64_t* b) {
+        if (PAIR) {
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) tc::mbar_arrive(b);
+        } else {
+            tc::mbar_arrive(b);
+        }
+    };
+    auto commit = [&](uint64_t* b) {
+        if (PAIR) tc::mma_commit_pair(b);
+        else tc::mma_commit(b);
+    };
     uint32_t* const sk_ticket = tmem_slot + 1;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -379,25 +437,35 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
 
     if (tid == 0) {
         tc::mbar_init(q_full, 1);
-        tc::mbar_init(q_empty, 1);
+        tc::mbar_init(q_empty, PAIR ? 2 : 1);   // PAIR: released by both issuer warps
         for (int i = 0; i < KST; ++i) {
             tc::mbar_init(&k_full[i], 1);
-            tc::mbar_init(&k_empty[i], 1);
+            tc::mbar_init(&k_empty[i], PAIR ? 2 : 1);
         }
+        // softmax arrivals per hand-off: a thread each; PAIR: a lane per warp, + rank 1's relay on rank 0
+        const uint32_t NSOFT = PAIR ? (crank == 0 ? 5u : 4u) : 128u;
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&v_full[i], 1);
             tc::mbar_init(&v_empty[i], 1);
             tc::mbar_init(&s_full[i], 1);
-            tc::mbar_init(&p_full[i], 128);
-            for (int part = 0; part + 1 < kPParts; ++part) tc::mbar_init(&p_part[i * (kPParts - 1) + part], 128);
+            tc::mbar_init(&p_full[i], NSOFT);
+            for (int part = 0; part + 1 < kPParts; ++part) tc::mbar_init(&p_part[i * (kPParts - 1) + part], NSOFT);
             tc::mbar_init(&o_final[i], 1);
-            tc::mbar_init(&o_empty[i], 128);
+            tc::mbar_init(&o_empty[i], NSOFT);
+            if (PAIR) {
+                tc::mbar_init(&s_free[i], NSOFT);
+                tc::mbar_init(&p_empty[i], 1);
+            }
         }
         tc::fence_mbar_init();
     }
-    if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
+    if (warp == 0) {
+        if (PAIR) tc::tmem_alloc_pair<512>(tmem_slot);
+        else tc::tmem_alloc<512>(tmem_slot);
+    }
     tc::tc_fence_before();
     __syncthreads();
+    if (PAIR) tc::cluster_sync();   // both CTAs' barriers exist before any remote arrive / TMA byte
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     K2_CTA_STAMP(0);
@@ -425,7 +493,46 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                         tc::tma_load_2d(smem + (g ? OFF_Q1 : OFF_Q0) + kb * BLK, &qmap, kb * 64, (int)(s.head_row + g * TILE),
                                         q_full);
             };
-            while (next_seg(sg)) {
+            // PAIR: this CTA's Q tiles and K / V halves; rank 0's barriers count the pair's bytes
+            auto load_q2 = [&](const Seg& s) {
+                if (crank == 0) tc::mbar_arrive_expect_tx(q_full, 2 * (s.two ? 2 : 1) * TILE_BYTES);
+                const uint32_t qf = tc::at_rank0(q_full);
+                for (int g = 0; g < (s.two ? 2 : 1); ++g)
+                    for (int kb = 0; kb < 2; ++kb)
+                        tc::tma_load_2d_pair(smem + (g ? OFF_Q1 : OFF_Q0) + kb * BLK, &qmap, kb * 64, (int)(s.head_row + g * TILE), qf);
+            };
+            // ring item `it` into slot it % KST: a K half (keys 64 r .. 64 r + 63 of the tile, as two
+            // [64 x 64] SW128 blocks) or a V half (d columns 64 r .. 64 r + 63 of its 128 keys)
+            auto ring_load = [&](int64_t it, bool is_v, int64_t row0) {
+                const int sl = (int)(it % KST);
+                if (it >= KST) tc::mbar_wait(&k_empty[sl], (uint32_t)((it / KST - 1) & 1));
+                if (crank == 0) tc::mbar_arrive_expect_tx(&k_full[sl], 2 * L::SLOT);
+                const uint32_t fb = tc::at_rank0(&k_full[sl]);
+                uint8_t* const dst = smem + L::OFF_K + sl * L::SLOT;
+                if (is_v) {
+                    tc::tma_load_2d_pair(dst, &vmap, 64 * (int)crank, (int)row0, fb);
+                } else {
+                    for (int kb = 0; kb < 2; ++kb)
+                        tc::tma_load_2d_pair(dst + kb * (L::SLOT / 2), &kmap, kb * 64, (int)(row0 + 64 * crank), fb);
+                }
+            };
+            while (PAIR && next_seg(sg)) {
+                if (sg.nkv == 0) continue;
+                if (si == 0) load_q2(sg);
+                const int64_t kvrow0 = (((int64_t)sg.b * p.kv_heads + sg.kvh) * p.kv_cap) + (int64_t)sg.t0 * TILE;
+                ring_load(jj++, false, kvrow0);                       // K(0)
+                if (si > 0) {
+                    tc::mbar_wait(q_empty, (uint32_t)((si - 1) & 1));
+                    load_q2(sg);
+                }
+                if (sg.nkv > 1) ring_load(jj++, false, kvrow0 + TILE);   // K(1)
+                for (int64_t j = 0; j < sg.nkv; ++j) {
+                    ring_load(jj++, true, kvrow0 + j * TILE);                              // V(j)
+                    if (j + 2 < sg.nkv) ring_load(jj++, false, kvrow0 + (j + 2) * TILE);   // K(j+2)
+                }
+                ++si;
+            }
+            while (!PAIR && next_seg(sg)) {
                 if (sg.nkv == 0) continue;
                 if (si == 0) load_q(sg);   // the first segment's Q ahead of its K/V (nothing to wait for)
                 const int64_t kvrow0 = (((int64_t)sg.b * p.kv_heads + sg.kvh) * p.kv_cap) + (int64_t)sg.t0 * TILE;
@@ -436,11 +543,11 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                     if (jj >= KST) tc::mbar_wait(&k_empty[sk], (uint32_t)((jj / KST - 1) & 1));
                     tc::mbar_arrive_expect_tx(&k_full[sk], TILE_BYTES);
                     for (int kb = 0; kb < 2; ++kb)
-                        tc::tma_load_2d(smem + OFF_K + sk * TILE_BYTES + kb * BLK, &kmap, kb * 64, (int)(kvrow0 + j * TILE), &k_full[sk]);
+                        tc::tma_load_2d(smem + L::OFF_K + sk * TILE_BYTES + kb * BLK, &kmap, kb * 64, (int)(kvrow0 + j * TILE), &k_full[sk]);
                     if (jj >= 2) tc::mbar_wait(&v_empty[st], ph);
                     tc::mbar_arrive_expect_tx(&v_full[st], TILE_BYTES);
                     for (int kb = 0; kb < 2; ++kb)
-                        tc::tma_load_2d(smem + OFF_V + st * TILE_BYTES + kb * BLK, &vmap, kb * 64, (int)(kvrow0 + j * TILE), &v_full[st]);
+                        tc::tma_load_2d(smem + L::OFF_V + st * TILE_BYTES + kb * BLK, &vmap, kb * 64, (int)(kvrow0 + j * TILE), &v_full[st]);
                     if (j == 0 && si > 0) {   // later segments: once the previous one's MMAs release Q
                         tc::mbar_wait(q_empty, (uint32_t)((si - 1) & 1));
                         load_q(sg);
@@ -449,14 +556,17 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 ++si;
             }
         }
-      } else if (warp == 9) {
+      } else if (warp == 9 || (PAIR && crank == 0 && warp == 10)) {
         // ------------------------------------------------------------------ MMA issuer
+        // (PAIR: warp 9 issues Q tile 0's MMAs, warp 10 tile 1's -- two issuers, so neither
+        // tile's MMAs queue behind the other tile's P)
         // the whole warp runs the loop (warp-uniform descriptors); the elected lane issues
         const bool leader = tc::elect_one();
         constexpr uint32_t IDESC_S = tc::idesc_bf16_f32(128, 128, false, false);   // Q K^T, both K-major
         constexpr uint32_t IDESC_O = tc::idesc_bf16_f32(128, 128, false, true);    // P V, V MN-major
         const uint32_t q0 = tc::smem_u32(smem + OFF_Q0), q1 = tc::smem_u32(smem + OFF_Q1);
-        const uint32_t kbase = tc::smem_u32(smem + OFF_K), vbase = tc::smem_u32(smem + OFF_V);
+        const uint32_t kbase = tc::smem_u32(smem + L::OFF_K), vbase = tc::smem_u32(smem + L::OFF_V);
+        const uint32_t pbase = tc::smem_u32(smem + L::OFF_P);   // PAIR
         auto issue_s = [&](int g, int st) {
             const uint32_t qa = g ? q1 : q0;
             const uint32_t kb = kbase + st * TILE_BYTES;
@@ -503,7 +613,95 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
         int si = 0;
         uint32_t pc[2] = {0u, 0u}, ou[2] = {0u, 0u};   // P tiles consumed / segments accumulated, per Q tile
         Seg sg;
-        while (next_seg(sg)) {
+        // ---- PAIR (rank 0 only): M = 256 MMAs over both CTAs' rows, one issuer warp per Q tile g.
+        // S runs two tiles ahead of P: per step PV_g(j) then S_g(j+2) -- PV_g(j) once P_g(j) is in
+        // both CTAs' SMEM, S_g(j+2) once both CTAs' softmax hold S_g(j+1) in registers (s_free).
+        // Ring slots and Q are released by both issuers (k_empty / q_empty count 2).
+        const int gi = warp - 9;
+        constexpr uint32_t IDESC_S2 = tc::idesc_bf16_f32(256, 128, false, false);
+        constexpr uint32_t IDESC_O2 = tc::idesc_bf16_f32(256, 128, false, true);
+        uint32_t ns[2] = {0u, 0u};   // S tiles issued per Q tile
+        auto s_next2 = [&](int g, int sl) {
+            if (ns[g] > 0) tc::mbar_wait_cluster(&s_free[g], (ns[g] - 1) & 1);
+            tc::tc_fence_after();
+            const uint32_t qa = g ? q1 : q0;
+            const uint32_t kb = kbase + sl * L::SLOT;
+#pragma unroll
+            for (int k = 0; k < D / 16; ++k) {
+                const uint64_t da = tc::sw128_desc(qa + (k >> 2) * BLK + (k & 3) * 32, 16, 1024);
+                const uint64_t db = tc::sw128_desc(kb + (k >> 2) * (L::SLOT / 2) + (k & 3) * 32, 16, 1024);
+                if (leader) tc::mma_bf16_ss_pair(tmem + (g ? COL_S1 : COL_S0), da, db, IDESC_S2, k > 0 ? 1u : 0u);
+            }
+            if (leader) tc::mma_commit_pair(&s_full[g]);
+            ++ns[g];
+        };
+        auto pv2 = [&](int g, int sl, bool acc, uint32_t n) {
+            const uint32_t ph = n & 1;
+            const uint32_t vb = kbase + sl * L::SLOT;
+            const uint32_t pa = pbase + g * TILE_BYTES;
+            auto issue = [&](int k0, int k1, bool a) {
+#pragma unroll
+                for (int k = k0; k < k1; ++k) {
+                    const uint64_t da = tc::sw128_desc(pa + (k >> 2) * BLK + (k & 3) * 32, 16, 1024);
+                    const uint64_t db = tc::sw128_desc(vb + k * 2048, BLK, 1024);
+                    if (leader) tc::mma_bf16_ss_pair(tmem + (g ? COL_O1 : COL_O0), da, db, IDESC_O2, (a || k > 0) ? 1u : 0u);
+                }
+            };
+            constexpr int KPP = TILE / 16 / kPParts;
+#pragma unroll
+            for (int part = 0; part + 1 < kPParts; ++part) {
+                tc::mbar_wait_cluster(&p_part[g * (kPParts - 1) + part], ph);
+                tc::tc_fence_after();
+                issue(part * KPP, (part + 1) * KPP, acc);
+            }
+            if (g == 0) K2_STAMP(18, n);
+            tc::mbar_wait_cluster(&p_full[g], ph);
+            if (g == 0) K2_STAMP(19, n);
+            tc::tc_fence_after();
+            issue((kPParts - 1) * KPP, TILE / 16, kPParts > 1 ? true : acc);
+        };
+        while (PAIR && crank == 0 && next_seg(sg)) {
+            if (sg.nkv == 0) continue;
+            tc::mbar_wait_cluster(q_full, (uint32_t)(si & 1));
+            for (int t = 0; t < 2 && t < sg.nkv; ++t) {   // K(0), K(1): S_g(0), S_g(1)
+                const int sl = (int)(jj % KST);
+                tc::mbar_wait_cluster(&k_full[sl], (uint32_t)((jj / KST) & 1));
+                s_next2(gi, sl);
+                if (leader) tc::mma_commit_pair(&k_empty[sl]);
+                ++jj;
+            }
+            for (int64_t j = 0; j < sg.nkv; ++j) {
+                const int slv = (int)(jj % KST);   // V(j)
+                const int64_t jk = jj + 1;         // K(j+2), if any
+                const int slk = (int)(jk % KST);
+                const bool more = j + 2 < sg.nkv;
+                if (gi == 0) K2_STAMP(6, j);
+                tc::mbar_wait_cluster(&k_full[slv], (uint32_t)((jj / KST) & 1));
+                if (gi == 0) K2_STAMP(7, j);
+                if (j == 0 && ou[gi] > 0) tc::mbar_wait_cluster(&o_empty[gi], (ou[gi] - 1) & 1);
+                K2_STAMP(4 + gi, j);
+                pv2(gi, slv, j > 0, pc[gi]);
+                ++pc[gi];
+                if (leader) tc::mma_commit_pair(&p_empty[gi]);
+                if (j + 1 == sg.nkv && leader) tc::mma_commit_pair(&o_final[gi]);
+                if (more) {
+                    if (gi == 0) K2_STAMP(9, j);
+                    tc::mbar_wait_cluster(&k_full[slk], (uint32_t)((jk / KST) & 1));
+                    if (gi == 0) K2_STAMP(10, j);
+                    s_next2(gi, slk);
+                }
+                if (leader) tc::mma_commit_pair(&k_empty[slv]);
+                ++jj;
+                if (more) {
+                    if (leader) tc::mma_commit_pair(&k_empty[slk]);
+                    ++jj;
+                }
+            }
+            ++ou[gi];
+            if (leader) tc::mma_commit_pair(q_empty);
+            ++si;
+        }
+        while (!PAIR && next_seg(sg)) {
             if (sg.nkv == 0) continue;
             const bool two = sg.two;
             tc::mbar_wait(q_full, (uint32_t)(si & 1));
@@ -554,6 +752,35 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             jj += sg.nkv;
             ++si;
         }
+      } else if (PAIR && crank == 1 && lane == 0) {
+        // ------------------------------------------------------------------ relay (PAIR, rank 1)
+        // Rank 1's softmax warps arrive on their own CTA's copies of s_free / p_part / p_full /
+        // o_empty (cta scope); warp 10 (Q tile 0) / 11 (tile 1) forwards each completed phase to
+        // rank 0's barrier with one relaxed cluster arrive. (A release.cluster arrive costs a
+        // MEMBAR.GPU, ~0.7 us: per softmax warp and hand-off that was ~1 us of every tile, and
+        // still ~0.7 us of hand-off latency in the relay.)
+        const int g = warp - 10;
+        uint32_t n_t = 0, n_o = 0;   // tiles / segments relayed
+        Seg sg;
+        while (next_seg(sg)) {
+            if (!(g == 0 || sg.two)) continue;
+            for (int j = 0; j < sg.nkv; ++j, ++n_t) {
+                tc::mbar_wait_spin(&s_free[g], n_t & 1);
+                tc::mbar_arrive_remote_relaxed(tc::at_rank0(&s_free[g]));
+                for (int part = 0; part + 1 < kPParts; ++part) {
+                    tc::mbar_wait_spin(&p_part[g * (kPParts - 1) + part], n_t & 1);
+                    tc::mbar_arrive_remote_relaxed(tc::at_rank0(&p_part[g * (kPParts - 1) + part]));
+                }
+                tc::mbar_wait_spin(&p_full[g], n_t & 1);
+                if (g == 0) K2_STAMP1(20, n_t);
+                tc::mbar_arrive_remote_relaxed(tc::at_rank0(&p_full[g]));
+            }
+            if (p.sk || sg.nkv > 0) {
+                tc::mbar_wait_spin(&o_empty[g], n_o & 1);
+                tc::mbar_arrive_remote_relaxed(tc::at_rank0(&o_empty[g]));
+                ++n_o;
+            }
+        }
       }
     } else {
 #if SDA_K2_SETMAXNREG
@@ -566,7 +793,11 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
         const uint32_t s_col = tmem + (g ? COL_S1 : COL_S0) + lane_off;
         const uint32_t o_col = tmem + (g ? COL_O1 : COL_O0) + lane_off;
         uint32_t sc = 0, oc = 0;                               // S tiles / segments seen by this group
-        SoftKeep* const keep = reinterpret_cast<SoftKeep*>(smem + OFF_SEG) + warp;
+        SoftKeep* const keep = reinterpret_cast<SoftKeep*>(smem + L::OFF_SEG) + warp;
+        static_assert(!PAIR || (SDA_K2_SUM_AFTER && !SDA_K2_SPEC), "pair form: row sum after P, no speculation");
+        // PAIR: this row of P_g in SMEM (SW128 K-major: 64-key blocks of 128-byte rows, 16-byte
+        // chunks XOR-swizzled by row & 7 -- 8 consecutive rows cover all banks)
+        const uint32_t p_row = tc::smem_u32(smem + L::OFF_P + g * TILE_BYTES) + (uint32_t)row * 128u;
         if (lane == 0) {
             keep->cur = cur;
             keep->T = T_sk;
@@ -610,12 +841,30 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 ++sc;
                 tc::tc_fence_after();
                 if ((warp & 3) == 0 && lane == 0) K2_STAMP(g, j);
+                // PAIR: P_g(t) may go into SMEM once PV_g(t-1) is done (t = sc - 1, this group's tiles)
+                bool pe_pending = PAIR && sc >= 2;
+                auto wait_pe = [&]() {
+                    if (pe_pending) {
+                        if (warp == 0 && lane == 0) K2_STAMP(16, j);
+                        tc::mbar_wait(&p_empty[g], (sc - 2) & 1);
+                        if (warp == 0 && lane == 0) K2_STAMP(17, j);
+                        tc::tc_fence_after();
+                        pe_pending = false;
+                    }
+                };
                 if (!warp_live) {
                     tc::tc_fence_before();
+                    if (PAIR) {
+                        // its P arrivals wait for PV_g(t-1) like the live warps' do: S_g(t) can be
+                        // in before the live warps have announced P_g(t-1), and an early arrival
+                        // would complete that phase of p_full
+                        arrive0(&s_free[g]);
+                        wait_pe();
+                    }
 #if SDA_K2_PSPLIT
-                    for (int part = 0; part + 1 < kPParts; ++part) tc::mbar_arrive(&p_part[g * (kPParts - 1) + part]);
+                    for (int part = 0; part + 1 < kPParts; ++part) arrive0(&p_part[g * (kPParts - 1) + part]);
 #endif
-                    tc::mbar_arrive(&p_full[g]);
+                    arrive0(&p_full[g]);
                     continue;
                 }
                 uint32_t s[128];
@@ -657,6 +906,20 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 };
                 auto exp_pass = [&](float mu, bool with_max, float& mr0, float& mr1) { exp_range(mu, with_max, mr0, mr1, 0, 64); };
                 load_s();
+                if (PAIR) {   // S_g is in registers: the MMA may compute S_g(j+1) into the same columns
+                    tc::tc_fence_before();
+                    arrive0(&s_free[g]);
+                }
+                // PAIR: keys 8cc .. 8cc+7 of this row of P into SMEM
+                auto st_chunk = [&](int cc) {
+                    const uint32_t a = p_row + (uint32_t)(cc >> 3) * BLK + ((uint32_t)((cc & 7) ^ (row & 7)) << 4);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                                 "r"(tc::pack_bf16(__uint_as_float(s[8 * cc + 0]), __uint_as_float(s[8 * cc + 1]))),
+                                 "r"(tc::pack_bf16(__uint_as_float(s[8 * cc + 2]), __uint_as_float(s[8 * cc + 3]))),
+                                 "r"(tc::pack_bf16(__uint_as_float(s[8 * cc + 4]), __uint_as_float(s[8 * cc + 5]))),
+                                 "r"(tc::pack_bf16(__uint_as_float(s[8 * cc + 6]), __uint_as_float(s[8 * cc + 7])))
+                                 : "memory");
+                };
                 float mr0 = -INFINITY, mr1 = -INFINITY;
 #if SDA_K2_SPEC
                 // speculative: once every row of the warp has a base, exponentiate against it with
@@ -696,6 +959,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 // lazy rescale: keep the exponent base unless the max grew by more than 8 (x256)
                 const bool need = m_new > m_use + 8.f;
                 if (__any_sync(0xffffffffu, need && j > 0 && m_use > -INFINITY)) {
+                    wait_pe();   // PAIR: O_g holds PV_g(j-1) only once it has completed
                     const float alpha = (need && m_use > -INFINITY) ? ex2(m_use - m_new) : 1.f;
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
@@ -725,17 +989,24 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                     for (int part = 0; part < kPParts; ++part) {
                         exp_range(mu, false, mr0, mr1, part * PP, (part + 1) * PP);
                         if (part + 1 == kPParts) break;
+                        if (PAIR) {
+                            wait_pe();
 #pragma unroll
-                        for (int c = part * PP / 8; c < (part + 1) * PP / 8; ++c) {
-                            uint32_t pk[8];
+                            for (int cc = part * PP / 4; cc < (part + 1) * PP / 4; ++cc) st_chunk(cc);
+                            tc::fence_proxy_async_smem();
+                        } else {
 #pragma unroll
-                            for (int e = 0; e < 8; ++e)
-                                pk[e] = tc::pack_bf16(__uint_as_float(s[16 * c + 2 * e]), __uint_as_float(s[16 * c + 2 * e + 1]));
-                            tc::tmem_st8(s_col + c * 8, pk);
+                            for (int c = part * PP / 8; c < (part + 1) * PP / 8; ++c) {
+                                uint32_t pk[8];
+#pragma unroll
+                                for (int e = 0; e < 8; ++e)
+                                    pk[e] = tc::pack_bf16(__uint_as_float(s[16 * c + 2 * e]), __uint_as_float(s[16 * c + 2 * e + 1]));
+                                tc::tmem_st8(s_col + c * 8, pk);
+                            }
+                            tc::tmem_st_wait();
                         }
-                        tc::tmem_st_wait();
                         tc::tc_fence_before();
-                        tc::mbar_arrive(&p_part[g * (kPParts - 1) + part]);
+                        arrive0(&p_part[g * (kPParts - 1) + part]);
                     }
                 } else if (!spec) {
                     exp_pass((m_use == -INFINITY) ? 0.f : m_use, false, mr0, mr1);
@@ -749,23 +1020,34 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
 #if SDA_K2_SUM_AFTER
                 // P to TMEM first (packed 16 at a time; the fp32 values stay in s[]), the row sum
                 // after the arrive: the FADD2 chains leave the softmax -> PV -> S chain
+                if (PAIR) {
+                    wait_pe();
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    if (psplit && c < (kPParts - 1) * 8 / kPParts) continue;   // already in TMEM
-                    uint32_t pk[8];
+                    for (int cc = 0; cc < 16; ++cc) {
+                        if (psplit && cc < (kPParts - 1) * 16 / kPParts) continue;   // already in SMEM
+                        st_chunk(cc);
+                    }
+                    tc::fence_proxy_async_smem();
+                } else {
 #pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        pk[e] = tc::pack_bf16(__uint_as_float(s[16 * c + 2 * e]), __uint_as_float(s[16 * c + 2 * e + 1]));
-                    tc::tmem_st8(s_col + c * 8, pk);
+                    for (int c = 0; c < 8; ++c) {
+                        if (psplit && c < (kPParts - 1) * 8 / kPParts) continue;   // already in TMEM
+                        uint32_t pk[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            pk[e] = tc::pack_bf16(__uint_as_float(s[16 * c + 2 * e]), __uint_as_float(s[16 * c + 2 * e + 1]));
+                        tc::tmem_st8(s_col + c * 8, pk);
+                    }
+                    tc::tmem_st_wait();
                 }
-                tc::tmem_st_wait();
                 tc::tc_fence_before();
                 if ((warp & 3) == 0 && lane == 0) K2_STAMP(2 + g, j);
+                if (warp == 0 && lane == 0) K2_STAMP1(21, j);
 #if SDA_K2_PSPLIT
                 if (!psplit)   // (speculative path: whole P at once)
-                    for (int part = 0; part + 1 < kPParts; ++part) tc::mbar_arrive(&p_part[g * (kPParts - 1) + part]);
+                    for (int part = 0; part + 1 < kPParts; ++part) arrive0(&p_part[g * (kPParts - 1) + part]);
 #endif
-                tc::mbar_arrive(&p_full[g]);
+                arrive0(&p_full[g]);
 #pragma unroll
                 for (int i = 0; i < 64; ++i)
                     acc[i & 3] = tc::fadd2(acc[i & 3], tc::f2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])));
@@ -837,7 +1119,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                     }
                     ++oc;
                     tc::tc_fence_before();
-                    tc::mbar_arrive(&o_empty[g]);   // O_g may be overwritten by the next segment
+                    arrive0(&o_empty[g]);   // O_g may be overwritten by the next segment
                     if (store) *reinterpret_cast<float2*>(dst_st + r_in * 2) = make_float2(st_max, st_sum);
                 }
                 if (tid == 0) K2_STAMP(13, si_tr);
@@ -979,7 +1261,8 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 // 16 KB run -- whole 512-byte rows per warp store instead of 32 scattered 16-byte
                 // pieces, which NVLink carries far less efficiently
                 // (rows of 512 B, 16-byte chunks XOR-swizzled by row & 7 against bank conflicts)
-                float* stg = reinterpret_cast<float*>(smem + (g ? OFF_V : OFF_K) + (warp & 3) * 32 * 128 * 4);
+                // (the pair form does not run split-mode remote records: launch_k2_prefill_tc)
+                float* stg = reinterpret_cast<float*>(smem + (g ? L::OFF_V : L::OFF_K) + (warp & 3) * 32 * 128 * 4);
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     uint32_t o[16];
@@ -1018,7 +1301,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             if (group_live && nkv > 0) {   // O_g may be overwritten by this CTA's next segment (causal pairs)
                 ++oc;
                 tc::tc_fence_before();
-                tc::mbar_arrive(&o_empty[g]);
+                arrive0(&o_empty[g]);
             }
         }
         if (p.sk) {
@@ -1076,7 +1359,12 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             flag_raise(p.peer_flag[dest], *p.epoch);
         }
     }
-    if (warp == 0) tc::tmem_dealloc<512>(tmem);
+    if (PAIR) {
+        tc::cluster_sync();   // the peer's MMAs (issued by rank 0) and TMEM reads are done
+        if (warp == 0) tc::tmem_dealloc_pair<512>(tmem);
+    } else if (warp == 0) {
+        tc::tmem_dealloc<512>(tmem);
+    }
 }
 
 bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
@@ -1138,10 +1426,31 @@ size_t k2_prefill_sk_workspace_bytes(const K2Params& q) {
     return sk_shape(q.n_batch, q.q_heads, q.q_rows, q.kv_cap).bytes;
 }
 
+// the CTA-pair form as a cluster-of-2 launch
+static cudaError_t launch_pair(dim3 grid, const K2TcParams& p, const CUtensorMap& qm, const CUtensorMap& km,
+                               const CUtensorMap& vm, cudaStream_t st) {
+    using namespace k2tc;
+    const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k2_prefill_tc_kernel<true>), Lay<true>::SMEM);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = Lay<true>::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k2_prefill_tc_kernel<true>, p, qm, km, vm);
+}
+
 cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
     using namespace k2tc;
     {
-        const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k2_prefill_tc_kernel), SMEM);
+        const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k2_prefill_tc_kernel<false>), SMEM);
         if (e != cudaSuccess) return e;
     }
     K2TcParams p;
@@ -1173,11 +1482,18 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
     p.causal = q.causal ? 1 : 0;
     p.causal_offset = q.causal_offset;
     if (p.causal && p.grouped) return cudaErrorInvalidValue;
-    CUtensorMap qm, km, vm;
+    CUtensorMap qm, km, vm, km64;
     if (!make_tmap_bf16_2d(&qm, q.q, q.n_batch * q.q_heads * q.q_rows, D, TILE) ||
         !make_tmap_bf16_2d(&km, q.k, q.n_batch * q.kv_heads * q.kv_cap, D, TILE) ||
-        !make_tmap_bf16_2d(&vm, q.v, q.n_batch * q.kv_heads * q.kv_cap, D, TILE))
+        !make_tmap_bf16_2d(&vm, q.v, q.n_batch * q.kv_heads * q.kv_cap, D, TILE) ||
+        !make_tmap_bf16_2d(&km64, q.k, q.n_batch * q.kv_heads * q.kv_cap, D, TILE / 2))
         return cudaErrorInvalidValue;
+    // CTA pairs (opt-in, SDA_K2_PAIR=1; measured slower on C3): whole 256-row Q-tile
+    // pairs everywhere, clusters of two CTAs that walk the same key tiles (stream-K groups of an
+    // even size, or split mode's even pair count), no causal mask / grouped rows / split-mode
+    // remote records
+    const char* pe = std::getenv("SDA_K2_PAIR");
+    const bool pair_ok = pe && pe[0] == '1' && !p.grouped && !p.causal && q.q_rows % (2 * TILE) == 0;
     // One split (not grouped) with the caller's workspace: stream-K over a persistent grid of
     // groups of n_qpairs CTAs, one CTA per SM, so the last wave is never partial (C3: 256 units
     // on 148 SMs ran as 2 waves, the second 73 % full).
@@ -1188,14 +1504,16 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
             p.sk_gq = (int)sh.gq;
             p.sk_tick = static_cast<uint32_t*>(q.sk_work);
             p.sk_buf = reinterpret_cast<float*>(static_cast<char*>(q.sk_work) + sh.tick_bytes);
-            k2_prefill_tc_kernel<<<dim3((unsigned)sh.ctas), THREADS, SMEM, st>>>(p, qm, km, vm);
+            if (pair_ok && sh.gq % 2 == 0) return launch_pair(dim3((unsigned)sh.ctas), p, qm, km64, vm, st);
+            k2_prefill_tc_kernel<false><<<dim3((unsigned)sh.ctas), THREADS, SMEM, st>>>(p, qm, km, vm);
             return cudaGetLastError();
         }
     }
     const dim3 grid = p.causal ? dim3((unsigned)q.q_heads, (unsigned)((p.n_qpairs + 1) / 2), (unsigned)(q.n_batch * q.n_splits))
                                : dim3((unsigned)p.n_qpairs, (unsigned)(p.grouped ? q.kv_heads : q.q_heads),
                                       (unsigned)(q.n_batch * q.n_splits));
-    k2_prefill_tc_kernel<<<grid, THREADS, SMEM, st>>>(p, qm, km, vm);
+    if (pair_ok && !p.remote && p.n_qpairs % 2 == 0) return launch_pair(grid, p, qm, km64, vm, st);
+    k2_prefill_tc_kernel<false><<<grid, THREADS, SMEM, st>>>(p, qm, km, vm);
     return cudaGetLastError();
 }
 

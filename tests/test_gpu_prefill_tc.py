@@ -43,6 +43,22 @@ def _k2(q, k, v, kv_len, n_splits, simt=False, grouped=False):
     (513, 384, [384], 1, 1, 1),
 ])
 def test_prefill_tc_vs_oracle(lq, cap, kv_len, n_splits, hq, hkv):
+    _check_vs_oracle(lq, cap, kv_len, n_splits, hq, hkv)
+
+
+@pytest.mark.parametrize("lq,cap,kv_len,n_splits,hq,hkv", [
+    (512, 1024, [1024], 2, 2, 2),            # split grid, two 256-row pairs per head = one cluster
+    (1024, 4096, [4096, 3000], 1, 4, 4),     # stream-K, groups of 4 CTAs = 2 clusters
+    (1024, 2000, [2000, 77], 3, 4, 2),       # split grid, ragged kv_len, GQA
+])
+def test_prefill_tc_pair_form_vs_oracle(lq, cap, kv_len, n_splits, hq, hkv, monkeypatch):
+    """The opt-in CTA-pair form (SDA_K2_PAIR=1: M = 256 tcgen05.mma over a cluster of two CTAs,
+    each holding half of every K / V tile, P in shared memory) against the oracle."""
+    monkeypatch.setenv("SDA_K2_PAIR", "1")
+    _check_vs_oracle(lq, cap, kv_len, n_splits, hq, hkv)
+
+
+def _check_vs_oracle(lq, cap, kv_len, n_splits, hq, hkv):
     B, d = len(kv_len), 128
     q = C.round_to_format(gauss(31, (B, hq, lq, d)), 2)
     k = C.round_to_format(gauss(32, (B, hkv, cap, d)), 2)

@@ -43,7 +43,12 @@ def check(lq, cap, kv_len, n_splits, hq, hkv):
     print(f"lq {lq} cap {cap} kv_len {kv_len} splits {n_splits} hq {hq} hkv {hkv}: {'OK' if not bad else f'{bad} bad (b,h,s)'}")
 
 
+SHAPES = [(128, 1024, [1024], 1, 2, 2), (256, 1024, [1024], 1, 2, 2), (256, 1024, [1024], 2, 2, 2),
+          (300, 1000, [1000, 517], 3, 4, 2), (300, 1000, [1000, 517], 1, 4, 2), (512, 2048, [2048], 1, 4, 4),
+          # CTA-pair shapes (whole 256-row pairs, an even pair count / stream-K group)
+          (512, 1024, [1024], 2, 2, 2), (1024, 4096, [4096, 3000], 1, 4, 4), (1024, 2000, [2000, 77], 3, 4, 2),
+          (2048, 16384, [16384], 1, 32, 32)]
+
 if __name__ == "__main__":
-    for args in [(128, 1024, [1024], 1, 2, 2), (256, 1024, [1024], 1, 2, 2), (256, 1024, [1024], 2, 2, 2),
-                 (300, 1000, [1000, 517], 3, 4, 2), (300, 1000, [1000, 517], 1, 4, 2), (512, 2048, [2048], 1, 4, 4)]:
+    for args in (SHAPES[int(sys.argv[1]):] if len(sys.argv) > 1 else SHAPES):
         check(*args)

@@ -23,7 +23,7 @@ def main():
     for _ in range(3):
         ops.partial_attention(q, k, v, n_splits=S)
     torch.cuda.synchronize()
-    buf = np.zeros((16, 64), dtype=np.uint64)
+    buf = np.zeros((24, 64), dtype=np.uint64)
     capi.LIB.sda_debug_k2_trace.argtypes = [ct.c_void_p]
     assert capi.LIB.sda_debug_k2_trace(buf.ctypes.data) == 0
     t = buf.astype(np.int64)
@@ -51,7 +51,7 @@ def main_causal():
     for _ in range(3):
         ops.partial_attention_causal(q, k, v, causal_offset=0, n_splits=1)
     torch.cuda.synchronize()
-    buf = np.zeros((16, 64), dtype=np.uint64)
+    buf = np.zeros((24, 64), dtype=np.uint64)
     capi.LIB.sda_debug_k2_trace.argtypes = [ct.c_void_p]
     assert capi.LIB.sda_debug_k2_trace(buf.ctypes.data) == 0
     t = buf.astype(np.int64)
@@ -84,7 +84,7 @@ def main_sk():
     for _ in range(3):
         ops.partial_attention(q, k, v, n_splits=1)
     torch.cuda.synchronize()
-    buf = np.zeros((16, 64), dtype=np.uint64)
+    buf = np.zeros((24, 64), dtype=np.uint64)
     capi.LIB.sda_debug_k2_trace.argtypes = [ct.c_void_p]
     assert capi.LIB.sda_debug_k2_trace(buf.ctypes.data) == 0
     t = buf.astype(np.int64)
@@ -112,5 +112,32 @@ def main_sk():
         pass
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not os.environ.get("PAIR"):
     main_causal() if os.environ.get("CAUSAL") else (main_sk() if os.environ.get("SK") else main())
+
+
+def main_pair():
+    """CTA-pair form (split grid, CTAs 0/1 = one cluster): per tile j of Q tile 0 -- the leader's
+    softmax wait for PV(j-1) before its P store (16/17), the rank-1 softmax's P arrive (21) and
+    its relay forwarding it (20), the MMA warp's wait for the pair's P (18 -> 19); ns from sm0_wait(j)."""
+    Lq, Lk, H, S, D = 2048, 16384, 32, 4, 128
+    dev = torch.device("cuda")
+    q = torch.randn((1, H, Lq, D), device=dev).to(torch.bfloat16)
+    k = torch.randn((1, H, Lk, D), device=dev).to(torch.bfloat16)
+    v = torch.randn((1, H, Lk, D), device=dev).to(torch.bfloat16)
+    for _ in range(3):
+        ops.partial_attention(q, k, v, n_splits=S)
+    torch.cuda.synchronize()
+    buf = np.zeros((24, 64), dtype=np.uint64)
+    capi.LIB.sda_debug_k2_trace.argtypes = [ct.c_void_p]
+    assert capi.LIB.sda_debug_k2_trace(buf.ctypes.data) == 0
+    t = buf.astype(np.int64)
+    print(" j  sm0_wait  pe_wait  pe_done  sm0_arr(r0)  sm0_arr(r1)  relay(r1)  mma_wait_p  mma_got_p  next sm0_wait")
+    for j in range(2, 30):
+        b = t[0][j]
+        f = lambda k, jj=j: int(t[k][jj] - b) if t[k][jj] else -1  # noqa: E731
+        print(f"{j:2d} {b - t[0][0]:9d} {f(16):8d} {f(17):8d} {f(2):11d} {f(21):11d} {f(20):10d} {f(18):11d} {f(19):10d} {int(t[0][j + 1] - b):10d}")
+
+
+if __name__ == "__main__" and os.environ.get("PAIR"):
+    main_pair()
