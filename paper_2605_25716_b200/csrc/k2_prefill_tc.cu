@@ -132,8 +132,24 @@ constexpr int OFF_BAR = OFF_V + 2 * TILE_BYTES;
 // barriers: q_full, k_full[KST], k_empty[KST], v_full[2], v_empty[2], s_full[2], p_full[2],
 // o_final[2], q_empty, o_empty[2], p_part[2][kPParts - 1]
 constexpr int NBAR = 14 + 2 * KST + 2 * (SDA_K2_PPARTS > 1 ? SDA_K2_PPARTS - 1 : 0);
+// Split rows (SDA_K2_HELP=1): each Q tile's softmax runs on two warpgroups -- the primary warps
+// 0-7 take keys 0-63 of every tile (and everything else: the O rescale, the epilogue, stream-K
+// merges), helper warps 12-19 keys 64-127 of the same rows (the same TMEM lanes: warp % 4). The
+// per-tile chain S -> softmax -> PV -> S then carries half the exponentials per thread. The two
+// halves of a row exchange their tile max (and, at a segment's end, the row sum) through shared
+// memory under a 64-thread named barrier per (tile, lane quarter); the primary hands P's first
+// 64 keys to the MMA on p_part, the helper the second 64 on p_full.
+#ifndef SDA_K2_HELP
+#define SDA_K2_HELP 0
+#endif
+constexpr bool kHelp = SDA_K2_HELP != 0;
+static_assert(!kHelp || SDA_K2_PPARTS == 2, "split rows hand P over in two parts");
+constexpr int SEG_SLOTS = kHelp ? 16 : 8;
+// exchange: tile max [tile parity][primary, helper][Q tile][row], row sum [segment parity][Q tile][row]
+constexpr int XCH_BYTES = kHelp ? (2 * 2 * 2 * 128 + 2 * 2 * 128) * 4 : 0;
 constexpr int OFF_SEG = OFF_BAR + NBAR * 8 + 16;   // per softmax warp: segment state (SoftKeep)
-constexpr int SMEM = OFF_SEG + 8 * 128;
+constexpr int OFF_XCH = OFF_SEG + SEG_SLOTS * 128;
+constexpr int SMEM = OFF_XCH + XCH_BYTES;
 // The CTA-pair form (PAIR; opt-in, SDA_K2_PAIR=1 -- parity-green but 495-505 us on C3 against
 // 445-454 us for the form above: with the chain decoupled both softmax groups run at once and
 // each takes 1.5-1.8 us per tile instead of 1.05, so the SM's softmax throughput, not the chain,
@@ -156,7 +172,8 @@ struct Lay {
     // + PAIR: s_free[2] (softmax holds S_g in registers), p_empty[2] (PV_g done: P_g reusable)
     static constexpr int NBAR = 14 + 2 * KST + 2 * (SDA_K2_PPARTS > 1 ? SDA_K2_PPARTS - 1 : 0) + (PAIR ? 4 : 0);
     static constexpr int OFF_SEG = OFF_BAR + NBAR * 8 + 16;
-    static constexpr int SMEM = OFF_SEG + 8 * 128;
+    static constexpr int OFF_XCH = OFF_SEG + (PAIR ? 8 : SEG_SLOTS) * 128;
+    static constexpr int SMEM = OFF_XCH + (PAIR ? 0 : XCH_BYTES);
 };
 static_assert(Lay<true>::SMEM <= 232448, "pair form exceeds the 227 KB opt-in SMEM");
 static_assert(Lay<false>::SMEM == SMEM, "layouts");
@@ -171,6 +188,15 @@ constexpr int THREADS = 384;
 constexpr int THREADS = 320;
 #endif
 constexpr int kSoftmaxRegs = 224, kIssueRegs = 56;
+// split rows: 20 warps (primaries 0-7, issue warpgroup 8-11, helpers 12-19) launch at 96
+// registers; setmaxnreg only moves registers within the CTA's own allocation, so
+// 256 x 120 + 256 x 96 + 128 x 48 = 640 x 96
+constexpr int kPrimRegs = 120, kHelpRegs = 96, kIssueRegsHelp = 48;
+static_assert(256 * kPrimRegs + 256 * kHelpRegs + 128 * kIssueRegsHelp == 640 * 96, "register balance");
+template <bool PAIR> struct Thr {
+    static constexpr bool HELP = kHelp && !PAIR;
+    static constexpr int N = HELP ? 640 : THREADS;
+};
 constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 384;
 // Exponentials per 4 pairs computed on the FMA pipe (tc::exp2_fma2) instead of MUFU.EX2. Measured
 // on C3 (exps batched ahead of the packing): 0 -> 489 us, 1 -> 485 us, 2 -> 547 us -- past one in
@@ -179,6 +205,12 @@ constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 384;
 #define SDA_K2_EMU_OF4 1
 #endif
 constexpr int kEmuOf4 = SDA_K2_EMU_OF4;
+// Packed form (tc::exp2_fma2_packed: FADD2 / FFMA2, 5 issue slots per value against 8): the
+// fraction of pairs on the FMA pipe in eighths (0 = the scalar form at kEmuOf4 of four)
+#ifndef SDA_K2_EMU_OF8P
+#define SDA_K2_EMU_OF8P 0
+#endif
+constexpr int kEmuOf8P = SDA_K2_EMU_OF8P;
 #ifndef SDA_K2_SUM_AFTER
 #define SDA_K2_SUM_AFTER 1
 #endif
@@ -188,6 +220,7 @@ constexpr int kEmuOf4 = SDA_K2_EMU_OF4;
 #ifndef SDA_K2_MAX4
 #define SDA_K2_MAX4 0
 #endif
+static_assert(!kHelp || (SDA_K2_SETMAXNREG && !SDA_K2_SPEC), "split rows: setmaxnreg, no speculation");
 }  // namespace k2tc
 
 namespace k2tc {
@@ -365,7 +398,7 @@ __device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" 
 }  // namespace k2tc
 
 template <bool PAIR>
-__global__ void __launch_bounds__(k2tc::THREADS, 1)
+__global__ void __launch_bounds__(k2tc::Thr<PAIR>::N, 1)
 k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                      const __grid_constant__ CUtensorMap vmap) {
     using namespace k2tc;
@@ -470,9 +503,11 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
     const uint32_t tmem = *tmem_slot;
     K2_CTA_STAMP(0);
 
-    if (warp >= 8) {
+    constexpr bool HX = Thr<PAIR>::HELP;
+    if (warp >= 8 && (!HX || warp < 12)) {
 #if SDA_K2_SETMAXNREG
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kIssueRegs));
+      if constexpr (HX) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kIssueRegsHelp));
+      else asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kIssueRegs));
 #endif
       if (warp == 8) {
         // ------------------------------------------------------------------ TMA producer
@@ -782,9 +817,136 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             }
         }
       }
+    } else if (HX && warp >= 12) {
+        // (helpers stay at the launch's 96 registers)
+        // ------------------------------------------------------------------ split-row helpers
+        // keys 64-127 of every tile for the rows of primary warp (warp - 12): the same segment
+        // sequence, S loads, max exchange, base updates and row sum as the primary's half; no O
+        // rescale (the primary rescales all of O_g before it hands over P's first half, and PV
+        // waits for both halves) and no epilogue
+        const int hw = warp - 12;
+        const int g = hw >> 2;
+        const int row = (hw & 3) * 32 + lane;
+        const uint32_t s_col = tmem + (g ? COL_S1 : COL_S0) + ((uint32_t)((hw & 3) * 32) << 16);
+        float* const xch = reinterpret_cast<float*>(smem + L::OFF_XCH);
+        const uint32_t bar_id = 2u + (uint32_t)(g * 4 + (hw & 3));
+        SoftKeep* const keep = reinterpret_cast<SoftKeep*>(smem + L::OFF_SEG) + 8 + hw;
+        if (lane == 0) keep->cur = cur;
+        __syncwarp();
+        uint32_t sc = 0, segc = 0;
+        Seg sg0;
+        for (;;) {
+            if (!p.sk) {
+                if (lseg >= split_nseg(p)) break;
+                split_seg(p, sg0, lseg++);
+            } else {
+                SoftKeep* const k = opaque(keep);
+                SkCursor c = k->cur;
+                const bool ok = sk_next(p, (int)blockIdx.x % p.sk_gq, c, sg0);
+                __syncwarp();
+                if (lane == 0) k->cur = c;
+                __syncwarp();
+                if (!ok) break;
+            }
+            const int nkv = sg0.nkv;
+            const bool group_live = g == 0 || sg0.two;
+            const bool warp_live = g * TILE + (hw & 3) * 32 < sg0.nrows;
+            int kv_left = sg0.len - sg0.t0 * TILE;
+            if (p.causal) {
+                const int64_t qrow = sg0.head_row % p.q_rows + (int64_t)g * TILE + row;
+                const int64_t lim = min((int64_t)len_of(p, sg0.b), qrow + p.causal_offset + 1);
+                kv_left = (int)max((int64_t)-TILE, lim - (int64_t)sg0.t0 * TILE);
+            }
+            float m_run = -INFINITY, m_use = -INFINITY, l = 0.f;
+            for (int j = 0; group_live && j < nkv; ++j) {
+                tc::mbar_wait(&s_full[g], sc & 1);
+                const uint32_t par = sc & 1;
+                ++sc;
+                tc::tc_fence_after();
+                if ((hw & 3) == 0 && lane == 0) K2_STAMP(g ? 22 : 18, j);
+                if (!warp_live) {
+                    tc::tc_fence_before();
+                    tc::mbar_arrive(&p_full[g]);
+                    continue;
+                }
+                uint32_t s[64];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tc::tmem_ld16(s_col + 64 + c * 16, s + c * 16);
+                tc::tmem_ld_wait();
+                const int valid = kv_left - j * TILE - 64;
+                if (valid < 64) {
+#pragma unroll
+                    for (int i = 0; i < 64; ++i)
+                        if (i >= valid) s[i] = 0xFF800000u;
+                }
+                float mr0 = -INFINITY, mr1 = -INFINITY;
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    mr0 = tc::fmax3(mr0, __uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
+                    mr1 = tc::fmax3(mr1, __uint_as_float(s[2 * i + 2]), __uint_as_float(s[2 * i + 3]));
+                }
+                float mt = fmaxf(mr0, mr1) * p.scale_log2;
+                xch[(par * 2 + 1) * 256 + g * 128 + row] = mt;
+                asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+                mt = fmaxf(mt, xch[(par * 2 + 0) * 256 + g * 128 + row]);
+                const float m_new = fmaxf(m_run, mt);
+                m_run = m_new;
+                if (m_new > m_use + 8.f) {
+                    if (m_use > -INFINITY) l *= ex2(m_use - m_new);
+                    m_use = m_new;
+                }
+                const float mu = (m_use == -INFINITY) ? 0.f : m_use;
+                const uint64_t sc2 = tc::f2(p.scale_log2, p.scale_log2), nmu2 = tc::f2(-mu, -mu);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    float x0, x1, p0, p1;
+                    tc::f2_split(tc::ffma2(tc::f2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sc2, nmu2), x0, x1);
+                    if (kEmuOf8P > 0 && (i & 7) < kEmuOf8P) {
+                        tc::exp2_fma2_packed(x0, x1, p0, p1);
+                    } else if (kEmuOf8P == 0 && (i & 3) < kEmuOf4) {
+                        tc::exp2_fma2(x0, x1, p0, p1);
+                    } else {
+                        p0 = ex2(x0);
+                        p1 = ex2(x1);
+                    }
+                    s[2 * i] = __float_as_uint(p0);
+                    s[2 * i + 1] = __float_as_uint(p1);
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t pk[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        pk[e] = tc::pack_bf16(__uint_as_float(s[16 * c + 2 * e]), __uint_as_float(s[16 * c + 2 * e + 1]));
+                    tc::tmem_st8(s_col + 32 + c * 8, pk);
+                }
+                tc::tmem_st_wait();
+                tc::tc_fence_before();
+                if ((hw & 3) == 0 && lane == 0) K2_STAMP(g ? 23 : 19, j);
+                tc::mbar_arrive(&p_full[g]);
+                uint64_t acc[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) acc[a] = tc::f2(0.f, 0.f);
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    acc[i & 3] = tc::fadd2(acc[i & 3], tc::f2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])));
+                float a0, a1, b0, b1, c0, c1, d0, d1;
+                tc::f2_split(acc[0], a0, a1);
+                tc::f2_split(acc[1], b0, b1);
+                tc::f2_split(acc[2], c0, c1);
+                tc::f2_split(acc[3], d0, d1);
+                l += ((a0 + a1) + (b0 + b1)) + ((c0 + c1) + (d0 + d1));
+            }
+            if (group_live) {   // this half's row sum to the primary (double-buffered by segment)
+                xch[2 * 2 * 2 * 128 + (segc & 1) * 256 + g * 128 + row] = l;
+                asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+            }
+            ++segc;
+        }
     } else {
 #if SDA_K2_SETMAXNREG
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
+        if constexpr (HX) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kPrimRegs));
+        else asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
 #endif
         // ------------------------------------------------------------------ softmax groups
         const int g = warp >> 2;                               // Q tile
@@ -794,6 +956,11 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
         const uint32_t o_col = tmem + (g ? COL_O1 : COL_O0) + lane_off;
         uint32_t sc = 0, oc = 0;                               // S tiles / segments seen by this group
         SoftKeep* const keep = reinterpret_cast<SoftKeep*>(smem + L::OFF_SEG) + warp;
+        // split rows: this warp's half of the exchange with helper warp 12 + warp
+        float* const xch = reinterpret_cast<float*>(smem + L::OFF_XCH);
+        const uint32_t bar_id = 2u + (uint32_t)warp;
+        uint32_t segc = 0;
+        constexpr int NV = HX ? 64 : 128;   // logits of a row this thread takes per tile
         static_assert(!PAIR || (SDA_K2_SUM_AFTER && !SDA_K2_SPEC), "pair form: row sum after P, no speculation");
         // PAIR: this row of P_g in SMEM (SW128 K-major: 64-key blocks of 128-byte rows, 16-byte
         // chunks XOR-swizzled by row & 7 -- 8 consecutive rows cover all banks)
@@ -864,18 +1031,18 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
 #if SDA_K2_PSPLIT
                     for (int part = 0; part + 1 < kPParts; ++part) arrive0(&p_part[g * (kPParts - 1) + part]);
 #endif
-                    arrive0(&p_full[g]);
+                    if (!HX) arrive0(&p_full[g]);   // (split rows: the helper completes p_full)
                     continue;
                 }
                 uint32_t s[128];
                 const int valid = kv_left - (int)j * TILE;            // keys of this tile still in range
                 auto load_s = [&]() {
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) tc::tmem_ld16(s_col + c * 16, s + c * 16);
+                    for (int c = 0; c < NV / 16; ++c) tc::tmem_ld16(s_col + c * 16, s + c * 16);
                     tc::tmem_ld_wait();
-                    if (valid < TILE) {                               // only the unit's last tile
+                    if (valid < NV) {                                 // only the unit's last tile
 #pragma unroll
-                        for (int i = 0; i < 128; ++i)
+                        for (int i = 0; i < NV; ++i)
                             if (i >= valid) s[i] = 0xFF800000u;       // -inf
                     }
                 };
@@ -894,7 +1061,9 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                         float x0, x1;
                         tc::f2_split(tc::ffma2(tc::f2(r0, r1), sc2, nmu2), x0, x1);
                         float p0, p1;
-                        if ((i & 3) < kEmuOf4) {
+                        if (kEmuOf8P > 0 && (i & 7) < kEmuOf8P) {
+                            tc::exp2_fma2_packed(x0, x1, p0, p1);
+                        } else if (kEmuOf8P == 0 && (i & 3) < kEmuOf4) {
                             tc::exp2_fma2(x0, x1, p0, p1);
                         } else {
                             p0 = ex2(x0);
@@ -947,13 +1116,20 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                     mr1 = fmaxf(mr1, mr3);
 #else
 #pragma unroll
-                    for (int i = 0; i < 64; i += 2) {
+                    for (int i = 0; i < NV / 2; i += 2) {
                         mr0 = tc::fmax3(mr0, __uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
                         mr1 = tc::fmax3(mr1, __uint_as_float(s[2 * i + 2]), __uint_as_float(s[2 * i + 3]));
                     }
 #endif
                 }
-                const float mt = fmaxf(mr0, mr1) * p.scale_log2;
+                float mt = fmaxf(mr0, mr1) * p.scale_log2;
+                if (HX) {   // the row's other half: the helper's tile max
+                    const uint32_t par = (sc - 1) & 1;
+                    xch[(par * 2 + 0) * 256 + g * 128 + row] = mt;
+                    asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+                    mt = fmaxf(mt, xch[(par * 2 + 1) * 256 + g * 128 + row]);
+                    if (warp == 0 && lane == 0) K2_STAMP(20, j);
+                }
                 const float m_new = fmaxf(m_run, mt);
                 m_run = m_new;
                 // lazy rescale: keep the exponent base unless the max grew by more than 8 (x256)
@@ -978,6 +1154,36 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 if (need) {
                     if (m_use > -INFINITY) l *= ex2(m_use - m_new);
                     m_use = m_new;
+                }
+                if (HX) {
+                    // keys 0-63: P into TMEM columns 0-31, announced on p_part; the helper
+                    // announces keys 64-127 on p_full
+                    exp_range((m_use == -INFINITY) ? 0.f : m_use, false, mr0, mr1, 0, 32);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t pk[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            pk[e] = tc::pack_bf16(__uint_as_float(s[16 * c + 2 * e]), __uint_as_float(s[16 * c + 2 * e + 1]));
+                        tc::tmem_st8(s_col + c * 8, pk);
+                    }
+                    tc::tmem_st_wait();
+                    tc::tc_fence_before();
+                    if ((warp & 3) == 0 && lane == 0) K2_STAMP(2 + g, j);
+                    arrive0(&p_part[g * (kPParts - 1)]);
+                    uint64_t acc[4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) acc[a] = tc::f2(0.f, 0.f);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        acc[i & 3] = tc::fadd2(acc[i & 3], tc::f2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])));
+                    float a0, a1, b0, b1, c0, c1, d0, d1;
+                    tc::f2_split(acc[0], a0, a1);
+                    tc::f2_split(acc[1], b0, b1);
+                    tc::f2_split(acc[2], c0, c1);
+                    tc::f2_split(acc[3], d0, d1);
+                    l += ((a0 + a1) + (b0 + b1)) + ((c0 + c1) + (d0 + d1));
+                    continue;
                 }
                 const bool psplit = SDA_K2_PSPLIT && !spec;
                 if (psplit) {
@@ -1074,6 +1280,13 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 tc::mbar_arrive(&p_full[g]);
 #endif
             }
+            if (HX) {
+                if (group_live) {   // the helper's half of the row sum
+                    asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+                    l += xch[2 * 2 * 2 * 128 + (segc & 1) * 256 + g * 128 + row];
+                }
+                ++segc;
+            }
             // epilogue: O / l, (row_max, exp_sum) in natural units
             if (tid == 0) K2_STAMP(12, si_tr);
             const SoftKeep* const kk = opaque(keep);
@@ -1163,12 +1376,13 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                             if (stt.y > 0.f) L += stt.y * ex2((stt.x - mx) * kLog2e);
                         }
                         const float iv = L > 0.f ? 1.f / L : 0.f;
+                        constexpr int MB = HX ? 8 : 16;   // rows per batch (split rows: 120 registers)
 #pragma unroll 1
-                        for (int h = 0; h < 2; ++h) {
-                            const int rb = warp * 32 + h * 16;     // first row of this batch
-                            float4 acc[16];
+                        for (int h = 0; h < 32 / MB; ++h) {
+                            const int rb = warp * 32 + h * MB;     // first row of this batch
+                            float4 acc[MB];
 #pragma unroll
-                            for (int u = 0; u < 16; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            for (int u = 0; u < MB; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
                             for (int k = 0; k < P; ++k) {
                                 const float* pk = piece(k);
                                 float wl = 0.f;
@@ -1176,14 +1390,14 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                                     const float2 stt = __ldcg(reinterpret_cast<const float2*>(pk + 2 * TILE * D + r_l * 2));
                                     wl = stt.y > 0.f ? stt.y * ex2((stt.x - mx) * kLog2e) * iv : 0.f;
                                 }
-                                float4 v[16];
+                                float4 v[MB];
 #pragma unroll
-                                for (int u = 0; u < 16; ++u)
+                                for (int u = 0; u < MB; ++u)
                                     v[u] = rb + u < sg.nrows ? __ldcg(reinterpret_cast<const float4*>(pk + (rb + u) * D) + lane)
                                                              : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-                                for (int u = 0; u < 16; ++u) {
-                                    const float w = __shfl_sync(0xffffffffu, wl, h * 16 + u);
+                                for (int u = 0; u < MB; ++u) {
+                                    const float w = __shfl_sync(0xffffffffu, wl, h * MB + u);
                                     acc[u].x += w * v[u].x;
                                     acc[u].y += w * v[u].y;
                                     acc[u].z += w * v[u].z;
@@ -1191,7 +1405,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                                 }
                             }
 #pragma unroll
-                            for (int u = 0; u < 16; ++u)
+                            for (int u = 0; u < MB; ++u)
                                 if (rb + u < sg.nrows) reinterpret_cast<float4*>(out_o + (orow0 + rb + u) * D)[lane] = acc[u];
                         }
                         if (live_l) *reinterpret_cast<float2*>(out_stats + (orow0 + r_l) * 2) = make_float2(L > 0.f ? mx : -INFINITY, L);
@@ -1434,7 +1648,7 @@ static cudaError_t launch_pair(dim3 grid, const K2TcParams& p, const CUtensorMap
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(THREADS);
+    cfg.blockDim = dim3(Thr<true>::N);
     cfg.dynamicSmemBytes = Lay<true>::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -1505,7 +1719,7 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
             p.sk_tick = static_cast<uint32_t*>(q.sk_work);
             p.sk_buf = reinterpret_cast<float*>(static_cast<char*>(q.sk_work) + sh.tick_bytes);
             if (pair_ok && sh.gq % 2 == 0) return launch_pair(dim3((unsigned)sh.ctas), p, qm, km64, vm, st);
-            k2_prefill_tc_kernel<false><<<dim3((unsigned)sh.ctas), THREADS, SMEM, st>>>(p, qm, km, vm);
+            k2_prefill_tc_kernel<false><<<dim3((unsigned)sh.ctas), Thr<false>::N, SMEM, st>>>(p, qm, km, vm);
             return cudaGetLastError();
         }
     }
@@ -1513,7 +1727,7 @@ cudaError_t launch_k2_prefill_tc(const K2Params& q, cudaStream_t st) {
                                : dim3((unsigned)p.n_qpairs, (unsigned)(p.grouped ? q.kv_heads : q.q_heads),
                                       (unsigned)(q.n_batch * q.n_splits));
     if (pair_ok && !p.remote && p.n_qpairs % 2 == 0) return launch_pair(grid, p, qm, km64, vm, st);
-    k2_prefill_tc_kernel<false><<<grid, THREADS, SMEM, st>>>(p, qm, km, vm);
+    k2_prefill_tc_kernel<false><<<grid, Thr<false>::N, SMEM, st>>>(p, qm, km, vm);
     return cudaGetLastError();
 }
 

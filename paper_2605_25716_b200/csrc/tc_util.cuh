@@ -318,6 +318,28 @@ __device__ __forceinline__ void exp2_fma2(float x0, float x1, float& p0, float& 
     p0 = exp2_fma(x0);
     p1 = exp2_fma(x1);
 }
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// The same 2^x on a packed pair: the rounding, the reduction and the polynomial as FADD2 / FFMA2
+// (half the issue slots of the scalar form; the FMA-pipe time per value is the same), the clamp
+// as two FMNMX and the exponent insertion as integer ops on the ALU pipe.
+__device__ __forceinline__ void exp2_fma2_packed(float x0, float x1, float& p0, float& p1) {
+    constexpr float kMagic = 12582912.f;
+    const uint64_t x = f2(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
+    const uint64_t t = fadd2(x, f2(kMagic, kMagic));
+    const uint64_t f = fsub2(x, fsub2(t, f2(kMagic, kMagic)));
+    uint64_t p = ffma2(f2(0.05517143f, 0.05517143f), f, f2(0.24261081f, 0.24261081f));
+    p = ffma2(p, f, f2(0.69326097f, 0.69326097f));
+    p = ffma2(p, f, f2(0.9999281f, 0.9999281f));
+    float t0, t1, q0, q1;
+    f2_split(t, t0, t1);
+    f2_split(p, q0, q1);
+    p0 = __uint_as_float((__float_as_uint(t0) << 23) + __float_as_uint(q0));
+    p1 = __uint_as_float((__float_as_uint(t1) << 23) + __float_as_uint(q1));
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     uint32_t r;
