@@ -68,6 +68,9 @@ class RankCompute:
     # (q, exchange) -> bool: K1 writing every domain's Q' straight into that domain's receive
     # slot and raising its SCR_Q flag (False: not eligible, use scramble_q_all + exchange_q)
     scramble_q_remote: Optional[Callable[[torch.Tensor, "PeerExchange"], bool]] = None
+    # () -> None: the current stream waits for work a step left behind off its path (the span's
+    # own K/V scrambled into the local cache, which no later kernel of the step reads)
+    drain: Optional[Callable[[], None]] = None
 
 
 def map_peer_buffers(bufs: dict, group: Optional[dist.ProcessGroup] = None):
@@ -520,12 +523,27 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
         state["fork"].record(cur)          # after K1 and after the previous step's K3 (it read lo / ls)
         side.wait_event(state["fork"])
         with torch.cuda.stream(side):
-            if side_work is not None:
+            # the causal span first: K3 joins it; the side work (nothing in this step reads it)
+            # follows behind the join, so K3 does not wait for it -- it fills the SMs K3 and the
+            # next step's K1 leave idle (SDA_SIDE_FIRST=1: side work ahead of the span, joined)
+            side_first = os.environ.get("SDA_SIDE_FIRST") == "1"
+            if side_work is not None and (side_first or local_kv is None):
                 side_work()
             if local_kv is not None:
                 run_local(q)
             state["join"].record(side)
+            if side_work is not None and not (side_first or local_kv is None):
+                side_work()
+                if state.get("tail") is None:
+                    state["tail"] = torch.cuda.Event()
+                state["tail"].record(side)
+                state["tail_pending"] = True
         state["local_ev"] = state["join"]
+
+    def drain():
+        if state.get("tail_pending"):
+            torch.cuda.current_stream().wait_event(state["tail"])
+            state["tail_pending"] = False
 
     def run_local(q):
         Bp, Hq, Lq, d = q.shape
@@ -627,4 +645,4 @@ def gpu_rank_compute(inquirer_keys: Sequence, shard, n_splits: Optional[int] = N
             srcs += ops.sources_from_splits(state["lo"], state["ls"])
         ops.unscramble_merge(srcs, out=out, key_heads=kv_heads or inquirer_keys[0].kv_heads)
 
-    return RankCompute(scramble_q, serve, finish, scramble_q_all, serve_remote, scramble_q_remote)
+    return RankCompute(scramble_q, serve, finish, scramble_q_all, serve_remote, scramble_q_remote, drain)
