@@ -106,7 +106,14 @@ __device__ __forceinline__ void k2_stamp1(int kind, int64_t j) {
 // The MMA warp's waits for P sit on the S -> softmax -> PV -> S chain of each Q tile: it spins
 // (test_wait) instead of suspending (try_wait), which trims ~100 ns of wake-up per hand-off
 // (tools/k2_trace.py; +2 % on C3).
+#ifndef SDA_K2_PWAIT_NS
+#define SDA_K2_PWAIT_NS 0
+#endif
+#if SDA_K2_PWAIT_NS > 0
+#define K2_WAIT_P(b, ph) tc::mbar_wait_backoff<SDA_K2_PWAIT_NS>(b, ph)
+#else
 #define K2_WAIT_P(b, ph) tc::mbar_wait_spin(b, ph)
+#endif
 
 namespace k2tc {
 constexpr int D = 128;
@@ -1248,6 +1255,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
                 }
                 tc::tc_fence_before();
                 if ((warp & 3) == 0 && lane == 0) K2_STAMP(2 + g, j);
+                if (!PAIR && g == 0 && (warp & 3) != 0 && lane == 0) K2_STAMP(17 + (warp & 3), j);   // warps 1-3: 18-20
                 if (warp == 0 && lane == 0) K2_STAMP1(21, j);
 #if SDA_K2_PSPLIT
                 if (!psplit)   // (speculative path: whole P at once)

@@ -46,6 +46,21 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Polling with a nanosleep between test_waits: the spinning warp leaves its SMSP's issue slots to
+// the warps it shares them with (the prefill K2's MMA warp sits on a softmax warp pair's SMSP).
+template <int NS>
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "nanosleep.u32 %2;\n\t"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(NS)
+        : "memory");
+}
 // 16-byte async copy global -> shared (LDGSTS), L2-only caching.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");

@@ -8,6 +8,8 @@
 //   1 TS, B MN-major       (O += P V: P from TMEM, V [keys x d] as an MN-major B, SW128 blocks)
 //   2 TS, B K-major
 //   3 mixed: 8 SS (mode 0) then 8 TS MN-major (mode 1) per group -- a prefill tile's S and PV
+// Contention 1: softmax-like TMEM ld/st (warps 1-8); 2: TMA-like bulk fills into shared memory
+// (warp 9, 32 KB per ~1850 cycles, the prefill kernel's average K/V fill rate).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2605_25716_b200/csrc -o tools/_mma_contend tools/mma_contend.cu
 #include <cstdio>
 #include <cstdint>
@@ -20,17 +22,20 @@ using namespace sda;
 constexpr int ITERS = 256;
 constexpr int BLK = 128 * 128;   // [128 x 64] bf16 SW128 block
 
-template <int MODE, bool CONTEND>
-__global__ void __launch_bounds__(288, 1) contend_kernel(unsigned long long* cycles, unsigned* sink) {
+template <int MODE, int CONTEND>
+__global__ void __launch_bounds__(320, 1) contend_kernel(unsigned long long* cycles, unsigned* sink, const uint8_t* gsrc) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* a = smem;                  // Q: [128 x 128] bf16 K-major = 2 blocks (32 KB)
     uint8_t* b = smem + 2 * BLK;        // K or V: [128 x 128] bf16 = 2 blocks (32 KB)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 4 * BLK);
+    uint8_t* land = smem + 4 * BLK;     // TMA-like landing area (32 KB), CONTEND == 2
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 6 * BLK);
+    uint64_t* bar2 = bar + 2;
     uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
     volatile uint32_t* stop = slot + 1;
     for (int i = threadIdx.x; i < 4 * BLK / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
     if (threadIdx.x == 0) {
         tc::mbar_init(bar, 1);
+        tc::mbar_init(bar2, 1);
         tc::fence_mbar_init();
         *stop = 0u;
     }
@@ -80,7 +85,27 @@ __global__ void __launch_bounds__(288, 1) contend_kernel(unsigned long long* cyc
             cycles[blockIdx.x] = t1 - t0;
             *stop = 1u;
         }
-    } else if (CONTEND) {
+    } else if (CONTEND == 2 && warp == 9) {
+        // TMA-like fills: 32 KB (a K and a V tile's worth per two Q tiles' step) per ~1850 cycles,
+        // the prefill kernel's average fill rate at its measured period, as two 16 KB bulk copies
+        uint32_t ph = 0;
+        int64_t off = 0;
+        while (*stop == 0u) {
+            const long long t = clock64();
+            if (tc::elect_one()) {
+                tc::mbar_arrive_expect_tx(bar2, 2 * BLK);
+                for (int c = 0; c < 2; ++c)
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                 ::"r"(tc::smem_u32(land + c * BLK)), "l"(gsrc + off + c * BLK), "r"(BLK), "r"(tc::smem_u32(bar2))
+                                 : "memory");
+            }
+            __syncwarp();
+            tc::mbar_wait(bar2, ph);
+            ph ^= 1u;
+            off = (off + 2 * BLK + (int64_t)blockIdx.x * 4096) % ((int64_t)256 << 20);
+            while (clock64() - t < 1850) {}
+        }
+    } else if (CONTEND == 1 && warp >= 1 && warp <= 8) {
         // softmax-like TMEM traffic on the other S columns (128..255) of this warp's lane quarter
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         unsigned acc = 0;
@@ -106,23 +131,23 @@ __global__ void __launch_bounds__(288, 1) contend_kernel(unsigned long long* cyc
     if (threadIdx.x < 32) tc::tmem_dealloc<512>(tmem);
 }
 
-template <int MODE, bool CONTEND>
-void run(int sms, const char* name) {
+template <int MODE, int CONTEND>
+void run(int sms, const char* name, const uint8_t* gsrc) {
     unsigned long long* d;
     unsigned* sink;
     cudaMalloc(&d, sms * 8);
     cudaMalloc(&sink, 4);
-    const int smem = 4 * BLK + 64;
+    const int smem = 6 * BLK + 64;
     cudaFuncSetAttribute(contend_kernel<MODE, CONTEND>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    contend_kernel<MODE, CONTEND><<<sms, 288, smem>>>(d, sink);
-    contend_kernel<MODE, CONTEND><<<sms, 288, smem>>>(d, sink);
+    contend_kernel<MODE, CONTEND><<<sms, 320, smem>>>(d, sink, gsrc);
+    contend_kernel<MODE, CONTEND><<<sms, 320, smem>>>(d, sink, gsrc);
     cudaDeviceSynchronize();
     unsigned long long h[256];
     cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
     double avg = 0;
     for (int i = 0; i < sms; ++i) avg += (double)h[i] / sms;
     const int per = MODE == 3 ? 16 : 8;
-    printf("%-34s %s: %6.1f cycles per MMA (nominal 64) (%s)\n", name, CONTEND ? "+ softmax TMEM ld/st" : "alone               ",
+    printf("%-34s %s: %6.1f cycles per MMA (nominal 64) (%s)\n", name, CONTEND == 1 ? "+ softmax TMEM ld/st" : CONTEND == 2 ? "+ TMA-like fills    " : "alone               ",
            avg / ((double)per * ITERS), cudaGetErrorString(cudaGetLastError()));
     cudaFree(d);
     cudaFree(sink);
@@ -131,13 +156,20 @@ void run(int sms, const char* name) {
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    run<0, false>(sms, "SS, B K-major (S = Q K^T)");
-    run<0, true>(sms, "SS, B K-major (S = Q K^T)");
-    run<1, false>(sms, "TS, B MN-major (O += P V)");
-    run<1, true>(sms, "TS, B MN-major (O += P V)");
-    run<2, false>(sms, "TS, B K-major");
-    run<2, true>(sms, "TS, B K-major");
-    run<3, false>(sms, "8 SS + 8 TS MN-major");
-    run<3, true>(sms, "8 SS + 8 TS MN-major");
+    uint8_t* g;
+    cudaMalloc(&g, ((size_t)256 << 20) + 4 * BLK);
+    cudaMemset(g, 0, ((size_t)256 << 20) + 4 * BLK);
+    run<0, 0>(sms, "SS, B K-major (S = Q K^T)", g);
+    run<0, 1>(sms, "SS, B K-major (S = Q K^T)", g);
+    run<0, 2>(sms, "SS, B K-major (S = Q K^T)", g);
+    run<1, 0>(sms, "TS, B MN-major (O += P V)", g);
+    run<1, 1>(sms, "TS, B MN-major (O += P V)", g);
+    run<1, 2>(sms, "TS, B MN-major (O += P V)", g);
+    run<2, 0>(sms, "TS, B K-major", g);
+    run<2, 1>(sms, "TS, B K-major", g);
+    run<3, 0>(sms, "8 SS + 8 TS MN-major", g);
+    run<3, 1>(sms, "8 SS + 8 TS MN-major", g);
+    run<3, 2>(sms, "8 SS + 8 TS MN-major", g);
+    cudaFree(g);
     return 0;
 }
