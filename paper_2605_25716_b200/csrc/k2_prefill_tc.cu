@@ -103,13 +103,29 @@ __device__ __forceinline__ void k2_stamp1(int kind, int64_t j) {
 #define K2_CTA_STAMP(w)
 #endif
 
-// The MMA warp's waits for P sit on the S -> softmax -> PV -> S chain of each Q tile: it spins
-// (test_wait) instead of suspending (try_wait), which trims ~100 ns of wake-up per hand-off
-// (tools/k2_trace.py; +2 % on C3).
+// The MMA warp's waits for P sit on the S -> softmax -> PV -> S chain of each Q tile. A plain
+// try_wait (suspending for the default time) cost ~100 ns of wake-up per hand-off against a
+// test_wait spin (+2 % on C3, tools/k2_trace.py); but the spin takes issue slots from the softmax
+// warps 1 and 5 on the MMA warp's SMSP, and warp 1 is the last of its group to hand P over in every
+// traced tile (tools/k2_trace_warps.py). try_wait with a suspend-time hint wakes on the phase and
+// leaves the slots free: C3 K2 454-457 us against 461-466 us spinning
+// (profiles/k2_prefill_split_rows_r02.txt). SDA_K2_PWAIT_NS: < 0 try_wait with a |n| ns hint,
+// 0 spin, > 0 spin with an n ns nanosleep between polls.
 #ifndef SDA_K2_PWAIT_NS
-#define SDA_K2_PWAIT_NS 0
+#define SDA_K2_PWAIT_NS -1000
 #endif
-#if SDA_K2_PWAIT_NS > 0
+// the softmax warps' wait for S: try_wait, optionally with a suspend-time hint (ns)
+#ifndef SDA_K2_SWAIT_NS
+#define SDA_K2_SWAIT_NS 0
+#endif
+#if SDA_K2_SWAIT_NS > 0
+#define K2_WAIT_S(b, ph) tc::mbar_wait_hint<SDA_K2_SWAIT_NS>(b, ph)
+#else
+#define K2_WAIT_S(b, ph) tc::mbar_wait(b, ph)
+#endif
+#if SDA_K2_PWAIT_NS < 0
+#define K2_WAIT_P(b, ph) tc::mbar_wait_hint<-(SDA_K2_PWAIT_NS)>(b, ph)
+#elif SDA_K2_PWAIT_NS > 0
 #define K2_WAIT_P(b, ph) tc::mbar_wait_backoff<SDA_K2_PWAIT_NS>(b, ph)
 #else
 #define K2_WAIT_P(b, ph) tc::mbar_wait_spin(b, ph)
@@ -866,7 +882,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             }
             float m_run = -INFINITY, m_use = -INFINITY, l = 0.f;
             for (int j = 0; group_live && j < nkv; ++j) {
-                tc::mbar_wait(&s_full[g], sc & 1);
+                K2_WAIT_S(&s_full[g], sc & 1);
                 const uint32_t par = sc & 1;
                 ++sc;
                 tc::tc_fence_after();
@@ -1011,7 +1027,7 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             __syncwarp();
             float m_run = -INFINITY, m_use = -INFINITY, l = 0.f;
             for (int j = 0; group_live && j < nkv; ++j) {
-                tc::mbar_wait(&s_full[g], sc & 1);
+                K2_WAIT_S(&s_full[g], sc & 1);
                 ++sc;
                 tc::tc_fence_after();
                 if ((warp & 3) == 0 && lane == 0) K2_STAMP(g, j);

@@ -61,6 +61,18 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
         "r"(parity), "n"(NS)
         : "memory");
 }
+// try_wait with a suspend-time hint (ns): the warp sleeps until the phase completes or the hint
+// elapses, then polls again.
+template <int NS>
+__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(NS)
+        : "memory");
+}
 // 16-byte async copy global -> shared (LDGSTS), L2-only caching.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
