@@ -629,11 +629,15 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             const uint32_t qa = g ? q1 : q0;
             const uint32_t kb = kbase + st * TILE_BYTES;
             const uint32_t d_tmem = tmem + (g ? COL_S1 : COL_S0);
+            // descriptors as base + (byte offset >> 4): the start-address field is the low 14 bits
+            // and SMEM offsets stay below 256 KB, so the add never carries out of it -- one uniform
+            // add per operand instead of the shift / mask / or of a fresh descriptor (the MMA warp
+            // shares SMSP 1's issue slots with two softmax warps)
+            const uint64_t da0 = tc::sw128_desc(qa, 16, 1024), db0 = tc::sw128_desc(kb, 16, 1024);
 #pragma unroll
             for (int k = 0; k < D / 16; ++k) {
-                const uint32_t off = (k >> 2) * BLK + (k & 3) * 32;
-                const uint64_t da = tc::sw128_desc(qa + off, 16, 1024), db = tc::sw128_desc(kb + off, 16, 1024);
-                if (leader) tc::mma_bf16_ss(d_tmem, da, db, IDESC_S, k > 0 ? 1u : 0u);
+                const uint32_t off = ((k >> 2) * BLK + (k & 3) * 32) >> 4;
+                if (leader) tc::mma_bf16_ss(d_tmem, da0 + off, db0 + off, IDESC_S, k > 0 ? 1u : 0u);
             }
             if (leader) tc::mma_commit(&s_full[g]);
         };
@@ -641,10 +645,10 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             const uint32_t vb = vbase + st * TILE_BYTES;
             const uint32_t d_tmem = tmem + (g ? COL_O1 : COL_O0);
             const uint32_t p_tmem = tmem + (g ? COL_S1 : COL_S0);
+            const uint64_t db0 = tc::sw128_desc(vb, BLK, 1024);
 #pragma unroll
             for (int k = k0; k < k1; ++k) {   // 16 keys per step: P columns 8k.., V rows 16k..
-                const uint64_t db = tc::sw128_desc(vb + k * 2048, BLK, 1024);
-                if (leader) tc::mma_bf16_ts(d_tmem, p_tmem + k * 8, db, IDESC_O, (acc || k > 0) ? 1u : 0u);
+                if (leader) tc::mma_bf16_ts(d_tmem, p_tmem + k * 8, db0 + (uint32_t)(k * 2048 >> 4), IDESC_O, (acc || k > 0) ? 1u : 0u);
             }
         };
         // PV of tile g: with PSPLIT the first 64 keys go as soon as their P is in TMEM
