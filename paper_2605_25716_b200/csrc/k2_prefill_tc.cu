@@ -229,9 +229,11 @@ constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 384;
 #endif
 constexpr int kEmuOf4 = SDA_K2_EMU_OF4;
 // Packed form (tc::exp2_fma2_packed: FADD2 / FFMA2, 5 issue slots per value against 8): the
-// fraction of pairs on the FMA pipe in eighths (0 = the scalar form at kEmuOf4 of four)
+// fraction of pairs on the FMA pipe in eighths (0 = the scalar form at kEmuOf4 of four). With the
+// MMA warp's suspend-hint waits and additive descriptors, 1 of 8 packed is the best mix on C3:
+// 439.7-440.7 us against 442.5-443.4 (scalar 1 of 4), 446.6-449.5 (all MUFU), 449.2-452.0 (2 of 8)
 #ifndef SDA_K2_EMU_OF8P
-#define SDA_K2_EMU_OF8P 0
+#define SDA_K2_EMU_OF8P 1
 #endif
 constexpr int kEmuOf8P = SDA_K2_EMU_OF8P;
 #ifndef SDA_K2_SUM_AFTER
