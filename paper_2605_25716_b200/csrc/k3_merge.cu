@@ -473,19 +473,54 @@ __global__ void __launch_bounds__(128) k3_merge_small_kernel(const K3Params p) {
 
 // fwht_group over U independent rows at once (lane owns elements [lane*E, lane*E+E) of each):
 // every stage runs across all rows before the next, so the shuffle latencies overlap
+// (E = 4: the butterflies as packed f32x2 adds / FMAs -- the kernel is issue-bound)
+__device__ __forceinline__ uint64_t k3_f2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void k3_split(uint64_t r, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); }
+__device__ __forceinline__ uint64_t k3_add2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t k3_sub2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t k3_fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
 template <int U, int E>
 __device__ __forceinline__ void fwht_rows(float (&v)[U][E], int lane) {
+    if constexpr (E == 4) {
 #pragma unroll
-    for (int h = 1; h < E; h <<= 1)
+        for (int u = 0; u < U; ++u) {   // (0,1) (2,3), then (0,2) (1,3): the same sums in the same order
+            const uint64_t a = k3_f2(v[u][0], v[u][2]), b = k3_f2(v[u][1], v[u][3]);
+            float s0, s1, d0, d1;
+            k3_split(k3_add2(a, b), s0, s1);   // v0 + v1, v2 + v3
+            k3_split(k3_sub2(a, b), d0, d1);   // v0 - v1, v2 - v3
+            const uint64_t a2 = k3_f2(s0, d0), b2 = k3_f2(s1, d1);
+            k3_split(k3_add2(a2, b2), v[u][0], v[u][1]);
+            k3_split(k3_sub2(a2, b2), v[u][2], v[u][3]);
+        }
+    } else {
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+        for (int h = 1; h < E; h <<= 1)
 #pragma unroll
-            for (int i = 0; i < E; ++i)
-                if ((i & h) == 0) {
-                    const float a = v[u][i], b = v[u][i + h];
-                    v[u][i] = a + b;
-                    v[u][i + h] = a - b;
-                }
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int i = 0; i < E; ++i)
+                    if ((i & h) == 0) {
+                        const float a = v[u][i], b = v[u][i + h];
+                        v[u][i] = a + b;
+                        v[u][i + h] = a - b;
+                    }
+    }
 #pragma unroll
     for (int m = 1; m < 32; m <<= 1) {
         const float sgn = (lane & m) ? -1.f : 1.f;
@@ -494,10 +529,19 @@ __device__ __forceinline__ void fwht_rows(float (&v)[U][E], int lane) {
         for (int u = 0; u < U; ++u)
 #pragma unroll
             for (int i = 0; i < E; ++i) o[u][i] = __shfl_xor_sync(0xffffffffu, v[u][i], m);
+        if constexpr (E % 2 == 0) {
+            const uint64_t sg2 = k3_f2(sgn, sgn);
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+            for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int i = 0; i < E; ++i) v[u][i] = fmaf(sgn, v[u][i], o[u][i]);
+                for (int i = 0; i < E; i += 2)
+                    k3_split(k3_fma2(k3_f2(v[u][i], v[u][i + 1]), sg2, k3_f2(o[u][i], o[u][i + 1])), v[u][i], v[u][i + 1]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int i = 0; i < E; ++i) v[u][i] = fmaf(sgn, v[u][i], o[u][i]);
+        }
     }
 }
 
