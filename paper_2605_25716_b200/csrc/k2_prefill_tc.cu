@@ -161,7 +161,9 @@ constexpr int NBAR = 14 + 2 * KST + 2 * (SDA_K2_PPARTS > 1 ? SDA_K2_PPARTS - 1 :
 // per-tile chain S -> softmax -> PV -> S then carries half the exponentials per thread. The two
 // halves of a row exchange their tile max (and, at a segment's end, the row sum) through shared
 // memory under a 64-thread named barrier per (tile, lane quarter); the primary hands P's first
-// 64 keys to the MMA on p_part, the helper the second 64 on p_full.
+// 64 keys to the MMA on p_part, the helper the second 64 on p_full. Opt-in: parity-green but
+// C3 498-501 us against 464-468 us for the default (half the logits per thread take ~90 % of the
+// whole row's time: the softmax is bound by the SM's shared throughput, K2 prefill).
 #ifndef SDA_K2_HELP
 #define SDA_K2_HELP 0
 #endif
