@@ -124,11 +124,38 @@ __device__ __forceinline__ void k2_stamp1(int kind, int64_t j) {
 #define K2_WAIT_S(b, ph) tc::mbar_wait(b, ph)
 #endif
 #if SDA_K2_PWAIT_NS < 0
-#define K2_WAIT_P(b, ph) tc::mbar_wait_hint<-(SDA_K2_PWAIT_NS)>(b, ph)
+#define K2_WAIT_P1(b, ph) tc::mbar_wait_hint<-(SDA_K2_PWAIT_NS)>(b, ph)
 #elif SDA_K2_PWAIT_NS > 0
-#define K2_WAIT_P(b, ph) tc::mbar_wait_backoff<SDA_K2_PWAIT_NS>(b, ph)
+#define K2_WAIT_P1(b, ph) tc::mbar_wait_backoff<SDA_K2_PWAIT_NS>(b, ph)
 #else
-#define K2_WAIT_P(b, ph) tc::mbar_wait_spin(b, ph)
+#define K2_WAIT_P1(b, ph) tc::mbar_wait_spin(b, ph)
+#endif
+// The pair form's issuers wait on barriers that rank 1's relays complete with remote arrives, which
+// do not wake a suspended try_wait: they poll (SDA_K2_PAIR_PWAIT_NS > 0: with that nanosleep between
+// polls). Its relay warps wait on their own CTA's barriers (SDA_K2_RELAY_HINT=1: suspend-hint
+// try_wait instead of a spin).
+#ifndef SDA_K2_PAIR_PWAIT_NS
+#define SDA_K2_PAIR_PWAIT_NS 0
+#endif
+#ifndef SDA_K2_RELAY_HINT
+#define SDA_K2_RELAY_HINT 1
+#endif
+#if SDA_K2_PAIR_PWAIT_NS > 0
+#define K2_WAIT_P2(b, ph) tc::mbar_wait_backoff<SDA_K2_PAIR_PWAIT_NS>(b, ph)
+#else
+#define K2_WAIT_P2(b, ph) tc::mbar_wait_spin(b, ph)
+#endif
+#define K2_WAIT_P(b, ph)             \
+    do {                             \
+        if constexpr (PAIR)          \
+            K2_WAIT_P2(b, ph);       \
+        else                         \
+            K2_WAIT_P1(b, ph);       \
+    } while (0)
+#if SDA_K2_RELAY_HINT
+#define K2_WAIT_RELAY(b, ph) tc::mbar_wait_hint<1000>(b, ph)
+#else
+#define K2_WAIT_RELAY(b, ph) tc::mbar_wait_spin(b, ph)
 #endif
 
 namespace k2tc {
@@ -176,7 +203,8 @@ constexpr int OFF_SEG = OFF_BAR + NBAR * 8 + 16;   // per softmax warp: segment 
 constexpr int OFF_XCH = OFF_SEG + SEG_SLOTS * 128;
 constexpr int SMEM = OFF_XCH + XCH_BYTES;
 // The CTA-pair form (PAIR; opt-in, SDA_K2_PAIR=1 -- parity-green but 495-505 us on C3 against
-// 445-454 us for the form above: with the chain decoupled both softmax groups run at once and
+// 445-454 us for the form above (second session, with the exponential mix and relay hint waits:
+// 469-476 us against 448 us): with the chain decoupled both softmax groups run at once and
 // each takes 1.5-1.8 us per tile instead of 1.05, so the SM's softmax throughput, not the chain,
 // bounds the step): a cluster of two CTAs issues every MMA as one M = 256 tcgen05.mma
 // (cta_group::2; rank 0 issues): each CTA keeps its own two Q tiles, S and O in its TMEM, and only
@@ -831,18 +859,18 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
         while (next_seg(sg)) {
             if (!(g == 0 || sg.two)) continue;
             for (int j = 0; j < sg.nkv; ++j, ++n_t) {
-                tc::mbar_wait_spin(&s_free[g], n_t & 1);
+                K2_WAIT_RELAY(&s_free[g], n_t & 1);
                 tc::mbar_arrive_remote_relaxed(tc::at_rank0(&s_free[g]));
                 for (int part = 0; part + 1 < kPParts; ++part) {
-                    tc::mbar_wait_spin(&p_part[g * (kPParts - 1) + part], n_t & 1);
+                    K2_WAIT_RELAY(&p_part[g * (kPParts - 1) + part], n_t & 1);
                     tc::mbar_arrive_remote_relaxed(tc::at_rank0(&p_part[g * (kPParts - 1) + part]));
                 }
-                tc::mbar_wait_spin(&p_full[g], n_t & 1);
+                K2_WAIT_RELAY(&p_full[g], n_t & 1);
                 if (g == 0) K2_STAMP1(20, n_t);
                 tc::mbar_arrive_remote_relaxed(tc::at_rank0(&p_full[g]));
             }
             if (p.sk || sg.nkv > 0) {
-                tc::mbar_wait_spin(&o_empty[g], n_o & 1);
+                K2_WAIT_RELAY(&o_empty[g], n_o & 1);
                 tc::mbar_arrive_remote_relaxed(tc::at_rank0(&o_empty[g]));
                 ++n_o;
             }
