@@ -720,10 +720,11 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             tc::tc_fence_after();
             const uint32_t qa = g ? q1 : q0;
             const uint32_t kb = kbase + sl * L::SLOT;
+            const uint64_t da0 = tc::sw128_desc(qa, 16, 1024), db0 = tc::sw128_desc(kb, 16, 1024);   // (as issue_s)
 #pragma unroll
             for (int k = 0; k < D / 16; ++k) {
-                const uint64_t da = tc::sw128_desc(qa + (k >> 2) * BLK + (k & 3) * 32, 16, 1024);
-                const uint64_t db = tc::sw128_desc(kb + (k >> 2) * (L::SLOT / 2) + (k & 3) * 32, 16, 1024);
+                const uint64_t da = da0 + (uint32_t)(((k >> 2) * BLK + (k & 3) * 32) >> 4);
+                const uint64_t db = db0 + (uint32_t)(((k >> 2) * (L::SLOT / 2) + (k & 3) * 32) >> 4);
                 if (leader) tc::mma_bf16_ss_pair(tmem + (g ? COL_S1 : COL_S0), da, db, IDESC_S2, k > 0 ? 1u : 0u);
             }
             if (leader) tc::mma_commit_pair(&s_full[g]);
@@ -733,11 +734,12 @@ k2_prefill_tc_kernel(const K2TcParams p, const __grid_constant__ CUtensorMap qma
             const uint32_t ph = n & 1;
             const uint32_t vb = kbase + sl * L::SLOT;
             const uint32_t pa = pbase + g * TILE_BYTES;
+            const uint64_t dp0 = tc::sw128_desc(pa, 16, 1024), dv0 = tc::sw128_desc(vb, BLK, 1024);
             auto issue = [&](int k0, int k1, bool a) {
 #pragma unroll
                 for (int k = k0; k < k1; ++k) {
-                    const uint64_t da = tc::sw128_desc(pa + (k >> 2) * BLK + (k & 3) * 32, 16, 1024);
-                    const uint64_t db = tc::sw128_desc(vb + k * 2048, BLK, 1024);
+                    const uint64_t da = dp0 + (uint32_t)(((k >> 2) * BLK + (k & 3) * 32) >> 4);
+                    const uint64_t db = dv0 + (uint32_t)(k * 2048 >> 4);
                     if (leader) tc::mma_bf16_ss_pair(tmem + (g ? COL_O1 : COL_O0), da, db, IDESC_O2, (a || k > 0) ? 1u : 0u);
                 }
             };
